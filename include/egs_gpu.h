@@ -1,0 +1,151 @@
+/*
+ * egs_gpu.h — C-ABI of the B200-native energy-game solver (libegs_b200.so).
+ *
+ * This is the drop-in boundary for the reference solve path of the
+ * arXiv 1710.03647 artifact (/root/reference/proj).  The reference binds the
+ * path through one C++ entry point,
+ *
+ *     SolveReport egsolve::solve(const GameArena&, Variant,
+ *                                const SolverOptions& = {});
+ *                                          proj/include/egsolve/solver.hpp:86-87
+ *
+ * (dispatch proj/src/solver_seq.cpp:233-244, parallel solvers
+ * proj/src/solver_par.cpp:126-435).  The C++ shim a maintainer adds next to it
+ * flattens the GameArena spans (arena.hpp:109-115) into an
+ * egs_arena_view, calls egs_gpu_solve, and rebuilds a SolveReport with the
+ * reference's own winning_sets (measure_ops.cpp:43-54).  Plain pointers and
+ * sizes only; no CUDA or torch types cross this boundary.
+ *
+ * Return codes mirror the exceptions the reference solve path can raise
+ * (errors.hpp:11-85):
+ *   EGS_OK 0, EGS_ERR_INVALID_CONFIG 1 (InvalidConfigError),
+ *   EGS_ERR_TIMEOUT 2 (TimeoutError), EGS_ERR_UNSUPPORTED 3 (OverflowError:
+ *   an arena outside the device representation), EGS_ERR_CUDA 4 (device or
+ *   NCCL failure), EGS_ERR_BOUND 5 (BoundExhaustedError), EGS_ERR_INTERNAL 6
+ *   (InternalInvariantError, debug checks).  egs_last_error() gives the text.
+ */
+#ifndef EGS_GPU_H
+#define EGS_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EGS_OK 0
+#define EGS_ERR_INVALID_CONFIG 1
+#define EGS_ERR_TIMEOUT 2
+#define EGS_ERR_UNSUPPORTED 3
+#define EGS_ERR_CUDA 4
+#define EGS_ERR_BOUND 5
+#define EGS_ERR_INTERNAL 6
+
+/* Flattened GameArena (arena.hpp:37-133).  All pointers are HOST memory and
+ * are only read during the call.  CSC spans are not needed: the predecessor
+ * transpose is rebuilt on the device. */
+typedef struct egs_arena_view {
+  uint32_t num_vertices;        /* GameArena::num_vertices()  arena.hpp:86 */
+  uint64_t num_edges;           /* GameArena::num_edges()     arena.hpp:87 */
+  const uint64_t* csr_offsets;  /* n+1   csr_offsets()  arena.hpp:109 */
+  const uint32_t* csr_targets;  /* m     csr_targets()  arena.hpp:110 */
+  const int64_t* csr_weights;   /* m     csr_weights()  arena.hpp:111 */
+  const uint8_t* owners;        /* n     owners(): 0 = player 0, 1 = player 1 */
+  int64_t credit_cap;           /* stats().credit_cap (M_G) arena.hpp:27 */
+  int64_t max_abs_weight;       /* stats().max_abs_weight   arena.hpp:28 */
+} egs_arena_view;
+
+/* Mode selector for the lift rounds. */
+#define EGS_MODE_AUTO 0   /* dense/sparse switch on frontier edge volume */
+#define EGS_MODE_DENSE 1  /* every round lifts every vertex (Alg. 2 shape) */
+#define EGS_MODE_SPARSE 2 /* worklist rounds only (Alg. 3 shape) */
+
+/* SolverOptions (solver.hpp:33-42) plus the device knobs. */
+typedef struct egs_gpu_opts {
+  int32_t n_gpus;          /* SolverOptions::workers: GPUs in this solve (1) */
+  int32_t device;          /* CUDA ordinal; -1 = current device */
+  int32_t certify;         /* 1: losing-region certificate (exact, default);
+                              0: plain value iteration up to credit_cap */
+  int32_t cert_interval;   /* rounds between certificate attempts (0 = 4) */
+  int32_t mode;            /* EGS_MODE_* */
+  int32_t debug_checks;    /* SolverOptions::debug_checks: monotonicity and
+                              fixpoint verification on the device */
+  double timeout_seconds;  /* SolverOptions::timeout_seconds; 0 disables */
+  uint64_t round_bound;    /* SolverOptions::sweep_bound; 0 = default budget
+                              |E|*(cap+1)+1 (solver_par.cpp:94-98) */
+} egs_gpu_opts;
+
+/* SolveReport counters (solver.hpp:47-59) plus device timings. */
+typedef struct egs_gpu_stats {
+  uint64_t lifts;          /* lift applications that raised a value */
+  uint64_t applications;   /* full lift applications (row scans) */
+  uint64_t pops;           /* worklist extractions (sparse rounds) */
+  uint64_t rounds;         /* lift rounds */
+  uint64_t edges_relaxed;  /* f(t) - w evaluations inside lifts */
+  uint64_t witness_checks; /* player-0 lifts skipped by the witness edge */
+  uint64_t dense_rounds;
+  uint64_t sparse_rounds;
+  uint64_t cert_attempts;  /* losing-region certificate attempts */
+  uint64_t cert_passes;    /* pruning passes over all attempts */
+  uint64_t certified;      /* vertices proven losing (set to top) */
+  uint64_t activations;    /* predecessor slots scanned by the worklist */
+  double upload_seconds;   /* H2D + device arena construction */
+  double solve_seconds;    /* device time from seed to fixpoint */
+  double download_seconds; /* D2H of the measure */
+  double wall_seconds;     /* call entry to return (SolveReport::wall_seconds) */
+  double lift_kernel_seconds; /* device time inside lift kernels */
+  uint64_t lift_bytes;     /* algorithmic bytes moved by the lift kernels */
+  uint32_t value_bits;     /* 32 or 64: device value width chosen */
+  uint32_t lanes;          /* lanes per vertex in the light lift */
+} egs_gpu_stats;
+
+void egs_gpu_opts_default(egs_gpu_opts* opts);
+
+/* One-shot solve: upload, solve, download.  f_out[n] receives the least
+ * energy progress measure in the reference's raw encoding (finite credit, or
+ * INT64_MAX for top; energy.hpp:16).  Replaces egsolve::solve(...)
+ * (solver.hpp:86-87) for the GPU variant. */
+int egs_gpu_solve(const egs_arena_view* arena, const egs_gpu_opts* opts,
+                  int64_t* f_out, egs_gpu_stats* stats);
+
+/* Device-resident context: the arena is uploaded once (the "cached per-arena"
+ * context of SURVEY.md §8b) and solved any number of times. */
+typedef struct egs_ctx egs_ctx;
+int egs_ctx_create(const egs_arena_view* arena, const egs_gpu_opts* opts,
+                   egs_ctx** out, egs_gpu_stats* stats);
+int egs_ctx_solve(egs_ctx* ctx, egs_gpu_stats* stats);
+int egs_ctx_read_measure(egs_ctx* ctx, int64_t* f_out);
+/* Device EPM verifier (measure_ops.cpp:33-41): 1 if f (host, n) is a progress
+ * measure of the context's arena, 0 if not, negative on error. */
+int egs_ctx_is_progress_measure(egs_ctx* ctx, const int64_t* f);
+void egs_ctx_destroy(egs_ctx* ctx);
+
+/* Output format: write_solution(make_solution(arena, report)) (io.cpp:178-210)
+ * with the first-witness strategy of extract_strategy (measure_ops.cpp:56-80).
+ * Returns the text length; writes at most cap bytes when buf != NULL;
+ * negative error code if some finite player-0 vertex has no witness. */
+int64_t egs_write_solution(const egs_arena_view* arena, const int64_t* f,
+                           char* buf, size_t cap);
+
+/* Synthetic canonical arenas in host memory,
+ * optionally pinned, for the bench and tests.  Owners alternate (even = P0). */
+typedef struct egs_host_arena egs_host_arena;
+int egs_host_arena_fixed(uint64_t n, uint32_t d, int64_t W, uint64_t seed,
+                         int pinned, egs_host_arena** out);
+int egs_host_arena_rmat(uint32_t scale, uint32_t edge_factor, int64_t W,
+                        uint64_t seed, int pinned, egs_host_arena** out);
+void egs_host_arena_view(const egs_host_arena* a, egs_arena_view* view);
+void egs_host_arena_free(egs_host_arena* a);
+
+/* Pinned host buffers for end-to-end timing. */
+void* egs_host_alloc_pinned(size_t bytes);
+void egs_host_free_pinned(void* p);
+
+const char* egs_last_error(void);
+const char* egs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EGS_GPU_H */

@@ -1,0 +1,413 @@
+"""ctypes binding of libegs_b200.so and the Python mirror of the reference API.
+
+Every struct below mirrors ``include/egs_gpu.h`` field for field.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libegs_b200.so")
+
+if not os.path.exists(lib_path):  # no CPU fallback: the product is the CUDA library
+    raise ImportError(
+        f"{lib_path} is missing: build it with `make` (or __graft_entry__.build())"
+    )
+lib = C.CDLL(lib_path)
+
+INT64_MAX = np.iinfo(np.int64).max
+
+# --------------------------------------------------------------- errors ----
+class EgsolveError(RuntimeError):
+    """egsolve::Error (errors.hpp:11)."""
+
+
+class InvalidConfigError(EgsolveError):
+    """egsolve::InvalidConfigError (errors.hpp:75)."""
+
+
+class TimeoutError_(EgsolveError):
+    """egsolve::TimeoutError (errors.hpp:79)."""
+
+
+class OverflowError_(EgsolveError):
+    """egsolve::OverflowError (errors.hpp:34); also arenas outside the device
+    representation (EGS_ERR_UNSUPPORTED)."""
+
+
+class CudaError(EgsolveError):
+    """Device failure (EGS_ERR_CUDA)."""
+
+
+class BoundExhaustedError(EgsolveError):
+    """egsolve::BoundExhaustedError (errors.hpp:67)."""
+
+
+class InternalInvariantError(EgsolveError):
+    """egsolve::InternalInvariantError (errors.hpp:83)."""
+
+
+_ERRORS = {
+    1: InvalidConfigError,
+    2: TimeoutError_,
+    3: OverflowError_,
+    4: CudaError,
+    5: BoundExhaustedError,
+    6: InternalInvariantError,
+}
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = lib.egs_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, EgsolveError)(msg)
+
+
+# -------------------------------------------------------------- structs ----
+class ArenaView(C.Structure):
+    _fields_ = [
+        ("num_vertices", C.c_uint32),
+        ("num_edges", C.c_uint64),
+        ("csr_offsets", C.c_void_p),
+        ("csr_targets", C.c_void_p),
+        ("csr_weights", C.c_void_p),
+        ("owners", C.c_void_p),
+        ("credit_cap", C.c_int64),
+        ("max_abs_weight", C.c_int64),
+    ]
+
+
+class GpuOpts(C.Structure):
+    _fields_ = [
+        ("n_gpus", C.c_int32),
+        ("device", C.c_int32),
+        ("certify", C.c_int32),
+        ("cert_interval", C.c_int32),
+        ("mode", C.c_int32),
+        ("debug_checks", C.c_int32),
+        ("timeout_seconds", C.c_double),
+        ("round_bound", C.c_uint64),
+    ]
+
+
+_STAT_U64 = [
+    "lifts", "applications", "pops", "rounds", "edges_relaxed", "witness_checks",
+    "dense_rounds", "sparse_rounds", "cert_attempts", "cert_passes", "certified",
+    "activations",
+]
+_STAT_F64 = [
+    "upload_seconds", "solve_seconds", "download_seconds", "wall_seconds",
+    "lift_kernel_seconds",
+]
+
+
+class GpuStats(C.Structure):
+    _fields_ = (
+        [(k, C.c_uint64) for k in _STAT_U64]
+        + [(k, C.c_double) for k in _STAT_F64]
+        + [("lift_bytes", C.c_uint64), ("value_bits", C.c_uint32), ("lanes", C.c_uint32)]
+    )
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_P = C.c_void_p
+lib.egs_gpu_opts_default.argtypes = [C.POINTER(GpuOpts)]
+lib.egs_gpu_solve.argtypes = [C.POINTER(ArenaView), C.POINTER(GpuOpts), _P, C.POINTER(GpuStats)]
+lib.egs_gpu_solve.restype = C.c_int
+lib.egs_ctx_create.argtypes = [C.POINTER(ArenaView), C.POINTER(GpuOpts), C.POINTER(_P), C.POINTER(GpuStats)]
+lib.egs_ctx_create.restype = C.c_int
+lib.egs_ctx_solve.argtypes = [_P, C.POINTER(GpuStats)]
+lib.egs_ctx_solve.restype = C.c_int
+lib.egs_ctx_read_measure.argtypes = [_P, _P]
+lib.egs_ctx_read_measure.restype = C.c_int
+lib.egs_ctx_is_progress_measure.argtypes = [_P, _P]
+lib.egs_ctx_is_progress_measure.restype = C.c_int
+lib.egs_ctx_destroy.argtypes = [_P]
+lib.egs_ctx_destroy.restype = None
+lib.egs_write_solution.argtypes = [C.POINTER(ArenaView), _P, _P, C.c_size_t]
+lib.egs_write_solution.restype = C.c_int64
+lib.egs_host_arena_fixed.argtypes = [C.c_uint64, C.c_uint32, C.c_int64, C.c_uint64, C.c_int, C.POINTER(_P)]
+lib.egs_host_arena_fixed.restype = C.c_int
+lib.egs_host_arena_rmat.argtypes = [C.c_uint32, C.c_uint32, C.c_int64, C.c_uint64, C.c_int, C.POINTER(_P)]
+lib.egs_host_arena_rmat.restype = C.c_int
+lib.egs_host_arena_view.argtypes = [_P, C.POINTER(ArenaView)]
+lib.egs_host_arena_view.restype = None
+lib.egs_host_arena_free.argtypes = [_P]
+lib.egs_host_arena_free.restype = None
+lib.egs_host_alloc_pinned.argtypes = [C.c_size_t]
+lib.egs_host_alloc_pinned.restype = _P
+lib.egs_host_free_pinned.argtypes = [_P]
+lib.egs_host_free_pinned.restype = None
+lib.egs_last_error.restype = C.c_char_p
+lib.egs_version.restype = C.c_char_p
+
+
+# ---------------------------------------------------------------- arena ----
+class GameArena:
+    """Flattened ``egsolve::GameArena``: CSR rows in input order, owners and the
+    cached ``ArenaStats`` fields the solve path needs (arena.hpp:24-31)."""
+
+    def __init__(self, csr_offsets, csr_targets, csr_weights, owners,
+                 credit_cap: int, max_abs_weight: int, _handle=None):
+        self.csr_offsets = csr_offsets
+        self.csr_targets = csr_targets
+        self.csr_weights = csr_weights
+        self.owners = owners
+        self.credit_cap = int(credit_cap)
+        self.max_abs_weight = int(max_abs_weight)
+        self._handle = _handle
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h:
+            lib.egs_host_arena_free(h)
+            self._handle = None
+
+    @property
+    def num_vertices(self) -> int:
+        return int(self.owners.shape[0])
+
+    @property
+    def num_edges(self) -> int:
+        return int(self.csr_targets.shape[0])
+
+    def is_player0(self, v: int) -> bool:
+        return int(self.owners[v]) == 0
+
+    def out_degree(self, v: int) -> int:
+        return int(self.csr_offsets[v + 1] - self.csr_offsets[v])
+
+    def view(self) -> ArenaView:
+        return ArenaView(
+            self.num_vertices, self.num_edges,
+            self.csr_offsets.ctypes.data, self.csr_targets.ctypes.data,
+            self.csr_weights.ctypes.data, self.owners.ctypes.data,
+            self.credit_cap, self.max_abs_weight,
+        )
+
+    # --- construction ------------------------------------------------------
+    @classmethod
+    def _from_native(cls, handle) -> "GameArena":
+        v = ArenaView()
+        lib.egs_host_arena_view(handle, C.byref(v))
+        n, m = v.num_vertices, v.num_edges
+
+        def arr(ptr, count, ctype, dtype):
+            if count == 0:
+                return np.zeros(0, dtype=dtype)
+            buf = (ctype * count).from_address(ptr)
+            return np.frombuffer(buf, dtype=dtype, count=count)
+
+        return cls(
+            arr(v.csr_offsets, n + 1, C.c_uint64, np.uint64),
+            arr(v.csr_targets, m, C.c_uint32, np.uint32),
+            arr(v.csr_weights, m, C.c_int64, np.int64),
+            arr(v.owners, n, C.c_uint8, np.uint8),
+            v.credit_cap, v.max_abs_weight, _handle=handle,
+        )
+
+    @classmethod
+    def fixed(cls, n: int, d: int, W: int, seed: int = 1, pinned: bool = False) -> "GameArena":
+        """Canonical ``fixed(n, d, W, seed)`` arena."""
+        h = _P()
+        _check(lib.egs_host_arena_fixed(n, d, W, seed, int(pinned), C.byref(h)))
+        return cls._from_native(h)
+
+    @classmethod
+    def rmat(cls, scale: int, edge_factor: int, W: int, seed: int = 1,
+             pinned: bool = False) -> "GameArena":
+        """Canonical ``rmat(scale, ef, W, seed)`` arena with sink fix."""
+        h = _P()
+        _check(lib.egs_host_arena_rmat(scale, edge_factor, W, seed, int(pinned), C.byref(h)))
+        return cls._from_native(h)
+
+    @classmethod
+    def build(cls, num_vertices: int, edges, owners) -> "GameArena":
+        """``GameArena::build`` (arena.cpp:17-78): validation, stable CSR rows
+        in input order, ``compute_stats`` (arena.cpp:80-108) with its overflow
+        headroom.  ``edges`` is an iterable of (src, dst, weight)."""
+        n = int(num_vertices)
+        edges = [tuple(int(x) for x in e) for e in edges]
+        own = np.asarray(owners, dtype=np.int64).reshape(-1)
+        if own.shape[0] != n:
+            raise EgsolveError("owner list does not cover every vertex")
+        for s_, d_, w_ in edges:
+            if not (0 <= s_ < n) or not (0 <= d_ < n):
+                raise EgsolveError("edge references unknown vertex id")
+            if not (-(2 ** 63) < w_ < 2 ** 63):
+                raise OverflowError_("edge weight magnitude not representable")
+        src = np.array([e[0] for e in edges], dtype=np.int64)
+        dst = np.array([e[1] for e in edges], dtype=np.int64)
+        w = np.array([e[2] for e in edges], dtype=np.int64)
+        counts = np.bincount(src, minlength=n) if n else np.zeros(0, np.int64)
+        if n and (counts == 0).any():
+            raise EgsolveError(f"vertex {int(np.argmax(counts == 0))} has no outgoing edge")
+        order = np.argsort(src, kind="stable")
+        off = np.zeros(n + 1, dtype=np.uint64)
+        off[1:] = np.cumsum(counts)
+        tgt = dst[order].astype(np.uint32)
+        wt = w[order]
+        cap = 0
+        maxw = 0
+        for v in range(n):
+            row = wt[int(off[v]):int(off[v + 1])]
+            worst = max(0, -int(row.min()))
+            maxw = max(maxw, int(np.abs(row).max()))
+            cap += worst
+        if cap > (2 ** 63 - 1) or cap > (2 ** 63 - 1) - maxw - 2:
+            raise OverflowError_("credit bound exceeds the representable range")
+        return cls(off, tgt, wt, (own != 0).astype(np.uint8), cap, maxw)
+
+
+# -------------------------------------------------------------- options ----
+class Variant(enum.IntEnum):
+    """egsolve::Variant (solver.hpp:16) plus the device variant."""
+    SEQ = 0
+    SWEEP = 1
+    FRONTIER = 2
+    GPU = 3
+
+
+_MODES = {"auto": 0, "dense": 1, "sparse": 2}
+
+
+@dataclass
+class SolverOptions:
+    """egsolve::SolverOptions (solver.hpp:33-42); ``workers`` counts GPUs."""
+    workers: int = 1
+    certify: bool = True
+    cert_interval: int = 4
+    mode: str = "auto"
+    debug_checks: bool = False
+    timeout_seconds: float = 0.0
+    sweep_bound: Optional[int] = None
+    device: int = -1
+
+    def to_c(self) -> GpuOpts:
+        if self.mode not in _MODES:
+            raise InvalidConfigError(f"unknown mode {self.mode!r}")
+        o = GpuOpts()
+        lib.egs_gpu_opts_default(C.byref(o))
+        o.n_gpus = int(self.workers)
+        o.device = int(self.device)
+        o.certify = int(bool(self.certify))
+        o.cert_interval = int(self.cert_interval)
+        o.mode = _MODES[self.mode]
+        o.debug_checks = int(bool(self.debug_checks))
+        o.timeout_seconds = float(self.timeout_seconds)
+        o.round_bound = int(self.sweep_bound or 0)
+        return o
+
+
+@dataclass
+class SolveReport:
+    """egsolve::SolveReport (solver.hpp:47-59); ``measure`` is the raw int64
+    encoding (INT64_MAX = top, energy.hpp:16)."""
+    measure: np.ndarray
+    w0: np.ndarray
+    w1: np.ndarray
+    lifts: int = 0
+    applications: int = 0
+    pops: int = 0
+    rounds: int = 0
+    wall_seconds: float = 0.0
+    variant: Variant = Variant.GPU
+    workers: int = 1
+    gpu: dict = field(default_factory=dict)
+
+
+def _report(measure: np.ndarray, st: GpuStats, workers: int) -> SolveReport:
+    top = measure == INT64_MAX
+    # winning_sets (measure_ops.cpp:43-54): W0 = finite, W1 = top
+    return SolveReport(
+        measure=measure,
+        w0=np.nonzero(~top)[0].astype(np.uint32),
+        w1=np.nonzero(top)[0].astype(np.uint32),
+        lifts=int(st.lifts), applications=int(st.applications), pops=int(st.pops),
+        rounds=int(st.rounds), wall_seconds=float(st.wall_seconds),
+        variant=Variant.GPU, workers=workers, gpu=st.as_dict(),
+    )
+
+
+def solve(arena: GameArena, variant: Variant = Variant.GPU,
+          options: Optional[SolverOptions] = None) -> SolveReport:
+    """``egsolve::solve`` (solver.hpp:86-87) for ``Variant.GPU``."""
+    if variant != Variant.GPU:
+        raise InvalidConfigError("this library implements only the GPU variant")
+    options = options or SolverOptions()
+    opts = options.to_c()
+    view = arena.view()
+    out = np.empty(arena.num_vertices, dtype=np.int64)
+    st = GpuStats()
+    _check(lib.egs_gpu_solve(C.byref(view), C.byref(opts), out.ctypes.data, C.byref(st)))
+    return _report(out, st, options.workers)
+
+
+def write_solution(arena: GameArena, measure) -> str:
+    """``write_solution(make_solution(arena, report))`` (io.cpp:178-210)."""
+    f = measure.measure if isinstance(measure, SolveReport) else measure
+    f = np.ascontiguousarray(f, dtype=np.int64)
+    view = arena.view()
+    n = lib.egs_write_solution(C.byref(view), f.ctypes.data, None, 0)
+    if n < 0:
+        _check(int(-n))
+    buf = C.create_string_buffer(int(n))
+    lib.egs_write_solution(C.byref(view), f.ctypes.data, buf, n)
+    return buf.raw[:n].decode()
+
+
+class DeviceSolver:
+    """Device-resident context (egs_ctx_*): upload once, solve many times."""
+
+    def __init__(self, arena: GameArena, options: Optional[SolverOptions] = None):
+        self.arena = arena
+        self.options = options or SolverOptions()
+        self._opts = self.options.to_c()
+        self._view = arena.view()
+        self._ctx = _P()
+        self.upload_stats = GpuStats()
+        _check(lib.egs_ctx_create(C.byref(self._view), C.byref(self._opts),
+                                  C.byref(self._ctx), C.byref(self.upload_stats)))
+
+    def solve(self) -> GpuStats:
+        st = GpuStats()
+        _check(lib.egs_ctx_solve(self._ctx, C.byref(st)))
+        return st
+
+    def read_measure(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        if out is None:
+            out = np.empty(self.arena.num_vertices, dtype=np.int64)
+        _check(lib.egs_ctx_read_measure(self._ctx, out.ctypes.data))
+        return out
+
+    def is_progress_measure(self, f: np.ndarray) -> bool:
+        f = np.ascontiguousarray(f, dtype=np.int64)
+        r = lib.egs_ctx_is_progress_measure(self._ctx, f.ctypes.data)
+        if r < 0:
+            _check(-r)
+        return bool(r)
+
+    def close(self):
+        if self._ctx:
+            lib.egs_ctx_destroy(self._ctx)
+            self._ctx = _P()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

@@ -1,0 +1,196 @@
+"""Parity of the CUDA path against the oracle and the compiled reference.
+
+Every case goes through the C-ABI (egs_gpu_solve / egs_ctx_*) and is compared
+bit-for-bit with the reference's least progress measure and byte-for-byte
+with its write_solution text."""
+import numpy as np
+import pytest
+
+from arena_gen import chain_arena, random_arena
+from oracle_bindings import INT64_MAX, fnv1a64
+
+pytestmark = pytest.mark.gpu
+
+MODES = ["auto", "dense", "sparse"]
+
+
+def _opts(egs, **kw):
+    return egs.SolverOptions(**kw)
+
+
+def _solve(egs, a, **kw):
+    return egs.solve(a, options=_opts(egs, **kw))
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("certify", [True, False])
+def test_spec_fixtures(egs, golden, mode, certify):
+    for key, rec in golden.items():
+        if not key.startswith("spec/"):
+            continue
+        a = egs.GameArena.build(rec["n"], [tuple(e) for e in rec["edges"]], rec["owners"])
+        rep = _solve(egs, a, mode=mode, certify=certify)
+        assert egs.write_solution(a, rep) == rec["solution"], key
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("certify", [True, False])
+def test_random_small_arenas(egs, oracle, mode, certify):
+    for seed in range(150):
+        n, edges, owners = random_arena(seed, max_n=16, max_deg=5)
+        a = egs.GameArena.build(n, edges, owners)
+        g = oracle.build(n, edges, owners)
+        want, _ = oracle.solve_seq(g)
+        rep = _solve(egs, a, mode=mode, certify=certify, cert_interval=1)
+        assert np.array_equal(rep.measure, want), (seed, mode, certify)
+        assert egs.write_solution(a, rep) == oracle.write_solution(g, want)
+        assert np.array_equal(rep.w1, np.nonzero(want == INT64_MAX)[0])
+
+
+def test_random_medium_arenas_all_lane_widths(egs, oracle):
+    # average degree 1..40 exercises lanes 1, 2, 4, 8, 16, 32
+    for seed, deg in enumerate([1, 2, 3, 5, 9, 17, 40]):
+        n, edges, owners = random_arena(1000 + seed, max_n=300, max_deg=2 * deg - 1, W=50)
+        a = egs.GameArena.build(n, edges, owners)
+        g = oracle.build(n, edges, owners)
+        want, _ = oracle.solve_seq(g)
+        for mode in MODES:
+            rep = _solve(egs, a, mode=mode)
+            assert np.array_equal(rep.measure, want), (seed, deg, mode)
+
+
+def test_slow_climb_gadget(egs, oracle):
+    n, edges, owners = chain_arena(20, w_cycle=-1, exit_w=-300)
+    a = egs.GameArena.build(n, edges, owners)
+    g = oracle.build(n, edges, owners)
+    want, _ = oracle.solve_seq(g)
+    for certify in (True, False):
+        rep = _solve(egs, a, certify=certify)
+        assert np.array_equal(rep.measure, want)
+
+
+def test_heavy_rows(egs, oracle):
+    # hubs longer than the heavy threshold take the CTA-per-row kernel
+    import random
+    r = random.Random(5)
+    n = 3000
+    owners = [v & 1 for v in range(n)]
+    edges = []
+    for v in range(n):
+        deg = 5000 if v in (0, 1, 7, 8) else r.randint(1, 3)
+        for _ in range(deg):
+            edges.append((v, r.randrange(n), r.randint(-100, 100)))
+    a = egs.GameArena.build(n, edges, owners)
+    g = oracle.build(n, edges, owners)
+    want, _ = oracle.solve_sweep(g)
+    for mode in MODES:
+        rep = _solve(egs, a, mode=mode)
+        assert np.array_equal(rep.measure, want), mode
+
+
+GOLDEN_SMALL = [
+    ("fixed/10000/4/100/1", lambda e: e.GameArena.fixed(10000, 4, 100, 1)),
+    ("fixed/1000/8/1000/1", lambda e: e.GameArena.fixed(1000, 8, 1000, 1)),
+    ("fixed/1000/8/100000/1", lambda e: e.GameArena.fixed(1000, 8, 100000, 1)),
+    ("fixed/2000/16/100/1", lambda e: e.GameArena.fixed(2000, 16, 100, 1)),
+    ("fixed/3000/2/50/1", lambda e: e.GameArena.fixed(3000, 2, 50, 1)),
+    ("rmat/12/16/100/1", lambda e: e.GameArena.rmat(12, 16, 100, 1)),
+    ("rmat/14/16/100/1", lambda e: e.GameArena.rmat(14, 16, 100, 1)),
+]
+
+
+@pytest.mark.parametrize("key,make", GOLDEN_SMALL, ids=[k for k, _ in GOLDEN_SMALL])
+@pytest.mark.parametrize("mode", MODES)
+def test_canonical_golden_small(egs, golden, key, make, mode):
+    rec = golden[key]
+    a = make(egs)
+    rep = _solve(egs, a, mode=mode)
+    sol = egs.write_solution(a, rep).encode()
+    assert (len(sol), f"{fnv1a64(sol):016x}") == (rec["solution_bytes"], rec["solution_fnv"])
+    assert int((rep.measure == INT64_MAX).sum()) == rec["tops"]
+
+
+def test_c1_plain_value_iteration_matches(egs, golden):
+    """certify=False runs the reference's own iteration to credit_cap."""
+    rec = golden["fixed/10000/4/100/1"]
+    a = egs.GameArena.fixed(10000, 4, 100, 1)
+    rep = _solve(egs, a, certify=False)
+    sol = egs.write_solution(a, rep).encode()
+    assert f"{fnv1a64(sol):016x}" == rec["solution_fnv"]
+    assert rep.gpu["certified"] == 0
+    assert rep.rounds > 1000  # the top climb to M_G really ran
+
+
+GOLDEN_BIG = [
+    ("fixed/100000/4/100/1", (100000, 4, 100)),
+    ("fixed/100000/8/1000/1", (100000, 8, 1000)),
+    ("fixed/100000/16/100/1", (100000, 16, 100)),
+    ("fixed/100000/8/100000/1", (100000, 8, 100000)),
+]
+
+
+@pytest.mark.parametrize("key,args", GOLDEN_BIG, ids=[k for k, _ in GOLDEN_BIG])
+def test_canonical_golden_1e5(egs, golden, key, args):
+    if key not in golden:
+        pytest.skip("golden vector not generated")
+    rec = golden[key]
+    a = egs.GameArena.fixed(*args, 1)
+    rep = _solve(egs, a)
+    sol = egs.write_solution(a, rep).encode()
+    assert f"{fnv1a64(sol):016x}" == rec["solution_fnv"]
+    assert rep.gpu["value_bits"] == (64 if rec["credit_cap"] >= 2 ** 32 - 1 else 32)
+
+
+def test_rmat16_golden(egs, golden):
+    key = "rmat/16/16/100/1"
+    if key not in golden:
+        pytest.skip("golden vector not generated")
+    a = egs.GameArena.rmat(16, 16, 100, 1)
+    rep = _solve(egs, a)
+    sol = egs.write_solution(a, rep).encode()
+    assert f"{fnv1a64(sol):016x}" == golden[key]["solution_fnv"]
+
+
+def test_value_width_boundary(egs, oracle):
+    # credit_cap = 2^32 - 2 stays on the u32 path, 2^32 - 1 takes u64
+    for cap in (2 ** 32 - 2, 2 ** 32 - 1):
+        x = [cap // 3, cap // 3, cap - 2 * (cap // 3)]
+        edges = [(0, 1, -x[0]), (1, 2, -x[1]), (2, 0, -x[2]), (0, 0, 3), (1, 1, 1),
+                 (2, 2, 0), (2, 1, 7)]
+        owners = [1, 0, 1]
+        a = egs.GameArena.build(3, edges, owners)
+        assert a.credit_cap == cap
+        g = oracle.build(3, edges, owners)
+        want, _ = oracle.solve_seq(g)
+        rep = _solve(egs, a)
+        assert np.array_equal(rep.measure, want)
+        assert rep.gpu["value_bits"] == (32 if cap < 2 ** 32 - 1 else 64)
+
+
+def test_device_context_reuse_and_epm(egs, oracle):
+    a = egs.GameArena.fixed(5000, 8, 1000, 3)
+    g = oracle.fixed(5000, 8, 1000, 3)
+    want, _ = oracle.solve_sweep(g)
+    with egs.DeviceSolver(a) as ds:
+        for _ in range(3):
+            ds.solve()
+            assert np.array_equal(ds.read_measure(), want)
+        assert ds.is_progress_measure(want)
+        bad = want.copy()
+        fin = np.nonzero(bad != INT64_MAX)[0]
+        bad[fin[bad[fin].argmax()]] = 0
+        assert ds.is_progress_measure(bad) == oracle.is_progress_measure(g, bad)
+
+
+def test_round_bound_and_timeout(egs):
+    a = egs.GameArena.fixed(10000, 4, 100, 1)
+    with pytest.raises(egs.BoundExhaustedError):
+        _solve(egs, a, certify=False, sweep_bound=10)
+
+
+def test_empty_and_single_vertex(egs):
+    a = egs.GameArena.build(0, [], [])
+    rep = _solve(egs, a)
+    assert rep.measure.shape == (0,)
+    a = egs.GameArena.build(1, [(0, 0, -7)], [1])
+    assert _solve(egs, a).measure.tolist() == [INT64_MAX]
