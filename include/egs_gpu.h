@@ -98,6 +98,10 @@ typedef struct egs_gpu_stats {
   uint64_t lift_bytes;     /* algorithmic bytes moved by the lift kernels */
   uint32_t value_bits;     /* 32 or 64: device value width chosen */
   uint32_t lanes;          /* lanes per vertex in the light lift */
+  uint64_t kernel_launches;   /* device kernels launched by the solve */
+  uint64_t lift_launches;     /* of which lift kernels (k_lift*) */
+  double cert_kernel_seconds; /* device time inside certificate kernels */
+  double activate_kernel_seconds; /* device time inside activation kernels */
 } egs_gpu_stats;
 
 void egs_gpu_opts_default(egs_gpu_opts* opts);

@@ -28,12 +28,14 @@ from ._native import (  # noqa: F401
     InternalInvariantError,
     InvalidConfigError,
     OverflowError_,
+    PinnedBuffer,
     SolveReport,
     SolverOptions,
     TimeoutError_,
     Variant,
     lib,
     lib_path,
+    pinned_empty,
     solve,
     write_solution,
 )
@@ -47,12 +49,14 @@ __all__ = [
     "InternalInvariantError",
     "InvalidConfigError",
     "OverflowError_",
+    "PinnedBuffer",
     "SolveReport",
     "SolverOptions",
     "TimeoutError_",
     "Variant",
     "lib",
     "lib_path",
+    "pinned_empty",
     "solve",
     "write_solution",
 ]

@@ -112,6 +112,8 @@ class GpuStats(C.Structure):
         [(k, C.c_uint64) for k in _STAT_U64]
         + [(k, C.c_double) for k in _STAT_F64]
         + [("lift_bytes", C.c_uint64), ("value_bits", C.c_uint32), ("lanes", C.c_uint32)]
+        + [("kernel_launches", C.c_uint64), ("lift_launches", C.c_uint64),
+           ("cert_kernel_seconds", C.c_double), ("activate_kernel_seconds", C.c_double)]
     )
 
     def as_dict(self) -> dict:
@@ -338,17 +340,49 @@ def _report(measure: np.ndarray, st: GpuStats, workers: int) -> SolveReport:
 
 
 def solve(arena: GameArena, variant: Variant = Variant.GPU,
-          options: Optional[SolverOptions] = None) -> SolveReport:
-    """``egsolve::solve`` (solver.hpp:86-87) for ``Variant.GPU``."""
+          options: Optional[SolverOptions] = None,
+          out: Optional[np.ndarray] = None) -> SolveReport:
+    """``egsolve::solve`` (solver.hpp:86-87) for ``Variant.GPU``.  ``out``
+    (int64[n], e.g. pinned via ``pinned_empty``) receives the measure."""
     if variant != Variant.GPU:
         raise InvalidConfigError("this library implements only the GPU variant")
     options = options or SolverOptions()
     opts = options.to_c()
     view = arena.view()
-    out = np.empty(arena.num_vertices, dtype=np.int64)
+    if out is None:
+        out = np.empty(arena.num_vertices, dtype=np.int64)
+    elif out.dtype != np.int64 or out.shape != (arena.num_vertices,) or not out.flags.c_contiguous:
+        raise InvalidConfigError("out must be a contiguous int64 array of num_vertices")
     st = GpuStats()
     _check(lib.egs_gpu_solve(C.byref(view), C.byref(opts), out.ctypes.data, C.byref(st)))
     return _report(out, st, options.workers)
+
+
+class PinnedBuffer:
+    """Page-locked host memory from egs_host_alloc_pinned (freed with the object)."""
+
+    def __init__(self, nbytes: int):
+        self.nbytes = int(nbytes)
+        self.ptr = lib.egs_host_alloc_pinned(max(self.nbytes, 1))
+        if not self.ptr:
+            raise CudaError("cudaMallocHost failed")
+
+    def array(self, dtype, count: int) -> np.ndarray:
+        buf = (C.c_uint8 * self.nbytes).from_address(self.ptr)
+        return np.frombuffer(buf, dtype=dtype, count=count)
+
+    def __del__(self):
+        p = getattr(self, "ptr", None)
+        if p:
+            lib.egs_host_free_pinned(p)
+            self.ptr = None
+
+
+def pinned_empty(count: int, dtype=np.int64):
+    """(array, owner): a page-locked numpy array; keep ``owner`` alive."""
+    dt = np.dtype(dtype)
+    pb = PinnedBuffer(count * dt.itemsize)
+    return pb.array(dt, count), pb
 
 
 def write_solution(arena: GameArena, measure) -> str:

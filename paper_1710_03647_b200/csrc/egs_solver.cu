@@ -118,7 +118,7 @@ struct egs_ctx {
   // pinned mirrors
   uint32_t* h_counts = nullptr;
   unsigned long long* h_ctr = nullptr;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev[8] = {};
   bool solved = false;
 
   egs::DevArena arena() const {
@@ -318,6 +318,8 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
   const egs_gpu_opts& o = c->opts;
   const size_t words = ((size_t)n + 31) / 32;
   const double vs = sizeof(V);
+  uint64_t launches = 0, lift_launches = 0;
+  double cert_ms = 0, act_ms = 0;
   int cur = 0;
   int frb = 0;
 
@@ -325,6 +327,7 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
   CK(cudaMemsetAsync(c->ctr, 0, egs::kNumCounters * sizeof(unsigned long long), s));
   CK(cudaMemsetAsync(c->bm[0], 0, words * 4, s));
   CK(cudaEventRecord(c->ev[2], s));
+  ++launches;
   egs::k_seed<V, G><<<c->grid_for(n, G), 256, 0, s>>>(
       g, f[0], f[1], c->wit, c->bm[0], c->fr[0], c->dcounts + 1);
   CK(cudaGetLastError());
@@ -379,6 +382,9 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
     }
     CK(cudaEventRecord(c->ev[0], s));
     egs::k_lift<V, G><<<c->grid_for(items, G), 256, 0, s>>>(a);
+    ++launches;
+    ++lift_launches;
+    if (c->nheavy) ++launches, ++lift_launches;
     if (c->nheavy)
       egs::k_lift_heavy<V><<<std::min<uint32_t>(c->nheavy, c->num_sms * 4),
                              512, 0, s>>>(a, c->heavy, c->nheavy, c->bm[frb]);
@@ -387,6 +393,7 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
     if (dense) {
       cur ^= 1;
     } else {
+      ++launches;
       egs::k_commit<V><<<c->grid_for(items, 1), 256, 0, s>>>(
           f[cur], f[cur ^ 1], c->changed, c->dcounts + 0);
       CK(cudaGetLastError());
@@ -419,9 +426,12 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
     if (o.certify && rounds >= next_cert) {
       ++cert_attempts;
       const unsigned long long before = c->h_ctr[egs::kCertified];
+      CK(cudaEventRecord(c->ev[4], s));
+      ++launches;
       egs::k_cert_init<V><<<c->grid_for(n, 1), 256, 0, s>>>(f[cur], c->cand, n);
       for (;;) {
         CK(cudaMemsetAsync(c->dcounts + 3, 0, sizeof(uint32_t), s));
+        ++launches;
         egs::k_cert_prune<V, G><<<c->grid_for(n, G), 256, 0, s>>>(
             g, f[cur], c->cand, c->dcounts + 3);
         CK(cudaGetLastError());
@@ -429,10 +439,17 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
         pull_counts(c);
         if (c->h_counts[3] == 0) break;
       }
+      ++launches;
       egs::k_cert_apply<V><<<c->grid_for(n, 1), 256, 0, s>>>(
           f[cur], c->cand, n, c->changed, c->dcounts + 0, c->ctr);
       CK(cudaGetLastError());
+      CK(cudaEventRecord(c->ev[5], s));
       pull_counts(c);
+      {
+        float cm = 0;
+        CK(cudaEventElapsedTime(&cm, c->ev[4], c->ev[5]));
+        cert_ms += cm;
+      }
       changed = c->h_counts[0];
       certified_any = c->h_ctr[egs::kCertified] > before;
       if (!certified_any) K = std::min(K * 2, 64);
@@ -446,11 +463,19 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
       const int nb = frb ^ 1;
       CK(cudaMemsetAsync(c->bm[nb], 0, words * 4, s));
       CK(cudaMemsetAsync(c->dcounts + 1 + nb, 0, sizeof(uint32_t), s));
+      CK(cudaEventRecord(c->ev[6], s));
+      ++launches;
       egs::k_activate<V, G><<<c->grid_for(changed, G), 256, 0, s>>>(
           g, f[cur], c->changed, c->dcounts + 0, c->bm[nb], c->fr[nb],
           c->dcounts + 1 + nb, c->ctr);
       CK(cudaGetLastError());
+      CK(cudaEventRecord(c->ev[7], s));
       pull_counts(c);
+      {
+        float am = 0;
+        CK(cudaEventElapsedTime(&am, c->ev[6], c->ev[7]));
+        act_ms += am;
+      }
       frb = nb;
       fr_n = c->h_counts[1 + nb];
       if (fr_n == 0) break;
@@ -482,6 +507,10 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
     st->lift_bytes = (uint64_t)lift_bytes;
     st->value_bits = (uint32_t)c->vbits;
     st->lanes = (uint32_t)c->lanes;
+    st->kernel_launches = launches;
+    st->lift_launches = lift_launches;
+    st->cert_kernel_seconds = cert_ms * 1e-3;
+    st->activate_kernel_seconds = act_ms * 1e-3;
   }
 }
 
