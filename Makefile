@@ -21,7 +21,7 @@ REF_LIB    := oracle/_ref/libegsolve_ref.so
 
 all: $(LIB) $(ORACLE_LIB) $(ORACLE_CLI) ref
 
-$(CSRC)/egs_solver.o: $(CSRC)/egs_solver.cu $(CSRC)/egs_kernels.cuh $(CSRC)/egs_device.cuh include/egs_gpu.h
+$(CSRC)/egs_solver.o: $(CSRC)/egs_solver.cu $(CSRC)/egs_solve.cuh $(CSRC)/egs_build.cuh $(CSRC)/egs_device.cuh include/egs_gpu.h
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/egs_solver.ptxas.log || (cat $(CSRC)/egs_solver.ptxas.log; false)
 
 $(CSRC)/egs_host.o: $(CSRC)/egs_host.cpp include/egs_gpu.h

@@ -68,6 +68,9 @@ typedef struct egs_gpu_opts {
   int32_t certify;         /* 1: losing-region certificate (exact, default);
                               0: plain value iteration up to credit_cap */
   int32_t cert_interval;   /* rounds between certificate attempts (0 = 4) */
+  int32_t sparse_div;      /* next round is sparse iff estimated frontier *
+                              sparse_div < n (0 = 4) */
+  int32_t grid_ctas;       /* persistent-kernel CTAs; 0 = auto */
   int32_t mode;            /* EGS_MODE_* */
   int32_t debug_checks;    /* SolverOptions::debug_checks: monotonicity and
                               fixpoint verification on the device */
@@ -76,32 +79,38 @@ typedef struct egs_gpu_opts {
                               |E|*(cap+1)+1 (solver_par.cpp:94-98) */
 } egs_gpu_opts;
 
-/* SolveReport counters (solver.hpp:47-59) plus device timings. */
+/* SolveReport counters (solver.hpp:47-59) plus device timings.  The whole
+ * solve is ONE persistent kernel (k_solve); its phases are timed on the
+ * device with %globaltimer at the grid barriers that separate them. */
 typedef struct egs_gpu_stats {
   uint64_t lifts;          /* lift applications that raised a value */
   uint64_t applications;   /* full lift applications (row scans) */
-  uint64_t pops;           /* worklist extractions (sparse rounds) */
+  uint64_t pops;           /* frontier entries of sparse rounds */
   uint64_t rounds;         /* lift rounds */
-  uint64_t edges_relaxed;  /* f(t) - w evaluations inside lifts */
-  uint64_t witness_checks; /* player-0 lifts skipped by the witness edge */
+  uint64_t edges_relaxed;  /* f(t) - w evaluations = sum of outdeg of applications */
+  uint64_t witness_checks; /* player-0 lifts skipped by a satisfied witness edge */
   uint64_t dense_rounds;
   uint64_t sparse_rounds;
   uint64_t cert_attempts;  /* losing-region certificate attempts */
   uint64_t cert_passes;    /* pruning passes over all attempts */
   uint64_t certified;      /* vertices proven losing (set to top) */
   uint64_t activations;    /* predecessor slots scanned by the worklist */
+  uint64_t visits;         /* vertices examined by lift phases */
+  uint64_t cert_rows;      /* rows visited by certificate passes */
+  uint64_t cert_edges;     /* edges evaluated by certificate passes */
   double upload_seconds;   /* H2D + device arena construction */
-  double solve_seconds;    /* device time from seed to fixpoint */
-  double download_seconds; /* D2H of the measure */
+  double solve_seconds;    /* device time from seed to fixpoint (CUDA events) */
+  double download_seconds; /* device export + D2H of the measure */
   double wall_seconds;     /* call entry to return (SolveReport::wall_seconds) */
-  double lift_kernel_seconds; /* device time inside lift kernels */
-  uint64_t lift_bytes;     /* algorithmic bytes moved by the lift kernels */
+  double seed_seconds;     /* device time per phase kind inside k_solve */
+  double lift_seconds;
+  double cert_seconds;
+  double activate_seconds;
+  uint64_t algo_bytes;     /* algorithmic bytes of the whole solve */
+  uint64_t lift_bytes;     /* of which the lift phases */
+  uint64_t kernel_launches;/* device kernels launched by the solve */
   uint32_t value_bits;     /* 32 or 64: device value width chosen */
-  uint32_t lanes;          /* lanes per vertex in the light lift */
-  uint64_t kernel_launches;   /* device kernels launched by the solve */
-  uint64_t lift_launches;     /* of which lift kernels (k_lift*) */
-  double cert_kernel_seconds; /* device time inside certificate kernels */
-  double activate_kernel_seconds; /* device time inside activation kernels */
+  uint32_t grid_ctas;      /* CTAs of the persistent solve kernel */
 } egs_gpu_stats;
 
 void egs_gpu_opts_default(egs_gpu_opts* opts);

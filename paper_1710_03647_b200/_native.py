@@ -89,6 +89,8 @@ class GpuOpts(C.Structure):
         ("device", C.c_int32),
         ("certify", C.c_int32),
         ("cert_interval", C.c_int32),
+        ("sparse_div", C.c_int32),
+        ("grid_ctas", C.c_int32),
         ("mode", C.c_int32),
         ("debug_checks", C.c_int32),
         ("timeout_seconds", C.c_double),
@@ -99,11 +101,11 @@ class GpuOpts(C.Structure):
 _STAT_U64 = [
     "lifts", "applications", "pops", "rounds", "edges_relaxed", "witness_checks",
     "dense_rounds", "sparse_rounds", "cert_attempts", "cert_passes", "certified",
-    "activations",
+    "activations", "visits", "cert_rows", "cert_edges",
 ]
 _STAT_F64 = [
     "upload_seconds", "solve_seconds", "download_seconds", "wall_seconds",
-    "lift_kernel_seconds",
+    "seed_seconds", "lift_seconds", "cert_seconds", "activate_seconds",
 ]
 
 
@@ -111,9 +113,9 @@ class GpuStats(C.Structure):
     _fields_ = (
         [(k, C.c_uint64) for k in _STAT_U64]
         + [(k, C.c_double) for k in _STAT_F64]
-        + [("lift_bytes", C.c_uint64), ("value_bits", C.c_uint32), ("lanes", C.c_uint32)]
-        + [("kernel_launches", C.c_uint64), ("lift_launches", C.c_uint64),
-           ("cert_kernel_seconds", C.c_double), ("activate_kernel_seconds", C.c_double)]
+        + [("algo_bytes", C.c_uint64), ("lift_bytes", C.c_uint64),
+           ("kernel_launches", C.c_uint64), ("value_bits", C.c_uint32),
+           ("grid_ctas", C.c_uint32)]
     )
 
     def as_dict(self) -> dict:
@@ -287,6 +289,8 @@ class SolverOptions:
     workers: int = 1
     certify: bool = True
     cert_interval: int = 4
+    sparse_div: int = 4
+    grid_ctas: int = 0
     mode: str = "auto"
     debug_checks: bool = False
     timeout_seconds: float = 0.0
@@ -302,6 +306,8 @@ class SolverOptions:
         o.device = int(self.device)
         o.certify = int(bool(self.certify))
         o.cert_interval = int(self.cert_interval)
+        o.sparse_div = int(self.sparse_div)
+        o.grid_ctas = int(self.grid_ctas)
         o.mode = _MODES[self.mode]
         o.debug_checks = int(bool(self.debug_checks))
         o.timeout_seconds = float(self.timeout_seconds)

@@ -1,0 +1,179 @@
+// egs_build.cuh — device-side arena construction:
+// the reference CSR (GameArena::build, proj/src/arena.cpp:17-78) is uploaded
+// as-is and rebuilt on the device into the solver layout:
+//
+//   * vertices relabelled into six contiguous ranges by (owner, out-degree
+//     class): the owner-sorted order of reorder_by_owner (arena.cpp:119-149;
+//     PAPER.md:506-511) refined by row length, stable inside each range;
+//   * rows re-packed as 8-byte edge records {u32 dst (relabelled), i32 w}
+//     (weights are validated to fit int32; arena.hpp:13 stores int64);
+//   * the predecessor transpose (CSC, arena.cpp:56-74; the paper's CUSPARSE
+//     csr2csc) built by a radix sort of (dst, src) pairs.
+//
+// Every kernel here runs once per arena upload, not per solve.
+#pragma once
+
+#include <cstdint>
+
+#include "egs_device.cuh"
+#include "egs_solve.cuh"
+
+namespace egs {
+
+// Class key of every vertex + histogram of the six classes; edge validation.
+__global__ void k_classify(uint32_t n, const uint64_t* off64, const uint8_t* owner,
+                           uint8_t* key, uint32_t* val, unsigned int* hist) {
+  __shared__ unsigned int s_hist[kNumClasses];
+  if (threadIdx.x < kNumClasses) s_hist[threadIdx.x] = 0;
+  __syncthreads();
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += gridDim.x * blockDim.x) {
+    const uint64_t deg = off64[v + 1] - off64[v];
+    const int cls = (owner[v] ? 3 : 0) + (deg <= kLightMax ? 0 : deg <= kMediumMax ? 1 : 2);
+    key[v] = (uint8_t)cls;
+    val[v] = v;
+    atomicAdd(&s_hist[cls], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < kNumClasses && s_hist[threadIdx.x])
+    atomicAdd(hist + threadIdx.x, s_hist[threadIdx.x]);
+}
+
+// bad |= 1: weight outside int32;  bad |= 2: target out of range.
+__global__ void k_validate(uint32_t n, uint64_t m, const uint32_t* dst,
+                           const int64_t* w64, unsigned int* bad) {
+  unsigned int b = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const int64_t w = w64[i];
+    if (w < -2147483647LL || w > 2147483647LL) b |= 1u;
+    if (dst[i] >= n) b |= 2u;
+  }
+  b = __reduce_or_sync(0xffffffffu, b);
+  if (lane_id() == 0 && b) atomicOr(bad, b);
+}
+
+// perm[old] = new; new row lengths (exclusive-scanned into offsets next).
+__global__ void k_permute(uint32_t n, const uint32_t* inv, const uint64_t* off64,
+                          uint32_t* perm, uint32_t* deg_new) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += gridDim.x * blockDim.x) {
+    const uint32_t o = inv[i];
+    perm[o] = i;
+    deg_new[i] = (uint32_t)(off64[o + 1] - off64[o]);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) deg_new[n] = 0;
+}
+
+// Copy every row into its relabelled slot, mapping targets through perm;
+// also emit the (dst, src) pairs for the transpose.  A warp handles 32 new
+// rows and expands their edges as one flat coalesced stream (warp_expand),
+// so short and long rows cost the same per edge.
+__global__ void __launch_bounds__(256)
+    k_relabel_edges(uint32_t n, const uint32_t* inv, const uint64_t* off64,
+                    const uint32_t* dst, const int64_t* w64, const uint32_t* perm,
+                    const uint32_t* off_new, int2* edge, uint32_t* ckey,
+                    uint32_t* cval) {
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (uint32_t r0 = gw * 32; r0 < n; r0 += nwarps * 32) {
+    const uint32_t r = r0 + lane_id();
+    uint32_t b = 0, e = 0, delta = 0;
+    if (r < n) {
+      const uint32_t o = inv[r];
+      b = (uint32_t)off64[o];
+      e = (uint32_t)off64[o + 1];
+      delta = off_new[r] - b;
+    }
+    warp_expand(b, e, [&](bool valid, uint32_t idx, uint32_t owner_lane) {
+      const uint32_t d = __shfl_sync(0xffffffffu, delta, owner_lane);
+      if (valid) {
+        const uint32_t pos = idx + d;
+        const uint32_t t = perm[dst[idx]];
+        edge[pos] = make_int2((int)t, (int)w64[idx]);
+        ckey[pos] = t;
+        cval[pos] = r0 + owner_lane;
+      }
+    });
+  }
+}
+
+// CSC column offsets from the dst-sorted keys: coff[t] = first j with
+// key[j] >= t, coff[n] = m.
+__global__ void k_col_offsets(uint32_t n, uint64_t m, const uint32_t* key,
+                              uint32_t* coff) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= m; j += stride) {
+    const uint32_t k = j < m ? key[j] : n;
+    const int64_t prev = j > 0 ? (int64_t)key[j - 1] : -1;
+    for (int64_t t = prev + 1; t <= (int64_t)k; ++t) coff[t] = (uint32_t)j;
+  }
+}
+
+// ---------------------------------------------------- measure I/O ----
+// out[old] = widen(f[perm[old]]): device values (u32/u64, top = all ones)
+// back to the reference raw encoding (INT64_MAX = top, energy.hpp:16).
+template <class V>
+__global__ void k_export(uint32_t n, const V* f, const uint32_t* perm, int64_t* out) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += gridDim.x * blockDim.x) {
+    const V x = f[perm[v]];
+    out[v] = x == Top<V>::v ? INT64_MAX : static_cast<int64_t>(x);
+  }
+}
+
+// fnew[perm[old]] = fin[old] (int64, raw encoding) for the verifier.
+__global__ void k_import(uint32_t n, const int64_t* fin, const uint32_t* perm,
+                         int64_t* fnew) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += gridDim.x * blockDim.x)
+    fnew[perm[v]] = fin[v];
+}
+
+// epm_condition_holds for every vertex (measure_ops.cpp:17-31) on a raw int64
+// measure in relabelled ids, with the reference's uncapped ⊖ (energy.hpp:
+// 20-31): player 0 needs some edge with f(v) >= f(t) ⊖ w, player 1 needs it
+// on every edge.  One warp per vertex so hub rows are read cooperatively.
+// *bad counts violating vertices; *overflow flags a raw_ominus overflow.
+__device__ __forceinline__ int64_t ominus_raw(int64_t ft, int32_t w, int* overflow) {
+  if (ft == INT64_MAX) return INT64_MAX;
+  if (w < 0 && ft > INT64_MAX + (int64_t)w) {
+    atomicExch(overflow, 1);
+    return INT64_MAX;
+  }
+  const int64_t c = ft - w;
+  return c < 0 ? 0 : c;
+}
+
+__global__ void __launch_bounds__(256)
+    k_epm(Graph g, const int64_t* f, unsigned long long* bad, int* overflow) {
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  unsigned long long nb = 0;
+  for (uint32_t v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < g.n; v += nwarps) {
+    const int64_t fv = f[v];
+    const bool p0 = v < g.rb[kP1L];
+    const uint32_t b = g.off[v], e = g.off[v + 1];
+    bool ok = !p0;
+    for (uint32_t i0 = b; i0 < e; i0 += 32) {
+      const uint32_t i = i0 + lane_id();
+      bool sat = true;  // f(v) >= f(t) ⊖ w on this edge
+      if (i < e) {
+        const int2 r = g.edge[i];
+        sat = fv >= ominus_raw(f[r.x], r.y, overflow);
+      }
+      if (p0) {
+        if (__any_sync(0xffffffffu, i < e && sat)) {
+          ok = true;
+          break;
+        }
+      } else if (!__all_sync(0xffffffffu, sat)) {
+        ok = false;
+        break;
+      }
+    }
+    if (!ok && lane_id() == 0) ++nb;
+  }
+  if (nb) atomicAdd(bad, nb);
+}
+
+}  // namespace egs

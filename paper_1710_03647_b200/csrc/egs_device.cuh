@@ -1,11 +1,12 @@
-// egs_device.cuh — value domain and warp/group primitives for the sm_100a
-// energy-game kernels.
+// egs_device.cuh — value domain, cache-policy loads and warp/block primitives
+// for the sm_100a energy-game kernels.
 //
 // Value domain (reference proj/include/egsolve/energy.hpp:14-31): a credit is
 // a non-negative integer or top.  On the device the measure is held in the
 // narrowest unsigned type that can represent every finite value <= credit_cap
-// (u32 when credit_cap < 2^32 - 1, else u64) with top = all-ones; the host
-// widens top back to INT64_MAX on copy-out.
+// (u32 when credit_cap < 2^32 - 1, else u64) with top = all-ones, so that
+// unsigned min/max order top above every finite credit exactly like the
+// reference's INT64_MAX sentinel; the host widens top back to INT64_MAX.
 #pragma once
 
 #include <cstdint>
@@ -28,8 +29,8 @@ struct Top<uint64_t> {
 // followed by the lift's `acc > credit_cap ? top : acc` (measure_ops.hpp:51).
 // Applying the cap per candidate is value-identical to applying it to the
 // min/max: min(c_i) > cap iff every c_i > cap; max(c_i) > cap iff some
-// c_i > cap.  Finite f(t) <= cap and |w| < 2^31, so the int64 difference
-// never overflows.
+// c_i > cap.  Finite f(t) <= cap < 2^63 - 2^31 and |w| < 2^31, so the int64
+// difference never overflows.
 template <class V>
 __device__ __forceinline__ V ominus_cap(V ft, int32_t w, int64_t cap) {
   if (ft == Top<V>::v) return Top<V>::v;
@@ -38,61 +39,122 @@ __device__ __forceinline__ V ominus_cap(V ft, int32_t w, int64_t cap) {
   return r > cap ? Top<V>::v : static_cast<V>(r);
 }
 
-__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+// u32 path (cap < 2^32 - 1): the same value, written as selects so an
+// unrolled row turns into straight-line predicated code.
+template <>
+__device__ __forceinline__ uint32_t ominus_cap<uint32_t>(uint32_t ft, int32_t w,
+                                                         int64_t cap) {
+  int64_t r = static_cast<int64_t>(ft) - static_cast<int64_t>(w);
+  r = r < 0 ? 0 : r;
+  uint32_t out = static_cast<uint32_t>(r);
+  out = r > cap ? 0xFFFFFFFFu : out;
+  return ft == 0xFFFFFFFFu ? 0xFFFFFFFFu : out;
+}
 
-// Min (player 0) or max (player 1) across the G aligned lanes of a group.
-// Every lane of the warp must call it (full-mask shuffles).
-template <int G, class T>
-__device__ __forceinline__ T group_minmax(T x, bool is_min) {
+// ------------------------------------------------------------ memory ----
+// Mutable solver state (measure, witnesses, candidate flags, bitmaps) is
+// read with ld.global.cg: it is written by other SMs inside the same
+// persistent launch, so it must come from L2, never from a stale L1 line.
+// The arena (offsets, edge records) is immutable during a solve: read-only
+// path (ld.global.nc), edge records with the streaming hint so the
+// once-per-round edge stream does not evict the L2-resident measure.
+__device__ __forceinline__ uint32_t ldcg(const uint32_t* p) { return __ldcg(p); }
+__device__ __forceinline__ uint64_t ldcg(const uint64_t* p) {
+  return (uint64_t)__ldcg(reinterpret_cast<const unsigned long long*>(p));
+}
+__device__ __forceinline__ uint8_t ldcg(const uint8_t* p) {
+  return (uint8_t)__ldcg(reinterpret_cast<const unsigned char*>(p));
+}
+__device__ __forceinline__ int2 ldcg(const int2* p) { return __ldcg(p); }
+__device__ __forceinline__ void stcg(uint32_t* p, uint32_t v) { __stcg(p, v); }
+__device__ __forceinline__ void stcg(uint64_t* p, uint64_t v) {
+  __stcg(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
+}
+__device__ __forceinline__ void stcg(uint8_t* p, uint8_t v) {
+  __stcg(reinterpret_cast<unsigned char*>(p), (unsigned char)v);
+}
+__device__ __forceinline__ void stcg(int2* p, int2 v) { __stcg(p, v); }
+__device__ __forceinline__ int2 ld_edge(const int2* p) { return __ldcs(p); }
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// ------------------------------------------------------ warp reduce ----
+__device__ __forceinline__ uint32_t warp_min(uint32_t x) {
+  return __reduce_min_sync(0xffffffffu, x);
+}
+__device__ __forceinline__ uint32_t warp_max(uint32_t x) {
+  return __reduce_max_sync(0xffffffffu, x);
+}
+__device__ __forceinline__ uint64_t warp_min(uint64_t x) {
 #pragma unroll
-  for (int s = G / 2; s > 0; s >>= 1) {
-    T y = __shfl_xor_sync(0xffffffffu, x, s);
-    x = is_min ? (y < x ? y : x) : (y > x ? y : x);
+  for (int s = 16; s > 0; s >>= 1) {
+    const uint64_t y = __shfl_xor_sync(0xffffffffu, x, s);
+    x = y < x ? y : x;
   }
   return x;
 }
-
-template <int G>
-__device__ __forceinline__ uint32_t group_mask() {
-  if constexpr (G == 32) {
-    return 0xffffffffu;
-  } else {
-    return ((1u << G) - 1u) << (lane_id() & ~(uint32_t)(G - 1));
+__device__ __forceinline__ uint64_t warp_max(uint64_t x) {
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    const uint64_t y = __shfl_xor_sync(0xffffffffu, x, s);
+    x = y > x ? y : x;
   }
+  return x;
 }
-
-template <int G>
-__device__ __forceinline__ bool group_any(bool p) {
-  return (__ballot_sync(0xffffffffu, p) & group_mask<G>()) != 0u;
-}
-
-template <int G>
-__device__ __forceinline__ bool group_all(bool p) {
-  return (__ballot_sync(0xffffffffu, p) & group_mask<G>()) == group_mask<G>();
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long x) {
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) x += __shfl_xor_sync(0xffffffffu, x, s);
+  return x;
 }
 
 // Warp-aggregated append of `val` to list[*count++] for every lane with
-// `pred`: one ballot, one atomicAdd per converged subset, popc ranks.
+// `pred`: one ballot, one atomicAdd per warp, popc ranks.  Warp-uniform call.
 __device__ __forceinline__ void warp_append(bool pred, uint32_t val,
                                             uint32_t* list, uint32_t* count) {
-  const uint32_t act = __activemask();
-  const uint32_t m = __ballot_sync(act, pred);
+  const uint32_t m = __ballot_sync(0xffffffffu, pred);
   if (m == 0u) return;
-  const uint32_t lane = lane_id();
   const int leader = __ffs(m) - 1;
   uint32_t base = 0;
-  if (lane == (uint32_t)leader) base = atomicAdd(count, (uint32_t)__popc(m));
-  base = __shfl_sync(act, base, leader);
-  if (pred) list[base + __popc(m & ((1u << lane) - 1u))] = val;
+  if (lane_id() == (uint32_t)leader) base = atomicAdd(count, (uint32_t)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (pred) list[base + __popc(m & lanemask_lt())] = val;
 }
 
-// Sum a per-thread counter over the warp and add it once to *dst.
-// Must be called by all 32 lanes.
-__device__ __forceinline__ void warp_add_u64(unsigned long long x,
-                                             unsigned long long* dst) {
+// Warp-cooperative expansion of up to 32 index segments [b, e) (one per
+// lane) into a flat stream: fn(item_index, owning_lane) is called once per
+// item, 32 items per step, so one long segment (an R-MAT hub column) is
+// shared by the whole warp instead of serialising one lane.  Warp-uniform.
+template <class Fn>
+__device__ __forceinline__ void warp_expand(uint32_t b, uint32_t e, Fn&& fn) {
+  const uint32_t lane = lane_id();
+  const uint32_t len = e - b;
+  uint32_t incl = len;
 #pragma unroll
-  for (int s = 16; s > 0; s >>= 1) x += __shfl_xor_sync(0xffffffffu, x, s);
-  if (lane_id() == 0 && x != 0ull) atomicAdd(dst, x);
+  for (int s = 1; s < 32; s <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, s);
+    if (lane >= (uint32_t)s) incl += y;
+  }
+  const uint32_t excl = incl - len;
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  for (uint32_t base = 0; base < total; base += 32) {
+    const uint32_t k = base + lane;
+    // last lane s with excl[s] <= k (excl is non-decreasing)
+    uint32_t lo = 0;
+#pragma unroll
+    for (uint32_t step = 16; step > 0; step >>= 1) {
+      const uint32_t c = lo + step;
+      const uint32_t ex = __shfl_sync(0xffffffffu, excl, c & 31u);
+      if (c < 32u && ex <= k) lo = c;
+    }
+    const uint32_t sb = __shfl_sync(0xffffffffu, b, lo);
+    const uint32_t sx = __shfl_sync(0xffffffffu, excl, lo);
+    fn(k < total, sb + (k - sx), lo);
+  }
 }
 
 }  // namespace egs

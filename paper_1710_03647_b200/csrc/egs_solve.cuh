@@ -1,0 +1,995 @@
+// egs_solve.cuh — the persistent value-iteration kernel (one launch per
+// solve, device-side convergence; no host round trip between rounds).
+//
+// It restates the reference solve path (/root/reference/proj):
+//   seed phase        solver_par.cpp:368-387 / solver_seq.cpp:136-154
+//   lift phases       raw_lift (measure_ops.hpp:32-52) applied as the rounds
+//                     of solve_frontier (solver_par.cpp:389-417, sparse) or
+//                     solve_sweep (solver_par.cpp:205-228, dense), with the
+//                     clamped store `cand > old` (solver_par.cpp:216,399)
+//   activation phase  predecessor activation + dedup (solver_par.cpp:402-410)
+//                     and the top filter of the gather (solver_par.cpp:305-311)
+//   certificate       DESIGN.md §3: proves a set of vertices losing for
+//                     player 0 so their value jumps to top instead of
+//                     climbing to credit_cap one weight at a time.
+//   termination       a lift round that raises nothing (solver_par.cpp:170-194)
+//
+// Vertices are relabelled on the device (egs_build.cuh) into six contiguous
+// ranges: player 0 light / medium / heavy, then player 1 light / medium /
+// heavy (the owner-sorted order of reorder_by_owner, arena.cpp:119-149,
+// PAPER.md:506-511, refined by out-degree).  Light rows (<= 32 edges) are
+// lifted by one thread, medium rows (<= 4096) by one warp, heavy rows (the
+// R-MAT hubs) by one CTA, so warps never mix min and max and never wait on
+// one long row.
+//
+// Phases are separated by grid-wide barriers (cooperative launch).  Updates
+// are in place (Gauss-Seidel within a round): every value read is a valid
+// under-approximation of the least fixpoint because values only rise, and a
+// round that raises nothing read only final values, so it certifies the
+// fixpoint exactly as the reference's `changed` latch does.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include <cstdint>
+
+#include "egs_device.cuh"
+
+namespace egs {
+
+namespace cg = cooperative_groups;
+
+constexpr int kBlock = 256;
+constexpr int kWarps = kBlock / 32;
+constexpr uint32_t kLightMax = 32;    // rows with <= 32 edges: one thread
+constexpr uint32_t kMediumMax = 4096; // <= 4096: one warp; longer: one CTA
+
+// Class ranges of the relabelled ids.
+enum : int { kP0L = 0, kP0M, kP0H, kP1L, kP1M, kP1H, kNumClasses };
+
+enum Counter : int {
+  kLifts = 0,      // lifts that raised a value (SolveReport::lifts)
+  kApps,           // full lift applications (row scans)
+  kEdges,          // edges relaxed = sum of out-degrees of applications
+  kWitness,        // player-0 lifts skipped by a satisfied witness edge
+  kActScanned,     // predecessor slots scanned by activation
+  kCertified,      // vertices proven losing by the certificate
+  kPops,           // sparse-round frontier entries
+  kCertScanned,    // rows visited by certificate passes
+  kCertEdges,      // edges evaluated by certificate passes
+  kVisits,         // vertices examined by lift phases (incl. top skips)
+  kRounds,
+  kDenseRounds,
+  kSparseRounds,
+  kCertAttempts,
+  kCertPasses,
+  kStatus,         // 0 fixpoint, 2 timeout, 5 round budget
+  kTimeSeed,       // ns of device time per phase kind (%globaltimer)
+  kTimeLift,
+  kTimeCert,
+  kTimeAct,
+  kNumCounters
+};
+
+enum Mode : int { kModeAuto = 0, kModeDense = 1, kModeSparse = 2 };
+
+struct Graph {
+  uint32_t n;
+  uint32_t rb[kNumClasses + 1];  // class k = [rb[k], rb[k+1])
+  const uint32_t* off;           // n+1 CSR row offsets (relabelled rows)
+  const int2* edge;              // m   {dst (relabelled), w}
+  const uint32_t* coff;          // n+1 CSC column offsets
+  const uint32_t* csrc;          // m   predecessors (relabelled)
+  int64_t cap;                   // credit_cap (M_G)
+};
+
+// Grid-shared scratch; the host zeroes it before each launch.
+struct Scratch {
+  unsigned int sum[4][4];    // per-phase-slot sums: 0 changed, 1 removed, 2 seeds
+  unsigned int dyn[4][4];    // per-phase-slot work cursors: 0 medium, 1 heavy
+  unsigned int fr_cnt[2][3]; // frontier sublist sizes [buffer][L, M, H]
+  unsigned int stop;         // timeout flag
+};
+
+template <class V>
+struct SolveParams {
+  Graph g;
+  V* f;                 // measure, relabelled ids
+  int2* wit;            // player-0 witness edge record (ids < rb[3])
+  uint32_t* chg[2];     // changed-vertex bitmaps, by round parity
+  uint32_t* frb;        // frontier membership bitmap
+  uint32_t* fr[2];      // frontier lists; sublist c starts at cbase[c]
+  uint32_t cbase[3];
+  uint8_t* cand;        // certificate candidates
+  Scratch* sh;
+  unsigned long long* ctr;  // kNumCounters
+  int mode;
+  int certify;
+  int cert_interval;
+  uint32_t sparse_div;      // next round sparse iff est. frontier * div < n
+  float avg_in_deg;
+  unsigned long long round_budget;
+  unsigned long long timeout_ns;   // 0 = none; measured from kernel start
+};
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ uint32_t vload(const volatile unsigned int* p) { return *p; }
+
+// Per-thread event counts of the current phase (u32: one phase touches every
+// row / edge at most once, so a block's sum stays below 2^32).  Flushed into
+// the u64 device counters at every phase end, so they are not live across
+// phases.
+struct Local {
+  unsigned int lifts = 0, apps = 0, edges = 0, witness = 0, act = 0, certified = 0,
+               pops = 0, cert_scanned = 0, cert_edges = 0, visits = 0;
+  unsigned int phase_count = 0;  // per-phase sum (changed / removed / seeds)
+};
+constexpr int kLocalCounters = 10;
+
+// Block-wide flush of the phase's counters: one atomicAdd per CTA and
+// counter; phase_count goes to the grid-shared slot `dst`.  Block-uniform.
+__device__ __forceinline__ void block_flush(Local& L, unsigned long long* ctr,
+                                            unsigned int* dst, unsigned int* s_cnt) {
+  unsigned int v[kLocalCounters + 1] = {L.lifts, L.apps,      L.edges,        L.witness,
+                                        L.act,   L.certified, L.pops,         L.cert_scanned,
+                                        L.cert_edges, L.visits, L.phase_count};
+  const uint32_t warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k <= kLocalCounters; ++k) v[k] = __reduce_add_sync(0xffffffffu, v[k]);
+  __syncthreads();
+  if (lane_id() == 0) {
+#pragma unroll
+    for (int k = 0; k <= kLocalCounters; ++k) s_cnt[warp * (kLocalCounters + 1) + k] = v[k];
+  }
+  __syncthreads();
+  if (threadIdx.x <= (unsigned)kLocalCounters) {
+    unsigned long long sum = 0;
+    for (int w = 0; w < kWarps; ++w) sum += s_cnt[w * (kLocalCounters + 1) + threadIdx.x];
+    if (sum) {
+      if (threadIdx.x < (unsigned)kLocalCounters)
+        atomicAdd(ctr + threadIdx.x, sum);
+      else
+        atomicAdd(dst, (unsigned int)sum);
+    }
+  }
+  L = Local();
+}
+
+// ============================================================== lifts ====
+// The lift of one vertex: delta(f, v) = min (player 0) / max (player 1) over
+// its row of f(t) ⊖ w, capped (raw_lift, measure_ops.hpp:32-52).  Returns
+// whether the value rose.  Player 0 first tests its witness edge (the argmin
+// of its last lift): values only rise, so while f(v) >= f(t) ⊖ w holds for
+// it the lift cannot raise f(v) and the row is not read (the GPU analogue of
+// the count(v) of Alg. 1, solver_seq.cpp:186-199).
+
+// ---- one thread per row (light rows)
+template <class V, bool P0>
+__device__ __forceinline__ bool lift_thread(const SolveParams<V>& p, uint32_t v,
+                                            Local& L) {
+  constexpr V TOP = Top<V>::v;
+  ++L.visits;
+  const V old = ldcg(p.f + v);
+  if (old == TOP) return false;
+  if (P0) {
+    const int2 we = ldcg(p.wit + v);
+    if (old >= ominus_cap<V>(ldcg(p.f + we.x), we.y, p.g.cap)) {
+      ++L.witness;
+      return false;
+    }
+  }
+  const uint32_t b = __ldg(p.g.off + v), e = __ldg(p.g.off + v + 1);
+  ++L.apps;
+  L.edges += e - b;
+  V acc = P0 ? TOP : V(0);
+  int2 best = make_int2(0, 0);
+  for (uint32_t i = b; i < e; i += 8) {
+    int2 r[8];
+    V c[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (i + k < e) r[k] = ld_edge(p.g.edge + i + k);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (i + k < e) c[k] = ominus_cap<V>(ldcg(p.f + r[k].x), r[k].y, p.g.cap);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (i + k < e) {
+        if (P0) {
+          if (c[k] < acc || (k == 0 && i == b)) {
+            acc = c[k];
+            best = r[k];
+          }
+        } else {
+          acc = c[k] > acc ? c[k] : acc;
+        }
+      }
+    }
+    if (P0 ? acc == V(0) : acc == TOP) break;  // raw_lift early exits (:41,46)
+  }
+  if (P0) stcg(p.wit + v, best);
+  if (acc > old) {
+    stcg(p.f + v, acc);
+    ++L.lifts;
+    return true;
+  }
+  return false;
+}
+
+// ---- one warp per row (medium rows).  Warp-uniform.
+template <class V, bool P0>
+__device__ __forceinline__ bool lift_warp(const SolveParams<V>& p, uint32_t v,
+                                          Local& L) {
+  constexpr V TOP = Top<V>::v;
+  const uint32_t lane = lane_id();
+  if (lane == 0) ++L.visits;
+  const V old = ldcg(p.f + v);
+  if (old == TOP) return false;
+  if (P0) {
+    bool sat = false;
+    if (lane == 0) {
+      const int2 we = ldcg(p.wit + v);
+      sat = old >= ominus_cap<V>(ldcg(p.f + we.x), we.y, p.g.cap);
+    }
+    if (__shfl_sync(0xffffffffu, sat, 0)) {
+      if (lane == 0) ++L.witness;
+      return false;
+    }
+  }
+  const uint32_t b = __ldg(p.g.off + v), e = __ldg(p.g.off + v + 1);
+  if (lane == 0) {
+    ++L.apps;
+    L.edges += e - b;
+  }
+  V acc = P0 ? TOP : V(0);
+  int2 best = make_int2(0, 0);
+  bool have = false;
+  for (uint32_t i0 = b; i0 < e; i0 += 128) {
+    int2 r[4];
+    V c[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t i = i0 + k * 32 + lane;
+      if (i < e) r[k] = ld_edge(p.g.edge + i);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t i = i0 + k * 32 + lane;
+      if (i < e) c[k] = ominus_cap<V>(ldcg(p.f + r[k].x), r[k].y, p.g.cap);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t i = i0 + k * 32 + lane;
+      if (i < e) {
+        if (P0) {
+          if (!have || c[k] < acc) {
+            acc = c[k];
+            best = r[k];
+            have = true;
+          }
+        } else {
+          acc = c[k] > acc ? c[k] : acc;
+        }
+      }
+    }
+    const V red = P0 ? warp_min(acc) : warp_max(acc);
+    if (P0 ? red == V(0) : red == TOP) break;
+  }
+  const V res = P0 ? warp_min(acc) : warp_max(acc);
+  bool raised = false;
+  if (P0) {
+    const uint32_t m = __ballot_sync(0xffffffffu, have && acc == res);
+    const int src = __ffs(m) - 1;
+    best.x = __shfl_sync(0xffffffffu, best.x, src);
+    best.y = __shfl_sync(0xffffffffu, best.y, src);
+  }
+  if (lane == 0) {
+    if (P0) stcg(p.wit + v, best);
+    if (res > old) {
+      stcg(p.f + v, res);
+      ++L.lifts;
+      raised = true;
+    }
+  }
+  return __shfl_sync(0xffffffffu, raised, 0);
+}
+
+// ---- one CTA per row (heavy rows).  Block-uniform.
+template <class V>
+struct BlockScratch {
+  V val[kWarps];
+  int2 rec[kWarps];
+  unsigned int red[kWarps];
+  unsigned int item;
+  int flag;
+};
+
+template <class V, bool P0>
+__device__ __forceinline__ bool lift_block(const SolveParams<V>& p, uint32_t v,
+                                           Local& L, BlockScratch<V>& s) {
+  constexpr V TOP = Top<V>::v;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) ++L.visits;
+  const V old = ldcg(p.f + v);
+  if (old == TOP) return false;
+  if (P0) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int2 we = ldcg(p.wit + v);
+      s.flag = old >= ominus_cap<V>(ldcg(p.f + we.x), we.y, p.g.cap);
+    }
+    __syncthreads();
+    if (s.flag) {
+      if (threadIdx.x == 0) ++L.witness;
+      return false;
+    }
+  }
+  const uint32_t b = __ldg(p.g.off + v), e = __ldg(p.g.off + v + 1);
+  if (threadIdx.x == 0) {
+    ++L.apps;
+    L.edges += e - b;
+  }
+  V acc = P0 ? TOP : V(0);
+  int2 best = make_int2(0, 0);
+  bool have = false;
+  for (uint32_t i0 = b; i0 < e; i0 += 4 * kBlock) {
+    int2 r[4];
+    V c[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t i = i0 + k * kBlock + threadIdx.x;
+      if (i < e) r[k] = ld_edge(p.g.edge + i);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t i = i0 + k * kBlock + threadIdx.x;
+      if (i < e) c[k] = ominus_cap<V>(ldcg(p.f + r[k].x), r[k].y, p.g.cap);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t i = i0 + k * kBlock + threadIdx.x;
+      if (i < e) {
+        if (P0) {
+          if (!have || c[k] < acc) {
+            acc = c[k];
+            best = r[k];
+            have = true;
+          }
+        } else {
+          acc = c[k] > acc ? c[k] : acc;
+        }
+      }
+    }
+    const bool done = P0 ? acc == V(0) : acc == TOP;
+    if (__syncthreads_or(done)) break;
+  }
+  // block reduction (value, then the witness record of a minimising lane)
+  V wv = P0 ? warp_min(acc) : warp_max(acc);
+  int2 wr = best;
+  if (P0) {
+    const uint32_t m = __ballot_sync(0xffffffffu, have && acc == wv);
+    const int src = m ? __ffs(m) - 1 : 0;
+    wr.x = __shfl_sync(0xffffffffu, best.x, src);
+    wr.y = __shfl_sync(0xffffffffu, best.y, src);
+    if (!m) wv = TOP;
+  }
+  __syncthreads();
+  if (lane == 0) {
+    s.val[warp] = wv;
+    s.rec[warp] = wr;
+  }
+  __syncthreads();
+  bool raised = false;
+  if (threadIdx.x == 0) {
+    V res = s.val[0];
+    int2 rec = s.rec[0];
+    for (int w = 1; w < kWarps; ++w) {
+      if (P0 ? s.val[w] < res : s.val[w] > res) {
+        res = s.val[w];
+        rec = s.rec[w];
+      }
+    }
+    if (P0) stcg(p.wit + v, rec);
+    if (res > old) {
+      stcg(p.f + v, res);
+      ++L.lifts;
+      raised = true;
+    }
+    s.flag = raised;
+  }
+  __syncthreads();
+  raised = s.flag;
+  __syncthreads();
+  return raised;
+}
+
+__device__ __forceinline__ void set_bit(uint32_t* bm, uint32_t v) {
+  atomicOr(bm + (v >> 5), 1u << (v & 31u));
+}
+
+// Light rows of the class ranges [lo, hi) in a dense round: aligned 32-vertex
+// words per warp so a warp publishes its changed bits with one atomicOr.
+template <class V, bool P0>
+__device__ __noinline__ void dense_light(const SolveParams<V>& p, uint32_t lo,
+                                            uint32_t hi, uint32_t* chg,
+                                            unsigned int* sum_dst) {
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  Local L;
+  const uint32_t nwarps = gridDim.x * kWarps;
+  const uint32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const uint32_t w0 = lo >> 5, w1 = (hi + 31) >> 5;
+  for (uint32_t w = w0 + gw; w < w1; w += nwarps) {
+    const uint32_t v = (w << 5) + lane_id();
+    bool ch = false;
+    if (v >= lo && v < hi) ch = lift_thread<V, P0>(p, v, L);
+    const uint32_t m = __ballot_sync(0xffffffffu, ch);
+    if (m && lane_id() == 0) atomicOr(chg + w, m);
+    L.phase_count += ch;
+  }
+  block_flush(L, p.ctr, sum_dst, s_cnt);
+}
+
+// Light rows of a sparse frontier list, one thread each.
+template <class V>
+__device__ __noinline__ void sparse_light(const SolveParams<V>& p, const uint32_t* list,
+                                          uint32_t count, uint32_t* chg,
+                                          unsigned int* sum_dst) {
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  Local L;
+  const uint32_t nthreads = gridDim.x * kBlock;
+  for (uint32_t i = blockIdx.x * kBlock + threadIdx.x; i < count; i += nthreads) {
+    const uint32_t v = ldcg(list + i);
+    const bool ch = v < p.g.rb[kP1L] ? lift_thread<V, true>(p, v, L)
+                                     : lift_thread<V, false>(p, v, L);
+    if (ch) {
+      set_bit(chg, v);
+      ++L.phase_count;
+    }
+  }
+  block_flush(L, p.ctr, sum_dst, s_cnt);
+}
+
+// Medium rows: warps claim rows from a per-phase cursor.  `items(i)` maps a
+// claim index to a vertex.
+template <class V, class Items>
+__device__ __noinline__ void warp_rows(const SolveParams<V>& p, uint32_t count,
+                                          unsigned int* cursor, Items items,
+                                          uint32_t* chg, unsigned int* sum_dst) {
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  Local L;
+  for (;;) {
+    uint32_t i = 0;
+    if (lane_id() == 0) i = atomicAdd(cursor, 1u);
+    i = __shfl_sync(0xffffffffu, i, 0);
+    if (i >= count) break;
+    const uint32_t v = items(i);
+    const bool p0 = v < p.g.rb[kP1L];
+    const bool ch = p0 ? lift_warp<V, true>(p, v, L) : lift_warp<V, false>(p, v, L);
+    if (ch && lane_id() == 0) {
+      set_bit(chg, v);
+      ++L.phase_count;
+    }
+  }
+  block_flush(L, p.ctr, sum_dst, s_cnt);
+}
+
+template <class V, class Items>
+__device__ __noinline__ void block_rows(const SolveParams<V>& p, uint32_t count,
+                                           unsigned int* cursor, Items items,
+                                           uint32_t* chg, unsigned int* sum_dst) {
+  __shared__ BlockScratch<V> s;
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  Local L;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s.item = atomicAdd(cursor, 1u);
+    __syncthreads();
+    const uint32_t i = s.item;
+    if (i >= count) break;
+    const uint32_t v = items(i);
+    const bool p0 = v < p.g.rb[kP1L];
+    const bool ch = p0 ? lift_block<V, true>(p, v, L, s) : lift_block<V, false>(p, v, L, s);
+    if (ch && threadIdx.x == 0) {
+      set_bit(chg, v);
+      ++L.phase_count;
+    }
+  }
+  __syncthreads();
+  block_flush(L, p.ctr, sum_dst, s_cnt);
+}
+
+// ======================================================= certificate ====
+// Losing-region certificate.  A pass keeps candidate v iff
+//   player 0: every edge (v,t) is good;  player 1: some edge (v,t) is good,
+// good(v,t) = f(t) = top, or t is a candidate and f(v) < f(t) - w(v,t).
+// Removal is in place; the greatest fixpoint is reached when a pass removes
+// nothing.  Every candidate left is in W1: under the good-edge choices every
+// step inside the set changes the energy by w <= f(t) - f(v) - 1, so any
+// cycle player 0 can close there is negative.
+template <class V>
+__device__ __forceinline__ bool good_edge(const SolveParams<V>& p, int64_t fv,
+                                          int2 r) {
+  const V ft = ldcg(p.f + r.x);
+  if (ft == Top<V>::v) return true;
+  return ldcg(p.cand + r.x) && fv < static_cast<int64_t>(ft) - r.y;
+}
+
+template <class V, bool P0>
+__device__ __forceinline__ bool cert_keep_thread(const SolveParams<V>& p,
+                                                 uint32_t v, int64_t fv, Local& L) {
+  const uint32_t b = __ldg(p.g.off + v), e = __ldg(p.g.off + v + 1);
+  for (uint32_t i = b; i < e; i += 4) {
+    int2 r[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (i + k < e) r[k] = ld_edge(p.g.edge + i + k);
+    bool all = true, any = false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (i + k < e) {
+        ++L.cert_edges;
+        const bool g = good_edge<V>(p, fv, r[k]);
+        all &= g;
+        any |= g;
+      }
+    }
+    if (P0 && !all) return false;
+    if (!P0 && any) return true;
+  }
+  return P0;
+}
+
+template <class V, bool P0>
+__device__ __forceinline__ bool cert_keep_warp(const SolveParams<V>& p, uint32_t v,
+                                               int64_t fv, Local& L) {
+  const uint32_t b = __ldg(p.g.off + v), e = __ldg(p.g.off + v + 1);
+  for (uint32_t i = b + lane_id(); i - lane_id() < e; i += 32) {
+    bool g = P0;
+    if (i < e) {
+      ++L.cert_edges;
+      g = good_edge<V>(p, fv, ld_edge(p.g.edge + i));
+    }
+    if (P0 && !__all_sync(0xffffffffu, g)) return false;
+    if (!P0 && __any_sync(0xffffffffu, g)) return true;
+  }
+  return P0;
+}
+
+template <class V, bool P0>
+__device__ __forceinline__ bool cert_keep_block(const SolveParams<V>& p, uint32_t v,
+                                                int64_t fv, Local& L) {
+  const uint32_t b = __ldg(p.g.off + v), e = __ldg(p.g.off + v + 1);
+  for (uint32_t i0 = b; i0 < e; i0 += kBlock) {
+    const uint32_t i = i0 + threadIdx.x;
+    bool g = P0;
+    if (i < e) {
+      ++L.cert_edges;
+      g = good_edge<V>(p, fv, ld_edge(p.g.edge + i));
+    }
+    if (P0 && !__syncthreads_and(g)) return false;
+    if (!P0 && __syncthreads_or(g)) return true;
+  }
+  return P0;
+}
+
+// ============================================================ phases ====
+// Each phase is a separate non-inlined function so it gets its own register
+// allocation; the kernel body only keeps the (grid-uniform) loop state.
+// Every phase ends with block_flush; the caller then crosses a grid barrier.
+
+__device__ __forceinline__ int size_class(const Graph& g, uint32_t v) {
+  if (v < g.rb[kP1L]) return v >= g.rb[kP0H] ? 2 : v >= g.rb[kP0M] ? 1 : 0;
+  return v >= g.rb[kP1H] ? 2 : v >= g.rb[kP1M] ? 1 : 0;
+}
+// i-th vertex of the union of the player-0 and player-1 ranges of class c
+__device__ __forceinline__ uint32_t class_item(const Graph& g, int c, uint32_t i) {
+  const uint32_t n0 = g.rb[c + 1] - g.rb[c];
+  return i < n0 ? g.rb[c] + i : g.rb[c + 3] + (i - n0);
+}
+__device__ __forceinline__ uint32_t class_size(const Graph& g, int c) {
+  return (g.rb[c + 1] - g.rb[c]) + (g.rb[c + 4] - g.rb[c + 3]);
+}
+
+// f = 0 (host memset); frontier = vertices violating their condition at
+// f = 0: player 0 with only negative moves, player 1 with some negative move
+// (solver_par.cpp:366-387).  The player-0 witness starts at the first
+// non-negative edge (satisfied at f = 0).  Seeds go to frontier buffer 0.
+template <class V>
+__device__ __noinline__ void phase_seed(const SolveParams<V>& p, unsigned int* slot_sum) {
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  const Graph& g = p.g;
+  const uint32_t n = g.n;
+  Local L;
+  const uint32_t nwarps = gridDim.x * kWarps;
+  const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+  for (uint32_t v0 = gw * 32; v0 < n; v0 += nwarps * 32) {
+    const uint32_t v = v0 + lane_id();
+    bool seeded = false;
+    const int cls = v < n ? size_class(g, v) : 0;
+    if (v < n && cls == 0) {
+      const bool p0 = v < g.rb[kP1L];
+      const uint32_t b = __ldg(g.off + v), e = __ldg(g.off + v + 1);
+      uint32_t first_nn = e;
+      bool any_neg = false;
+      for (uint32_t i = b; i < e; ++i) {
+        const int w = __ldg(&g.edge[i].y);
+        if (w < 0)
+          any_neg = true;
+        else if (first_nn == e)
+          first_nn = i;
+      }
+      if (p0) {
+        seeded = first_nn == e;
+        p.wit[v] = __ldg(g.edge + (seeded ? b : first_nn));
+      } else {
+        seeded = any_neg;
+      }
+    }
+    // medium/heavy rows: the warp scans each such row cooperatively
+    uint32_t todo = __ballot_sync(0xffffffffu, v < n && cls != 0);
+    while (todo) {
+      const int src = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint32_t u = v0 + src;
+      const bool p0 = u < g.rb[kP1L];
+      const uint32_t b = __ldg(g.off + u), e = __ldg(g.off + u + 1);
+      uint32_t first_nn = 0xFFFFFFFFu;
+      bool any_neg = false;
+      for (uint32_t i = b + lane_id(); i - lane_id() < e; i += 32) {
+        bool neg = false, nn = false;
+        if (i < e) {
+          const int w = __ldg(&g.edge[i].y);
+          neg = w < 0;
+          nn = !neg;
+        }
+        any_neg |= __any_sync(0xffffffffu, neg);
+        const uint32_t m = __ballot_sync(0xffffffffu, nn);
+        if (m && first_nn == 0xFFFFFFFFu) first_nn = i - lane_id() + __ffs(m) - 1;
+        if (p0 ? first_nn != 0xFFFFFFFFu : any_neg) break;
+      }
+      const bool sd = p0 ? first_nn == 0xFFFFFFFFu : any_neg;
+      if (lane_id() == (uint32_t)src) {
+        seeded = sd;
+        if (p0) p.wit[u] = __ldg(g.edge + (sd ? b : first_nn));
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      warp_append(seeded && cls == c, v, p.fr[0] + p.cbase[c], &p.sh->fr_cnt[0][c]);
+    if (seeded) set_bit(p.frb, v);
+    L.phase_count += seeded;
+  }
+  block_flush(L, p.ctr, slot_sum + 2, s_cnt);
+}
+
+// One lift round.  Dense: every vertex (top ones are skipped after one
+// load); sparse: the frontier lists of buffer `buf`.  Raised vertices are
+// marked in `chg`; the other round's bitmap is cleared for reuse.
+template <class V>
+__device__ __noinline__ void phase_lift(const SolveParams<V>& p, bool dense, int buf,
+                                        uint32_t* chg, uint32_t* other,
+                                        unsigned int* slot_sum, unsigned int* slot_dyn) {
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  const Graph& g = p.g;
+  const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
+  const uint32_t nthreads = gridDim.x * kBlock;
+  const uint32_t nwords = (g.n + 31) >> 5;
+  Scratch* sh = p.sh;
+  Local L;
+  unsigned int* sum_dst = slot_sum + 0;
+  for (uint32_t w = tid; w < nwords; w += nthreads) {
+    other[w] = 0u;
+    if (dense) p.frb[w] = 0u;
+  }
+  if (tid == 0)
+    for (int c = 0; c < 3; ++c) {
+      sh->fr_cnt[buf ^ 1][c] = 0;
+      if (dense) sh->fr_cnt[buf][c] = 0;
+    }
+  if (dense) {
+    block_rows<V>(p, class_size(g, 2), slot_dyn + 1,
+                  [gp = &g](uint32_t i) { return class_item(*gp, 2, i); }, chg, sum_dst);
+    warp_rows<V>(p, class_size(g, 1), slot_dyn + 0,
+                 [gp = &g](uint32_t i) { return class_item(*gp, 1, i); }, chg, sum_dst);
+    dense_light<V, true>(p, g.rb[kP0L], g.rb[kP0M], chg, sum_dst);
+    dense_light<V, false>(p, g.rb[kP1L], g.rb[kP1M], chg, sum_dst);
+  } else {
+    const uint32_t* list = p.fr[buf];
+    const uint32_t cL = vload(&sh->fr_cnt[buf][0]);
+    const uint32_t cM = vload(&sh->fr_cnt[buf][1]);
+    const uint32_t cH = vload(&sh->fr_cnt[buf][2]);
+    const uint32_t* lM = list + p.cbase[1];
+    const uint32_t* lH = list + p.cbase[2];
+    block_rows<V>(p, cH, slot_dyn + 1, [=](uint32_t i) { return ldcg(lH + i); }, chg,
+                  sum_dst);
+    warp_rows<V>(p, cM, slot_dyn + 0, [=](uint32_t i) { return ldcg(lM + i); }, chg, sum_dst);
+    sparse_light<V>(p, list, cL, chg, sum_dst);
+    // leave the membership bitmap clear for the next activation
+    for (uint32_t i = tid; i < cL + cM + cH; i += nthreads) {
+      const uint32_t v = i < cL        ? ldcg(list + i)
+                         : i < cL + cM ? ldcg(lM + (i - cL))
+                                       : ldcg(lH + (i - cL - cM));
+      atomicAnd(p.frb + (v >> 5), ~(1u << (v & 31u)));
+    }
+    if (tid == 0) L.pops += cL + cM + cH;
+  }
+  block_flush(L, p.ctr, sum_dst, s_cnt);
+}
+
+// Certificate, step 1: every non-top vertex is a candidate.
+template <class V>
+__device__ __noinline__ void phase_cert_init(const SolveParams<V>& p, unsigned int* slot_sum) {
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
+  const uint32_t nthreads = gridDim.x * kBlock;
+  Local L;
+  for (uint32_t v = tid; v < p.g.n; v += nthreads)
+    stcg(p.cand + v, (uint8_t)(ldcg(p.f + v) != Top<V>::v));
+  block_flush(L, p.ctr, slot_sum + 1, s_cnt);
+}
+
+// Certificate, step 2: one pruning pass (removed count -> slot_sum[1]).
+template <class V>
+__device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned int* slot_sum,
+                                              unsigned int* slot_dyn) {
+  __shared__ unsigned int s_item;
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  const Graph& g = p.g;
+  const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
+  const uint32_t nthreads = gridDim.x * kBlock;
+  Local L;
+  // heavy candidates: a CTA each
+  const uint32_t nH = class_size(g, 2);
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_item = atomicAdd(slot_dyn + 1, 1u);
+    __syncthreads();
+    const uint32_t i = s_item;
+    if (i >= nH) break;
+    const uint32_t v = class_item(g, 2, i);
+    if (!ldcg(p.cand + v)) continue;
+    const int64_t fv = (int64_t)ldcg(p.f + v);
+    const bool keep = v < g.rb[kP1L] ? cert_keep_block<V, true>(p, v, fv, L)
+                                     : cert_keep_block<V, false>(p, v, fv, L);
+    if (threadIdx.x == 0) {
+      ++L.cert_scanned;
+      if (!keep) {
+        stcg(p.cand + v, (uint8_t)0);
+        ++L.phase_count;
+      }
+    }
+  }
+  __syncthreads();
+  // medium candidates: a warp each
+  const uint32_t nM = class_size(g, 1);
+  for (;;) {
+    uint32_t i = 0;
+    if (lane_id() == 0) i = atomicAdd(slot_dyn + 0, 1u);
+    i = __shfl_sync(0xffffffffu, i, 0);
+    if (i >= nM) break;
+    const uint32_t v = class_item(g, 1, i);
+    if (!ldcg(p.cand + v)) continue;
+    const int64_t fv = (int64_t)ldcg(p.f + v);
+    const bool keep = v < g.rb[kP1L] ? cert_keep_warp<V, true>(p, v, fv, L)
+                                     : cert_keep_warp<V, false>(p, v, fv, L);
+    if (lane_id() == 0) {
+      ++L.cert_scanned;
+      if (!keep) {
+        stcg(p.cand + v, (uint8_t)0);
+        ++L.phase_count;
+      }
+    }
+  }
+  // light candidates: a thread each
+  for (int side = 0; side < 2; ++side) {
+    const uint32_t lo = side ? g.rb[kP1L] : g.rb[kP0L];
+    const uint32_t hi = side ? g.rb[kP1M] : g.rb[kP0M];
+    for (uint32_t v = lo + tid; v < hi; v += nthreads) {
+      if (!ldcg(p.cand + v)) continue;
+      const int64_t fv = (int64_t)ldcg(p.f + v);
+      const bool keep = side ? cert_keep_thread<V, false>(p, v, fv, L)
+                             : cert_keep_thread<V, true>(p, v, fv, L);
+      ++L.cert_scanned;
+      if (!keep) {
+        stcg(p.cand + v, (uint8_t)0);
+        ++L.phase_count;
+      }
+    }
+  }
+  block_flush(L, p.ctr, slot_sum + 1, s_cnt);
+}
+
+// Certificate, step 3: certified vertices jump to top and count as changed
+// in this round so their predecessors are re-lifted (count -> slot_sum[0]).
+template <class V>
+__device__ __noinline__ void phase_cert_apply(const SolveParams<V>& p, uint32_t* chg,
+                                              unsigned int* slot_sum) {
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  const uint32_t n = p.g.n;
+  const uint32_t nwarps = gridDim.x * kWarps;
+  const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+  Local L;
+  for (uint32_t w = gw; w < (n + 31) >> 5; w += nwarps) {
+    const uint32_t v = (w << 5) + lane_id();
+    bool hit = false;
+    if (v < n && ldcg(p.cand + v) && ldcg(p.f + v) != Top<V>::v) {
+      stcg(p.f + v, Top<V>::v);
+      hit = true;
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, hit);
+    if (m && lane_id() == 0) atomicOr(chg + w, m);
+    L.phase_count += hit;
+    L.certified += hit;
+  }
+  block_flush(L, p.ctr, slot_sum + 0, s_cnt);
+}
+
+// Activation (solver_par.cpp:402-410): every non-top predecessor of a vertex
+// marked in `chg` enters frontier buffer `nb` once (bitmap dedup), sorted
+// into its size-class sublist; the warp expands CSC columns as one stream.
+template <class V>
+__device__ __noinline__ void phase_activate(const SolveParams<V>& p, const uint32_t* chg,
+                                            int nb, unsigned int* slot_sum) {
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  const Graph& g = p.g;
+  const uint32_t nwords = (g.n + 31) >> 5;
+  const uint32_t nwarps = gridDim.x * kWarps;
+  const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+  Local L;
+  for (uint32_t w0 = gw * 32; w0 < nwords; w0 += nwarps * 32) {
+    const uint32_t wi = w0 + lane_id();
+    uint32_t bits = wi < nwords ? ldcg(chg + wi) : 0u;
+    while (__any_sync(0xffffffffu, bits != 0u)) {
+      uint32_t b = 0, e = 0;
+      if (bits) {
+        const uint32_t v = (wi << 5) + (__ffs(bits) - 1);
+        bits &= bits - 1;
+        b = __ldg(g.coff + v);
+        e = __ldg(g.coff + v + 1);
+      }
+      warp_expand(b, e, [&](bool valid, uint32_t idx, uint32_t) {
+        bool add = false;
+        uint32_t u = 0;
+        int c = 0;
+        if (valid) {
+          ++L.act;
+          u = __ldg(g.csrc + idx);
+          if (ldcg(p.f + u) != Top<V>::v) {
+            const uint32_t bit = 1u << (u & 31u);
+            add = !(atomicOr(p.frb + (u >> 5), bit) & bit);
+            c = size_class(g, u);
+          }
+        }
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc)
+          warp_append(add && c == cc, u, p.fr[nb] + p.cbase[cc], &p.sh->fr_cnt[nb][cc]);
+        L.phase_count += add;
+      });
+    }
+  }
+  block_flush(L, p.ctr, slot_sum + 2, s_cnt);
+}
+
+// ========================================================== the kernel ===
+template <class V>
+__global__ void __launch_bounds__(kBlock, 2)
+    k_solve(const __grid_constant__ SolveParams<V> p) {
+  cg::grid_group grid = cg::this_grid();
+  const Graph& g = p.g;
+  const uint32_t n = g.n;
+  const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+  Scratch* sh = p.sh;
+  uint32_t phase = 0;
+  // phase timing, kept by the leader thread only: seed, lift, cert, activation
+  const unsigned long long t_start = leader ? globaltimer() : 0ull;
+  unsigned long long t_prev = t_start;
+
+  auto slot_sum = [&]() { return sh->sum[phase & 3]; };
+  auto slot_dyn = [&]() { return sh->dyn[phase & 3]; };
+  auto prev_sum = [&](int k) { return vload(&sh->sum[(phase - 1) & 3][k]); };
+  // zero the per-phase slots two phases ahead (last read two phases ago)
+  auto begin_phase = [&]() {
+    if (leader)
+      for (int k = 0; k < 4; ++k) {
+        sh->sum[(phase + 2) & 3][k] = 0;
+        sh->dyn[(phase + 2) & 3][k] = 0;
+      }
+  };
+  auto end_phase = [&](int kind) {
+    grid.sync();
+    ++phase;
+    if (leader) {
+      const unsigned long long t = globaltimer();
+      p.ctr[kTimeSeed + kind] += t - t_prev;
+      t_prev = t;
+    }
+  };
+
+  begin_phase();
+  phase_seed<V>(p, slot_sum());
+  end_phase(0);
+  uint32_t frontier = prev_sum(2);
+
+  unsigned long long round = 0, rounds_dense = 0, rounds_sparse = 0, cert_attempts = 0,
+                     cert_passes = 0;
+  int K = p.cert_interval > 0 ? p.cert_interval : 4;
+  unsigned long long next_cert = (unsigned long long)K;
+  int buf = 0;
+  bool dense = p.mode == kModeDense ||
+               (p.mode == kModeAuto && (unsigned long long)frontier * p.sparse_div >= n);
+  unsigned int status = 0;
+
+  while (frontier > 0 || dense) {
+    uint32_t* chg = p.chg[round & 1];
+    begin_phase();
+    if (leader && p.timeout_ns && t_prev - t_start > p.timeout_ns) sh->stop = 1;
+    phase_lift<V>(p, dense, buf, chg, p.chg[(round + 1) & 1], slot_sum(), slot_dyn());
+    end_phase(1);
+    ++(dense ? rounds_dense : rounds_sparse);
+    uint32_t changed = prev_sum(0);
+    ++round;
+    if (changed == 0) break;  // a round that raised nothing: least fixpoint
+    if (round >= p.round_budget) {
+      status = 5;
+      break;
+    }
+    if (vload(&sh->stop)) {
+      status = 2;
+      break;
+    }
+
+    bool certified_any = false;
+    if (p.certify && round >= next_cert) {
+      ++cert_attempts;
+      begin_phase();
+      phase_cert_init<V>(p, slot_sum());
+      end_phase(2);
+      for (;;) {
+        begin_phase();
+        phase_cert_prune<V>(p, slot_sum(), slot_dyn());
+        end_phase(2);
+        ++cert_passes;
+        if (prev_sum(1) == 0) break;
+      }
+      begin_phase();
+      phase_cert_apply<V>(p, chg, slot_sum());
+      end_phase(2);
+      const uint32_t cert = prev_sum(0);
+      certified_any = cert > 0;
+      changed += cert;
+      if (!certified_any) K = K * 2 < 64 ? K * 2 : 64;
+      next_cert = round + (unsigned long long)K;
+    }
+
+    // next round: dense, or activate the predecessors of changed vertices
+    const bool dense_next =
+        p.mode == kModeDense ||
+        (p.mode == kModeAuto &&
+         (certified_any || (double)changed * p.avg_in_deg * p.sparse_div >= (double)n));
+    if (!dense_next) {
+      begin_phase();
+      phase_activate<V>(p, chg, buf ^ 1, slot_sum());
+      end_phase(3);
+      buf ^= 1;
+      frontier = prev_sum(2);
+      if (frontier == 0) break;  // every changed vertex has only top predecessors
+    }
+    dense = dense_next;
+  }
+
+  if (leader) {
+    p.ctr[kRounds] = round;
+    p.ctr[kDenseRounds] = rounds_dense;
+    p.ctr[kSparseRounds] = rounds_sparse;
+    p.ctr[kCertAttempts] = cert_attempts;
+    p.ctr[kCertPasses] = cert_passes;
+    p.ctr[kStatus] = status;
+  }
+}
+
+}  // namespace egs

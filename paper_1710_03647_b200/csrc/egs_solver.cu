@@ -1,25 +1,33 @@
 // egs_solver.cu — host orchestration of the B200 energy-game solver and the
 // device half of the C-ABI declared in include/egs_gpu.h.
 //
-// The solve is the reference's value iteration (solve_frontier,
-// proj/src/solver_par.cpp:247-435) run as synchronous rounds on the device:
-//   seed -> { lift round (dense or worklist) -> [certificate] -> activation }*
-// until a round raises nothing.  Rounds read the measure of the previous
-// round (Jacobi), so the output is schedule-independent and identical to the
-// reference's least fixpoint; see DESIGN.md §3 for the proof that the
-// losing-region certificate preserves it.
+//   egs_ctx_create   upload the reference CSR (GameArena spans, arena.hpp:
+//                    109-115) and rebuild it on the device (egs_build.cuh)
+//   egs_ctx_solve    ONE cooperative launch of k_solve (egs_solve.cuh): seed,
+//                    lift rounds, certificate, activation and the fixpoint
+//                    test all run on the device; the host waits once
+//   egs_ctx_read_measure / egs_gpu_solve
+//                    export the least progress measure in the reference's
+//                    raw int64 encoding (energy.hpp:16), original vertex ids
+//
+// It replaces egsolve::solve (proj/include/egsolve/solver.hpp:86-87) for the
+// GPU variant; the output is the same least fixpoint the reference solvers
+// compute (solver_seq.cpp:124-212, solver_par.cpp:126-435).
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
 
+#include "egs_build.cuh"
 #include "egs_gpu.h"
-#include "egs_kernels.cuh"
+#include "egs_solve.cuh"
 
 namespace {
 
@@ -58,27 +66,37 @@ T* dalloc(size_t count) {
   return static_cast<T*>(p);
 }
 
-// Lanes per vertex: the reference's choose_chunk_size (solver_seq.cpp:214-219)
-// clamped to one warp.
-int choose_lanes(uint32_t n, uint64_t m) {
-  if (n == 0) return 1;
-  long long r = llround(static_cast<double>(m) / static_cast<double>(n));
-  r = std::max(1LL, std::min(32LL, r));
-  int g = 1;
-  while (g * 2 <= r) g *= 2;
-  return g;
+// RAII for upload temporaries.
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  template <class T>
+  T* as() {
+    return static_cast<T*>(p);
+  }
+  template <class T>
+  T* alloc(size_t count) {
+    p = dalloc<T>(count);
+    return as<T>();
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+  }
+};
+
+uint32_t grid_for(uint64_t items, int num_sms, int block = 256) {
+  const uint64_t blocks = (items + block - 1) / block;
+  const uint64_t maxb = (uint64_t)num_sms * 8;
+  return (uint32_t)std::max<uint64_t>(1, std::min(blocks, maxb));
 }
 
-__global__ void k_heavy_select(uint32_t n, const uint32_t* off,
-                               uint32_t thresh, uint32_t* list,
-                               uint32_t* count) {
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t base = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u;
-       base < n; base += stride) {
-    const uint32_t v = base + (threadIdx.x & 31u);
-    const bool h = v < n && off[v + 1] - off[v] > thresh;
-    egs::warp_append(h, v, list, count);
-  }
+int bits_for(uint32_t n) {
+  int b = 1;
+  while (b < 32 && (1ull << b) < (uint64_t)n) ++b;
+  return b;
 }
 
 }  // namespace
@@ -89,46 +107,42 @@ struct egs_ctx {
   int num_sms = 148;
   cudaStream_t stream = nullptr;
   uint32_t n = 0;
-  uint32_t m = 0;
+  uint64_t m = 0;
   int64_t cap = 0;
   int vbits = 32;
-  int lanes = 1;
-  uint32_t heavy_thresh = 0xFFFFFFFFu;
-  double avg_deg = 0;
   egs_gpu_opts opts{};
-  // arena
+  uint32_t rb[egs::kNumClasses + 1] = {};
+  // arena (relabelled)
   uint32_t* off = nullptr;
   int2* edge = nullptr;
-  uint8_t* owner = nullptr;
   uint32_t* coff = nullptr;
   uint32_t* csrc = nullptr;
-  uint32_t* heavy = nullptr;
-  uint32_t nheavy = 0;
+  uint32_t* perm = nullptr;  // old id -> new id
   // solver state
-  void* f[2] = {nullptr, nullptr};
-  int cur = 0;
+  void* f = nullptr;
   int2* wit = nullptr;
-  uint32_t* changed = nullptr;
+  uint32_t* chg[2] = {nullptr, nullptr};
+  uint32_t* frb = nullptr;
   uint32_t* fr[2] = {nullptr, nullptr};
-  uint32_t* bm[2] = {nullptr, nullptr};
   uint8_t* cand = nullptr;
-  uint32_t* dcounts = nullptr;  // [0] changed [1] fr0 [2] fr1 [3] removed [4] scratch
+  egs::Scratch* scratch = nullptr;
   unsigned long long* ctr = nullptr;
   int64_t* f64 = nullptr;
-  // pinned mirrors
-  uint32_t* h_counts = nullptr;
-  unsigned long long* h_ctr = nullptr;
-  cudaEvent_t ev[8] = {};
+  unsigned long long* h_ctr = nullptr;  // pinned mirror
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  int grid = 0;
   bool solved = false;
 
-  egs::DevArena arena() const {
-    return egs::DevArena{n, m, off, edge, owner, coff, csrc, cap};
-  }
-  uint32_t grid_for(uint64_t items, int lanes_per_item, int block = 256) const {
-    uint64_t threads = items * (uint64_t)lanes_per_item;
-    uint64_t blocks = (threads + block - 1) / block;
-    uint64_t maxb = (uint64_t)num_sms * 8;
-    return (uint32_t)std::max<uint64_t>(1, std::min(blocks, maxb));
+  egs::Graph graph() const {
+    egs::Graph g{};
+    g.n = n;
+    std::memcpy(g.rb, rb, sizeof(rb));
+    g.off = off;
+    g.edge = edge;
+    g.coff = coff;
+    g.csrc = csrc;
+    g.cap = cap;
+    return g;
   }
 };
 
@@ -137,13 +151,12 @@ namespace {
 void ctx_free(egs_ctx* c) {
   if (!c) return;
   if (c->device >= 0) cudaSetDevice(c->device);
-  void* ptrs[] = {c->off,   c->edge,   c->owner, c->coff,    c->csrc,
-                  c->heavy, c->f[0],   c->f[1],  c->wit,     c->changed,
-                  c->fr[0], c->fr[1],  c->bm[0], c->bm[1],   c->cand,
-                  c->dcounts, c->ctr,  c->f64};
+  void* ptrs[] = {c->off,    c->edge,   c->coff, c->csrc,  c->perm,
+                  c->f,      c->wit,    c->chg[0], c->chg[1], c->frb,
+                  c->fr[0],  c->fr[1],  c->cand, c->scratch, c->ctr,
+                  c->f64};
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  if (c->h_counts) cudaFreeHost(c->h_counts);
   if (c->h_ctr) cudaFreeHost(c->h_ctr);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
@@ -154,30 +167,140 @@ void ctx_free(egs_ctx* c) {
 void validate_opts(const egs_gpu_opts& o) {
   if (o.n_gpus != 1)
     throw Fail(EGS_ERR_INVALID_CONFIG,
-               "egs_gpu_solve drives one GPU per process; use the "
-               "partitioned driver for n_gpus > 1");
+               "egs_gpu_solve drives one GPU; use egs_part_* for n_gpus > 1");
   if (o.mode < EGS_MODE_AUTO || o.mode > EGS_MODE_SPARSE)
     throw Fail(EGS_ERR_INVALID_CONFIG, "mode must be 0, 1 or 2");
-  if (o.cert_interval < 0)
-    throw Fail(EGS_ERR_INVALID_CONFIG, "cert_interval must be >= 0");
+  if (o.cert_interval < 0 || o.sparse_div < 0 || o.grid_ctas < 0)
+    throw Fail(EGS_ERR_INVALID_CONFIG, "negative tuning knob");
   if (o.timeout_seconds < 0)
     throw Fail(EGS_ERR_INVALID_CONFIG, "timeout must be >= 0");
 }
 
-egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts,
-                    egs_gpu_stats* st) {
+template <class V>
+const void* solve_kernel() {
+  return reinterpret_cast<const void*>(&egs::k_solve<V>);
+}
+
+// EGS_VERBOSE=1 prints the device arena construction steps (host clock,
+// stream-synchronised) to stderr.
+struct StepTimer {
+  cudaStream_t s;
+  bool on;
+  Clock::time_point t;
+  explicit StepTimer(cudaStream_t st) : s(st), on(std::getenv("EGS_VERBOSE") != nullptr) {
+    t = Clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    std::fprintf(stderr, "[egs] %-28s %9.3f ms\n", what, secs_since(t) * 1e3);
+    t = Clock::now();
+  }
+};
+
+// Build the relabelled device arena from the reference CSR (host spans).
+void build_arena(egs_ctx* c, const egs_arena_view* a) {
+  StepTimer tm(c->stream);
+  const uint32_t n = c->n;
+  const uint64_t m = c->m;
+  cudaStream_t s = c->stream;
+  const int sms = c->num_sms;
+  DevBuf d_off64, d_dst, d_w64, d_owner, d_key, d_keys, d_val, d_inv, d_hist, d_bad,
+      d_tmp;
+  uint64_t* off64 = d_off64.alloc<uint64_t>((size_t)n + 1);
+  uint32_t* dst = d_dst.alloc<uint32_t>(m);
+  int64_t* w64 = d_w64.alloc<int64_t>(m);
+  uint8_t* owner = d_owner.alloc<uint8_t>(n);
+  CK(cudaMemcpyAsync(off64, a->csr_offsets, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dst, a->csr_targets, m * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(w64, a->csr_weights, m * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(owner, a->owners, n, cudaMemcpyHostToDevice, s));
+  tm.mark("alloc + H2D");
+
+  unsigned int* hist = d_hist.alloc<unsigned int>(16);
+  unsigned int* bad = d_bad.alloc<unsigned int>(1);
+  CK(cudaMemsetAsync(hist, 0, 16 * sizeof(unsigned int), s));
+  CK(cudaMemsetAsync(bad, 0, sizeof(unsigned int), s));
+  uint8_t* key = d_key.alloc<uint8_t>(n);
+  uint8_t* keys_sorted = d_keys.alloc<uint8_t>(n);
+  uint32_t* val = d_val.alloc<uint32_t>(n);
+  uint32_t* inv = d_inv.alloc<uint32_t>(n);
+  egs::k_classify<<<grid_for(n, sms), 256, 0, s>>>(n, off64, owner, key, val, hist);
+  CK(cudaGetLastError());
+  egs::k_validate<<<grid_for(m, sms), 256, 0, s>>>(n, m, dst, w64, bad);
+  CK(cudaGetLastError());
+  unsigned int h_hist[16] = {0}, h_bad = 0;
+  CK(cudaMemcpyAsync(h_hist, hist, sizeof(h_hist), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&h_bad, bad, sizeof(h_bad), cudaMemcpyDeviceToHost, s));
+  // stable partition of the vertices by class (radix sort on 3 key bits)
+  size_t tmp_bytes = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, keys_sorted, val, inv, n, 0, 3, s));
+  void* tmp = d_tmp.alloc<uint8_t>(tmp_bytes);
+  CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, keys_sorted, val, inv, n, 0, 3, s));
+  d_tmp.release();
+  CK(cudaStreamSynchronize(s));
+  if (h_bad & 1u)
+    throw Fail(EGS_ERR_UNSUPPORTED, "edge weight outside int32 on the device path");
+  if (h_bad & 2u) throw Fail(EGS_ERR_INVALID_CONFIG, "edge target out of range");
+  c->rb[0] = 0;
+  for (int k = 0; k < egs::kNumClasses; ++k) c->rb[k + 1] = c->rb[k] + h_hist[k];
+  d_key.release();
+  d_keys.release();
+  d_val.release();
+  tm.mark("classify + vertex sort");
+
+  // relabelled offsets
+  c->perm = dalloc<uint32_t>(n);
+  c->off = dalloc<uint32_t>((size_t)n + 1);
+  egs::k_permute<<<grid_for(n, sms), 256, 0, s>>>(n, inv, off64, c->perm, c->off);
+  CK(cudaGetLastError());
+  tmp_bytes = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, c->off, c->off, (int64_t)n + 1, s));
+  tmp = d_tmp.alloc<uint8_t>(tmp_bytes);
+  CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, c->off, c->off, (int64_t)n + 1, s));
+  d_tmp.release();
+
+  // relabelled edge records + (dst, src) pairs of the transpose
+  c->edge = dalloc<int2>(m);
+  DevBuf d_ck0, d_cv0, d_ck1;
+  uint32_t* ck0 = d_ck0.alloc<uint32_t>(m);
+  uint32_t* cv0 = d_cv0.alloc<uint32_t>(m);
+  egs::k_relabel_edges<<<grid_for((uint64_t)n, sms), 256, 0, s>>>(
+      n, inv, off64, dst, w64, c->perm, c->off, c->edge, ck0, cv0);
+  CK(cudaGetLastError());
+  tm.mark("offsets + edge relabel");
+  CK(cudaStreamSynchronize(s));
+  d_off64.release();
+  d_dst.release();
+  d_w64.release();
+  d_owner.release();
+  d_inv.release();
+
+  // CSC: sort the pairs by dst; sources in a column come out in row order
+  uint32_t* ck1 = d_ck1.alloc<uint32_t>(m);
+  c->csrc = dalloc<uint32_t>(m);
+  tmp_bytes = 0;
+  const int kb = bits_for(n);
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, ck0, ck1, cv0, c->csrc, m, 0, kb, s));
+  tmp = d_tmp.alloc<uint8_t>(tmp_bytes);
+  CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, ck0, ck1, cv0, c->csrc, m, 0, kb, s));
+  c->coff = dalloc<uint32_t>((size_t)n + 1);
+  egs::k_col_offsets<<<grid_for(m + 1, sms), 256, 0, s>>>(n, m, ck1, c->coff);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
+  tm.mark("CSC sort + offsets");
+}
+
+egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_stats* st) {
   validate_opts(opts);
   if (!a) throw Fail(EGS_ERR_INVALID_CONFIG, "null arena");
   if (a->num_edges >= 0xFFFFFFFFull)
-    throw Fail(EGS_ERR_UNSUPPORTED,
-               "arenas with >= 2^32 edges are not supported on the device");
+    throw Fail(EGS_ERR_UNSUPPORTED, "arenas with >= 2^32 edges are not supported on the device");
   if (a->num_vertices > 0 && a->num_edges < a->num_vertices)
     throw Fail(EGS_ERR_INVALID_CONFIG, "arena is not total");
-  if (a->credit_cap < 0)
-    throw Fail(EGS_ERR_INVALID_CONFIG, "negative credit_cap");
+  if (a->credit_cap < 0) throw Fail(EGS_ERR_INVALID_CONFIG, "negative credit_cap");
   if (a->max_abs_weight > 2147483647LL)
-    throw Fail(EGS_ERR_UNSUPPORTED,
-               "edge weights beyond int32 are not supported on the device");
+    throw Fail(EGS_ERR_UNSUPPORTED, "edge weights beyond int32 are not supported on the device");
   auto t0 = Clock::now();
   egs_ctx* c = new egs_ctx();
   try {
@@ -188,108 +311,80 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts,
     } else {
       CK(cudaGetDevice(&c->device));
     }
-    CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount,
-                              c->device));
+    CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
+    int coop = 0;
+    CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->device));
+    if (!coop) throw Fail(EGS_ERR_CUDA, "device does not support cooperative launch");
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
     c->n = a->num_vertices;
-    c->m = (uint32_t)a->num_edges;
+    c->m = a->num_edges;
     c->cap = a->credit_cap;
     c->vbits = a->credit_cap < 0xFFFFFFFFLL ? 32 : 64;
-    c->lanes = choose_lanes(c->n, c->m);
-    c->avg_deg = c->n ? (double)c->m / c->n : 0.0;
-    c->heavy_thresh = (uint32_t)std::max(256, 32 * c->lanes);
-    const uint32_t n = c->n, m = c->m;
+    const uint32_t n = c->n;
     const size_t vsz = c->vbits / 8;
-    cudaStream_t s = c->stream;
+    const size_t words = ((size_t)n + 31) / 32;
 
-    CK(cudaMallocHost(&c->h_counts, 8 * sizeof(uint32_t)));
     CK(cudaMallocHost(&c->h_ctr, egs::kNumCounters * sizeof(unsigned long long)));
-    c->dcounts = dalloc<uint32_t>(8);
     c->ctr = dalloc<unsigned long long>(egs::kNumCounters);
-    c->off = dalloc<uint32_t>((size_t)n + 1);
-    c->edge = dalloc<int2>(m);
-    c->owner = dalloc<uint8_t>(n);
-    c->coff = dalloc<uint32_t>((size_t)n + 1);
-    c->csrc = dalloc<uint32_t>(m);
-    c->heavy = dalloc<uint32_t>(n);
-    c->f[0] = dalloc<uint8_t>((size_t)n * vsz);
-    c->f[1] = dalloc<uint8_t>((size_t)n * vsz);
-    c->wit = dalloc<int2>(n);
-    c->changed = dalloc<uint32_t>((size_t)n * 2 + 1);
+    c->scratch = dalloc<egs::Scratch>(1);
+    c->f = dalloc<uint8_t>((size_t)n * vsz);
+    c->chg[0] = dalloc<uint32_t>(words);
+    c->chg[1] = dalloc<uint32_t>(words);
+    c->frb = dalloc<uint32_t>(words);
     c->fr[0] = dalloc<uint32_t>(n);
     c->fr[1] = dalloc<uint32_t>(n);
-    const size_t words = ((size_t)n + 31) / 32;
-    c->bm[0] = dalloc<uint32_t>(words);
-    c->bm[1] = dalloc<uint32_t>(words);
     c->cand = dalloc<uint8_t>(n);
     c->f64 = dalloc<int64_t>(n);
-
     if (n > 0) {
-      // Upload the reference CSR as-is and pack it on the device.
-      uint64_t* off64 = dalloc<uint64_t>((size_t)n + 1);
-      uint32_t* dst = dalloc<uint32_t>(m);
-      int64_t* w64 = dalloc<int64_t>(m);
-      int* bad = dalloc<int>(1);
-      CK(cudaMemcpyAsync(off64, a->csr_offsets, ((size_t)n + 1) * 8,
-                         cudaMemcpyHostToDevice, s));
-      CK(cudaMemcpyAsync(dst, a->csr_targets, (size_t)m * 4,
-                         cudaMemcpyHostToDevice, s));
-      CK(cudaMemcpyAsync(w64, a->csr_weights, (size_t)m * 8,
-                         cudaMemcpyHostToDevice, s));
-      CK(cudaMemcpyAsync(c->owner, a->owners, n, cudaMemcpyHostToDevice, s));
-      CK(cudaMemsetAsync(bad, 0, sizeof(int), s));
-      CK(cudaMemsetAsync(c->coff, 0, ((size_t)n + 1) * 4, s));
-      const uint32_t grid = c->grid_for(std::max<uint64_t>(m, n), 1);
-      egs::k_pack<<<grid, 256, 0, s>>>(n, m, off64, dst, w64, c->off, c->edge,
-                                       c->coff, bad);
-      CK(cudaGetLastError());
-      // exclusive scan of in-degrees -> CSC offsets (n+1 entries, last = 0)
-      size_t tmp_bytes = 0;
-      CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, c->coff, c->coff,
-                                       (int)(n + 1), s));
-      void* tmp = dalloc<uint8_t>(tmp_bytes);
-      CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, c->coff, c->coff,
-                                       (int)(n + 1), s));
-      // cursor: reuse the (now unneeded) dst buffer
-      CK(cudaMemcpyAsync(dst, c->coff, (size_t)n * 4,
-                         cudaMemcpyDeviceToDevice, s));
-      switch (c->lanes) {
-#define EGS_SCATTER(G)                                                       \
-  case G:                                                                    \
-    egs::k_csc_scatter<G><<<c->grid_for(n, G), 256, 0, s>>>(                 \
-        n, c->off, c->edge, dst, c->csrc);                                   \
-    break;
-        EGS_SCATTER(1) EGS_SCATTER(2) EGS_SCATTER(4) EGS_SCATTER(8)
-        EGS_SCATTER(16) EGS_SCATTER(32)
-#undef EGS_SCATTER
+      build_arena(c, a);
+    } else {
+      c->off = dalloc<uint32_t>(1);
+      c->coff = dalloc<uint32_t>(1);
+      c->edge = dalloc<int2>(1);
+      c->csrc = dalloc<uint32_t>(1);
+      c->perm = dalloc<uint32_t>(1);
+    }
+    c->wit = dalloc<int2>(std::max<uint32_t>(1, c->rb[egs::kP1L]));
+
+    // Persistent grid: every CTA co-resident (cooperative launch).
+    int per_sm = 0;
+    const void* kfn = c->vbits == 32 ? solve_kernel<uint32_t>() : solve_kernel<uint64_t>();
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, egs::kBlock, 0));
+    if (per_sm < 1) throw Fail(EGS_ERR_CUDA, "solve kernel cannot be resident");
+    const int full = per_sm * c->num_sms;
+    int want = opts.grid_ctas > 0 ? opts.grid_ctas
+                                  : (int)std::min<uint64_t>(full, std::max<uint64_t>(
+                                        1, ((uint64_t)n + egs::kBlock - 1) / egs::kBlock));
+    if (const char* e = std::getenv("EGS_GRID")) want = std::atoi(e);
+    c->grid = std::max(1, std::min(want, full));
+
+    // Keep the measure resident in L2 while the edge stream goes through.
+    int max_win = 0;
+    if (cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, c->device) ==
+            cudaSuccess &&
+        max_win > 0 && n > 0) {
+      int persist_max = 0;
+      cudaDeviceGetAttribute(&persist_max, cudaDevAttrMaxPersistingL2CacheSize, c->device);
+      const size_t fbytes = (size_t)n * vsz;
+      const size_t win = std::min<size_t>(fbytes, (size_t)max_win);
+      if (persist_max > 0) {
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(win, persist_max));
+        cudaStreamAttrValue attr{};
+        attr.accessPolicyWindow.base_ptr = c->f;
+        attr.accessPolicyWindow.num_bytes = win;
+        attr.accessPolicyWindow.hitRatio =
+            std::min(1.0f, (float)std::min<size_t>(win, persist_max) / (float)win);
+        attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &attr);
       }
-      CK(cudaGetLastError());
-      CK(cudaMemsetAsync(c->dcounts, 0, 8 * sizeof(uint32_t), s));
-      k_heavy_select<<<c->grid_for(n, 1), 256, 0, s>>>(
-          n, c->off, c->heavy_thresh, c->heavy, c->dcounts + 4);
-      CK(cudaGetLastError());
-      int h_bad = 0;
-      CK(cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
-      CK(cudaMemcpyAsync(c->h_counts, c->dcounts, 8 * sizeof(uint32_t),
-                         cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      c->nheavy = c->h_counts[4];
-      cudaFree(off64);
-      cudaFree(dst);
-      cudaFree(w64);
-      cudaFree(bad);
-      cudaFree(tmp);
-      if (h_bad == 1)
-        throw Fail(EGS_ERR_UNSUPPORTED,
-                   "edge weight outside int32 on the device path");
-      if (h_bad == 2)
-        throw Fail(EGS_ERR_INVALID_CONFIG, "edge target out of range");
+      cudaGetLastError();  // the window is a hint; never fail on it
     }
     if (st) {
       st->upload_seconds = secs_since(t0);
       st->value_bits = (uint32_t)c->vbits;
-      st->lanes = (uint32_t)c->lanes;
+      st->grid_ctas = (uint32_t)c->grid;
     }
     return c;
   } catch (...) {
@@ -298,232 +393,104 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts,
   }
 }
 
-// Read device counters into the pinned mirrors (synchronises the stream).
-void pull_counts(egs_ctx* c) {
-  CK(cudaMemcpyAsync(c->h_counts, c->dcounts, 8 * sizeof(uint32_t),
-                     cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(c->h_ctr, c->ctr,
-                     egs::kNumCounters * sizeof(unsigned long long),
-                     cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-}
-
-template <class V, int G>
+template <class V>
 void run_solve(egs_ctx* c, egs_gpu_stats* st) {
-  const auto t0 = Clock::now();
   cudaStream_t s = c->stream;
   const uint32_t n = c->n;
-  const egs::DevArena g = c->arena();
-  V* f[2] = {static_cast<V*>(c->f[0]), static_cast<V*>(c->f[1])};
   const egs_gpu_opts& o = c->opts;
   const size_t words = ((size_t)n + 31) / 32;
-  const double vs = sizeof(V);
-  uint64_t launches = 0, lift_launches = 0;
-  double cert_ms = 0, act_ms = 0;
-  int cur = 0;
-  int frb = 0;
+  const uint32_t szL = (c->rb[1] - c->rb[0]) + (c->rb[4] - c->rb[3]);
+  const uint32_t szM = (c->rb[2] - c->rb[1]) + (c->rb[5] - c->rb[4]);
 
-  CK(cudaMemsetAsync(c->dcounts, 0, 8 * sizeof(uint32_t), s));
-  CK(cudaMemsetAsync(c->ctr, 0, egs::kNumCounters * sizeof(unsigned long long), s));
-  CK(cudaMemsetAsync(c->bm[0], 0, words * 4, s));
-  CK(cudaEventRecord(c->ev[2], s));
-  ++launches;
-  egs::k_seed<V, G><<<c->grid_for(n, G), 256, 0, s>>>(
-      g, f[0], f[1], c->wit, c->bm[0], c->fr[0], c->dcounts + 1);
-  CK(cudaGetLastError());
-  pull_counts(c);
-  uint32_t fr_n = c->h_counts[1];
-
-  uint64_t rounds = 0, dense_rounds = 0, sparse_rounds = 0, pops = 0;
-  uint64_t cert_attempts = 0, cert_passes = 0;
-  double lift_ms = 0;
-  double lift_bytes = 0;
-  unsigned long long prev[egs::kNumCounters] = {0};
-  int K = o.cert_interval > 0 ? o.cert_interval : 4;
-  uint64_t next_cert = (uint64_t)K;
-  const uint64_t budget =
-      o.round_bound ? o.round_bound
-                    : (c->m > 0 && (uint64_t)c->cap + 1 >
-                                       UINT64_MAX / std::max<uint64_t>(1, c->m)
-                           ? UINT64_MAX
-                           : (uint64_t)c->m * ((uint64_t)c->cap + 1) + 1);
-  auto want_dense = [&](uint64_t frontier) {
-    if (o.mode == EGS_MODE_DENSE) return true;
-    if (o.mode == EGS_MODE_SPARSE) return false;
-    return (double)frontier * 16.0 > (double)n;
-  };
-  bool dense = want_dense(fr_n);
-  bool converged = fr_n == 0;
-
-  while (!converged) {
-    CK(cudaMemsetAsync(c->dcounts + 0, 0, sizeof(uint32_t), s));
-    egs::LiftArgs<V> a{};
-    a.g = g;
-    a.fcur = f[cur];
-    a.fnxt = f[cur ^ 1];
-    a.wit = c->wit;
-    a.heavy_thresh = c->heavy_thresh;
-    a.changed_list = c->changed;
-    a.changed_count = c->dcounts + 0;
-    a.ctr = c->ctr;
-    uint64_t items;
-    if (dense) {
-      a.items = nullptr;
-      a.count_dev = nullptr;
-      a.count = n;
-      a.dense = 1;
-      items = n;
-    } else {
-      a.items = c->fr[frb];
-      a.count_dev = c->dcounts + 1 + frb;
-      a.count = 0;
-      a.dense = 0;
-      items = fr_n;
-    }
-    CK(cudaEventRecord(c->ev[0], s));
-    egs::k_lift<V, G><<<c->grid_for(items, G), 256, 0, s>>>(a);
-    ++launches;
-    ++lift_launches;
-    if (c->nheavy) ++launches, ++lift_launches;
-    if (c->nheavy)
-      egs::k_lift_heavy<V><<<std::min<uint32_t>(c->nheavy, c->num_sms * 4),
-                             512, 0, s>>>(a, c->heavy, c->nheavy, c->bm[frb]);
-    CK(cudaEventRecord(c->ev[1], s));
-    CK(cudaGetLastError());
-    if (dense) {
-      cur ^= 1;
-    } else {
-      ++launches;
-      egs::k_commit<V><<<c->grid_for(items, 1), 256, 0, s>>>(
-          f[cur], f[cur ^ 1], c->changed, c->dcounts + 0);
-      CK(cudaGetLastError());
-    }
-    pull_counts(c);
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
-    lift_ms += ms;
-    {
-      const unsigned long long* h = c->h_ctr;
-      const double d_edges = (double)(h[egs::kEdges] - prev[egs::kEdges]);
-      const double d_apps = (double)(h[egs::kApps] - prev[egs::kApps]);
-      const double d_wit = (double)(h[egs::kWitness] - prev[egs::kWitness]);
-      lift_bytes += d_edges * (8 + vs) + d_apps * (4 + 2 * vs) +
-                    d_wit * (8 + 2 * vs) + (dense ? 0.0 : (double)items * 4);
-      std::memcpy(prev, h, sizeof(prev));
-    }
-    ++rounds;
-    pops += items;
-    (dense ? dense_rounds : sparse_rounds)++;
-    uint32_t changed = c->h_counts[0];
-    if (changed == 0) break;
-    if (rounds >= budget)
-      throw Fail(EGS_ERR_BOUND, "round budget of " + std::to_string(budget) +
-                                    " exhausted before reaching a fixpoint");
-    if (o.timeout_seconds > 0 && secs_since(t0) >= o.timeout_seconds)
-      throw Fail(EGS_ERR_TIMEOUT, "solve timed out");
-
-    bool certified_any = false;
-    if (o.certify && rounds >= next_cert) {
-      ++cert_attempts;
-      const unsigned long long before = c->h_ctr[egs::kCertified];
-      CK(cudaEventRecord(c->ev[4], s));
-      ++launches;
-      egs::k_cert_init<V><<<c->grid_for(n, 1), 256, 0, s>>>(f[cur], c->cand, n);
-      for (;;) {
-        CK(cudaMemsetAsync(c->dcounts + 3, 0, sizeof(uint32_t), s));
-        ++launches;
-        egs::k_cert_prune<V, G><<<c->grid_for(n, G), 256, 0, s>>>(
-            g, f[cur], c->cand, c->dcounts + 3);
-        CK(cudaGetLastError());
-        ++cert_passes;
-        pull_counts(c);
-        if (c->h_counts[3] == 0) break;
-      }
-      ++launches;
-      egs::k_cert_apply<V><<<c->grid_for(n, 1), 256, 0, s>>>(
-          f[cur], c->cand, n, c->changed, c->dcounts + 0, c->ctr);
-      CK(cudaGetLastError());
-      CK(cudaEventRecord(c->ev[5], s));
-      pull_counts(c);
-      {
-        float cm = 0;
-        CK(cudaEventElapsedTime(&cm, c->ev[4], c->ev[5]));
-        cert_ms += cm;
-      }
-      changed = c->h_counts[0];
-      certified_any = c->h_ctr[egs::kCertified] > before;
-      if (!certified_any) K = std::min(K * 2, 64);
-      next_cert = rounds + (uint64_t)K;
-    }
-
-    const bool dense_next =
-        want_dense((uint64_t)((double)changed * std::max(1.0, c->avg_deg))) ||
-        (certified_any && o.mode == EGS_MODE_AUTO);
-    if (!dense_next) {
-      const int nb = frb ^ 1;
-      CK(cudaMemsetAsync(c->bm[nb], 0, words * 4, s));
-      CK(cudaMemsetAsync(c->dcounts + 1 + nb, 0, sizeof(uint32_t), s));
-      CK(cudaEventRecord(c->ev[6], s));
-      ++launches;
-      egs::k_activate<V, G><<<c->grid_for(changed, G), 256, 0, s>>>(
-          g, f[cur], c->changed, c->dcounts + 0, c->bm[nb], c->fr[nb],
-          c->dcounts + 1 + nb, c->ctr);
-      CK(cudaGetLastError());
-      CK(cudaEventRecord(c->ev[7], s));
-      pull_counts(c);
-      {
-        float am = 0;
-        CK(cudaEventElapsedTime(&am, c->ev[6], c->ev[7]));
-        act_ms += am;
-      }
-      frb = nb;
-      fr_n = c->h_counts[1 + nb];
-      if (fr_n == 0) break;
-    }
-    dense = dense_next;
+  egs::SolveParams<V> p{};
+  p.g = c->graph();
+  p.f = static_cast<V*>(c->f);
+  p.wit = c->wit;
+  p.chg[0] = c->chg[0];
+  p.chg[1] = c->chg[1];
+  p.frb = c->frb;
+  p.fr[0] = c->fr[0];
+  p.fr[1] = c->fr[1];
+  p.cbase[0] = 0;
+  p.cbase[1] = szL;
+  p.cbase[2] = szL + szM;
+  p.cand = c->cand;
+  p.sh = c->scratch;
+  p.ctr = c->ctr;
+  p.mode = o.mode;
+  p.certify = o.certify;
+  p.cert_interval = o.cert_interval > 0 ? o.cert_interval : 4;
+  p.sparse_div = o.sparse_div > 0 ? (uint32_t)o.sparse_div : 4u;
+  p.avg_in_deg = n ? (float)((double)c->m / (double)n) : 1.0f;
+  if (p.avg_in_deg < 1.0f) p.avg_in_deg = 1.0f;
+  // default budget |E|*(cap+1)+1 (solver_par.cpp:94-98), saturating
+  unsigned long long budget = o.round_bound;
+  if (!budget) {
+    const unsigned long long per = (unsigned long long)c->cap + 1ull;
+    budget = (c->m && per > ~0ull / c->m) ? ~0ull : c->m * per + 1ull;
   }
-  CK(cudaEventRecord(c->ev[3], s));
+  p.round_budget = budget;
+  p.timeout_ns = o.timeout_seconds > 0 ? (unsigned long long)(o.timeout_seconds * 1e9) : 0ull;
+
+  CK(cudaEventRecord(c->ev[0], s));
+  CK(cudaMemsetAsync(c->f, 0, (size_t)n * sizeof(V), s));
+  CK(cudaMemsetAsync(c->chg[0], 0, words * 4, s));
+  CK(cudaMemsetAsync(c->chg[1], 0, words * 4, s));
+  CK(cudaMemsetAsync(c->frb, 0, words * 4, s));
+  CK(cudaMemsetAsync(c->scratch, 0, sizeof(egs::Scratch), s));
+  CK(cudaMemsetAsync(c->ctr, 0, egs::kNumCounters * sizeof(unsigned long long), s));
+  void* args[] = {&p};
+  CK(cudaLaunchCooperativeKernel(solve_kernel<V>(), dim3(c->grid), dim3(egs::kBlock), args,
+                                 0, s));
+  CK(cudaEventRecord(c->ev[1], s));
+  CK(cudaMemcpyAsync(c->h_ctr, c->ctr, egs::kNumCounters * sizeof(unsigned long long),
+                     cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  float solve_ms = 0;
-  CK(cudaEventElapsedTime(&solve_ms, c->ev[2], c->ev[3]));
-  c->cur = cur;
-  c->solved = true;
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+  const unsigned long long* h = c->h_ctr;
+  c->solved = h[egs::kStatus] == 0;
   if (st) {
-    const unsigned long long* h = c->h_ctr;
+    const double sv = sizeof(V);
     st->lifts = h[egs::kLifts];
     st->applications = h[egs::kApps];
     st->edges_relaxed = h[egs::kEdges];
     st->witness_checks = h[egs::kWitness];
     st->activations = h[egs::kActScanned];
     st->certified = h[egs::kCertified];
-    st->pops = pops;
-    st->rounds = rounds;
-    st->dense_rounds = dense_rounds;
-    st->sparse_rounds = sparse_rounds;
-    st->cert_attempts = cert_attempts;
-    st->cert_passes = cert_passes;
-    st->solve_seconds = solve_ms * 1e-3;
-    st->lift_kernel_seconds = lift_ms * 1e-3;
-    st->lift_bytes = (uint64_t)lift_bytes;
+    st->pops = h[egs::kPops];
+    st->visits = h[egs::kVisits];
+    st->cert_rows = h[egs::kCertScanned];
+    st->cert_edges = h[egs::kCertEdges];
+    st->rounds = h[egs::kRounds];
+    st->dense_rounds = h[egs::kDenseRounds];
+    st->sparse_rounds = h[egs::kSparseRounds];
+    st->cert_attempts = h[egs::kCertAttempts];
+    st->cert_passes = h[egs::kCertPasses];
+    st->solve_seconds = ms * 1e-3;
+    st->seed_seconds = h[egs::kTimeSeed] * 1e-9;
+    st->lift_seconds = h[egs::kTimeLift] * 1e-9;
+    st->cert_seconds = h[egs::kTimeCert] * 1e-9;
+    st->activate_seconds = h[egs::kTimeAct] * 1e-9;
+    // Algorithmic bytes: what each phase must move at least.
+    const double lift = (double)st->visits * sv + (double)st->witness_checks * (8 + sv) +
+                        (double)st->applications * 8 + (double)st->edges_relaxed * (8 + sv) +
+                        (double)st->lifts * sv;
+    const double seed = (double)c->m * 8 + (double)n * 8;
+    const double cert = (double)st->cert_attempts * n * (2 * (sv + 1)) +
+                        (double)st->cert_rows * (1 + sv + 8) +
+                        (double)st->cert_edges * (8 + sv + 1);
+    const double act = (double)st->activations * (4 + sv) + (double)st->sparse_rounds * words * 4;
+    st->lift_bytes = (uint64_t)lift;
+    st->algo_bytes = (uint64_t)(lift + seed + cert + act);
+    st->kernel_launches = 1;
     st->value_bits = (uint32_t)c->vbits;
-    st->lanes = (uint32_t)c->lanes;
-    st->kernel_launches = launches;
-    st->lift_launches = lift_launches;
-    st->cert_kernel_seconds = cert_ms * 1e-3;
-    st->activate_kernel_seconds = act_ms * 1e-3;
+    st->grid_ctas = (uint32_t)c->grid;
   }
-}
-
-template <class V>
-void dispatch_lanes(egs_ctx* c, egs_gpu_stats* st) {
-  switch (c->lanes) {
-    case 1: return run_solve<V, 1>(c, st);
-    case 2: return run_solve<V, 2>(c, st);
-    case 4: return run_solve<V, 4>(c, st);
-    case 8: return run_solve<V, 8>(c, st);
-    case 16: return run_solve<V, 16>(c, st);
-    default: return run_solve<V, 32>(c, st);
-  }
+  if (h[egs::kStatus] == 2) throw Fail(EGS_ERR_TIMEOUT, "solve timed out");
+  if (h[egs::kStatus] == 5)
+    throw Fail(EGS_ERR_BOUND, "round budget of " + std::to_string(budget) +
+                                  " exhausted before reaching a fixpoint");
 }
 
 void ctx_solve(egs_ctx* c, egs_gpu_stats* st) {
@@ -533,9 +500,9 @@ void ctx_solve(egs_ctx* c, egs_gpu_stats* st) {
     return;
   }
   if (c->vbits == 32)
-    dispatch_lanes<uint32_t>(c, st);
+    run_solve<uint32_t>(c, st);
   else
-    dispatch_lanes<uint64_t>(c, st);
+    run_solve<uint64_t>(c, st);
 }
 
 void ctx_read(egs_ctx* c, int64_t* out) {
@@ -543,12 +510,13 @@ void ctx_read(egs_ctx* c, int64_t* out) {
   if (c->n == 0) return;
   CK(cudaSetDevice(c->device));
   cudaStream_t s = c->stream;
+  const uint32_t grid = grid_for(c->n, c->num_sms);
   if (c->vbits == 32)
-    egs::k_widen<uint32_t><<<c->grid_for(c->n, 1), 256, 0, s>>>(
-        static_cast<uint32_t*>(c->f[c->cur]), c->f64, c->n);
+    egs::k_export<uint32_t><<<grid, 256, 0, s>>>(c->n, static_cast<uint32_t*>(c->f), c->perm,
+                                                  c->f64);
   else
-    egs::k_widen<uint64_t><<<c->grid_for(c->n, 1), 256, 0, s>>>(
-        static_cast<uint64_t*>(c->f[c->cur]), c->f64, c->n);
+    egs::k_export<uint64_t><<<grid, 256, 0, s>>>(c->n, static_cast<uint64_t*>(c->f), c->perm,
+                                                  c->f64);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out, c->f64, (size_t)c->n * 8, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
@@ -558,16 +526,22 @@ int ctx_epm(egs_ctx* c, const int64_t* f) {
   CK(cudaSetDevice(c->device));
   if (c->n == 0) return 1;
   cudaStream_t s = c->stream;
-  CK(cudaMemcpyAsync(c->f64, f, (size_t)c->n * 8, cudaMemcpyHostToDevice, s));
-  CK(cudaMemsetAsync(c->ctr, 0, egs::kNumCounters * sizeof(unsigned long long), s));
-  CK(cudaMemsetAsync(c->dcounts, 0, 8 * sizeof(uint32_t), s));
-  egs::k_epm<<<c->grid_for(c->n, 1), 256, 0, s>>>(
-      c->arena(), c->f64, c->ctr, reinterpret_cast<int*>(c->dcounts + 5));
+  DevBuf d_in, d_misc;
+  int64_t* fin = d_in.alloc<int64_t>(c->n);
+  unsigned long long* misc = d_misc.alloc<unsigned long long>(2);
+  CK(cudaMemcpyAsync(fin, f, (size_t)c->n * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(misc, 0, 2 * sizeof(unsigned long long), s));
+  const uint32_t grid = grid_for(c->n, c->num_sms);
+  egs::k_import<<<grid, 256, 0, s>>>(c->n, fin, c->perm, c->f64);
+  egs::k_epm<<<grid_for((uint64_t)c->n * 32, c->num_sms), 256, 0, s>>>(
+      c->graph(), c->f64, misc, reinterpret_cast<int*>(misc + 1));
   CK(cudaGetLastError());
-  pull_counts(c);
+  unsigned long long h[2] = {0, 0};
+  CK(cudaMemcpyAsync(h, misc, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
   c->solved = false;  // f64 scratch reused
-  if (c->h_counts[5]) throw Fail(EGS_ERR_UNSUPPORTED, "energy subtraction out of range");
-  return c->h_ctr[0] == 0 ? 1 : 0;
+  if (h[1]) throw Fail(EGS_ERR_UNSUPPORTED, "energy subtraction out of range");
+  return h[0] == 0 ? 1 : 0;
 }
 
 template <class F>
@@ -597,14 +571,18 @@ void egs_gpu_opts_default(egs_gpu_opts* o) {
   o->device = -1;
   o->certify = 1;
   o->cert_interval = 4;
+  o->sparse_div = 4;
   o->mode = EGS_MODE_AUTO;
 }
 
-int egs_ctx_create(const egs_arena_view* arena, const egs_gpu_opts* opts,
-                   egs_ctx** out, egs_gpu_stats* stats) {
+int egs_ctx_create(const egs_arena_view* arena, const egs_gpu_opts* opts, egs_ctx** out,
+                   egs_gpu_stats* stats) {
   return guarded([&] {
     egs_gpu_opts o;
-    if (opts) o = *opts; else egs_gpu_opts_default(&o);
+    if (opts)
+      o = *opts;
+    else
+      egs_gpu_opts_default(&o);
     if (stats) std::memset(stats, 0, sizeof(*stats));
     *out = ctx_create(arena, o, stats);
   });
@@ -614,13 +592,9 @@ int egs_ctx_solve(egs_ctx* ctx, egs_gpu_stats* stats) {
   return guarded([&] {
     if (!ctx) throw Fail(EGS_ERR_INVALID_CONFIG, "null context");
     auto t0 = Clock::now();
-    double up = stats ? stats->upload_seconds : 0;
     if (stats) std::memset(stats, 0, sizeof(*stats));
     ctx_solve(ctx, stats);
-    if (stats) {
-      stats->upload_seconds = up;
-      stats->wall_seconds = secs_since(t0);
-    }
+    if (stats) stats->wall_seconds = secs_since(t0);
   });
 }
 
@@ -642,12 +616,15 @@ int egs_ctx_is_progress_measure(egs_ctx* ctx, const int64_t* f) {
 
 void egs_ctx_destroy(egs_ctx* ctx) { ctx_free(ctx); }
 
-int egs_gpu_solve(const egs_arena_view* arena, const egs_gpu_opts* opts,
-                  int64_t* f_out, egs_gpu_stats* stats) {
+int egs_gpu_solve(const egs_arena_view* arena, const egs_gpu_opts* opts, int64_t* f_out,
+                  egs_gpu_stats* stats) {
   return guarded([&] {
     auto t0 = Clock::now();
     egs_gpu_opts o;
-    if (opts) o = *opts; else egs_gpu_opts_default(&o);
+    if (opts)
+      o = *opts;
+    else
+      egs_gpu_opts_default(&o);
     egs_gpu_stats local{};
     egs_gpu_stats* st = stats ? stats : &local;
     std::memset(st, 0, sizeof(*st));

@@ -34,7 +34,8 @@ def main():
                 ds.close()
                 d.update(config=name, mode=mode, certify=certify, gen_s=round(tg, 2),
                          upload_s=ds.upload_stats.upload_seconds, tops=tops,
-                         lift_GBps=d["lift_bytes"] / max(d["lift_kernel_seconds"], 1e-12) / 1e9)
+                         lift_GBps=d["lift_bytes"] / max(d["lift_seconds"], 1e-12) / 1e9,
+                         solve_GBps=d["algo_bytes"] / max(d["solve_seconds"], 1e-12) / 1e9)
                 print(json.dumps(d), flush=True)
 
 
