@@ -9,7 +9,7 @@ CXX       ?= g++
 CC        ?= gcc
 ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v \
-             --expt-relaxed-constexpr -Iinclude
+             --expt-relaxed-constexpr -Iinclude $(EXTRA_NVFLAGS)
 PKG       := paper_1710_03647_b200
 LIB       := $(PKG)/libegs_b200.so
 CSRC      := $(PKG)/csrc

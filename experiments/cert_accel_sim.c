@@ -6,9 +6,11 @@
 #include <time.h>
 static double now(void){struct timespec ts;clock_gettime(CLOCK_MONOTONIC,&ts);return ts.tv_sec+ts.tv_nsec*1e-9;}
 /* certificate: returns number of vertices newly set to TOP */
+static const int64_t* g_prev=0;
 static uint64_t certify(const eo_arena*g,int64_t*f,uint8_t*cand,int64_t*snap,int*passes){
   uint32_t n=g->n; memcpy(snap,f,n*8); if(getenv("JSTEP")) for(uint32_t v=0;v<n;v++){int64_t c=eo_raw_lift(g,v,f); if(c>snap[v]) snap[v]=c;}
-  for(uint32_t v=0;v<n;v++) cand[v]=snap[v]!=EO_TOP;
+  for(uint32_t v=0;v<n;v++) cand[v]=snap[v]!=EO_TOP && (!getenv("CANDCHG") || !g_prev || g_prev[v]!=f[v]);
+  uint64_t nc=0; for(uint32_t v=0;v<n;v++) nc+=cand[v]; if(getenv("VERB")) fprintf(stderr,"  cand=%llu\n",(unsigned long long)nc);
   int changed=1; *passes=0;
   while(changed){changed=0;(*passes)++;
     for(uint32_t v=0;v<n;v++){ if(!cand[v]) continue; int ok;
@@ -35,7 +37,7 @@ int main(int argc,char**argv){
     for(uint32_t v=0;v<n;v++){ int64_t c=eo_raw_lift(&g,v,src); if(c>f[v]){f[v]=c;changed=1;} }
     rounds++;
     if(!changed) break; if(rounds%1000==0) fprintf(stderr,"r%llu\n",(unsigned long long)rounds); if(getenv("MAXR") && rounds>=atoll(getenv("MAXR"))) break;
-    if(K>0 && rounds%K==0){int p; uint64_t c=certify(&g,f,cand,snap,&p); certs++; ncert+=c; totpass+=p;
+    if(K>0 && rounds%K==0){int p; g_prev=jacobi?prev:0; uint64_t c=certify(&g,f,cand,snap,&p); certs++; ncert+=c; totpass+=p;
        if(c) fprintf(stderr,"  round %llu: certified %llu (passes %d)\n",(unsigned long long)rounds,(unsigned long long)c,p);}
   }
   uint64_t tops=0; long long sum=0; int64_t mx=0; for(uint32_t v=0;v<n;v++){ if(f[v]==EO_TOP) tops++; else {sum+=f[v]; if(f[v]>mx) mx=f[v];}} fprintf(stderr,"tops=%llu sum=%lld max=%lld pm=%d\n",(unsigned long long)tops,sum,(long long)mx,eo_is_progress_measure(&g,f));

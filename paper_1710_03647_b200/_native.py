@@ -13,7 +13,8 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "libegs_b200.so")
+# EGS_LIB selects an alternative build of the same library (tuning experiments)
+lib_path = os.environ.get("EGS_LIB") or os.path.join(_HERE, "libegs_b200.so")
 
 if not os.path.exists(lib_path):  # no CPU fallback: the product is the CUDA library
     raise ImportError(

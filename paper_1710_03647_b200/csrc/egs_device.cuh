@@ -4,7 +4,7 @@
 // Value domain (reference proj/include/egsolve/energy.hpp:14-31): a credit is
 // a non-negative integer or top.  On the device the measure is held in the
 // narrowest unsigned type that can represent every finite value <= credit_cap
-// (u32 when credit_cap < 2^32 - 1, else u64) with top = all-ones, so that
+// (u32 when credit_cap < 2^32 - 2, else u64) with top = all-ones, so that
 // unsigned min/max order top above every finite credit exactly like the
 // reference's INT64_MAX sentinel; the host widens top back to INT64_MAX.
 #pragma once

@@ -22,11 +22,13 @@
 // R-MAT hubs) by one CTA, so warps never mix min and max and never wait on
 // one long row.
 //
-// Phases are separated by grid-wide barriers (cooperative launch).  Updates
-// are in place (Gauss-Seidel within a round): every value read is a valid
-// under-approximation of the least fixpoint because values only rise, and a
-// round that raises nothing read only final values, so it certifies the
-// fixpoint exactly as the reference's `changed` latch does.
+// Phases are separated by grid-wide barriers (cooperative launch).  Rounds
+// are synchronous (Jacobi): lifts read the measure of the previous round
+// and stage raised values, which a commit phase publishes; a round that
+// raises nothing has reached the least fixpoint, exactly as the reference's
+// `changed` latch decides (solver_par.cpp:170-194).  Jacobi iterates keep
+// the per-round climb of losing vertices regular, which is what lets the
+// certificate prove the whole losing region in one attempt.
 #pragma once
 
 #include <cooperative_groups.h>
@@ -94,13 +96,14 @@ struct Scratch {
 template <class V>
 struct SolveParams {
   Graph g;
-  V* f;                 // measure, relabelled ids
+  V* f;                 // measure, relabelled ids (read-only inside a lift round)
+  V* stage;             // lift rounds: raised values, committed after the round;
+                        // certificate: candidate values (f, or kNotCand)
   int2* wit;            // player-0 witness edge record (ids < rb[3])
   uint32_t* chg[2];     // changed-vertex bitmaps, by round parity
   uint32_t* frb;        // frontier membership bitmap
   uint32_t* fr[2];      // frontier lists; sublist c starts at cbase[c]
   uint32_t cbase[3];
-  uint8_t* cand;        // certificate candidates
   Scratch* sh;
   unsigned long long* ctr;  // kNumCounters
   int mode;
@@ -214,7 +217,7 @@ __device__ __forceinline__ bool lift_thread(const SolveParams<V>& p, uint32_t v,
   }
   if (P0) stcg(p.wit + v, best);
   if (acc > old) {
-    stcg(p.f + v, acc);
+    stcg(p.stage + v, acc);
     ++L.lifts;
     return true;
   }
@@ -291,7 +294,7 @@ __device__ __forceinline__ bool lift_warp(const SolveParams<V>& p, uint32_t v,
   if (lane == 0) {
     if (P0) stcg(p.wit + v, best);
     if (res > old) {
-      stcg(p.f + v, res);
+      stcg(p.stage + v, res);
       ++L.lifts;
       raised = true;
     }
@@ -396,7 +399,7 @@ __device__ __forceinline__ bool lift_block(const SolveParams<V>& p, uint32_t v,
     }
     if (P0) stcg(p.wit + v, rec);
     if (res > old) {
-      stcg(p.f + v, res);
+      stcg(p.stage + v, res);
       ++L.lifts;
       raised = true;
     }
@@ -511,12 +514,19 @@ __device__ __noinline__ void block_rows(const SolveParams<V>& p, uint32_t count,
 // nothing.  Every candidate left is in W1: under the good-edge choices every
 // step inside the set changes the energy by w <= f(t) - f(v) - 1, so any
 // cycle player 0 can close there is negative.
+// Candidate values live in p.stage: f(t) for a candidate, top for a vertex
+// already at top, kNotCand otherwise -- one gather per edge.
+template <class V>
+struct NotCand {
+  static constexpr V v = Top<V>::v - 1;
+};
+
 template <class V>
 __device__ __forceinline__ bool good_edge(const SolveParams<V>& p, int64_t fv,
                                           int2 r) {
-  const V ft = ldcg(p.f + r.x);
-  if (ft == Top<V>::v) return true;
-  return ldcg(p.cand + r.x) && fv < static_cast<int64_t>(ft) - r.y;
+  const V ct = ldcg(p.stage + r.x);
+  if (ct == Top<V>::v) return true;
+  return ct != NotCand<V>::v && fv < static_cast<int64_t>(ct) - r.y;
 }
 
 template <class V, bool P0>
@@ -721,15 +731,38 @@ __device__ __noinline__ void phase_lift(const SolveParams<V>& p, bool dense, int
   block_flush(L, p.ctr, sum_dst, s_cnt);
 }
 
-// Certificate, step 1: every non-top vertex is a candidate.
+// Commit of a Jacobi round: every vertex raised in the round (marked in
+// `chg`) takes its staged value.  Lifts of the round all read the measure
+// of the previous round, exactly the synchronous rounds of solve_frontier /
+// solve_sweep (solver_par.cpp:205-228, 389-417).
 template <class V>
-__device__ __noinline__ void phase_cert_init(const SolveParams<V>& p, unsigned int* slot_sum) {
+__device__ __noinline__ void phase_commit(const SolveParams<V>& p, const uint32_t* chg) {
+  const uint32_t n = p.g.n;
+  const uint32_t nwarps = gridDim.x * kWarps;
+  const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+  for (uint32_t w = gw; w < (n + 31) >> 5; w += nwarps) {
+    const uint32_t bits = ldcg(chg + w);
+    const uint32_t v = (w << 5) + lane_id();
+    if ((bits >> lane_id()) & 1u) stcg(p.f + v, ldcg(p.stage + v));
+  }
+}
+
+// Certificate, step 1: the candidates are the non-top vertices raised in the
+// round just finished (`chg`): losing vertices keep climbing, and starting
+// from any subset is sound (the pruned set is still closed).  Candidate
+// values are a snapshot of f in p.stage.
+template <class V>
+__device__ __noinline__ void phase_cert_init(const SolveParams<V>& p, const uint32_t* chg,
+                                             unsigned int* slot_sum) {
   __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
   const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
   const uint32_t nthreads = gridDim.x * kBlock;
   Local L;
-  for (uint32_t v = tid; v < p.g.n; v += nthreads)
-    stcg(p.cand + v, (uint8_t)(ldcg(p.f + v) != Top<V>::v));
+  for (uint32_t v = tid; v < p.g.n; v += nthreads) {
+    const V fv = ldcg(p.f + v);
+    const bool raised = (ldcg(chg + (v >> 5)) >> (v & 31u)) & 1u;
+    stcg(p.stage + v, fv == Top<V>::v ? fv : raised ? fv : NotCand<V>::v);
+  }
   block_flush(L, p.ctr, slot_sum + 1, s_cnt);
 }
 
@@ -752,14 +785,15 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
     const uint32_t i = s_item;
     if (i >= nH) break;
     const uint32_t v = class_item(g, 2, i);
-    if (!ldcg(p.cand + v)) continue;
-    const int64_t fv = (int64_t)ldcg(p.f + v);
+    const V cvv = ldcg(p.stage + v);
+    if (cvv == Top<V>::v || cvv == NotCand<V>::v) continue;
+    const int64_t fv = (int64_t)cvv;
     const bool keep = v < g.rb[kP1L] ? cert_keep_block<V, true>(p, v, fv, L)
                                      : cert_keep_block<V, false>(p, v, fv, L);
     if (threadIdx.x == 0) {
       ++L.cert_scanned;
       if (!keep) {
-        stcg(p.cand + v, (uint8_t)0);
+        stcg(p.stage + v, NotCand<V>::v);
         ++L.phase_count;
       }
     }
@@ -773,14 +807,15 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
     i = __shfl_sync(0xffffffffu, i, 0);
     if (i >= nM) break;
     const uint32_t v = class_item(g, 1, i);
-    if (!ldcg(p.cand + v)) continue;
-    const int64_t fv = (int64_t)ldcg(p.f + v);
+    const V cvv = ldcg(p.stage + v);
+    if (cvv == Top<V>::v || cvv == NotCand<V>::v) continue;
+    const int64_t fv = (int64_t)cvv;
     const bool keep = v < g.rb[kP1L] ? cert_keep_warp<V, true>(p, v, fv, L)
                                      : cert_keep_warp<V, false>(p, v, fv, L);
     if (lane_id() == 0) {
       ++L.cert_scanned;
       if (!keep) {
-        stcg(p.cand + v, (uint8_t)0);
+        stcg(p.stage + v, NotCand<V>::v);
         ++L.phase_count;
       }
     }
@@ -790,13 +825,14 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
     const uint32_t lo = side ? g.rb[kP1L] : g.rb[kP0L];
     const uint32_t hi = side ? g.rb[kP1M] : g.rb[kP0M];
     for (uint32_t v = lo + tid; v < hi; v += nthreads) {
-      if (!ldcg(p.cand + v)) continue;
-      const int64_t fv = (int64_t)ldcg(p.f + v);
+      const V cvv = ldcg(p.stage + v);
+      if (cvv == Top<V>::v || cvv == NotCand<V>::v) continue;
+      const int64_t fv = (int64_t)cvv;
       const bool keep = side ? cert_keep_thread<V, false>(p, v, fv, L)
                              : cert_keep_thread<V, true>(p, v, fv, L);
       ++L.cert_scanned;
       if (!keep) {
-        stcg(p.cand + v, (uint8_t)0);
+        stcg(p.stage + v, NotCand<V>::v);
         ++L.phase_count;
       }
     }
@@ -817,9 +853,12 @@ __device__ __noinline__ void phase_cert_apply(const SolveParams<V>& p, uint32_t*
   for (uint32_t w = gw; w < (n + 31) >> 5; w += nwarps) {
     const uint32_t v = (w << 5) + lane_id();
     bool hit = false;
-    if (v < n && ldcg(p.cand + v) && ldcg(p.f + v) != Top<V>::v) {
-      stcg(p.f + v, Top<V>::v);
-      hit = true;
+    if (v < n) {
+      const V cvv = ldcg(p.stage + v);
+      if (cvv != Top<V>::v && cvv != NotCand<V>::v) {
+        stcg(p.f + v, Top<V>::v);
+        hit = true;
+      }
     }
     const uint32_t m = __ballot_sync(0xffffffffu, hit);
     if (m && lane_id() == 0) atomicOr(chg + w, m);
@@ -876,8 +915,11 @@ __device__ __noinline__ void phase_activate(const SolveParams<V>& p, const uint3
 }
 
 // ========================================================== the kernel ===
+#ifndef EGS_MIN_BLOCKS
+#define EGS_MIN_BLOCKS 4  // resident CTAs per SM the register budget must allow
+#endif
 template <class V>
-__global__ void __launch_bounds__(kBlock, 2)
+__global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
     k_solve(const __grid_constant__ SolveParams<V> p) {
   cg::grid_group grid = cg::this_grid();
   const Graph& g = p.g;
@@ -934,6 +976,9 @@ __global__ void __launch_bounds__(kBlock, 2)
     uint32_t changed = prev_sum(0);
     ++round;
     if (changed == 0) break;  // a round that raised nothing: least fixpoint
+    begin_phase();
+    phase_commit<V>(p, chg);
+    end_phase(1);
     if (round >= p.round_budget) {
       status = 5;
       break;
@@ -947,7 +992,7 @@ __global__ void __launch_bounds__(kBlock, 2)
     if (p.certify && round >= next_cert) {
       ++cert_attempts;
       begin_phase();
-      phase_cert_init<V>(p, slot_sum());
+      phase_cert_init<V>(p, chg, slot_sum());
       end_phase(2);
       for (;;) {
         begin_phase();

@@ -124,7 +124,7 @@ struct egs_ctx {
   uint32_t* chg[2] = {nullptr, nullptr};
   uint32_t* frb = nullptr;
   uint32_t* fr[2] = {nullptr, nullptr};
-  uint8_t* cand = nullptr;
+  void* stage = nullptr;
   egs::Scratch* scratch = nullptr;
   unsigned long long* ctr = nullptr;
   int64_t* f64 = nullptr;
@@ -153,7 +153,7 @@ void ctx_free(egs_ctx* c) {
   if (c->device >= 0) cudaSetDevice(c->device);
   void* ptrs[] = {c->off,    c->edge,   c->coff, c->csrc,  c->perm,
                   c->f,      c->wit,    c->chg[0], c->chg[1], c->frb,
-                  c->fr[0],  c->fr[1],  c->cand, c->scratch, c->ctr,
+                  c->fr[0],  c->fr[1],  c->stage, c->scratch, c->ctr,
                   c->f64};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -320,7 +320,9 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     c->n = a->num_vertices;
     c->m = a->num_edges;
     c->cap = a->credit_cap;
-    c->vbits = a->credit_cap < 0xFFFFFFFFLL ? 32 : 64;
+    // u32 values need top (2^32-1) and the certificate's not-a-candidate
+    // marker (2^32-2) above every finite credit <= credit_cap
+    c->vbits = a->credit_cap < 0xFFFFFFFELL ? 32 : 64;
     const uint32_t n = c->n;
     const size_t vsz = c->vbits / 8;
     const size_t words = ((size_t)n + 31) / 32;
@@ -334,7 +336,7 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     c->frb = dalloc<uint32_t>(words);
     c->fr[0] = dalloc<uint32_t>(n);
     c->fr[1] = dalloc<uint32_t>(n);
-    c->cand = dalloc<uint8_t>(n);
+    c->stage = dalloc<uint8_t>((size_t)n * vsz);
     c->f64 = dalloc<int64_t>(n);
     if (n > 0) {
       build_arena(c, a);
@@ -414,7 +416,7 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
   p.cbase[0] = 0;
   p.cbase[1] = szL;
   p.cbase[2] = szL + szM;
-  p.cand = c->cand;
+  p.stage = static_cast<V*>(c->stage);
   p.sh = c->scratch;
   p.ctr = c->ctr;
   p.mode = o.mode;

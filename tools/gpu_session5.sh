@@ -1,0 +1,5 @@
+# Jacobi rounds + single-gather certificate: parity, probes for two register budgets
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15 > gpurun_out/p5_pytest.log
+timeout 600 python tools/probe_solve.py C1,C2,C5,C3,C4 auto > gpurun_out/p5_probe_mb4.jsonl 2> gpurun_out/p5_probe_mb4.err
+EGS_LIB=build/libegs_b200_mb2.so timeout 600 python tools/probe_solve.py C1,C2,C5,C3,C4 auto > gpurun_out/p5_probe_mb2.jsonl 2> gpurun_out/p5_probe_mb2.err
+cat gpurun_out/p5_pytest.log; tail -n 3 gpurun_out/p5_probe_mb4.err
