@@ -71,6 +71,8 @@ typedef struct egs_gpu_opts {
   int32_t sparse_div;      /* next round is sparse iff estimated frontier *
                               sparse_div < n (0 = 4) */
   int32_t grid_ctas;       /* persistent-kernel CTAs; 0 = auto */
+  int32_t no_tma;          /* 1: stage no edge spans through TMA (A/B and
+                              debugging); the result is identical */
   int32_t mode;            /* EGS_MODE_* */
   int32_t debug_checks;    /* SolverOptions::debug_checks: monotonicity and
                               fixpoint verification on the device */
@@ -111,6 +113,9 @@ typedef struct egs_gpu_stats {
   uint64_t kernel_launches;/* device kernels launched by the solve */
   uint32_t value_bits;     /* 32 or 64: device value width chosen */
   uint32_t grid_ctas;      /* CTAs of the persistent solve kernel */
+  double lift_sub_seconds[5]; /* per-CTA mean time in the lift sub-phases:
+                                 heavy rows, medium rows, light player-0 rows,
+                                 light player-1 rows, sparse light rows */
 } egs_gpu_stats;
 
 void egs_gpu_opts_default(egs_gpu_opts* opts);

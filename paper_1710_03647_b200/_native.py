@@ -92,6 +92,7 @@ class GpuOpts(C.Structure):
         ("cert_interval", C.c_int32),
         ("sparse_div", C.c_int32),
         ("grid_ctas", C.c_int32),
+        ("no_tma", C.c_int32),
         ("mode", C.c_int32),
         ("debug_checks", C.c_int32),
         ("timeout_seconds", C.c_double),
@@ -116,11 +117,13 @@ class GpuStats(C.Structure):
         + [(k, C.c_double) for k in _STAT_F64]
         + [("algo_bytes", C.c_uint64), ("lift_bytes", C.c_uint64),
            ("kernel_launches", C.c_uint64), ("value_bits", C.c_uint32),
-           ("grid_ctas", C.c_uint32)]
+           ("grid_ctas", C.c_uint32), ("lift_sub_seconds", C.c_double * 5)]
     )
 
     def as_dict(self) -> dict:
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["lift_sub_seconds"] = list(self.lift_sub_seconds)
+        return d
 
 
 _P = C.c_void_p
@@ -292,6 +295,7 @@ class SolverOptions:
     cert_interval: int = 4
     sparse_div: int = 4
     grid_ctas: int = 0
+    no_tma: bool = False
     mode: str = "auto"
     debug_checks: bool = False
     timeout_seconds: float = 0.0
@@ -309,6 +313,7 @@ class SolverOptions:
         o.cert_interval = int(self.cert_interval)
         o.sparse_div = int(self.sparse_div)
         o.grid_ctas = int(self.grid_ctas)
+        o.no_tma = int(bool(self.no_tma) or os.environ.get("EGS_NO_TMA") == "1")
         o.mode = _MODES[self.mode]
         o.debug_checks = int(bool(self.debug_checks))
         o.timeout_seconds = float(self.timeout_seconds)

@@ -76,6 +76,34 @@ __device__ __forceinline__ void stcg(uint8_t* p, uint8_t v) {
 __device__ __forceinline__ void stcg(int2* p, int2 v) { __stcg(p, v); }
 __device__ __forceinline__ int2 ld_edge(const int2* p) { return __ldcs(p); }
 
+// L2 eviction-priority policies (createpolicy; not volatile so the compiler
+// hoists them).  The random gathers of the measure use evict_last so the
+// measure stays L2-resident while the edge stream (evict_first) passes.
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint32_t gather(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;"
+               : "=r"(v)
+               : "l"(p), "l"(l2_evict_last()));
+  return v;
+}
+__device__ __forceinline__ uint64_t gather(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.global.cg.L2::cache_hint.u64 %0, [%1], %2;"
+               : "=l"(v)
+               : "l"(p), "l"(l2_evict_last()));
+  return v;
+}
+
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
@@ -154,6 +182,59 @@ __device__ __forceinline__ void warp_expand(uint32_t b, uint32_t e, Fn&& fn) {
     const uint32_t sb = __shfl_sync(0xffffffffu, b, lo);
     const uint32_t sx = __shfl_sync(0xffffffffu, excl, lo);
     fn(k < total, sb + (k - sx), lo);
+  }
+}
+
+// ------------------------------------------------ TMA bulk copies ----
+// 1-D bulk copies global -> shared (cp.async.bulk, SASS UBLKCP) completing
+// on an mbarrier transaction count.  Source/destination 16-byte aligned,
+// size a multiple of 16.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+// make barrier initialisation visible to the async (TMA) proxy
+__device__ __forceinline__ void mbar_init_fence() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// order earlier generic-proxy accesses of a buffer before an async-proxy
+// write into it (buffer reuse)
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(l2_evict_first())
+      : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// A transfer that never lands (a bug, or a faulted copy) traps instead of
+// hanging the persistent grid (~2^22 polls, far beyond any copy latency).
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t spins = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    if (++spins > (1u << 22)) __trap();
   }
 }
 

@@ -70,6 +70,11 @@ enum Counter : int {
   kTimeLift,
   kTimeCert,
   kTimeAct,
+  kSubHeavy,       // ns summed over CTAs inside each lift sub-phase
+  kSubMedium,
+  kSubLightP0,
+  kSubLightP1,
+  kSubSparseLight,
   kNumCounters
 };
 
@@ -107,6 +112,7 @@ struct SolveParams {
   Scratch* sh;
   unsigned long long* ctr;  // kNumCounters
   int mode;
+  int use_tma;
   int certify;
   int cert_interval;
   uint32_t sparse_div;      // next round sparse iff est. frontier * div < n
@@ -122,6 +128,23 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 
 __device__ __forceinline__ uint32_t vload(const volatile unsigned int* p) { return *p; }
+
+// Per-CTA time spent in the sub-phases of a lift phase (thread 0 of each
+// CTA adds its own wall time; divide by the grid size for a per-CTA mean).
+struct SubTimer {
+  unsigned long long* ctr;
+  unsigned long long t;
+  __device__ explicit SubTimer(unsigned long long* c) : ctr(c), t(0) {
+    if (threadIdx.x == 0) t = globaltimer();
+  }
+  __device__ void lap(int k) {
+    if (threadIdx.x == 0) {
+      const unsigned long long now = globaltimer();
+      atomicAdd(ctr + k, now - t);
+      t = now;
+    }
+  }
+};
 
 // Per-thread event counts of the current phase (u32: one phase touches every
 // row / edge at most once, so a block's sum stays below 2^32).  Flushed into
@@ -172,6 +195,8 @@ __device__ __forceinline__ void block_flush(Local& L, unsigned long long* ctr,
 // the count(v) of Alg. 1, solver_seq.cpp:186-199).
 
 // ---- one thread per row (light rows)
+constexpr int kChunk = 8;  // edges whose gathers a thread keeps in flight
+
 template <class V, bool P0>
 __device__ __forceinline__ bool lift_thread(const SolveParams<V>& p, uint32_t v,
                                             Local& L) {
@@ -181,7 +206,7 @@ __device__ __forceinline__ bool lift_thread(const SolveParams<V>& p, uint32_t v,
   if (old == TOP) return false;
   if (P0) {
     const int2 we = ldcg(p.wit + v);
-    if (old >= ominus_cap<V>(ldcg(p.f + we.x), we.y, p.g.cap)) {
+    if (old >= ominus_cap<V>(gather(p.f + we.x), we.y, p.g.cap)) {
       ++L.witness;
       return false;
     }
@@ -191,26 +216,26 @@ __device__ __forceinline__ bool lift_thread(const SolveParams<V>& p, uint32_t v,
   L.edges += e - b;
   V acc = P0 ? TOP : V(0);
   int2 best = make_int2(0, 0);
-  for (uint32_t i = b; i < e; i += 8) {
-    int2 r[8];
-    V c[8];
+  // Branch-free chunks: indices past the row end re-read its last edge
+  // (a duplicate cannot change a min or a max), so all loads of a chunk
+  // issue back to back before the first use.
+  for (uint32_t i = b; i < e; i += kChunk) {
+    int2 r[kChunk];
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (i + k < e) r[k] = ld_edge(p.g.edge + i + k);
+    for (int k = 0; k < kChunk; ++k) r[k] = ld_edge(p.g.edge + min(i + k, e - 1));
+    V c[kChunk];
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (i + k < e) c[k] = ominus_cap<V>(ldcg(p.f + r[k].x), r[k].y, p.g.cap);
+    for (int k = 0; k < kChunk; ++k) c[k] = gather(p.f + r[k].x);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      if (i + k < e) {
-        if (P0) {
-          if (c[k] < acc || (k == 0 && i == b)) {
-            acc = c[k];
-            best = r[k];
-          }
-        } else {
-          acc = c[k] > acc ? c[k] : acc;
+    for (int k = 0; k < kChunk; ++k) {
+      const V x = ominus_cap<V>(c[k], r[k].y, p.g.cap);
+      if (P0) {
+        if (x < acc || (k == 0 && i == b)) {
+          acc = x;
+          best = r[k];
         }
+      } else {
+        acc = x > acc ? x : acc;
       }
     }
     if (P0 ? acc == V(0) : acc == TOP) break;  // raw_lift early exits (:41,46)
@@ -237,7 +262,7 @@ __device__ __forceinline__ bool lift_warp(const SolveParams<V>& p, uint32_t v,
     bool sat = false;
     if (lane == 0) {
       const int2 we = ldcg(p.wit + v);
-      sat = old >= ominus_cap<V>(ldcg(p.f + we.x), we.y, p.g.cap);
+      sat = old >= ominus_cap<V>(gather(p.f + we.x), we.y, p.g.cap);
     }
     if (__shfl_sync(0xffffffffu, sat, 0)) {
       if (lane == 0) ++L.witness;
@@ -263,7 +288,7 @@ __device__ __forceinline__ bool lift_warp(const SolveParams<V>& p, uint32_t v,
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const uint32_t i = i0 + k * 32 + lane;
-      if (i < e) c[k] = ominus_cap<V>(ldcg(p.f + r[k].x), r[k].y, p.g.cap);
+      if (i < e) c[k] = ominus_cap<V>(gather(p.f + r[k].x), r[k].y, p.g.cap);
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -324,7 +349,7 @@ __device__ __forceinline__ bool lift_block(const SolveParams<V>& p, uint32_t v,
     __syncthreads();
     if (threadIdx.x == 0) {
       const int2 we = ldcg(p.wit + v);
-      s.flag = old >= ominus_cap<V>(ldcg(p.f + we.x), we.y, p.g.cap);
+      s.flag = old >= ominus_cap<V>(gather(p.f + we.x), we.y, p.g.cap);
     }
     __syncthreads();
     if (s.flag) {
@@ -351,7 +376,7 @@ __device__ __forceinline__ bool lift_block(const SolveParams<V>& p, uint32_t v,
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const uint32_t i = i0 + k * kBlock + threadIdx.x;
-      if (i < e) c[k] = ominus_cap<V>(ldcg(p.f + r[k].x), r[k].y, p.g.cap);
+      if (i < e) c[k] = ominus_cap<V>(gather(p.f + r[k].x), r[k].y, p.g.cap);
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -434,6 +459,144 @@ __device__ __noinline__ void dense_light(const SolveParams<V>& p, uint32_t lo,
     if (m && lane_id() == 0) atomicOr(chg + w, m);
     L.phase_count += ch;
   }
+  block_flush(L, p.ctr, sum_dst, s_cnt);
+}
+
+// Player-1 light rows of a dense round, TMA-staged.  A warp owns aligned
+// 32-vertex tiles; the tile's contiguous span of edge records is brought
+// into the warp's shared-memory stage by one bulk copy (cp.async.bulk,
+// mbarrier completion) issued one tile ahead, so the HBM stream overlaps the
+// gathers of the current tile and never goes through the per-thread LSU
+// path.  Tiles whose vertices are all at top are skipped without a copy.
+// Each lane then lifts its own row from shared memory (reads rotated by
+// lane, so a half-warp hits distinct banks).
+constexpr uint32_t kStageRecs = 512;  // 4 KB of edge records per warp stage
+constexpr uint32_t kStages = 2;
+constexpr size_t kLiftSmemBytes = (size_t)kWarps * kStages * kStageRecs * sizeof(int2);
+
+// Per-warp stage barriers live for the whole persistent launch: initialised
+// once by k_solve, their phase parity carried across rounds.
+__shared__ __align__(8) uint64_t g_tma_bar[kWarps][kStages];
+__shared__ uint32_t g_tma_parity[kWarps];
+
+__device__ __forceinline__ void tma_init_barriers() {
+  if (lane_id() == 0) {
+    const uint32_t warp = threadIdx.x >> 5;
+    for (uint32_t s = 0; s < kStages; ++s) mbar_init(&g_tma_bar[warp][s], 1);
+    g_tma_parity[warp] = 0;
+    mbar_init_fence();
+  }
+  __syncthreads();
+}
+
+template <class V>
+__device__ __noinline__ void dense_light_p1(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
+                                            uint32_t* chg, unsigned int* sum_dst) {
+  constexpr V TOP = Top<V>::v;
+  extern __shared__ __align__(128) int2 dsm[];
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  Local L;
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  int2* stage_base = dsm + (size_t)warp * kStages * kStageRecs;
+  uint64_t* s_bar = g_tma_bar[warp];
+  const uint32_t nwarps = gridDim.x * kWarps;
+  const uint32_t w1 = (hi + 31) >> 5;
+  const uint32_t wfirst = (lo >> 5) + blockIdx.x * kWarps + warp;
+
+  struct Tile {
+    V old;
+    uint32_t b, e, base;
+    bool work, any, staged;
+  };
+  // Load the tile's vertex state and, if any row needs a lift, start the
+  // bulk copy of its edge span into stage `s`.
+  auto prepare = [&](uint32_t w, uint32_t s, Tile& t) {
+    const uint32_t v = (w << 5) + lane;
+    const bool in = w < w1 && v >= lo && v < hi;
+    t.old = in ? ldcg(p.f + v) : TOP;
+    t.work = in && t.old != TOP;
+    t.any = __any_sync(0xffffffffu, t.work);
+    t.staged = false;
+    if (!t.any) return;
+    t.b = in ? __ldg(p.g.off + v) : 0u;
+    t.e = in ? __ldg(p.g.off + v + 1) : 0u;
+    const uint32_t first = max(w << 5, lo), last = min((w << 5) + 32, hi);
+    const uint32_t span_lo = __shfl_sync(0xffffffffu, t.b, first - (w << 5));
+    const uint32_t span_hi = __shfl_sync(0xffffffffu, t.e, last - 1 - (w << 5));
+    const uint32_t a_lo = span_lo & ~1u, a_hi = (span_hi + 1u) & ~1u;  // 16 B aligned
+    t.base = a_lo;
+    if (a_hi - a_lo <= kStageRecs) {
+      t.staged = true;
+      if (lane == 0) {
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&s_bar[s], (a_hi - a_lo) * (uint32_t)sizeof(int2));
+        bulk_g2s(stage_base + s * kStageRecs, p.g.edge + a_lo,
+                 (a_hi - a_lo) * (uint32_t)sizeof(int2), &s_bar[s]);
+      }
+    }
+  };
+  auto compute = [&](uint32_t w, uint32_t s, const Tile& t, uint32_t& parity) {
+    if (!t.any) return;
+    bool ch = false;
+    if (t.staged) {
+      mbar_wait(&s_bar[s], (parity >> s) & 1u);
+      parity ^= 1u << s;
+      if (t.work) {
+        ++L.visits;
+        ++L.apps;
+        const uint32_t len = t.e - t.b;
+        L.edges += len;
+        const int2* row = stage_base + s * kStageRecs + (t.b - t.base);
+        const uint32_t rot = lane % len;  // light rows are non-empty
+        V acc = 0;
+        for (uint32_t k0 = 0; k0 < len; k0 += kChunk) {
+          int2 r[kChunk];
+#pragma unroll
+          for (int k = 0; k < kChunk; ++k) {
+            uint32_t j = min(k0 + k, len - 1) + rot;  // clamp (duplicate), rotate banks
+            j = j >= len ? j - len : j;
+            r[k] = row[j];
+          }
+          V c[kChunk];
+#pragma unroll
+          for (int k = 0; k < kChunk; ++k) c[k] = gather(p.f + r[k].x);
+#pragma unroll
+          for (int k = 0; k < kChunk; ++k) {
+            const V x = ominus_cap<V>(c[k], r[k].y, p.g.cap);
+            acc = x > acc ? x : acc;
+          }
+          if (acc == TOP) break;
+        }
+        if (acc > t.old) {
+          stcg(p.stage + ((w << 5) + lane), acc);
+          ++L.lifts;
+          ch = true;
+        }
+      } else if ((w << 5) + lane >= lo && (w << 5) + lane < hi) {
+        ++L.visits;  // a top vertex: one load, no lift
+      }
+    } else {
+      const uint32_t v = (w << 5) + lane;
+      if (v >= lo && v < hi) ch = lift_thread<V, false>(p, v, L);
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, ch);
+    if (m && lane == 0) atomicOr(chg + w, m);
+    L.phase_count += ch;
+  };
+
+  uint32_t parity = g_tma_parity[warp];
+  Tile cur, nxt;
+  uint32_t s = 0;
+  if (wfirst < w1) prepare(wfirst, 0, cur);
+  for (uint32_t w = wfirst; w < w1; w += nwarps) {
+    __syncwarp();  // stage s^1 was last read by this warp's previous tile
+    if (w + nwarps < w1) prepare(w + nwarps, s ^ 1u, nxt);
+    compute(w, s, cur, parity);
+    cur = nxt;
+    s ^= 1u;
+  }
+  __syncwarp();
+  if (lane == 0) g_tma_parity[warp] = parity;
   block_flush(L, p.ctr, sum_dst, s_cnt);
 }
 
@@ -524,7 +687,7 @@ struct NotCand {
 template <class V>
 __device__ __forceinline__ bool good_edge(const SolveParams<V>& p, int64_t fv,
                                           int2 r) {
-  const V ct = ldcg(p.stage + r.x);
+  const V ct = gather(p.stage + r.x);
   if (ct == Top<V>::v) return true;
   return ct != NotCand<V>::v && fv < static_cast<int64_t>(ct) - r.y;
 }
@@ -536,18 +699,19 @@ __device__ __forceinline__ bool cert_keep_thread(const SolveParams<V>& p,
   for (uint32_t i = b; i < e; i += 4) {
     int2 r[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (i + k < e) r[k] = ld_edge(p.g.edge + i + k);
+    for (int k = 0; k < 4; ++k) r[k] = ld_edge(p.g.edge + min(i + k, e - 1));
+    V c[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c[k] = gather(p.stage + r[k].x);
     bool all = true, any = false;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      if (i + k < e) {
-        ++L.cert_edges;
-        const bool g = good_edge<V>(p, fv, r[k]);
-        all &= g;
-        any |= g;
-      }
+      const bool g = c[k] == Top<V>::v ||
+                     (c[k] != NotCand<V>::v && fv < static_cast<int64_t>(c[k]) - r[k].y);
+      all &= g;
+      any |= g;
     }
+    L.cert_edges += min(4u, e - i);
     if (P0 && !all) return false;
     if (!P0 && any) return true;
   }
@@ -626,12 +790,15 @@ __device__ __noinline__ void phase_seed(const SolveParams<V>& p, unsigned int* s
       const uint32_t b = __ldg(g.off + v), e = __ldg(g.off + v + 1);
       uint32_t first_nn = e;
       bool any_neg = false;
-      for (uint32_t i = b; i < e; ++i) {
-        const int w = __ldg(&g.edge[i].y);
-        if (w < 0)
-          any_neg = true;
-        else if (first_nn == e)
-          first_nn = i;
+      for (uint32_t i = b; i < e && (p0 ? first_nn == e : !any_neg); i += kChunk) {
+        int w[kChunk];
+#pragma unroll
+        for (int k = 0; k < kChunk; ++k) w[k] = __ldg(&g.edge[min(i + k, e - 1)].y);
+#pragma unroll
+        for (int k = kChunk - 1; k >= 0; --k) {
+          if (w[k] < 0) any_neg = true;
+          else if (i + k < e) first_nn = min(first_nn, i + k);
+        }
       }
       if (p0) {
         seeded = first_nn == e;
@@ -702,12 +869,20 @@ __device__ __noinline__ void phase_lift(const SolveParams<V>& p, bool dense, int
       if (dense) sh->fr_cnt[buf][c] = 0;
     }
   if (dense) {
+    SubTimer st(p.ctr);
     block_rows<V>(p, class_size(g, 2), slot_dyn + 1,
                   [gp = &g](uint32_t i) { return class_item(*gp, 2, i); }, chg, sum_dst);
+    st.lap(kSubHeavy);
     warp_rows<V>(p, class_size(g, 1), slot_dyn + 0,
                  [gp = &g](uint32_t i) { return class_item(*gp, 1, i); }, chg, sum_dst);
+    st.lap(kSubMedium);
     dense_light<V, true>(p, g.rb[kP0L], g.rb[kP0M], chg, sum_dst);
-    dense_light<V, false>(p, g.rb[kP1L], g.rb[kP1M], chg, sum_dst);
+    st.lap(kSubLightP0);
+    if (p.use_tma)
+      dense_light_p1<V>(p, g.rb[kP1L], g.rb[kP1M], chg, sum_dst);
+    else
+      dense_light<V, false>(p, g.rb[kP1L], g.rb[kP1M], chg, sum_dst);
+    st.lap(kSubLightP1);
   } else {
     const uint32_t* list = p.fr[buf];
     const uint32_t cL = vload(&sh->fr_cnt[buf][0]);
@@ -718,7 +893,9 @@ __device__ __noinline__ void phase_lift(const SolveParams<V>& p, bool dense, int
     block_rows<V>(p, cH, slot_dyn + 1, [=](uint32_t i) { return ldcg(lH + i); }, chg,
                   sum_dst);
     warp_rows<V>(p, cM, slot_dyn + 0, [=](uint32_t i) { return ldcg(lM + i); }, chg, sum_dst);
+    SubTimer st(p.ctr);
     sparse_light<V>(p, list, cL, chg, sum_dst);
+    st.lap(kSubSparseLight);
     // leave the membership bitmap clear for the next activation
     for (uint32_t i = tid; i < cL + cM + cH; i += nthreads) {
       const uint32_t v = i < cL        ? ldcg(list + i)
@@ -898,7 +1075,7 @@ __device__ __noinline__ void phase_activate(const SolveParams<V>& p, const uint3
         if (valid) {
           ++L.act;
           u = __ldg(g.csrc + idx);
-          if (ldcg(p.f + u) != Top<V>::v) {
+          if (gather(p.f + u) != Top<V>::v) {
             const uint32_t bit = 1u << (u & 31u);
             add = !(atomicOr(p.frb + (u >> 5), bit) & bit);
             c = size_class(g, u);
@@ -916,7 +1093,7 @@ __device__ __noinline__ void phase_activate(const SolveParams<V>& p, const uint3
 
 // ========================================================== the kernel ===
 #ifndef EGS_MIN_BLOCKS
-#define EGS_MIN_BLOCKS 4  // resident CTAs per SM the register budget must allow
+#define EGS_MIN_BLOCKS 2  // resident CTAs per SM: 128 registers, no spills in the lift loops
 #endif
 template <class V>
 __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
@@ -952,6 +1129,7 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
     }
   };
 
+  tma_init_barriers();
   begin_phase();
   phase_seed<V>(p, slot_sum());
   end_phase(0);

@@ -261,7 +261,7 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   d_tmp.release();
 
   // relabelled edge records + (dst, src) pairs of the transpose
-  c->edge = dalloc<int2>(m);
+  c->edge = dalloc<int2>(m + 2);  // +2: 16-byte rounding of TMA spans
   DevBuf d_ck0, d_cv0, d_ck1;
   uint32_t* ck0 = d_ck0.alloc<uint32_t>(m);
   uint32_t* cv0 = d_cv0.alloc<uint32_t>(m);
@@ -352,7 +352,10 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     // Persistent grid: every CTA co-resident (cooperative launch).
     int per_sm = 0;
     const void* kfn = c->vbits == 32 ? solve_kernel<uint32_t>() : solve_kernel<uint64_t>();
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, egs::kBlock, 0));
+    CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)egs::kLiftSmemBytes));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, egs::kBlock,
+                                                     egs::kLiftSmemBytes));
     if (per_sm < 1) throw Fail(EGS_ERR_CUDA, "solve kernel cannot be resident");
     const int full = per_sm * c->num_sms;
     int want = opts.grid_ctas > 0 ? opts.grid_ctas
@@ -363,7 +366,9 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
 
     // Keep the measure resident in L2 while the edge stream goes through.
     int max_win = 0;
-    if (cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, c->device) ==
+    const bool want_win = std::getenv("EGS_NO_L2WIN") == nullptr;
+    if (want_win &&
+        cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, c->device) ==
             cudaSuccess &&
         max_win > 0 && n > 0) {
       int persist_max = 0;
@@ -420,6 +425,7 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
   p.sh = c->scratch;
   p.ctr = c->ctr;
   p.mode = o.mode;
+  p.use_tma = o.no_tma ? 0 : 1;
   p.certify = o.certify;
   p.cert_interval = o.cert_interval > 0 ? o.cert_interval : 4;
   p.sparse_div = o.sparse_div > 0 ? (uint32_t)o.sparse_div : 4u;
@@ -443,7 +449,7 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
   CK(cudaMemsetAsync(c->ctr, 0, egs::kNumCounters * sizeof(unsigned long long), s));
   void* args[] = {&p};
   CK(cudaLaunchCooperativeKernel(solve_kernel<V>(), dim3(c->grid), dim3(egs::kBlock), args,
-                                 0, s));
+                                 egs::kLiftSmemBytes, s));
   CK(cudaEventRecord(c->ev[1], s));
   CK(cudaMemcpyAsync(c->h_ctr, c->ctr, egs::kNumCounters * sizeof(unsigned long long),
                      cudaMemcpyDeviceToHost, s));
@@ -486,6 +492,8 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
     st->lift_bytes = (uint64_t)lift;
     st->algo_bytes = (uint64_t)(lift + seed + cert + act);
     st->kernel_launches = 1;
+    for (int k = 0; k < 5; ++k)
+      st->lift_sub_seconds[k] = h[egs::kSubHeavy + k] * 1e-9 / (double)c->grid;
     st->value_bits = (uint32_t)c->vbits;
     st->grid_ctas = (uint32_t)c->grid;
   }
