@@ -600,6 +600,83 @@ __device__ __noinline__ void dense_light_p1(const SolveParams<V>& p, uint32_t lo
   block_flush(L, p.ctr, sum_dst, s_cnt);
 }
 
+// Player-0 light rows of a dense round.  Almost every player-0 lift is
+// settled by its witness edge, so the cost is one dependent gather per
+// vertex; a lane takes four vertices (one per 32-vertex word of a 128-vertex
+// group) so four witness gathers are in flight per thread.  Vertices whose
+// witness is violated are compacted into a per-warp shared-memory queue and
+// re-lifted 32 at a time, one row per lane, so a few violated rows never
+// serialise a warp.
+constexpr int kP0Unroll = 4;
+
+template <class V>
+__device__ __noinline__ void dense_light_p0(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
+                                            uint32_t* chg, unsigned int* sum_dst) {
+  constexpr V TOP = Top<V>::v;
+  constexpr int U = kP0Unroll;
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  __shared__ uint32_t s_q[kWarps][32 * U + 32];
+  Local L;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  uint32_t* q = s_q[warp];
+  uint32_t qn = 0;  // warp-uniform queue length
+  auto drain = [&](uint32_t keep) {
+    while (qn > keep) {
+      const uint32_t take = qn - keep < 32u ? qn - keep : 32u;
+      const uint32_t base = qn - take;
+      __syncwarp();
+      bool ch = false;
+      uint32_t v = 0;
+      if (lane < take) {
+        v = q[base + lane];
+        ch = lift_thread<V, true>(p, v, L);
+      }
+      if (ch) set_bit(chg, v);
+      L.phase_count += ch;
+      qn = base;
+      __syncwarp();
+    }
+  };
+  const uint32_t nwarps = gridDim.x * kWarps;
+  const uint32_t gw = blockIdx.x * kWarps + warp;
+  const uint32_t w0 = lo >> 5, w1 = (hi + 31) >> 5;
+  for (uint32_t wb = w0 + gw * U; wb < w1; wb += nwarps * U) {
+    V old[U], cw[U];
+    int2 we[U];
+    bool in[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const uint32_t v = ((wb + k) << 5) + lane;
+      in[k] = wb + k < w1 && v >= lo && v < hi;
+      old[k] = in[k] ? ldcg(p.f + v) : TOP;
+      we[k] = in[k] ? ldcg(p.wit + v) : make_int2(0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) cw[k] = old[k] != TOP ? gather(p.f + we[k].x) : TOP;
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const uint32_t v = ((wb + k) << 5) + lane;
+      bool viol = false;
+      if (in[k]) {
+        ++L.visits;
+        if (old[k] != TOP) {
+          viol = old[k] < ominus_cap<V>(cw[k], we[k].y, p.g.cap);
+          L.witness += !viol;
+        }
+      }
+      const uint32_t m = __ballot_sync(0xffffffffu, viol);
+      if (viol) {
+        --L.visits;  // lift_thread counts its own visit
+        q[qn + __popc(m & lanemask_lt())] = v;
+      }
+      qn += __popc(m);
+    }
+    drain(31);  // keep fewer than a warp's worth queued
+  }
+  drain(0);
+  block_flush(L, p.ctr, sum_dst, s_cnt);
+}
+
 // Light rows of a sparse frontier list, one thread each.
 template <class V>
 __device__ __noinline__ void sparse_light(const SolveParams<V>& p, const uint32_t* list,
@@ -769,79 +846,179 @@ __device__ __forceinline__ uint32_t class_size(const Graph& g, int c) {
   return (g.rb[c + 1] - g.rb[c]) + (g.rb[c + 4] - g.rb[c + 3]);
 }
 
-// f = 0 (host memset); frontier = vertices violating their condition at
-// f = 0: player 0 with only negative moves, player 1 with some negative move
-// (solver_par.cpp:366-387).  The player-0 witness starts at the first
-// non-negative edge (satisfied at f = 0).  Seeds go to frontier buffer 0.
+// Round 1 straight from the weights.  With f = 0 everywhere a lift reads no
+// measure at all: f(t) ⊖ w = max(0, -w), so delta(0)(v) = max(0, -min_w)
+// for player 1 and max(0, -max_w) for player 0.  The vertices it raises are
+// exactly the reference's seeds (solver_par.cpp:366-387: player 0 with only
+// negative moves, player 1 with some negative move), so this one pass over
+// the weights is both the seeding and the first synchronous round of
+// solve_frontier / solve_sweep.  The player-0 witness starts at the argmin:
+// the first non-negative edge, else the least negative one.
 template <class V>
-__device__ __noinline__ void phase_seed(const SolveParams<V>& p, unsigned int* slot_sum) {
+__device__ __forceinline__ void round1_finish(const SolveParams<V>& p, uint32_t v, bool p0,
+                                              int minw, int maxw, uint32_t imax, V& val) {
+  val = ominus_cap<V>(V(0), p0 ? maxw : minw, p.g.cap);
+  if (p0) p.wit[v] = __ldg(p.g.edge + imax);
+  if (val > V(0)) stcg(p.stage + v, val);
+}
+
+// light rows: one thread per row, aligned 32-vertex words per warp
+template <class V>
+__device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
+                                          uint32_t* chg, unsigned int* sum_dst) {
   __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
   const Graph& g = p.g;
-  const uint32_t n = g.n;
   Local L;
+  const uint32_t lane = lane_id();
   const uint32_t nwarps = gridDim.x * kWarps;
   const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5;
-  for (uint32_t v0 = gw * 32; v0 < n; v0 += nwarps * 32) {
-    const uint32_t v = v0 + lane_id();
-    bool seeded = false;
-    const int cls = v < n ? size_class(g, v) : 0;
-    if (v < n && cls == 0) {
+  for (uint32_t w = (lo >> 5) + gw; w < (hi + 31) >> 5; w += nwarps) {
+    const uint32_t v = (w << 5) + lane;
+    V val = 0;
+    if (v >= lo && v < hi) {
       const bool p0 = v < g.rb[kP1L];
       const uint32_t b = __ldg(g.off + v), e = __ldg(g.off + v + 1);
-      uint32_t first_nn = e;
-      bool any_neg = false;
-      for (uint32_t i = b; i < e && (p0 ? first_nn == e : !any_neg); i += kChunk) {
-        int w[kChunk];
+      int minw = INT32_MAX, maxw = INT32_MIN;
+      uint32_t imax = b;
+      for (uint32_t i = b; i < e; i += kChunk) {
+        int wt[kChunk];
 #pragma unroll
-        for (int k = 0; k < kChunk; ++k) w[k] = __ldg(&g.edge[min(i + k, e - 1)].y);
+        for (int k = 0; k < kChunk; ++k) wt[k] = __ldcs(&g.edge[min(i + k, e - 1)].y);
 #pragma unroll
-        for (int k = kChunk - 1; k >= 0; --k) {
-          if (w[k] < 0) any_neg = true;
-          else if (i + k < e) first_nn = min(first_nn, i + k);
+        for (int k = 0; k < kChunk; ++k) {
+          minw = min(minw, wt[k]);
+          if (wt[k] > maxw) {
+            maxw = wt[k];
+            imax = min(i + k, e - 1);
+          }
         }
+        if (p0 && maxw >= 0) break;  // a satisfied move: delta = 0
       }
-      if (p0) {
-        seeded = first_nn == e;
-        p.wit[v] = __ldg(g.edge + (seeded ? b : first_nn));
-      } else {
-        seeded = any_neg;
-      }
+      round1_finish<V>(p, v, p0, minw, maxw, imax, val);
+      ++L.visits;
+      ++L.apps;
+      L.edges += e - b;
     }
-    // medium/heavy rows: the warp scans each such row cooperatively
-    uint32_t todo = __ballot_sync(0xffffffffu, v < n && cls != 0);
-    while (todo) {
-      const int src = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const uint32_t u = v0 + src;
-      const bool p0 = u < g.rb[kP1L];
-      const uint32_t b = __ldg(g.off + u), e = __ldg(g.off + u + 1);
-      uint32_t first_nn = 0xFFFFFFFFu;
-      bool any_neg = false;
-      for (uint32_t i = b + lane_id(); i - lane_id() < e; i += 32) {
-        bool neg = false, nn = false;
-        if (i < e) {
-          const int w = __ldg(&g.edge[i].y);
-          neg = w < 0;
-          nn = !neg;
-        }
-        any_neg |= __any_sync(0xffffffffu, neg);
-        const uint32_t m = __ballot_sync(0xffffffffu, nn);
-        if (m && first_nn == 0xFFFFFFFFu) first_nn = i - lane_id() + __ffs(m) - 1;
-        if (p0 ? first_nn != 0xFFFFFFFFu : any_neg) break;
-      }
-      const bool sd = p0 ? first_nn == 0xFFFFFFFFu : any_neg;
-      if (lane_id() == (uint32_t)src) {
-        seeded = sd;
-        if (p0) p.wit[u] = __ldg(g.edge + (sd ? b : first_nn));
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-      warp_append(seeded && cls == c, v, p.fr[0] + p.cbase[c], &p.sh->fr_cnt[0][c]);
-    if (seeded) set_bit(p.frb, v);
-    L.phase_count += seeded;
+    const bool raised = val > V(0);
+    const uint32_t m = __ballot_sync(0xffffffffu, raised);
+    if (m && lane == 0) atomicOr(chg + w, m);
+    L.phase_count += raised;
+    L.lifts += raised;
   }
-  block_flush(L, p.ctr, slot_sum + 2, s_cnt);
+  block_flush(L, p.ctr, sum_dst, s_cnt);
+}
+
+// medium rows: one warp per row; heavy rows: one CTA per row (dynamic claims)
+template <class V>
+__device__ __noinline__ void round1_long(const SolveParams<V>& p, uint32_t* chg,
+                                         unsigned int* sum_dst, unsigned int* slot_dyn) {
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  __shared__ int s_min[kWarps], s_max[kWarps];
+  __shared__ uint32_t s_imax[kWarps];
+  __shared__ unsigned int s_item;
+  const Graph& g = p.g;
+  Local L;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  // heavy: the CTA strides the row, block-reduces min / max / argmax
+  const uint32_t nH = class_size(g, 2);
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_item = atomicAdd(slot_dyn + 1, 1u);
+    __syncthreads();
+    const uint32_t it = s_item;
+    if (it >= nH) break;
+    const uint32_t u = class_item(g, 2, it);
+    const bool p0 = u < g.rb[kP1L];
+    const uint32_t b = __ldg(g.off + u), e = __ldg(g.off + u + 1);
+    int minw = INT32_MAX, maxw = INT32_MIN;
+    uint32_t imax = b;
+    for (uint32_t i = b + threadIdx.x; i < e; i += kBlock) {
+      const int w = __ldcs(&g.edge[i].y);
+      minw = min(minw, w);
+      if (w > maxw) {
+        maxw = w;
+        imax = i;
+      }
+    }
+    const int wmin = __reduce_min_sync(0xffffffffu, minw);
+    const int wmax = __reduce_max_sync(0xffffffffu, maxw);
+    const uint32_t bal = __ballot_sync(0xffffffffu, maxw == wmax);
+    const uint32_t wimax = __shfl_sync(0xffffffffu, imax, __ffs(bal) - 1);
+    if (lane == 0) {
+      s_min[warp] = wmin;
+      s_max[warp] = wmax;
+      s_imax[warp] = wimax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int mn = s_min[0], mx = s_max[0];
+      uint32_t im = s_imax[0];
+      for (int k = 1; k < kWarps; ++k) {
+        mn = min(mn, s_min[k]);
+        if (s_max[k] > mx) {
+          mx = s_max[k];
+          im = s_imax[k];
+        }
+      }
+      V val;
+      round1_finish<V>(p, u, p0, mn, mx, im, val);
+      ++L.visits;
+      ++L.apps;
+      L.edges += e - b;
+      if (val > V(0)) {
+        set_bit(chg, u);
+        ++L.phase_count;
+        ++L.lifts;
+      }
+    }
+  }
+  __syncthreads();
+  // medium: one warp per row
+  const uint32_t nM = class_size(g, 1);
+  for (;;) {
+    uint32_t it = 0;
+    if (lane == 0) it = atomicAdd(slot_dyn + 0, 1u);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= nM) break;
+    const uint32_t u = class_item(g, 1, it);
+    const bool p0 = u < g.rb[kP1L];
+    const uint32_t b = __ldg(g.off + u), e = __ldg(g.off + u + 1);
+    int minw = INT32_MAX, maxw = INT32_MIN;
+    uint32_t imax = b;
+    for (uint32_t i0 = b; i0 < e; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      const int w = i < e ? __ldcs(&g.edge[i].y) : INT32_MAX;
+      minw = min(minw, __reduce_min_sync(0xffffffffu, w));
+      const int cmax = __reduce_max_sync(0xffffffffu, i < e ? w : INT32_MIN);
+      if (cmax > maxw) {
+        maxw = cmax;
+        imax = i0 + __ffs(__ballot_sync(0xffffffffu, i < e && w == cmax)) - 1;
+      }
+      if (p0 && maxw >= 0) break;
+    }
+    if (lane == 0) {
+      V val;
+      round1_finish<V>(p, u, p0, minw, maxw, imax, val);
+      ++L.visits;
+      ++L.apps;
+      L.edges += e - b;
+      if (val > V(0)) {
+        set_bit(chg, u);
+        ++L.phase_count;
+        ++L.lifts;
+      }
+    }
+  }
+  block_flush(L, p.ctr, sum_dst, s_cnt);
+}
+
+template <class V>
+__device__ __noinline__ void phase_round1(const SolveParams<V>& p, uint32_t* chg,
+                                          unsigned int* slot_sum, unsigned int* slot_dyn) {
+  const Graph& g = p.g;
+  round1_long<V>(p, chg, slot_sum + 0, slot_dyn);
+  round1_light<V>(p, g.rb[kP0L], g.rb[kP0M], chg, slot_sum + 0);
+  round1_light<V>(p, g.rb[kP1L], g.rb[kP1M], chg, slot_sum + 0);
 }
 
 // One lift round.  Dense: every vertex (top ones are skipped after one
@@ -876,7 +1053,7 @@ __device__ __noinline__ void phase_lift(const SolveParams<V>& p, bool dense, int
     warp_rows<V>(p, class_size(g, 1), slot_dyn + 0,
                  [gp = &g](uint32_t i) { return class_item(*gp, 1, i); }, chg, sum_dst);
     st.lap(kSubMedium);
-    dense_light<V, true>(p, g.rb[kP0L], g.rb[kP0M], chg, sum_dst);
+    dense_light_p0<V>(p, g.rb[kP0L], g.rb[kP0M], chg, sum_dst);
     st.lap(kSubLightP0);
     if (p.use_tma)
       dense_light_p1<V>(p, g.rb[kP1L], g.rb[kP1M], chg, sum_dst);
@@ -1130,29 +1307,22 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
   };
 
   tma_init_barriers();
-  begin_phase();
-  phase_seed<V>(p, slot_sum());
-  end_phase(0);
-  uint32_t frontier = prev_sum(2);
 
-  unsigned long long round = 0, rounds_dense = 0, rounds_sparse = 0, cert_attempts = 0,
+  // ---- round 1: seeding + the first lift, from the weights alone
+  begin_phase();
+  phase_round1<V>(p, p.chg[0], slot_sum(), slot_dyn());
+  end_phase(0);
+  uint32_t changed = prev_sum(0);
+  unsigned long long round = 1, rounds_dense = 1, rounds_sparse = 0, cert_attempts = 0,
                      cert_passes = 0;
   int K = p.cert_interval > 0 ? p.cert_interval : 4;
   unsigned long long next_cert = (unsigned long long)K;
   int buf = 0;
-  bool dense = p.mode == kModeDense ||
-               (p.mode == kModeAuto && (unsigned long long)frontier * p.sparse_div >= n);
   unsigned int status = 0;
 
-  while (frontier > 0 || dense) {
-    uint32_t* chg = p.chg[round & 1];
-    begin_phase();
-    if (leader && p.timeout_ns && t_prev - t_start > p.timeout_ns) sh->stop = 1;
-    phase_lift<V>(p, dense, buf, chg, p.chg[(round + 1) & 1], slot_sum(), slot_dyn());
-    end_phase(1);
-    ++(dense ? rounds_dense : rounds_sparse);
-    uint32_t changed = prev_sum(0);
-    ++round;
+  for (;;) {
+    // `changed` vertices were raised by round `round`, marked in chg
+    uint32_t* chg = p.chg[(round - 1) & 1];
     if (changed == 0) break;  // a round that raised nothing: least fixpoint
     begin_phase();
     phase_commit<V>(p, chg);
@@ -1166,6 +1336,7 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
       break;
     }
 
+    // ---- certificate
     bool certified_any = false;
     if (p.certify && round >= next_cert) {
       ++cert_attempts;
@@ -1189,20 +1360,29 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
       next_cert = round + (unsigned long long)K;
     }
 
-    // next round: dense, or activate the predecessors of changed vertices
-    const bool dense_next =
+    // ---- next round: dense, or a frontier of the predecessors of changed
+    // vertices (solver_par.cpp:402-410)
+    const bool dense =
         p.mode == kModeDense ||
         (p.mode == kModeAuto &&
          (certified_any || (double)changed * p.avg_in_deg * p.sparse_div >= (double)n));
-    if (!dense_next) {
+    if (!dense) {
       begin_phase();
       phase_activate<V>(p, chg, buf ^ 1, slot_sum());
       end_phase(3);
       buf ^= 1;
-      frontier = prev_sum(2);
-      if (frontier == 0) break;  // every changed vertex has only top predecessors
+      if (prev_sum(2) == 0) break;  // every changed vertex has only top predecessors
     }
-    dense = dense_next;
+
+    // ---- lift round `round + 1`
+    uint32_t* next = p.chg[round & 1];
+    begin_phase();
+    if (leader && p.timeout_ns && t_prev - t_start > p.timeout_ns) sh->stop = 1;
+    phase_lift<V>(p, dense, buf, next, chg, slot_sum(), slot_dyn());
+    end_phase(1);
+    ++(dense ? rounds_dense : rounds_sparse);
+    ++round;
+    changed = prev_sum(0);
   }
 
   if (leader) {
