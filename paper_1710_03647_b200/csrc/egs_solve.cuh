@@ -1091,13 +1091,25 @@ __device__ __noinline__ void phase_lift(const SolveParams<V>& p, bool dense, int
 // solve_sweep (solver_par.cpp:205-228, 389-417).
 template <class V>
 __device__ __noinline__ void phase_commit(const SolveParams<V>& p, const uint32_t* chg) {
+  constexpr int U = 8;  // words per warp step, all loads issued before any store
   const uint32_t n = p.g.n;
+  const uint32_t nwords = (n + 31) >> 5;
   const uint32_t nwarps = gridDim.x * kWarps;
   const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5;
-  for (uint32_t w = gw; w < (n + 31) >> 5; w += nwarps) {
-    const uint32_t bits = ldcg(chg + w);
-    const uint32_t v = (w << 5) + lane_id();
-    if ((bits >> lane_id()) & 1u) stcg(p.f + v, ldcg(p.stage + v));
+  const uint32_t lane = lane_id();
+  for (uint32_t w0 = gw * U; w0 < nwords; w0 += nwarps * U) {
+    uint32_t bits[U];
+    V val[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) bits[k] = w0 + k < nwords ? ldcg(chg + w0 + k) : 0u;
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const uint32_t v = ((w0 + k) << 5) + lane;
+      val[k] = ((bits[k] >> lane) & 1u) ? ldcg(p.stage + v) : V(0);
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if ((bits[k] >> lane) & 1u) stcg(p.f + ((w0 + k) << 5) + lane, val[k]);
   }
 }
 
