@@ -41,7 +41,7 @@ $(ORACLE_CLI): oracle/egs_oracle_cli.c oracle/egs_oracle.c oracle/egs_oracle.h
 # calling llround without <cmath>.  Skipped when the reference is absent (the
 # GPU box uses the prebuilt .so that travels with the snapshot).
 ref:
-	@if [ -d $(REF)/src ]; then $(MAKE) --no-print-directory $(REF_LIB); \
+	@if [ -d $(REF)/src ]; then $(MAKE) --no-print-directory $(REF_LIB) $(DROPIN_BINS); \
 	 else echo "reference sources absent; using prebuilt $(REF_LIB) if present"; fi
 
 REF_SRCS := $(wildcard $(REF)/src/*.cpp)
@@ -58,7 +58,26 @@ oracle/_ref/ref_shim.o: oracle/ref_shim.cpp
 $(REF_LIB): $(REF_OBJS) oracle/_ref/ref_shim.o
 	$(CXX) -shared -o $@ $^ -lpthread
 
+# The C++ drop-in (integration/), compiled against the reference headers and
+# linked with the reference library + libegs_b200.so: its parity test and
+# the `egsolve solve` equivalent.  Built where /root/reference exists; the
+# binaries travel to the GPU box with oracle/_ref.
+DROPIN_BINS := oracle/_ref/test_solver_gpu oracle/_ref/egsolve_gpu
+DROPIN_FLAGS := -std=c++20 -O2 -Iinclude -Iintegration -I$(REF)/include
+DROPIN_LINK := oracle/_ref/solver_gpu.o -Loracle/_ref -legsolve_ref -L$(PKG) -l:libegs_b200.so \
+	-Wl,-rpath,'$$ORIGIN:$$ORIGIN/../../$(PKG)' -lpthread
+
+oracle/_ref/solver_gpu.o: integration/solver_gpu.cpp integration/solver_gpu.hpp include/egs_gpu.h
+	@mkdir -p oracle/_ref
+	$(CXX) $(DROPIN_FLAGS) -fPIC -c $< -o $@
+
+oracle/_ref/test_solver_gpu: tests/cpp/test_solver_gpu.cpp oracle/_ref/solver_gpu.o $(REF_LIB) $(LIB)
+	$(CXX) $(DROPIN_FLAGS) $< -o $@ $(DROPIN_LINK)
+
+oracle/_ref/egsolve_gpu: integration/egsolve_gpu.cpp oracle/_ref/solver_gpu.o $(REF_LIB) $(LIB)
+	$(CXX) $(DROPIN_FLAGS) $< -o $@ $(DROPIN_LINK)
+
 clean:
-	rm -f $(CSRC)/*.o $(LIB) $(ORACLE_LIB) $(ORACLE_CLI) oracle/_ref/*.o $(REF_LIB)
+	rm -f $(CSRC)/*.o $(LIB) $(ORACLE_LIB) $(ORACLE_CLI) oracle/_ref/*.o $(REF_LIB) $(DROPIN_BINS)
 
 .PHONY: all ref clean
