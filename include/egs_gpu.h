@@ -139,6 +139,51 @@ int egs_ctx_read_measure(egs_ctx* ctx, int64_t* f_out);
 int egs_ctx_is_progress_measure(egs_ctx* ctx, const int64_t* f);
 void egs_ctx_destroy(egs_ctx* ctx);
 
+/* ---------------------------------------------------------------------
+ * Multi-GPU partition.  One process per GPU; rank r owns the
+ * relabelled vertex range [own_lo, own_hi) of `slice` vertices.  The
+ * arena is replicated on every GPU, the measure f and the staging /
+ * candidate array are replicated with `padded` = world * slice entries, and
+ * the host exchanges the owned slices between steps (all-gather over NCCL:
+ * paper_1710_03647_b200/distributed.py).  The device addresses of those two
+ * arrays are returned so a collective library can operate on them in place.
+ * Steps restate the phases of egs_ctx_solve restricted to the owned range. */
+typedef struct egs_part egs_part;
+typedef struct egs_part_layout {
+  uint32_t num_vertices;  /* n */
+  uint32_t slice;         /* vertices per rank, multiple of 32 */
+  uint32_t padded;        /* world * slice: entries of the replicated arrays */
+  uint32_t own_lo;        /* this rank's range of relabelled ids */
+  uint32_t own_hi;
+  uint32_t value_bytes;   /* 4 (u32) or 8 (u64); top = all ones */
+  uint64_t f_dev;         /* device address of the replicated measure */
+  uint64_t stage_dev;     /* device address of the replicated staging array */
+} egs_part_layout;
+
+#define EGS_STEP_ROUND1 0     /* seeding + round 1 from the weights */
+#define EGS_STEP_LIFT 1       /* one dense lift round (stages raised values) */
+#define EGS_STEP_COMMIT 2     /* staged -> f for this rank's raised vertices */
+#define EGS_STEP_CERT_INIT 3  /* candidate snapshot into the staging array */
+#define EGS_STEP_CERT_PRUNE 4 /* one certificate pass */
+#define EGS_STEP_CERT_APPLY 5 /* certified vertices -> top */
+
+/* opts->n_gpus must equal world. */
+int egs_part_create(const egs_arena_view* arena, const egs_gpu_opts* opts, int32_t rank,
+                    int32_t world, egs_part** out, egs_part_layout* layout,
+                    egs_gpu_stats* stats);
+/* Runs one step on this rank's range.  `parity` selects the changed bitmap
+ * of the current round (round & 1).  counts[0] = vertices raised (ROUND1,
+ * LIFT) or certified (CERT_APPLY); counts[1] = candidates removed
+ * (CERT_PRUNE).  Blocks until the step is done. */
+int egs_part_step(egs_part* part, int32_t step, int32_t parity, uint64_t* counts);
+/* Resets f, the bitmaps and the counters for a new solve. */
+int egs_part_reset(egs_part* part);
+/* The replicated measure in the reference's raw encoding, original ids. */
+int egs_part_read_measure(egs_part* part, int64_t* f_out);
+/* Counters accumulated by this rank's steps since the last reset. */
+int egs_part_counters(egs_part* part, egs_gpu_stats* stats);
+void egs_part_destroy(egs_part* part);
+
 /* Output format: write_solution(make_solution(arena, report)) (io.cpp:178-210)
  * with the first-witness strategy of extract_strategy (measure_ops.cpp:56-80).
  * Returns the text length; writes at most cap bytes when buf != NULL;

@@ -126,7 +126,28 @@ class GpuStats(C.Structure):
         return d
 
 
+class PartLayout(C.Structure):
+    _fields_ = [
+        ("num_vertices", C.c_uint32), ("slice", C.c_uint32), ("padded", C.c_uint32),
+        ("own_lo", C.c_uint32), ("own_hi", C.c_uint32), ("value_bytes", C.c_uint32),
+        ("f_dev", C.c_uint64), ("stage_dev", C.c_uint64),
+    ]
+
+
 _P = C.c_void_p
+lib.egs_part_create.argtypes = [C.POINTER(ArenaView), C.POINTER(GpuOpts), C.c_int32, C.c_int32,
+                                C.POINTER(_P), C.POINTER(PartLayout), C.POINTER(GpuStats)]
+lib.egs_part_create.restype = C.c_int
+lib.egs_part_step.argtypes = [_P, C.c_int32, C.c_int32, C.POINTER(C.c_uint64)]
+lib.egs_part_step.restype = C.c_int
+lib.egs_part_reset.argtypes = [_P]
+lib.egs_part_reset.restype = C.c_int
+lib.egs_part_read_measure.argtypes = [_P, _P]
+lib.egs_part_read_measure.restype = C.c_int
+lib.egs_part_counters.argtypes = [_P, C.POINTER(GpuStats)]
+lib.egs_part_counters.restype = C.c_int
+lib.egs_part_destroy.argtypes = [_P]
+lib.egs_part_destroy.restype = None
 lib.egs_gpu_opts_default.argtypes = [C.POINTER(GpuOpts)]
 lib.egs_gpu_solve.argtypes = [C.POINTER(ArenaView), C.POINTER(GpuOpts), _P, C.POINTER(GpuStats)]
 lib.egs_gpu_solve.restype = C.c_int

@@ -111,6 +111,7 @@ struct SolveParams {
   uint32_t cbase[3];
   Scratch* sh;
   unsigned long long* ctr;  // kNumCounters
+  uint32_t own_lo, own_hi;  // vertex range this GPU lifts (multi-GPU); [0, n) alone
   int mode;
   int use_tma;
   int certify;
@@ -711,6 +712,7 @@ __device__ __noinline__ void warp_rows(const SolveParams<V>& p, uint32_t count,
     i = __shfl_sync(0xffffffffu, i, 0);
     if (i >= count) break;
     const uint32_t v = items(i);
+    if (!owned(p, v)) continue;
     const bool p0 = v < p.g.rb[kP1L];
     const bool ch = p0 ? lift_warp<V, true>(p, v, L) : lift_warp<V, false>(p, v, L);
     if (ch && lane_id() == 0) {
@@ -735,6 +737,7 @@ __device__ __noinline__ void block_rows(const SolveParams<V>& p, uint32_t count,
     const uint32_t i = s.item;
     if (i >= count) break;
     const uint32_t v = items(i);
+    if (!owned(p, v)) continue;
     const bool p0 = v < p.g.rb[kP1L];
     const bool ch = p0 ? lift_block<V, true>(p, v, L, s) : lift_block<V, false>(p, v, L, s);
     if (ch && threadIdx.x == 0) {
@@ -845,6 +848,18 @@ __device__ __forceinline__ uint32_t class_item(const Graph& g, int c, uint32_t i
 __device__ __forceinline__ uint32_t class_size(const Graph& g, int c) {
   return (g.rb[c + 1] - g.rb[c]) + (g.rb[c + 4] - g.rb[c + 3]);
 }
+template <class V>
+__device__ __forceinline__ bool owned(const SolveParams<V>& p, uint32_t v) {
+  return v >= p.own_lo && v < p.own_hi;
+}
+template <class V>
+__device__ __forceinline__ uint32_t clip_lo(const SolveParams<V>& p, uint32_t lo) {
+  return lo > p.own_lo ? lo : p.own_lo;
+}
+template <class V>
+__device__ __forceinline__ uint32_t clip_hi(const SolveParams<V>& p, uint32_t hi) {
+  return hi < p.own_hi ? hi : p.own_hi;
+}
 
 // Round 1 straight from the weights.  With f = 0 everywhere a lift reads no
 // measure at all: f(t) ⊖ w = max(0, -w), so delta(0)(v) = max(0, -min_w)
@@ -928,6 +943,7 @@ __device__ __noinline__ void round1_long(const SolveParams<V>& p, uint32_t* chg,
     const uint32_t it = s_item;
     if (it >= nH) break;
     const uint32_t u = class_item(g, 2, it);
+    if (!owned(p, u)) continue;
     const bool p0 = u < g.rb[kP1L];
     const uint32_t b = __ldg(g.off + u), e = __ldg(g.off + u + 1);
     int minw = INT32_MAX, maxw = INT32_MIN;
@@ -981,6 +997,7 @@ __device__ __noinline__ void round1_long(const SolveParams<V>& p, uint32_t* chg,
     it = __shfl_sync(0xffffffffu, it, 0);
     if (it >= nM) break;
     const uint32_t u = class_item(g, 1, it);
+    if (!owned(p, u)) continue;
     const bool p0 = u < g.rb[kP1L];
     const uint32_t b = __ldg(g.off + u), e = __ldg(g.off + u + 1);
     int minw = INT32_MAX, maxw = INT32_MIN;
@@ -1017,8 +1034,8 @@ __device__ __noinline__ void phase_round1(const SolveParams<V>& p, uint32_t* chg
                                           unsigned int* slot_sum, unsigned int* slot_dyn) {
   const Graph& g = p.g;
   round1_long<V>(p, chg, slot_sum + 0, slot_dyn);
-  round1_light<V>(p, g.rb[kP0L], g.rb[kP0M], chg, slot_sum + 0);
-  round1_light<V>(p, g.rb[kP1L], g.rb[kP1M], chg, slot_sum + 0);
+  round1_light<V>(p, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]), chg, slot_sum + 0);
+  round1_light<V>(p, clip_lo(p, g.rb[kP1L]), clip_hi(p, g.rb[kP1M]), chg, slot_sum + 0);
 }
 
 // One lift round.  Dense: every vertex (top ones are skipped after one
@@ -1053,12 +1070,12 @@ __device__ __noinline__ void phase_lift(const SolveParams<V>& p, bool dense, int
     warp_rows<V>(p, class_size(g, 1), slot_dyn + 0,
                  [gp = &g](uint32_t i) { return class_item(*gp, 1, i); }, chg, sum_dst);
     st.lap(kSubMedium);
-    dense_light_p0<V>(p, g.rb[kP0L], g.rb[kP0M], chg, sum_dst);
+    dense_light_p0<V>(p, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]), chg, sum_dst);
     st.lap(kSubLightP0);
     if (p.use_tma)
-      dense_light_p1<V>(p, g.rb[kP1L], g.rb[kP1M], chg, sum_dst);
+      dense_light_p1<V>(p, clip_lo(p, g.rb[kP1L]), clip_hi(p, g.rb[kP1M]), chg, sum_dst);
     else
-      dense_light<V, false>(p, g.rb[kP1L], g.rb[kP1M], chg, sum_dst);
+      dense_light<V, false>(p, clip_lo(p, g.rb[kP1L]), clip_hi(p, g.rb[kP1M]), chg, sum_dst);
     st.lap(kSubLightP1);
   } else {
     const uint32_t* list = p.fr[buf];
@@ -1097,11 +1114,12 @@ __device__ __noinline__ void phase_commit(const SolveParams<V>& p, const uint32_
   const uint32_t nwarps = gridDim.x * kWarps;
   const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5;
   const uint32_t lane = lane_id();
-  for (uint32_t w0 = gw * U; w0 < nwords; w0 += nwarps * U) {
+  const uint32_t wlo = p.own_lo >> 5, whi = min(nwords, (p.own_hi + 31) >> 5);
+  for (uint32_t w0 = wlo + gw * U; w0 < whi; w0 += nwarps * U) {
     uint32_t bits[U];
     V val[U];
 #pragma unroll
-    for (int k = 0; k < U; ++k) bits[k] = w0 + k < nwords ? ldcg(chg + w0 + k) : 0u;
+    for (int k = 0; k < U; ++k) bits[k] = w0 + k < whi ? ldcg(chg + w0 + k) : 0u;
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       const uint32_t v = ((w0 + k) << 5) + lane;
@@ -1124,7 +1142,7 @@ __device__ __noinline__ void phase_cert_init(const SolveParams<V>& p, const uint
   const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
   const uint32_t nthreads = gridDim.x * kBlock;
   Local L;
-  for (uint32_t v = tid; v < p.g.n; v += nthreads) {
+  for (uint32_t v = p.own_lo + tid; v < p.own_hi; v += nthreads) {
     const V fv = ldcg(p.f + v);
     const bool raised = (ldcg(chg + (v >> 5)) >> (v & 31u)) & 1u;
     stcg(p.stage + v, fv == Top<V>::v ? fv : raised ? fv : NotCand<V>::v);
@@ -1151,6 +1169,7 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
     const uint32_t i = s_item;
     if (i >= nH) break;
     const uint32_t v = class_item(g, 2, i);
+    if (!owned(p, v)) continue;
     const V cvv = ldcg(p.stage + v);
     if (cvv == Top<V>::v || cvv == NotCand<V>::v) continue;
     const int64_t fv = (int64_t)cvv;
@@ -1173,6 +1192,7 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
     i = __shfl_sync(0xffffffffu, i, 0);
     if (i >= nM) break;
     const uint32_t v = class_item(g, 1, i);
+    if (!owned(p, v)) continue;
     const V cvv = ldcg(p.stage + v);
     if (cvv == Top<V>::v || cvv == NotCand<V>::v) continue;
     const int64_t fv = (int64_t)cvv;
@@ -1188,8 +1208,8 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
   }
   // light candidates: a thread each
   for (int side = 0; side < 2; ++side) {
-    const uint32_t lo = side ? g.rb[kP1L] : g.rb[kP0L];
-    const uint32_t hi = side ? g.rb[kP1M] : g.rb[kP0M];
+    const uint32_t lo = clip_lo(p, side ? g.rb[kP1L] : g.rb[kP0L]);
+    const uint32_t hi = clip_hi(p, side ? g.rb[kP1M] : g.rb[kP0M]);
     for (uint32_t v = lo + tid; v < hi; v += nthreads) {
       const V cvv = ldcg(p.stage + v);
       if (cvv == Top<V>::v || cvv == NotCand<V>::v) continue;
@@ -1216,10 +1236,10 @@ __device__ __noinline__ void phase_cert_apply(const SolveParams<V>& p, uint32_t*
   const uint32_t nwarps = gridDim.x * kWarps;
   const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5;
   Local L;
-  for (uint32_t w = gw; w < (n + 31) >> 5; w += nwarps) {
+  for (uint32_t w = (p.own_lo >> 5) + gw; w < (p.own_hi + 31) >> 5; w += nwarps) {
     const uint32_t v = (w << 5) + lane_id();
     bool hit = false;
-    if (v < n) {
+    if (v < n && owned(p, v)) {
       const V cvv = ldcg(p.stage + v);
       if (cvv != Top<V>::v && cvv != NotCand<V>::v) {
         stcg(p.f + v, Top<V>::v);
@@ -1404,6 +1424,39 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
     p.ctr[kCertAttempts] = cert_attempts;
     p.ctr[kCertPasses] = cert_passes;
     p.ctr[kStatus] = status;
+  }
+}
+
+// ============================================== multi-GPU step kernel ===
+// One phase of the partitioned solve, restricted to this
+// GPU's vertex range [own_lo, own_hi).  The host exchanges the owned slices
+// of f / stage between steps (NCCL all-gather) and decides the schedule,
+// which is the same as k_solve's dense schedule.
+enum PartStep : int {
+  kStepRound1 = 0,
+  kStepLift = 1,
+  kStepCommit = 2,
+  kStepCertInit = 3,
+  kStepCertPrune = 4,
+  kStepCertApply = 5
+};
+
+template <class V>
+__global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
+    k_part_step(const __grid_constant__ SolveParams<V> p, int step, int parity) {
+  tma_init_barriers();
+  unsigned int* sum = p.sh->sum[0];
+  unsigned int* dyn = p.sh->dyn[0];
+  uint32_t* cur = p.chg[parity & 1];
+  uint32_t* other = p.chg[(parity & 1) ^ 1];
+  switch (step) {
+    case kStepRound1: phase_round1<V>(p, cur, sum, dyn); break;
+    case kStepLift: phase_lift<V>(p, true, 0, cur, other, sum, dyn); break;
+    case kStepCommit: phase_commit<V>(p, cur); break;
+    case kStepCertInit: phase_cert_init<V>(p, cur, sum); break;
+    case kStepCertPrune: phase_cert_prune<V>(p, sum, dyn); break;
+    case kStepCertApply: phase_cert_apply<V>(p, cur, sum); break;
+    default: break;
   }
 }
 

@@ -132,6 +132,11 @@ struct egs_ctx {
   cudaEvent_t ev[2] = {nullptr, nullptr};
   int grid = 0;
   bool solved = false;
+  // multi-GPU partition (egs_part_*): this rank's range of relabelled ids and
+  // the padded length of the replicated arrays (world * slice)
+  int rank = 0, world = 1;
+  uint32_t slice = 0, n_pad = 0, own_lo = 0, own_hi = 0;
+  int full_grid = 0;
 
   egs::Graph graph() const {
     egs::Graph g{};
@@ -291,8 +296,9 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   tm.mark("CSC sort + offsets");
 }
 
-egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_stats* st) {
-  validate_opts(opts);
+egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_stats* st,
+                    int rank = 0, int world = 1) {
+  if (world == 1) validate_opts(opts);
   if (!a) throw Fail(EGS_ERR_INVALID_CONFIG, "null arena");
   if (a->num_edges >= 0xFFFFFFFFull)
     throw Fail(EGS_ERR_UNSUPPORTED, "arenas with >= 2^32 edges are not supported on the device");
@@ -330,13 +336,19 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     CK(cudaMallocHost(&c->h_ctr, egs::kNumCounters * sizeof(unsigned long long)));
     c->ctr = dalloc<unsigned long long>(egs::kNumCounters);
     c->scratch = dalloc<egs::Scratch>(1);
-    c->f = dalloc<uint8_t>((size_t)n * vsz);
+    c->rank = rank;
+    c->world = world;
+    c->slice = (uint32_t)((((uint64_t)n + world - 1) / world + 31) / 32 * 32);
+    c->n_pad = world == 1 ? n : c->slice * (uint32_t)world;
+    c->own_lo = world == 1 ? 0 : std::min<uint32_t>(n, c->slice * (uint32_t)rank);
+    c->own_hi = world == 1 ? n : std::min<uint32_t>(n, c->slice * (uint32_t)(rank + 1));
+    c->f = dalloc<uint8_t>((size_t)std::max<uint32_t>(c->n_pad, 1) * vsz);
     c->chg[0] = dalloc<uint32_t>(words);
     c->chg[1] = dalloc<uint32_t>(words);
     c->frb = dalloc<uint32_t>(words);
     c->fr[0] = dalloc<uint32_t>(n);
     c->fr[1] = dalloc<uint32_t>(n);
-    c->stage = dalloc<uint8_t>((size_t)n * vsz);
+    c->stage = dalloc<uint8_t>((size_t)std::max<uint32_t>(c->n_pad, 1) * vsz);
     c->f64 = dalloc<int64_t>(n);
     if (n > 0) {
       build_arena(c, a);
@@ -354,6 +366,11 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     const void* kfn = c->vbits == 32 ? solve_kernel<uint32_t>() : solve_kernel<uint64_t>();
     CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)egs::kLiftSmemBytes));
+    const void* pfn = c->vbits == 32
+                          ? reinterpret_cast<const void*>(&egs::k_part_step<uint32_t>)
+                          : reinterpret_cast<const void*>(&egs::k_part_step<uint64_t>);
+    CK(cudaFuncSetAttribute(pfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)egs::kLiftSmemBytes));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, egs::kBlock,
                                                      egs::kLiftSmemBytes));
     if (per_sm < 1) throw Fail(EGS_ERR_CUDA, "solve kernel cannot be resident");
@@ -363,6 +380,7 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
                                         1, ((uint64_t)n + egs::kBlock - 1) / egs::kBlock));
     if (const char* e = std::getenv("EGS_GRID")) want = std::atoi(e);
     c->grid = std::max(1, std::min(want, full));
+    c->full_grid = full;
 
     // Keep the measure resident in L2 while the edge stream goes through.
     int max_win = 0;
@@ -401,14 +419,11 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
 }
 
 template <class V>
-void run_solve(egs_ctx* c, egs_gpu_stats* st) {
-  cudaStream_t s = c->stream;
+egs::SolveParams<V> make_params(egs_ctx* c, unsigned long long* budget_out) {
   const uint32_t n = c->n;
   const egs_gpu_opts& o = c->opts;
-  const size_t words = ((size_t)n + 31) / 32;
   const uint32_t szL = (c->rb[1] - c->rb[0]) + (c->rb[4] - c->rb[3]);
   const uint32_t szM = (c->rb[2] - c->rb[1]) + (c->rb[5] - c->rb[4]);
-
   egs::SolveParams<V> p{};
   p.g = c->graph();
   p.f = static_cast<V*>(c->f);
@@ -439,6 +454,67 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
   }
   p.round_budget = budget;
   p.timeout_ns = o.timeout_seconds > 0 ? (unsigned long long)(o.timeout_seconds * 1e9) : 0ull;
+  p.own_lo = c->world == 1 ? 0 : c->own_lo;
+  p.own_hi = c->world == 1 ? n : c->own_hi;
+  if (budget_out) *budget_out = budget;
+  return p;
+}
+
+// SolveReport-style counters from the device counter block (algorithmic
+// bytes as defined in DESIGN.md §4).
+template <class V>
+void fill_stats(egs_ctx* c, const unsigned long long* h, double ms, egs_gpu_stats* st) {
+  const uint32_t n = c->n;
+  const size_t words = ((size_t)n + 31) / 32;
+  const double sv = sizeof(V);
+  st->lifts = h[egs::kLifts];
+  st->applications = h[egs::kApps];
+  st->edges_relaxed = h[egs::kEdges];
+  st->witness_checks = h[egs::kWitness];
+  st->activations = h[egs::kActScanned];
+  st->certified = h[egs::kCertified];
+  st->pops = h[egs::kPops];
+  st->visits = h[egs::kVisits];
+  st->cert_rows = h[egs::kCertScanned];
+  st->cert_edges = h[egs::kCertEdges];
+  st->rounds = h[egs::kRounds];
+  st->dense_rounds = h[egs::kDenseRounds];
+  st->sparse_rounds = h[egs::kSparseRounds];
+  st->cert_attempts = h[egs::kCertAttempts];
+  st->cert_passes = h[egs::kCertPasses];
+  st->solve_seconds = ms * 1e-3;
+  st->seed_seconds = h[egs::kTimeSeed] * 1e-9;
+  st->lift_seconds = h[egs::kTimeLift] * 1e-9;
+  st->cert_seconds = h[egs::kTimeCert] * 1e-9;
+  st->activate_seconds = h[egs::kTimeAct] * 1e-9;
+  // Algorithmic bytes: what each phase must move at least.
+  // round 1 (counted as one dense round: n visits, m edges) reads records
+  // but neither f(v) nor f(t): drop those gathers from the lift formula
+  const double r1 = (double)c->m * sv + (double)n * sv;
+  const double lift = (double)st->visits * sv + (double)st->witness_checks * (8 + sv) +
+                      (double)st->applications * 8 + (double)st->edges_relaxed * (8 + sv) +
+                      (double)st->lifts * sv - (st->rounds ? r1 : 0.0);
+  const double seed = 0.0;
+  const double cert = (double)st->cert_attempts * n * (2 * (sv + 1)) +
+                      (double)st->cert_rows * (1 + sv + 8) +
+                      (double)st->cert_edges * (8 + sv + 1);
+  const double act = (double)st->activations * (4 + sv) + (double)st->sparse_rounds * words * 4;
+  st->lift_bytes = (uint64_t)lift;
+  st->algo_bytes = (uint64_t)(lift + seed + cert + act);
+  st->kernel_launches = 1;
+  for (int k = 0; k < 5; ++k)
+    st->lift_sub_seconds[k] = h[egs::kSubHeavy + k] * 1e-9 / (double)c->grid;
+  st->value_bits = (uint32_t)c->vbits;
+  st->grid_ctas = (uint32_t)c->grid;
+}
+
+template <class V>
+void run_solve(egs_ctx* c, egs_gpu_stats* st) {
+  cudaStream_t s = c->stream;
+  const uint32_t n = c->n;
+  const size_t words = ((size_t)n + 31) / 32;
+  unsigned long long budget = 0;
+  egs::SolveParams<V> p = make_params<V>(c, &budget);
 
   CK(cudaEventRecord(c->ev[0], s));
   CK(cudaMemsetAsync(c->f, 0, (size_t)n * sizeof(V), s));
@@ -458,45 +534,7 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
   CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
   const unsigned long long* h = c->h_ctr;
   c->solved = h[egs::kStatus] == 0;
-  if (st) {
-    const double sv = sizeof(V);
-    st->lifts = h[egs::kLifts];
-    st->applications = h[egs::kApps];
-    st->edges_relaxed = h[egs::kEdges];
-    st->witness_checks = h[egs::kWitness];
-    st->activations = h[egs::kActScanned];
-    st->certified = h[egs::kCertified];
-    st->pops = h[egs::kPops];
-    st->visits = h[egs::kVisits];
-    st->cert_rows = h[egs::kCertScanned];
-    st->cert_edges = h[egs::kCertEdges];
-    st->rounds = h[egs::kRounds];
-    st->dense_rounds = h[egs::kDenseRounds];
-    st->sparse_rounds = h[egs::kSparseRounds];
-    st->cert_attempts = h[egs::kCertAttempts];
-    st->cert_passes = h[egs::kCertPasses];
-    st->solve_seconds = ms * 1e-3;
-    st->seed_seconds = h[egs::kTimeSeed] * 1e-9;
-    st->lift_seconds = h[egs::kTimeLift] * 1e-9;
-    st->cert_seconds = h[egs::kTimeCert] * 1e-9;
-    st->activate_seconds = h[egs::kTimeAct] * 1e-9;
-    // Algorithmic bytes: what each phase must move at least.
-    const double lift = (double)st->visits * sv + (double)st->witness_checks * (8 + sv) +
-                        (double)st->applications * 8 + (double)st->edges_relaxed * (8 + sv) +
-                        (double)st->lifts * sv;
-    const double seed = (double)c->m * 8 + (double)n * 8;
-    const double cert = (double)st->cert_attempts * n * (2 * (sv + 1)) +
-                        (double)st->cert_rows * (1 + sv + 8) +
-                        (double)st->cert_edges * (8 + sv + 1);
-    const double act = (double)st->activations * (4 + sv) + (double)st->sparse_rounds * words * 4;
-    st->lift_bytes = (uint64_t)lift;
-    st->algo_bytes = (uint64_t)(lift + seed + cert + act);
-    st->kernel_launches = 1;
-    for (int k = 0; k < 5; ++k)
-      st->lift_sub_seconds[k] = h[egs::kSubHeavy + k] * 1e-9 / (double)c->grid;
-    st->value_bits = (uint32_t)c->vbits;
-    st->grid_ctas = (uint32_t)c->grid;
-  }
+  if (st) fill_stats<V>(c, h, ms, st);
   if (h[egs::kStatus] == 2) throw Fail(EGS_ERR_TIMEOUT, "solve timed out");
   if (h[egs::kStatus] == 5)
     throw Fail(EGS_ERR_BOUND, "round budget of " + std::to_string(budget) +
@@ -573,7 +611,138 @@ int guarded(F&& fn) {
 
 }  // namespace
 
+struct egs_part {
+  egs_ctx* c = nullptr;
+};
+
+namespace {
+
+template <class V>
+void part_step(egs_ctx* c, int step, int parity, uint64_t* counts) {
+  cudaStream_t s = c->stream;
+  egs::SolveParams<V> p = make_params<V>(c, nullptr);
+  CK(cudaMemsetAsync(c->scratch, 0, sizeof(egs::Scratch), s));
+  void* args[] = {&p, &step, &parity};
+  const void* fn = reinterpret_cast<const void*>(&egs::k_part_step<V>);
+  CK(cudaLaunchKernel(fn, dim3(c->full_grid), dim3(egs::kBlock), args, egs::kLiftSmemBytes, s));
+  CK(cudaGetLastError());
+  unsigned int sums[4] = {0, 0, 0, 0};
+  CK(cudaMemcpyAsync(sums, c->scratch->sum[0], sizeof(sums), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (counts) {
+    counts[0] = sums[0];
+    counts[1] = sums[1];
+  }
+}
+
+void part_reset(egs_ctx* c) {
+  cudaStream_t s = c->stream;
+  const size_t words = ((size_t)c->n + 31) / 32;
+  const size_t vsz = c->vbits / 8;
+  CK(cudaMemsetAsync(c->f, 0, (size_t)std::max<uint32_t>(c->n_pad, 1) * vsz, s));
+  CK(cudaMemsetAsync(c->chg[0], 0, words * 4, s));
+  CK(cudaMemsetAsync(c->chg[1], 0, words * 4, s));
+  CK(cudaMemsetAsync(c->frb, 0, words * 4, s));
+  CK(cudaMemsetAsync(c->ctr, 0, egs::kNumCounters * sizeof(unsigned long long), s));
+  CK(cudaStreamSynchronize(s));
+  c->solved = true;
+}
+
+}  // namespace
+
 extern "C" {
+
+int egs_part_create(const egs_arena_view* arena, const egs_gpu_opts* opts, int32_t rank,
+                    int32_t world, egs_part** out, egs_part_layout* layout,
+                    egs_gpu_stats* stats) {
+  return guarded([&] {
+    egs_gpu_opts o;
+    if (opts)
+      o = *opts;
+    else
+      egs_gpu_opts_default(&o);
+    if (world < 1 || rank < 0 || rank >= world)
+      throw Fail(EGS_ERR_INVALID_CONFIG, "rank must be in [0, world)");
+    if (o.n_gpus != world) throw Fail(EGS_ERR_INVALID_CONFIG, "opts.n_gpus must equal world");
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    egs_ctx* c = ctx_create(arena, o, stats, rank, world);
+    egs_part* p = new egs_part();
+    p->c = c;
+    try {
+      part_reset(c);
+    } catch (...) {
+      ctx_free(c);
+      delete p;
+      throw;
+    }
+    if (layout) {
+      layout->num_vertices = c->n;
+      layout->slice = c->slice;
+      layout->padded = c->n_pad;
+      layout->own_lo = c->own_lo;
+      layout->own_hi = c->own_hi;
+      layout->value_bytes = (uint32_t)(c->vbits / 8);
+      layout->f_dev = (uint64_t)(uintptr_t)c->f;
+      layout->stage_dev = (uint64_t)(uintptr_t)c->stage;
+    }
+    *out = p;
+  });
+}
+
+int egs_part_step(egs_part* part, int32_t step, int32_t parity, uint64_t* counts) {
+  return guarded([&] {
+    if (!part) throw Fail(EGS_ERR_INVALID_CONFIG, "null partition");
+    if (step < EGS_STEP_ROUND1 || step > EGS_STEP_CERT_APPLY)
+      throw Fail(EGS_ERR_INVALID_CONFIG, "unknown step");
+    egs_ctx* c = part->c;
+    CK(cudaSetDevice(c->device));
+    if (c->n == 0) {
+      if (counts) counts[0] = counts[1] = 0;
+      return;
+    }
+    if (c->vbits == 32)
+      part_step<uint32_t>(c, step, parity, counts);
+    else
+      part_step<uint64_t>(c, step, parity, counts);
+  });
+}
+
+int egs_part_reset(egs_part* part) {
+  return guarded([&] {
+    if (!part) throw Fail(EGS_ERR_INVALID_CONFIG, "null partition");
+    CK(cudaSetDevice(part->c->device));
+    part_reset(part->c);
+  });
+}
+
+int egs_part_read_measure(egs_part* part, int64_t* f_out) {
+  return guarded([&] {
+    if (!part) throw Fail(EGS_ERR_INVALID_CONFIG, "null partition");
+    part->c->solved = true;
+    ctx_read(part->c, f_out);
+  });
+}
+
+int egs_part_counters(egs_part* part, egs_gpu_stats* stats) {
+  return guarded([&] {
+    if (!part || !stats) throw Fail(EGS_ERR_INVALID_CONFIG, "null argument");
+    egs_ctx* c = part->c;
+    CK(cudaSetDevice(c->device));
+    CK(cudaMemcpy(c->h_ctr, c->ctr, egs::kNumCounters * sizeof(unsigned long long),
+                  cudaMemcpyDeviceToHost));
+    std::memset(stats, 0, sizeof(*stats));
+    if (c->vbits == 32)
+      fill_stats<uint32_t>(c, c->h_ctr, 0.0, stats);
+    else
+      fill_stats<uint64_t>(c, c->h_ctr, 0.0, stats);
+  });
+}
+
+void egs_part_destroy(egs_part* part) {
+  if (!part) return;
+  ctx_free(part->c);
+  delete part;
+}
 
 void egs_gpu_opts_default(egs_gpu_opts* o) {
   std::memset(o, 0, sizeof(*o));

@@ -1,0 +1,141 @@
+"""Multi-rank orchestration of the partitioned solve (distributed.py).
+
+CPU: world_size 2 and 3 over gloo, each rank driving the numpy model of its
+partition steps (tests/partition_model.py); the result must equal the
+reference's least measure.  GPU: two ranks sharing one GPU, each driving the
+real device steps (egs_part_*) with a staged gloo exchange; and one rank over
+NCCL."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from arena_gen import random_arena
+from oracle_bindings import INT64_MAX, Oracle
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _cases():
+    cases = []
+    for seed in range(12):
+        n, edges, owners = random_arena(500 + seed, max_n=60, max_deg=5)
+        cases.append(("random", (n, edges, owners)))
+    cases.append(("fixed", (3000, 4, 100, 1)))
+    cases.append(("fixed", (2000, 8, 100000, 1)))
+    return cases
+
+
+def _worker_cpu(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+        from partition_model import NumpySteps
+        from paper_1710_03647_b200.distributed import TorchComm, solve_partitioned
+        oracle = Oracle()
+        out = []
+        for kind, args in _cases():
+            g = oracle.build(*args) if kind == "random" else oracle.fixed(*args)
+            off, dst, w, own = g.csr()
+            steps = NumpySteps(off, dst, w, own, g.a.credit_cap, rank, world)
+            comm = TorchComm(rank, world, staged=True)
+            rep = solve_partitioned(steps, comm)
+            want, _ = oracle.solve_seq(g)
+            out.append((kind, bool(np.array_equal(rep.measure, want)), rep.rounds,
+                        rep.cert_attempts))
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_partitioned_orchestration_gloo_cpu(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_cpu, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = results[0]
+    for r in range(world):
+        assert all(ok for _, ok, _, _ in results[r]), results[r]
+        # every rank agrees on the schedule
+        assert [x[2:] for x in results[r]] == [x[2:] for x in ref]
+
+
+def _worker_gpu(rank, world, port, q, backend):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group(backend, rank=rank, world_size=world)
+    try:
+        import json
+        import paper_1710_03647_b200 as egs
+        from paper_1710_03647_b200.distributed import DeviceSteps, TorchComm, solve_partitioned
+        from oracle_bindings import fnv1a64
+        golden = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))
+        out = []
+        for key, make in [("fixed/10000/4/100/1", lambda: egs.GameArena.fixed(10000, 4, 100, 1)),
+                          ("fixed/100000/16/100/1", lambda: egs.GameArena.fixed(100000, 16, 100, 1)),
+                          ("fixed/100000/8/100000/1", lambda: egs.GameArena.fixed(100000, 8, 100000, 1)),
+                          ("rmat/14/16/100/1", lambda: egs.GameArena.rmat(14, 16, 100, 1))]:
+            a = make()
+            steps = DeviceSteps(a, rank, world, egs.SolverOptions(device=0))
+            comm = TorchComm(rank, world, staged=(backend == "gloo"), device="cuda:0")
+            rep = solve_partitioned(steps, comm)
+            sol = egs.write_solution(a, rep.measure).encode()
+            out.append((key, f"{fnv1a64(sol):016x}" == golden[key]["solution_fnv"], rep.rounds))
+            steps.close()
+        for seed in range(20):
+            n, edges, owners = random_arena(900 + seed, max_n=80, max_deg=6)
+            a = egs.GameArena.build(n, edges, owners)
+            steps = DeviceSteps(a, rank, world, egs.SolverOptions(device=0))
+            rep = solve_partitioned(steps, TorchComm(rank, world, staged=True))
+            want = egs.solve(a, options=egs.SolverOptions(device=0)).measure
+            out.append((f"random{seed}", bool(np.array_equal(rep.measure, want)), rep.rounds))
+            steps.close()
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_gpu(world, backend):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_gpu, args=(r, world, port, q, backend))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=900) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        assert all(ok for _, ok, _ in results[r]), results[r]
+
+
+@pytest.mark.gpu
+def test_partitioned_device_two_ranks_one_gpu():
+    _run_gpu(2, "gloo")
+
+
+@pytest.mark.gpu
+def test_partitioned_device_nccl_single_rank():
+    _run_gpu(1, "nccl")
