@@ -136,6 +136,8 @@ class TorchComm:
         mine = t.narrow(0, self.rank * slice_, slice_)
         if not self.staged:
             self.dist.all_gather_into_tensor(t, mine)
+            # the next step runs on the library's own stream: wait for NCCL
+            self.torch.cuda.synchronize(t.device)
             return
         host = mine.detach().to("cpu", copy=True)
         parts = [self.torch.empty_like(host) for _ in range(self.world)]
@@ -162,6 +164,7 @@ class PartitionReport:
     wall_seconds: float = 0.0
     collectives: int = 0
     bytes_gathered: int = 0
+    kernel_launches: int = 0
     counters: dict = field(default_factory=dict)
 
 
@@ -174,14 +177,22 @@ def solve_partitioned(steps, comm, certify: bool = True, cert_interval: int = 4,
     ``comm`` exchanges the owned slices (``TorchComm``).  Every rank returns
     the same least progress measure."""
     t0 = time.perf_counter()
+    launches = 0
+    step_fn = steps.step
+
+    def step(kind, par):
+        nonlocal launches
+        launches += 1  # one k_part_step launch per call
+        return step_fn(kind, par)
+
     parity = 0
-    changed = comm.allreduce_sum(steps.step(STEP_ROUND1, parity)[0])
+    changed = comm.allreduce_sum(step(STEP_ROUND1, parity)[0])
     rounds = 1
     K = cert_interval if cert_interval > 0 else 4
     next_cert = K
     attempts = passes = certified = 0
     while changed:
-        steps.step(STEP_COMMIT, parity)
+        step(STEP_COMMIT, parity)
         comm.allgather(steps.f, steps.slice)
         if round_budget is not None and rounds >= round_budget:
             raise N.BoundExhaustedError(
@@ -190,27 +201,28 @@ def solve_partitioned(steps, comm, certify: bool = True, cert_interval: int = 4,
             raise N.TimeoutError_("solve timed out")
         if certify and rounds >= next_cert:
             attempts += 1
-            steps.step(STEP_CERT_INIT, parity)
+            step(STEP_CERT_INIT, parity)
             comm.allgather(steps.stage, steps.slice)
             while True:
-                removed = comm.allreduce_sum(steps.step(STEP_CERT_PRUNE, parity)[1])
+                removed = comm.allreduce_sum(step(STEP_CERT_PRUNE, parity)[1])
                 comm.allgather(steps.stage, steps.slice)
                 passes += 1
                 if removed == 0:
                     break
-            cert = comm.allreduce_sum(steps.step(STEP_CERT_APPLY, parity)[0])
+            cert = comm.allreduce_sum(step(STEP_CERT_APPLY, parity)[0])
             comm.allgather(steps.f, steps.slice)
             certified += cert
             if cert == 0:
                 K = min(2 * K, 64)
             next_cert = rounds + K
         parity ^= 1
-        changed = comm.allreduce_sum(steps.step(STEP_LIFT, parity)[0])
+        changed = comm.allreduce_sum(step(STEP_LIFT, parity)[0])
         rounds += 1
     f = steps.read_measure()
     return PartitionReport(
         measure=f, rounds=rounds, cert_attempts=attempts, cert_passes=passes,
         certified=certified, wall_seconds=time.perf_counter() - t0,
         collectives=comm.collectives, bytes_gathered=comm.bytes_gathered,
+        kernel_launches=launches,
         counters=steps.counters() if hasattr(steps, "counters") else {},
     )
