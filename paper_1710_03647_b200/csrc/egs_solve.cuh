@@ -107,6 +107,8 @@ struct SolveParams {
   int2* wit;            // player-0 witness edge record (ids < rb[3])
   uint32_t* chg[2];     // changed-vertex bitmaps, by round parity
   uint32_t* frb;        // frontier membership bitmap
+  uint32_t* rbm[2];     // certificate: removed-in-pass bitmaps
+  uint32_t* cbm;        // certificate: re-check dedup bitmap
   uint32_t* fr[2];      // frontier lists; sublist c starts at cbase[c]
   uint32_t cbase[3];
   Scratch* sh;
@@ -1142,6 +1144,7 @@ __device__ __noinline__ void phase_cert_init(const SolveParams<V>& p, const uint
   const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
   const uint32_t nthreads = gridDim.x * kBlock;
   Local L;
+  for (uint32_t w = tid; w < ((p.g.n + 31) >> 5); w += nthreads) p.rbm[1][w] = 0u;
   for (uint32_t v = p.own_lo + tid; v < p.own_hi; v += nthreads) {
     const V fv = ldcg(p.f + v);
     const bool raised = (ldcg(chg + (v >> 5)) >> (v & 31u)) & 1u;
@@ -1150,78 +1153,189 @@ __device__ __noinline__ void phase_cert_init(const SolveParams<V>& p, const uint
   block_flush(L, p.ctr, slot_sum + 1, s_cnt);
 }
 
-// Certificate, step 2: one pruning pass (removed count -> slot_sum[1]).
+// Certificate, step 2: pruning passes.  A removed candidate becomes
+// kNotCand in p.stage and its bit is set in `rbm` (removed in this pass), so
+// the next pass can be sparse: only candidate predecessors of this pass's
+// removals (phase_cert_mark, via the CSC) can lose their condition.
 template <class V>
-__device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned int* slot_sum,
-                                              unsigned int* slot_dyn) {
+__device__ __forceinline__ bool is_cand(V c) {
+  return c != Top<V>::v && c != NotCand<V>::v;
+}
+
+// One candidate, evaluated by the lanes a row's class gets; returns removed.
+template <class V>
+__device__ __forceinline__ bool cert_check_thread(const SolveParams<V>& p, uint32_t v, Local& L) {
+  const V cvv = ldcg(p.stage + v);
+  if (!is_cand<V>(cvv)) return false;
+  const bool keep = v < p.g.rb[kP1L] ? cert_keep_thread<V, true>(p, v, (int64_t)cvv, L)
+                                     : cert_keep_thread<V, false>(p, v, (int64_t)cvv, L);
+  ++L.cert_scanned;
+  if (!keep) stcg(p.stage + v, NotCand<V>::v);
+  return !keep;
+}
+
+// Heavy (CTA) and medium (warp) candidates from an item source; removal
+// bits go to `rbm`.  Block-uniform.
+template <class V, class ItemsH, class ItemsM>
+__device__ __forceinline__ void cert_long_rows(const SolveParams<V>& p, uint32_t nH,
+                                               ItemsH itemsH, uint32_t nM, ItemsM itemsM,
+                                               unsigned int* slot_dyn, uint32_t* rbm, Local& L) {
   __shared__ unsigned int s_item;
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
   const Graph& g = p.g;
-  const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
-  const uint32_t nthreads = gridDim.x * kBlock;
-  Local L;
-  // heavy candidates: a CTA each
-  const uint32_t nH = class_size(g, 2);
   for (;;) {
     __syncthreads();
     if (threadIdx.x == 0) s_item = atomicAdd(slot_dyn + 1, 1u);
     __syncthreads();
     const uint32_t i = s_item;
     if (i >= nH) break;
-    const uint32_t v = class_item(g, 2, i);
+    const uint32_t v = itemsH(i);
     if (!owned(p, v)) continue;
     const V cvv = ldcg(p.stage + v);
-    if (cvv == Top<V>::v || cvv == NotCand<V>::v) continue;
-    const int64_t fv = (int64_t)cvv;
-    const bool keep = v < g.rb[kP1L] ? cert_keep_block<V, true>(p, v, fv, L)
-                                     : cert_keep_block<V, false>(p, v, fv, L);
+    if (!is_cand<V>(cvv)) continue;
+    const bool keep = v < g.rb[kP1L] ? cert_keep_block<V, true>(p, v, (int64_t)cvv, L)
+                                     : cert_keep_block<V, false>(p, v, (int64_t)cvv, L);
     if (threadIdx.x == 0) {
       ++L.cert_scanned;
       if (!keep) {
         stcg(p.stage + v, NotCand<V>::v);
+        set_bit(rbm, v);
         ++L.phase_count;
       }
     }
   }
   __syncthreads();
-  // medium candidates: a warp each
-  const uint32_t nM = class_size(g, 1);
   for (;;) {
     uint32_t i = 0;
     if (lane_id() == 0) i = atomicAdd(slot_dyn + 0, 1u);
     i = __shfl_sync(0xffffffffu, i, 0);
     if (i >= nM) break;
-    const uint32_t v = class_item(g, 1, i);
+    const uint32_t v = itemsM(i);
     if (!owned(p, v)) continue;
     const V cvv = ldcg(p.stage + v);
-    if (cvv == Top<V>::v || cvv == NotCand<V>::v) continue;
-    const int64_t fv = (int64_t)cvv;
-    const bool keep = v < g.rb[kP1L] ? cert_keep_warp<V, true>(p, v, fv, L)
-                                     : cert_keep_warp<V, false>(p, v, fv, L);
+    if (!is_cand<V>(cvv)) continue;
+    const bool keep = v < g.rb[kP1L] ? cert_keep_warp<V, true>(p, v, (int64_t)cvv, L)
+                                     : cert_keep_warp<V, false>(p, v, (int64_t)cvv, L);
     if (lane_id() == 0) {
       ++L.cert_scanned;
       if (!keep) {
         stcg(p.stage + v, NotCand<V>::v);
+        set_bit(rbm, v);
         ++L.phase_count;
       }
     }
   }
-  // light candidates: a thread each
+}
+
+// Dense pass over every owned candidate (removed count -> slot_sum[1]).
+// `rbm_clear` (the bitmap two passes old) is zeroed for reuse.
+template <class V>
+__device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned int* slot_sum,
+                                              unsigned int* slot_dyn, uint32_t* rbm,
+                                              uint32_t* rbm_clear) {
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  const Graph& g = p.g;
+  const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
+  const uint32_t nthreads = gridDim.x * kBlock;
+  const uint32_t nwords = (g.n + 31) >> 5;
+  Local L;
+  for (uint32_t w = tid; w < nwords; w += nthreads) rbm_clear[w] = 0u;
+  auto itH = [gp = &g](uint32_t i) { return class_item(*gp, 2, i); };
+  auto itM = [gp = &g](uint32_t i) { return class_item(*gp, 1, i); };
+  cert_long_rows<V>(p, class_size(g, 2), itH, class_size(g, 1), itM, slot_dyn, rbm, L);
+  // light candidates: a thread each, aligned 32-vertex words per warp
+  const uint32_t nwarps = gridDim.x * kWarps;
+  const uint32_t gw = tid >> 5;
   for (int side = 0; side < 2; ++side) {
     const uint32_t lo = clip_lo(p, side ? g.rb[kP1L] : g.rb[kP0L]);
     const uint32_t hi = clip_hi(p, side ? g.rb[kP1M] : g.rb[kP0M]);
-    for (uint32_t v = lo + tid; v < hi; v += nthreads) {
-      const V cvv = ldcg(p.stage + v);
-      if (cvv == Top<V>::v || cvv == NotCand<V>::v) continue;
-      const int64_t fv = (int64_t)cvv;
-      const bool keep = side ? cert_keep_thread<V, false>(p, v, fv, L)
-                             : cert_keep_thread<V, true>(p, v, fv, L);
-      ++L.cert_scanned;
-      if (!keep) {
-        stcg(p.stage + v, NotCand<V>::v);
-        ++L.phase_count;
-      }
+    for (uint32_t w = (lo >> 5) + gw; w < (hi + 31) >> 5; w += nwarps) {
+      const uint32_t v = (w << 5) + lane_id();
+      const bool rem = v >= lo && v < hi && cert_check_thread<V>(p, v, L);
+      const uint32_t m = __ballot_sync(0xffffffffu, rem);
+      if (m && lane_id() == 0) atomicOr(rbm + w, m);
+      L.phase_count += rem;
     }
+  }
+  block_flush(L, p.ctr, slot_sum + 1, s_cnt);
+}
+
+// Sparse pass, step 1: the candidate predecessors of the vertices removed in
+// the last pass (bits of `rbm_in`) are queued once each (dedup bitmap cbm)
+// into the class sublists of p.fr[0], sized by qcnt[0..2] (this phase's
+// zeroed cursor slot); count -> slot_sum[2].
+template <class V>
+__device__ __noinline__ void phase_cert_mark(const SolveParams<V>& p, const uint32_t* rbm_in,
+                                             unsigned int* slot_sum, unsigned int* qcnt) {
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  const Graph& g = p.g;
+  const uint32_t nwords = (g.n + 31) >> 5;
+  const uint32_t nwarps = gridDim.x * kWarps;
+  const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+  Local L;
+  for (uint32_t w0 = gw * 32; w0 < nwords; w0 += nwarps * 32) {
+    const uint32_t wi = w0 + lane_id();
+    uint32_t bits = wi < nwords ? ldcg(rbm_in + wi) : 0u;
+    while (__any_sync(0xffffffffu, bits != 0u)) {
+      uint32_t b = 0, e = 0;
+      if (bits) {
+        const uint32_t u = (wi << 5) + (__ffs(bits) - 1);
+        bits &= bits - 1;
+        b = __ldg(g.coff + u);
+        e = __ldg(g.coff + u + 1);
+      }
+      warp_expand(b, e, [&](bool valid, uint32_t idx, uint32_t) {
+        bool add = false;
+        uint32_t v = 0;
+        int c = 0;
+        if (valid) {
+          v = __ldg(g.csrc + idx);
+          if (owned(p, v) && is_cand<V>(ldcg(p.stage + v))) {
+            const uint32_t bit = 1u << (v & 31u);
+            add = !(atomicOr(p.cbm + (v >> 5), bit) & bit);
+            c = size_class(g, v);
+          }
+        }
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc)
+          warp_append(add && c == cc, v, p.fr[0] + p.cbase[cc], qcnt + cc);
+        L.phase_count += add;
+      });
+    }
+  }
+  block_flush(L, p.ctr, slot_sum + 2, s_cnt);
+}
+
+// Sparse pass, step 2: re-check the queued candidates (removed -> slot_sum[1],
+// bits -> rbm); clears their dedup bits and the stale bitmap rbm_clear.
+template <class V>
+__device__ __noinline__ void phase_cert_check(const SolveParams<V>& p, const unsigned int* qcnt,
+                                              unsigned int* slot_sum, unsigned int* slot_dyn,
+                                              uint32_t* rbm, uint32_t* rbm_clear) {
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
+  const uint32_t nthreads = gridDim.x * kBlock;
+  const uint32_t nwords = (p.g.n + 31) >> 5;
+  Local L;
+  for (uint32_t w = tid; w < nwords; w += nthreads) rbm_clear[w] = 0u;
+  const uint32_t cL = vload(qcnt + 0);
+  const uint32_t cM = vload(qcnt + 1);
+  const uint32_t cH = vload(qcnt + 2);
+  const uint32_t* list = p.fr[0];
+  const uint32_t* lM = list + p.cbase[1];
+  const uint32_t* lH = list + p.cbase[2];
+  auto itH = [=](uint32_t i) { return ldcg(lH + i); };
+  auto itM = [=](uint32_t i) { return ldcg(lM + i); };
+  cert_long_rows<V>(p, cH, itH, cM, itM, slot_dyn, rbm, L);
+  for (uint32_t i = tid; i < cL; i += nthreads) {
+    const uint32_t v = ldcg(list + i);
+    if (cert_check_thread<V>(p, v, L)) {
+      set_bit(rbm, v);
+      ++L.phase_count;
+    }
+  }
+  for (uint32_t i = tid; i < cL + cM + cH; i += nthreads) {
+    const uint32_t v = i < cL ? ldcg(list + i) : i < cL + cM ? ldcg(lM + (i - cL)) : ldcg(lH + (i - cL - cM));
+    atomicAnd(p.cbm + (v >> 5), ~(1u << (v & 31u)));
   }
   block_flush(L, p.ctr, slot_sum + 1, s_cnt);
 }
@@ -1375,12 +1489,33 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
       begin_phase();
       phase_cert_init<V>(p, chg, slot_sum());
       end_phase(2);
-      for (;;) {
-        begin_phase();
-        phase_cert_prune<V>(p, slot_sum(), slot_dyn());
-        end_phase(2);
+      // pass 1 dense; later passes sparse while the removals are few
+      int rb = 1;
+      begin_phase();
+      phase_cert_prune<V>(p, slot_sum(), slot_dyn(), p.rbm[1], p.rbm[0]);
+      end_phase(2);
+      ++cert_passes;
+      uint32_t removed = prev_sum(1);
+      while (removed > 0) {
+        const bool sparse_pass =
+            p.mode != kModeDense &&
+            (double)removed * p.avg_in_deg * p.sparse_div < (double)n;
+        if (sparse_pass) {
+          begin_phase();
+          phase_cert_mark<V>(p, p.rbm[rb], slot_sum(), slot_dyn());
+          end_phase(2);
+          const unsigned int* queued = sh->dyn[(phase - 1) & 3];
+          begin_phase();
+          phase_cert_check<V>(p, queued, slot_sum(), slot_dyn(), p.rbm[rb ^ 1], p.rbm[rb]);
+          end_phase(2);
+        } else {
+          begin_phase();
+          phase_cert_prune<V>(p, slot_sum(), slot_dyn(), p.rbm[rb ^ 1], p.rbm[rb]);
+          end_phase(2);
+        }
+        rb ^= 1;
         ++cert_passes;
-        if (prev_sum(1) == 0) break;
+        removed = prev_sum(1);
       }
       begin_phase();
       phase_cert_apply<V>(p, chg, slot_sum());
@@ -1454,7 +1589,7 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
     case kStepLift: phase_lift<V>(p, true, 0, cur, other, sum, dyn); break;
     case kStepCommit: phase_commit<V>(p, cur); break;
     case kStepCertInit: phase_cert_init<V>(p, cur, sum); break;
-    case kStepCertPrune: phase_cert_prune<V>(p, sum, dyn); break;
+    case kStepCertPrune: phase_cert_prune<V>(p, sum, dyn, p.rbm[0], p.rbm[1]); break;
     case kStepCertApply: phase_cert_apply<V>(p, cur, sum); break;
     default: break;
   }

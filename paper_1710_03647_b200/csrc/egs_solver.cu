@@ -123,6 +123,8 @@ struct egs_ctx {
   int2* wit = nullptr;
   uint32_t* chg[2] = {nullptr, nullptr};
   uint32_t* frb = nullptr;
+  uint32_t* rbm[2] = {nullptr, nullptr};
+  uint32_t* cbm = nullptr;
   uint32_t* fr[2] = {nullptr, nullptr};
   void* stage = nullptr;
   egs::Scratch* scratch = nullptr;
@@ -158,7 +160,7 @@ void ctx_free(egs_ctx* c) {
   if (c->device >= 0) cudaSetDevice(c->device);
   void* ptrs[] = {c->off,    c->edge,   c->coff, c->csrc,  c->perm,
                   c->f,      c->wit,    c->chg[0], c->chg[1], c->frb,
-                  c->fr[0],  c->fr[1],  c->stage, c->scratch, c->ctr,
+                  c->fr[0],  c->fr[1],  c->stage, c->scratch, c->ctr, c->rbm[0], c->rbm[1], c->cbm,
                   c->f64};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -346,6 +348,9 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     c->chg[0] = dalloc<uint32_t>(words);
     c->chg[1] = dalloc<uint32_t>(words);
     c->frb = dalloc<uint32_t>(words);
+    c->rbm[0] = dalloc<uint32_t>(words);
+    c->rbm[1] = dalloc<uint32_t>(words);
+    c->cbm = dalloc<uint32_t>(words);
     c->fr[0] = dalloc<uint32_t>(n);
     c->fr[1] = dalloc<uint32_t>(n);
     c->stage = dalloc<uint8_t>((size_t)std::max<uint32_t>(c->n_pad, 1) * vsz);
@@ -431,6 +436,9 @@ egs::SolveParams<V> make_params(egs_ctx* c, unsigned long long* budget_out) {
   p.chg[0] = c->chg[0];
   p.chg[1] = c->chg[1];
   p.frb = c->frb;
+  p.rbm[0] = c->rbm[0];
+  p.rbm[1] = c->rbm[1];
+  p.cbm = c->cbm;
   p.fr[0] = c->fr[0];
   p.fr[1] = c->fr[1];
   p.cbase[0] = 0;
@@ -521,6 +529,7 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
   CK(cudaMemsetAsync(c->chg[0], 0, words * 4, s));
   CK(cudaMemsetAsync(c->chg[1], 0, words * 4, s));
   CK(cudaMemsetAsync(c->frb, 0, words * 4, s));
+  CK(cudaMemsetAsync(c->cbm, 0, words * 4, s));
   CK(cudaMemsetAsync(c->scratch, 0, sizeof(egs::Scratch), s));
   CK(cudaMemsetAsync(c->ctr, 0, egs::kNumCounters * sizeof(unsigned long long), s));
   void* args[] = {&p};
@@ -643,6 +652,7 @@ void part_reset(egs_ctx* c) {
   CK(cudaMemsetAsync(c->chg[0], 0, words * 4, s));
   CK(cudaMemsetAsync(c->chg[1], 0, words * 4, s));
   CK(cudaMemsetAsync(c->frb, 0, words * 4, s));
+  CK(cudaMemsetAsync(c->cbm, 0, words * 4, s));
   CK(cudaMemsetAsync(c->ctr, 0, egs::kNumCounters * sizeof(unsigned long long), s));
   CK(cudaStreamSynchronize(s));
   c->solved = true;

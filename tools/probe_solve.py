@@ -1,5 +1,6 @@
 """Quick device probe: solve the canonical configs and print stats (dev tool)."""
 import json
+import os
 import sys
 import time
 
@@ -25,7 +26,8 @@ def main():
         tg = time.time() - t0
         for mode in modes:
             for certify in (True,):
-                ds = egs.DeviceSolver(a, egs.SolverOptions(mode=mode, certify=certify))
+                kw = json.loads(os.environ.get("EGS_PROBE_OPTS", "{}"))
+                ds = egs.DeviceSolver(a, egs.SolverOptions(mode=mode, certify=certify, **kw))
                 for rep in range(3):
                     st = ds.solve()
                 d = st.as_dict()
