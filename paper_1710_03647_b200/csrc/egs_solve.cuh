@@ -1461,7 +1461,7 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
   uint32_t changed = prev_sum(0);
   unsigned long long round = 1, rounds_dense = 1, rounds_sparse = 0, cert_attempts = 0,
                      cert_passes = 0;
-  int K = p.cert_interval > 0 ? p.cert_interval : 4;
+  int K = p.cert_interval > 0 ? p.cert_interval : 2;
   unsigned long long next_cert = (unsigned long long)K;
   int buf = 0;
   unsigned int status = 0;
@@ -1523,7 +1523,11 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
       const uint32_t cert = prev_sum(0);
       certified_any = cert > 0;
       changed += cert;
-      if (!certified_any) K = K * 2 < 64 ? K * 2 : 64;
+      // geometric schedule: early attempts catch regular climbs (the
+      // canonical configs certify their losing region at round 2-4), later
+      // ones get rarer so a game without a climbing region pays O(log)
+      // attempts
+      K = K * 2 < 64 ? K * 2 : 64;
       next_cert = round + (unsigned long long)K;
     }
 
