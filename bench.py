@@ -466,7 +466,7 @@ def main():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="C4", choices=sorted(CONFIGS))
-    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--ref-sweeps", type=int, default=3,
                    help="reference sweeps per timed sample")
     p.add_argument("--cpu-steps", type=int, default=2)

@@ -342,32 +342,41 @@ class SolverOptions:
         return o
 
 
-@dataclass
 class SolveReport:
     """egsolve::SolveReport (solver.hpp:47-59); ``measure`` is the raw int64
-    encoding (INT64_MAX = top, energy.hpp:16)."""
-    measure: np.ndarray
-    w0: np.ndarray
-    w1: np.ndarray
-    lifts: int = 0
-    applications: int = 0
-    pops: int = 0
-    rounds: int = 0
-    wall_seconds: float = 0.0
-    variant: Variant = Variant.GPU
-    workers: int = 1
-    gpu: dict = field(default_factory=dict)
+    encoding (INT64_MAX = top, energy.hpp:16).  ``w0`` / ``w1`` are the
+    reference's winning_sets (measure_ops.cpp:43-54), computed on first use."""
+
+    def __init__(self, measure: np.ndarray, lifts: int = 0, applications: int = 0,
+                 pops: int = 0, rounds: int = 0, wall_seconds: float = 0.0,
+                 variant: "Variant" = None, workers: int = 1, gpu: Optional[dict] = None):
+        self.measure = measure
+        self.lifts, self.applications, self.pops, self.rounds = lifts, applications, pops, rounds
+        self.wall_seconds = wall_seconds
+        self.variant = Variant.GPU if variant is None else variant
+        self.workers = workers
+        self.gpu = gpu or {}
+        self._w = None
+
+    def _sets(self):
+        if self._w is None:
+            top = self.measure == INT64_MAX
+            self._w = (np.nonzero(~top)[0].astype(np.uint32), np.nonzero(top)[0].astype(np.uint32))
+        return self._w
+
+    @property
+    def w0(self) -> np.ndarray:
+        return self._sets()[0]
+
+    @property
+    def w1(self) -> np.ndarray:
+        return self._sets()[1]
 
 
 def _report(measure: np.ndarray, st: GpuStats, workers: int) -> SolveReport:
-    top = measure == INT64_MAX
-    # winning_sets (measure_ops.cpp:43-54): W0 = finite, W1 = top
     return SolveReport(
-        measure=measure,
-        w0=np.nonzero(~top)[0].astype(np.uint32),
-        w1=np.nonzero(top)[0].astype(np.uint32),
-        lifts=int(st.lifts), applications=int(st.applications), pops=int(st.pops),
-        rounds=int(st.rounds), wall_seconds=float(st.wall_seconds),
+        measure=measure, lifts=int(st.lifts), applications=int(st.applications),
+        pops=int(st.pops), rounds=int(st.rounds), wall_seconds=float(st.wall_seconds),
         variant=Variant.GPU, workers=workers, gpu=st.as_dict(),
     )
 

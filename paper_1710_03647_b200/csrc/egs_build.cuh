@@ -20,7 +20,7 @@
 
 namespace egs {
 
-// Class key of every vertex + histogram of the six classes; edge validation.
+// Class key of every vertex + histogram of the six classes.
 __global__ void k_classify(uint32_t n, const uint64_t* off64, const uint8_t* owner,
                            uint8_t* key, uint32_t* val, unsigned int* hist) {
   __shared__ unsigned int s_hist[kNumClasses];
@@ -39,20 +39,6 @@ __global__ void k_classify(uint32_t n, const uint64_t* off64, const uint8_t* own
     atomicAdd(hist + threadIdx.x, s_hist[threadIdx.x]);
 }
 
-// bad |= 1: weight outside int32;  bad |= 2: target out of range.
-__global__ void k_validate(uint32_t n, uint64_t m, const uint32_t* dst,
-                           const int64_t* w64, unsigned int* bad) {
-  unsigned int b = 0;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
-    const int64_t w = w64[i];
-    if (w < -2147483647LL || w > 2147483647LL) b |= 1u;
-    if (dst[i] >= n) b |= 2u;
-  }
-  b = __reduce_or_sync(0xffffffffu, b);
-  if (lane_id() == 0 && b) atomicOr(bad, b);
-}
-
 // perm[old] = new; new row lengths (exclusive-scanned into offsets next).
 __global__ void k_permute(uint32_t n, const uint32_t* inv, const uint64_t* off64,
                           uint32_t* perm, uint32_t* deg_new) {
@@ -65,37 +51,76 @@ __global__ void k_permute(uint32_t n, const uint32_t* inv, const uint64_t* off64
   if (blockIdx.x == 0 && threadIdx.x == 0) deg_new[n] = 0;
 }
 
-// Copy every row into its relabelled slot, mapping targets through perm;
-// also emit the (dst, src) pairs for the transpose.  A warp handles 32 new
-// rows and expands their edges as one flat coalesced stream (warp_expand),
-// so short and long rows cost the same per edge.
+// Edge relabelling, pipelined with the chunked upload (egs_solver.cu
+// build_arena): old rows [r0, r1) whose targets have arrived are copied to
+// their relabelled slots, targets mapped through perm, with the (dst, src)
+// pairs of the transpose; targets out of range set bit 2 of *bad.  A warp
+// handles 32 rows and expands their edges as one flat coalesced stream
+// (warp_expand), so short and long rows cost the same per edge.
 __global__ void __launch_bounds__(256)
-    k_relabel_edges(uint32_t n, const uint32_t* inv, const uint64_t* off64,
-                    const uint32_t* dst, const int64_t* w64, const uint32_t* perm,
-                    const uint32_t* off_new, int2* edge, uint32_t* ckey,
-                    uint32_t* cval) {
+    k_relabel_targets(uint32_t n, uint32_t r0, uint32_t r1, const uint64_t* off64,
+                      const uint32_t* dst, const uint32_t* perm, const uint32_t* off_new,
+                      int2* edge, uint32_t* ckey, uint32_t* cval, unsigned int* bad) {
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  for (uint32_t r0 = gw * 32; r0 < n; r0 += nwarps * 32) {
-    const uint32_t r = r0 + lane_id();
-    uint32_t b = 0, e = 0, delta = 0;
-    if (r < n) {
-      const uint32_t o = inv[r];
+  int* ex = reinterpret_cast<int*>(edge);
+  unsigned int flag = 0;
+  for (uint32_t o0 = r0 + gw * 32; o0 < r1; o0 += nwarps * 32) {
+    const uint32_t o = o0 + lane_id();
+    uint32_t b = 0, e = 0, delta = 0, rn = 0;
+    if (o < r1) {
       b = (uint32_t)off64[o];
       e = (uint32_t)off64[o + 1];
-      delta = off_new[r] - b;
+      rn = perm[o];
+      delta = off_new[rn] - b;
+    }
+    warp_expand(b, e, [&](bool valid, uint32_t idx, uint32_t owner_lane) {
+      const uint32_t d = __shfl_sync(0xffffffffu, delta, owner_lane);
+      const uint32_t src = __shfl_sync(0xffffffffu, rn, owner_lane);
+      if (valid) {
+        const uint32_t pos = idx + d;
+        const uint32_t t0 = dst[idx];
+        if (t0 >= n) flag |= 2u;
+        const uint32_t t = perm[t0 < n ? t0 : 0];
+        ex[2 * (size_t)pos] = (int)t;
+        ckey[pos] = t;
+        cval[pos] = src;
+      }
+    });
+  }
+  flag = __reduce_or_sync(0xffffffffu, flag);
+  if (lane_id() == 0 && flag) atomicOr(bad, flag);
+}
+
+// ... and the weight half once the weights of rows [r0, r1) have arrived
+// (weights must fit int32: arena.hpp:13 stores int64).
+__global__ void __launch_bounds__(256)
+    k_relabel_weights(uint32_t r0, uint32_t r1, const uint64_t* off64, const int64_t* w64,
+                      const uint32_t* perm, const uint32_t* off_new, int2* edge,
+                      unsigned int* bad) {
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int* ex = reinterpret_cast<int*>(edge);
+  unsigned int flag = 0;
+  for (uint32_t o0 = r0 + gw * 32; o0 < r1; o0 += nwarps * 32) {
+    const uint32_t o = o0 + lane_id();
+    uint32_t b = 0, e = 0, delta = 0;
+    if (o < r1) {
+      b = (uint32_t)off64[o];
+      e = (uint32_t)off64[o + 1];
+      delta = off_new[perm[o]] - b;
     }
     warp_expand(b, e, [&](bool valid, uint32_t idx, uint32_t owner_lane) {
       const uint32_t d = __shfl_sync(0xffffffffu, delta, owner_lane);
       if (valid) {
-        const uint32_t pos = idx + d;
-        const uint32_t t = perm[dst[idx]];
-        edge[pos] = make_int2((int)t, (int)w64[idx]);
-        ckey[pos] = t;
-        cval[pos] = r0 + owner_lane;
+        const int64_t w = w64[idx];
+        if (w < -2147483647LL || w > 2147483647LL) flag |= 1u;
+        ex[2 * (size_t)(idx + d) + 1] = (int)w;
       }
     });
   }
+  flag = __reduce_or_sync(0xffffffffu, flag);
+  if (lane_id() == 0 && flag) atomicOr(bad, flag);
 }
 
 // CSC column offsets from the dst-sorted keys: coff[t] = first j with

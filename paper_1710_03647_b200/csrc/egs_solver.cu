@@ -24,6 +24,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "egs_build.cuh"
 #include "egs_gpu.h"
@@ -58,31 +59,52 @@ double secs_since(Clock::time_point t0) {
   return std::chrono::duration<double>(Clock::now() - t0).count();
 }
 
+// Device memory comes from the device's stream-ordered pool with an
+// unbounded release threshold: a repeated one-shot solve (egs_gpu_solve)
+// re-uses the previous call's gigabytes instead of mapping them again.
+void use_caching_pool(int device) {
+  static bool done[64] = {};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
+  done[device] = true;
+}
+
+thread_local cudaStream_t g_alloc_stream = nullptr;  // stream of the ctx being built
+
 template <class T>
 T* dalloc(size_t count) {
   void* p = nullptr;
   if (count == 0) count = 1;
-  CK(cudaMalloc(&p, count * sizeof(T)));
+  CK(cudaMallocAsync(&p, count * sizeof(T), g_alloc_stream));
   return static_cast<T*>(p);
 }
 
-// RAII for upload temporaries.
+void dfree(void* p, cudaStream_t s) {
+  if (p) cudaFreeAsync(p, s);
+}
+
+// RAII for upload temporaries (freed in stream order).
 struct DevBuf {
   void* p = nullptr;
-  ~DevBuf() {
-    if (p) cudaFree(p);
-  }
+  cudaStream_t s = nullptr;
+  ~DevBuf() { dfree(p, s); }
   template <class T>
   T* as() {
     return static_cast<T*>(p);
   }
   template <class T>
   T* alloc(size_t count) {
+    s = g_alloc_stream;
     p = dalloc<T>(count);
     return as<T>();
   }
   void release() {
-    if (p) cudaFree(p);
+    dfree(p, s);
     p = nullptr;
   }
 };
@@ -106,6 +128,8 @@ struct egs_ctx {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // arena upload
+  cudaStream_t aux_stream = nullptr;   // weight relabel, overlapping the CSC sort
   uint32_t n = 0;
   uint64_t m = 0;
   int64_t cap = 0;
@@ -155,19 +179,44 @@ struct egs_ctx {
 
 namespace {
 
+// EGS_VERBOSE=1 prints the device arena construction steps (host clock,
+// stream-synchronised) to stderr.
+struct StepTimer {
+  cudaStream_t s;
+  bool on;
+  Clock::time_point t;
+  explicit StepTimer(cudaStream_t st) : s(st), on(std::getenv("EGS_VERBOSE") != nullptr) {
+    t = Clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    if (s) cudaStreamSynchronize(s);
+    std::fprintf(stderr, "[egs] %-28s %9.3f ms\n", what, secs_since(t) * 1e3);
+    t = Clock::now();
+  }
+};
+
 void ctx_free(egs_ctx* c) {
   if (!c) return;
+  StepTimer tm(c->stream);
   if (c->device >= 0) cudaSetDevice(c->device);
   void* ptrs[] = {c->off,    c->edge,   c->coff, c->csrc,  c->perm,
                   c->f,      c->wit,    c->chg[0], c->chg[1], c->frb,
                   c->fr[0],  c->fr[1],  c->stage, c->scratch, c->ctr, c->rbm[0], c->rbm[1], c->cbm,
                   c->f64};
-  for (void* p : ptrs)
-    if (p) cudaFree(p);
+  if (c->stream) {
+    for (void* p : ptrs) dfree(p, c->stream);
+    cudaStreamSynchronize(c->stream);
+  }
+  tm.mark("free: device buffers");
   if (c->h_ctr) cudaFreeHost(c->h_ctr);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
+  tm.s = nullptr;
+  tm.mark("free: host, events, streams");
   delete c;
 }
 
@@ -188,77 +237,93 @@ const void* solve_kernel() {
   return reinterpret_cast<const void*>(&egs::k_solve<V>);
 }
 
-// EGS_VERBOSE=1 prints the device arena construction steps (host clock,
-// stream-synchronised) to stderr.
-struct StepTimer {
-  cudaStream_t s;
-  bool on;
-  Clock::time_point t;
-  explicit StepTimer(cudaStream_t st) : s(st), on(std::getenv("EGS_VERBOSE") != nullptr) {
-    t = Clock::now();
-  }
-  void mark(const char* what) {
-    if (!on) return;
-    cudaStreamSynchronize(s);
-    std::fprintf(stderr, "[egs] %-28s %9.3f ms\n", what, secs_since(t) * 1e3);
-    t = Clock::now();
-  }
-};
-
-// Build the relabelled device arena from the reference CSR (host spans).
+// Build the relabelled device arena from the reference CSR (host spans),
+// pipelined with the upload: the copy stream brings offsets + owners, then
+// the targets and the weights in row-range chunks of ~m/16 edges; the main
+// stream classifies and relabels the vertices and relabels each target chunk
+// as it lands, then sorts the transpose while the weights are still on the
+// wire; the aux stream writes each weight chunk as it lands.  The result is
+// ready when the last weight chunk is (PCIe-bound).
 void build_arena(egs_ctx* c, const egs_arena_view* a) {
   StepTimer tm(c->stream);
   const uint32_t n = c->n;
   const uint64_t m = c->m;
-  cudaStream_t s = c->stream;
+  cudaStream_t s = c->stream, sc = c->copy_stream, sw = c->aux_stream;
   const int sms = c->num_sms;
-  DevBuf d_off64, d_dst, d_w64, d_owner, d_key, d_keys, d_val, d_inv, d_hist, d_bad,
-      d_tmp;
+  DevBuf d_off64, d_dst, d_w64, d_owner, d_key, d_keys, d_val, d_inv, d_misc, d_tmp, d_ck0,
+      d_cv0, d_ck1;
   uint64_t* off64 = d_off64.alloc<uint64_t>((size_t)n + 1);
   uint32_t* dst = d_dst.alloc<uint32_t>(m);
   int64_t* w64 = d_w64.alloc<int64_t>(m);
   uint8_t* owner = d_owner.alloc<uint8_t>(n);
-  CK(cudaMemcpyAsync(off64, a->csr_offsets, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(dst, a->csr_targets, m * 4, cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(w64, a->csr_weights, m * 8, cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(owner, a->owners, n, cudaMemcpyHostToDevice, s));
-  tm.mark("alloc + H2D");
-
-  unsigned int* hist = d_hist.alloc<unsigned int>(16);
-  unsigned int* bad = d_bad.alloc<unsigned int>(1);
-  CK(cudaMemsetAsync(hist, 0, 16 * sizeof(unsigned int), s));
-  CK(cudaMemsetAsync(bad, 0, sizeof(unsigned int), s));
+  unsigned int* misc = d_misc.alloc<unsigned int>(32);  // [0..15] hist, [16] bad
   uint8_t* key = d_key.alloc<uint8_t>(n);
   uint8_t* keys_sorted = d_keys.alloc<uint8_t>(n);
   uint32_t* val = d_val.alloc<uint32_t>(n);
   uint32_t* inv = d_inv.alloc<uint32_t>(n);
-  egs::k_classify<<<grid_for(n, sms), 256, 0, s>>>(n, off64, owner, key, val, hist);
+  uint32_t* ck0 = d_ck0.alloc<uint32_t>(m);
+  uint32_t* cv0 = d_cv0.alloc<uint32_t>(m);
+  uint32_t* ck1 = d_ck1.alloc<uint32_t>(m);
+  c->perm = dalloc<uint32_t>(n);
+  c->off = dalloc<uint32_t>((size_t)n + 1);
+  c->edge = dalloc<int2>(m + 2);  // +2: 16-byte rounding of TMA spans
+  c->csrc = dalloc<uint32_t>(m);
+  c->coff = dalloc<uint32_t>((size_t)n + 1);
+  CK(cudaMemsetAsync(misc, 0, 32 * sizeof(unsigned int), s));
+  tm.mark("pool allocations");
+  cudaEvent_t e_alloc, e_vert, e_perm, e_tail;
+  CK(cudaEventCreateWithFlags(&e_alloc, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&e_vert, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&e_perm, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&e_tail, cudaEventDisableTiming));
+  CK(cudaEventRecord(e_alloc, s));
+  CK(cudaStreamWaitEvent(sc, e_alloc, 0));
+  CK(cudaStreamWaitEvent(sw, e_alloc, 0));
+
+  // row-range chunks of ~m/16 edges (host offsets are at hand)
+  constexpr int kChunks = 16;
+  std::vector<uint32_t> rows{0};
+  for (int k = 1; k < kChunks; ++k) {
+    const uint64_t target = m * (uint64_t)k / kChunks;
+    const uint64_t* it = std::lower_bound(a->csr_offsets, a->csr_offsets + n + 1, target);
+    const uint32_t r = (uint32_t)std::min<uint64_t>(n, it - a->csr_offsets);
+    if (r > rows.back()) rows.push_back(r);
+  }
+  if (rows.back() < n) rows.push_back(n);
+  const int nch = (int)rows.size() - 1;
+  std::vector<cudaEvent_t> ex(nch), ew(nch);
+  for (int k = 0; k < nch; ++k) {
+    CK(cudaEventCreateWithFlags(&ex[k], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ew[k], cudaEventDisableTiming));
+  }
+  auto span_of = [&](int k) {
+    return std::make_pair(a->csr_offsets[rows[k]], a->csr_offsets[rows[k + 1]]);
+  };
+
+  // upload: vertices, then targets, then weights
+  CK(cudaMemcpyAsync(off64, a->csr_offsets, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice, sc));
+  CK(cudaMemcpyAsync(owner, a->owners, n, cudaMemcpyHostToDevice, sc));
+  CK(cudaEventRecord(e_vert, sc));
+  for (int k = 0; k < nch; ++k) {
+    const auto [e0, e1] = span_of(k);
+    CK(cudaMemcpyAsync(dst + e0, a->csr_targets + e0, (e1 - e0) * 4, cudaMemcpyHostToDevice, sc));
+    CK(cudaEventRecord(ex[k], sc));
+  }
+  for (int k = 0; k < nch; ++k) {
+    const auto [e0, e1] = span_of(k);
+    CK(cudaMemcpyAsync(w64 + e0, a->csr_weights + e0, (e1 - e0) * 8, cudaMemcpyHostToDevice, sc));
+    CK(cudaEventRecord(ew[k], sc));
+  }
+
+  // vertices: class keys, stable partition by class, relabelled offsets
+  CK(cudaStreamWaitEvent(s, e_vert, 0));
+  egs::k_classify<<<grid_for(n, sms), 256, 0, s>>>(n, off64, owner, key, val, misc);
   CK(cudaGetLastError());
-  egs::k_validate<<<grid_for(m, sms), 256, 0, s>>>(n, m, dst, w64, bad);
-  CK(cudaGetLastError());
-  unsigned int h_hist[16] = {0}, h_bad = 0;
-  CK(cudaMemcpyAsync(h_hist, hist, sizeof(h_hist), cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(&h_bad, bad, sizeof(h_bad), cudaMemcpyDeviceToHost, s));
-  // stable partition of the vertices by class (radix sort on 3 key bits)
   size_t tmp_bytes = 0;
   CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, keys_sorted, val, inv, n, 0, 3, s));
   void* tmp = d_tmp.alloc<uint8_t>(tmp_bytes);
   CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, keys_sorted, val, inv, n, 0, 3, s));
   d_tmp.release();
-  CK(cudaStreamSynchronize(s));
-  if (h_bad & 1u)
-    throw Fail(EGS_ERR_UNSUPPORTED, "edge weight outside int32 on the device path");
-  if (h_bad & 2u) throw Fail(EGS_ERR_INVALID_CONFIG, "edge target out of range");
-  c->rb[0] = 0;
-  for (int k = 0; k < egs::kNumClasses; ++k) c->rb[k + 1] = c->rb[k] + h_hist[k];
-  d_key.release();
-  d_keys.release();
-  d_val.release();
-  tm.mark("classify + vertex sort");
-
-  // relabelled offsets
-  c->perm = dalloc<uint32_t>(n);
-  c->off = dalloc<uint32_t>((size_t)n + 1);
   egs::k_permute<<<grid_for(n, sms), 256, 0, s>>>(n, inv, off64, c->perm, c->off);
   CK(cudaGetLastError());
   tmp_bytes = 0;
@@ -266,36 +331,63 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   tmp = d_tmp.alloc<uint8_t>(tmp_bytes);
   CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, c->off, c->off, (int64_t)n + 1, s));
   d_tmp.release();
+  CK(cudaEventRecord(e_perm, s));
+  tm.mark("vertices (classify, sort, offsets)");
 
-  // relabelled edge records + (dst, src) pairs of the transpose
-  c->edge = dalloc<int2>(m + 2);  // +2: 16-byte rounding of TMA spans
-  DevBuf d_ck0, d_cv0, d_ck1;
-  uint32_t* ck0 = d_ck0.alloc<uint32_t>(m);
-  uint32_t* cv0 = d_cv0.alloc<uint32_t>(m);
-  egs::k_relabel_edges<<<grid_for((uint64_t)n, sms), 256, 0, s>>>(
-      n, inv, off64, dst, w64, c->perm, c->off, c->edge, ck0, cv0);
-  CK(cudaGetLastError());
-  tm.mark("offsets + edge relabel");
-  CK(cudaStreamSynchronize(s));
-  d_off64.release();
-  d_dst.release();
-  d_w64.release();
-  d_owner.release();
-  d_inv.release();
+  // targets as they land (main stream), weights as they land (aux stream)
+  CK(cudaStreamWaitEvent(sw, e_perm, 0));
+  for (int k = 0; k < nch; ++k) {
+    CK(cudaStreamWaitEvent(s, ex[k], 0));
+    egs::k_relabel_targets<<<grid_for((uint64_t)(rows[k + 1] - rows[k]) * 4, sms), 256, 0, s>>>(
+        n, rows[k], rows[k + 1], off64, dst, c->perm, c->off, c->edge, ck0, cv0, misc + 16);
+    CK(cudaGetLastError());
+    CK(cudaStreamWaitEvent(sw, ew[k], 0));
+    egs::k_relabel_weights<<<grid_for((uint64_t)(rows[k + 1] - rows[k]) * 4, sms), 256, 0, sw>>>(
+        rows[k], rows[k + 1], off64, w64, c->perm, c->off, c->edge, misc + 16);
+    CK(cudaGetLastError());
+  }
+  tm.mark("upload + relabel targets");
 
-  // CSC: sort the pairs by dst; sources in a column come out in row order
-  uint32_t* ck1 = d_ck1.alloc<uint32_t>(m);
-  c->csrc = dalloc<uint32_t>(m);
+  // transpose: sort the (dst, src) pairs by dst while the weights stream in
   tmp_bytes = 0;
   const int kb = bits_for(n);
   CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, ck0, ck1, cv0, c->csrc, m, 0, kb, s));
   tmp = d_tmp.alloc<uint8_t>(tmp_bytes);
   CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, ck0, ck1, cv0, c->csrc, m, 0, kb, s));
-  c->coff = dalloc<uint32_t>((size_t)n + 1);
   egs::k_col_offsets<<<grid_for(m + 1, sms), 256, 0, s>>>(n, m, ck1, c->coff);
   CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(s));
   tm.mark("CSC sort + offsets");
+  CK(cudaEventRecord(e_tail, sw));
+  CK(cudaStreamWaitEvent(s, e_tail, 0));
+  unsigned int h_misc[32] = {0};
+  CK(cudaMemcpyAsync(h_misc, misc, sizeof(h_misc), cudaMemcpyDeviceToHost, s));
+  // temporaries go back to the pool in stream order
+  d_off64.release();
+  d_dst.release();
+  d_w64.release();
+  d_owner.release();
+  d_key.release();
+  d_keys.release();
+  d_val.release();
+  d_inv.release();
+  d_ck0.release();
+  d_cv0.release();
+  d_ck1.release();
+  d_tmp.release();
+  d_misc.release();
+  CK(cudaStreamSynchronize(s));
+  tm.mark("weights + join");
+  for (auto e : ex) cudaEventDestroy(e);
+  for (auto e : ew) cudaEventDestroy(e);
+  cudaEventDestroy(e_alloc);
+  cudaEventDestroy(e_vert);
+  cudaEventDestroy(e_perm);
+  cudaEventDestroy(e_tail);
+  const unsigned int bad = h_misc[16];
+  if (bad & 1u) throw Fail(EGS_ERR_UNSUPPORTED, "edge weight outside int32 on the device path");
+  if (bad & 2u) throw Fail(EGS_ERR_INVALID_CONFIG, "edge target out of range");
+  c->rb[0] = 0;
+  for (int k = 0; k < egs::kNumClasses; ++k) c->rb[k + 1] = c->rb[k] + h_misc[k];
 }
 
 egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_stats* st,
@@ -323,7 +415,12 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     int coop = 0;
     CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->device));
     if (!coop) throw Fail(EGS_ERR_CUDA, "device does not support cooperative launch");
+    StepTimer tm0(nullptr);
+    use_caching_pool(c->device);
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
+    g_alloc_stream = c->stream;
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
     c->n = a->num_vertices;
     c->m = a->num_edges;
@@ -336,6 +433,7 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     const size_t words = ((size_t)n + 31) / 32;
 
     CK(cudaMallocHost(&c->h_ctr, egs::kNumCounters * sizeof(unsigned long long)));
+    tm0.mark("create: streams, events, pinned");
     c->ctr = dalloc<unsigned long long>(egs::kNumCounters);
     c->scratch = dalloc<egs::Scratch>(1);
     c->rank = rank;
@@ -355,6 +453,8 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     c->fr[1] = dalloc<uint32_t>(n);
     c->stage = dalloc<uint8_t>((size_t)std::max<uint32_t>(c->n_pad, 1) * vsz);
     c->f64 = dalloc<int64_t>(n);
+    tm0.s = c->stream;
+    tm0.mark("create: state buffers");
     if (n > 0) {
       build_arena(c, a);
     } else {
@@ -411,6 +511,7 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
       }
       cudaGetLastError();  // the window is a hint; never fail on it
     }
+    tm0.mark("create: occupancy, L2 window");
     if (st) {
       st->upload_seconds = secs_since(t0);
       st->value_bits = (uint32_t)c->vbits;
@@ -581,6 +682,7 @@ void ctx_read(egs_ctx* c, int64_t* out) {
 
 int ctx_epm(egs_ctx* c, const int64_t* f) {
   CK(cudaSetDevice(c->device));
+  g_alloc_stream = c->stream;
   if (c->n == 0) return 1;
   cudaStream_t s = c->stream;
   DevBuf d_in, d_misc;
