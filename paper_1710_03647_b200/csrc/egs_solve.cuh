@@ -492,13 +492,17 @@ __device__ __forceinline__ void tma_init_barriers() {
   __syncthreads();
 }
 
-template <class V>
-__device__ __noinline__ void dense_light_p1(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
-                                            uint32_t* chg, unsigned int* sum_dst) {
-  constexpr V TOP = Top<V>::v;
+// The TMA tile pipeline of one warp over the aligned 32-vertex words of
+// [lo, hi): `need(v, aux)` says whether vertex v's row must be read (and
+// fills a per-lane value carried to the row step), `row(v, rec, len, b, aux)`
+// processes a row held in shared memory, `fallback(v, aux)` a row whose tile
+// span does not fit a stage (direct loads).  Both return "raised"; raised
+// vertices are published in `chg` with one atomicOr per word.
+template <class V, class Need, class Row, class Fallback>
+__device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
+                                          uint32_t* chg, Local& L, Need need, Row row,
+                                          Fallback fallback) {
   extern __shared__ __align__(128) int2 dsm[];
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
-  Local L;
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   int2* stage_base = dsm + (size_t)warp * kStages * kStageRecs;
   uint64_t* s_bar = g_tma_bar[warp];
@@ -507,22 +511,22 @@ __device__ __noinline__ void dense_light_p1(const SolveParams<V>& p, uint32_t lo
   const uint32_t wfirst = (lo >> 5) + blockIdx.x * kWarps + warp;
 
   struct Tile {
-    V old;
+    V aux;
     uint32_t b, e, base;
-    bool work, any, staged;
+    bool in, work, any, staged;
   };
-  // Load the tile's vertex state and, if any row needs a lift, start the
-  // bulk copy of its edge span into stage `s`.
+  // Load the tile's vertex state and, if any row is needed, start the bulk
+  // copy of the tile's edge span into stage `s`.
   auto prepare = [&](uint32_t w, uint32_t s, Tile& t) {
     const uint32_t v = (w << 5) + lane;
-    const bool in = w < w1 && v >= lo && v < hi;
-    t.old = in ? ldcg(p.f + v) : TOP;
-    t.work = in && t.old != TOP;
+    t.in = w < w1 && v >= lo && v < hi;
+    t.aux = V(0);
+    t.work = t.in && need(v, t.aux);
     t.any = __any_sync(0xffffffffu, t.work);
     t.staged = false;
     if (!t.any) return;
-    t.b = in ? __ldg(p.g.off + v) : 0u;
-    t.e = in ? __ldg(p.g.off + v + 1) : 0u;
+    t.b = t.in ? __ldg(p.g.off + v) : 0u;
+    t.e = t.in ? __ldg(p.g.off + v + 1) : 0u;
     const uint32_t first = max(w << 5, lo), last = min((w << 5) + 32, hi);
     const uint32_t span_lo = __shfl_sync(0xffffffffu, t.b, first - (w << 5));
     const uint32_t span_hi = __shfl_sync(0xffffffffu, t.e, last - 1 - (w << 5));
@@ -539,48 +543,16 @@ __device__ __noinline__ void dense_light_p1(const SolveParams<V>& p, uint32_t lo
     }
   };
   auto compute = [&](uint32_t w, uint32_t s, const Tile& t, uint32_t& parity) {
+    if (t.in && !t.work) ++L.visits;  // e.g. a top vertex: one load, no lift
     if (!t.any) return;
+    const uint32_t v = (w << 5) + lane;
     bool ch = false;
     if (t.staged) {
       mbar_wait(&s_bar[s], (parity >> s) & 1u);
       parity ^= 1u << s;
-      if (t.work) {
-        ++L.visits;
-        ++L.apps;
-        const uint32_t len = t.e - t.b;
-        L.edges += len;
-        const int2* row = stage_base + s * kStageRecs + (t.b - t.base);
-        const uint32_t rot = lane % len;  // light rows are non-empty
-        V acc = 0;
-        for (uint32_t k0 = 0; k0 < len; k0 += kChunk) {
-          int2 r[kChunk];
-#pragma unroll
-          for (int k = 0; k < kChunk; ++k) {
-            uint32_t j = min(k0 + k, len - 1) + rot;  // clamp (duplicate), rotate banks
-            j = j >= len ? j - len : j;
-            r[k] = row[j];
-          }
-          V c[kChunk];
-#pragma unroll
-          for (int k = 0; k < kChunk; ++k) c[k] = gather(p.f + r[k].x);
-#pragma unroll
-          for (int k = 0; k < kChunk; ++k) {
-            const V x = ominus_cap<V>(c[k], r[k].y, p.g.cap);
-            acc = x > acc ? x : acc;
-          }
-          if (acc == TOP) break;
-        }
-        if (acc > t.old) {
-          stcg(p.stage + ((w << 5) + lane), acc);
-          ++L.lifts;
-          ch = true;
-        }
-      } else if ((w << 5) + lane >= lo && (w << 5) + lane < hi) {
-        ++L.visits;  // a top vertex: one load, no lift
-      }
-    } else {
-      const uint32_t v = (w << 5) + lane;
-      if (v >= lo && v < hi) ch = lift_thread<V, false>(p, v, L);
+      if (t.work) ch = row(v, stage_base + s * kStageRecs + (t.b - t.base), t.e - t.b, t.b, t.aux);
+    } else if (t.work) {
+      ch = fallback(v, t.aux);
     }
     const uint32_t m = __ballot_sync(0xffffffffu, ch);
     if (m && lane == 0) atomicOr(chg + w, m);
@@ -600,6 +572,55 @@ __device__ __noinline__ void dense_light_p1(const SolveParams<V>& p, uint32_t lo
   }
   __syncwarp();
   if (lane == 0) g_tma_parity[warp] = parity;
+}
+
+// Player-1 light rows of a dense round through the tile pipeline: tiles of
+// all-top vertices are skipped without a copy; each lane lifts its own row
+// from shared memory (reads rotated by lane so a half-warp hits distinct
+// banks), 8 gathers in flight.
+template <class V>
+__device__ __noinline__ void dense_light_p1(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
+                                            uint32_t* chg, unsigned int* sum_dst) {
+  constexpr V TOP = Top<V>::v;
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  Local L;
+  auto need = [&](uint32_t v, V& old) {
+    old = ldcg(p.f + v);
+    return old != TOP;
+  };
+  auto row = [&](uint32_t v, const int2* rec, uint32_t len, uint32_t, V old) {
+    ++L.visits;
+    ++L.apps;
+    L.edges += len;
+    const uint32_t rot = lane_id() % len;  // light rows are non-empty
+    V acc = 0;
+    for (uint32_t k0 = 0; k0 < len; k0 += kChunk) {
+      int2 r[kChunk];
+#pragma unroll
+      for (int k = 0; k < kChunk; ++k) {
+        uint32_t j = min(k0 + k, len - 1) + rot;  // clamp (duplicate), rotate banks
+        j = j >= len ? j - len : j;
+        r[k] = rec[j];
+      }
+      V c[kChunk];
+#pragma unroll
+      for (int k = 0; k < kChunk; ++k) c[k] = gather(p.f + r[k].x);
+#pragma unroll
+      for (int k = 0; k < kChunk; ++k) {
+        const V x = ominus_cap<V>(c[k], r[k].y, p.g.cap);
+        acc = x > acc ? x : acc;
+      }
+      if (acc == TOP) break;
+    }
+    if (acc > old) {
+      stcg(p.stage + v, acc);
+      ++L.lifts;
+      return true;
+    }
+    return false;
+  };
+  auto fallback = [&](uint32_t v, V) { return lift_thread<V, false>(p, v, L); };
+  tma_tiles<V>(p, lo, hi, chg, L, need, row, fallback);
   block_flush(L, p.ctr, sum_dst, s_cnt);
 }
 
@@ -879,49 +900,69 @@ __device__ __forceinline__ void round1_finish(const SolveParams<V>& p, uint32_t 
   if (val > V(0)) stcg(p.stage + v, val);
 }
 
-// light rows: one thread per row, aligned 32-vertex words per warp
+// light rows: one thread per row over the TMA tile pipeline (the weight scan
+// streams the whole edge array once)
 template <class V>
 __device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
                                           uint32_t* chg, unsigned int* sum_dst) {
   __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
   const Graph& g = p.g;
   Local L;
-  const uint32_t lane = lane_id();
-  const uint32_t nwarps = gridDim.x * kWarps;
-  const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5;
-  for (uint32_t w = (lo >> 5) + gw; w < (hi + 31) >> 5; w += nwarps) {
-    const uint32_t v = (w << 5) + lane;
-    V val = 0;
-    if (v >= lo && v < hi) {
-      const bool p0 = v < g.rb[kP1L];
-      const uint32_t b = __ldg(g.off + v), e = __ldg(g.off + v + 1);
-      int minw = INT32_MAX, maxw = INT32_MIN;
-      uint32_t imax = b;
-      for (uint32_t i = b; i < e; i += kChunk) {
-        int wt[kChunk];
-#pragma unroll
-        for (int k = 0; k < kChunk; ++k) wt[k] = __ldcs(&g.edge[min(i + k, e - 1)].y);
-#pragma unroll
-        for (int k = 0; k < kChunk; ++k) {
-          minw = min(minw, wt[k]);
-          if (wt[k] > maxw) {
-            maxw = wt[k];
-            imax = min(i + k, e - 1);
-          }
-        }
-        if (p0 && maxw >= 0) break;  // a satisfied move: delta = 0
-      }
-      round1_finish<V>(p, v, p0, minw, maxw, imax, val);
-      ++L.visits;
-      ++L.apps;
-      L.edges += e - b;
+  auto need = [](uint32_t, V&) { return true; };
+  auto finish = [&](uint32_t v, bool p0, int minw, int maxw, int2 wrec, uint32_t len) {
+    const V val = ominus_cap<V>(V(0), p0 ? maxw : minw, g.cap);
+    if (p0) p.wit[v] = wrec;
+    ++L.visits;
+    ++L.apps;
+    L.edges += len;
+    if (val > V(0)) {
+      stcg(p.stage + v, val);
+      ++L.lifts;
+      return true;
     }
-    const bool raised = val > V(0);
-    const uint32_t m = __ballot_sync(0xffffffffu, raised);
-    if (m && lane == 0) atomicOr(chg + w, m);
-    L.phase_count += raised;
-    L.lifts += raised;
-  }
+    return false;
+  };
+  auto row = [&](uint32_t v, const int2* rec, uint32_t len, uint32_t, V) {
+    const bool p0 = v < g.rb[kP1L];
+    const uint32_t rot = lane_id() % len;
+    int minw = INT32_MAX, maxw = INT32_MIN;
+    uint32_t jmax = 0;
+    for (uint32_t k0 = 0; k0 < len; k0 += kChunk) {
+#pragma unroll
+      for (int k = 0; k < kChunk; ++k) {
+        uint32_t j = min(k0 + k, len - 1) + rot;
+        j = j >= len ? j - len : j;
+        const int w = rec[j].y;
+        minw = min(minw, w);
+        if (w > maxw) {
+          maxw = w;
+          jmax = j;
+        }
+      }
+    }
+    return finish(v, p0, minw, maxw, rec[jmax], len);
+  };
+  auto fallback = [&](uint32_t v, V) {
+    const bool p0 = v < g.rb[kP1L];
+    const uint32_t b = __ldg(g.off + v), e = __ldg(g.off + v + 1);
+    int minw = INT32_MAX, maxw = INT32_MIN;
+    uint32_t imax = b;
+    for (uint32_t i = b; i < e; i += kChunk) {
+      int wt[kChunk];
+#pragma unroll
+      for (int k = 0; k < kChunk; ++k) wt[k] = __ldcs(&g.edge[min(i + k, e - 1)].y);
+#pragma unroll
+      for (int k = 0; k < kChunk; ++k) {
+        minw = min(minw, wt[k]);
+        if (wt[k] > maxw) {
+          maxw = wt[k];
+          imax = min(i + k, e - 1);
+        }
+      }
+    }
+    return finish(v, p0, minw, maxw, __ldg(g.edge + imax), e - b);
+  };
+  tma_tiles<V>(p, lo, hi, chg, L, need, row, fallback);
   block_flush(L, p.ctr, sum_dst, s_cnt);
 }
 
