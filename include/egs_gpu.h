@@ -138,6 +138,11 @@ int egs_ctx_read_measure(egs_ctx* ctx, int64_t* f_out);
 /* Device EPM verifier (measure_ops.cpp:33-41): 1 if f (host, n) is a progress
  * measure of the context's arena, 0 if not, negative on error. */
 int egs_ctx_is_progress_measure(egs_ctx* ctx, const int64_t* f);
+/* Fixpoint check: 1 if delta(f) == f at every vertex under the lift with the
+ * credit cap (measure_ops.hpp:32-52) -- what the least progress measure must
+ * satisfy exactly; 0 if not, negative on error.  Size-independent parity
+ * check for arenas the CPU reference cannot finish. */
+int egs_ctx_is_fixpoint(egs_ctx* ctx, const int64_t* f);
 void egs_ctx_destroy(egs_ctx* ctx);
 
 /* ---------------------------------------------------------------------

@@ -159,6 +159,8 @@ lib.egs_ctx_read_measure.argtypes = [_P, _P]
 lib.egs_ctx_read_measure.restype = C.c_int
 lib.egs_ctx_is_progress_measure.argtypes = [_P, _P]
 lib.egs_ctx_is_progress_measure.restype = C.c_int
+lib.egs_ctx_is_fixpoint.argtypes = [_P, _P]
+lib.egs_ctx_is_fixpoint.restype = C.c_int
 lib.egs_ctx_destroy.argtypes = [_P]
 lib.egs_ctx_destroy.restype = None
 lib.egs_write_solution.argtypes = [C.POINTER(ArenaView), _P, _P, C.c_size_t]
@@ -467,6 +469,14 @@ class DeviceSolver:
     def is_progress_measure(self, f: np.ndarray) -> bool:
         f = np.ascontiguousarray(f, dtype=np.int64)
         r = lib.egs_ctx_is_progress_measure(self._ctx, f.ctypes.data)
+        if r < 0:
+            _check(-r)
+        return bool(r)
+
+    def is_fixpoint(self, f: np.ndarray) -> bool:
+        """delta(f) == f everywhere (egs_ctx_is_fixpoint)."""
+        f = np.ascontiguousarray(f, dtype=np.int64)
+        r = lib.egs_ctx_is_fixpoint(self._ctx, f.ctypes.data)
         if r < 0:
             _check(-r)
         return bool(r)

@@ -201,4 +201,37 @@ __global__ void __launch_bounds__(256)
   if (nb) atomicAdd(bad, nb);
 }
 
+// Fixpoint check of a raw int64 measure (relabelled ids): delta(f)(v) ==
+// f(v) for every vertex, with the lift's cap (`> credit_cap -> top`,
+// measure_ops.hpp:51).  The least progress measure is the least fixpoint of
+// this lift, so a solve result must pass it exactly; *bad counts vertices
+// where the lift differs from f.  One warp per vertex.
+__global__ void __launch_bounds__(256)
+    k_fixpoint(Graph g, const int64_t* f, unsigned long long* bad) {
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  unsigned long long nb = 0;
+  for (uint32_t v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < g.n; v += nwarps) {
+    const bool p0 = v < g.rb[kP1L];
+    const uint32_t b = g.off[v], e = g.off[v + 1];
+    int64_t acc = p0 ? INT64_MAX : 0;
+    for (uint32_t i = b + lane_id(); i < e; i += 32) {
+      const int2 r = g.edge[i];
+      const int64_t ft = f[r.x];
+      int64_t c = ft == INT64_MAX ? INT64_MAX : ft - (int64_t)r.y;
+      if (c != INT64_MAX) {
+        c = c < 0 ? 0 : c;
+        c = c > g.cap ? INT64_MAX : c;
+      }
+      acc = p0 ? (c < acc ? c : acc) : (c > acc ? c : acc);
+    }
+#pragma unroll
+    for (int sft = 16; sft > 0; sft >>= 1) {
+      const int64_t y = __shfl_xor_sync(0xffffffffu, acc, sft);
+      acc = p0 ? (y < acc ? y : acc) : (y > acc ? y : acc);
+    }
+    if (lane_id() == 0 && acc != f[v]) ++nb;
+  }
+  if (nb) atomicAdd(bad, nb);
+}
+
 }  // namespace egs

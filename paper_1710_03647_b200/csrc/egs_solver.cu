@@ -680,6 +680,28 @@ void ctx_read(egs_ctx* c, int64_t* out) {
   CK(cudaStreamSynchronize(s));
 }
 
+int ctx_fixpoint(egs_ctx* c, const int64_t* f) {
+  CK(cudaSetDevice(c->device));
+  g_alloc_stream = c->stream;
+  if (c->n == 0) return 1;
+  cudaStream_t s = c->stream;
+  DevBuf d_in, d_misc;
+  int64_t* fin = d_in.alloc<int64_t>(c->n);
+  unsigned long long* misc = d_misc.alloc<unsigned long long>(1);
+  CK(cudaMemcpyAsync(fin, f, (size_t)c->n * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(misc, 0, sizeof(unsigned long long), s));
+  const uint32_t grid = grid_for(c->n, c->num_sms);
+  egs::k_import<<<grid, 256, 0, s>>>(c->n, fin, c->perm, c->f64);
+  egs::k_fixpoint<<<grid_for((uint64_t)c->n * 32, c->num_sms), 256, 0, s>>>(c->graph(), c->f64,
+                                                                            misc);
+  CK(cudaGetLastError());
+  unsigned long long h = 0;
+  CK(cudaMemcpyAsync(&h, misc, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  c->solved = false;  // f64 scratch reused
+  return h == 0 ? 1 : 0;
+}
+
 int ctx_epm(egs_ctx* c, const int64_t* f) {
   CK(cudaSetDevice(c->device));
   g_alloc_stream = c->stream;
@@ -901,6 +923,15 @@ int egs_ctx_is_progress_measure(egs_ctx* ctx, const int64_t* f) {
   int rc = guarded([&] {
     if (!ctx) throw Fail(EGS_ERR_INVALID_CONFIG, "null context");
     r = ctx_epm(ctx, f);
+  });
+  return rc == EGS_OK ? r : -rc;
+}
+
+int egs_ctx_is_fixpoint(egs_ctx* ctx, const int64_t* f) {
+  int r = 0;
+  int rc = guarded([&] {
+    if (!ctx) throw Fail(EGS_ERR_INVALID_CONFIG, "null context");
+    r = ctx_fixpoint(ctx, f);
   });
   return rc == EGS_OK ? r : -rc;
 }

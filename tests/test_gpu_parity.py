@@ -195,3 +195,47 @@ def test_empty_and_single_vertex(egs):
     assert rep.measure.shape == (0,)
     a = egs.GameArena.build(1, [(0, 0, -7)], [1])
     assert _solve(egs, a).measure.tolist() == [INT64_MAX]
+
+
+def test_fixpoint_check_small(egs, oracle):
+    """The device fixpoint check accepts the reference's least measure and
+    rejects perturbations of it (it backs the full-size tests below)."""
+    for seed in range(40):
+        n, edges, owners = random_arena(3000 + seed, max_n=30, max_deg=5)
+        a = egs.GameArena.build(n, edges, owners)
+        g = oracle.build(n, edges, owners)
+        want, _ = oracle.solve_seq(g)
+        with egs.DeviceSolver(a) as ds:
+            assert ds.is_fixpoint(want)
+            fin = np.nonzero((want != INT64_MAX) & (want > 0))[0]
+            if fin.size:
+                bad = want.copy()
+                bad[fin[0]] -= 1
+                assert not ds.is_fixpoint(bad)
+
+
+FULL = [("C4", ("fixed", (16_000_000, 16, 100))), ("C3", ("rmat", (22, 16, 100))),
+        ("C2", ("fixed", (1_000_000, 8, 1000))), ("C5", ("fixed", (1_000_000, 8, 100_000)))]
+
+
+@pytest.mark.parametrize("name,spec", FULL, ids=[n for n, _ in FULL])
+def test_full_size_configs_properties(egs, name, spec):
+    """Full BASELINE configs, where the CPU reference cannot finish (C4 ~4
+    days projected): the result is a fixpoint of the capped lift and a
+    progress measure (device checks), and every schedule -- auto, dense,
+    sparse, a late certificate -- gives the identical measure."""
+    kind, args = spec
+    a = getattr(egs.GameArena, kind)(*args, 1)
+    base = None
+    for opts in [dict(), dict(mode="dense"), dict(mode="sparse"), dict(cert_interval=7)]:
+        with egs.DeviceSolver(a, egs.SolverOptions(**opts)) as ds:
+            ds.solve()
+            f = ds.read_measure()
+            if base is None:
+                base = f
+                assert ds.is_fixpoint(f)
+                assert ds.is_progress_measure(f)
+                tops = int((f == INT64_MAX).sum())
+                assert 0 < tops < a.num_vertices
+            else:
+                assert np.array_equal(f, base), opts
