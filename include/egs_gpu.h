@@ -143,6 +143,13 @@ int egs_ctx_is_progress_measure(egs_ctx* ctx, const int64_t* f);
  * satisfy exactly; 0 if not, negative on error.  Size-independent parity
  * check for arenas the CPU reference cannot finish. */
 int egs_ctx_is_fixpoint(egs_ctx* ctx, const int64_t* f);
+/* write_solution(make_solution(arena, report)) (io.cpp:178-210) of the
+ * context's solved measure, computed on the device: first-witness strategy
+ * (extract_strategy, measure_ops.cpp:56-80), line lengths, scan, format.
+ * Returns the text length (bytes) and copies min(cap, length) bytes into buf
+ * when buf != NULL; negative error code otherwise (EGS_ERR_INTERNAL = the
+ * reference's NoWitnessError).  Byte-identical to egs_write_solution. */
+int64_t egs_ctx_write_solution(egs_ctx* ctx, char* buf, size_t cap);
 void egs_ctx_destroy(egs_ctx* ctx);
 
 /* ---------------------------------------------------------------------

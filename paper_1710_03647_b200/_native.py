@@ -159,6 +159,8 @@ lib.egs_ctx_read_measure.argtypes = [_P, _P]
 lib.egs_ctx_read_measure.restype = C.c_int
 lib.egs_ctx_is_progress_measure.argtypes = [_P, _P]
 lib.egs_ctx_is_progress_measure.restype = C.c_int
+lib.egs_ctx_write_solution.argtypes = [_P, _P, C.c_size_t]
+lib.egs_ctx_write_solution.restype = C.c_int64
 lib.egs_ctx_is_fixpoint.argtypes = [_P, _P]
 lib.egs_ctx_is_fixpoint.restype = C.c_int
 lib.egs_ctx_destroy.argtypes = [_P]
@@ -472,6 +474,17 @@ class DeviceSolver:
         if r < 0:
             _check(-r)
         return bool(r)
+
+    def write_solution(self) -> str:
+        """write_solution(make_solution(...)) of the solved measure, on the device."""
+        n = lib.egs_ctx_write_solution(self._ctx, None, 0)
+        if n < 0:
+            _check(int(-n))
+        buf = C.create_string_buffer(max(int(n), 1))
+        r = lib.egs_ctx_write_solution(self._ctx, buf, n)
+        if r < 0:
+            _check(int(-r))
+        return buf.raw[:n].decode()
 
     def is_fixpoint(self, f: np.ndarray) -> bool:
         """delta(f) == f everywhere (egs_ctx_is_fixpoint)."""

@@ -234,4 +234,101 @@ __global__ void __launch_bounds__(256)
   if (nb) atomicAdd(bad, nb);
 }
 
+// ---------------------------------------------- solution output ----
+// write_solution(make_solution(...)) (io.cpp:178-210) on the device.  The
+// strategy of a finite player-0 vertex is the FIRST successor in row order
+// with f(v) >= f(t) ⊖ w (extract_strategy, measure_ops.cpp:56-80); rows keep
+// their input order through the relabelling, so the first witness of the
+// relabelled row is the reference's.  strat[old id] = old target or ~0u.
+constexpr uint32_t kNoTarget = 0xFFFFFFFFu;
+
+template <class V>
+__device__ __forceinline__ int64_t raw_of(V x) {
+  return x == Top<V>::v ? INT64_MAX : static_cast<int64_t>(x);
+}
+
+template <class V>
+__global__ void __launch_bounds__(256)
+    k_strategy(Graph g, const V* f, const uint32_t* inv, uint32_t* strat, int* err) {
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < g.n; v += nwarps) {
+    const int64_t fv = raw_of<V>(f[v]);
+    uint32_t target = kNoTarget;
+    if (v < g.rb[kP1L] && fv != INT64_MAX) {
+      const uint32_t b = g.off[v], e = g.off[v + 1];
+      for (uint32_t i0 = b; i0 < e; i0 += 32) {
+        const uint32_t i = i0 + lane_id();
+        bool sat = false;
+        int2 r = make_int2(0, 0);
+        if (i < e) {
+          r = g.edge[i];
+          sat = fv >= ominus_raw(raw_of<V>(f[r.x]), r.y, err);
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, sat);
+        if (m) {
+          const int src = __ffs(m) - 1;
+          target = inv[__shfl_sync(0xffffffffu, r.x, src)];
+          break;
+        }
+      }
+      if (target == kNoTarget && lane_id() == 0) atomicExch(err, 2);  // NoWitnessError
+    }
+    if (lane_id() == 0) strat[inv[v]] = target;
+  }
+}
+
+__device__ __forceinline__ uint32_t dec_digits(uint64_t x) {
+  uint32_t d = 1;
+  while (x >= 10) {
+    x /= 10;
+    ++d;
+  }
+  return d;
+}
+__device__ __forceinline__ void dec_write(char* out, uint64_t x, uint32_t d) {
+  for (uint32_t k = d; k > 0; --k) {
+    out[k - 1] = (char)('0' + x % 10);
+    x /= 10;
+  }
+}
+
+// Line lengths "<id> <value|T>[ <target>]\n" by original id.
+template <class V>
+__global__ void k_line_len(uint32_t n, const V* f, const uint32_t* perm, const uint32_t* strat,
+                           unsigned long long* len) {
+  for (uint32_t o = blockIdx.x * blockDim.x + threadIdx.x; o < n; o += gridDim.x * blockDim.x) {
+    const V x = f[perm[o]];
+    uint64_t l = dec_digits(o) + 2 + (x == Top<V>::v ? 1 : dec_digits(x));
+    if (strat[o] != kNoTarget) l += 1 + dec_digits(strat[o]);
+    len[o] = l;
+  }
+}
+
+template <class V>
+__global__ void k_format(uint32_t n, const V* f, const uint32_t* perm, const uint32_t* strat,
+                         const unsigned long long* pos, char* text) {
+  for (uint32_t o = blockIdx.x * blockDim.x + threadIdx.x; o < n; o += gridDim.x * blockDim.x) {
+    char* p = text + pos[o];
+    uint32_t d = dec_digits(o);
+    dec_write(p, o, d);
+    p += d;
+    *p++ = ' ';
+    const V x = f[perm[o]];
+    if (x == Top<V>::v) {
+      *p++ = 'T';
+    } else {
+      d = dec_digits(x);
+      dec_write(p, x, d);
+      p += d;
+    }
+    if (strat[o] != kNoTarget) {
+      *p++ = ' ';
+      d = dec_digits(strat[o]);
+      dec_write(p, strat[o], d);
+      p += d;
+    }
+    *p = '\n';
+  }
+}
+
 }  // namespace egs

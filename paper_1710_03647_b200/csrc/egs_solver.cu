@@ -142,6 +142,7 @@ struct egs_ctx {
   uint32_t* coff = nullptr;
   uint32_t* csrc = nullptr;
   uint32_t* perm = nullptr;  // old id -> new id
+  uint32_t* inv = nullptr;   // new id -> old id
   // solver state
   void* f = nullptr;
   int2* wit = nullptr;
@@ -200,7 +201,7 @@ void ctx_free(egs_ctx* c) {
   if (!c) return;
   StepTimer tm(c->stream);
   if (c->device >= 0) cudaSetDevice(c->device);
-  void* ptrs[] = {c->off,    c->edge,   c->coff, c->csrc,  c->perm,
+  void* ptrs[] = {c->off,    c->edge,   c->coff, c->csrc,  c->perm, c->inv,
                   c->f,      c->wit,    c->chg[0], c->chg[1], c->frb,
                   c->fr[0],  c->fr[1],  c->stage, c->scratch, c->ctr, c->rbm[0], c->rbm[1], c->cbm,
                   c->f64};
@@ -250,8 +251,8 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   const uint64_t m = c->m;
   cudaStream_t s = c->stream, sc = c->copy_stream, sw = c->aux_stream;
   const int sms = c->num_sms;
-  DevBuf d_off64, d_dst, d_w64, d_owner, d_key, d_keys, d_val, d_inv, d_misc, d_tmp, d_ck0,
-      d_cv0, d_ck1;
+  DevBuf d_off64, d_dst, d_w64, d_owner, d_key, d_keys, d_val, d_misc, d_tmp, d_ck0, d_cv0,
+      d_ck1;
   uint64_t* off64 = d_off64.alloc<uint64_t>((size_t)n + 1);
   uint32_t* dst = d_dst.alloc<uint32_t>(m);
   int64_t* w64 = d_w64.alloc<int64_t>(m);
@@ -260,7 +261,8 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   uint8_t* key = d_key.alloc<uint8_t>(n);
   uint8_t* keys_sorted = d_keys.alloc<uint8_t>(n);
   uint32_t* val = d_val.alloc<uint32_t>(n);
-  uint32_t* inv = d_inv.alloc<uint32_t>(n);
+  c->inv = dalloc<uint32_t>(n);
+  uint32_t* inv = c->inv;
   uint32_t* ck0 = d_ck0.alloc<uint32_t>(m);
   uint32_t* cv0 = d_cv0.alloc<uint32_t>(m);
   uint32_t* ck1 = d_ck1.alloc<uint32_t>(m);
@@ -369,7 +371,6 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   d_key.release();
   d_keys.release();
   d_val.release();
-  d_inv.release();
   d_ck0.release();
   d_cv0.release();
   d_ck1.release();
@@ -463,6 +464,7 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
       c->edge = dalloc<int2>(1);
       c->csrc = dalloc<uint32_t>(1);
       c->perm = dalloc<uint32_t>(1);
+      c->inv = dalloc<uint32_t>(1);
     }
     c->wit = dalloc<int2>(std::max<uint32_t>(1, c->rb[egs::kP1L]));
 
@@ -680,6 +682,44 @@ void ctx_read(egs_ctx* c, int64_t* out) {
   CK(cudaStreamSynchronize(s));
 }
 
+template <class V>
+int64_t write_solution_dev(egs_ctx* c, char* buf, size_t cap) {
+  cudaStream_t s = c->stream;
+  const uint32_t n = c->n;
+  DevBuf d_strat, d_len, d_pos, d_text, d_err, d_tmp;
+  uint32_t* strat = d_strat.alloc<uint32_t>(n);
+  unsigned long long* len = d_len.alloc<unsigned long long>(n);
+  unsigned long long* pos = d_pos.alloc<unsigned long long>(n);
+  int* err = d_err.alloc<int>(1);
+  CK(cudaMemsetAsync(err, 0, sizeof(int), s));
+  const V* f = static_cast<const V*>(c->f);
+  egs::k_strategy<V><<<grid_for((uint64_t)n * 32, c->num_sms), 256, 0, s>>>(c->graph(), f,
+                                                                           c->inv, strat, err);
+  egs::k_line_len<V><<<grid_for(n, c->num_sms), 256, 0, s>>>(n, f, c->perm, strat, len);
+  CK(cudaGetLastError());
+  size_t tmp_bytes = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, len, pos, n, s));
+  void* tmp = d_tmp.alloc<uint8_t>(tmp_bytes);
+  CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, len, pos, n, s));
+  unsigned long long last[2] = {0, 0};
+  int h_err = 0;
+  CK(cudaMemcpyAsync(&last[0], pos + (n - 1), 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&last[1], len + (n - 1), 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&h_err, err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (h_err == 1) throw Fail(EGS_ERR_UNSUPPORTED, "energy subtraction out of range");
+  if (h_err == 2) throw Fail(EGS_ERR_INTERNAL, "no witness successor for a finite player-0 vertex");
+  const uint64_t total = last[0] + last[1];
+  if (buf && cap) {
+    char* text = d_text.alloc<char>(total);
+    egs::k_format<V><<<grid_for(n, c->num_sms), 256, 0, s>>>(n, f, c->perm, strat, pos, text);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(buf, text, std::min<uint64_t>(cap, total), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  return (int64_t)total;
+}
+
 int ctx_fixpoint(egs_ctx* c, const int64_t* f) {
   CK(cudaSetDevice(c->device));
   g_alloc_stream = c->stream;
@@ -698,7 +738,7 @@ int ctx_fixpoint(egs_ctx* c, const int64_t* f) {
   unsigned long long h = 0;
   CK(cudaMemcpyAsync(&h, misc, sizeof(h), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  c->solved = false;  // f64 scratch reused
+
   return h == 0 ? 1 : 0;
 }
 
@@ -720,7 +760,7 @@ int ctx_epm(egs_ctx* c, const int64_t* f) {
   unsigned long long h[2] = {0, 0};
   CK(cudaMemcpyAsync(h, misc, sizeof(h), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  c->solved = false;  // f64 scratch reused
+
   if (h[1]) throw Fail(EGS_ERR_UNSUPPORTED, "energy subtraction out of range");
   return h[0] == 0 ? 1 : 0;
 }
@@ -923,6 +963,23 @@ int egs_ctx_is_progress_measure(egs_ctx* ctx, const int64_t* f) {
   int rc = guarded([&] {
     if (!ctx) throw Fail(EGS_ERR_INVALID_CONFIG, "null context");
     r = ctx_epm(ctx, f);
+  });
+  return rc == EGS_OK ? r : -rc;
+}
+
+int64_t egs_ctx_write_solution(egs_ctx* ctx, char* buf, size_t cap) {
+  int64_t r = 0;
+  int rc = guarded([&] {
+    if (!ctx) throw Fail(EGS_ERR_INVALID_CONFIG, "null context");
+    if (!ctx->solved) throw Fail(EGS_ERR_INVALID_CONFIG, "context not solved");
+    CK(cudaSetDevice(ctx->device));
+    g_alloc_stream = ctx->stream;
+    if (ctx->n == 0) {
+      r = 0;
+      return;
+    }
+    r = ctx->vbits == 32 ? write_solution_dev<uint32_t>(ctx, buf, cap)
+                         : write_solution_dev<uint64_t>(ctx, buf, cap);
   });
   return rc == EGS_OK ? r : -rc;
 }

@@ -100,6 +100,34 @@ GOLDEN_SMALL = [
 
 
 @pytest.mark.parametrize("key,make", GOLDEN_SMALL, ids=[k for k, _ in GOLDEN_SMALL])
+def test_device_write_solution_golden(egs, golden, key, make):
+    """egs_ctx_write_solution (device strategy + formatting) reproduces the
+    reference's write_solution bytes."""
+    rec = golden[key]
+    with egs.DeviceSolver(make(egs)) as ds:
+        ds.solve()
+        sol = ds.write_solution().encode()
+    assert (len(sol), f"{fnv1a64(sol):016x}") == (rec["solution_bytes"], rec["solution_fnv"])
+
+
+def test_device_write_solution_spec_and_random(egs, golden, oracle):
+    for key, rec in golden.items():
+        if key.startswith("spec/"):
+            a = egs.GameArena.build(rec["n"], [tuple(e) for e in rec["edges"]], rec["owners"])
+            with egs.DeviceSolver(a) as ds:
+                ds.solve()
+                assert ds.write_solution() == rec["solution"], key
+    for seed in range(60):
+        n, edges, owners = random_arena(7000 + seed, max_n=40, max_deg=5)
+        a = egs.GameArena.build(n, edges, owners)
+        g = oracle.build(n, edges, owners)
+        want, _ = oracle.solve_seq(g)
+        with egs.DeviceSolver(a) as ds:
+            ds.solve()
+            assert ds.write_solution() == oracle.write_solution(g, want), seed
+
+
+@pytest.mark.parametrize("key,make", GOLDEN_SMALL, ids=[k for k, _ in GOLDEN_SMALL])
 @pytest.mark.parametrize("mode", MODES)
 def test_canonical_golden_small(egs, golden, key, make, mode):
     rec = golden[key]
@@ -237,5 +265,7 @@ def test_full_size_configs_properties(egs, name, spec):
                 assert ds.is_progress_measure(f)
                 tops = int((f == INT64_MAX).sum())
                 assert 0 < tops < a.num_vertices
+                # device output path == host output path, byte for byte
+                assert ds.write_solution() == egs.write_solution(a, f)
             else:
                 assert np.array_equal(f, base), opts
