@@ -381,15 +381,19 @@ def run_our_arm_partitioned(a):
     import paper_1710_03647_b200 as egs
     from paper_1710_03647_b200.distributed import DeviceSteps, TorchComm, solve_partitioned
 
-    rank, world = dist_setup(a.gpus, "nccl")
-    dev = env_int("LOCAL_RANK", 0)
+    # EGS_BENCH_STAGED=1: gloo with host staging and ranks sharing the visible
+    # GPUs -- only to exercise this path on a single-GPU box; never a bench value
+    staged = os.environ.get("EGS_BENCH_STAGED") == "1"
+    rank, world = dist_setup(a.gpus, "gloo" if staged else "nccl")
+    dev = env_int("LOCAL_RANK", 0) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev)
     log = (lambda s: print(f"[rank {rank}] {s}", file=sys.stderr, flush=True))
     kind, args = CONFIGS[a.config]
     arena = getattr(egs.GameArena, kind)(*args, 1, pinned=True)
     n, m = arena.num_vertices, arena.num_edges
     opts = egs.SolverOptions(device=dev)
-    comm = TorchComm(rank, world, staged=False, device=f"cuda:{dev}")
+    comm = TorchComm(rank, world, staged=staged, device=f"cuda:{dev}")
+    red_dev = "cpu" if staged else f"cuda:{dev}"
 
     def timed(fn):
         barrier(world)
@@ -414,8 +418,8 @@ def run_our_arm_partitioned(a):
             total_s += dt
             edges += rep.counters.get("edges_relaxed", 0)
             launches += rep.kernel_launches
-    total_s = max_over_ranks(total_s, world, f"cuda:{dev}")
-    edges_all = sum_over_ranks(edges, world, f"cuda:{dev}")
+    total_s = max_over_ranks(total_s, world, red_dev)
+    edges_all = sum_over_ranks(edges, world, red_dev)
     f_dev = rep.measure
     steps.close()
 
@@ -432,8 +436,8 @@ def run_our_arm_partitioned(a):
         e2e_t += dt
         e2e_edges += r.counters.get("edges_relaxed", 0)
         assert (r.measure == f_dev).all()
-    e2e_t = max_over_ranks(e2e_t, world, f"cuda:{dev}")
-    e2e_edges = sum_over_ranks(e2e_edges, world, f"cuda:{dev}")
+    e2e_t = max_over_ranks(e2e_t, world, red_dev)
+    e2e_edges = sum_over_ranks(e2e_edges, world, red_dev)
     line = {
         "metric": METRIC, "value": edges_all / total_s / 1e9, "unit": UNIT, "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_s / a.steps * 1e3,
@@ -442,7 +446,9 @@ def run_our_arm_partitioned(a):
         "dtype": "u32" if steps.value_bytes == 4 else "u64",
         "data": "synthetic (canonical splitmix64 generator, SURVEY.md Appendix B)",
         "config": {"workload": workload_name(a.config), "vertices": n, "edges": m,
-                   "parallelism": f"vertex-range partition x{world}, NCCL all-gather per step",
+                   "parallelism": f"vertex-range partition x{world}, "
+                                  + ("gloo staged (path test only)" if staged else
+                                     "NCCL all-gather per step"),
                    "l2": "inputs larger than L2; no flush"},
         "solve": {"rounds": rep.rounds, "cert_attempts": rep.cert_attempts,
                   "cert_passes": rep.cert_passes, "certified": rep.certified,
