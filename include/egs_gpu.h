@@ -117,6 +117,8 @@ typedef struct egs_gpu_stats {
   double lift_sub_seconds[5]; /* per-CTA mean time in the lift sub-phases:
                                  heavy rows, medium rows, light player-0 rows,
                                  light player-1 rows, sparse light rows */
+  double phase_detail_seconds[5]; /* device time of: commit phases, certificate
+                                     init, dense passes, sparse passes, apply */
 } egs_gpu_stats;
 
 void egs_gpu_opts_default(egs_gpu_opts* opts);

@@ -117,12 +117,14 @@ class GpuStats(C.Structure):
         + [(k, C.c_double) for k in _STAT_F64]
         + [("algo_bytes", C.c_uint64), ("lift_bytes", C.c_uint64),
            ("kernel_launches", C.c_uint64), ("value_bits", C.c_uint32),
-           ("grid_ctas", C.c_uint32), ("lift_sub_seconds", C.c_double * 5)]
+           ("grid_ctas", C.c_uint32), ("lift_sub_seconds", C.c_double * 5),
+           ("phase_detail_seconds", C.c_double * 5)]
     )
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_}
         d["lift_sub_seconds"] = list(self.lift_sub_seconds)
+        d["phase_detail_seconds"] = list(self.phase_detail_seconds)
         return d
 
 

@@ -75,6 +75,11 @@ enum Counter : int {
   kSubLightP0,
   kSubLightP1,
   kSubSparseLight,
+  kFineCommit,     // ns of device time: commit, certificate init / dense pass /
+  kFineCertInit,   // sparse pass (mark + check) / apply
+  kFineCertDense,
+  kFineCertSparse,
+  kFineCertApply,
   kNumCounters
 };
 
@@ -439,6 +444,27 @@ __device__ __forceinline__ bool lift_block(const SolveParams<V>& p, uint32_t v,
   return raised;
 }
 
+// Warp-uniform dynamic claims of medium rows, kClaim consecutive items per
+// atomic so hundreds of thousands of R-MAT rows do not serialise on one
+// cursor.  Returns false when the items are exhausted.
+constexpr uint32_t kClaim = 8;
+struct WarpClaim {
+  uint32_t next = 0, end = 0;
+};
+__device__ __forceinline__ bool warp_claim(unsigned int* cursor, uint32_t count, WarpClaim& c,
+                                           uint32_t& item) {
+  if (c.next >= c.end) {
+    uint32_t base = 0;
+    if (lane_id() == 0) base = atomicAdd(cursor, kClaim);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= count) return false;
+    c.next = base;
+    c.end = base + kClaim < count ? base + kClaim : count;
+  }
+  item = c.next++;
+  return true;
+}
+
 __device__ __forceinline__ void set_bit(uint32_t* bm, uint32_t v) {
   atomicOr(bm + (v >> 5), 1u << (v & 31u));
 }
@@ -729,11 +755,9 @@ __device__ __noinline__ void warp_rows(const SolveParams<V>& p, uint32_t count,
                                           uint32_t* chg, unsigned int* sum_dst) {
   __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
   Local L;
-  for (;;) {
-    uint32_t i = 0;
-    if (lane_id() == 0) i = atomicAdd(cursor, 1u);
-    i = __shfl_sync(0xffffffffu, i, 0);
-    if (i >= count) break;
+  WarpClaim wc;
+  uint32_t i;
+  while (warp_claim(cursor, count, wc, i)) {
     const uint32_t v = items(i);
     if (!owned(p, v)) continue;
     const bool p0 = v < p.g.rb[kP1L];
@@ -1034,11 +1058,9 @@ __device__ __noinline__ void round1_long(const SolveParams<V>& p, uint32_t* chg,
   __syncthreads();
   // medium: one warp per row
   const uint32_t nM = class_size(g, 1);
-  for (;;) {
-    uint32_t it = 0;
-    if (lane == 0) it = atomicAdd(slot_dyn + 0, 1u);
-    it = __shfl_sync(0xffffffffu, it, 0);
-    if (it >= nM) break;
+  WarpClaim wc;
+  uint32_t it;
+  while (warp_claim(slot_dyn + 0, nM, wc, it)) {
     const uint32_t u = class_item(g, 1, it);
     if (!owned(p, u)) continue;
     const bool p0 = u < g.rb[kP1L];
@@ -1245,11 +1267,9 @@ __device__ __forceinline__ void cert_long_rows(const SolveParams<V>& p, uint32_t
     }
   }
   __syncthreads();
-  for (;;) {
-    uint32_t i = 0;
-    if (lane_id() == 0) i = atomicAdd(slot_dyn + 0, 1u);
-    i = __shfl_sync(0xffffffffu, i, 0);
-    if (i >= nM) break;
+  WarpClaim wc;
+  uint32_t i;
+  while (warp_claim(slot_dyn + 0, nM, wc, i)) {
     const uint32_t v = itemsM(i);
     if (!owned(p, v)) continue;
     const V cvv = ldcg(p.stage + v);
@@ -1483,12 +1503,13 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
         sh->dyn[(phase + 2) & 3][k] = 0;
       }
   };
-  auto end_phase = [&](int kind) {
+  auto end_phase = [&](int kind, int fine = -1) {
     grid.sync();
     ++phase;
     if (leader) {
       const unsigned long long t = globaltimer();
       p.ctr[kTimeSeed + kind] += t - t_prev;
+      if (fine >= 0) p.ctr[kFineCommit + fine] += t - t_prev;
       t_prev = t;
     }
   };
@@ -1513,7 +1534,7 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
     if (changed == 0) break;  // a round that raised nothing: least fixpoint
     begin_phase();
     phase_commit<V>(p, chg);
-    end_phase(1);
+    end_phase(1, 0);
     if (round >= p.round_budget) {
       status = 5;
       break;
@@ -1529,12 +1550,12 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
       ++cert_attempts;
       begin_phase();
       phase_cert_init<V>(p, chg, slot_sum());
-      end_phase(2);
+      end_phase(2, 1);
       // pass 1 dense; later passes sparse while the removals are few
       int rb = 1;
       begin_phase();
       phase_cert_prune<V>(p, slot_sum(), slot_dyn(), p.rbm[1], p.rbm[0]);
-      end_phase(2);
+      end_phase(2, 2);
       ++cert_passes;
       uint32_t removed = prev_sum(1);
       while (removed > 0) {
@@ -1544,15 +1565,15 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
         if (sparse_pass) {
           begin_phase();
           phase_cert_mark<V>(p, p.rbm[rb], slot_sum(), slot_dyn());
-          end_phase(2);
+          end_phase(2, 3);
           const unsigned int* queued = sh->dyn[(phase - 1) & 3];
           begin_phase();
           phase_cert_check<V>(p, queued, slot_sum(), slot_dyn(), p.rbm[rb ^ 1], p.rbm[rb]);
-          end_phase(2);
+          end_phase(2, 3);
         } else {
           begin_phase();
           phase_cert_prune<V>(p, slot_sum(), slot_dyn(), p.rbm[rb ^ 1], p.rbm[rb]);
-          end_phase(2);
+          end_phase(2, 2);
         }
         rb ^= 1;
         ++cert_passes;
@@ -1560,7 +1581,7 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
       }
       begin_phase();
       phase_cert_apply<V>(p, chg, slot_sum());
-      end_phase(2);
+      end_phase(2, 4);
       const uint32_t cert = prev_sum(0);
       certified_any = cert > 0;
       changed += cert;

@@ -615,6 +615,7 @@ void fill_stats(egs_ctx* c, const unsigned long long* h, double ms, egs_gpu_stat
   st->kernel_launches = 1;
   for (int k = 0; k < 5; ++k)
     st->lift_sub_seconds[k] = h[egs::kSubHeavy + k] * 1e-9 / (double)c->grid;
+  for (int k = 0; k < 5; ++k) st->phase_detail_seconds[k] = h[egs::kFineCommit + k] * 1e-9;
   st->value_bits = (uint32_t)c->vbits;
   st->grid_ctas = (uint32_t)c->grid;
 }

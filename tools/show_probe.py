@@ -15,3 +15,6 @@ for path in sys.argv[1:]:
         if "lift_sub_seconds" in d:
             print("     lift sub (H/M/L0/L1/sparse ms):",
                   " ".join(f"{x * 1e3:.3f}" for x in d["lift_sub_seconds"]))
+        if "phase_detail_seconds" in d:
+            print("     commit / cert init, dense, sparse, apply (ms):",
+                  " ".join(f"{x * 1e3:.3f}" for x in d["phase_detail_seconds"]))
