@@ -819,26 +819,31 @@ __device__ __forceinline__ bool good_edge(const SolveParams<V>& p, int64_t fv,
   return ct != NotCand<V>::v && fv < static_cast<int64_t>(ct) - r.y;
 }
 
+#ifndef EGS_CERT_CHUNK
+#define EGS_CERT_CHUNK 4
+#endif
+constexpr int kCertChunk = EGS_CERT_CHUNK;  // edges tested per step (early exit between)
+
 template <class V, bool P0>
 __device__ __forceinline__ bool cert_keep_thread(const SolveParams<V>& p,
                                                  uint32_t v, int64_t fv, Local& L) {
   const uint32_t b = __ldg(p.g.off + v), e = __ldg(p.g.off + v + 1);
-  for (uint32_t i = b; i < e; i += 4) {
-    int2 r[4];
+  for (uint32_t i = b; i < e; i += kCertChunk) {
+    int2 r[kCertChunk];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) r[k] = ld_edge(p.g.edge + min(i + k, e - 1));
-    V c[4];
+    for (int k = 0; k < kCertChunk; ++k) r[k] = ld_edge(p.g.edge + min(i + k, e - 1));
+    V c[kCertChunk];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) c[k] = gather(p.stage + r[k].x);
+    for (int k = 0; k < kCertChunk; ++k) c[k] = gather(p.stage + r[k].x);
     bool all = true, any = false;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < kCertChunk; ++k) {
       const bool g = c[k] == Top<V>::v ||
                      (c[k] != NotCand<V>::v && fv < static_cast<int64_t>(c[k]) - r[k].y);
       all &= g;
       any |= g;
     }
-    L.cert_edges += min(4u, e - i);
+    L.cert_edges += min((uint32_t)kCertChunk, e - i);
     if (P0 && !all) return false;
     if (!P0 && any) return true;
   }
@@ -1303,19 +1308,50 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
   auto itH = [gp = &g](uint32_t i) { return class_item(*gp, 2, i); };
   auto itM = [gp = &g](uint32_t i) { return class_item(*gp, 1, i); };
   cert_long_rows<V>(p, class_size(g, 2), itH, class_size(g, 1), itM, slot_dyn, rbm, L);
-  // light candidates: a thread each, aligned 32-vertex words per warp
-  const uint32_t nwarps = gridDim.x * kWarps;
-  const uint32_t gw = tid >> 5;
+  // light candidates: one row per lane through the TMA tile pipeline (tiles
+  // without a candidate are skipped); removals are published in rbm
   for (int side = 0; side < 2; ++side) {
     const uint32_t lo = clip_lo(p, side ? g.rb[kP1L] : g.rb[kP0L]);
     const uint32_t hi = clip_hi(p, side ? g.rb[kP1M] : g.rb[kP0M]);
-    for (uint32_t w = (lo >> 5) + gw; w < (hi + 31) >> 5; w += nwarps) {
-      const uint32_t v = (w << 5) + lane_id();
-      const bool rem = v >= lo && v < hi && cert_check_thread<V>(p, v, L);
-      const uint32_t m = __ballot_sync(0xffffffffu, rem);
-      if (m && lane_id() == 0) atomicOr(rbm + w, m);
-      L.phase_count += rem;
-    }
+    auto need = [&](uint32_t v, V& cv) {
+      cv = ldcg(p.stage + v);
+      return is_cand<V>(cv);
+    };
+    auto row = [&](uint32_t v, const int2* rec, uint32_t len, uint32_t, V cv) {
+      const int64_t fv = (int64_t)cv;
+      const bool p0 = side == 0;
+      ++L.cert_scanned;
+      bool keep = p0;
+      for (uint32_t k0 = 0; k0 < len; k0 += kCertChunk) {
+        int2 r[kCertChunk];
+#pragma unroll
+        for (int k = 0; k < kCertChunk; ++k) r[k] = rec[min(k0 + k, len - 1)];
+        V c[kCertChunk];
+#pragma unroll
+        for (int k = 0; k < kCertChunk; ++k) c[k] = gather(p.stage + r[k].x);
+        bool all = true, any = false;
+#pragma unroll
+        for (int k = 0; k < kCertChunk; ++k) {
+          const bool gd = c[k] == Top<V>::v ||
+                          (c[k] != NotCand<V>::v && fv < static_cast<int64_t>(c[k]) - r[k].y);
+          all &= gd;
+          any |= gd;
+        }
+        L.cert_edges += min((uint32_t)kCertChunk, len - k0);
+        if (p0 && !all) {
+          keep = false;
+          break;
+        }
+        if (!p0 && any) {
+          keep = true;
+          break;
+        }
+      }
+      if (!keep) stcg(p.stage + v, NotCand<V>::v);
+      return !keep;
+    };
+    auto fallback = [&](uint32_t v, V) { return cert_check_thread<V>(p, v, L); };
+    tma_tiles<V>(p, lo, hi, rbm, L, need, row, fallback);
   }
   block_flush(L, p.ctr, slot_sum + 1, s_cnt);
 }
