@@ -93,15 +93,14 @@ __global__ void __launch_bounds__(256)
 }
 
 // ... and the weight half once the weights of rows [r0, r1) have arrived
-// (weights must fit int32: arena.hpp:13 stores int64).
+// (narrowed to int32 on the host, which checks the range: arena.hpp:13
+// stores int64).
 __global__ void __launch_bounds__(256)
-    k_relabel_weights(uint32_t r0, uint32_t r1, const uint64_t* off64, const int64_t* w64,
-                      const uint32_t* perm, const uint32_t* off_new, int2* edge,
-                      unsigned int* bad) {
+    k_relabel_weights(uint32_t r0, uint32_t r1, const uint64_t* off64, const int32_t* w32,
+                      const uint32_t* perm, const uint32_t* off_new, int2* edge) {
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int* ex = reinterpret_cast<int*>(edge);
-  unsigned int flag = 0;
   for (uint32_t o0 = r0 + gw * 32; o0 < r1; o0 += nwarps * 32) {
     const uint32_t o = o0 + lane_id();
     uint32_t b = 0, e = 0, delta = 0;
@@ -112,15 +111,9 @@ __global__ void __launch_bounds__(256)
     }
     warp_expand(b, e, [&](bool valid, uint32_t idx, uint32_t owner_lane) {
       const uint32_t d = __shfl_sync(0xffffffffu, delta, owner_lane);
-      if (valid) {
-        const int64_t w = w64[idx];
-        if (w < -2147483647LL || w > 2147483647LL) flag |= 1u;
-        ex[2 * (size_t)(idx + d) + 1] = (int)w;
-      }
+      if (valid) ex[2 * (size_t)(idx + d) + 1] = w32[idx];
     });
   }
-  flag = __reduce_or_sync(0xffffffffu, flag);
-  if (lane_id() == 0 && flag) atomicOr(bad, flag);
 }
 
 // CSC column offsets from the dst-sorted keys: coff[t] = first j with

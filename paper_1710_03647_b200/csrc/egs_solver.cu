@@ -25,6 +25,9 @@
 #include <stdexcept>
 #include <string>
 #include <vector>
+#include <atomic>
+#include <mutex>
+#include <thread>
 
 #include "egs_build.cuh"
 #include "egs_gpu.h"
@@ -238,6 +241,25 @@ const void* solve_kernel() {
   return reinterpret_cast<const void*>(&egs::k_solve<V>);
 }
 
+// Process-wide pinned staging buffer for the narrowed weights (grows on
+// demand; one upload at a time uses it).
+std::mutex g_stage_mu;
+int32_t* g_stage = nullptr;
+size_t g_stage_cap = 0;
+
+int32_t* pinned_stage(uint64_t count) {
+  if (count > g_stage_cap) {
+    if (g_stage) cudaFreeHost(g_stage);
+    g_stage = nullptr;
+    g_stage_cap = 0;
+    void* p = nullptr;
+    CK(cudaMallocHost(&p, std::max<uint64_t>(count, 1) * sizeof(int32_t)));
+    g_stage = static_cast<int32_t*>(p);
+    g_stage_cap = count;
+  }
+  return g_stage;
+}
+
 // Build the relabelled device arena from the reference CSR (host spans),
 // pipelined with the upload: the copy stream brings offsets + owners, then
 // the targets and the weights in row-range chunks of ~m/16 edges; the main
@@ -249,13 +271,14 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   StepTimer tm(c->stream);
   const uint32_t n = c->n;
   const uint64_t m = c->m;
+  bool h_stage_bad = false;
   cudaStream_t s = c->stream, sc = c->copy_stream, sw = c->aux_stream;
   const int sms = c->num_sms;
-  DevBuf d_off64, d_dst, d_w64, d_owner, d_key, d_keys, d_val, d_misc, d_tmp, d_ck0, d_cv0,
+  DevBuf d_off64, d_dst, d_w32, d_owner, d_key, d_keys, d_val, d_misc, d_tmp, d_ck0, d_cv0,
       d_ck1;
   uint64_t* off64 = d_off64.alloc<uint64_t>((size_t)n + 1);
   uint32_t* dst = d_dst.alloc<uint32_t>(m);
-  int64_t* w64 = d_w64.alloc<int64_t>(m);
+  int32_t* w32 = d_w32.alloc<int32_t>(m);
   uint8_t* owner = d_owner.alloc<uint8_t>(n);
   unsigned int* misc = d_misc.alloc<unsigned int>(32);  // [0..15] hist, [16] bad
   uint8_t* key = d_key.alloc<uint8_t>(n);
@@ -311,11 +334,6 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
     CK(cudaMemcpyAsync(dst + e0, a->csr_targets + e0, (e1 - e0) * 4, cudaMemcpyHostToDevice, sc));
     CK(cudaEventRecord(ex[k], sc));
   }
-  for (int k = 0; k < nch; ++k) {
-    const auto [e0, e1] = span_of(k);
-    CK(cudaMemcpyAsync(w64 + e0, a->csr_weights + e0, (e1 - e0) * 8, cudaMemcpyHostToDevice, sc));
-    CK(cudaEventRecord(ew[k], sc));
-  }
 
   // vertices: class keys, stable partition by class, relabelled offsets
   CK(cudaStreamWaitEvent(s, e_vert, 0));
@@ -336,19 +354,13 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   CK(cudaEventRecord(e_perm, s));
   tm.mark("vertices (classify, sort, offsets)");
 
-  // targets as they land (main stream), weights as they land (aux stream)
-  CK(cudaStreamWaitEvent(sw, e_perm, 0));
+  // targets as they land (main stream)
   for (int k = 0; k < nch; ++k) {
     CK(cudaStreamWaitEvent(s, ex[k], 0));
     egs::k_relabel_targets<<<grid_for((uint64_t)(rows[k + 1] - rows[k]) * 4, sms), 256, 0, s>>>(
         n, rows[k], rows[k + 1], off64, dst, c->perm, c->off, c->edge, ck0, cv0, misc + 16);
     CK(cudaGetLastError());
-    CK(cudaStreamWaitEvent(sw, ew[k], 0));
-    egs::k_relabel_weights<<<grid_for((uint64_t)(rows[k + 1] - rows[k]) * 4, sms), 256, 0, sw>>>(
-        rows[k], rows[k + 1], off64, w64, c->perm, c->off, c->edge, misc + 16);
-    CK(cudaGetLastError());
   }
-  tm.mark("upload + relabel targets");
 
   // transpose: sort the (dst, src) pairs by dst while the weights stream in
   tmp_bytes = 0;
@@ -358,7 +370,58 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, ck0, ck1, cv0, c->csrc, m, 0, kb, s));
   egs::k_col_offsets<<<grid_for(m + 1, sms), 256, 0, s>>>(n, m, ck1, c->coff);
   CK(cudaGetLastError());
-  tm.mark("CSC sort + offsets");
+
+  // weights: host threads narrow int64 -> int32 into a pinned staging buffer
+  // chunk by chunk (checking the range), each chunk's DMA and device relabel
+  // queued as soon as it is converted -- while the targets are still on the
+  // wire and the transpose sorts.  Half the weight bytes cross PCIe, always
+  // from pinned memory.
+  CK(cudaStreamWaitEvent(sw, e_perm, 0));
+  {
+    std::lock_guard<std::mutex> lk(g_stage_mu);
+    int32_t* stage = pinned_stage(m);
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const int T = m >= (1u << 20) ? (int)hw : 1;
+    std::vector<std::atomic<int>> done(nch);
+    for (auto& d : done) d.store(0);
+    std::atomic<bool> out_of_range{false};
+    const int64_t* w = a->csr_weights;
+    auto work = [&](int t) {
+      bool bad = false;
+      for (int k = 0; k < nch; ++k) {
+        const auto [e0, e1] = span_of(k);
+        const uint64_t lo = e0 + (e1 - e0) * t / T, hi = e0 + (e1 - e0) * (t + 1) / T;
+        for (uint64_t i = lo; i < hi; ++i) {
+          const int64_t x = w[i];
+          bad |= x < -2147483647LL || x > 2147483647LL;
+          stage[i] = (int32_t)x;
+        }
+        done[k].fetch_add(1, std::memory_order_release);
+      }
+      if (bad) out_of_range.store(true);
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < T; ++t) pool.emplace_back(work, t);
+    std::thread self_worker;
+    if (T == 1) work(0);
+    else self_worker = std::thread(work, 0);
+    for (int k = 0; k < nch; ++k) {
+      while (done[k].load(std::memory_order_acquire) < T) std::this_thread::yield();
+      const auto [e0, e1] = span_of(k);
+      CK(cudaMemcpyAsync(w32 + e0, stage + e0, (e1 - e0) * 4, cudaMemcpyHostToDevice, sc));
+      CK(cudaEventRecord(ew[k], sc));
+      CK(cudaStreamWaitEvent(sw, ew[k], 0));
+      egs::k_relabel_weights<<<grid_for((uint64_t)(rows[k + 1] - rows[k]) * 4, sms), 256, 0,
+                               sw>>>(rows[k], rows[k + 1], off64, w32, c->perm, c->off, c->edge);
+      CK(cudaGetLastError());
+    }
+    if (self_worker.joinable()) self_worker.join();
+    for (auto& th : pool) th.join();
+    // the staging buffer is re-used by the next upload: wait for its DMA
+    CK(cudaStreamSynchronize(sc));
+    if (out_of_range.load()) h_stage_bad = true;
+  }
+  tm.mark("upload + relabel + CSC sort");
   CK(cudaEventRecord(e_tail, sw));
   CK(cudaStreamWaitEvent(s, e_tail, 0));
   unsigned int h_misc[32] = {0};
@@ -366,7 +429,7 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   // temporaries go back to the pool in stream order
   d_off64.release();
   d_dst.release();
-  d_w64.release();
+  d_w32.release();
   d_owner.release();
   d_key.release();
   d_keys.release();
@@ -384,7 +447,7 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   cudaEventDestroy(e_vert);
   cudaEventDestroy(e_perm);
   cudaEventDestroy(e_tail);
-  const unsigned int bad = h_misc[16];
+  const unsigned int bad = h_misc[16] | (h_stage_bad ? 1u : 0u);
   if (bad & 1u) throw Fail(EGS_ERR_UNSUPPORTED, "edge weight outside int32 on the device path");
   if (bad & 2u) throw Fail(EGS_ERR_INVALID_CONFIG, "edge target out of range");
   c->rb[0] = 0;
