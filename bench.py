@@ -292,7 +292,9 @@ def run_our_arm(a):
 
     # ---- end to end through the C-ABI one-shot call: e2e ---------------
     out, _owner = egs.pinned_empty(n)
-    h2d = (n + 1) * 8 + m * 4 + m * 8 + n
+    # bytes that cross PCIe per call: offsets (u64) + owners + targets (u32)
+    # + weights narrowed to int32 on the host (egs_solver.cu build_arena)
+    h2d = (n + 1) * 8 + n + m * 4 + m * 4
     d2h = n * 8
     for _ in range(max(1, a.warmup // 2)):
         egs.solve(arena, options=opts, out=out)
@@ -424,7 +426,7 @@ def run_our_arm_partitioned(a):
     steps.close()
 
     # e2e: partition upload (H2D + device build) + solve + export, per rank
-    h2d = (n + 1) * 8 + m * 4 + m * 8 + n
+    h2d = (n + 1) * 8 + n + m * 4 + m * 4
     e2e_t, e2e_edges = 0.0, 0
     for _ in range(a.e2e_steps):
         def one():

@@ -598,6 +598,7 @@ __device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, uint32_t lo, 
   }
   __syncwarp();
   if (lane == 0) g_tma_parity[warp] = parity;
+  __syncwarp();  // every lane sees the new parity before the warp's next pipeline
 }
 
 // Player-1 light rows of a dense round through the tile pipeline: tiles of
