@@ -319,7 +319,7 @@ class SolverOptions:
     """egsolve::SolverOptions (solver.hpp:33-42); ``workers`` counts GPUs."""
     workers: int = 1
     certify: bool = True
-    cert_interval: int = 2
+    cert_interval: int = 1
     sparse_div: int = 4
     grid_ctas: int = 0
     no_tma: bool = False

@@ -1222,6 +1222,41 @@ __device__ __noinline__ void phase_cert_init(const SolveParams<V>& p, const uint
   block_flush(L, p.ctr, slot_sum + 1, s_cnt);
 }
 
+// Commit fused with certificate step 1 (one pass over the vertices instead
+// of two): a raised vertex publishes its staged value and, unless it reached
+// top, becomes a candidate with that value; every other vertex is top or
+// not a candidate.
+template <class V>
+__device__ __noinline__ void phase_commit_cert_init(const SolveParams<V>& p, const uint32_t* chg) {
+  constexpr V TOP = Top<V>::v;
+  constexpr int U = 4;  // vertices per thread per step, loads issued together
+  const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
+  const uint32_t nthreads = gridDim.x * kBlock;
+  const uint32_t nwords = (p.g.n + 31) >> 5;
+  for (uint32_t w = tid; w < nwords; w += nthreads) p.rbm[1][w] = 0u;
+  for (uint32_t v0 = p.own_lo + tid; v0 < p.own_hi; v0 += nthreads * U) {
+    uint32_t bits[U];
+    V fv[U], sv[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const uint32_t v = v0 + k * nthreads;
+      const bool in = v < p.own_hi;
+      bits[k] = in ? ldcg(chg + (v >> 5)) : 0u;
+      fv[k] = in ? ldcg(p.f + v) : TOP;
+      sv[k] = in ? ldcg(p.stage + v) : TOP;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const uint32_t v = v0 + k * nthreads;
+      if (v >= p.own_hi) continue;
+      const bool raised = (bits[k] >> (v & 31u)) & 1u;
+      const V val = raised ? sv[k] : fv[k];
+      if (raised) stcg(p.f + v, val);
+      stcg(p.stage + v, val == TOP ? TOP : raised ? val : NotCand<V>::v);
+    }
+  }
+}
+
 // Certificate, step 2: pruning passes.  A removed candidate becomes
 // kNotCand in p.stage and its bit is set in `rbm` (removed in this pass), so
 // the next pass can be sparse: only candidate predecessors of this pass's
@@ -1560,7 +1595,7 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
   uint32_t changed = prev_sum(0);
   unsigned long long round = 1, rounds_dense = 1, rounds_sparse = 0, cert_attempts = 0,
                      cert_passes = 0;
-  int K = p.cert_interval > 0 ? p.cert_interval : 2;
+  int K = p.cert_interval > 0 ? p.cert_interval : 1;
   unsigned long long next_cert = (unsigned long long)K;
   int buf = 0;
   unsigned int status = 0;
@@ -1569,8 +1604,12 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
     // `changed` vertices were raised by round `round`, marked in chg
     uint32_t* chg = p.chg[(round - 1) & 1];
     if (changed == 0) break;  // a round that raised nothing: least fixpoint
+    const bool cert_now = p.certify && round >= next_cert;
     begin_phase();
-    phase_commit<V>(p, chg);
+    if (cert_now)
+      phase_commit_cert_init<V>(p, chg);  // commit + certificate step 1
+    else
+      phase_commit<V>(p, chg);
     end_phase(1, 0);
     if (round >= p.round_budget) {
       status = 5;
@@ -1583,11 +1622,8 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
 
     // ---- certificate
     bool certified_any = false;
-    if (p.certify && round >= next_cert) {
+    if (cert_now) {
       ++cert_attempts;
-      begin_phase();
-      phase_cert_init<V>(p, chg, slot_sum());
-      end_phase(2, 1);
       // pass 1 dense; later passes sparse while the removals are few
       int rb = 1;
       begin_phase();

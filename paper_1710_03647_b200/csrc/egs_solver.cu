@@ -616,7 +616,7 @@ egs::SolveParams<V> make_params(egs_ctx* c, unsigned long long* budget_out) {
   p.mode = o.mode;
   p.use_tma = o.no_tma ? 0 : 1;
   p.certify = o.certify;
-  p.cert_interval = o.cert_interval > 0 ? o.cert_interval : 2;
+  p.cert_interval = o.cert_interval > 0 ? o.cert_interval : 1;
   p.sparse_div = o.sparse_div > 0 ? (uint32_t)o.sparse_div : 4u;
   p.avg_in_deg = n ? (float)((double)c->m / (double)n) : 1.0f;
   if (p.avg_in_deg < 1.0f) p.avg_in_deg = 1.0f;
@@ -987,7 +987,7 @@ void egs_gpu_opts_default(egs_gpu_opts* o) {
   o->n_gpus = 1;
   o->device = -1;
   o->certify = 1;
-  o->cert_interval = 2;
+  o->cert_interval = 1;
   o->sparse_div = 4;
   o->mode = EGS_MODE_AUTO;
 }

@@ -168,7 +168,7 @@ class PartitionReport:
     counters: dict = field(default_factory=dict)
 
 
-def solve_partitioned(steps, comm, certify: bool = True, cert_interval: int = 2,
+def solve_partitioned(steps, comm, certify: bool = True, cert_interval: int = 1,
                       round_budget: Optional[int] = None,
                       timeout_seconds: float = 0.0) -> PartitionReport:
     """The dense schedule of k_solve (egs_solve.cuh), one step at a time.
@@ -188,7 +188,7 @@ def solve_partitioned(steps, comm, certify: bool = True, cert_interval: int = 2,
     parity = 0
     changed = comm.allreduce_sum(step(STEP_ROUND1, parity)[0])
     rounds = 1
-    K = cert_interval if cert_interval > 0 else 2
+    K = cert_interval if cert_interval > 0 else 1
     next_cert = K
     attempts = passes = certified = 0
     while changed:
