@@ -1483,20 +1483,25 @@ __device__ __noinline__ void phase_cert_apply(const SolveParams<V>& p, uint32_t*
   const uint32_t nwarps = gridDim.x * kWarps;
   const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5;
   Local L;
-  for (uint32_t w = (p.own_lo >> 5) + gw; w < (p.own_hi + 31) >> 5; w += nwarps) {
-    const uint32_t v = (w << 5) + lane_id();
-    bool hit = false;
-    if (v < n && owned(p, v)) {
-      const V cvv = ldcg(p.stage + v);
-      if (cvv != Top<V>::v && cvv != NotCand<V>::v) {
-        stcg(p.f + v, Top<V>::v);
-        hit = true;
-      }
+  constexpr uint32_t U = 4;  // words per warp step, loads issued together
+  const uint32_t w_lo = p.own_lo >> 5, w_hi = (p.own_hi + 31) >> 5;
+  for (uint32_t w0 = w_lo + gw * U; w0 < w_hi; w0 += nwarps * U) {
+    V cv[U];
+#pragma unroll
+    for (uint32_t k = 0; k < U; ++k) {
+      const uint32_t v = ((w0 + k) << 5) + lane_id();
+      cv[k] = (w0 + k < w_hi && v < n && owned(p, v)) ? ldcg(p.stage + v) : Top<V>::v;
     }
-    const uint32_t m = __ballot_sync(0xffffffffu, hit);
-    if (m && lane_id() == 0) atomicOr(chg + w, m);
-    L.phase_count += hit;
-    L.certified += hit;
+#pragma unroll
+    for (uint32_t k = 0; k < U; ++k) {
+      const uint32_t v = ((w0 + k) << 5) + lane_id();
+      const bool hit = is_cand<V>(cv[k]);
+      if (hit) stcg(p.f + v, Top<V>::v);
+      const uint32_t m = __ballot_sync(0xffffffffu, hit);
+      if (m && lane_id() == 0) atomicOr(chg + w0 + k, m);
+      L.phase_count += hit;
+      L.certified += hit;
+    }
   }
   block_flush(L, p.ctr, slot_sum + 0, s_cnt);
 }
