@@ -84,6 +84,7 @@ enum Counter : int {
 };
 
 enum Mode : int { kModeAuto = 0, kModeDense = 1, kModeSparse = 2 };
+constexpr unsigned kTraceCap = 512;
 
 struct Graph {
   uint32_t n;
@@ -125,6 +126,7 @@ struct SolveParams {
   int cert_interval;
   uint32_t sparse_div;      // next round sparse iff est. frontier * div < n
   float avg_in_deg;
+  unsigned long long* trace;   // optional: per-phase (kind << 56 | ns) log, kTraceCap entries
   unsigned long long round_budget;
   unsigned long long timeout_ns;   // 0 = none; measured from kernel start
 };
@@ -238,7 +240,10 @@ __device__ __forceinline__ bool lift_thread(const SolveParams<V>& p, uint32_t v,
     for (int k = 0; k < kChunk; ++k) {
       const V x = ominus_cap<V>(c[k], r[k].y, p.g.cap);
       if (P0) {
-        if (x < acc || (k == 0 && i == b)) {
+        // argmin; among equal values prefer a player-0 target (see round 1)
+        const bool tp1 = (uint32_t)r[k].x >= p.g.rb[kP1L];
+        if (x < acc || (k == 0 && i == b) ||
+            (x == acc && !tp1 && (uint32_t)best.x >= p.g.rb[kP1L])) {
           acc = x;
           best = r[k];
         }
@@ -952,25 +957,35 @@ __device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo, 
     }
     return false;
   };
+  // the player-0 witness: an edge of least max(0, -w), preferring a
+  // player-0 target (player-1 targets are the ones the certificate sends to
+  // top, which would void the witness in the next round)
   auto row = [&](uint32_t v, const int2* rec, uint32_t len, uint32_t, V) {
-    const bool p0 = v < g.rb[kP1L];
+    const bool p0 = v < g.rb[kP1L];  // warp-uniform: the ranges are split by owner
     const uint32_t rot = lane_id() % len;
     int minw = INT32_MAX, maxw = INT32_MIN;
-    uint32_t jmax = 0;
+    uint32_t jbest = 0, kbest = 0xFFFFFFFFu;
     for (uint32_t k0 = 0; k0 < len; k0 += kChunk) {
 #pragma unroll
       for (int k = 0; k < kChunk; ++k) {
         uint32_t j = min(k0 + k, len - 1) + rot;
         j = j >= len ? j - len : j;
-        const int w = rec[j].y;
-        minw = min(minw, w);
-        if (w > maxw) {
-          maxw = w;
-          jmax = j;
+        const int2 r = rec[j];
+        if (p0) {
+          maxw = max(maxw, r.y);
+          // key = 2 * max(0, -w) + (target is player 1): fits 32 bits
+          const uint32_t key = ((r.y >= 0 ? 0u : (uint32_t)(-r.y)) << 1) |
+                               (uint32_t)((uint32_t)r.x >= g.rb[kP1L]);
+          if (key < kbest) {
+            kbest = key;
+            jbest = j;
+          }
+        } else {
+          minw = min(minw, r.y);
         }
       }
     }
-    return finish(v, p0, minw, maxw, rec[jmax], len);
+    return finish(v, p0, minw, maxw, rec[jbest], len);
   };
   auto fallback = [&](uint32_t v, V) {
     const bool p0 = v < g.rb[kP1L];
@@ -1587,6 +1602,8 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
       const unsigned long long t = globaltimer();
       p.ctr[kTimeSeed + kind] += t - t_prev;
       if (fine >= 0) p.ctr[kFineCommit + fine] += t - t_prev;
+      if (p.trace && phase < kTraceCap)
+        p.trace[phase] = ((unsigned long long)(kind * 8 + fine + 1) << 56) | (t - t_prev);
       t_prev = t;
     }
   };

@@ -159,6 +159,7 @@ struct egs_ctx {
   unsigned long long* ctr = nullptr;
   int64_t* f64 = nullptr;
   unsigned long long* h_ctr = nullptr;  // pinned mirror
+  unsigned long long* trace = nullptr;  // EGS_TRACE=1: per-phase device times
   cudaEvent_t ev[2] = {nullptr, nullptr};
   int grid = 0;
   bool solved = false;
@@ -206,7 +207,7 @@ void ctx_free(egs_ctx* c) {
   if (c->device >= 0) cudaSetDevice(c->device);
   void* ptrs[] = {c->off,    c->edge,   c->coff, c->csrc,  c->perm, c->inv,
                   c->f,      c->wit,    c->chg[0], c->chg[1], c->frb,
-                  c->fr[0],  c->fr[1],  c->stage, c->scratch, c->ctr, c->rbm[0], c->rbm[1], c->cbm,
+                  c->fr[0],  c->fr[1],  c->stage, c->scratch, c->ctr, c->rbm[0], c->rbm[1], c->cbm, c->trace,
                   c->f64};
   if (c->stream) {
     for (void* p : ptrs) dfree(p, c->stream);
@@ -499,6 +500,7 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     CK(cudaMallocHost(&c->h_ctr, egs::kNumCounters * sizeof(unsigned long long)));
     tm0.mark("create: streams, events, pinned");
     c->ctr = dalloc<unsigned long long>(egs::kNumCounters);
+    if (std::getenv("EGS_TRACE")) c->trace = dalloc<unsigned long long>(egs::kTraceCap);
     c->scratch = dalloc<egs::Scratch>(1);
     c->rank = rank;
     c->world = world;
@@ -613,6 +615,7 @@ egs::SolveParams<V> make_params(egs_ctx* c, unsigned long long* budget_out) {
   p.stage = static_cast<V*>(c->stage);
   p.sh = c->scratch;
   p.ctr = c->ctr;
+  p.trace = c->trace;
   p.mode = o.mode;
   p.use_tma = o.no_tma ? 0 : 1;
   p.certify = o.certify;
@@ -711,6 +714,20 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
   const unsigned long long* h = c->h_ctr;
   c->solved = h[egs::kStatus] == 0;
   if (st) fill_stats<V>(c, h, ms, st);
+  if (c->trace) {  // EGS_TRACE=1: one line per phase on stderr
+    std::vector<unsigned long long> tr(egs::kTraceCap);
+    CK(cudaMemcpy(tr.data(), c->trace, tr.size() * 8, cudaMemcpyDeviceToHost));
+    static const char* names[4] = {"round1", "lift", "cert", "activate"};
+    static const char* fine[6] = {"", "/commit", "/cert-init", "/cert-dense", "/cert-sparse",
+                                  "/cert-apply"};
+    for (unsigned k = 1; k < egs::kTraceCap && tr[k]; ++k) {
+      const int code = (int)(tr[k] >> 56) - 1;
+      std::fprintf(stderr, "[egs trace] %3u %-8s%-13s %9.1f us\n", k, names[code / 8 % 4],
+                   fine[code % 8 + 1 < 6 ? code % 8 + 1 : 0],
+                   (tr[k] & ((1ull << 56) - 1)) * 1e-3);
+    }
+    CK(cudaMemset(c->trace, 0, egs::kTraceCap * 8));
+  }
   if (h[egs::kStatus] == 2) throw Fail(EGS_ERR_TIMEOUT, "solve timed out");
   if (h[egs::kStatus] == 5)
     throw Fail(EGS_ERR_BOUND, "round budget of " + std::to_string(budget) +
