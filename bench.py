@@ -222,6 +222,14 @@ def run_reference_arm(a):
 
 
 # --------------------------------------------------------- our arm ----
+def h2d_bytes(arena):
+    """Bytes that cross PCIe per upload: offsets (u64) + owners + targets (u32)
+    + weights narrowed on the host to int8/int16/int32 by max |w|
+    (egs_solver.cu upload_weights)."""
+    n, m, mw = arena.num_vertices, arena.num_edges, arena.max_abs_weight
+    wb = 1 if mw <= 127 else 2 if mw <= 32767 else 4
+    return (n + 1) * 8 + n + m * 4 + m * wb
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -292,9 +300,7 @@ def run_our_arm(a):
 
     # ---- end to end through the C-ABI one-shot call: e2e ---------------
     out, _owner = egs.pinned_empty(n)
-    # bytes that cross PCIe per call: offsets (u64) + owners + targets (u32)
-    # + weights narrowed to int32 on the host (egs_solver.cu build_arena)
-    h2d = (n + 1) * 8 + n + m * 4 + m * 4
+    h2d = h2d_bytes(arena)
     d2h = n * 8
     for _ in range(max(1, a.warmup // 2)):
         egs.solve(arena, options=opts, out=out)
@@ -426,7 +432,7 @@ def run_our_arm_partitioned(a):
     steps.close()
 
     # e2e: partition upload (H2D + device build) + solve + export, per rank
-    h2d = (n + 1) * 8 + n + m * 4 + m * 4
+    h2d = h2d_bytes(arena)
     e2e_t, e2e_edges = 0.0, 0
     for _ in range(a.e2e_steps):
         def one():

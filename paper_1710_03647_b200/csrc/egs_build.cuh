@@ -93,10 +93,11 @@ __global__ void __launch_bounds__(256)
 }
 
 // ... and the weight half once the weights of rows [r0, r1) have arrived
-// (narrowed to int32 on the host, which checks the range: arena.hpp:13
-// stores int64).
+// (narrowed on the host to the narrowest of int8/int16/int32 that holds
+// max |w|, range-checked there: arena.hpp:13 stores int64).
+template <class W>
 __global__ void __launch_bounds__(256)
-    k_relabel_weights(uint32_t r0, uint32_t r1, const uint64_t* off64, const int32_t* w32,
+    k_relabel_weights(uint32_t r0, uint32_t r1, const uint64_t* off64, const W* wn,
                       const uint32_t* perm, const uint32_t* off_new, int2* edge) {
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -111,7 +112,7 @@ __global__ void __launch_bounds__(256)
     }
     warp_expand(b, e, [&](bool valid, uint32_t idx, uint32_t owner_lane) {
       const uint32_t d = __shfl_sync(0xffffffffu, delta, owner_lane);
-      if (valid) ex[2 * (size_t)(idx + d) + 1] = w32[idx];
+      if (valid) ex[2 * (size_t)(idx + d) + 1] = (int)wn[idx];
     });
   }
 }

@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
+#include <limits>
 #include <string>
 #include <vector>
 #include <atomic>
@@ -245,20 +246,83 @@ const void* solve_kernel() {
 // Process-wide pinned staging buffer for the narrowed weights (grows on
 // demand; one upload at a time uses it).
 std::mutex g_stage_mu;
-int32_t* g_stage = nullptr;
+void* g_stage = nullptr;
 size_t g_stage_cap = 0;
 
-int32_t* pinned_stage(uint64_t count) {
-  if (count > g_stage_cap) {
+void* pinned_stage(uint64_t bytes) {
+  if (bytes > g_stage_cap) {
     if (g_stage) cudaFreeHost(g_stage);
     g_stage = nullptr;
     g_stage_cap = 0;
     void* p = nullptr;
-    CK(cudaMallocHost(&p, std::max<uint64_t>(count, 1) * sizeof(int32_t)));
-    g_stage = static_cast<int32_t*>(p);
-    g_stage_cap = count;
+    CK(cudaMallocHost(&p, std::max<uint64_t>(bytes, 1)));
+    g_stage = p;
+    g_stage_cap = bytes;
   }
   return g_stage;
+}
+
+// Weights: host threads narrow int64 -> W (int8 / int16 / int32, the
+// narrowest that holds max |w|) into the pinned stage chunk by chunk,
+// checking the range; each chunk's DMA and device relabel are queued as soon
+// as it is converted, while the targets are still on the wire and the
+// transpose sorts.  C4 (|w| <= 100) sends 1 byte per weight instead of 8.
+template <class W>
+bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint32_t>& rows,
+                    std::vector<cudaEvent_t>& ew, const uint64_t* off64, void* wdev) {
+  cudaStream_t sc = c->copy_stream, sw = c->aux_stream;
+  const int nch = (int)rows.size() - 1;
+  const uint64_t m = c->m;
+  const int64_t wmax = std::numeric_limits<W>::max();
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  W* stage = static_cast<W*>(pinned_stage(m * sizeof(W)));
+  W* wd = static_cast<W*>(wdev);
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const int T = m >= (1u << 20) ? (int)hw : 1;
+  std::vector<std::atomic<int>> done(nch);
+  for (auto& d : done) d.store(0);
+  std::atomic<bool> out_of_range{false};
+  const int64_t* w = a->csr_weights;
+  auto span_of = [&](int k) {
+    return std::make_pair(a->csr_offsets[rows[k]], a->csr_offsets[rows[k + 1]]);
+  };
+  auto work = [&](int t) {
+    bool bad = false;
+    for (int k = 0; k < nch; ++k) {
+      const auto [e0, e1] = span_of(k);
+      const uint64_t lo = e0 + (e1 - e0) * t / T, hi = e0 + (e1 - e0) * (t + 1) / T;
+      for (uint64_t i = lo; i < hi; ++i) {
+        const int64_t x = w[i];
+        bad |= x < -wmax || x > wmax;
+        stage[i] = (W)x;
+      }
+      done[k].fetch_add(1, std::memory_order_release);
+    }
+    if (bad) out_of_range.store(true);
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < T; ++t) pool.emplace_back(work, t);
+  std::thread self_worker;
+  if (T == 1)
+    work(0);
+  else
+    self_worker = std::thread(work, 0);
+  for (int k = 0; k < nch; ++k) {
+    while (done[k].load(std::memory_order_acquire) < T) std::this_thread::yield();
+    const auto [e0, e1] = span_of(k);
+    CK(cudaMemcpyAsync(wd + e0, stage + e0, (e1 - e0) * sizeof(W), cudaMemcpyHostToDevice, sc));
+    CK(cudaEventRecord(ew[k], sc));
+    CK(cudaStreamWaitEvent(sw, ew[k], 0));
+    egs::k_relabel_weights<W><<<grid_for((uint64_t)(rows[k + 1] - rows[k]) * 4, c->num_sms),
+                                256, 0, sw>>>(rows[k], rows[k + 1], off64, wd, c->perm, c->off,
+                                              c->edge);
+    CK(cudaGetLastError());
+  }
+  if (self_worker.joinable()) self_worker.join();
+  for (auto& th : pool) th.join();
+  // the staging buffer is re-used by the next upload: wait for its DMA
+  CK(cudaStreamSynchronize(sc));
+  return out_of_range.load();
 }
 
 // Build the relabelled device arena from the reference CSR (host spans),
@@ -275,11 +339,11 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   bool h_stage_bad = false;
   cudaStream_t s = c->stream, sc = c->copy_stream, sw = c->aux_stream;
   const int sms = c->num_sms;
-  DevBuf d_off64, d_dst, d_w32, d_owner, d_key, d_keys, d_val, d_misc, d_tmp, d_ck0, d_cv0,
+  DevBuf d_off64, d_dst, d_wn, d_owner, d_key, d_keys, d_val, d_misc, d_tmp, d_ck0, d_cv0,
       d_ck1;
   uint64_t* off64 = d_off64.alloc<uint64_t>((size_t)n + 1);
   uint32_t* dst = d_dst.alloc<uint32_t>(m);
-  int32_t* w32 = d_w32.alloc<int32_t>(m);
+  void* wn = d_wn.alloc<int32_t>(m);  // narrowed weights (int8/16/32)
   uint8_t* owner = d_owner.alloc<uint8_t>(n);
   unsigned int* misc = d_misc.alloc<unsigned int>(32);  // [0..15] hist, [16] bad
   uint8_t* key = d_key.alloc<uint8_t>(n);
@@ -372,55 +436,15 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   egs::k_col_offsets<<<grid_for(m + 1, sms), 256, 0, s>>>(n, m, ck1, c->coff);
   CK(cudaGetLastError());
 
-  // weights: host threads narrow int64 -> int32 into a pinned staging buffer
-  // chunk by chunk (checking the range), each chunk's DMA and device relabel
-  // queued as soon as it is converted -- while the targets are still on the
-  // wire and the transpose sorts.  Half the weight bytes cross PCIe, always
-  // from pinned memory.
   CK(cudaStreamWaitEvent(sw, e_perm, 0));
   {
-    std::lock_guard<std::mutex> lk(g_stage_mu);
-    int32_t* stage = pinned_stage(m);
-    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-    const int T = m >= (1u << 20) ? (int)hw : 1;
-    std::vector<std::atomic<int>> done(nch);
-    for (auto& d : done) d.store(0);
-    std::atomic<bool> out_of_range{false};
-    const int64_t* w = a->csr_weights;
-    auto work = [&](int t) {
-      bool bad = false;
-      for (int k = 0; k < nch; ++k) {
-        const auto [e0, e1] = span_of(k);
-        const uint64_t lo = e0 + (e1 - e0) * t / T, hi = e0 + (e1 - e0) * (t + 1) / T;
-        for (uint64_t i = lo; i < hi; ++i) {
-          const int64_t x = w[i];
-          bad |= x < -2147483647LL || x > 2147483647LL;
-          stage[i] = (int32_t)x;
-        }
-        done[k].fetch_add(1, std::memory_order_release);
-      }
-      if (bad) out_of_range.store(true);
-    };
-    std::vector<std::thread> pool;
-    for (int t = 1; t < T; ++t) pool.emplace_back(work, t);
-    std::thread self_worker;
-    if (T == 1) work(0);
-    else self_worker = std::thread(work, 0);
-    for (int k = 0; k < nch; ++k) {
-      while (done[k].load(std::memory_order_acquire) < T) std::this_thread::yield();
-      const auto [e0, e1] = span_of(k);
-      CK(cudaMemcpyAsync(w32 + e0, stage + e0, (e1 - e0) * 4, cudaMemcpyHostToDevice, sc));
-      CK(cudaEventRecord(ew[k], sc));
-      CK(cudaStreamWaitEvent(sw, ew[k], 0));
-      egs::k_relabel_weights<<<grid_for((uint64_t)(rows[k + 1] - rows[k]) * 4, sms), 256, 0,
-                               sw>>>(rows[k], rows[k + 1], off64, w32, c->perm, c->off, c->edge);
-      CK(cudaGetLastError());
-    }
-    if (self_worker.joinable()) self_worker.join();
-    for (auto& th : pool) th.join();
-    // the staging buffer is re-used by the next upload: wait for its DMA
-    CK(cudaStreamSynchronize(sc));
-    if (out_of_range.load()) h_stage_bad = true;
+    const int64_t mw = a->max_abs_weight;
+    if (mw <= 127)
+      h_stage_bad = upload_weights<int8_t>(c, a, rows, ew, off64, wn);
+    else if (mw <= 32767)
+      h_stage_bad = upload_weights<int16_t>(c, a, rows, ew, off64, wn);
+    else
+      h_stage_bad = upload_weights<int32_t>(c, a, rows, ew, off64, wn);
   }
   tm.mark("upload + relabel + CSC sort");
   CK(cudaEventRecord(e_tail, sw));
@@ -430,7 +454,7 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   // temporaries go back to the pool in stream order
   d_off64.release();
   d_dst.release();
-  d_w32.release();
+  d_wn.release();
   d_owner.release();
   d_key.release();
   d_keys.release();
@@ -449,7 +473,9 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   cudaEventDestroy(e_perm);
   cudaEventDestroy(e_tail);
   const unsigned int bad = h_misc[16] | (h_stage_bad ? 1u : 0u);
-  if (bad & 1u) throw Fail(EGS_ERR_UNSUPPORTED, "edge weight outside int32 on the device path");
+  if (bad & 1u)
+    throw Fail(a->max_abs_weight > 2147483647LL ? EGS_ERR_UNSUPPORTED : EGS_ERR_INVALID_CONFIG,
+               "edge weight outside int32 on the device path, or beyond max_abs_weight");
   if (bad & 2u) throw Fail(EGS_ERR_INVALID_CONFIG, "edge target out of range");
   c->rb[0] = 0;
   for (int k = 0; k < egs::kNumClasses; ++k) c->rb[k + 1] = c->rb[k] + h_misc[k];
