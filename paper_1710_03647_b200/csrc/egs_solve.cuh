@@ -1627,11 +1627,20 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
     uint32_t* chg = p.chg[(round - 1) & 1];
     if (changed == 0) break;  // a round that raised nothing: least fixpoint
     const bool cert_now = p.certify && round >= next_cert;
+    // without a certificate attempt the next round's mode is known already:
+    // a sparse next round gets its activation in the commit phase (the
+    // activation's top filter may see either the old or the committed value
+    // of a predecessor; a stale one only adds a harmless frontier entry)
+    const bool fuse_act =
+        !cert_now && p.mode != kModeDense &&
+        !(p.mode == kModeAuto && (double)changed * p.avg_in_deg * p.sparse_div >= (double)n);
     begin_phase();
-    if (cert_now)
+    if (cert_now) {
       phase_commit_cert_init<V>(p, chg);  // commit + certificate step 1
-    else
+    } else {
       phase_commit<V>(p, chg);
+      if (fuse_act) phase_activate<V>(p, chg, buf ^ 1, slot_sum());
+    }
     end_phase(1, 0);
     if (round >= p.round_budget) {
       status = 5;
@@ -1695,9 +1704,11 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
         (p.mode == kModeAuto &&
          (certified_any || (double)changed * p.avg_in_deg * p.sparse_div >= (double)n));
     if (!dense) {
-      begin_phase();
-      phase_activate<V>(p, chg, buf ^ 1, slot_sum());
-      end_phase(3);
+      if (!fuse_act) {
+        begin_phase();
+        phase_activate<V>(p, chg, buf ^ 1, slot_sum());
+        end_phase(3);
+      }
       buf ^= 1;
       if (prev_sum(2) == 0) break;  // every changed vertex has only top predecessors
     }

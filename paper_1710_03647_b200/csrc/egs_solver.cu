@@ -747,10 +747,10 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
     static const char* fine[6] = {"", "/commit", "/cert-init", "/cert-dense", "/cert-sparse",
                                   "/cert-apply"};
     for (unsigned k = 1; k < egs::kTraceCap && tr[k]; ++k) {
-      const int code = (int)(tr[k] >> 56) - 1;
-      std::fprintf(stderr, "[egs trace] %3u %-8s%-13s %9.1f us\n", k, names[code / 8 % 4],
-                   fine[code % 8 + 1 < 6 ? code % 8 + 1 : 0],
-                   (tr[k] & ((1ull << 56) - 1)) * 1e-3);
+      const int code = (int)(tr[k] >> 56);  // kind * 8 + fine + 1
+      const int kind = code / 8, f = code % 8;  // f = fine + 1 (0: none)
+      std::fprintf(stderr, "[egs trace] %3u %-8s%-13s %9.1f us\n", k, names[kind % 4],
+                   fine[f < 6 ? f : 0], (tr[k] & ((1ull << 56) - 1)) * 1e-3);
     }
     CK(cudaMemset(c->trace, 0, egs::kTraceCap * 8));
   }
