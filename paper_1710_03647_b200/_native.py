@@ -90,6 +90,7 @@ class GpuOpts(C.Structure):
         ("device", C.c_int32),
         ("certify", C.c_int32),
         ("cert_interval", C.c_int32),
+        ("cert_growth", C.c_int32),
         ("sparse_div", C.c_int32),
         ("grid_ctas", C.c_int32),
         ("no_tma", C.c_int32),
@@ -320,6 +321,7 @@ class SolverOptions:
     workers: int = 1
     certify: bool = True
     cert_interval: int = 1
+    cert_growth: int = 4
     sparse_div: int = 4
     grid_ctas: int = 0
     no_tma: bool = False
@@ -338,6 +340,7 @@ class SolverOptions:
         o.device = int(self.device)
         o.certify = int(bool(self.certify))
         o.cert_interval = int(self.cert_interval)
+        o.cert_growth = int(self.cert_growth)
         o.sparse_div = int(self.sparse_div)
         o.grid_ctas = int(self.grid_ctas)
         o.no_tma = int(bool(self.no_tma) or os.environ.get("EGS_NO_TMA") == "1")

@@ -124,6 +124,7 @@ struct SolveParams {
   int use_tma;
   int certify;
   int cert_interval;
+  int cert_growth;          // interval multiplier after each attempt (4)
   uint32_t sparse_div;      // next round sparse iff est. frontier * div < n
   float avg_in_deg;
   unsigned long long* trace;   // optional: per-phase (kind << 56 | ns) log, kTraceCap entries
@@ -1689,11 +1690,11 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
       const uint32_t cert = prev_sum(0);
       certified_any = cert > 0;
       changed += cert;
-      // geometric schedule: early attempts catch regular climbs (the
-      // canonical configs certify their losing region at round 2-4), later
-      // ones get rarer so a game without a climbing region pays O(log)
-      // attempts
-      K = K * 2 < 64 ? K * 2 : 64;
+      // geometric schedule (rounds 1, 5, 21, 85, ... by default): the first
+      // attempt catches the regular climbs (the canonical configs certify
+      // their losing region at round 1), later ones get rarer so a game
+      // without a climbing region pays O(log) attempts
+      K = K * p.cert_growth < 64 ? K * p.cert_growth : 64;
       next_cert = round + (unsigned long long)K;
     }
 

@@ -232,7 +232,7 @@ void validate_opts(const egs_gpu_opts& o) {
                "egs_gpu_solve drives one GPU; use egs_part_* for n_gpus > 1");
   if (o.mode < EGS_MODE_AUTO || o.mode > EGS_MODE_SPARSE)
     throw Fail(EGS_ERR_INVALID_CONFIG, "mode must be 0, 1 or 2");
-  if (o.cert_interval < 0 || o.sparse_div < 0 || o.grid_ctas < 0)
+  if (o.cert_interval < 0 || o.cert_growth < 0 || o.sparse_div < 0 || o.grid_ctas < 0)
     throw Fail(EGS_ERR_INVALID_CONFIG, "negative tuning knob");
   if (o.timeout_seconds < 0)
     throw Fail(EGS_ERR_INVALID_CONFIG, "timeout must be >= 0");
@@ -646,6 +646,7 @@ egs::SolveParams<V> make_params(egs_ctx* c, unsigned long long* budget_out) {
   p.use_tma = o.no_tma ? 0 : 1;
   p.certify = o.certify;
   p.cert_interval = o.cert_interval > 0 ? o.cert_interval : 1;
+  p.cert_growth = o.cert_growth > 0 ? o.cert_growth : 4;
   p.sparse_div = o.sparse_div > 0 ? (uint32_t)o.sparse_div : 4u;
   p.avg_in_deg = n ? (float)((double)c->m / (double)n) : 1.0f;
   if (p.avg_in_deg < 1.0f) p.avg_in_deg = 1.0f;
@@ -1031,6 +1032,7 @@ void egs_gpu_opts_default(egs_gpu_opts* o) {
   o->device = -1;
   o->certify = 1;
   o->cert_interval = 1;
+  o->cert_growth = 4;
   o->sparse_div = 4;
   o->mode = EGS_MODE_AUTO;
 }

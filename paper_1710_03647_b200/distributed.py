@@ -169,6 +169,7 @@ class PartitionReport:
 
 
 def solve_partitioned(steps, comm, certify: bool = True, cert_interval: int = 1,
+                      cert_growth: int = 4,
                       round_budget: Optional[int] = None,
                       timeout_seconds: float = 0.0) -> PartitionReport:
     """The dense schedule of k_solve (egs_solve.cuh), one step at a time.
@@ -212,7 +213,7 @@ def solve_partitioned(steps, comm, certify: bool = True, cert_interval: int = 1,
             cert = comm.allreduce_sum(step(STEP_CERT_APPLY, parity)[0])
             comm.allgather(steps.f, steps.slice)
             certified += cert
-            K = min(2 * K, 64)  # the geometric schedule of k_solve
+            K = min(cert_growth * K, 64)  # the geometric schedule of k_solve
             next_cert = rounds + K
         parity ^= 1
         changed = comm.allreduce_sum(step(STEP_LIFT, parity)[0])
