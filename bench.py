@@ -68,7 +68,7 @@ def workload_name(cfg):
 
 # ----------------------------------------------------------- clocks ----
 class ClockSampler:
-    """NVML SM clock + throttle reasons sampled every 20 ms while running."""
+    """NVML SM clock + throttle reasons sampled every 5 ms while running."""
 
     REASONS = {
         0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
@@ -98,7 +98,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.02)
+            time.sleep(0.005)
 
     def __enter__(self):
         if self.nv is not None:
@@ -476,7 +476,7 @@ def run_our_arm_partitioned(a):
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="C4", choices=sorted(CONFIGS))
