@@ -215,6 +215,38 @@ def test_round_bound_and_timeout(egs):
     a = egs.GameArena.fixed(10000, 4, 100, 1)
     with pytest.raises(egs.BoundExhaustedError):
         _solve(egs, a, certify=False, sweep_bound=10)
+    # plain value iteration on C1 climbs ~10^4 rounds; a 1 ms budget stops it
+    # on the device (%globaltimer) with the reference's TimeoutError
+    with pytest.raises(egs.TimeoutError_):
+        _solve(egs, a, certify=False, timeout_seconds=0.001)
+    # a context survives a failed solve: the next solve starts clean
+    with egs.DeviceSolver(a, egs.SolverOptions(certify=False, sweep_bound=3)) as ds:
+        for _ in range(2):
+            with pytest.raises(egs.BoundExhaustedError):
+                ds.solve()
+    with egs.DeviceSolver(a) as ds:
+        ds.solve()
+        assert ds.is_fixpoint(ds.read_measure())
+
+
+def test_weight_width_paths(egs, oracle):
+    """Weights travel as int8 / int16 / int32 by max |w|; every width gives
+    the reference's measure, and a weight beyond int32 is refused loudly."""
+    import random
+    for W in (100, 127, 128, 30000, 32768, 10 ** 6, 2 ** 31 - 1):
+        r = random.Random(W)
+        n = 200
+        edges = [(v, r.randrange(n), r.randint(-W, W)) for v in range(n) for _ in range(3)]
+        edges.append((0, 1, W))
+        owners = [v & 1 for v in range(n)]
+        a = egs.GameArena.build(n, edges, owners)
+        assert a.max_abs_weight == W
+        g = oracle.build(n, edges, owners)
+        want, _ = oracle.solve_seq(g)
+        assert np.array_equal(_solve(egs, a).measure, want), W
+    big = egs.GameArena.build(2, [(0, 1, -(2 ** 31)), (1, 0, 5)], [0, 1])
+    with pytest.raises(egs.OverflowError_):
+        _solve(egs, big)
 
 
 def test_empty_and_single_vertex(egs):
