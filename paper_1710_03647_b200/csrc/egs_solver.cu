@@ -202,6 +202,34 @@ struct StepTimer {
   }
 };
 
+// Streams, events and the pinned counter block of finished contexts are
+// kept per device and handed to the next context: a repeated one-shot
+// egs_gpu_solve does not pay their creation (~2-3 ms) again.
+struct Shell {
+  cudaStream_t stream, copy_stream, aux_stream;
+  cudaEvent_t ev[2];
+  unsigned long long* h_ctr;
+};
+std::mutex g_shell_mu;
+std::vector<std::pair<int, Shell>> g_shells;
+
+void shell_put(int device, const Shell& sh) {
+  std::lock_guard<std::mutex> lk(g_shell_mu);
+  g_shells.emplace_back(device, sh);
+}
+
+bool shell_get(int device, Shell& sh) {
+  std::lock_guard<std::mutex> lk(g_shell_mu);
+  for (size_t i = 0; i < g_shells.size(); ++i) {
+    if (g_shells[i].first == device) {
+      sh = g_shells[i].second;
+      g_shells.erase(g_shells.begin() + i);
+      return true;
+    }
+  }
+  return false;
+}
+
 void ctx_free(egs_ctx* c) {
   if (!c) return;
   StepTimer tm(c->stream);
@@ -215,12 +243,19 @@ void ctx_free(egs_ctx* c) {
     cudaStreamSynchronize(c->stream);
   }
   tm.mark("free: device buffers");
-  if (c->h_ctr) cudaFreeHost(c->h_ctr);
-  for (auto& e : c->ev)
-    if (e) cudaEventDestroy(e);
-  if (c->stream) cudaStreamDestroy(c->stream);
-  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
-  if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
+  if (c->stream && c->copy_stream && c->aux_stream && c->h_ctr && c->ev[0] && c->ev[1]) {
+    cudaStreamSynchronize(c->copy_stream);
+    cudaStreamSynchronize(c->aux_stream);
+    shell_put(c->device, Shell{c->stream, c->copy_stream, c->aux_stream, {c->ev[0], c->ev[1]},
+                               c->h_ctr});
+  } else {
+    if (c->h_ctr) cudaFreeHost(c->h_ctr);
+    for (auto& e : c->ev)
+      if (e) cudaEventDestroy(e);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
+  }
   tm.s = nullptr;
   tm.mark("free: host, events, streams");
   delete c;
@@ -508,11 +543,22 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     if (!coop) throw Fail(EGS_ERR_CUDA, "device does not support cooperative launch");
     StepTimer tm0(nullptr);
     use_caching_pool(c->device);
-    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
+    Shell shell;
+    if (shell_get(c->device, shell)) {
+      c->stream = shell.stream;
+      c->copy_stream = shell.copy_stream;
+      c->aux_stream = shell.aux_stream;
+      c->ev[0] = shell.ev[0];
+      c->ev[1] = shell.ev[1];
+      c->h_ctr = shell.h_ctr;
+    } else {
+      CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
+      for (auto& e : c->ev) CK(cudaEventCreate(&e));
+      CK(cudaMallocHost(&c->h_ctr, egs::kNumCounters * sizeof(unsigned long long)));
+    }
     g_alloc_stream = c->stream;
-    for (auto& e : c->ev) CK(cudaEventCreate(&e));
     c->n = a->num_vertices;
     c->m = a->num_edges;
     c->cap = a->credit_cap;
@@ -523,7 +569,6 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     const size_t vsz = c->vbits / 8;
     const size_t words = ((size_t)n + 31) / 32;
 
-    CK(cudaMallocHost(&c->h_ctr, egs::kNumCounters * sizeof(unsigned long long)));
     tm0.mark("create: streams, events, pinned");
     c->ctr = dalloc<unsigned long long>(egs::kNumCounters);
     if (std::getenv("EGS_TRACE")) c->trace = dalloc<unsigned long long>(egs::kTraceCap);
@@ -581,6 +626,12 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     c->full_grid = full;
 
     // Keep the measure resident in L2 while the edge stream goes through.
+    // (A re-used stream may still carry the window of a previous context.)
+    {
+      cudaStreamAttrValue none{};
+      cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &none);
+      cudaGetLastError();
+    }
     int max_win = 0;
     const bool want_win = std::getenv("EGS_NO_L2WIN") == nullptr;
     if (want_win &&
