@@ -115,6 +115,7 @@ struct SolveParams {
   uint32_t* frb;        // frontier membership bitmap
   uint32_t* rbm[2];     // certificate: removed-in-pass bitmaps
   uint32_t* cbm;        // certificate: re-check dedup bitmap
+  uint32_t* longcol;    // activation: queued long CSC columns {vertex, chunk cursor}
   uint32_t* fr[2];      // frontier lists; sublist c starts at cbase[c]
   uint32_t cbase[3];
   Scratch* sh;
@@ -1525,9 +1526,37 @@ __device__ __noinline__ void phase_cert_apply(const SolveParams<V>& p, uint32_t*
 // Activation (solver_par.cpp:402-410): every non-top predecessor of a vertex
 // marked in `chg` enters frontier buffer `nb` once (bitmap dedup), sorted
 // into its size-class sublist; the warp expands CSC columns as one stream.
+// Columns longer than kLongCol (the in-hubs of a power-law arena) are not
+// expanded by one warp: they are queued in p.longcol (count in qlong) for
+// phase_activate_long, which spreads their chunks over the whole grid.
+constexpr uint32_t kLongCol = 4096;
+constexpr uint32_t kColChunk = 1024;
+
+template <class V>
+__device__ __forceinline__ void activate_pred(const SolveParams<V>& p, bool valid, uint32_t idx,
+                                              int nb, Local& L) {
+  const Graph& g = p.g;
+  bool add = false;
+  uint32_t u = 0;
+  int c = 0;
+  if (valid) {
+    ++L.act;
+    u = __ldg(g.csrc + idx);
+    if (gather(p.f + u) != Top<V>::v) {
+      const uint32_t bit = 1u << (u & 31u);
+      add = !(atomicOr(p.frb + (u >> 5), bit) & bit);
+      c = size_class(g, u);
+    }
+  }
+#pragma unroll
+  for (int cc = 0; cc < 3; ++cc)
+    warp_append(add && c == cc, u, p.fr[nb] + p.cbase[cc], &p.sh->fr_cnt[nb][cc]);
+  L.phase_count += add;
+}
+
 template <class V>
 __device__ __noinline__ void phase_activate(const SolveParams<V>& p, const uint32_t* chg,
-                                            int nb, unsigned int* slot_sum) {
+                                            int nb, unsigned int* slot_sum, unsigned int* qlong) {
   __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
   const Graph& g = p.g;
   const uint32_t nwords = (g.n + 31) >> 5;
@@ -1544,25 +1573,44 @@ __device__ __noinline__ void phase_activate(const SolveParams<V>& p, const uint3
         bits &= bits - 1;
         b = __ldg(g.coff + v);
         e = __ldg(g.coff + v + 1);
+        if (e - b > kLongCol) {
+          const uint32_t k = atomicAdd(qlong, 1u);
+          p.longcol[2 * k] = v;
+          p.longcol[2 * k + 1] = 0u;  // this column's chunk cursor
+          e = b;
+        }
       }
       warp_expand(b, e, [&](bool valid, uint32_t idx, uint32_t) {
-        bool add = false;
-        uint32_t u = 0;
-        int c = 0;
-        if (valid) {
-          ++L.act;
-          u = __ldg(g.csrc + idx);
-          if (gather(p.f + u) != Top<V>::v) {
-            const uint32_t bit = 1u << (u & 31u);
-            add = !(atomicOr(p.frb + (u >> 5), bit) & bit);
-            c = size_class(g, u);
-          }
-        }
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc)
-          warp_append(add && c == cc, u, p.fr[nb] + p.cbase[cc], &p.sh->fr_cnt[nb][cc]);
-        L.phase_count += add;
+        activate_pred<V>(p, valid, idx, nb, L);
       });
+    }
+  }
+  block_flush(L, p.ctr, slot_sum + 2, s_cnt);
+}
+
+// The long columns queued by phase_activate: every warp walks the queue and
+// claims kColChunk-entry chunks of each column from its cursor.
+template <class V>
+__device__ __noinline__ void phase_activate_long(const SolveParams<V>& p, int nb,
+                                                 const unsigned int* qlong,
+                                                 unsigned int* slot_sum) {
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  const Graph& g = p.g;
+  Local L;
+  const uint32_t ncols = vload(qlong);
+  for (uint32_t k = 0; k < ncols; ++k) {
+    const uint32_t v = ldcg(p.longcol + 2 * k);
+    const uint32_t b = __ldg(g.coff + v), e = __ldg(g.coff + v + 1);
+    const uint32_t nch = (e - b + kColChunk - 1) / kColChunk;
+    for (;;) {
+      uint32_t c = 0;
+      if (lane_id() == 0) c = atomicAdd(p.longcol + 2 * k + 1, 1u);
+      c = __shfl_sync(0xffffffffu, c, 0);
+      if (c >= nch) break;
+      const uint32_t cb = b + c * kColChunk;
+      const uint32_t ce = cb + kColChunk < e ? cb + kColChunk : e;
+      for (uint32_t i0 = cb; i0 < ce; i0 += 32)
+        activate_pred<V>(p, i0 + lane_id() < ce, i0 + lane_id(), nb, L);
     }
   }
   block_flush(L, p.ctr, slot_sum + 2, s_cnt);
@@ -1640,7 +1688,7 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
       phase_commit_cert_init<V>(p, chg);  // commit + certificate step 1
     } else {
       phase_commit<V>(p, chg);
-      if (fuse_act) phase_activate<V>(p, chg, buf ^ 1, slot_sum());
+      if (fuse_act) phase_activate<V>(p, chg, buf ^ 1, slot_sum(), slot_dyn() + 2);
     }
     end_phase(1, 0);
     if (round >= p.round_budget) {
@@ -1707,11 +1755,19 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
     if (!dense) {
       if (!fuse_act) {
         begin_phase();
-        phase_activate<V>(p, chg, buf ^ 1, slot_sum());
+        phase_activate<V>(p, chg, buf ^ 1, slot_sum(), slot_dyn() + 2);
         end_phase(3);
       }
+      uint32_t frontier = prev_sum(2);
+      const unsigned int* qlong = sh->dyn[(phase - 1) & 3] + 2;
+      if (vload(qlong) > 0) {  // in-hub columns: one more phase, chunks over the grid
+        begin_phase();
+        phase_activate_long<V>(p, buf ^ 1, qlong, slot_sum());
+        end_phase(3);
+        frontier += prev_sum(2);
+      }
       buf ^= 1;
-      if (prev_sum(2) == 0) break;  // every changed vertex has only top predecessors
+      if (frontier == 0) break;  // every changed vertex has only top predecessors
     }
 
     // ---- lift round `round + 1`

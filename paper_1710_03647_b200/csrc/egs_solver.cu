@@ -154,6 +154,7 @@ struct egs_ctx {
   uint32_t* frb = nullptr;
   uint32_t* rbm[2] = {nullptr, nullptr};
   uint32_t* cbm = nullptr;
+  uint32_t* longcol = nullptr;
   uint32_t* fr[2] = {nullptr, nullptr};
   void* stage = nullptr;
   egs::Scratch* scratch = nullptr;
@@ -236,7 +237,7 @@ void ctx_free(egs_ctx* c) {
   if (c->device >= 0) cudaSetDevice(c->device);
   void* ptrs[] = {c->off,    c->edge,   c->coff, c->csrc,  c->perm, c->inv,
                   c->f,      c->wit,    c->chg[0], c->chg[1], c->frb,
-                  c->fr[0],  c->fr[1],  c->stage, c->scratch, c->ctr, c->rbm[0], c->rbm[1], c->cbm, c->trace,
+                  c->fr[0],  c->fr[1],  c->stage, c->scratch, c->ctr, c->rbm[0], c->rbm[1], c->cbm, c->trace, c->longcol,
                   c->f64};
   if (c->stream) {
     for (void* p : ptrs) dfree(p, c->stream);
@@ -586,6 +587,8 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     c->rbm[0] = dalloc<uint32_t>(words);
     c->rbm[1] = dalloc<uint32_t>(words);
     c->cbm = dalloc<uint32_t>(words);
+    // at most m / kLongCol columns are longer than kLongCol
+    c->longcol = dalloc<uint32_t>(2 * (a->num_edges / egs::kLongCol + 1));
     c->fr[0] = dalloc<uint32_t>(n);
     c->fr[1] = dalloc<uint32_t>(n);
     c->stage = dalloc<uint8_t>((size_t)std::max<uint32_t>(c->n_pad, 1) * vsz);
@@ -684,6 +687,7 @@ egs::SolveParams<V> make_params(egs_ctx* c, unsigned long long* budget_out) {
   p.rbm[0] = c->rbm[0];
   p.rbm[1] = c->rbm[1];
   p.cbm = c->cbm;
+  p.longcol = c->longcol;
   p.fr[0] = c->fr[0];
   p.fr[1] = c->fr[1];
   p.cbase[0] = 0;
