@@ -1532,9 +1532,59 @@ __device__ __noinline__ void phase_cert_apply(const SolveParams<V>& p, uint32_t*
 constexpr uint32_t kLongCol = 4096;
 constexpr uint32_t kColChunk = 1024;
 
+// Frontier appends are buffered per warp in shared memory (the TMA stage
+// area, idle during activation) and published up to kAppendCap entries per
+// atomicAdd, so a large frontier does not serialise on the three list
+// counters.  Warp-uniform.
+constexpr uint32_t kAppendCap = 512;  // entries per class per warp (3 * 2 KB)
+
+struct WarpLists {
+  uint32_t* buf[3];
+  uint32_t cnt[3];
+};
+
+__device__ __forceinline__ WarpLists warp_lists() {
+  extern __shared__ __align__(128) int2 dsm[];
+  uint32_t* base = reinterpret_cast<uint32_t*>(dsm) +
+                   (size_t)(threadIdx.x >> 5) * (kStages * kStageRecs * 2);
+  WarpLists q;
+  for (int c = 0; c < 3; ++c) {
+    q.buf[c] = base + c * kAppendCap;
+    q.cnt[c] = 0;
+  }
+  return q;
+}
+
+__device__ __forceinline__ void lists_flush(WarpLists& q, int c, uint32_t* list,
+                                            unsigned int* count) {
+  __syncwarp();
+  const uint32_t k = q.cnt[c];
+  if (k == 0) return;
+  uint32_t base = 0;
+  if (lane_id() == 0) base = atomicAdd(count, k);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  for (uint32_t i = lane_id(); i < k; i += 32) list[base + i] = q.buf[c][i];
+  q.cnt[c] = 0;
+  __syncwarp();
+}
+
+__device__ __forceinline__ void lists_append(WarpLists& q, bool pred, int c, uint32_t v,
+                                             uint32_t* const* lists, unsigned int* counts) {
+#pragma unroll
+  for (int cc = 0; cc < 3; ++cc) {
+    const bool mine = pred && c == cc;
+    const uint32_t m = __ballot_sync(0xffffffffu, mine);
+    if (!m) continue;
+    if (mine) q.buf[cc][q.cnt[cc] + __popc(m & lanemask_lt())] = v;
+    q.cnt[cc] += __popc(m);
+    if (q.cnt[cc] + 32 > kAppendCap) lists_flush(q, cc, lists[cc], counts + cc);
+  }
+}
+
 template <class V>
 __device__ __forceinline__ void activate_pred(const SolveParams<V>& p, bool valid, uint32_t idx,
-                                              int nb, Local& L) {
+                                              WarpLists& q, uint32_t* const* lists,
+                                              unsigned int* counts, Local& L) {
   const Graph& g = p.g;
   bool add = false;
   uint32_t u = 0;
@@ -1542,15 +1592,15 @@ __device__ __forceinline__ void activate_pred(const SolveParams<V>& p, bool vali
   if (valid) {
     ++L.act;
     u = __ldg(g.csrc + idx);
-    if (gather(p.f + u) != Top<V>::v) {
-      const uint32_t bit = 1u << (u & 31u);
+    const uint32_t bit = 1u << (u & 31u);
+    // a plain read first: predecessors shared by many changed vertices (the
+    // in-hubs' neighbours) are already marked and skip the atomic
+    if (!(ldcg(p.frb + (u >> 5)) & bit) && gather(p.f + u) != Top<V>::v) {
       add = !(atomicOr(p.frb + (u >> 5), bit) & bit);
       c = size_class(g, u);
     }
   }
-#pragma unroll
-  for (int cc = 0; cc < 3; ++cc)
-    warp_append(add && c == cc, u, p.fr[nb] + p.cbase[cc], &p.sh->fr_cnt[nb][cc]);
+  lists_append(q, add, c, u, lists, counts);
   L.phase_count += add;
 }
 
@@ -1563,6 +1613,10 @@ __device__ __noinline__ void phase_activate(const SolveParams<V>& p, const uint3
   const uint32_t nwarps = gridDim.x * kWarps;
   const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5;
   Local L;
+  WarpLists q = warp_lists();
+  uint32_t* const lists[3] = {p.fr[nb] + p.cbase[0], p.fr[nb] + p.cbase[1],
+                              p.fr[nb] + p.cbase[2]};
+  unsigned int* counts = p.sh->fr_cnt[nb];
   for (uint32_t w0 = gw * 32; w0 < nwords; w0 += nwarps * 32) {
     const uint32_t wi = w0 + lane_id();
     uint32_t bits = wi < nwords ? ldcg(chg + wi) : 0u;
@@ -1581,10 +1635,11 @@ __device__ __noinline__ void phase_activate(const SolveParams<V>& p, const uint3
         }
       }
       warp_expand(b, e, [&](bool valid, uint32_t idx, uint32_t) {
-        activate_pred<V>(p, valid, idx, nb, L);
+        activate_pred<V>(p, valid, idx, q, lists, counts, L);
       });
     }
   }
+  for (int c = 0; c < 3; ++c) lists_flush(q, c, lists[c], counts + c);
   block_flush(L, p.ctr, slot_sum + 2, s_cnt);
 }
 
@@ -1597,6 +1652,10 @@ __device__ __noinline__ void phase_activate_long(const SolveParams<V>& p, int nb
   __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
   const Graph& g = p.g;
   Local L;
+  WarpLists q = warp_lists();
+  uint32_t* const lists[3] = {p.fr[nb] + p.cbase[0], p.fr[nb] + p.cbase[1],
+                              p.fr[nb] + p.cbase[2]};
+  unsigned int* counts = p.sh->fr_cnt[nb];
   const uint32_t ncols = vload(qlong);
   for (uint32_t k = 0; k < ncols; ++k) {
     const uint32_t v = ldcg(p.longcol + 2 * k);
@@ -1610,9 +1669,10 @@ __device__ __noinline__ void phase_activate_long(const SolveParams<V>& p, int nb
       const uint32_t cb = b + c * kColChunk;
       const uint32_t ce = cb + kColChunk < e ? cb + kColChunk : e;
       for (uint32_t i0 = cb; i0 < ce; i0 += 32)
-        activate_pred<V>(p, i0 + lane_id() < ce, i0 + lane_id(), nb, L);
+        activate_pred<V>(p, i0 + lane_id() < ce, i0 + lane_id(), q, lists, counts, L);
     }
   }
+  for (int c = 0; c < 3; ++c) lists_flush(q, c, lists[c], counts + c);
   block_flush(L, p.ctr, slot_sum + 2, s_cnt);
 }
 
