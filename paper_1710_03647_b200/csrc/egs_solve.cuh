@@ -1088,19 +1088,34 @@ __device__ __noinline__ void round1_long(const SolveParams<V>& p, uint32_t* chg,
     if (!owned(p, u)) continue;
     const bool p0 = u < g.rb[kP1L];
     const uint32_t b = __ldg(g.off + u), e = __ldg(g.off + u + 1);
-    int minw = INT32_MAX, maxw = INT32_MIN;
-    uint32_t imax = b;
-    for (uint32_t i0 = b; i0 < e; i0 += 32) {
-      const uint32_t i = i0 + lane;
-      const int w = i < e ? __ldcs(&g.edge[i].y) : INT32_MAX;
-      minw = min(minw, __reduce_min_sync(0xffffffffu, w));
-      const int cmax = __reduce_max_sync(0xffffffffu, i < e ? w : INT32_MIN);
-      if (cmax > maxw) {
-        maxw = cmax;
-        imax = i0 + __ffs(__ballot_sync(0xffffffffu, i < e && w == cmax)) - 1;
+    // per-lane min / max / argmax over a 128-edge stride (4 independent
+    // loads in flight), one warp reduction at the end
+    int lmin = INT32_MAX, lmax = INT32_MIN;
+    uint32_t limax = b;
+    for (uint32_t i0 = b; i0 < e; i0 += 128) {
+      int wv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t i = i0 + k * 32 + lane;
+        wv[k] = i < e ? __ldcs(&g.edge[i].y) : INT32_MIN;
       }
-      if (p0 && maxw >= 0) break;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t i = i0 + k * 32 + lane;
+        if (i < e) {
+          lmin = min(lmin, wv[k]);
+          if (wv[k] > lmax) {
+            lmax = wv[k];
+            limax = i;
+          }
+        }
+      }
+      if (p0 && __any_sync(0xffffffffu, lmax >= 0)) break;  // a satisfied move
     }
+    const int minw = __reduce_min_sync(0xffffffffu, lmin);
+    const int maxw = __reduce_max_sync(0xffffffffu, lmax);
+    const uint32_t imax = __shfl_sync(0xffffffffu, limax,
+                                      __ffs(__ballot_sync(0xffffffffu, lmax == maxw)) - 1);
     if (lane == 0) {
       V val;
       round1_finish<V>(p, u, p0, minw, maxw, imax, val);
