@@ -21,13 +21,22 @@ REF_LIB    := oracle/_ref/libegsolve_ref.so
 
 all: $(LIB) $(ORACLE_LIB) $(ORACLE_CLI) ref
 
-$(CSRC)/egs_solver.o: $(CSRC)/egs_solver.cu $(CSRC)/egs_solve.cuh $(CSRC)/egs_build.cuh $(CSRC)/egs_device.cuh include/egs_gpu.h
+HDRS := $(CSRC)/egs_types.cuh $(CSRC)/egs_device.cuh include/egs_gpu.h
+
+$(CSRC)/egs_solver.o: $(CSRC)/egs_solver.cu $(CSRC)/egs_build.cuh $(HDRS)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/egs_solver.ptxas.log || (cat $(CSRC)/egs_solver.ptxas.log; false)
+
+# the solve kernels, once per edge-record format (8-byte int2 / packed 4-byte)
+$(CSRC)/egs_kern_e8.o: $(CSRC)/egs_kern.cu $(CSRC)/egs_solve.cuh $(HDRS)
+	$(NVCC) $(NVFLAGS) -DEGS_EDGE_BYTES=8 -DEGS_FMT_NS=e8 -c $< -o $@ 2> $(CSRC)/egs_kern_e8.ptxas.log || (cat $(CSRC)/egs_kern_e8.ptxas.log; false)
+
+$(CSRC)/egs_kern_e4.o: $(CSRC)/egs_kern.cu $(CSRC)/egs_solve.cuh $(HDRS)
+	$(NVCC) $(NVFLAGS) -DEGS_EDGE_BYTES=4 -DEGS_FMT_NS=e4 -c $< -o $@ 2> $(CSRC)/egs_kern_e4.ptxas.log || (cat $(CSRC)/egs_kern_e4.ptxas.log; false)
 
 $(CSRC)/egs_host.o: $(CSRC)/egs_host.cpp include/egs_gpu.h
 	$(CXX) -O3 -std=c++17 -fPIC -Iinclude -I/usr/local/cuda/include -c $< -o $@
 
-$(LIB): $(CSRC)/egs_solver.o $(CSRC)/egs_host.o
+$(LIB): $(CSRC)/egs_solver.o $(CSRC)/egs_kern_e8.o $(CSRC)/egs_kern_e4.o $(CSRC)/egs_host.o
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -lpthread
 
 $(ORACLE_LIB): oracle/egs_oracle.c oracle/egs_oracle.h

@@ -120,6 +120,8 @@ typedef struct egs_gpu_stats {
                                  light player-1 rows, sparse light rows */
   double phase_detail_seconds[5]; /* device time of: commit phases, certificate
                                      init, dense passes, sparse passes, apply */
+  uint32_t edge_bytes;     /* 4 (packed dst | w << target bits) or 8 ({dst, w}) */
+  uint32_t reserved0;
 } egs_gpu_stats;
 
 void egs_gpu_opts_default(egs_gpu_opts* opts);

@@ -5,7 +5,8 @@
 //   * vertices relabelled into six contiguous ranges by (owner, out-degree
 //     class): the owner-sorted order of reorder_by_owner (arena.cpp:119-149;
 //     PAPER.md:506-511) refined by row length, stable inside each range;
-//   * rows re-packed as 8-byte edge records {u32 dst (relabelled), i32 w}
+//   * rows re-packed as edge records: 4-byte packed {dst | w << tbits} when
+//     every weight fits beside the target bits, else 8-byte {u32 dst, i32 w}
 //     (weights are validated to fit int32; arena.hpp:13 stores int64);
 //   * the predecessor transpose (CSC, arena.cpp:56-74; the paper's CUSPARSE
 //     csr2csc) built by a radix sort of (dst, src) pairs.
@@ -16,7 +17,7 @@
 #include <cstdint>
 
 #include "egs_device.cuh"
-#include "egs_solve.cuh"
+#include "egs_types.cuh"
 
 namespace egs {
 
@@ -60,10 +61,12 @@ __global__ void k_permute(uint32_t n, const uint32_t* inv, const uint64_t* off64
 __global__ void __launch_bounds__(256)
     k_relabel_targets(uint32_t n, uint32_t r0, uint32_t r1, const uint64_t* off64,
                       const uint32_t* dst, const uint32_t* perm, const uint32_t* off_new,
-                      int2* edge, uint32_t* ckey, uint32_t* cval, unsigned int* bad) {
+                      void* edge, uint32_t tbits, uint32_t* ckey, uint32_t* cval,
+                      unsigned int* bad) {
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int* ex = reinterpret_cast<int*>(edge);
+  int* ex = static_cast<int*>(edge);
+  uint32_t* px = static_cast<uint32_t*>(edge);
   unsigned int flag = 0;
   for (uint32_t o0 = r0 + gw * 32; o0 < r1; o0 += nwarps * 32) {
     const uint32_t o = o0 + lane_id();
@@ -82,7 +85,10 @@ __global__ void __launch_bounds__(256)
         const uint32_t t0 = dst[idx];
         if (t0 >= n) flag |= 2u;
         const uint32_t t = perm[t0 < n ? t0 : 0];
-        ex[2 * (size_t)pos] = (int)t;
+        if (tbits)
+          px[pos] = t;  // the weight half is or-ed in by k_relabel_weights
+        else
+          ex[2 * (size_t)pos] = (int)t;
         ckey[pos] = t;
         cval[pos] = src;
       }
@@ -98,10 +104,12 @@ __global__ void __launch_bounds__(256)
 template <class W>
 __global__ void __launch_bounds__(256)
     k_relabel_weights(uint32_t r0, uint32_t r1, const uint64_t* off64, const W* wn,
-                      const uint32_t* perm, const uint32_t* off_new, int2* edge) {
+                      const uint32_t* perm, const uint32_t* off_new, void* edge,
+                      uint32_t tbits) {
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int* ex = reinterpret_cast<int*>(edge);
+  int* ex = static_cast<int*>(edge);
+  uint32_t* px = static_cast<uint32_t*>(edge);
   for (uint32_t o0 = r0 + gw * 32; o0 < r1; o0 += nwarps * 32) {
     const uint32_t o = o0 + lane_id();
     uint32_t b = 0, e = 0, delta = 0;
@@ -112,7 +120,12 @@ __global__ void __launch_bounds__(256)
     }
     warp_expand(b, e, [&](bool valid, uint32_t idx, uint32_t owner_lane) {
       const uint32_t d = __shfl_sync(0xffffffffu, delta, owner_lane);
-      if (valid) ex[2 * (size_t)(idx + d) + 1] = (int)wn[idx];
+      if (valid) {
+        if (tbits)  // after k_relabel_targets of the same rows (stream order)
+          px[idx + d] |= (uint32_t)(int)wn[idx] << tbits;
+        else
+          ex[2 * (size_t)(idx + d) + 1] = (int)wn[idx];
+      }
     });
   }
 }
@@ -177,7 +190,7 @@ __global__ void __launch_bounds__(256)
       const uint32_t i = i0 + lane_id();
       bool sat = true;  // f(v) >= f(t) ⊖ w on this edge
       if (i < e) {
-        const int2 r = g.edge[i];
+        const int2 r = edge_at(g, i);
         sat = fv >= ominus_raw(f[r.x], r.y, overflow);
       }
       if (p0) {
@@ -209,7 +222,7 @@ __global__ void __launch_bounds__(256)
     const uint32_t b = g.off[v], e = g.off[v + 1];
     int64_t acc = p0 ? INT64_MAX : 0;
     for (uint32_t i = b + lane_id(); i < e; i += 32) {
-      const int2 r = g.edge[i];
+      const int2 r = edge_at(g, i);
       const int64_t ft = f[r.x];
       int64_t c = ft == INT64_MAX ? INT64_MAX : ft - (int64_t)r.y;
       if (c != INT64_MAX) {
@@ -255,7 +268,7 @@ __global__ void __launch_bounds__(256)
         bool sat = false;
         int2 r = make_int2(0, 0);
         if (i < e) {
-          r = g.edge[i];
+          r = edge_at(g, i);
           sat = fv >= ominus_raw(raw_of<V>(f[r.x]), r.y, err);
         }
         const uint32_t m = __ballot_sync(0xffffffffu, sat);

@@ -36,102 +36,80 @@
 #include <cstdint>
 
 #include "egs_device.cuh"
+#include "egs_types.cuh"
+
+#ifndef EGS_EDGE_BYTES
+#define EGS_EDGE_BYTES 8
+#endif
+#ifndef EGS_FMT_NS
+#define EGS_FMT_NS e8
+#endif
 
 namespace egs {
+namespace EGS_FMT_NS {
 
 namespace cg = cooperative_groups;
 
-constexpr int kBlock = 256;
-constexpr int kWarps = kBlock / 32;
-constexpr uint32_t kLightMax = 32;    // rows with <= 32 edges: one thread
-constexpr uint32_t kMediumMax = 4096; // <= 4096: one warp; longer: one CTA
-
-// Class ranges of the relabelled ids.
-enum : int { kP0L = 0, kP0M, kP0H, kP1L, kP1M, kP1H, kNumClasses };
-
-enum Counter : int {
-  kLifts = 0,      // lifts that raised a value (SolveReport::lifts)
-  kApps,           // full lift applications (row scans)
-  kEdges,          // edges relaxed = sum of out-degrees of applications
-  kWitness,        // player-0 lifts skipped by a satisfied witness edge
-  kActScanned,     // predecessor slots scanned by activation
-  kCertified,      // vertices proven losing by the certificate
-  kPops,           // sparse-round frontier entries
-  kCertScanned,    // rows visited by certificate passes
-  kCertEdges,      // edges evaluated by certificate passes
-  kVisits,         // vertices examined by lift phases (incl. top skips)
-  kRounds,
-  kDenseRounds,
-  kSparseRounds,
-  kCertAttempts,
-  kCertPasses,
-  kStatus,         // 0 fixpoint, 2 timeout, 5 round budget
-  kTimeSeed,       // ns of device time per phase kind (%globaltimer)
-  kTimeLift,
-  kTimeCert,
-  kTimeAct,
-  kSubHeavy,       // ns summed over CTAs inside each lift sub-phase
-  kSubMedium,
-  kSubLightP0,
-  kSubLightP1,
-  kSubSparseLight,
-  kFineCommit,     // ns of device time: commit, certificate init / dense pass /
-  kFineCertInit,   // sparse pass (mark + check) / apply
-  kFineCertDense,
-  kFineCertSparse,
-  kFineCertApply,
-  kNumCounters
-};
-
-enum Mode : int { kModeAuto = 0, kModeDense = 1, kModeSparse = 2 };
-constexpr unsigned kTraceCap = 512;
-
-struct Graph {
-  uint32_t n;
-  uint32_t rb[kNumClasses + 1];  // class k = [rb[k], rb[k+1])
-  const uint32_t* off;           // n+1 CSR row offsets (relabelled rows)
-  const int2* edge;              // m   {dst (relabelled), w}
-  const uint32_t* coff;          // n+1 CSC column offsets
-  const uint32_t* csrc;          // m   predecessors (relabelled)
-  int64_t cap;                   // credit_cap (M_G)
-};
-
-// Grid-shared scratch; the host zeroes it before each launch.
-struct Scratch {
-  unsigned int sum[4][4];    // per-phase-slot sums: 0 changed, 1 removed, 2 seeds
-  unsigned int dyn[4][4];    // per-phase-slot work cursors: 0 medium, 1 heavy
-  unsigned int fr_cnt[2][3]; // frontier sublist sizes [buffer][L, M, H]
-  unsigned int stop;         // timeout flag
-};
-
+// ---- the edge-record format of this translation unit (egs_types.cuh)
+#if EGS_EDGE_BYTES == 4
+using ERec = uint32_t;
+__device__ __forceinline__ int2 dec(const Graph& g, ERec r) { return edge_dec(r, g.tbits); }
+__device__ __forceinline__ ERec enc(const Graph& g, int2 e) {
+  return (uint32_t)e.x | ((uint32_t)e.y << g.tbits);
+}
+__device__ __forceinline__ int rec_w(const Graph& g, ERec r) { return (int)r >> g.tbits; }
+#else
+using ERec = int2;
+__device__ __forceinline__ int2 dec(const Graph&, ERec r) { return r; }
+__device__ __forceinline__ ERec enc(const Graph&, int2 e) { return e; }
+__device__ __forceinline__ int rec_w(const Graph&, ERec r) { return r.y; }
+#endif
+__device__ __forceinline__ const ERec* erecs(const Graph& g) {
+  return static_cast<const ERec*>(g.edge);
+}
+// streaming (evict-first) load of edge i, decoded
+__device__ __forceinline__ int2 ld_rec(const Graph& g, uint32_t i) {
+  return dec(g, __ldcs(erecs(g) + i));
+}
 template <class V>
-struct SolveParams {
-  Graph g;
-  V* f;                 // measure, relabelled ids (read-only inside a lift round)
-  V* stage;             // lift rounds: raised values, committed after the round;
-                        // certificate: candidate values (f, or kNotCand)
-  int2* wit;            // player-0 witness edge record (ids < rb[3])
-  uint32_t* chg[2];     // changed-vertex bitmaps, by round parity
-  uint32_t* frb;        // frontier membership bitmap
-  uint32_t* rbm[2];     // certificate: removed-in-pass bitmaps
-  uint32_t* cbm;        // certificate: re-check dedup bitmap
-  uint32_t* longcol;    // activation: queued long CSC columns {vertex, chunk cursor}
-  uint32_t* fr[2];      // frontier lists; sublist c starts at cbase[c]
-  uint32_t cbase[3];
-  Scratch* sh;
-  unsigned long long* ctr;  // kNumCounters
-  uint32_t own_lo, own_hi;  // vertex range this GPU lifts (multi-GPU); [0, n) alone
-  int mode;
-  int use_tma;
-  int certify;
-  int cert_interval;
-  int cert_growth;          // interval multiplier after each attempt (4)
-  uint32_t sparse_div;      // next round sparse iff est. frontier * div < n
-  float avg_in_deg;
-  unsigned long long* trace;   // optional: per-phase (kind << 56 | ns) log, kTraceCap entries
-  unsigned long long round_budget;
-  unsigned long long timeout_ns;   // 0 = none; measured from kernel start
-};
+__device__ __forceinline__ ERec* wit_of(const SolveParams<V>& p) {
+  return static_cast<ERec*>(p.wit);
+}
+template <class V>
+__device__ __forceinline__ int2 ld_wit(const SolveParams<V>& p, uint32_t v) {
+  return dec(p.g, ldcg(wit_of(p) + v));
+}
+template <class V>
+__device__ __forceinline__ void st_wit(const SolveParams<V>& p, uint32_t v, int2 e) {
+  stcg(wit_of(p) + v, enc(p.g, e));
+}
+
+// ---- class ranges and the owned vertex range (multi-GPU)
+__device__ __forceinline__ int size_class(const Graph& g, uint32_t v) {
+  if (v < g.rb[kP1L]) return v >= g.rb[kP0H] ? 2 : v >= g.rb[kP0M] ? 1 : 0;
+  return v >= g.rb[kP1H] ? 2 : v >= g.rb[kP1M] ? 1 : 0;
+}
+// i-th vertex of the union of the player-0 and player-1 ranges of class c
+__device__ __forceinline__ uint32_t class_item(const Graph& g, int c, uint32_t i) {
+  const uint32_t n0 = g.rb[c + 1] - g.rb[c];
+  return i < n0 ? g.rb[c] + i : g.rb[c + 3] + (i - n0);
+}
+__device__ __forceinline__ uint32_t class_size(const Graph& g, int c) {
+  return (g.rb[c + 1] - g.rb[c]) + (g.rb[c + 4] - g.rb[c + 3]);
+}
+template <class V>
+__device__ __forceinline__ bool owned(const SolveParams<V>& p, uint32_t v) {
+  return v >= p.own_lo && v < p.own_hi;
+}
+template <class V>
+__device__ __forceinline__ uint32_t clip_lo(const SolveParams<V>& p, uint32_t lo) {
+  return lo > p.own_lo ? lo : p.own_lo;
+}
+template <class V>
+__device__ __forceinline__ uint32_t clip_hi(const SolveParams<V>& p, uint32_t hi) {
+  return hi < p.own_hi ? hi : p.own_hi;
+}
+
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -217,7 +195,7 @@ __device__ __forceinline__ bool lift_thread(const SolveParams<V>& p, uint32_t v,
   const V old = ldcg(p.f + v);
   if (old == TOP) return false;
   if (P0) {
-    const int2 we = ldcg(p.wit + v);
+    const int2 we = ld_wit(p, v);
     if (old >= ominus_cap<V>(gather(p.f + we.x), we.y, p.g.cap)) {
       ++L.witness;
       return false;
@@ -234,7 +212,7 @@ __device__ __forceinline__ bool lift_thread(const SolveParams<V>& p, uint32_t v,
   for (uint32_t i = b; i < e; i += kChunk) {
     int2 r[kChunk];
 #pragma unroll
-    for (int k = 0; k < kChunk; ++k) r[k] = ld_edge(p.g.edge + min(i + k, e - 1));
+    for (int k = 0; k < kChunk; ++k) r[k] = ld_rec(p.g, min(i + k, e - 1));
     V c[kChunk];
 #pragma unroll
     for (int k = 0; k < kChunk; ++k) c[k] = gather(p.f + r[k].x);
@@ -255,7 +233,7 @@ __device__ __forceinline__ bool lift_thread(const SolveParams<V>& p, uint32_t v,
     }
     if (P0 ? acc == V(0) : acc == TOP) break;  // raw_lift early exits (:41,46)
   }
-  if (P0) stcg(p.wit + v, best);
+  if (P0) st_wit(p, v, best);
   if (acc > old) {
     stcg(p.stage + v, acc);
     ++L.lifts;
@@ -276,7 +254,7 @@ __device__ __forceinline__ bool lift_warp(const SolveParams<V>& p, uint32_t v,
   if (P0) {
     bool sat = false;
     if (lane == 0) {
-      const int2 we = ldcg(p.wit + v);
+      const int2 we = ld_wit(p, v);
       sat = old >= ominus_cap<V>(gather(p.f + we.x), we.y, p.g.cap);
     }
     if (__shfl_sync(0xffffffffu, sat, 0)) {
@@ -298,7 +276,7 @@ __device__ __forceinline__ bool lift_warp(const SolveParams<V>& p, uint32_t v,
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const uint32_t i = i0 + k * 32 + lane;
-      if (i < e) r[k] = ld_edge(p.g.edge + i);
+      if (i < e) r[k] = ld_rec(p.g, i);
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -332,7 +310,7 @@ __device__ __forceinline__ bool lift_warp(const SolveParams<V>& p, uint32_t v,
     best.y = __shfl_sync(0xffffffffu, best.y, src);
   }
   if (lane == 0) {
-    if (P0) stcg(p.wit + v, best);
+    if (P0) st_wit(p, v, best);
     if (res > old) {
       stcg(p.stage + v, res);
       ++L.lifts;
@@ -363,7 +341,7 @@ __device__ __forceinline__ bool lift_block(const SolveParams<V>& p, uint32_t v,
   if (P0) {
     __syncthreads();
     if (threadIdx.x == 0) {
-      const int2 we = ldcg(p.wit + v);
+      const int2 we = ld_wit(p, v);
       s.flag = old >= ominus_cap<V>(gather(p.f + we.x), we.y, p.g.cap);
     }
     __syncthreads();
@@ -386,7 +364,7 @@ __device__ __forceinline__ bool lift_block(const SolveParams<V>& p, uint32_t v,
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const uint32_t i = i0 + k * kBlock + threadIdx.x;
-      if (i < e) r[k] = ld_edge(p.g.edge + i);
+      if (i < e) r[k] = ld_rec(p.g, i);
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -437,7 +415,7 @@ __device__ __forceinline__ bool lift_block(const SolveParams<V>& p, uint32_t v,
         rec = s.rec[w];
       }
     }
-    if (P0) stcg(p.wit + v, rec);
+    if (P0) st_wit(p, v, rec);
     if (res > old) {
       stcg(p.stage + v, res);
       ++L.lifts;
@@ -506,9 +484,9 @@ __device__ __noinline__ void dense_light(const SolveParams<V>& p, uint32_t lo,
 // path.  Tiles whose vertices are all at top are skipped without a copy.
 // Each lane then lifts its own row from shared memory (reads rotated by
 // lane, so a half-warp hits distinct banks).
-constexpr uint32_t kStageRecs = 512;  // 4 KB of edge records per warp stage
-constexpr uint32_t kStages = 2;
-constexpr size_t kLiftSmemBytes = (size_t)kWarps * kStages * kStageRecs * sizeof(int2);
+constexpr uint32_t kStageRecs = kStageBytes / sizeof(ERec);  // 4 KB per warp stage
+// bulk copies move 16-byte multiples from 16-byte aligned addresses
+constexpr uint32_t kRecAlign = 16 / sizeof(ERec);
 
 // Per-warp stage barriers live for the whole persistent launch: initialised
 // once by k_solve, their phase parity carried across rounds.
@@ -526,18 +504,22 @@ __device__ __forceinline__ void tma_init_barriers() {
 }
 
 // The TMA tile pipeline of one warp over the aligned 32-vertex words of
-// [lo, hi): `need(v, aux)` says whether vertex v's row must be read (and
-// fills a per-lane value carried to the row step), `row(v, rec, len, b, aux)`
-// processes a row held in shared memory, `fallback(v, aux)` a row whose tile
-// span does not fit a stage (direct loads).  Both return "raised"; raised
-// vertices are published in `chg` with one atomicOr per word.
-template <class V, class Need, class Row, class Fallback>
+// [lo, hi): `load(v, aux)` issues the loads of vertex v's state into a
+// per-lane value carried to the row step, `test(v, aux)` says whether v's
+// row must be read, `row(v, rec, len, b, aux)` processes a row held in
+// shared memory, `fallback(v, aux)` a row whose tile span does not fit a
+// stage (direct loads).  Both return "raised"; raised vertices are
+// published in `chg` with one atomicOr per word.
+// Three tiles are in flight per warp: the vertex state and row offsets of
+// tile i+2 are loading while the bulk copy of tile i+1 runs and tile i is
+// processed, so neither the offset loads nor the copy is on the critical path.
+template <class V, class Load, class Test, class Row, class Fallback>
 __device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
-                                          uint32_t* chg, Local& L, Need need, Row row,
-                                          Fallback fallback) {
-  extern __shared__ __align__(128) int2 dsm[];
+                                          uint32_t* chg, Local& L, Load load, Test test,
+                                          Row row, Fallback fallback) {
+  extern __shared__ __align__(128) ERec dsm[];
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-  int2* stage_base = dsm + (size_t)warp * kStages * kStageRecs;
+  ERec* stage_base = dsm + (size_t)warp * kStages * kStageRecs;
   uint64_t* s_bar = g_tma_bar[warp];
   const uint32_t nwarps = gridDim.x * kWarps;
   const uint32_t w1 = (hi + 31) >> 5;
@@ -548,30 +530,39 @@ __device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, uint32_t lo, 
     uint32_t b, e, base;
     bool in, work, any, staged;
   };
-  // Load the tile's vertex state and, if any row is needed, start the bulk
-  // copy of the tile's edge span into stage `s`.
-  auto prepare = [&](uint32_t w, uint32_t s, Tile& t) {
+  // step 1: issue the loads of the tile's vertex state and row offsets
+  auto fetch = [&](uint32_t w, Tile& t) {
     const uint32_t v = (w << 5) + lane;
     t.in = w < w1 && v >= lo && v < hi;
     t.aux = V(0);
-    t.work = t.in && need(v, t.aux);
+    t.b = t.e = 0;
+    if (t.in) {
+      load(v, t.aux);
+      t.b = __ldg(p.g.off + v);
+      t.e = __ldg(p.g.off + v + 1);
+    }
+  };
+  // step 2: if any row of the tile is needed, start the bulk copy of the
+  // tile's edge span into stage `s`
+  auto prepare = [&](uint32_t w, uint32_t s, Tile& t) {
+    const uint32_t v = (w << 5) + lane;
+    t.work = t.in && test(v, t.aux);
     t.any = __any_sync(0xffffffffu, t.work);
     t.staged = false;
     if (!t.any) return;
-    t.b = t.in ? __ldg(p.g.off + v) : 0u;
-    t.e = t.in ? __ldg(p.g.off + v + 1) : 0u;
     const uint32_t first = max(w << 5, lo), last = min((w << 5) + 32, hi);
     const uint32_t span_lo = __shfl_sync(0xffffffffu, t.b, first - (w << 5));
     const uint32_t span_hi = __shfl_sync(0xffffffffu, t.e, last - 1 - (w << 5));
-    const uint32_t a_lo = span_lo & ~1u, a_hi = (span_hi + 1u) & ~1u;  // 16 B aligned
+    const uint32_t a_lo = span_lo & ~(kRecAlign - 1u);  // 16 B aligned
+    const uint32_t a_hi = (span_hi + kRecAlign - 1u) & ~(kRecAlign - 1u);
     t.base = a_lo;
     if (a_hi - a_lo <= kStageRecs) {
       t.staged = true;
       if (lane == 0) {
         fence_proxy_async();
-        mbar_arrive_expect_tx(&s_bar[s], (a_hi - a_lo) * (uint32_t)sizeof(int2));
-        bulk_g2s(stage_base + s * kStageRecs, p.g.edge + a_lo,
-                 (a_hi - a_lo) * (uint32_t)sizeof(int2), &s_bar[s]);
+        mbar_arrive_expect_tx(&s_bar[s], (a_hi - a_lo) * (uint32_t)sizeof(ERec));
+        bulk_g2s(stage_base + s * kStageRecs, erecs(p.g) + a_lo,
+                 (a_hi - a_lo) * (uint32_t)sizeof(ERec), &s_bar[s]);
       }
     }
   };
@@ -593,19 +584,32 @@ __device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, uint32_t lo, 
   };
 
   uint32_t parity = g_tma_parity[warp];
-  Tile cur, nxt;
+  Tile cur, nxt, far;
   uint32_t s = 0;
+  fetch(wfirst, cur);
   if (wfirst < w1) prepare(wfirst, 0, cur);
+  fetch(wfirst + nwarps, nxt);
   for (uint32_t w = wfirst; w < w1; w += nwarps) {
     __syncwarp();  // stage s^1 was last read by this warp's previous tile
     if (w + nwarps < w1) prepare(w + nwarps, s ^ 1u, nxt);
+    fetch(w + 2 * nwarps, far);
     compute(w, s, cur, parity);
     cur = nxt;
+    nxt = far;
     s ^= 1u;
   }
   __syncwarp();
   if (lane == 0) g_tma_parity[warp] = parity;
   __syncwarp();  // every lane sees the new parity before the warp's next pipeline
+}
+
+// Rows of a tile sit back to back in the stage; a lane starts its row at a
+// rotation chosen so the lanes of one shared-memory wavefront (32 lanes of
+// 4-byte records, 16 of 8-byte ones) hit distinct banks when the rows have
+// equal length (exact for lengths dividing 32 / 16).
+__device__ __forceinline__ uint32_t row_rot(uint32_t len) {
+  constexpr uint32_t G = 128 / sizeof(ERec);  // lanes per wavefront
+  return (((lane_id() % G) * len) / G) % len;
 }
 
 // Player-1 light rows of a dense round through the tile pipeline: tiles of
@@ -618,15 +622,13 @@ __device__ __noinline__ void dense_light_p1(const SolveParams<V>& p, uint32_t lo
   constexpr V TOP = Top<V>::v;
   __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
   Local L;
-  auto need = [&](uint32_t v, V& old) {
-    old = ldcg(p.f + v);
-    return old != TOP;
-  };
-  auto row = [&](uint32_t v, const int2* rec, uint32_t len, uint32_t, V old) {
+  auto load = [&](uint32_t v, V& old) { old = ldcg(p.f + v); };
+  auto test = [&](uint32_t, V old) { return old != TOP; };
+  auto row = [&](uint32_t v, const ERec* rec, uint32_t len, uint32_t, V old) {
     ++L.visits;
     ++L.apps;
     L.edges += len;
-    const uint32_t rot = lane_id() % len;  // light rows are non-empty
+    const uint32_t rot = row_rot(len);  // light rows are non-empty
     V acc = 0;
     for (uint32_t k0 = 0; k0 < len; k0 += kChunk) {
       int2 r[kChunk];
@@ -634,7 +636,7 @@ __device__ __noinline__ void dense_light_p1(const SolveParams<V>& p, uint32_t lo
       for (int k = 0; k < kChunk; ++k) {
         uint32_t j = min(k0 + k, len - 1) + rot;  // clamp (duplicate), rotate banks
         j = j >= len ? j - len : j;
-        r[k] = rec[j];
+        r[k] = dec(p.g, rec[j]);
       }
       V c[kChunk];
 #pragma unroll
@@ -654,7 +656,7 @@ __device__ __noinline__ void dense_light_p1(const SolveParams<V>& p, uint32_t lo
     return false;
   };
   auto fallback = [&](uint32_t v, V) { return lift_thread<V, false>(p, v, L); };
-  tma_tiles<V>(p, lo, hi, chg, L, need, row, fallback);
+  tma_tiles<V>(p, lo, hi, chg, L, load, test, row, fallback);
   block_flush(L, p.ctr, sum_dst, s_cnt);
 }
 
@@ -707,7 +709,7 @@ __device__ __noinline__ void dense_light_p0(const SolveParams<V>& p, uint32_t lo
       const uint32_t v = ((wb + k) << 5) + lane;
       in[k] = wb + k < w1 && v >= lo && v < hi;
       old[k] = in[k] ? ldcg(p.f + v) : TOP;
-      we[k] = in[k] ? ldcg(p.wit + v) : make_int2(0, 0);
+      we[k] = in[k] ? ld_wit(p, v) : make_int2(0, 0);
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) cw[k] = old[k] != TOP ? gather(p.f + we[k].x) : TOP;
@@ -839,7 +841,7 @@ __device__ __forceinline__ bool cert_keep_thread(const SolveParams<V>& p,
   for (uint32_t i = b; i < e; i += kCertChunk) {
     int2 r[kCertChunk];
 #pragma unroll
-    for (int k = 0; k < kCertChunk; ++k) r[k] = ld_edge(p.g.edge + min(i + k, e - 1));
+    for (int k = 0; k < kCertChunk; ++k) r[k] = ld_rec(p.g, min(i + k, e - 1));
     V c[kCertChunk];
 #pragma unroll
     for (int k = 0; k < kCertChunk; ++k) c[k] = gather(p.stage + r[k].x);
@@ -866,7 +868,7 @@ __device__ __forceinline__ bool cert_keep_warp(const SolveParams<V>& p, uint32_t
     bool g = P0;
     if (i < e) {
       ++L.cert_edges;
-      g = good_edge<V>(p, fv, ld_edge(p.g.edge + i));
+      g = good_edge<V>(p, fv, ld_rec(p.g, i));
     }
     if (P0 && !__all_sync(0xffffffffu, g)) return false;
     if (!P0 && __any_sync(0xffffffffu, g)) return true;
@@ -883,7 +885,7 @@ __device__ __forceinline__ bool cert_keep_block(const SolveParams<V>& p, uint32_
     bool g = P0;
     if (i < e) {
       ++L.cert_edges;
-      g = good_edge<V>(p, fv, ld_edge(p.g.edge + i));
+      g = good_edge<V>(p, fv, ld_rec(p.g, i));
     }
     if (P0 && !__syncthreads_and(g)) return false;
     if (!P0 && __syncthreads_or(g)) return true;
@@ -895,31 +897,6 @@ __device__ __forceinline__ bool cert_keep_block(const SolveParams<V>& p, uint32_
 // Each phase is a separate non-inlined function so it gets its own register
 // allocation; the kernel body only keeps the (grid-uniform) loop state.
 // Every phase ends with block_flush; the caller then crosses a grid barrier.
-
-__device__ __forceinline__ int size_class(const Graph& g, uint32_t v) {
-  if (v < g.rb[kP1L]) return v >= g.rb[kP0H] ? 2 : v >= g.rb[kP0M] ? 1 : 0;
-  return v >= g.rb[kP1H] ? 2 : v >= g.rb[kP1M] ? 1 : 0;
-}
-// i-th vertex of the union of the player-0 and player-1 ranges of class c
-__device__ __forceinline__ uint32_t class_item(const Graph& g, int c, uint32_t i) {
-  const uint32_t n0 = g.rb[c + 1] - g.rb[c];
-  return i < n0 ? g.rb[c] + i : g.rb[c + 3] + (i - n0);
-}
-__device__ __forceinline__ uint32_t class_size(const Graph& g, int c) {
-  return (g.rb[c + 1] - g.rb[c]) + (g.rb[c + 4] - g.rb[c + 3]);
-}
-template <class V>
-__device__ __forceinline__ bool owned(const SolveParams<V>& p, uint32_t v) {
-  return v >= p.own_lo && v < p.own_hi;
-}
-template <class V>
-__device__ __forceinline__ uint32_t clip_lo(const SolveParams<V>& p, uint32_t lo) {
-  return lo > p.own_lo ? lo : p.own_lo;
-}
-template <class V>
-__device__ __forceinline__ uint32_t clip_hi(const SolveParams<V>& p, uint32_t hi) {
-  return hi < p.own_hi ? hi : p.own_hi;
-}
 
 // Round 1 straight from the weights.  With f = 0 everywhere a lift reads no
 // measure at all: f(t) ⊖ w = max(0, -w), so delta(0)(v) = max(0, -min_w)
@@ -933,7 +910,7 @@ template <class V>
 __device__ __forceinline__ void round1_finish(const SolveParams<V>& p, uint32_t v, bool p0,
                                               int minw, int maxw, uint32_t imax, V& val) {
   val = ominus_cap<V>(V(0), p0 ? maxw : minw, p.g.cap);
-  if (p0) p.wit[v] = __ldg(p.g.edge + imax);
+  if (p0) stcg(wit_of(p) + v, __ldg(erecs(p.g) + imax));
   if (val > V(0)) stcg(p.stage + v, val);
 }
 
@@ -945,10 +922,11 @@ __device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo, 
   __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
   const Graph& g = p.g;
   Local L;
-  auto need = [](uint32_t, V&) { return true; };
-  auto finish = [&](uint32_t v, bool p0, int minw, int maxw, int2 wrec, uint32_t len) {
+  auto load = [](uint32_t, V&) {};
+  auto test = [](uint32_t, V) { return true; };
+  auto finish = [&](uint32_t v, bool p0, int minw, int maxw, ERec wrec, uint32_t len) {
     const V val = ominus_cap<V>(V(0), p0 ? maxw : minw, g.cap);
-    if (p0) p.wit[v] = wrec;
+    if (p0) stcg(wit_of(p) + v, wrec);
     ++L.visits;
     ++L.apps;
     L.edges += len;
@@ -962,9 +940,9 @@ __device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo, 
   // the player-0 witness: an edge of least max(0, -w), preferring a
   // player-0 target (player-1 targets are the ones the certificate sends to
   // top, which would void the witness in the next round)
-  auto row = [&](uint32_t v, const int2* rec, uint32_t len, uint32_t, V) {
+  auto row = [&](uint32_t v, const ERec* rec, uint32_t len, uint32_t, V) {
     const bool p0 = v < g.rb[kP1L];  // warp-uniform: the ranges are split by owner
-    const uint32_t rot = lane_id() % len;
+    const uint32_t rot = row_rot(len);
     int minw = INT32_MAX, maxw = INT32_MIN;
     uint32_t jbest = 0, kbest = 0xFFFFFFFFu;
     for (uint32_t k0 = 0; k0 < len; k0 += kChunk) {
@@ -972,7 +950,7 @@ __device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo, 
       for (int k = 0; k < kChunk; ++k) {
         uint32_t j = min(k0 + k, len - 1) + rot;
         j = j >= len ? j - len : j;
-        const int2 r = rec[j];
+        const int2 r = dec(g, rec[j]);
         if (p0) {
           maxw = max(maxw, r.y);
           // key = 2 * max(0, -w) + (target is player 1): fits 32 bits
@@ -997,7 +975,7 @@ __device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo, 
     for (uint32_t i = b; i < e; i += kChunk) {
       int wt[kChunk];
 #pragma unroll
-      for (int k = 0; k < kChunk; ++k) wt[k] = __ldcs(&g.edge[min(i + k, e - 1)].y);
+      for (int k = 0; k < kChunk; ++k) wt[k] = rec_w(g, __ldcs(erecs(g) + min(i + k, e - 1)));
 #pragma unroll
       for (int k = 0; k < kChunk; ++k) {
         minw = min(minw, wt[k]);
@@ -1007,9 +985,9 @@ __device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo, 
         }
       }
     }
-    return finish(v, p0, minw, maxw, __ldg(g.edge + imax), e - b);
+    return finish(v, p0, minw, maxw, __ldg(erecs(g) + imax), e - b);
   };
-  tma_tiles<V>(p, lo, hi, chg, L, need, row, fallback);
+  tma_tiles<V>(p, lo, hi, chg, L, load, test, row, fallback);
   block_flush(L, p.ctr, sum_dst, s_cnt);
 }
 
@@ -1039,7 +1017,7 @@ __device__ __noinline__ void round1_long(const SolveParams<V>& p, uint32_t* chg,
     int minw = INT32_MAX, maxw = INT32_MIN;
     uint32_t imax = b;
     for (uint32_t i = b + threadIdx.x; i < e; i += kBlock) {
-      const int w = __ldcs(&g.edge[i].y);
+      const int w = rec_w(g, __ldcs(erecs(g) + i));
       minw = min(minw, w);
       if (w > maxw) {
         maxw = w;
@@ -1097,7 +1075,7 @@ __device__ __noinline__ void round1_long(const SolveParams<V>& p, uint32_t* chg,
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const uint32_t i = i0 + k * 32 + lane;
-        wv[k] = i < e ? __ldcs(&g.edge[i].y) : INT32_MIN;
+        wv[k] = i < e ? rec_w(g, __ldcs(erecs(g) + i)) : INT32_MIN;
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -1381,19 +1359,22 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
   for (int side = 0; side < 2; ++side) {
     const uint32_t lo = clip_lo(p, side ? g.rb[kP1L] : g.rb[kP0L]);
     const uint32_t hi = clip_hi(p, side ? g.rb[kP1M] : g.rb[kP0M]);
-    auto need = [&](uint32_t v, V& cv) {
-      cv = ldcg(p.stage + v);
-      return is_cand<V>(cv);
-    };
-    auto row = [&](uint32_t v, const int2* rec, uint32_t len, uint32_t, V cv) {
+    auto load = [&](uint32_t v, V& cv) { cv = ldcg(p.stage + v); };
+    auto test = [&](uint32_t, V cv) { return is_cand<V>(cv); };
+    auto row = [&](uint32_t v, const ERec* rec, uint32_t len, uint32_t, V cv) {
       const int64_t fv = (int64_t)cv;
       const bool p0 = side == 0;
+      const uint32_t rot = row_rot(len);
       ++L.cert_scanned;
       bool keep = p0;
       for (uint32_t k0 = 0; k0 < len; k0 += kCertChunk) {
         int2 r[kCertChunk];
 #pragma unroll
-        for (int k = 0; k < kCertChunk; ++k) r[k] = rec[min(k0 + k, len - 1)];
+        for (int k = 0; k < kCertChunk; ++k) {
+          uint32_t j = min(k0 + k, len - 1) + rot;
+          j = j >= len ? j - len : j;
+          r[k] = dec(g, rec[j]);
+        }
         V c[kCertChunk];
 #pragma unroll
         for (int k = 0; k < kCertChunk; ++k) c[k] = gather(p.stage + r[k].x);
@@ -1419,7 +1400,7 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
       return !keep;
     };
     auto fallback = [&](uint32_t v, V) { return cert_check_thread<V>(p, v, L); };
-    tma_tiles<V>(p, lo, hi, rbm, L, need, row, fallback);
+    tma_tiles<V>(p, lo, hi, rbm, L, load, test, row, fallback);
   }
   block_flush(L, p.ctr, slot_sum + 1, s_cnt);
 }
@@ -1544,8 +1525,6 @@ __device__ __noinline__ void phase_cert_apply(const SolveParams<V>& p, uint32_t*
 // Columns longer than kLongCol (the in-hubs of a power-law arena) are not
 // expanded by one warp: they are queued in p.longcol (count in qlong) for
 // phase_activate_long, which spreads their chunks over the whole grid.
-constexpr uint32_t kLongCol = 4096;
-constexpr uint32_t kColChunk = 1024;
 
 // Frontier appends are buffered per warp in shared memory (the TMA stage
 // area, idle during activation) and published up to kAppendCap entries per
@@ -1559,9 +1538,9 @@ struct WarpLists {
 };
 
 __device__ __forceinline__ WarpLists warp_lists() {
-  extern __shared__ __align__(128) int2 dsm[];
+  extern __shared__ __align__(128) ERec dsm[];
   uint32_t* base = reinterpret_cast<uint32_t*>(dsm) +
-                   (size_t)(threadIdx.x >> 5) * (kStages * kStageRecs * 2);
+                   (size_t)(threadIdx.x >> 5) * (kStages * kStageBytes / 4);
   WarpLists q;
   for (int c = 0; c < 3; ++c) {
     q.buf[c] = base + c * kAppendCap;
@@ -1899,4 +1878,5 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
   }
 }
 
+}  // namespace EGS_FMT_NS
 }  // namespace egs

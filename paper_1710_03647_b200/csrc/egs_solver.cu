@@ -32,7 +32,20 @@
 
 #include "egs_build.cuh"
 #include "egs_gpu.h"
-#include "egs_solve.cuh"
+#include "egs_types.cuh"
+
+// The solve kernels, compiled once per edge-record format (egs_kern.cu):
+// e8 = int2 {dst, w} records, e4 = packed u32 records.
+namespace egs {
+namespace e8 {
+const void* solve_kernel(int vbits);
+const void* part_kernel(int vbits);
+}  // namespace e8
+namespace e4 {
+const void* solve_kernel(int vbits);
+const void* part_kernel(int vbits);
+}  // namespace e4
+}  // namespace egs
 
 namespace {
 
@@ -142,7 +155,8 @@ struct egs_ctx {
   uint32_t rb[egs::kNumClasses + 1] = {};
   // arena (relabelled)
   uint32_t* off = nullptr;
-  int2* edge = nullptr;
+  void* edge = nullptr;
+  uint32_t tbits = 0;  // 0: int2 records; else packed u32 (egs_types.cuh)
   uint32_t* coff = nullptr;
   uint32_t* csrc = nullptr;
   uint32_t* perm = nullptr;  // old id -> new id
@@ -177,6 +191,7 @@ struct egs_ctx {
     std::memcpy(g.rb, rb, sizeof(rb));
     g.off = off;
     g.edge = edge;
+    g.tbits = tbits;
     g.coff = coff;
     g.csrc = csrc;
     g.cap = cap;
@@ -274,10 +289,13 @@ void validate_opts(const egs_gpu_opts& o) {
     throw Fail(EGS_ERR_INVALID_CONFIG, "timeout must be >= 0");
 }
 
-template <class V>
-const void* solve_kernel() {
-  return reinterpret_cast<const void*>(&egs::k_solve<V>);
+const void* solve_kernel(const egs_ctx* c) {
+  return c->tbits ? egs::e4::solve_kernel(c->vbits) : egs::e8::solve_kernel(c->vbits);
 }
+const void* part_kernel(const egs_ctx* c) {
+  return c->tbits ? egs::e4::part_kernel(c->vbits) : egs::e8::part_kernel(c->vbits);
+}
+size_t rec_bytes(const egs_ctx* c) { return c->tbits ? 4 : 8; }
 
 // Process-wide pinned staging buffer for the narrowed weights (grows on
 // demand; one upload at a time uses it).
@@ -305,7 +323,8 @@ void* pinned_stage(uint64_t bytes) {
 // transpose sorts.  C4 (|w| <= 100) sends 1 byte per weight instead of 8.
 template <class W>
 bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint32_t>& rows,
-                    std::vector<cudaEvent_t>& ew, const uint64_t* off64, void* wdev) {
+                    std::vector<cudaEvent_t>& ew, std::vector<cudaEvent_t>& et,
+                    const uint64_t* off64, void* wdev) {
   cudaStream_t sc = c->copy_stream, sw = c->aux_stream;
   const int nch = (int)rows.size() - 1;
   const uint64_t m = c->m;
@@ -349,9 +368,11 @@ bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint3
     CK(cudaMemcpyAsync(wd + e0, stage + e0, (e1 - e0) * sizeof(W), cudaMemcpyHostToDevice, sc));
     CK(cudaEventRecord(ew[k], sc));
     CK(cudaStreamWaitEvent(sw, ew[k], 0));
+    // packed records: the weight bits are or-ed into the target words
+    if (c->tbits) CK(cudaStreamWaitEvent(sw, et[k], 0));
     egs::k_relabel_weights<W><<<grid_for((uint64_t)(rows[k + 1] - rows[k]) * 4, c->num_sms),
                                 256, 0, sw>>>(rows[k], rows[k + 1], off64, wd, c->perm, c->off,
-                                              c->edge);
+                                              c->edge, c->tbits);
     CK(cudaGetLastError());
   }
   if (self_worker.joinable()) self_worker.join();
@@ -392,7 +413,16 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   uint32_t* ck1 = d_ck1.alloc<uint32_t>(m);
   c->perm = dalloc<uint32_t>(n);
   c->off = dalloc<uint32_t>((size_t)n + 1);
-  c->edge = dalloc<int2>(m + 2);  // +2: 16-byte rounding of TMA spans
+  // packed 4-byte records when every weight fits beside the target bits
+  // (EGS_EDGE_FORMAT=8 forces the 8-byte format)
+  {
+    const uint32_t tb = bits_for(n);  // ids < n fit tb bits
+    const char* fmt = std::getenv("EGS_EDGE_FORMAT");
+    const bool wide = fmt && std::atoi(fmt) == 8;
+    c->tbits = (!wide && tb <= 24 && a->max_abs_weight < (1ll << (31 - tb))) ? tb : 0;
+  }
+  // +16 bytes: 16-byte rounding of TMA spans
+  c->edge = dalloc<uint8_t>(m * rec_bytes(c) + 16);
   c->csrc = dalloc<uint32_t>(m);
   c->coff = dalloc<uint32_t>((size_t)n + 1);
   CK(cudaMemsetAsync(misc, 0, 32 * sizeof(unsigned int), s));
@@ -417,10 +447,11 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   }
   if (rows.back() < n) rows.push_back(n);
   const int nch = (int)rows.size() - 1;
-  std::vector<cudaEvent_t> ex(nch), ew(nch);
+  std::vector<cudaEvent_t> ex(nch), ew(nch), et(nch);
   for (int k = 0; k < nch; ++k) {
     CK(cudaEventCreateWithFlags(&ex[k], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ew[k], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&et[k], cudaEventDisableTiming));
   }
   auto span_of = [&](int k) {
     return std::make_pair(a->csr_offsets[rows[k]], a->csr_offsets[rows[k + 1]]);
@@ -459,8 +490,10 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   for (int k = 0; k < nch; ++k) {
     CK(cudaStreamWaitEvent(s, ex[k], 0));
     egs::k_relabel_targets<<<grid_for((uint64_t)(rows[k + 1] - rows[k]) * 4, sms), 256, 0, s>>>(
-        n, rows[k], rows[k + 1], off64, dst, c->perm, c->off, c->edge, ck0, cv0, misc + 16);
+        n, rows[k], rows[k + 1], off64, dst, c->perm, c->off, c->edge, c->tbits, ck0, cv0,
+        misc + 16);
     CK(cudaGetLastError());
+    CK(cudaEventRecord(et[k], s));
   }
 
   // transpose: sort the (dst, src) pairs by dst while the weights stream in
@@ -476,11 +509,11 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   {
     const int64_t mw = a->max_abs_weight;
     if (mw <= 127)
-      h_stage_bad = upload_weights<int8_t>(c, a, rows, ew, off64, wn);
+      h_stage_bad = upload_weights<int8_t>(c, a, rows, ew, et, off64, wn);
     else if (mw <= 32767)
-      h_stage_bad = upload_weights<int16_t>(c, a, rows, ew, off64, wn);
+      h_stage_bad = upload_weights<int16_t>(c, a, rows, ew, et, off64, wn);
     else
-      h_stage_bad = upload_weights<int32_t>(c, a, rows, ew, off64, wn);
+      h_stage_bad = upload_weights<int32_t>(c, a, rows, ew, et, off64, wn);
   }
   tm.mark("upload + relabel + CSC sort");
   CK(cudaEventRecord(e_tail, sw));
@@ -504,6 +537,7 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   tm.mark("weights + join");
   for (auto e : ex) cudaEventDestroy(e);
   for (auto e : ew) cudaEventDestroy(e);
+  for (auto e : et) cudaEventDestroy(e);
   cudaEventDestroy(e_alloc);
   cudaEventDestroy(e_vert);
   cudaEventDestroy(e_perm);
@@ -600,7 +634,7 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     } else {
       c->off = dalloc<uint32_t>(1);
       c->coff = dalloc<uint32_t>(1);
-      c->edge = dalloc<int2>(1);
+      c->edge = dalloc<uint8_t>(16);
       c->csrc = dalloc<uint32_t>(1);
       c->perm = dalloc<uint32_t>(1);
       c->inv = dalloc<uint32_t>(1);
@@ -609,12 +643,10 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
 
     // Persistent grid: every CTA co-resident (cooperative launch).
     int per_sm = 0;
-    const void* kfn = c->vbits == 32 ? solve_kernel<uint32_t>() : solve_kernel<uint64_t>();
+    const void* kfn = solve_kernel(c);
     CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)egs::kLiftSmemBytes));
-    const void* pfn = c->vbits == 32
-                          ? reinterpret_cast<const void*>(&egs::k_part_step<uint32_t>)
-                          : reinterpret_cast<const void*>(&egs::k_part_step<uint64_t>);
+    const void* pfn = part_kernel(c);
     CK(cudaFuncSetAttribute(pfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)egs::kLiftSmemBytes));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, egs::kBlock,
@@ -663,6 +695,7 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
       st->upload_seconds = secs_since(t0);
       st->value_bits = (uint32_t)c->vbits;
       st->grid_ctas = (uint32_t)c->grid;
+      st->edge_bytes = (uint32_t)rec_bytes(c);
     }
     return c;
   } catch (...) {
@@ -726,6 +759,7 @@ void fill_stats(egs_ctx* c, const unsigned long long* h, double ms, egs_gpu_stat
   const uint32_t n = c->n;
   const size_t words = ((size_t)n + 31) / 32;
   const double sv = sizeof(V);
+  const double er = (double)rec_bytes(c);  // edge record bytes
   st->lifts = h[egs::kLifts];
   st->applications = h[egs::kApps];
   st->edges_relaxed = h[egs::kEdges];
@@ -750,13 +784,13 @@ void fill_stats(egs_ctx* c, const unsigned long long* h, double ms, egs_gpu_stat
   // round 1 (counted as one dense round: n visits, m edges) reads records
   // but neither f(v) nor f(t): drop those gathers from the lift formula
   const double r1 = (double)c->m * sv + (double)n * sv;
-  const double lift = (double)st->visits * sv + (double)st->witness_checks * (8 + sv) +
-                      (double)st->applications * 8 + (double)st->edges_relaxed * (8 + sv) +
+  const double lift = (double)st->visits * sv + (double)st->witness_checks * (er + sv) +
+                      (double)st->applications * 8 + (double)st->edges_relaxed * (er + sv) +
                       (double)st->lifts * sv - (st->rounds ? r1 : 0.0);
   const double seed = 0.0;
   const double cert = (double)st->cert_attempts * n * (2 * (sv + 1)) +
                       (double)st->cert_rows * (1 + sv + 8) +
-                      (double)st->cert_edges * (8 + sv + 1);
+                      (double)st->cert_edges * (er + sv + 1);
   const double act = (double)st->activations * (4 + sv) + (double)st->sparse_rounds * words * 4;
   st->lift_bytes = (uint64_t)lift;
   st->algo_bytes = (uint64_t)(lift + seed + cert + act);
@@ -766,6 +800,7 @@ void fill_stats(egs_ctx* c, const unsigned long long* h, double ms, egs_gpu_stat
   for (int k = 0; k < 5; ++k) st->phase_detail_seconds[k] = h[egs::kFineCommit + k] * 1e-9;
   st->value_bits = (uint32_t)c->vbits;
   st->grid_ctas = (uint32_t)c->grid;
+  st->edge_bytes = (uint32_t)rec_bytes(c);
 }
 
 template <class V>
@@ -785,7 +820,7 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
   CK(cudaMemsetAsync(c->scratch, 0, sizeof(egs::Scratch), s));
   CK(cudaMemsetAsync(c->ctr, 0, egs::kNumCounters * sizeof(unsigned long long), s));
   void* args[] = {&p};
-  CK(cudaLaunchCooperativeKernel(solve_kernel<V>(), dim3(c->grid), dim3(egs::kBlock), args,
+  CK(cudaLaunchCooperativeKernel(solve_kernel(c), dim3(c->grid), dim3(egs::kBlock), args,
                                  egs::kLiftSmemBytes, s));
   CK(cudaEventRecord(c->ev[1], s));
   CK(cudaMemcpyAsync(c->h_ctr, c->ctr, egs::kNumCounters * sizeof(unsigned long long),
@@ -959,7 +994,7 @@ void part_step(egs_ctx* c, int step, int parity, uint64_t* counts) {
   egs::SolveParams<V> p = make_params<V>(c, nullptr);
   CK(cudaMemsetAsync(c->scratch, 0, sizeof(egs::Scratch), s));
   void* args[] = {&p, &step, &parity};
-  const void* fn = reinterpret_cast<const void*>(&egs::k_part_step<V>);
+  const void* fn = part_kernel(c);
   CK(cudaLaunchKernel(fn, dim3(c->full_grid), dim3(egs::kBlock), args, egs::kLiftSmemBytes, s));
   CK(cudaGetLastError());
   unsigned int sums[4] = {0, 0, 0, 0};

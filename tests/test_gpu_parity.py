@@ -249,6 +249,45 @@ def test_weight_width_paths(egs, oracle):
         _solve(egs, big)
 
 
+def _bits(n):
+    b = 1
+    while (1 << b) < n:
+        b += 1
+    return b
+
+
+@pytest.mark.parametrize("forced_wide", [False, True])
+def test_edge_record_formats(egs, oracle, monkeypatch, forced_wide):
+    """Packed 4-byte records (dst | w << tb) hold every id < n in tb bits and
+    weights up to 2^(31-tb) - 1; one more and the arena takes 8-byte records.
+    Vertex counts at and just past powers of two, weights at the limit."""
+    import random
+    if forced_wide:
+        monkeypatch.setenv("EGS_EDGE_FORMAT", "8")
+    for n in (2, 3, 16, 17, 32, 33, 255, 256, 257, 1025):
+        tb = _bits(n)
+        lim = (1 << (31 - tb)) - 1
+        for W, packed in ((lim, True), (lim + 1, False)):
+            r = random.Random(n * 7 + packed)
+            edges = [(v, r.randrange(n), r.randint(-W, W)) for v in range(n) for _ in range(3)]
+            edges += [(0, n - 1, -W), (n - 1, 0, W)]
+            owners = [r.randint(0, 1) for _ in range(n)]
+            a = egs.GameArena.build(n, edges, owners)
+            g = oracle.build(n, edges, owners)
+            want, _ = oracle.solve_seq(g)
+            with egs.DeviceSolver(a) as ds:
+                want_bytes = 4 if packed and not forced_wide else 8
+                assert ds.upload_stats.edge_bytes == want_bytes, (n, W)
+                ds.solve()
+                got = ds.read_measure()
+                assert np.array_equal(got, want), (n, W, forced_wide)
+                assert ds.is_fixpoint(got)
+            for mode in MODES:
+                rep = _solve(egs, a, mode=mode)
+                assert np.array_equal(rep.measure, want), (n, W, mode, forced_wide)
+                assert egs.write_solution(a, rep) == oracle.write_solution(g, want)
+
+
 def test_empty_and_single_vertex(egs):
     a = egs.GameArena.build(0, [], [])
     rep = _solve(egs, a)
