@@ -510,9 +510,10 @@ __device__ __forceinline__ void tma_init_barriers() {
 // shared memory, `fallback(v, aux)` a row whose tile span does not fit a
 // stage (direct loads).  Both return "raised"; raised vertices are
 // published in `chg` with one atomicOr per word.
-// Three tiles are in flight per warp: the vertex state and row offsets of
-// tile i+2 are loading while the bulk copy of tile i+1 runs and tile i is
-// processed, so neither the offset loads nor the copy is on the critical path.
+// Per warp, while tile i is processed from its stage, the bulk copies of
+// tiles i+1 .. i+kStages-1 are in flight and the vertex state and row
+// offsets of the tile after them are loading: the HBM latency of a copy
+// (~1-2 us) is covered by kStages-1 tiles of work instead of one.
 template <class V, class Load, class Test, class Row, class Fallback>
 __device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
                                           uint32_t* chg, Local& L, Load load, Test test,
@@ -583,20 +584,25 @@ __device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, uint32_t lo, 
     L.phase_count += ch;
   };
 
+  // tile i is processed from slot i % kStages while the copies of tiles
+  // i+1 .. i+D are in flight and the offsets of tile i+D+1 are loading
+  constexpr uint32_t D = kStages - 1;
   uint32_t parity = g_tma_parity[warp];
-  Tile cur, nxt, far;
+  Tile t[D + 2];
+#pragma unroll
+  for (uint32_t k = 0; k <= D; ++k) fetch(wfirst + k * nwarps, t[k]);
+#pragma unroll
+  for (uint32_t k = 0; k < D; ++k)
+    if (wfirst + k * nwarps < w1) prepare(wfirst + k * nwarps, k, t[k]);
   uint32_t s = 0;
-  fetch(wfirst, cur);
-  if (wfirst < w1) prepare(wfirst, 0, cur);
-  fetch(wfirst + nwarps, nxt);
   for (uint32_t w = wfirst; w < w1; w += nwarps) {
-    __syncwarp();  // stage s^1 was last read by this warp's previous tile
-    if (w + nwarps < w1) prepare(w + nwarps, s ^ 1u, nxt);
-    fetch(w + 2 * nwarps, far);
-    compute(w, s, cur, parity);
-    cur = nxt;
-    nxt = far;
-    s ^= 1u;
+    __syncwarp();  // slot (s + D) % kStages was last read by this warp's previous tile
+    if (w + D * nwarps < w1) prepare(w + D * nwarps, s == 0 ? D : s - 1, t[D]);
+    fetch(w + (D + 1) * nwarps, t[D + 1]);
+    compute(w, s, t[0], parity);
+#pragma unroll
+    for (uint32_t k = 0; k <= D; ++k) t[k] = t[k + 1];
+    s = s == D ? 0 : s + 1;
   }
   __syncwarp();
   if (lane == 0) g_tma_parity[warp] = parity;

@@ -112,7 +112,10 @@ struct SolveParams {
 // The solve kernels are compiled once per format (egs_kern.cu); the one-shot
 // build and verification kernels decode at run time with edge_at.
 constexpr uint32_t kStageBytes = 4096;  // per warp TMA stage
-constexpr uint32_t kStages = 2;
+#ifndef EGS_TMA_STAGES
+#define EGS_TMA_STAGES 2
+#endif
+constexpr uint32_t kStages = EGS_TMA_STAGES;  // per warp: kStages - 1 copies ahead
 constexpr size_t kLiftSmemBytes = (size_t)kWarps * kStages * kStageBytes;
 
 // Activation: CSC columns longer than kLongCol are chunked over the grid.

@@ -5,6 +5,9 @@ import sys
 for path in sys.argv[1:]:
     print("==", path)
     for line in open(path):
+        if not line.startswith("{"):
+            print(line.rstrip())
+            continue
         d = json.loads(line)
         print(f"{d['config']} {d['mode']:6s} r={d['rounds']:3d} d/s={d['dense_rounds']}/{d['sparse_rounds']} "
               f"cert={d['cert_attempts']}/{d['cert_passes']} ({d['certified']}) "
