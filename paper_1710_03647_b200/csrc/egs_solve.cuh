@@ -185,7 +185,10 @@ __device__ __forceinline__ void block_flush(Local& L, unsigned long long* ctr,
 // the count(v) of Alg. 1, solver_seq.cpp:186-199).
 
 // ---- one thread per row (light rows)
-constexpr int kChunk = 8;  // edges whose gathers a thread keeps in flight
+#ifndef EGS_LIFT_CHUNK
+#define EGS_LIFT_CHUNK 8
+#endif
+constexpr int kChunk = EGS_LIFT_CHUNK;  // edges whose gathers a thread keeps in flight
 
 template <class V, bool P0>
 __device__ __forceinline__ bool lift_thread(const SolveParams<V>& p, uint32_t v,
@@ -503,8 +506,11 @@ __device__ __forceinline__ void tma_init_barriers() {
   __syncthreads();
 }
 
-// The TMA tile pipeline of one warp over the aligned 32-vertex words of
-// [lo, hi): `load(v, aux)` issues the loads of vertex v's state into a
+// The TMA tile pipeline over the aligned 32-vertex words (tiles) of the
+// vertex ranges [lo0, hi0) and [lo1, hi1) (either may be empty): warps claim
+// kTileClaim consecutive tiles at a time from `cursor` (a zeroed per-phase
+// counter), so a slow SM or a tile of long rows does not hold up the phase.
+// Per tile, `load(v, aux)` issues the loads of vertex v's state into a
 // per-lane value carried to the row step, `test(v, aux)` says whether v's
 // row must be read, `row(v, rec, len, b, aux)` processes a row held in
 // shared memory, `fallback(v, aux)` a row whose tile span does not fit a
@@ -513,30 +519,53 @@ __device__ __forceinline__ void tma_init_barriers() {
 // Per warp, while tile i is processed from its stage, the bulk copies of
 // tiles i+1 .. i+kStages-1 are in flight and the vertex state and row
 // offsets of the tile after them are loading: the HBM latency of a copy
-// (~1-2 us) is covered by kStages-1 tiles of work instead of one.
+// (~1-2 us) is covered by the work of the tiles ahead of it.
+constexpr uint32_t kTileClaim = 4;
+
 template <class V, class Load, class Test, class Row, class Fallback>
-__device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
+__device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, uint32_t lo0, uint32_t hi0,
+                                          uint32_t lo1, uint32_t hi1, unsigned int* cursor,
                                           uint32_t* chg, Local& L, Load load, Test test,
                                           Row row, Fallback fallback) {
   extern __shared__ __align__(128) ERec dsm[];
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   ERec* stage_base = dsm + (size_t)warp * kStages * kStageRecs;
   uint64_t* s_bar = g_tma_bar[warp];
-  const uint32_t nwarps = gridDim.x * kWarps;
-  const uint32_t w1 = (hi + 31) >> 5;
-  const uint32_t wfirst = (lo >> 5) + blockIdx.x * kWarps + warp;
+  const uint32_t T0 = hi0 > lo0 ? ((hi0 + 31) >> 5) - (lo0 >> 5) : 0u;
+  const uint32_t T1 = hi1 > lo1 ? ((hi1 + 31) >> 5) - (lo1 >> 5) : 0u;
+  const uint32_t T = T0 + T1;
+  uint32_t c_next = 0, c_end = 0;  // this warp's current claim (warp-uniform)
+  auto claim = [&]() -> uint32_t {
+    if (c_next >= c_end) {
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(cursor, kTileClaim);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      c_next = base;
+      c_end = base + kTileClaim < T ? base + kTileClaim : T;
+      if (base >= T) return 0xFFFFFFFFu;
+    }
+    return c_next++;
+  };
 
   struct Tile {
     V aux;
-    uint32_t b, e, base;
-    bool in, work, any, staged;
+    uint32_t w, lo, hi, b, e, base;
+    bool valid, in, work, any, staged;
   };
-  // step 1: issue the loads of the tile's vertex state and row offsets
-  auto fetch = [&](uint32_t w, Tile& t) {
-    const uint32_t v = (w << 5) + lane;
-    t.in = w < w1 && v >= lo && v < hi;
+  // step 1: claim a tile and issue the loads of its vertex state and offsets
+  auto fetch = [&](Tile& t) {
+    const uint32_t i = claim();
+    t.valid = i < T;
+    t.in = false;
     t.aux = V(0);
     t.b = t.e = 0;
+    if (!t.valid) return;
+    const bool second = i >= T0;
+    t.w = second ? (lo1 >> 5) + (i - T0) : (lo0 >> 5) + i;
+    t.lo = second ? lo1 : lo0;
+    t.hi = second ? hi1 : hi0;
+    const uint32_t v = (t.w << 5) + lane;
+    t.in = v >= t.lo && v < t.hi;
     if (t.in) {
       load(v, t.aux);
       t.b = __ldg(p.g.off + v);
@@ -545,15 +574,15 @@ __device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, uint32_t lo, 
   };
   // step 2: if any row of the tile is needed, start the bulk copy of the
   // tile's edge span into stage `s`
-  auto prepare = [&](uint32_t w, uint32_t s, Tile& t) {
-    const uint32_t v = (w << 5) + lane;
+  auto prepare = [&](uint32_t s, Tile& t) {
+    const uint32_t v = (t.w << 5) + lane;
     t.work = t.in && test(v, t.aux);
     t.any = __any_sync(0xffffffffu, t.work);
     t.staged = false;
     if (!t.any) return;
-    const uint32_t first = max(w << 5, lo), last = min((w << 5) + 32, hi);
-    const uint32_t span_lo = __shfl_sync(0xffffffffu, t.b, first - (w << 5));
-    const uint32_t span_hi = __shfl_sync(0xffffffffu, t.e, last - 1 - (w << 5));
+    const uint32_t first = max(t.w << 5, t.lo), last = min((t.w << 5) + 32, t.hi);
+    const uint32_t span_lo = __shfl_sync(0xffffffffu, t.b, first - (t.w << 5));
+    const uint32_t span_hi = __shfl_sync(0xffffffffu, t.e, last - 1 - (t.w << 5));
     const uint32_t a_lo = span_lo & ~(kRecAlign - 1u);  // 16 B aligned
     const uint32_t a_hi = (span_hi + kRecAlign - 1u) & ~(kRecAlign - 1u);
     t.base = a_lo;
@@ -567,10 +596,10 @@ __device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, uint32_t lo, 
       }
     }
   };
-  auto compute = [&](uint32_t w, uint32_t s, const Tile& t, uint32_t& parity) {
+  auto compute = [&](uint32_t s, const Tile& t, uint32_t& parity) {
     if (t.in && !t.work) ++L.visits;  // e.g. a top vertex: one load, no lift
     if (!t.any) return;
-    const uint32_t v = (w << 5) + lane;
+    const uint32_t v = (t.w << 5) + lane;
     bool ch = false;
     if (t.staged) {
       mbar_wait(&s_bar[s], (parity >> s) & 1u);
@@ -580,26 +609,26 @@ __device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, uint32_t lo, 
       ch = fallback(v, t.aux);
     }
     const uint32_t m = __ballot_sync(0xffffffffu, ch);
-    if (m && lane == 0) atomicOr(chg + w, m);
+    if (m && lane == 0) atomicOr(chg + t.w, m);
     L.phase_count += ch;
   };
 
   // tile i is processed from slot i % kStages while the copies of tiles
-  // i+1 .. i+D are in flight and the offsets of tile i+D+1 are loading
+  // i+1 .. i+D are in flight and tile i+D+1 is loading its offsets
   constexpr uint32_t D = kStages - 1;
   uint32_t parity = g_tma_parity[warp];
   Tile t[D + 2];
 #pragma unroll
-  for (uint32_t k = 0; k <= D; ++k) fetch(wfirst + k * nwarps, t[k]);
+  for (uint32_t k = 0; k <= D; ++k) fetch(t[k]);
 #pragma unroll
   for (uint32_t k = 0; k < D; ++k)
-    if (wfirst + k * nwarps < w1) prepare(wfirst + k * nwarps, k, t[k]);
+    if (t[k].valid) prepare(k, t[k]);
   uint32_t s = 0;
-  for (uint32_t w = wfirst; w < w1; w += nwarps) {
+  while (t[0].valid) {
     __syncwarp();  // slot (s + D) % kStages was last read by this warp's previous tile
-    if (w + D * nwarps < w1) prepare(w + D * nwarps, s == 0 ? D : s - 1, t[D]);
-    fetch(w + (D + 1) * nwarps, t[D + 1]);
-    compute(w, s, t[0], parity);
+    if (t[D].valid) prepare(s == 0 ? D : s - 1, t[D]);
+    fetch(t[D + 1]);
+    compute(s, t[0], parity);
 #pragma unroll
     for (uint32_t k = 0; k <= D; ++k) t[k] = t[k + 1];
     s = s == D ? 0 : s + 1;
@@ -624,7 +653,8 @@ __device__ __forceinline__ uint32_t row_rot(uint32_t len) {
 // banks), 8 gathers in flight.
 template <class V>
 __device__ __noinline__ void dense_light_p1(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
-                                            uint32_t* chg, unsigned int* sum_dst) {
+                                            unsigned int* cursor, uint32_t* chg,
+                                            unsigned int* sum_dst) {
   constexpr V TOP = Top<V>::v;
   __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
   Local L;
@@ -662,7 +692,7 @@ __device__ __noinline__ void dense_light_p1(const SolveParams<V>& p, uint32_t lo
     return false;
   };
   auto fallback = [&](uint32_t v, V) { return lift_thread<V, false>(p, v, L); };
-  tma_tiles<V>(p, lo, hi, chg, L, load, test, row, fallback);
+  tma_tiles<V>(p, lo, hi, 0u, 0u, cursor, chg, L, load, test, row, fallback);
   block_flush(L, p.ctr, sum_dst, s_cnt);
 }
 
@@ -923,7 +953,8 @@ __device__ __forceinline__ void round1_finish(const SolveParams<V>& p, uint32_t 
 // light rows: one thread per row over the TMA tile pipeline (the weight scan
 // streams the whole edge array once)
 template <class V>
-__device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
+__device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo0, uint32_t hi0,
+                                          uint32_t lo1, uint32_t hi1, unsigned int* cursor,
                                           uint32_t* chg, unsigned int* sum_dst) {
   __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
   const Graph& g = p.g;
@@ -947,7 +978,7 @@ __device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo, 
   // player-0 target (player-1 targets are the ones the certificate sends to
   // top, which would void the witness in the next round)
   auto row = [&](uint32_t v, const ERec* rec, uint32_t len, uint32_t, V) {
-    const bool p0 = v < g.rb[kP1L];  // warp-uniform: the ranges are split by owner
+    const bool p0 = v < g.rb[kP1L];  // uniform over a tile's working lanes
     const uint32_t rot = row_rot(len);
     int minw = INT32_MAX, maxw = INT32_MIN;
     uint32_t jbest = 0, kbest = 0xFFFFFFFFu;
@@ -993,7 +1024,7 @@ __device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo, 
     }
     return finish(v, p0, minw, maxw, __ldg(erecs(g) + imax), e - b);
   };
-  tma_tiles<V>(p, lo, hi, chg, L, load, test, row, fallback);
+  tma_tiles<V>(p, lo0, hi0, lo1, hi1, cursor, chg, L, load, test, row, fallback);
   block_flush(L, p.ctr, sum_dst, s_cnt);
 }
 
@@ -1121,8 +1152,8 @@ __device__ __noinline__ void phase_round1(const SolveParams<V>& p, uint32_t* chg
                                           unsigned int* slot_sum, unsigned int* slot_dyn) {
   const Graph& g = p.g;
   round1_long<V>(p, chg, slot_sum + 0, slot_dyn);
-  round1_light<V>(p, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]), chg, slot_sum + 0);
-  round1_light<V>(p, clip_lo(p, g.rb[kP1L]), clip_hi(p, g.rb[kP1M]), chg, slot_sum + 0);
+  round1_light<V>(p, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]), clip_lo(p, g.rb[kP1L]),
+                  clip_hi(p, g.rb[kP1M]), slot_dyn + kTileCursor, chg, slot_sum + 0);
 }
 
 // One lift round.  Dense: every vertex (top ones are skipped after one
@@ -1160,7 +1191,8 @@ __device__ __noinline__ void phase_lift(const SolveParams<V>& p, bool dense, int
     dense_light_p0<V>(p, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]), chg, sum_dst);
     st.lap(kSubLightP0);
     if (p.use_tma)
-      dense_light_p1<V>(p, clip_lo(p, g.rb[kP1L]), clip_hi(p, g.rb[kP1M]), chg, sum_dst);
+      dense_light_p1<V>(p, clip_lo(p, g.rb[kP1L]), clip_hi(p, g.rb[kP1M]),
+                        slot_dyn + kTileCursor, chg, sum_dst);
     else
       dense_light<V, false>(p, clip_lo(p, g.rb[kP1L]), clip_hi(p, g.rb[kP1M]), chg, sum_dst);
     st.lap(kSubLightP1);
@@ -1362,14 +1394,12 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
   cert_long_rows<V>(p, class_size(g, 2), itH, class_size(g, 1), itM, slot_dyn, rbm, L);
   // light candidates: one row per lane through the TMA tile pipeline (tiles
   // without a candidate are skipped); removals are published in rbm
-  for (int side = 0; side < 2; ++side) {
-    const uint32_t lo = clip_lo(p, side ? g.rb[kP1L] : g.rb[kP0L]);
-    const uint32_t hi = clip_hi(p, side ? g.rb[kP1M] : g.rb[kP0M]);
+  {
     auto load = [&](uint32_t v, V& cv) { cv = ldcg(p.stage + v); };
     auto test = [&](uint32_t, V cv) { return is_cand<V>(cv); };
     auto row = [&](uint32_t v, const ERec* rec, uint32_t len, uint32_t, V cv) {
       const int64_t fv = (int64_t)cv;
-      const bool p0 = side == 0;
+      const bool p0 = v < g.rb[kP1L];
       const uint32_t rot = row_rot(len);
       ++L.cert_scanned;
       bool keep = p0;
@@ -1406,7 +1436,9 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
       return !keep;
     };
     auto fallback = [&](uint32_t v, V) { return cert_check_thread<V>(p, v, L); };
-    tma_tiles<V>(p, lo, hi, rbm, L, load, test, row, fallback);
+    tma_tiles<V>(p, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]), clip_lo(p, g.rb[kP1L]),
+                 clip_hi(p, g.rb[kP1M]), slot_dyn + kTileCursor, rbm, L, load, test, row,
+                 fallback);
   }
   block_flush(L, p.ctr, slot_sum + 1, s_cnt);
 }
@@ -1699,8 +1731,8 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
   // zero the per-phase slots two phases ahead (last read two phases ago)
   auto begin_phase = [&]() {
     if (leader)
-      for (int k = 0; k < 4; ++k) {
-        sh->sum[(phase + 2) & 3][k] = 0;
+      for (int k = 0; k < 8; ++k) {
+        if (k < 4) sh->sum[(phase + 2) & 3][k] = 0;
         sh->dyn[(phase + 2) & 3][k] = 0;
       }
   };

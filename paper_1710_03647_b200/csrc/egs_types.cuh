@@ -66,10 +66,13 @@ struct Graph {
   int64_t cap;                   // credit_cap (M_G)
 };
 
+constexpr int kTileCursor = 7;  // Scratch::dyn slot of the TMA tile claims
+
 // Grid-shared scratch; the host zeroes it before each launch.
 struct Scratch {
   unsigned int sum[4][4];    // per-phase-slot sums: 0 changed, 1 removed, 2 seeds
-  unsigned int dyn[4][4];    // per-phase-slot work cursors: 0 medium, 1 heavy
+  unsigned int dyn[4][8];    // per-phase-slot work cursors: 0 medium, 1 heavy,
+                             // 2.. activation / certificate queues, 7 TMA tiles
   unsigned int fr_cnt[2][3]; // frontier sublist sizes [buffer][L, M, H]
   unsigned int stop;         // timeout flag
 };
