@@ -160,10 +160,11 @@ void egs_ctx_destroy(egs_ctx* ctx);
 /* ---------------------------------------------------------------------
  * Multi-GPU partition.  One process per GPU; rank r owns the
  * relabelled vertex range [own_lo, own_hi) of `slice` vertices.  The
- * arena is replicated on every GPU, the measure f and the staging /
- * candidate array are replicated with `padded` = world * slice entries, and
- * the host exchanges the owned slices between steps (all-gather over NCCL:
- * paper_1710_03647_b200/distributed.py).  The device addresses of those two
+ * arena is replicated on every GPU, the measure f and the staging array are
+ * replicated with `padded` = world * slice entries and the certificate
+ * candidate bitmap with padded / 32 words, and the host exchanges the owned
+ * slices between steps (all-gather over NCCL:
+ * paper_1710_03647_b200/distributed.py).  The device addresses of those
  * arrays are returned so a collective library can operate on them in place.
  * Steps restate the phases of egs_ctx_solve restricted to the owned range. */
 typedef struct egs_part egs_part;
@@ -176,12 +177,14 @@ typedef struct egs_part_layout {
   uint32_t value_bytes;   /* 4 (u32) or 8 (u64); top = all ones */
   uint64_t f_dev;         /* device address of the replicated measure */
   uint64_t stage_dev;     /* device address of the replicated staging array */
+  uint64_t cand_dev;      /* device address of the replicated certificate candidate
+                             bitmap (padded / 32 u32 words) */
 } egs_part_layout;
 
 #define EGS_STEP_ROUND1 0     /* seeding + round 1 from the weights */
 #define EGS_STEP_LIFT 1       /* one dense lift round (stages raised values) */
 #define EGS_STEP_COMMIT 2     /* staged -> f for this rank's raised vertices */
-#define EGS_STEP_CERT_INIT 3  /* candidate snapshot into the staging array */
+#define EGS_STEP_CERT_INIT 3  /* candidate bits (raised, non-top) into the bitmap */
 #define EGS_STEP_CERT_PRUNE 4 /* one certificate pass */
 #define EGS_STEP_CERT_APPLY 5 /* certified vertices -> top */
 

@@ -134,7 +134,7 @@ class PartLayout(C.Structure):
     _fields_ = [
         ("num_vertices", C.c_uint32), ("slice", C.c_uint32), ("padded", C.c_uint32),
         ("own_lo", C.c_uint32), ("own_hi", C.c_uint32), ("value_bytes", C.c_uint32),
-        ("f_dev", C.c_uint64), ("stage_dev", C.c_uint64),
+        ("f_dev", C.c_uint64), ("stage_dev", C.c_uint64), ("cand_dev", C.c_uint64),
     ]
 
 

@@ -512,7 +512,8 @@ __device__ __forceinline__ void tma_init_barriers() {
 // counter), so a slow SM or a tile of long rows does not hold up the phase.
 // Per tile, `load(v, aux)` issues the loads of vertex v's state into a
 // per-lane value carried to the row step, `test(v, aux)` says whether v's
-// row must be read, `row(v, rec, len, b, aux)` processes a row held in
+// row must be read (only asked for the set bits of the tile's word of
+// `mask`, when given), `row(v, rec, len, b, aux)` processes a row held in
 // shared memory, `fallback(v, aux)` a row whose tile span does not fit a
 // stage (direct loads).  Both return "raised"; raised vertices are
 // published in `chg` with one atomicOr per word.
@@ -525,8 +526,8 @@ constexpr uint32_t kTileClaim = 4;
 template <class V, class Load, class Test, class Row, class Fallback>
 __device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, uint32_t lo0, uint32_t hi0,
                                           uint32_t lo1, uint32_t hi1, unsigned int* cursor,
-                                          uint32_t* chg, Local& L, Load load, Test test,
-                                          Row row, Fallback fallback) {
+                                          const uint32_t* mask, uint32_t* chg, Local& L,
+                                          Load load, Test test, Row row, Fallback fallback) {
   extern __shared__ __align__(128) ERec dsm[];
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   ERec* stage_base = dsm + (size_t)warp * kStages * kStageRecs;
@@ -549,7 +550,7 @@ __device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, uint32_t lo0,
 
   struct Tile {
     V aux;
-    uint32_t w, lo, hi, b, e, base;
+    uint32_t w, lo, hi, b, e, base, mask;
     bool valid, in, work, any, staged;
   };
   // step 1: claim a tile and issue the loads of its vertex state and offsets
@@ -566,6 +567,7 @@ __device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, uint32_t lo0,
     t.hi = second ? hi1 : hi0;
     const uint32_t v = (t.w << 5) + lane;
     t.in = v >= t.lo && v < t.hi;
+    t.mask = mask ? ldcg(mask + t.w) : ~0u;
     if (t.in) {
       load(v, t.aux);
       t.b = __ldg(p.g.off + v);
@@ -576,7 +578,7 @@ __device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, uint32_t lo0,
   // tile's edge span into stage `s`
   auto prepare = [&](uint32_t s, Tile& t) {
     const uint32_t v = (t.w << 5) + lane;
-    t.work = t.in && test(v, t.aux);
+    t.work = t.in && ((t.mask >> lane) & 1u) && test(v, t.aux);
     t.any = __any_sync(0xffffffffu, t.work);
     t.staged = false;
     if (!t.any) return;
@@ -692,7 +694,7 @@ __device__ __noinline__ void dense_light_p1(const SolveParams<V>& p, uint32_t lo
     return false;
   };
   auto fallback = [&](uint32_t v, V) { return lift_thread<V, false>(p, v, L); };
-  tma_tiles<V>(p, lo, hi, 0u, 0u, cursor, chg, L, load, test, row, fallback);
+  tma_tiles<V>(p, lo, hi, 0u, 0u, cursor, nullptr, chg, L, load, test, row, fallback);
   block_flush(L, p.ctr, sum_dst, s_cnt);
 }
 
@@ -850,19 +852,38 @@ __device__ __noinline__ void block_rows(const SolveParams<V>& p, uint32_t count,
 // nothing.  Every candidate left is in W1: under the good-edge choices every
 // step inside the set changes the energy by w <= f(t) - f(v) - 1, so any
 // cycle player 0 can close there is negative.
-// Candidate values live in p.stage: f(t) for a candidate, top for a vertex
-// already at top, kNotCand otherwise -- one gather per edge.
+// Candidates are marked twice: a bit in p.cand (one per vertex, 2 MB at
+// C4: tile masks, the sparse passes, apply) and the top bit of their value in
+// f (kCand, free because credit_cap < 2^(bits-1) - 1 on the device), so an
+// edge test is ONE gather: good(v,t) = f(t) = top, or f(t) carries kCand and
+// f(v) < value(t) - w(v,t).  f is not otherwise written during the
+// certificate; a removed candidate gets its plain value back, a certified one
+// becomes top (which has every bit set), so no mark outlives the attempt.
 template <class V>
-struct NotCand {
-  static constexpr V v = Top<V>::v - 1;
+struct CandFlag {
+  static constexpr V v = V(1) << (sizeof(V) * 8 - 1);
 };
-
 template <class V>
-__device__ __forceinline__ bool good_edge(const SolveParams<V>& p, int64_t fv,
-                                          int2 r) {
-  const V ct = gather(p.stage + r.x);
-  if (ct == Top<V>::v) return true;
-  return ct != NotCand<V>::v && fv < static_cast<int64_t>(ct) - r.y;
+__device__ __forceinline__ int64_t cand_value(V x) {
+  return static_cast<int64_t>(x & ~CandFlag<V>::v);
+}
+template <class V>
+__device__ __forceinline__ bool good_target(int64_t fv, V ft, int w) {
+  return ft == Top<V>::v || ((ft & CandFlag<V>::v) && fv < cand_value<V>(ft) - w);
+}
+template <class V>
+__device__ __forceinline__ bool cand_bit(const SolveParams<V>& p, uint32_t v) {
+  return (ldcg(p.cand + (v >> 5)) >> (v & 31u)) & 1u;
+}
+// removal of candidate v with value fv: clear its bit and its mark in f
+template <class V>
+__device__ __forceinline__ void cand_clear(const SolveParams<V>& p, uint32_t v, int64_t fv) {
+  atomicAnd(p.cand + (v >> 5), ~(1u << (v & 31u)));
+  stcg(p.f + v, static_cast<V>(fv));
+}
+template <class V>
+__device__ __forceinline__ bool good_edge(const SolveParams<V>& p, int64_t fv, int2 r) {
+  return good_target<V>(fv, gather(p.f + r.x), r.y);
 }
 
 #ifndef EGS_CERT_CHUNK
@@ -880,12 +901,11 @@ __device__ __forceinline__ bool cert_keep_thread(const SolveParams<V>& p,
     for (int k = 0; k < kCertChunk; ++k) r[k] = ld_rec(p.g, min(i + k, e - 1));
     V c[kCertChunk];
 #pragma unroll
-    for (int k = 0; k < kCertChunk; ++k) c[k] = gather(p.stage + r[k].x);
+    for (int k = 0; k < kCertChunk; ++k) c[k] = gather(p.f + r[k].x);
     bool all = true, any = false;
 #pragma unroll
     for (int k = 0; k < kCertChunk; ++k) {
-      const bool g = c[k] == Top<V>::v ||
-                     (c[k] != NotCand<V>::v && fv < static_cast<int64_t>(c[k]) - r[k].y);
+      const bool g = good_target<V>(fv, c[k], r[k].y);
       all &= g;
       any |= g;
     }
@@ -1024,7 +1044,7 @@ __device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo0,
     }
     return finish(v, p0, minw, maxw, __ldg(erecs(g) + imax), e - b);
   };
-  tma_tiles<V>(p, lo0, hi0, lo1, hi1, cursor, chg, L, load, test, row, fallback);
+  tma_tiles<V>(p, lo0, hi0, lo1, hi1, cursor, nullptr, chg, L, load, test, row, fallback);
   block_flush(L, p.ctr, sum_dst, s_cnt);
 }
 
@@ -1253,76 +1273,80 @@ __device__ __noinline__ void phase_commit(const SolveParams<V>& p, const uint32_
 // Certificate, step 1: the candidates are the non-top vertices raised in the
 // round just finished (`chg`): losing vertices keep climbing, and starting
 // from any subset is sound (the pruned set is still closed).  Candidate
-// values are a snapshot of f in p.stage.
+// bits go to p.cand, one word per 32 vertices.
 template <class V>
 __device__ __noinline__ void phase_cert_init(const SolveParams<V>& p, const uint32_t* chg,
                                              unsigned int* slot_sum) {
   __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
   const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
   const uint32_t nthreads = gridDim.x * kBlock;
+  const uint32_t nwarps = gridDim.x * kWarps;
+  const uint32_t gw = tid >> 5, lane = lane_id();
   Local L;
   for (uint32_t w = tid; w < ((p.g.n + 31) >> 5); w += nthreads) p.rbm[1][w] = 0u;
-  for (uint32_t v = p.own_lo + tid; v < p.own_hi; v += nthreads) {
-    const V fv = ldcg(p.f + v);
-    const bool raised = (ldcg(chg + (v >> 5)) >> (v & 31u)) & 1u;
-    stcg(p.stage + v, fv == Top<V>::v ? fv : raised ? fv : NotCand<V>::v);
+  const uint32_t wlo = p.own_lo >> 5, whi = (p.own_hi + 31) >> 5;
+  for (uint32_t w = wlo + gw; w < whi; w += nwarps) {
+    const uint32_t v = (w << 5) + lane;
+    const uint32_t bits = ldcg(chg + w);
+    const bool in = v >= p.own_lo && v < p.own_hi;
+    const V fv = in ? ldcg(p.f + v) : Top<V>::v;
+    const bool c = in && ((bits >> lane) & 1u) && fv != Top<V>::v;
+    if (c) stcg(p.f + v, fv | CandFlag<V>::v);
+    const uint32_t m = __ballot_sync(0xffffffffu, c);
+    if (lane == 0) stcg(p.cand + w, m);
   }
   block_flush(L, p.ctr, slot_sum + 1, s_cnt);
 }
 
-// Commit fused with certificate step 1 (one pass over the vertices instead
-// of two): a raised vertex publishes its staged value and, unless it reached
-// top, becomes a candidate with that value; every other vertex is top or
-// not a candidate.
+// Commit fused with certificate step 1 (one pass over the words of `chg`
+// instead of two): a raised vertex publishes its staged value and, unless it
+// reached top, becomes a candidate (bit + mark).
 template <class V>
 __device__ __noinline__ void phase_commit_cert_init(const SolveParams<V>& p, const uint32_t* chg) {
   constexpr V TOP = Top<V>::v;
-  constexpr int U = 4;  // vertices per thread per step, loads issued together
-  const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
-  const uint32_t nthreads = gridDim.x * kBlock;
+  constexpr int U = 8;  // words per warp step, all loads issued before any store
   const uint32_t nwords = (p.g.n + 31) >> 5;
-  for (uint32_t w = tid; w < nwords; w += nthreads) p.rbm[1][w] = 0u;
-  for (uint32_t v0 = p.own_lo + tid; v0 < p.own_hi; v0 += nthreads * U) {
+  const uint32_t nwarps = gridDim.x * kWarps;
+  const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
+  const uint32_t gw = tid >> 5, lane = lane_id();
+  for (uint32_t w = tid; w < nwords; w += gridDim.x * kBlock) p.rbm[1][w] = 0u;
+  const uint32_t wlo = p.own_lo >> 5, whi = min(nwords, (p.own_hi + 31) >> 5);
+  for (uint32_t w0 = wlo + gw * U; w0 < whi; w0 += nwarps * U) {
     uint32_t bits[U];
-    V fv[U], sv[U];
+    V val[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) bits[k] = w0 + k < whi ? ldcg(chg + w0 + k) : 0u;
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-      const uint32_t v = v0 + k * nthreads;
-      const bool in = v < p.own_hi;
-      bits[k] = in ? ldcg(chg + (v >> 5)) : 0u;
-      fv[k] = in ? ldcg(p.f + v) : TOP;
-      sv[k] = in ? ldcg(p.stage + v) : TOP;
+      const uint32_t v = ((w0 + k) << 5) + lane;
+      val[k] = ((bits[k] >> lane) & 1u) ? ldcg(p.stage + v) : TOP;
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-      const uint32_t v = v0 + k * nthreads;
-      if (v >= p.own_hi) continue;
-      const bool raised = (bits[k] >> (v & 31u)) & 1u;
-      const V val = raised ? sv[k] : fv[k];
-      if (raised) stcg(p.f + v, val);
-      stcg(p.stage + v, val == TOP ? TOP : raised ? val : NotCand<V>::v);
+      if (w0 + k >= whi) break;
+      const bool raised = (bits[k] >> lane) & 1u;
+      const bool c = raised && val[k] != TOP;
+      if (raised) stcg(p.f + ((w0 + k) << 5) + lane, c ? val[k] | CandFlag<V>::v : val[k]);
+      const uint32_t m = __ballot_sync(0xffffffffu, c);
+      if (lane == 0) stcg(p.cand + w0 + k, m);
     }
   }
 }
 
-// Certificate, step 2: pruning passes.  A removed candidate becomes
-// kNotCand in p.stage and its bit is set in `rbm` (removed in this pass), so
-// the next pass can be sparse: only candidate predecessors of this pass's
-// removals (phase_cert_mark, via the CSC) can lose their condition.
-template <class V>
-__device__ __forceinline__ bool is_cand(V c) {
-  return c != Top<V>::v && c != NotCand<V>::v;
-}
+// Certificate, step 2: pruning passes.  A removed candidate loses its bit
+// in p.cand and its mark in f and gets a bit in `rbm` (removed in this pass), so the next pass
+// can be sparse: only candidate predecessors of this pass's removals
+// (phase_cert_mark, via the CSC) can lose their condition.
 
 // One candidate, evaluated by the lanes a row's class gets; returns removed.
 template <class V>
 __device__ __forceinline__ bool cert_check_thread(const SolveParams<V>& p, uint32_t v, Local& L) {
-  const V cvv = ldcg(p.stage + v);
-  if (!is_cand<V>(cvv)) return false;
-  const bool keep = v < p.g.rb[kP1L] ? cert_keep_thread<V, true>(p, v, (int64_t)cvv, L)
-                                     : cert_keep_thread<V, false>(p, v, (int64_t)cvv, L);
+  if (!cand_bit(p, v)) return false;
+  const int64_t fv = cand_value<V>(ldcg(p.f + v));
+  const bool keep = v < p.g.rb[kP1L] ? cert_keep_thread<V, true>(p, v, fv, L)
+                                     : cert_keep_thread<V, false>(p, v, fv, L);
   ++L.cert_scanned;
-  if (!keep) stcg(p.stage + v, NotCand<V>::v);
+  if (!keep) cand_clear(p, v, fv);
   return !keep;
 }
 
@@ -1342,14 +1366,14 @@ __device__ __forceinline__ void cert_long_rows(const SolveParams<V>& p, uint32_t
     if (i >= nH) break;
     const uint32_t v = itemsH(i);
     if (!owned(p, v)) continue;
-    const V cvv = ldcg(p.stage + v);
-    if (!is_cand<V>(cvv)) continue;
-    const bool keep = v < g.rb[kP1L] ? cert_keep_block<V, true>(p, v, (int64_t)cvv, L)
-                                     : cert_keep_block<V, false>(p, v, (int64_t)cvv, L);
+    if (!cand_bit(p, v)) continue;
+    const int64_t fv = cand_value<V>(ldcg(p.f + v));
+    const bool keep = v < g.rb[kP1L] ? cert_keep_block<V, true>(p, v, fv, L)
+                                     : cert_keep_block<V, false>(p, v, fv, L);
     if (threadIdx.x == 0) {
       ++L.cert_scanned;
       if (!keep) {
-        stcg(p.stage + v, NotCand<V>::v);
+        cand_clear(p, v, fv);
         set_bit(rbm, v);
         ++L.phase_count;
       }
@@ -1361,14 +1385,14 @@ __device__ __forceinline__ void cert_long_rows(const SolveParams<V>& p, uint32_t
   while (warp_claim(slot_dyn + 0, nM, wc, i)) {
     const uint32_t v = itemsM(i);
     if (!owned(p, v)) continue;
-    const V cvv = ldcg(p.stage + v);
-    if (!is_cand<V>(cvv)) continue;
-    const bool keep = v < g.rb[kP1L] ? cert_keep_warp<V, true>(p, v, (int64_t)cvv, L)
-                                     : cert_keep_warp<V, false>(p, v, (int64_t)cvv, L);
+    if (!cand_bit(p, v)) continue;
+    const int64_t fv = cand_value<V>(ldcg(p.f + v));
+    const bool keep = v < g.rb[kP1L] ? cert_keep_warp<V, true>(p, v, fv, L)
+                                     : cert_keep_warp<V, false>(p, v, fv, L);
     if (lane_id() == 0) {
       ++L.cert_scanned;
       if (!keep) {
-        stcg(p.stage + v, NotCand<V>::v);
+        cand_clear(p, v, fv);
         set_bit(rbm, v);
         ++L.phase_count;
       }
@@ -1395,10 +1419,10 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
   // light candidates: one row per lane through the TMA tile pipeline (tiles
   // without a candidate are skipped); removals are published in rbm
   {
-    auto load = [&](uint32_t v, V& cv) { cv = ldcg(p.stage + v); };
-    auto test = [&](uint32_t, V cv) { return is_cand<V>(cv); };
+    auto load = [&](uint32_t v, V& fv) { fv = ldcg(p.f + v); };
+    auto test = [&](uint32_t, V) { return true; };  // the tile mask is the candidate word
     auto row = [&](uint32_t v, const ERec* rec, uint32_t len, uint32_t, V cv) {
-      const int64_t fv = (int64_t)cv;
+      const int64_t fv = cand_value<V>(cv);
       const bool p0 = v < g.rb[kP1L];
       const uint32_t rot = row_rot(len);
       ++L.cert_scanned;
@@ -1413,12 +1437,11 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
         }
         V c[kCertChunk];
 #pragma unroll
-        for (int k = 0; k < kCertChunk; ++k) c[k] = gather(p.stage + r[k].x);
+        for (int k = 0; k < kCertChunk; ++k) c[k] = gather(p.f + r[k].x);
         bool all = true, any = false;
 #pragma unroll
         for (int k = 0; k < kCertChunk; ++k) {
-          const bool gd = c[k] == Top<V>::v ||
-                          (c[k] != NotCand<V>::v && fv < static_cast<int64_t>(c[k]) - r[k].y);
+          const bool gd = good_target<V>(fv, c[k], r[k].y);
           all &= gd;
           any |= gd;
         }
@@ -1432,13 +1455,13 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
           break;
         }
       }
-      if (!keep) stcg(p.stage + v, NotCand<V>::v);
+      if (!keep) cand_clear(p, v, fv);
       return !keep;
     };
     auto fallback = [&](uint32_t v, V) { return cert_check_thread<V>(p, v, L); };
     tma_tiles<V>(p, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]), clip_lo(p, g.rb[kP1L]),
-                 clip_hi(p, g.rb[kP1M]), slot_dyn + kTileCursor, rbm, L, load, test, row,
-                 fallback);
+                 clip_hi(p, g.rb[kP1M]), slot_dyn + kTileCursor, p.cand, rbm, L, load, test,
+                 row, fallback);
   }
   block_flush(L, p.ctr, slot_sum + 1, s_cnt);
 }
@@ -1473,7 +1496,7 @@ __device__ __noinline__ void phase_cert_mark(const SolveParams<V>& p, const uint
         int c = 0;
         if (valid) {
           v = __ldg(g.csrc + idx);
-          if (owned(p, v) && is_cand<V>(ldcg(p.stage + v))) {
+          if (owned(p, v) && cand_bit(p, v)) {
             const uint32_t bit = 1u << (v & 31u);
             add = !(atomicOr(p.cbm + (v >> 5), bit) & bit);
             c = size_class(g, v);
@@ -1530,26 +1553,21 @@ template <class V>
 __device__ __noinline__ void phase_cert_apply(const SolveParams<V>& p, uint32_t* chg,
                                               unsigned int* slot_sum) {
   __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
-  const uint32_t n = p.g.n;
   const uint32_t nwarps = gridDim.x * kWarps;
   const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const uint32_t lane = lane_id();
   Local L;
-  constexpr uint32_t U = 4;  // words per warp step, loads issued together
+  constexpr uint32_t U = 8;  // words per warp step, loads issued together
   const uint32_t w_lo = p.own_lo >> 5, w_hi = (p.own_hi + 31) >> 5;
   for (uint32_t w0 = w_lo + gw * U; w0 < w_hi; w0 += nwarps * U) {
-    V cv[U];
+    uint32_t m[U];
+#pragma unroll
+    for (uint32_t k = 0; k < U; ++k) m[k] = w0 + k < w_hi ? ldcg(p.cand + w0 + k) : 0u;
 #pragma unroll
     for (uint32_t k = 0; k < U; ++k) {
-      const uint32_t v = ((w0 + k) << 5) + lane_id();
-      cv[k] = (w0 + k < w_hi && v < n && owned(p, v)) ? ldcg(p.stage + v) : Top<V>::v;
-    }
-#pragma unroll
-    for (uint32_t k = 0; k < U; ++k) {
-      const uint32_t v = ((w0 + k) << 5) + lane_id();
-      const bool hit = is_cand<V>(cv[k]);
-      if (hit) stcg(p.f + v, Top<V>::v);
-      const uint32_t m = __ballot_sync(0xffffffffu, hit);
-      if (m && lane_id() == 0) atomicOr(chg + w0 + k, m);
+      const bool hit = (m[k] >> lane) & 1u;  // candidate words hold owned, non-top ids only
+      if (hit) stcg(p.f + ((w0 + k) << 5) + lane, Top<V>::v);
+      if (m[k] && lane == 0) atomicOr(chg + w0 + k, m[k]);
       L.phase_count += hit;
       L.certified += hit;
     }
@@ -1767,7 +1785,10 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
     // `changed` vertices were raised by round `round`, marked in chg
     uint32_t* chg = p.chg[(round - 1) & 1];
     if (changed == 0) break;  // a round that raised nothing: least fixpoint
-    const bool cert_now = p.certify && round >= next_cert;
+    // (no attempt in a round that stops the solve: the candidate marks in f
+    // never outlive an attempt)
+    const bool cert_now = p.certify && round >= next_cert && round < p.round_budget &&
+                          !vload(&sh->stop);
     // without a certificate attempt the next round's mode is known already:
     // a sparse next round gets its activation in the commit phase (the
     // activation's top filter may see either the old or the committed value

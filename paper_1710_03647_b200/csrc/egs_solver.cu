@@ -168,6 +168,7 @@ struct egs_ctx {
   uint32_t* frb = nullptr;
   uint32_t* rbm[2] = {nullptr, nullptr};
   uint32_t* cbm = nullptr;
+  uint32_t* cand = nullptr;  // certificate candidate bitmap (n_pad / 32 words)
   uint32_t* longcol = nullptr;
   uint32_t* fr[2] = {nullptr, nullptr};
   void* stage = nullptr;
@@ -252,7 +253,7 @@ void ctx_free(egs_ctx* c) {
   if (c->device >= 0) cudaSetDevice(c->device);
   void* ptrs[] = {c->off,    c->edge,   c->coff, c->csrc,  c->perm, c->inv,
                   c->f,      c->wit,    c->chg[0], c->chg[1], c->frb,
-                  c->fr[0],  c->fr[1],  c->stage, c->scratch, c->ctr, c->rbm[0], c->rbm[1], c->cbm, c->trace, c->longcol,
+                  c->fr[0],  c->fr[1],  c->stage, c->scratch, c->ctr, c->rbm[0], c->rbm[1], c->cbm, c->cand, c->trace, c->longcol,
                   c->f64};
   if (c->stream) {
     for (void* p : ptrs) dfree(p, c->stream);
@@ -597,9 +598,10 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     c->n = a->num_vertices;
     c->m = a->num_edges;
     c->cap = a->credit_cap;
-    // u32 values need top (2^32-1) and the certificate's not-a-candidate
-    // marker (2^32-2) above every finite credit <= credit_cap
-    c->vbits = a->credit_cap < 0xFFFFFFFELL ? 32 : 64;
+    // u32 values keep top = 2^32-1 and the top bit free for the
+    // certificate's candidate mark (egs_solve.cuh CandFlag): every finite
+    // credit <= credit_cap must stay below 2^31 - 1
+    c->vbits = a->credit_cap < 0x7FFFFFFFLL ? 32 : 64;
     const uint32_t n = c->n;
     const size_t vsz = c->vbits / 8;
     const size_t words = ((size_t)n + 31) / 32;
@@ -621,6 +623,9 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     c->rbm[0] = dalloc<uint32_t>(words);
     c->rbm[1] = dalloc<uint32_t>(words);
     c->cbm = dalloc<uint32_t>(words);
+    c->cand = dalloc<uint32_t>(std::max<size_t>(words, ((size_t)c->n_pad + 31) / 32));
+    CK(cudaMemsetAsync(c->cand, 0, std::max<size_t>(words, ((size_t)c->n_pad + 31) / 32) * 4,
+                       c->stream));
     // at most m / kLongCol columns are longer than kLongCol
     c->longcol = dalloc<uint32_t>(2 * (a->num_edges / egs::kLongCol + 1));
     c->fr[0] = dalloc<uint32_t>(n);
@@ -720,6 +725,7 @@ egs::SolveParams<V> make_params(egs_ctx* c, unsigned long long* budget_out) {
   p.rbm[0] = c->rbm[0];
   p.rbm[1] = c->rbm[1];
   p.cbm = c->cbm;
+  p.cand = c->cand;
   p.longcol = c->longcol;
   p.fr[0] = c->fr[0];
   p.fr[1] = c->fr[1];
@@ -732,7 +738,9 @@ egs::SolveParams<V> make_params(egs_ctx* c, unsigned long long* budget_out) {
   p.trace = c->trace;
   p.mode = o.mode;
   p.use_tma = o.no_tma ? 0 : 1;
-  p.certify = o.certify;
+  // the candidate mark needs a free top bit: u64 values with credit_cap at
+  // INT64_MAX (a saturated cap) solve without the certificate (still exact)
+  p.certify = o.certify && !(c->vbits == 64 && c->cap >= INT64_MAX - 1);
   p.cert_interval = o.cert_interval > 0 ? o.cert_interval : 1;
   p.cert_growth = o.cert_growth > 0 ? o.cert_growth : 4;
   p.sparse_div = o.sparse_div > 0 ? (uint32_t)o.sparse_div : 4u;
@@ -1056,6 +1064,7 @@ int egs_part_create(const egs_arena_view* arena, const egs_gpu_opts* opts, int32
       layout->value_bytes = (uint32_t)(c->vbits / 8);
       layout->f_dev = (uint64_t)(uintptr_t)c->f;
       layout->stage_dev = (uint64_t)(uintptr_t)c->stage;
+      layout->cand_dev = (uint64_t)(uintptr_t)c->cand;
     }
     *out = p;
   });

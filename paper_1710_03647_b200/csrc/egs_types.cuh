@@ -81,13 +81,13 @@ template <class V>
 struct SolveParams {
   Graph g;
   V* f;                 // measure, relabelled ids (read-only inside a lift round)
-  V* stage;             // lift rounds: raised values, committed after the round;
-                        // certificate: candidate values (f, or kNotCand)
+  V* stage;             // lift rounds: raised values, committed after the round
   void* wit;            // player-0 witness edge record (ids < rb[3]), edge format
   uint32_t* chg[2];     // changed-vertex bitmaps, by round parity
   uint32_t* frb;        // frontier membership bitmap
   uint32_t* rbm[2];     // certificate: removed-in-pass bitmaps
   uint32_t* cbm;        // certificate: re-check dedup bitmap
+  uint32_t* cand;       // certificate: candidate bitmap
   uint32_t* longcol;    // activation: queued long CSC columns {vertex, chunk cursor}
   uint32_t* fr[2];      // frontier lists; sublist c starts at cbase[c]
   uint32_t cbase[3];

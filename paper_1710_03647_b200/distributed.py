@@ -79,6 +79,9 @@ class DeviceSteps:
         count = max(self.padded, 1)
         self.f = torch.as_tensor(_CudaArray(lay.f_dev, count, typestr), device=dev)
         self.stage = torch.as_tensor(_CudaArray(lay.stage_dev, count, typestr), device=dev)
+        # certificate candidate bitmap: one u32 word per 32 vertices
+        self.cand = torch.as_tensor(_CudaArray(lay.cand_dev, max(self.padded // 32, 1), "<i4"),
+                                    device=dev)
         self._counts = (C.c_uint64 * 2)()
 
     def step(self, kind: int, parity: int):
@@ -202,11 +205,13 @@ def solve_partitioned(steps, comm, certify: bool = True, cert_interval: int = 1,
             raise N.TimeoutError_("solve timed out")
         if certify and rounds >= next_cert:
             attempts += 1
+            # candidates carry a mark in f (egs_solve.cuh CandFlag): the passes
+            # read the other ranks' marks, so f is exchanged after each step
             step(STEP_CERT_INIT, parity)
-            comm.allgather(steps.stage, steps.slice)
+            comm.allgather(steps.f, steps.slice)
             while True:
                 removed = comm.allreduce_sum(step(STEP_CERT_PRUNE, parity)[1])
-                comm.allgather(steps.stage, steps.slice)
+                comm.allgather(steps.f, steps.slice)
                 passes += 1
                 if removed == 0:
                     break

@@ -11,7 +11,7 @@ import torch
 from paper_1710_03647_b200.distributed import partition_layout
 
 TOP = np.iinfo(np.int64).max
-NOTCAND = TOP - 1
+CAND = np.int64(1) << np.int64(62)  # the certificate's candidate mark in f (values < 2^62)
 
 
 class NumpySteps:
@@ -31,6 +31,10 @@ class NumpySteps:
         r = np.maximum(ft - w, 0)
         r = np.where(r > self.cap, TOP, r)
         return np.where(ft == TOP, TOP, r)
+
+    @staticmethod
+    def _is_cand(x):
+        return (x != TOP) & ((x & CAND) != 0)
 
     def _rows(self):
         lo, hi = self.own_lo, self.own_hi
@@ -66,29 +70,30 @@ class NumpySteps:
             idx = np.nonzero(chg)[0]
             f[idx] = st[idx]
             return 0, 0
-        if kind == 3:  # certificate init
-            fo = f[lo:hi]
-            st[lo:hi] = np.where(fo == TOP, TOP, np.where(chg[lo:hi], fo, NOTCAND))
+        if kind == 3:  # certificate init: raised, non-top vertices get the mark
+            c = chg[lo:hi] & (f[lo:hi] != TOP)
+            f[lo:hi][c] |= CAND
             return 0, 0
         if kind == 4:  # one pruning pass (snapshot semantics; same greatest fixpoint)
             if hi <= lo:
                 return 0, 0
             b, e = roff[0], roff[-1]
-            ct = st[self.dst[b:e]]
+            t = self.dst[b:e]
+            ft = f[t]
             src = np.repeat(np.arange(lo, hi), np.diff(roff))
-            fv = st[src]
+            fv = f[src] & ~CAND
             with np.errstate(over="ignore"):
-                good = (ct == TOP) | ((ct != NOTCAND) & (fv < ct - self.w[b:e]))
+                good = (ft == TOP) | (self._is_cand(ft) & (fv < (ft & ~CAND) - self.w[b:e]))
             seg = roff[:-1] - b
             allg = np.minimum.reduceat(good.astype(np.int8), seg).astype(bool)
             anyg = np.maximum.reduceat(good.astype(np.int8), seg).astype(bool)
             keep = np.where(self.p0[lo:hi], allg, anyg)
-            cand = (st[lo:hi] != TOP) & (st[lo:hi] != NOTCAND)
-            drop = cand & ~keep
-            st[lo:hi][drop] = NOTCAND
+            own = f[lo:hi]
+            drop = self._is_cand(own) & ~keep
+            own[drop] &= ~CAND
             return 0, int(drop.sum())
         if kind == 5:  # apply
-            cand = (st[lo:hi] != TOP) & (st[lo:hi] != NOTCAND) & (f[lo:hi] != TOP)
+            cand = self._is_cand(f[lo:hi])
             f[lo:hi][cand] = TOP
             chg[lo:hi] |= cand
             return int(cand.sum()), 0

@@ -166,7 +166,7 @@ def test_canonical_golden_1e5(egs, golden, key, args):
     rep = _solve(egs, a)
     sol = egs.write_solution(a, rep).encode()
     assert f"{fnv1a64(sol):016x}" == rec["solution_fnv"]
-    assert rep.gpu["value_bits"] == (64 if rec["credit_cap"] >= 2 ** 32 - 2 else 32)
+    assert rep.gpu["value_bits"] == (64 if rec["credit_cap"] >= 2 ** 31 - 1 else 32)
 
 
 def test_rmat16_golden(egs, golden):
@@ -180,9 +180,10 @@ def test_rmat16_golden(egs, golden):
 
 
 def test_value_width_boundary(egs, oracle):
-    # credit_cap = 2^32 - 3 stays on the u32 path, 2^32 - 2 takes u64
-    # (u32 reserves 2^32 - 1 for top and 2^32 - 2 for the certificate)
-    for cap in (2 ** 32 - 3, 2 ** 32 - 2):
+    # credit_cap = 2^31 - 2 stays on the u32 path, 2^31 - 1 takes u64 (u32
+    # reserves 2^32 - 1 for top and the top bit for the certificate's mark);
+    # 2^32 - 2 is the old boundary, now deep in the u64 range
+    for cap in (2 ** 31 - 2, 2 ** 31 - 1, 2 ** 32 - 3, 2 ** 32 - 2):
         x = [cap // 3, cap // 3, cap - 2 * (cap // 3)]
         edges = [(0, 1, -x[0]), (1, 2, -x[1]), (2, 0, -x[2]), (0, 0, 3), (1, 1, 1),
                  (2, 2, 0), (2, 1, 7)]
@@ -193,7 +194,7 @@ def test_value_width_boundary(egs, oracle):
         want, _ = oracle.solve_seq(g)
         rep = _solve(egs, a)
         assert np.array_equal(rep.measure, want)
-        assert rep.gpu["value_bits"] == (32 if cap < 2 ** 32 - 2 else 64)
+        assert rep.gpu["value_bits"] == (32 if cap < 2 ** 31 - 1 else 64)
 
 
 def test_device_context_reuse_and_epm(egs, oracle):
