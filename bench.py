@@ -306,11 +306,14 @@ def run_our_arm(a):
         egs.solve(arena, options=opts, out=out)
     barrier(world)
     e2e_t, e2e_edges = 0.0, 0
+    e2e_steps = []
     for _ in range(a.e2e_steps):
         t1 = time.perf_counter()
         rep = egs.solve(arena, options=opts, out=out)
-        e2e_t += time.perf_counter() - t1
+        e2e_steps.append(time.perf_counter() - t1)
         e2e_edges += rep.gpu["edges_relaxed"]
+    e2e_t = sum(e2e_steps)
+    log("e2e steps (ms): " + " ".join(f"{x * 1e3:.1f}" for x in e2e_steps))
     barrier(world)
     e2e_t = max_over_ranks(e2e_t, world, "cuda")
     e2e_edges = sum_over_ranks(e2e_edges, world, "cuda")
