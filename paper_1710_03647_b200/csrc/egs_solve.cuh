@@ -34,6 +34,7 @@
 #include <cooperative_groups.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "egs_device.cuh"
 #include "egs_types.cuh"
@@ -890,6 +891,10 @@ __device__ __forceinline__ bool good_edge(const SolveParams<V>& p, int64_t fv, i
 #define EGS_CERT_CHUNK 4
 #endif
 constexpr int kCertChunk = EGS_CERT_CHUNK;  // edges tested per step (early exit between)
+#ifndef EGS_CERT_CHUNK_P0
+#define EGS_CERT_CHUNK_P0 8
+#endif
+constexpr int kCertChunkP0 = EGS_CERT_CHUNK_P0;  // player-0 rows in the TMA pass
 
 template <class V, bool P0>
 __device__ __forceinline__ bool cert_keep_thread(const SolveParams<V>& p,
@@ -1421,40 +1426,45 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
   {
     auto load = [&](uint32_t v, V& fv) { fv = ldcg(p.f + v); };
     auto test = [&](uint32_t, V) { return true; };  // the tile mask is the candidate word
+    // a pass keeps most player-0 candidates, and keeping one reads its whole
+    // row: player-0 rows test kCertChunkP0 edges per step, player-1 rows
+    // (kept by their first good edge) kCertChunk
+    auto scan = [&](auto chunk, bool p0, const ERec* rec, uint32_t len, uint32_t rot,
+                    int64_t fv) {
+      constexpr int C = decltype(chunk)::value;
+      for (uint32_t k0 = 0; k0 < len; k0 += C) {
+        int2 r[C];
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+          uint32_t j = min(k0 + k, len - 1) + rot;
+          j = j >= len ? j - len : j;
+          r[k] = dec(g, rec[j]);
+        }
+        V c[C];
+#pragma unroll
+        for (int k = 0; k < C; ++k) c[k] = gather(p.f + r[k].x);
+        bool all = true, any = false;
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+          const bool gd = good_target<V>(fv, c[k], r[k].y);
+          all &= gd;
+          any |= gd;
+        }
+        L.cert_edges += min((uint32_t)C, len - k0);
+        if (p0 && !all) return false;
+        if (!p0 && any) return true;
+      }
+      return p0;
+    };
     auto row = [&](uint32_t v, const ERec* rec, uint32_t len, uint32_t, V cv) {
       const int64_t fv = cand_value<V>(cv);
       const bool p0 = v < g.rb[kP1L];
       const uint32_t rot = row_rot(len);
       ++L.cert_scanned;
-      bool keep = p0;
-      for (uint32_t k0 = 0; k0 < len; k0 += kCertChunk) {
-        int2 r[kCertChunk];
-#pragma unroll
-        for (int k = 0; k < kCertChunk; ++k) {
-          uint32_t j = min(k0 + k, len - 1) + rot;
-          j = j >= len ? j - len : j;
-          r[k] = dec(g, rec[j]);
-        }
-        V c[kCertChunk];
-#pragma unroll
-        for (int k = 0; k < kCertChunk; ++k) c[k] = gather(p.f + r[k].x);
-        bool all = true, any = false;
-#pragma unroll
-        for (int k = 0; k < kCertChunk; ++k) {
-          const bool gd = good_target<V>(fv, c[k], r[k].y);
-          all &= gd;
-          any |= gd;
-        }
-        L.cert_edges += min((uint32_t)kCertChunk, len - k0);
-        if (p0 && !all) {
-          keep = false;
-          break;
-        }
-        if (!p0 && any) {
-          keep = true;
-          break;
-        }
-      }
+      const bool keep = p0 ? scan(std::integral_constant<int, kCertChunkP0>{}, true, rec, len,
+                                  rot, fv)
+                           : scan(std::integral_constant<int, kCertChunk>{}, false, rec, len,
+                                  rot, fv);
       if (!keep) cand_clear(p, v, fv);
       return !keep;
     };
