@@ -179,6 +179,10 @@ typedef struct egs_part_layout {
   uint64_t stage_dev;     /* device address of the replicated staging array */
   uint64_t cand_dev;      /* device address of the replicated certificate candidate
                              bitmap (padded / 32 u32 words) */
+  uint64_t send_dev;      /* sparse exchange: this rank's packed entries (slice entries) */
+  uint64_t recv_dev;      /* sparse exchange: world * slice entries, rank r's at r * stride */
+  uint32_t entry_bytes;   /* 8 ({id << 32 | u32 value}) or 16 ({id, u64 value}) */
+  uint32_t reserved0;
 } egs_part_layout;
 
 #define EGS_STEP_ROUND1 0     /* seeding + round 1 from the weights */
@@ -197,6 +201,16 @@ int egs_part_create(const egs_arena_view* arena, const egs_gpu_opts* opts, int32
  * LIFT) or certified (CERT_APPLY); counts[1] = candidates removed
  * (CERT_PRUNE).  Blocks until the step is done. */
 int egs_part_step(egs_part* part, int32_t step, int32_t parity, uint64_t* counts);
+/* Sparse exchange.  egs_part_pack writes this rank's vertices
+ * marked by `which` -- EGS_PACK_CHANGED: raised in the round of `parity`
+ * (after EGS_STEP_COMMIT); EGS_PACK_REMOVED: dropped by the last
+ * EGS_STEP_CERT_PRUNE -- as (id, value) entries to send_dev; *count = entries.
+ * After the host all-gathers them into recv_dev (rank r's entries at
+ * r * stride), egs_part_unpack scatters the other ranks' entries into f. */
+#define EGS_PACK_CHANGED 0
+#define EGS_PACK_REMOVED 1
+int egs_part_pack(egs_part* part, int32_t which, int32_t parity, uint32_t* count);
+int egs_part_unpack(egs_part* part, const uint32_t* counts, uint32_t stride);
 /* Resets f, the bitmaps and the counters for a new solve. */
 int egs_part_reset(egs_part* part);
 /* The replicated measure in the reference's raw encoding, original ids. */

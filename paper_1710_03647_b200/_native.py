@@ -135,6 +135,8 @@ class PartLayout(C.Structure):
         ("num_vertices", C.c_uint32), ("slice", C.c_uint32), ("padded", C.c_uint32),
         ("own_lo", C.c_uint32), ("own_hi", C.c_uint32), ("value_bytes", C.c_uint32),
         ("f_dev", C.c_uint64), ("stage_dev", C.c_uint64), ("cand_dev", C.c_uint64),
+        ("send_dev", C.c_uint64), ("recv_dev", C.c_uint64), ("entry_bytes", C.c_uint32),
+        ("reserved0", C.c_uint32),
     ]
 
 
@@ -144,6 +146,10 @@ lib.egs_part_create.argtypes = [C.POINTER(ArenaView), C.POINTER(GpuOpts), C.c_in
 lib.egs_part_create.restype = C.c_int
 lib.egs_part_step.argtypes = [_P, C.c_int32, C.c_int32, C.POINTER(C.c_uint64)]
 lib.egs_part_step.restype = C.c_int
+lib.egs_part_pack.argtypes = [_P, C.c_int32, C.c_int32, C.POINTER(C.c_uint32)]
+lib.egs_part_pack.restype = C.c_int
+lib.egs_part_unpack.argtypes = [_P, C.POINTER(C.c_uint32), C.c_uint32]
+lib.egs_part_unpack.restype = C.c_int
 lib.egs_part_reset.argtypes = [_P]
 lib.egs_part_reset.restype = C.c_int
 lib.egs_part_read_measure.argtypes = [_P, _P]

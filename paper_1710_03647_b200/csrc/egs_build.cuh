@@ -338,4 +338,60 @@ __global__ void k_format(uint32_t n, const V* f, const uint32_t* perm, const uin
   }
 }
 
+// ------------------------------------------ multi-GPU sparse exchange ----
+// The owned vertices marked in `bits` (a round's raised
+// vertices, or a certificate pass's removals) are packed as (id, value)
+// entries -- one u64 word {id << 32 | value} for u32 values, two words for
+// u64 -- so the ranks all-gather entries instead of their whole slices when
+// few vertices changed.  A warp packs one bitmap word; order is irrelevant.
+template <class V>
+__global__ void __launch_bounds__(256)
+    k_pack(uint32_t lo, uint32_t hi, const uint32_t* bits, const V* f, uint64_t* out,
+           unsigned int* count) {
+  constexpr uint32_t EW = sizeof(V) / 4;  // words per entry: 1 or 2
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  const uint32_t lane = lane_id();
+  for (uint32_t w = (lo >> 5) + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+       w < ((hi + 31) >> 5); w += nwarps) {
+    const uint32_t v = (w << 5) + lane;
+    const bool mine = v >= lo && v < hi && ((__ldcg(bits + w) >> lane) & 1u);
+    const uint32_t m = __ballot_sync(0xffffffffu, mine);
+    if (!m) continue;
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(count, (unsigned int)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (mine) {
+      const uint32_t pos = base + __popc(m & lanemask_lt());
+      const V x = f[v];
+      if (EW == 1)
+        out[pos] = ((uint64_t)v << 32) | (uint64_t)x;
+      else {
+        out[2 * (size_t)pos] = v;
+        out[2 * (size_t)pos + 1] = (uint64_t)x;
+      }
+    }
+  }
+}
+
+// Scatter of the received entries: rank r's count[r] entries start at entry
+// r * stride; the own rank's are skipped (its f is already current).
+template <class V>
+__global__ void __launch_bounds__(256)
+    k_unpack(const uint64_t* in, const uint32_t* count, uint32_t world, uint32_t stride,
+             uint32_t self, V* f) {
+  constexpr uint32_t EW = sizeof(V) / 4;
+  const uint64_t total = (uint64_t)world * stride;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = (uint32_t)(e / stride), i = (uint32_t)(e % stride);
+    if (r == self || i >= count[r]) continue;
+    if (EW == 1) {
+      const uint64_t x = in[e];
+      f[(uint32_t)(x >> 32)] = (V)(uint32_t)x;
+    } else {
+      f[(uint32_t)in[2 * e]] = (V)in[2 * e + 1];
+    }
+  }
+}
+
 }  // namespace egs

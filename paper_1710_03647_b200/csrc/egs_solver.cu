@@ -169,6 +169,10 @@ struct egs_ctx {
   uint32_t* rbm[2] = {nullptr, nullptr};
   uint32_t* cbm = nullptr;
   uint32_t* cand = nullptr;  // certificate candidate bitmap (n_pad / 32 words)
+  // multi-GPU sparse exchange buffers (egs_part_pack / egs_part_unpack)
+  uint64_t* xsend = nullptr;
+  uint64_t* xrecv = nullptr;
+  uint32_t* xcount = nullptr;  // [0]: pack cursor; [1..world]: received counts
   uint32_t* longcol = nullptr;
   uint32_t* fr[2] = {nullptr, nullptr};
   void* stage = nullptr;
@@ -253,7 +257,7 @@ void ctx_free(egs_ctx* c) {
   if (c->device >= 0) cudaSetDevice(c->device);
   void* ptrs[] = {c->off,    c->edge,   c->coff, c->csrc,  c->perm, c->inv,
                   c->f,      c->wit,    c->chg[0], c->chg[1], c->frb,
-                  c->fr[0],  c->fr[1],  c->stage, c->scratch, c->ctr, c->rbm[0], c->rbm[1], c->cbm, c->cand, c->trace, c->longcol,
+                  c->fr[0],  c->fr[1],  c->stage, c->scratch, c->ctr, c->rbm[0], c->rbm[1], c->cbm, c->cand, c->xsend, c->xrecv, c->xcount, c->trace, c->longcol,
                   c->f64};
   if (c->stream) {
     for (void* p : ptrs) dfree(p, c->stream);
@@ -632,6 +636,12 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     c->fr[1] = dalloc<uint32_t>(n);
     c->stage = dalloc<uint8_t>((size_t)std::max<uint32_t>(c->n_pad, 1) * vsz);
     c->f64 = dalloc<int64_t>(n);
+    if (world > 1) {
+      const size_t ew = c->vbits / 32;  // u64 words per entry
+      c->xsend = dalloc<uint64_t>((size_t)c->slice * ew + 1);
+      c->xrecv = dalloc<uint64_t>((size_t)c->slice * world * ew + 1);
+      c->xcount = dalloc<uint32_t>((size_t)world + 1);
+    }
     tm0.s = c->stream;
     tm0.mark("create: state buffers");
     if (n > 0) {
@@ -1001,6 +1011,10 @@ void part_step(egs_ctx* c, int step, int parity, uint64_t* counts) {
   cudaStream_t s = c->stream;
   egs::SolveParams<V> p = make_params<V>(c, nullptr);
   CK(cudaMemsetAsync(c->scratch, 0, sizeof(egs::Scratch), s));
+  // a prune step marks its removals in rbm[0]: start it empty, so the
+  // removed set of the step is exactly what egs_part_pack sends
+  if (step == EGS_STEP_CERT_PRUNE)
+    CK(cudaMemsetAsync(c->rbm[0], 0, ((size_t)c->n + 31) / 32 * 4, s));
   void* args[] = {&p, &step, &parity};
   const void* fn = part_kernel(c);
   CK(cudaLaunchKernel(fn, dim3(c->full_grid), dim3(egs::kBlock), args, egs::kLiftSmemBytes, s));
@@ -1065,6 +1079,9 @@ int egs_part_create(const egs_arena_view* arena, const egs_gpu_opts* opts, int32
       layout->f_dev = (uint64_t)(uintptr_t)c->f;
       layout->stage_dev = (uint64_t)(uintptr_t)c->stage;
       layout->cand_dev = (uint64_t)(uintptr_t)c->cand;
+      layout->send_dev = (uint64_t)(uintptr_t)c->xsend;
+      layout->recv_dev = (uint64_t)(uintptr_t)c->xrecv;
+      layout->entry_bytes = (uint32_t)(c->vbits / 4);
     }
     *out = p;
   });
@@ -1085,6 +1102,57 @@ int egs_part_step(egs_part* part, int32_t step, int32_t parity, uint64_t* counts
       part_step<uint32_t>(c, step, parity, counts);
     else
       part_step<uint64_t>(c, step, parity, counts);
+  });
+}
+
+int egs_part_pack(egs_part* part, int32_t which, int32_t parity, uint32_t* count) {
+  return guarded([&] {
+    if (!part || !count) throw Fail(EGS_ERR_INVALID_CONFIG, "null argument");
+    if (which != EGS_PACK_CHANGED && which != EGS_PACK_REMOVED)
+      throw Fail(EGS_ERR_INVALID_CONFIG, "unknown pack selector");
+    egs_ctx* c = part->c;
+    *count = 0;
+    if (c->n == 0 || c->world < 2 || c->own_hi <= c->own_lo) return;
+    CK(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    const uint32_t* bits = which == EGS_PACK_CHANGED ? c->chg[parity & 1] : c->rbm[0];
+    CK(cudaMemsetAsync(c->xcount, 0, sizeof(uint32_t), s));
+    const uint32_t grid = grid_for((uint64_t)(c->own_hi - c->own_lo), c->num_sms);
+    if (c->vbits == 32)
+      egs::k_pack<uint32_t><<<grid, 256, 0, s>>>(c->own_lo, c->own_hi, bits,
+                                                 static_cast<uint32_t*>(c->f), c->xsend,
+                                                 c->xcount);
+    else
+      egs::k_pack<uint64_t><<<grid, 256, 0, s>>>(c->own_lo, c->own_hi, bits,
+                                                 static_cast<uint64_t*>(c->f), c->xsend,
+                                                 c->xcount);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(count, c->xcount, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  });
+}
+
+int egs_part_unpack(egs_part* part, const uint32_t* counts, uint32_t stride) {
+  return guarded([&] {
+    if (!part || !counts) throw Fail(EGS_ERR_INVALID_CONFIG, "null argument");
+    egs_ctx* c = part->c;
+    if (c->n == 0 || c->world < 2) return;
+    if (stride > c->slice) throw Fail(EGS_ERR_INVALID_CONFIG, "stride beyond the slice");
+    for (int r = 0; r < c->world; ++r)
+      if (counts[r] > stride) throw Fail(EGS_ERR_INVALID_CONFIG, "count beyond the stride");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    CK(cudaMemcpyAsync(c->xcount + 1, counts, c->world * sizeof(uint32_t),
+                       cudaMemcpyHostToDevice, s));
+    const uint32_t grid = grid_for((uint64_t)stride * c->world, c->num_sms);
+    if (c->vbits == 32)
+      egs::k_unpack<uint32_t><<<grid, 256, 0, s>>>(c->xrecv, c->xcount + 1, c->world, stride,
+                                                   c->rank, static_cast<uint32_t*>(c->f));
+    else
+      egs::k_unpack<uint64_t><<<grid, 256, 0, s>>>(c->xrecv, c->xcount + 1, c->world, stride,
+                                                   c->rank, static_cast<uint64_t*>(c->f));
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
   });
 }
 

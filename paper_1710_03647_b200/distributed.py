@@ -32,6 +32,7 @@ import numpy as np
 from . import _native as N
 
 STEP_ROUND1, STEP_LIFT, STEP_COMMIT, STEP_CERT_INIT, STEP_CERT_PRUNE, STEP_CERT_APPLY = range(6)
+PACK_CHANGED, PACK_REMOVED = 0, 1
 
 
 def partition_layout(n: int, world: int, rank: int):
@@ -79,14 +80,28 @@ class DeviceSteps:
         count = max(self.padded, 1)
         self.f = torch.as_tensor(_CudaArray(lay.f_dev, count, typestr), device=dev)
         self.stage = torch.as_tensor(_CudaArray(lay.stage_dev, count, typestr), device=dev)
-        # certificate candidate bitmap: one u32 word per 32 vertices
-        self.cand = torch.as_tensor(_CudaArray(lay.cand_dev, max(self.padded // 32, 1), "<i4"),
-                                    device=dev)
+        # sparse exchange: packed (id, value) entries, `entry_words` u64 each
+        self.entry_words = max(lay.entry_bytes // 8, 1)
+        if world > 1:
+            self.send = torch.as_tensor(
+                _CudaArray(lay.send_dev, self.slice * self.entry_words + 1, "<i8"), device=dev)
+            self.recv = torch.as_tensor(
+                _CudaArray(lay.recv_dev, world * self.slice * self.entry_words + 1, "<i8"),
+                device=dev)
         self._counts = (C.c_uint64 * 2)()
 
     def step(self, kind: int, parity: int):
         N._check(N.lib.egs_part_step(self._part, kind, parity, self._counts))
         return int(self._counts[0]), int(self._counts[1])
+
+    def pack(self, which: int, parity: int) -> int:
+        cnt = C.c_uint32(0)
+        N._check(N.lib.egs_part_pack(self._part, which, parity, C.byref(cnt)))
+        return int(cnt.value)
+
+    def unpack(self, counts, stride: int):
+        arr = (C.c_uint32 * len(counts))(*counts)
+        N._check(N.lib.egs_part_unpack(self._part, arr, stride))
 
     def reset(self):
         N._check(N.lib.egs_part_reset(self._part))
@@ -146,6 +161,40 @@ class TorchComm:
         parts = [self.torch.empty_like(host) for _ in range(self.world)]
         self.dist.all_gather(parts, host)
         t.copy_(self.torch.cat(parts).to(t.device))
+        self._sync(t)
+
+    def allgather_ints(self, x: int) -> list:
+        """Every rank's x (one small collective; its sum is the all-reduce)."""
+        self.collectives += 1
+        if self.world == 1:
+            return [int(x)]
+        dev = self.device if (self.device is not None and not self.staged) else "cpu"
+        v = self.torch.tensor([int(x)], dtype=self.torch.int64, device=dev)
+        out = self.torch.empty(self.world, dtype=self.torch.int64, device=dev)
+        self.dist.all_gather_into_tensor(out, v)
+        return [int(y) for y in out.tolist()]
+
+    def gather_entries(self, send, recv, n: int):
+        """send[:n] of every rank r into recv[r*n:(r+1)*n] on every rank."""
+        self.collectives += 1
+        self.bytes_gathered += n * self.world * send.element_size()
+        if self.world == 1 or n == 0:
+            return
+        if not self.staged:
+            self.dist.all_gather_into_tensor(recv.narrow(0, 0, n * self.world), send.narrow(0, 0, n))
+            self.torch.cuda.synchronize(recv.device)
+            return
+        host = send.narrow(0, 0, n).detach().to("cpu", copy=True)
+        parts = [self.torch.empty_like(host) for _ in range(self.world)]
+        self.dist.all_gather(parts, host)
+        recv.narrow(0, 0, n * self.world).copy_(self.torch.cat(parts).to(recv.device))
+        self._sync(recv)
+
+    def _sync(self, t):
+        # the library's next step runs on its own non-blocking stream: the
+        # copy on torch's stream must have landed
+        if t.is_cuda:
+            self.torch.cuda.synchronize(t.device)
 
     def allreduce_sum(self, x: int) -> int:
         self.collectives += 1
@@ -168,6 +217,7 @@ class PartitionReport:
     collectives: int = 0
     bytes_gathered: int = 0
     kernel_launches: int = 0
+    sparse_exchanges: int = 0
     counters: dict = field(default_factory=dict)
 
 
@@ -189,15 +239,36 @@ def solve_partitioned(steps, comm, certify: bool = True, cert_interval: int = 1,
         launches += 1  # one k_part_step launch per call
         return step_fn(kind, par)
 
+    sparse_exchanges = 0
+
+    def exchange(which, parity, counts):
+        """Bring every rank's marked values into the replicas: (id, value)
+        entries when few changed, else the whole owned slices of f."""
+        nonlocal sparse_exchanges
+        maxc = max(counts)
+        if maxc == 0 or comm.world == 1:
+            return
+        ew = getattr(steps, "entry_words", 1)
+        dense_words = steps.slice * steps.f.element_size() / 8
+        if maxc * ew * 2 > dense_words or not hasattr(steps, "pack"):
+            comm.allgather(steps.f, steps.slice)
+            return
+        n = steps.pack(which, parity)
+        assert n == counts[comm.rank], "pack count differs from the step's count"
+        comm.gather_entries(steps.send, steps.recv, maxc * ew)
+        steps.unpack(counts, maxc)
+        sparse_exchanges += 1
+
     parity = 0
-    changed = comm.allreduce_sum(step(STEP_ROUND1, parity)[0])
+    counts = comm.allgather_ints(step(STEP_ROUND1, parity)[0])
+    changed = sum(counts)
     rounds = 1
     K = cert_interval if cert_interval > 0 else 1
     next_cert = K
     attempts = passes = certified = 0
     while changed:
         step(STEP_COMMIT, parity)
-        comm.allgather(steps.f, steps.slice)
+        exchange(PACK_CHANGED, parity, counts)
         if round_budget is not None and rounds >= round_budget:
             raise N.BoundExhaustedError(
                 f"round budget of {round_budget} exhausted before reaching a fixpoint")
@@ -210,8 +281,9 @@ def solve_partitioned(steps, comm, certify: bool = True, cert_interval: int = 1,
             step(STEP_CERT_INIT, parity)
             comm.allgather(steps.f, steps.slice)
             while True:
-                removed = comm.allreduce_sum(step(STEP_CERT_PRUNE, parity)[1])
-                comm.allgather(steps.f, steps.slice)
+                rc = comm.allgather_ints(step(STEP_CERT_PRUNE, parity)[1])
+                removed = sum(rc)
+                exchange(PACK_REMOVED, parity, rc)
                 passes += 1
                 if removed == 0:
                     break
@@ -221,13 +293,15 @@ def solve_partitioned(steps, comm, certify: bool = True, cert_interval: int = 1,
             K = min(cert_growth * K, 64)  # the geometric schedule of k_solve
             next_cert = rounds + K
         parity ^= 1
-        changed = comm.allreduce_sum(step(STEP_LIFT, parity)[0])
+        counts = comm.allgather_ints(step(STEP_LIFT, parity)[0])
+        changed = sum(counts)
         rounds += 1
     f = steps.read_measure()
     return PartitionReport(
         measure=f, rounds=rounds, cert_attempts=attempts, cert_passes=passes,
         certified=certified, wall_seconds=time.perf_counter() - t0,
         collectives=comm.collectives, bytes_gathered=comm.bytes_gathered,
+        sparse_exchanges=sparse_exchanges,
         kernel_launches=launches,
         counters=steps.counters() if hasattr(steps, "counters") else {},
     )

@@ -26,6 +26,12 @@ class NumpySteps:
         self.f = torch.zeros(max(self.padded, 1), dtype=torch.int64)
         self.stage = torch.zeros(max(self.padded, 1), dtype=torch.int64)
         self.chg = [np.zeros(self.n, bool), np.zeros(self.n, bool)]
+        self.removed = np.zeros(self.n, bool)  # the last pruning pass's removals
+        # sparse exchange buffers: (id, value) entries of 2 int64 words
+        self.entry_words = 2
+        self.send = torch.zeros(2 * max(self.slice, 1) + 1, dtype=torch.int64)
+        self.recv = torch.zeros(2 * max(self.slice, 1) * world + 1, dtype=torch.int64)
+        self.world, self.rank = world, rank
 
     def _ominus(self, ft, w):
         r = np.maximum(ft - w, 0)
@@ -91,6 +97,8 @@ class NumpySteps:
             own = f[lo:hi]
             drop = self._is_cand(own) & ~keep
             own[drop] &= ~CAND
+            self.removed[:] = False
+            self.removed[lo:hi] = drop
             return 0, int(drop.sum())
         if kind == 5:  # apply
             cand = self._is_cand(f[lo:hi])
@@ -98,6 +106,24 @@ class NumpySteps:
             chg[lo:hi] |= cand
             return int(cand.sum()), 0
         raise ValueError(kind)
+
+    def pack(self, which, parity):
+        lo, hi = self.own_lo, self.own_hi
+        marks = self.chg[parity & 1] if which == 0 else self.removed
+        ids = np.nonzero(marks[lo:hi])[0] + lo
+        buf = self.send.numpy()
+        buf[0:2 * len(ids):2] = ids
+        buf[1:2 * len(ids):2] = self.f.numpy()[ids]
+        return len(ids)
+
+    def unpack(self, counts, stride):
+        buf = self.recv.numpy()
+        f = self.f.numpy()
+        for r, cnt in enumerate(counts):
+            if r == self.rank or cnt == 0:
+                continue
+            seg = buf[2 * r * stride: 2 * r * stride + 2 * cnt]  # stride in entries
+            f[seg[0::2]] = seg[1::2]
 
     def read_measure(self):
         return self.f.numpy()[: self.n].copy()
