@@ -777,7 +777,10 @@ void fill_stats(egs_ctx* c, const unsigned long long* h, double ms, egs_gpu_stat
   const uint32_t n = c->n;
   const size_t words = ((size_t)n + 31) / 32;
   const double sv = sizeof(V);
-  const double er = (double)rec_bytes(c);  // edge record bytes
+  // SURVEY §8(d)'s per-unit figure: an 8-byte {u32 dst, i32 w} record per
+  // edge, whatever the stored format (packed arenas stream 4 bytes; the
+  // bench's `traffic` is the measured DRAM side)
+  const double er = 8.0;
   st->lifts = h[egs::kLifts];
   st->applications = h[egs::kApps];
   st->edges_relaxed = h[egs::kEdges];

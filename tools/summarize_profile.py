@@ -45,8 +45,23 @@ json.dump({"kernel": "k_solve", "bytes_per_launch": rd + wr, "dram_read": rd, "d
            "source": f"ncu --set full --clock-control none -k regex:k_solve -c 1 "
                      f"python tools/ncu_target.py C4 1 ({tag})"},
           open(os.path.join(dst, "lift_traffic.json"), "w"), indent=1)
-hot = subprocess.run([sys.executable, "tools/ncu_lines.py", rep, "30"], capture_output=True, text=True).stdout
-open(os.path.join(dst, f"r01_{tag.split('_')[-1]}_source_hotspots.txt"), "w").write(hot)
+hot = subprocess.run([sys.executable, "tools/ncu_stalls.py", rep, "40"], capture_output=True,
+                     text=True).stdout
+open(os.path.join(dst, f"r01_{tag.split('_')[-1]}_source_hotspots.txt"), "w").write(
+    "# warp-stall samples per source line, top stall reasons (tools/ncu_stalls.py)\n" + hot)
+# C3 (R-MAT) capture: the same summary keys
+rep3 = os.path.join(src, "solve_c3.ncu-rep")
+if os.path.exists(rep3):
+    raw3 = subprocess.run(["ncu", "-i", rep3, "--page", "raw", "--csv"], capture_output=True,
+                          text=True).stdout
+    rows3 = list(csv.reader(io.StringIO(raw3)))
+    h3, u3, r3 = rows3[0], rows3[1], rows3[2]
+    json.dump({k: (r3[h3.index(k)], u3[h3.index(k)]) for k in keys if k in h3},
+              open(os.path.join(dst, f"r01_{tag.split('_')[-1]}_ncu_k_solve_c3.json"), "w"), indent=1)
+for extra in ("bench_2rank_staged.json",):
+    if os.path.exists(os.path.join(src, extra)) and os.path.getsize(os.path.join(src, extra)):
+        shutil.copy(os.path.join(src, extra),
+                    os.path.join(dst, f"r01_{tag.split('_')[-1]}_{extra}"))
 lrows = list(csv.reader(open(os.path.join(src, "launches.csv"))))
 hdr = next(i for i, x in enumerate(lrows) if x and x[0] == "ID")
 hh, data = lrows[hdr], lrows[hdr + 1:]
