@@ -458,28 +458,6 @@ __device__ __forceinline__ void set_bit(uint32_t* bm, uint32_t v) {
   atomicOr(bm + (v >> 5), 1u << (v & 31u));
 }
 
-// Light rows of the class ranges [lo, hi) in a dense round: aligned 32-vertex
-// words per warp so a warp publishes its changed bits with one atomicOr.
-template <class V, bool P0>
-__device__ __noinline__ void dense_light(const SolveParams<V>& p, uint32_t lo,
-                                            uint32_t hi, uint32_t* chg,
-                                            unsigned int* sum_dst) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
-  Local L;
-  const uint32_t nwarps = gridDim.x * kWarps;
-  const uint32_t gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
-  const uint32_t w0 = lo >> 5, w1 = (hi + 31) >> 5;
-  for (uint32_t w = w0 + gw; w < w1; w += nwarps) {
-    const uint32_t v = (w << 5) + lane_id();
-    bool ch = false;
-    if (v >= lo && v < hi) ch = lift_thread<V, P0>(p, v, L);
-    const uint32_t m = __ballot_sync(0xffffffffu, ch);
-    if (m && lane_id() == 0) atomicOr(chg + w, m);
-    L.phase_count += ch;
-  }
-  block_flush(L, p.ctr, sum_dst, s_cnt);
-}
-
 // Player-1 light rows of a dense round, TMA-staged.  A warp owns aligned
 // 32-vertex tiles; the tile's contiguous span of edge records is brought
 // into the warp's shared-memory stage by one bulk copy (cp.async.bulk,
@@ -525,10 +503,11 @@ __device__ __forceinline__ void tma_init_barriers() {
 constexpr uint32_t kTileClaim = 4;
 
 template <class V, class Load, class Test, class Row, class Fallback>
-__device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, uint32_t lo0, uint32_t hi0,
-                                          uint32_t lo1, uint32_t hi1, unsigned int* cursor,
-                                          const uint32_t* mask, uint32_t* chg, Local& L,
-                                          Load load, Test test, Row row, Fallback fallback) {
+__device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, bool staged, uint32_t lo0,
+                                          uint32_t hi0, uint32_t lo1, uint32_t hi1,
+                                          unsigned int* cursor, const uint32_t* mask,
+                                          uint32_t* chg, Local& L, Load load, Test test,
+                                          Row row, Fallback fallback) {
   extern __shared__ __align__(128) ERec dsm[];
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   ERec* stage_base = dsm + (size_t)warp * kStages * kStageRecs;
@@ -548,6 +527,30 @@ __device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, uint32_t lo0,
     }
     return c_next++;
   };
+
+  if (!staged) {  // direct: every needed row through `fallback` (plain loads)
+    for (;;) {
+      const uint32_t i = claim();
+      if (i >= T) break;
+      const bool second = i >= T0;
+      const uint32_t w = second ? (lo1 >> 5) + (i - T0) : (lo0 >> 5) + i;
+      const uint32_t v = (w << 5) + lane;
+      const bool in = v >= (second ? lo1 : lo0) && v < (second ? hi1 : hi0);
+      const uint32_t mw = mask ? ldcg(mask + w) : ~0u;
+      V aux = V(0);
+      bool work = false;
+      if (in && ((mw >> lane) & 1u)) {
+        load(v, aux);
+        work = test(v, aux);
+      }
+      if (in && !work) ++L.visits;
+      const bool ch = work && fallback(v, aux);
+      const uint32_t m = __ballot_sync(0xffffffffu, ch);
+      if (m && lane == 0) atomicOr(chg + w, m);
+      L.phase_count += ch;
+    }
+    return;
+  }
 
   struct Tile {
     V aux;
@@ -695,7 +698,8 @@ __device__ __noinline__ void dense_light_p1(const SolveParams<V>& p, uint32_t lo
     return false;
   };
   auto fallback = [&](uint32_t v, V) { return lift_thread<V, false>(p, v, L); };
-  tma_tiles<V>(p, lo, hi, 0u, 0u, cursor, nullptr, chg, L, load, test, row, fallback);
+  tma_tiles<V>(p, (p.use_tma & kTmaLift) != 0, lo, hi, 0u, 0u, cursor, nullptr, chg, L, load,
+               test, row, fallback);
   block_flush(L, p.ctr, sum_dst, s_cnt);
 }
 
@@ -1033,23 +1037,28 @@ __device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo0,
     const bool p0 = v < g.rb[kP1L];
     const uint32_t b = __ldg(g.off + v), e = __ldg(g.off + v + 1);
     int minw = INT32_MAX, maxw = INT32_MIN;
-    uint32_t imax = b;
+    uint32_t ibest = b, kbest = 0xFFFFFFFFu;
     for (uint32_t i = b; i < e; i += kChunk) {
-      int wt[kChunk];
+      int2 r[kChunk];
 #pragma unroll
-      for (int k = 0; k < kChunk; ++k) wt[k] = rec_w(g, __ldcs(erecs(g) + min(i + k, e - 1)));
+      for (int k = 0; k < kChunk; ++k) r[k] = ld_rec(g, min(i + k, e - 1));
 #pragma unroll
       for (int k = 0; k < kChunk; ++k) {
-        minw = min(minw, wt[k]);
-        if (wt[k] > maxw) {
-          maxw = wt[k];
-          imax = min(i + k, e - 1);
+        minw = min(minw, r[k].y);
+        maxw = max(maxw, r[k].y);
+        // the witness key of the tile path: least max(0, -w), player-0 target first
+        const uint32_t key = ((r[k].y >= 0 ? 0u : (uint32_t)(-r[k].y)) << 1) |
+                             (uint32_t)((uint32_t)r[k].x >= g.rb[kP1L]);
+        if (key < kbest) {
+          kbest = key;
+          ibest = min(i + k, e - 1);
         }
       }
     }
-    return finish(v, p0, minw, maxw, __ldg(erecs(g) + imax), e - b);
+    return finish(v, p0, minw, maxw, __ldg(erecs(g) + ibest), e - b);
   };
-  tma_tiles<V>(p, lo0, hi0, lo1, hi1, cursor, nullptr, chg, L, load, test, row, fallback);
+  tma_tiles<V>(p, (p.use_tma & kTmaRound1) != 0, lo0, hi0, lo1, hi1, cursor, nullptr, chg, L,
+               load, test, row, fallback);
   block_flush(L, p.ctr, sum_dst, s_cnt);
 }
 
@@ -1215,11 +1224,8 @@ __device__ __noinline__ void phase_lift(const SolveParams<V>& p, bool dense, int
     st.lap(kSubMedium);
     dense_light_p0<V>(p, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]), chg, sum_dst);
     st.lap(kSubLightP0);
-    if (p.use_tma)
-      dense_light_p1<V>(p, clip_lo(p, g.rb[kP1L]), clip_hi(p, g.rb[kP1M]),
-                        slot_dyn + kTileCursor, chg, sum_dst);
-    else
-      dense_light<V, false>(p, clip_lo(p, g.rb[kP1L]), clip_hi(p, g.rb[kP1M]), chg, sum_dst);
+    dense_light_p1<V>(p, clip_lo(p, g.rb[kP1L]), clip_hi(p, g.rb[kP1M]),
+                      slot_dyn + kTileCursor, chg, sum_dst);
     st.lap(kSubLightP1);
   } else {
     const uint32_t* list = p.fr[buf];
@@ -1469,7 +1475,8 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
       return !keep;
     };
     auto fallback = [&](uint32_t v, V) { return cert_check_thread<V>(p, v, L); };
-    tma_tiles<V>(p, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]), clip_lo(p, g.rb[kP1L]),
+    tma_tiles<V>(p, (p.use_tma & kTmaCert) != 0, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]),
+                 clip_lo(p, g.rb[kP1L]),
                  clip_hi(p, g.rb[kP1M]), slot_dyn + kTileCursor, p.cand, rbm, L, load, test,
                  row, fallback);
   }

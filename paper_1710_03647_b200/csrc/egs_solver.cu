@@ -301,6 +301,10 @@ const void* part_kernel(const egs_ctx* c) {
   return c->tbits ? egs::e4::part_kernel(c->vbits) : egs::e8::part_kernel(c->vbits);
 }
 size_t rec_bytes(const egs_ctx* c) { return c->tbits ? 4 : 8; }
+// light-row phases staged through TMA tiles by default, measured per phase
+// (profiles/README.md): round 1 and the certificate pass stream whole rows
+// and gain; the dense player-1 lift is faster with plain row loads
+constexpr int kDefaultTma = egs::kTmaRound1 | egs::kTmaCert;
 
 // Process-wide pinned staging buffer for the narrowed weights (grows on
 // demand; one upload at a time uses it).
@@ -747,7 +751,8 @@ egs::SolveParams<V> make_params(egs_ctx* c, unsigned long long* budget_out) {
   p.ctr = c->ctr;
   p.trace = c->trace;
   p.mode = o.mode;
-  p.use_tma = o.no_tma ? 0 : 1;
+  p.use_tma = o.no_tma ? 0 : kDefaultTma;
+  if (const char* e = std::getenv("EGS_TMA_MASK")) p.use_tma = std::atoi(e) & egs::kTmaAll;
   // the candidate mark needs a free top bit: u64 values with credit_cap at
   // INT64_MAX (a saturated cap) solve without the certificate (still exact)
   p.certify = o.certify && !(c->vbits == 64 && c->cap >= INT64_MAX - 1);
