@@ -49,7 +49,7 @@ $(ORACLE_CLI): oracle/egs_oracle_cli.c oracle/egs_oracle.c oracle/egs_oracle.h
 # they lie, never copied.  `-include cmath` works around solver_seq.cpp:215
 # calling llround without <cmath>.  Skipped when the reference is absent (the
 # GPU box uses the prebuilt .so that travels with the snapshot).
-ref:
+ref: $(LIB)
 	@if [ -d $(REF)/src ]; then $(MAKE) --no-print-directory $(REF_LIB) $(DROPIN_BINS); \
 	 else echo "reference sources absent; using prebuilt $(REF_LIB) if present"; fi
 
