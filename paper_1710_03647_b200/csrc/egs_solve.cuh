@@ -145,33 +145,38 @@ struct Local {
   unsigned int lifts = 0, apps = 0, edges = 0, witness = 0, act = 0, certified = 0,
                pops = 0, cert_scanned = 0, cert_edges = 0, visits = 0;
   unsigned int phase_count = 0;  // per-phase sum (changed / removed / seeds)
+  unsigned int pushed = 0;       // frontier entries added by a sparse lift's pushes
 };
 constexpr int kLocalCounters = 10;
 
 // Block-wide flush of the phase's counters: one atomicAdd per CTA and
 // counter; phase_count goes to the grid-shared slot `dst`.  Block-uniform.
 __device__ __forceinline__ void block_flush(Local& L, unsigned long long* ctr,
-                                            unsigned int* dst, unsigned int* s_cnt) {
-  unsigned int v[kLocalCounters + 1] = {L.lifts, L.apps,      L.edges,        L.witness,
-                                        L.act,   L.certified, L.pops,         L.cert_scanned,
-                                        L.cert_edges, L.visits, L.phase_count};
+                                            unsigned int* dst, unsigned int* s_cnt,
+                                            unsigned int* dst2 = nullptr) {
+  constexpr int K = kLocalCounters + 2;  // + phase_count, pushed
+  unsigned int v[K] = {L.lifts, L.apps,      L.edges,        L.witness,
+                       L.act,   L.certified, L.pops,         L.cert_scanned,
+                       L.cert_edges, L.visits, L.phase_count, L.pushed};
   const uint32_t warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int k = 0; k <= kLocalCounters; ++k) v[k] = __reduce_add_sync(0xffffffffu, v[k]);
+  for (int k = 0; k < K; ++k) v[k] = __reduce_add_sync(0xffffffffu, v[k]);
   __syncthreads();
   if (lane_id() == 0) {
 #pragma unroll
-    for (int k = 0; k <= kLocalCounters; ++k) s_cnt[warp * (kLocalCounters + 1) + k] = v[k];
+    for (int k = 0; k < K; ++k) s_cnt[warp * K + k] = v[k];
   }
   __syncthreads();
-  if (threadIdx.x <= (unsigned)kLocalCounters) {
+  if (threadIdx.x < (unsigned)K) {
     unsigned long long sum = 0;
-    for (int w = 0; w < kWarps; ++w) sum += s_cnt[w * (kLocalCounters + 1) + threadIdx.x];
+    for (int w = 0; w < kWarps; ++w) sum += s_cnt[w * K + threadIdx.x];
     if (sum) {
       if (threadIdx.x < (unsigned)kLocalCounters)
         atomicAdd(ctr + threadIdx.x, sum);
-      else
+      else if (threadIdx.x == (unsigned)kLocalCounters)
         atomicAdd(dst, (unsigned int)sum);
+      else if (dst2)
+        atomicAdd(dst2, (unsigned int)sum);
     }
   }
   L = Local();
@@ -185,13 +190,29 @@ __device__ __forceinline__ void block_flush(Local& L, unsigned long long* ctr,
 // it the lift cannot raise f(v) and the row is not read (the GPU analogue of
 // the count(v) of Alg. 1, solver_seq.cpp:186-199).
 
+// A raised value is staged for the round's commit (Jacobi rounds), or, in a
+// sparse round, stored in place with atomicMax -- the in-place atomic store
+// of solve_frontier (solver_par.cpp:399) -- and then true iff it rose.
+template <class V, bool INPLACE>
+__device__ __forceinline__ bool store_raise(const SolveParams<V>& p, uint32_t v, V acc, V old) {
+  if (!(acc > old)) return false;
+  if (!INPLACE) {
+    stcg(p.stage + v, acc);
+    return true;
+  }
+  if (sizeof(V) == 8)
+    return atomicMax(reinterpret_cast<unsigned long long*>(p.f + v),
+                     (unsigned long long)acc) < (unsigned long long)acc;
+  return atomicMax(reinterpret_cast<unsigned int*>(p.f + v), (unsigned int)acc) < (unsigned int)acc;
+}
+
 // ---- one thread per row (light rows)
 #ifndef EGS_LIFT_CHUNK
 #define EGS_LIFT_CHUNK 8
 #endif
 constexpr int kChunk = EGS_LIFT_CHUNK;  // edges whose gathers a thread keeps in flight
 
-template <class V, bool P0>
+template <class V, bool P0, bool INPLACE = false>
 __device__ __forceinline__ bool lift_thread(const SolveParams<V>& p, uint32_t v,
                                             Local& L) {
   constexpr V TOP = Top<V>::v;
@@ -238,8 +259,7 @@ __device__ __forceinline__ bool lift_thread(const SolveParams<V>& p, uint32_t v,
     if (P0 ? acc == V(0) : acc == TOP) break;  // raw_lift early exits (:41,46)
   }
   if (P0) st_wit(p, v, best);
-  if (acc > old) {
-    stcg(p.stage + v, acc);
+  if (store_raise<V, INPLACE>(p, v, acc, old)) {
     ++L.lifts;
     return true;
   }
@@ -247,7 +267,7 @@ __device__ __forceinline__ bool lift_thread(const SolveParams<V>& p, uint32_t v,
 }
 
 // ---- one warp per row (medium rows).  Warp-uniform.
-template <class V, bool P0>
+template <class V, bool P0, bool INPLACE = false>
 __device__ __forceinline__ bool lift_warp(const SolveParams<V>& p, uint32_t v,
                                           Local& L) {
   constexpr V TOP = Top<V>::v;
@@ -315,8 +335,7 @@ __device__ __forceinline__ bool lift_warp(const SolveParams<V>& p, uint32_t v,
   }
   if (lane == 0) {
     if (P0) st_wit(p, v, best);
-    if (res > old) {
-      stcg(p.stage + v, res);
+    if (store_raise<V, INPLACE>(p, v, res, old)) {
       ++L.lifts;
       raised = true;
     }
@@ -334,7 +353,7 @@ struct BlockScratch {
   int flag;
 };
 
-template <class V, bool P0>
+template <class V, bool P0, bool INPLACE = false>
 __device__ __forceinline__ bool lift_block(const SolveParams<V>& p, uint32_t v,
                                            Local& L, BlockScratch<V>& s) {
   constexpr V TOP = Top<V>::v;
@@ -420,8 +439,7 @@ __device__ __forceinline__ bool lift_block(const SolveParams<V>& p, uint32_t v,
       }
     }
     if (P0) st_wit(p, v, rec);
-    if (res > old) {
-      stcg(p.stage + v, res);
+    if (store_raise<V, INPLACE>(p, v, res, old)) {
       ++L.lifts;
       raised = true;
     }
@@ -662,7 +680,7 @@ __device__ __noinline__ void dense_light_p1(const SolveParams<V>& p, uint32_t lo
                                             unsigned int* cursor, uint32_t* chg,
                                             unsigned int* sum_dst) {
   constexpr V TOP = Top<V>::v;
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   Local L;
   auto load = [&](uint32_t v, V& old) { old = ldcg(p.f + v); };
   auto test = [&](uint32_t, V old) { return old != TOP; };
@@ -717,7 +735,7 @@ __device__ __noinline__ void dense_light_p0(const SolveParams<V>& p, uint32_t lo
                                             uint32_t* chg, unsigned int* sum_dst) {
   constexpr V TOP = Top<V>::v;
   constexpr int U = kP0Unroll;
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   __shared__ uint32_t s_q[kWarps][32 * U + 32];
   Local L;
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
@@ -780,56 +798,202 @@ __device__ __noinline__ void dense_light_p0(const SolveParams<V>& p, uint32_t lo
   block_flush(L, p.ctr, sum_dst, s_cnt);
 }
 
-// Light rows of a sparse frontier list, one thread each.
+// Activation (solver_par.cpp:402-410): every non-top predecessor of a vertex
+// marked in `chg` enters frontier buffer `nb` once (bitmap dedup), sorted
+// into its size-class sublist; the warp expands CSC columns as one stream.
+// Columns longer than kLongCol (the in-hubs of a power-law arena) are not
+// expanded by one warp: they are queued in p.longcol (count in qlong) for
+// phase_activate_long, which spreads their chunks over the whole grid.
+
+// Frontier appends are buffered per warp in shared memory (the TMA stage
+// area, idle during activation) and published up to kAppendCap entries per
+// atomicAdd, so a large frontier does not serialise on the three list
+// counters.  Warp-uniform.
+constexpr uint32_t kAppendCap = 512;  // entries per class per warp (3 * 2 KB)
+
+struct WarpLists {
+  uint32_t* buf[3];
+  uint32_t cnt[3];
+};
+
+// A frontier being produced: its three class sublists, their counters and
+// its membership (dedup) bitmap.  Frontiers are numbered tokens: token k
+// lives in list buffer k & 1 with bitmap p.frb[k & 1] and counters
+// fr_cnt[k % 3], so the producer of token k can zero the counters of token
+// k + 1 while token k - 1 is still being read (k_solve main loop).
+struct Frontier {
+  uint32_t* list[3];
+  unsigned int* cnt;
+  uint32_t* frb;
+};
+
+__device__ __forceinline__ WarpLists warp_lists() {
+  extern __shared__ __align__(128) ERec dsm[];
+  uint32_t* base = reinterpret_cast<uint32_t*>(dsm) +
+                   (size_t)(threadIdx.x >> 5) * (kStages * kStageBytes / 4);
+  WarpLists q;
+  for (int c = 0; c < 3; ++c) {
+    q.buf[c] = base + c * kAppendCap;
+    q.cnt[c] = 0;
+  }
+  return q;
+}
+
+__device__ __forceinline__ void lists_flush(WarpLists& q, int c, uint32_t* list,
+                                            unsigned int* count) {
+  __syncwarp();
+  const uint32_t k = q.cnt[c];
+  if (k == 0) return;
+  uint32_t base = 0;
+  if (lane_id() == 0) base = atomicAdd(count, k);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  for (uint32_t i = lane_id(); i < k; i += 32) list[base + i] = q.buf[c][i];
+  q.cnt[c] = 0;
+  __syncwarp();
+}
+
+__device__ __forceinline__ void lists_append(WarpLists& q, bool pred, int c, uint32_t v,
+                                             uint32_t* const* lists, unsigned int* counts) {
+#pragma unroll
+  for (int cc = 0; cc < 3; ++cc) {
+    const bool mine = pred && c == cc;
+    const uint32_t m = __ballot_sync(0xffffffffu, mine);
+    if (!m) continue;
+    if (mine) q.buf[cc][q.cnt[cc] + __popc(m & lanemask_lt())] = v;
+    q.cnt[cc] += __popc(m);
+    if (q.cnt[cc] + 32 > kAppendCap) lists_flush(q, cc, lists[cc], counts + cc);
+  }
+}
+
+template <class V>
+__device__ __forceinline__ void activate_pred(const SolveParams<V>& p, bool valid, uint32_t idx,
+                                              WarpLists& q, const Frontier& t, Local& L,
+                                              bool pushing = false) {
+  const Graph& g = p.g;
+  bool add = false;
+  uint32_t u = 0;
+  int c = 0;
+  if (valid) {
+    ++L.act;
+    u = __ldg(g.csrc + idx);
+    const uint32_t bit = 1u << (u & 31u);
+    // a plain read first: predecessors shared by many changed vertices (the
+    // in-hubs' neighbours) are already marked and skip the atomic
+    if (!(ldcg(t.frb + (u >> 5)) & bit) && gather(p.f + u) != Top<V>::v) {
+      add = !(atomicOr(t.frb + (u >> 5), bit) & bit);
+      c = size_class(g, u);
+    }
+  }
+  lists_append(q, add, c, u, t.list, t.cnt);
+  if (pushing)
+    L.pushed += add;
+  else
+    L.phase_count += add;
+}
+
+// Push activation of a sparse round: the predecessors of the vertices of the
+// lanes with `raised` enter frontier t right away (one CSC column per such
+// lane, expanded by the whole warp; columns longer than kLongCol are queued
+// for phase_activate_long).  Warp-uniform.
+template <class V>
+__device__ __forceinline__ void push_preds(const SolveParams<V>& p, bool raised, uint32_t v,
+                                           WarpLists& q, const Frontier& t,
+                                           unsigned int* qlong, Local& L) {
+  if (!__any_sync(0xffffffffu, raised)) return;
+  uint32_t b = 0, e = 0;
+  if (raised) {
+    b = __ldg(p.g.coff + v);
+    e = __ldg(p.g.coff + v + 1);
+    if (e - b > kLongCol) {
+      const uint32_t k = atomicAdd(qlong, 1u);
+      p.longcol[2 * k] = v;
+      p.longcol[2 * k + 1] = 0u;
+      e = b;
+    }
+  }
+  warp_expand(b, e, [&](bool valid, uint32_t idx, uint32_t) {
+    activate_pred<V>(p, valid, idx, q, t, L, true);
+  });
+}
+
+// Light rows of a sparse frontier list, one thread each, lifted in place;
+// raised vertices push their predecessors into frontier `nxt`.
 template <class V>
 __device__ __noinline__ void sparse_light(const SolveParams<V>& p, const uint32_t* list,
                                           uint32_t count, uint32_t* chg,
-                                          unsigned int* sum_dst) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+                                          unsigned int* sum_dst, Frontier nxt,
+                                          unsigned int* qlong, unsigned int* act_dst) {
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   Local L;
+  WarpLists q = warp_lists();
   const uint32_t nthreads = gridDim.x * kBlock;
-  for (uint32_t i = blockIdx.x * kBlock + threadIdx.x; i < count; i += nthreads) {
-    const uint32_t v = ldcg(list + i);
-    const bool ch = v < p.g.rb[kP1L] ? lift_thread<V, true>(p, v, L)
-                                     : lift_thread<V, false>(p, v, L);
+  const uint32_t base = blockIdx.x * kBlock + (threadIdx.x & ~31u);
+  for (uint32_t i0 = base; i0 < count; i0 += nthreads) {  // warp-uniform loop
+    const uint32_t i = i0 + lane_id();
+    uint32_t v = 0;
+    bool ch = false;
+    if (i < count) {
+      v = ldcg(list + i);
+      ch = v < p.g.rb[kP1L] ? lift_thread<V, true, true>(p, v, L)
+                            : lift_thread<V, false, true>(p, v, L);
+    }
     if (ch) {
       set_bit(chg, v);
       ++L.phase_count;
     }
+    push_preds<V>(p, ch, v, q, nxt, qlong, L);
   }
-  block_flush(L, p.ctr, sum_dst, s_cnt);
+  for (int c = 0; c < 3; ++c) lists_flush(q, c, nxt.list[c], nxt.cnt + c);
+  block_flush(L, p.ctr, sum_dst, s_cnt, act_dst);
 }
 
 // Medium rows: warps claim rows from a per-phase cursor.  `items(i)` maps a
 // claim index to a vertex.
+// With `push` (sparse rounds) rows are lifted in place and a raised row
+// pushes its predecessors into frontier `nxt`.
 template <class V, class Items>
 __device__ __noinline__ void warp_rows(const SolveParams<V>& p, uint32_t count,
                                           unsigned int* cursor, Items items,
-                                          uint32_t* chg, unsigned int* sum_dst) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+                                          uint32_t* chg, unsigned int* sum_dst,
+                                          bool push = false, Frontier nxt = Frontier{},
+                                          unsigned int* qlong = nullptr,
+                                          unsigned int* act_dst = nullptr) {
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   Local L;
+  WarpLists q = warp_lists();
   WarpClaim wc;
   uint32_t i;
   while (warp_claim(cursor, count, wc, i)) {
     const uint32_t v = items(i);
     if (!owned(p, v)) continue;
     const bool p0 = v < p.g.rb[kP1L];
-    const bool ch = p0 ? lift_warp<V, true>(p, v, L) : lift_warp<V, false>(p, v, L);
+    bool ch;
+    if (push)
+      ch = p0 ? lift_warp<V, true, true>(p, v, L) : lift_warp<V, false, true>(p, v, L);
+    else
+      ch = p0 ? lift_warp<V, true>(p, v, L) : lift_warp<V, false>(p, v, L);
     if (ch && lane_id() == 0) {
       set_bit(chg, v);
       ++L.phase_count;
     }
+    if (push) push_preds<V>(p, ch && lane_id() == 0, v, q, nxt, qlong, L);
   }
-  block_flush(L, p.ctr, sum_dst, s_cnt);
+  if (push)
+    for (int c = 0; c < 3; ++c) lists_flush(q, c, nxt.list[c], nxt.cnt + c);
+  block_flush(L, p.ctr, sum_dst, s_cnt, act_dst);
 }
 
 template <class V, class Items>
 __device__ __noinline__ void block_rows(const SolveParams<V>& p, uint32_t count,
                                            unsigned int* cursor, Items items,
-                                           uint32_t* chg, unsigned int* sum_dst) {
+                                           uint32_t* chg, unsigned int* sum_dst,
+                                           bool push = false, Frontier nxt = Frontier{},
+                                           unsigned int* qlong = nullptr,
+                                           unsigned int* act_dst = nullptr) {
   __shared__ BlockScratch<V> s;
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   Local L;
+  WarpLists q = warp_lists();
   for (;;) {
     __syncthreads();
     if (threadIdx.x == 0) s.item = atomicAdd(cursor, 1u);
@@ -839,14 +1003,22 @@ __device__ __noinline__ void block_rows(const SolveParams<V>& p, uint32_t count,
     const uint32_t v = items(i);
     if (!owned(p, v)) continue;
     const bool p0 = v < p.g.rb[kP1L];
-    const bool ch = p0 ? lift_block<V, true>(p, v, L, s) : lift_block<V, false>(p, v, L, s);
+    bool ch;
+    if (push)
+      ch = p0 ? lift_block<V, true, true>(p, v, L, s) : lift_block<V, false, true>(p, v, L, s);
+    else
+      ch = p0 ? lift_block<V, true>(p, v, L, s) : lift_block<V, false>(p, v, L, s);
     if (ch && threadIdx.x == 0) {
       set_bit(chg, v);
       ++L.phase_count;
     }
+    if (push && threadIdx.x < 32)  // warp 0 expands the raised hub's column
+      push_preds<V>(p, ch && threadIdx.x == 0, v, q, nxt, qlong, L);
   }
   __syncthreads();
-  block_flush(L, p.ctr, sum_dst, s_cnt);
+  if (push && threadIdx.x < 32)
+    for (int c = 0; c < 3; ++c) lists_flush(q, c, nxt.list[c], nxt.cnt + c);
+  block_flush(L, p.ctr, sum_dst, s_cnt, act_dst);
 }
 
 // ======================================================= certificate ====
@@ -985,7 +1157,7 @@ template <class V>
 __device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo0, uint32_t hi0,
                                           uint32_t lo1, uint32_t hi1, unsigned int* cursor,
                                           uint32_t* chg, unsigned int* sum_dst) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   const Graph& g = p.g;
   Local L;
   auto load = [](uint32_t, V&) {};
@@ -1066,7 +1238,7 @@ __device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo0,
 template <class V>
 __device__ __noinline__ void round1_long(const SolveParams<V>& p, uint32_t* chg,
                                          unsigned int* sum_dst, unsigned int* slot_dyn) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   __shared__ int s_min[kWarps], s_max[kWarps];
   __shared__ uint32_t s_imax[kWarps];
   __shared__ unsigned int s_item;
@@ -1190,30 +1362,32 @@ __device__ __noinline__ void phase_round1(const SolveParams<V>& p, uint32_t* chg
                   clip_hi(p, g.rb[kP1M]), slot_dyn + kTileCursor, chg, slot_sum + 0);
 }
 
-// One lift round.  Dense: every vertex (top ones are skipped after one
-// load); sparse: the frontier lists of buffer `buf`.  Raised vertices are
-// marked in `chg`; the other round's bitmap is cleared for reuse.
+// One lift round.  Dense (Jacobi): every vertex, raised values staged for
+// the commit phase.  Sparse (solve_frontier, solver_par.cpp:389-417): the
+// vertices of frontier `cur`, lifted in place, each raised vertex pushing its
+// predecessors into frontier `nxt` -- one phase per sparse round.  Raised
+// vertices are marked in `chg`; the other round's bitmap is cleared for
+// reuse.  The produced frontier's size goes to slot_sum[2], its queued long
+// columns to slot_dyn[2].
 template <class V>
-__device__ __noinline__ void phase_lift(const SolveParams<V>& p, bool dense, int buf,
+__device__ __noinline__ void phase_lift(const SolveParams<V>& p, bool dense, Frontier cur,
+                                        Frontier nxt, unsigned int* cnt_after,
                                         uint32_t* chg, uint32_t* other,
                                         unsigned int* slot_sum, unsigned int* slot_dyn) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   const Graph& g = p.g;
   const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
   const uint32_t nthreads = gridDim.x * kBlock;
   const uint32_t nwords = (g.n + 31) >> 5;
-  Scratch* sh = p.sh;
   Local L;
   unsigned int* sum_dst = slot_sum + 0;
   for (uint32_t w = tid; w < nwords; w += nthreads) {
     other[w] = 0u;
-    if (dense) p.frb[w] = 0u;
-  }
-  if (tid == 0)
-    for (int c = 0; c < 3; ++c) {
-      sh->fr_cnt[buf ^ 1][c] = 0;
-      if (dense) sh->fr_cnt[buf][c] = 0;
+    if (dense) {  // no frontier survives a dense round
+      p.frb[0][w] = 0u;
+      p.frb[1][w] = 0u;
     }
+  }
   if (dense) {
     SubTimer st(p.ctr);
     block_rows<V>(p, class_size(g, 2), slot_dyn + 1,
@@ -1228,24 +1402,30 @@ __device__ __noinline__ void phase_lift(const SolveParams<V>& p, bool dense, int
                       slot_dyn + kTileCursor, chg, sum_dst);
     st.lap(kSubLightP1);
   } else {
-    const uint32_t* list = p.fr[buf];
-    const uint32_t cL = vload(&sh->fr_cnt[buf][0]);
-    const uint32_t cM = vload(&sh->fr_cnt[buf][1]);
-    const uint32_t cH = vload(&sh->fr_cnt[buf][2]);
-    const uint32_t* lM = list + p.cbase[1];
-    const uint32_t* lH = list + p.cbase[2];
-    block_rows<V>(p, cH, slot_dyn + 1, [=](uint32_t i) { return ldcg(lH + i); }, chg,
-                  sum_dst);
-    warp_rows<V>(p, cM, slot_dyn + 0, [=](uint32_t i) { return ldcg(lM + i); }, chg, sum_dst);
+    if (blockIdx.x == 0 && threadIdx.x < 3) cnt_after[threadIdx.x] = 0u;
+    const uint32_t cL = vload(cur.cnt + 0);
+    const uint32_t cM = vload(cur.cnt + 1);
+    const uint32_t cH = vload(cur.cnt + 2);
+    const uint32_t* lL = cur.list[0];
+    const uint32_t* lM = cur.list[1];
+    const uint32_t* lH = cur.list[2];
+    unsigned int* act_dst = slot_sum + 2;
+    unsigned int* qlong = slot_dyn + 2;
     SubTimer st(p.ctr);
-    sparse_light<V>(p, list, cL, chg, sum_dst);
+    block_rows<V>(p, cH, slot_dyn + 1, [=](uint32_t i) { return ldcg(lH + i); }, chg, sum_dst,
+                  true, nxt, qlong, act_dst);
+    st.lap(kSubHeavy);
+    warp_rows<V>(p, cM, slot_dyn + 0, [=](uint32_t i) { return ldcg(lM + i); }, chg, sum_dst,
+                 true, nxt, qlong, act_dst);
+    st.lap(kSubMedium);
+    sparse_light<V>(p, lL, cL, chg, sum_dst, nxt, qlong, act_dst);
     st.lap(kSubSparseLight);
-    // leave the membership bitmap clear for the next activation
+    // leave this frontier's membership bits clear for the token after next
     for (uint32_t i = tid; i < cL + cM + cH; i += nthreads) {
-      const uint32_t v = i < cL        ? ldcg(list + i)
+      const uint32_t v = i < cL        ? ldcg(lL + i)
                          : i < cL + cM ? ldcg(lM + (i - cL))
                                        : ldcg(lH + (i - cL - cM));
-      atomicAnd(p.frb + (v >> 5), ~(1u << (v & 31u)));
+      atomicAnd(cur.frb + (v >> 5), ~(1u << (v & 31u)));
     }
     if (tid == 0) L.pops += cL + cM + cH;
   }
@@ -1288,7 +1468,7 @@ __device__ __noinline__ void phase_commit(const SolveParams<V>& p, const uint32_
 template <class V>
 __device__ __noinline__ void phase_cert_init(const SolveParams<V>& p, const uint32_t* chg,
                                              unsigned int* slot_sum) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
   const uint32_t nthreads = gridDim.x * kBlock;
   const uint32_t nwarps = gridDim.x * kWarps;
@@ -1417,7 +1597,7 @@ template <class V>
 __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned int* slot_sum,
                                               unsigned int* slot_dyn, uint32_t* rbm,
                                               uint32_t* rbm_clear) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   const Graph& g = p.g;
   const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
   const uint32_t nthreads = gridDim.x * kBlock;
@@ -1490,7 +1670,7 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
 template <class V>
 __device__ __noinline__ void phase_cert_mark(const SolveParams<V>& p, const uint32_t* rbm_in,
                                              unsigned int* slot_sum, unsigned int* qcnt) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   const Graph& g = p.g;
   const uint32_t nwords = (g.n + 31) >> 5;
   const uint32_t nwarps = gridDim.x * kWarps;
@@ -1535,7 +1715,7 @@ template <class V>
 __device__ __noinline__ void phase_cert_check(const SolveParams<V>& p, const unsigned int* qcnt,
                                               unsigned int* slot_sum, unsigned int* slot_dyn,
                                               uint32_t* rbm, uint32_t* rbm_clear) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
   const uint32_t nthreads = gridDim.x * kBlock;
   const uint32_t nwords = (p.g.n + 31) >> 5;
@@ -1569,7 +1749,7 @@ __device__ __noinline__ void phase_cert_check(const SolveParams<V>& p, const uns
 template <class V>
 __device__ __noinline__ void phase_cert_apply(const SolveParams<V>& p, uint32_t* chg,
                                               unsigned int* slot_sum) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   const uint32_t nwarps = gridDim.x * kWarps;
   const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5;
   const uint32_t lane = lane_id();
@@ -1592,98 +1772,23 @@ __device__ __noinline__ void phase_cert_apply(const SolveParams<V>& p, uint32_t*
   block_flush(L, p.ctr, slot_sum + 0, s_cnt);
 }
 
-// Activation (solver_par.cpp:402-410): every non-top predecessor of a vertex
-// marked in `chg` enters frontier buffer `nb` once (bitmap dedup), sorted
-// into its size-class sublist; the warp expands CSC columns as one stream.
-// Columns longer than kLongCol (the in-hubs of a power-law arena) are not
-// expanded by one warp: they are queued in p.longcol (count in qlong) for
-// phase_activate_long, which spreads their chunks over the whole grid.
-
-// Frontier appends are buffered per warp in shared memory (the TMA stage
-// area, idle during activation) and published up to kAppendCap entries per
-// atomicAdd, so a large frontier does not serialise on the three list
-// counters.  Warp-uniform.
-constexpr uint32_t kAppendCap = 512;  // entries per class per warp (3 * 2 KB)
-
-struct WarpLists {
-  uint32_t* buf[3];
-  uint32_t cnt[3];
-};
-
-__device__ __forceinline__ WarpLists warp_lists() {
-  extern __shared__ __align__(128) ERec dsm[];
-  uint32_t* base = reinterpret_cast<uint32_t*>(dsm) +
-                   (size_t)(threadIdx.x >> 5) * (kStages * kStageBytes / 4);
-  WarpLists q;
-  for (int c = 0; c < 3; ++c) {
-    q.buf[c] = base + c * kAppendCap;
-    q.cnt[c] = 0;
-  }
-  return q;
-}
-
-__device__ __forceinline__ void lists_flush(WarpLists& q, int c, uint32_t* list,
-                                            unsigned int* count) {
-  __syncwarp();
-  const uint32_t k = q.cnt[c];
-  if (k == 0) return;
-  uint32_t base = 0;
-  if (lane_id() == 0) base = atomicAdd(count, k);
-  base = __shfl_sync(0xffffffffu, base, 0);
-  for (uint32_t i = lane_id(); i < k; i += 32) list[base + i] = q.buf[c][i];
-  q.cnt[c] = 0;
-  __syncwarp();
-}
-
-__device__ __forceinline__ void lists_append(WarpLists& q, bool pred, int c, uint32_t v,
-                                             uint32_t* const* lists, unsigned int* counts) {
-#pragma unroll
-  for (int cc = 0; cc < 3; ++cc) {
-    const bool mine = pred && c == cc;
-    const uint32_t m = __ballot_sync(0xffffffffu, mine);
-    if (!m) continue;
-    if (mine) q.buf[cc][q.cnt[cc] + __popc(m & lanemask_lt())] = v;
-    q.cnt[cc] += __popc(m);
-    if (q.cnt[cc] + 32 > kAppendCap) lists_flush(q, cc, lists[cc], counts + cc);
-  }
-}
-
-template <class V>
-__device__ __forceinline__ void activate_pred(const SolveParams<V>& p, bool valid, uint32_t idx,
-                                              WarpLists& q, uint32_t* const* lists,
-                                              unsigned int* counts, Local& L) {
-  const Graph& g = p.g;
-  bool add = false;
-  uint32_t u = 0;
-  int c = 0;
-  if (valid) {
-    ++L.act;
-    u = __ldg(g.csrc + idx);
-    const uint32_t bit = 1u << (u & 31u);
-    // a plain read first: predecessors shared by many changed vertices (the
-    // in-hubs' neighbours) are already marked and skip the atomic
-    if (!(ldcg(p.frb + (u >> 5)) & bit) && gather(p.f + u) != Top<V>::v) {
-      add = !(atomicOr(p.frb + (u >> 5), bit) & bit);
-      c = size_class(g, u);
-    }
-  }
-  lists_append(q, add, c, u, lists, counts);
-  L.phase_count += add;
-}
-
 template <class V>
 __device__ __noinline__ void phase_activate(const SolveParams<V>& p, const uint32_t* chg,
-                                            int nb, unsigned int* slot_sum, unsigned int* qlong) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+                                            Frontier t, uint32_t* frb_other,
+                                            unsigned int* cnt_next, unsigned int* slot_sum,
+                                            unsigned int* qlong) {
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   const Graph& g = p.g;
   const uint32_t nwords = (g.n + 31) >> 5;
   const uint32_t nwarps = gridDim.x * kWarps;
   const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5;
   Local L;
   WarpLists q = warp_lists();
-  uint32_t* const lists[3] = {p.fr[nb] + p.cbase[0], p.fr[nb] + p.cbase[1],
-                              p.fr[nb] + p.cbase[2]};
-  unsigned int* counts = p.sh->fr_cnt[nb];
+  // the other frontier bitmap may hold a discarded frontier's marks; the
+  // counters of the token after this one start at zero
+  for (uint32_t w = blockIdx.x * kBlock + threadIdx.x; w < nwords; w += gridDim.x * kBlock)
+    frb_other[w] = 0u;
+  if (blockIdx.x == 0 && threadIdx.x < 3) cnt_next[threadIdx.x] = 0u;
   for (uint32_t w0 = gw * 32; w0 < nwords; w0 += nwarps * 32) {
     const uint32_t wi = w0 + lane_id();
     uint32_t bits = wi < nwords ? ldcg(chg + wi) : 0u;
@@ -1702,28 +1807,23 @@ __device__ __noinline__ void phase_activate(const SolveParams<V>& p, const uint3
         }
       }
       warp_expand(b, e, [&](bool valid, uint32_t idx, uint32_t) {
-        activate_pred<V>(p, valid, idx, q, lists, counts, L);
+        activate_pred<V>(p, valid, idx, q, t, L);
       });
     }
   }
-  for (int c = 0; c < 3; ++c) lists_flush(q, c, lists[c], counts + c);
+  for (int c = 0; c < 3; ++c) lists_flush(q, c, t.list[c], t.cnt + c);
   block_flush(L, p.ctr, slot_sum + 2, s_cnt);
 }
 
 // The long columns queued by phase_activate: every warp walks the queue and
 // claims kColChunk-entry chunks of each column from its cursor.
 template <class V>
-__device__ __noinline__ void phase_activate_long(const SolveParams<V>& p, int nb,
-                                                 const unsigned int* qlong,
-                                                 unsigned int* slot_sum) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 1)];
+__device__ __noinline__ void phase_activate_long(const SolveParams<V>& p, Frontier t,
+                                                 uint32_t ncols, unsigned int* slot_sum) {
+  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   const Graph& g = p.g;
   Local L;
   WarpLists q = warp_lists();
-  uint32_t* const lists[3] = {p.fr[nb] + p.cbase[0], p.fr[nb] + p.cbase[1],
-                              p.fr[nb] + p.cbase[2]};
-  unsigned int* counts = p.sh->fr_cnt[nb];
-  const uint32_t ncols = vload(qlong);
   for (uint32_t k = 0; k < ncols; ++k) {
     const uint32_t v = ldcg(p.longcol + 2 * k);
     const uint32_t b = __ldg(g.coff + v), e = __ldg(g.coff + v + 1);
@@ -1736,10 +1836,10 @@ __device__ __noinline__ void phase_activate_long(const SolveParams<V>& p, int nb
       const uint32_t cb = b + c * kColChunk;
       const uint32_t ce = cb + kColChunk < e ? cb + kColChunk : e;
       for (uint32_t i0 = cb; i0 < ce; i0 += 32)
-        activate_pred<V>(p, i0 + lane_id() < ce, i0 + lane_id(), q, lists, counts, L);
+        activate_pred<V>(p, i0 + lane_id() < ce, i0 + lane_id(), q, t, L);
     }
   }
-  for (int c = 0; c < 3; ++c) lists_flush(q, c, lists[c], counts + c);
+  for (int c = 0; c < 3; ++c) lists_flush(q, c, t.list[c], t.cnt + c);
   block_flush(L, p.ctr, slot_sum + 2, s_cnt);
 }
 
@@ -1795,8 +1895,22 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
                      cert_passes = 0;
   int K = p.cert_interval > 0 ? p.cert_interval : 1;
   unsigned long long next_cert = (unsigned long long)K;
-  int buf = 0;
   unsigned int status = 0;
+  // Frontier tokens (struct Frontier): `tok` is the last one consumed or
+  // discarded; the next sparse lift reads tok + 1.  `inplace`: the last lift
+  // was a sparse round that already pushed frontier tok + 1 (`pushed`
+  // entries, `pushed_long` queued long columns).
+  unsigned int tok = 0;
+  bool inplace = false;
+  uint32_t pushed = 0, pushed_long = 0;
+  auto frontier = [&](unsigned int k) {
+    Frontier t;
+    const int b = k & 1;
+    for (int c = 0; c < 3; ++c) t.list[c] = p.fr[b] + p.cbase[c];
+    t.cnt = sh->fr_cnt[k % 3];
+    t.frb = p.frb[b];
+    return t;
+  };
 
   for (;;) {
     // `changed` vertices were raised by round `round`, marked in chg
@@ -1811,16 +1925,24 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
     // activation's top filter may see either the old or the committed value
     // of a predecessor; a stale one only adds a harmless frontier entry)
     const bool fuse_act =
-        !cert_now && p.mode != kModeDense &&
+        !inplace && !cert_now && p.mode != kModeDense &&
         !(p.mode == kModeAuto && (double)changed * p.avg_in_deg * p.sparse_div >= (double)n);
-    begin_phase();
-    if (cert_now) {
-      phase_commit_cert_init<V>(p, chg);  // commit + certificate step 1
-    } else {
-      phase_commit<V>(p, chg);
-      if (fuse_act) phase_activate<V>(p, chg, buf ^ 1, slot_sum(), slot_dyn() + 2);
+    if (!inplace) {  // a Jacobi round: publish its staged values
+      begin_phase();
+      if (cert_now) {
+        phase_commit_cert_init<V>(p, chg);  // commit + certificate step 1
+      } else {
+        phase_commit<V>(p, chg);
+        if (fuse_act)
+          phase_activate<V>(p, chg, frontier(tok + 1), p.frb[tok & 1], sh->fr_cnt[(tok + 2) % 3],
+                            slot_sum(), slot_dyn() + 2);
+      }
+      end_phase(1, 0);
+    } else if (cert_now) {  // in-place round: f is current, only mark the candidates
+      begin_phase();
+      phase_cert_init<V>(p, chg, slot_sum());
+      end_phase(2, 1);
     }
-    end_phase(1, 0);
     if (round >= p.round_budget) {
       status = 5;
       break;
@@ -1883,29 +2005,48 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
         (p.mode == kModeAuto &&
          (certified_any || (double)changed * p.avg_in_deg * p.sparse_div >= (double)n));
     if (!dense) {
-      if (!fuse_act) {
+      uint32_t frontier_n, ncols;
+      if (inplace && !cert_now) {  // pushed by the sparse lift
+        frontier_n = pushed;
+        ncols = pushed_long;
+      } else if (fuse_act) {  // produced by the commit phase
+        frontier_n = prev_sum(2);
+        ncols = vload(sh->dyn[(phase - 1) & 3] + 2);
+      } else {
+        // a certificate attempt after an in-place round used the frontier
+        // lists as its queues: the pushed frontier is discarded and rebuilt
+        if (inplace) ++tok;
         begin_phase();
-        phase_activate<V>(p, chg, buf ^ 1, slot_sum(), slot_dyn() + 2);
+        phase_activate<V>(p, chg, frontier(tok + 1), p.frb[tok & 1], sh->fr_cnt[(tok + 2) % 3],
+                          slot_sum(), slot_dyn() + 2);
         end_phase(3);
+        frontier_n = prev_sum(2);
+        ncols = vload(sh->dyn[(phase - 1) & 3] + 2);
       }
-      uint32_t frontier = prev_sum(2);
-      const unsigned int* qlong = sh->dyn[(phase - 1) & 3] + 2;
-      if (vload(qlong) > 0) {  // in-hub columns: one more phase, chunks over the grid
+      if (ncols > 0) {  // in-hub columns: one more phase, chunks over the grid
         begin_phase();
-        phase_activate_long<V>(p, buf ^ 1, qlong, slot_sum());
+        phase_activate_long<V>(p, frontier(tok + 1), ncols, slot_sum());
         end_phase(3);
-        frontier += prev_sum(2);
+        frontier_n += prev_sum(2);
       }
-      buf ^= 1;
-      if (frontier == 0) break;  // every changed vertex has only top predecessors
+      ++tok;  // the next lift consumes it
+      if (frontier_n == 0) break;  // every changed vertex has only top predecessors
+    } else if (inplace) {
+      ++tok;  // the pushed frontier is discarded (the dense lift clears both bitmaps)
     }
 
     // ---- lift round `round + 1`
     uint32_t* next = p.chg[round & 1];
     begin_phase();
     if (leader && p.timeout_ns && t_prev - t_start > p.timeout_ns) sh->stop = 1;
-    phase_lift<V>(p, dense, buf, next, chg, slot_sum(), slot_dyn());
+    phase_lift<V>(p, dense, frontier(tok), frontier(tok + 1), sh->fr_cnt[(tok + 2) % 3], next,
+                  chg, slot_sum(), slot_dyn());
     end_phase(1);
+    inplace = !dense;
+    if (inplace) {
+      pushed = prev_sum(2);
+      pushed_long = vload(sh->dyn[(phase - 1) & 3] + 2);
+    }
     ++(dense ? rounds_dense : rounds_sparse);
     ++round;
     changed = prev_sum(0);
@@ -1945,7 +2086,9 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
   uint32_t* other = p.chg[(parity & 1) ^ 1];
   switch (step) {
     case kStepRound1: phase_round1<V>(p, cur, sum, dyn); break;
-    case kStepLift: phase_lift<V>(p, true, 0, cur, other, sum, dyn); break;
+    case kStepLift:
+      phase_lift<V>(p, true, Frontier{}, Frontier{}, nullptr, cur, other, sum, dyn);
+      break;
     case kStepCommit: phase_commit<V>(p, cur); break;
     case kStepCertInit: phase_cert_init<V>(p, cur, sum); break;
     case kStepCertPrune: phase_cert_prune<V>(p, sum, dyn, p.rbm[0], p.rbm[1]); break;

@@ -165,7 +165,7 @@ struct egs_ctx {
   void* f = nullptr;
   int2* wit = nullptr;
   uint32_t* chg[2] = {nullptr, nullptr};
-  uint32_t* frb = nullptr;
+  uint32_t* frb[2] = {nullptr, nullptr};  // frontier membership bitmaps
   uint32_t* rbm[2] = {nullptr, nullptr};
   uint32_t* cbm = nullptr;
   uint32_t* cand = nullptr;  // certificate candidate bitmap (n_pad / 32 words)
@@ -256,7 +256,7 @@ void ctx_free(egs_ctx* c) {
   StepTimer tm(c->stream);
   if (c->device >= 0) cudaSetDevice(c->device);
   void* ptrs[] = {c->off,    c->edge,   c->coff, c->csrc,  c->perm, c->inv,
-                  c->f,      c->wit,    c->chg[0], c->chg[1], c->frb,
+                  c->f,      c->wit,    c->chg[0], c->chg[1], c->frb[0], c->frb[1],
                   c->fr[0],  c->fr[1],  c->stage, c->scratch, c->ctr, c->rbm[0], c->rbm[1], c->cbm, c->cand, c->xsend, c->xrecv, c->xcount, c->trace, c->longcol,
                   c->f64};
   if (c->stream) {
@@ -627,7 +627,8 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     c->f = dalloc<uint8_t>((size_t)std::max<uint32_t>(c->n_pad, 1) * vsz);
     c->chg[0] = dalloc<uint32_t>(words);
     c->chg[1] = dalloc<uint32_t>(words);
-    c->frb = dalloc<uint32_t>(words);
+    c->frb[0] = dalloc<uint32_t>(words);
+    c->frb[1] = dalloc<uint32_t>(words);
     c->rbm[0] = dalloc<uint32_t>(words);
     c->rbm[1] = dalloc<uint32_t>(words);
     c->cbm = dalloc<uint32_t>(words);
@@ -735,7 +736,8 @@ egs::SolveParams<V> make_params(egs_ctx* c, unsigned long long* budget_out) {
   p.wit = c->wit;
   p.chg[0] = c->chg[0];
   p.chg[1] = c->chg[1];
-  p.frb = c->frb;
+  p.frb[0] = c->frb[0];
+  p.frb[1] = c->frb[1];
   p.rbm[0] = c->rbm[0];
   p.rbm[1] = c->rbm[1];
   p.cbm = c->cbm;
@@ -841,7 +843,8 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
   CK(cudaMemsetAsync(c->f, 0, (size_t)n * sizeof(V), s));
   CK(cudaMemsetAsync(c->chg[0], 0, words * 4, s));
   CK(cudaMemsetAsync(c->chg[1], 0, words * 4, s));
-  CK(cudaMemsetAsync(c->frb, 0, words * 4, s));
+  CK(cudaMemsetAsync(c->frb[0], 0, words * 4, s));
+  CK(cudaMemsetAsync(c->frb[1], 0, words * 4, s));
   CK(cudaMemsetAsync(c->cbm, 0, words * 4, s));
   CK(cudaMemsetAsync(c->scratch, 0, sizeof(egs::Scratch), s));
   CK(cudaMemsetAsync(c->ctr, 0, egs::kNumCounters * sizeof(unsigned long long), s));
@@ -1043,7 +1046,8 @@ void part_reset(egs_ctx* c) {
   CK(cudaMemsetAsync(c->f, 0, (size_t)std::max<uint32_t>(c->n_pad, 1) * vsz, s));
   CK(cudaMemsetAsync(c->chg[0], 0, words * 4, s));
   CK(cudaMemsetAsync(c->chg[1], 0, words * 4, s));
-  CK(cudaMemsetAsync(c->frb, 0, words * 4, s));
+  CK(cudaMemsetAsync(c->frb[0], 0, words * 4, s));
+  CK(cudaMemsetAsync(c->frb[1], 0, words * 4, s));
   CK(cudaMemsetAsync(c->cbm, 0, words * 4, s));
   CK(cudaMemsetAsync(c->ctr, 0, egs::kNumCounters * sizeof(unsigned long long), s));
   CK(cudaStreamSynchronize(s));

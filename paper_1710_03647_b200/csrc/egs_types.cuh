@@ -76,7 +76,7 @@ struct Scratch {
   unsigned int sum[4][4];    // per-phase-slot sums: 0 changed, 1 removed, 2 seeds
   unsigned int dyn[4][8];    // per-phase-slot work cursors: 0 medium, 1 heavy,
                              // 2.. activation / certificate queues, 7 TMA tiles
-  unsigned int fr_cnt[2][3]; // frontier sublist sizes [buffer][L, M, H]
+  unsigned int fr_cnt[3][3]; // frontier sublist sizes [token % 3][L, M, H]
   unsigned int stop;         // timeout flag
 };
 
@@ -87,7 +87,7 @@ struct SolveParams {
   V* stage;             // lift rounds: raised values, committed after the round
   void* wit;            // player-0 witness edge record (ids < rb[3]), edge format
   uint32_t* chg[2];     // changed-vertex bitmaps, by round parity
-  uint32_t* frb;        // frontier membership bitmap
+  uint32_t* frb[2];     // frontier membership bitmaps [token & 1]
   uint32_t* rbm[2];     // certificate: removed-in-pass bitmaps
   uint32_t* cbm;        // certificate: re-check dedup bitmap
   uint32_t* cand;       // certificate: candidate bitmap
