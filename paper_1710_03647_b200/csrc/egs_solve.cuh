@@ -520,12 +520,16 @@ __device__ __forceinline__ void tma_init_barriers() {
 // (~1-2 us) is covered by the work of the tiles ahead of it.
 constexpr uint32_t kTileClaim = 4;
 
-template <class V, class Load, class Test, class Row, class Fallback>
+struct NoAfter {
+  __device__ void operator()(uint32_t, bool) const {}
+};
+
+template <class V, class Load, class Test, class Row, class Fallback, class After = NoAfter>
 __device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, bool staged, uint32_t lo0,
                                           uint32_t hi0, uint32_t lo1, uint32_t hi1,
                                           unsigned int* cursor, const uint32_t* mask,
                                           uint32_t* chg, Local& L, Load load, Test test,
-                                          Row row, Fallback fallback) {
+                                          Row row, Fallback fallback, After after = After{}) {
   extern __shared__ __align__(128) ERec dsm[];
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   ERec* stage_base = dsm + (size_t)warp * kStages * kStageRecs;
@@ -566,6 +570,7 @@ __device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, bool staged, 
       const uint32_t m = __ballot_sync(0xffffffffu, ch);
       if (m && lane == 0) atomicOr(chg + w, m);
       L.phase_count += ch;
+      after(v, ch);  // warp-uniform
     }
     return;
   }
@@ -635,6 +640,7 @@ __device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, bool staged, 
     const uint32_t m = __ballot_sync(0xffffffffu, ch);
     if (m && lane == 0) atomicOr(chg + t.w, m);
     L.phase_count += ch;
+    after(v, ch);  // warp-uniform
   };
 
   // tile i is processed from slot i % kStages while the copies of tiles
@@ -814,6 +820,7 @@ constexpr uint32_t kAppendCap = 512;  // entries per class per warp (3 * 2 KB)
 struct WarpLists {
   uint32_t* buf[3];
   uint32_t cnt[3];
+  uint32_t cap;  // entries per class buffer
 };
 
 // A frontier being produced: its three class sublists, their counters and
@@ -836,6 +843,21 @@ __device__ __forceinline__ WarpLists warp_lists() {
     q.buf[c] = base + c * kAppendCap;
     q.cnt[c] = 0;
   }
+  q.cap = kAppendCap;
+  return q;
+}
+
+// Small per-warp buffers in static shared memory, for phases whose dynamic
+// shared memory holds TMA stages (the certificate pass's re-check pushes).
+constexpr uint32_t kSmallAppendCap = 64;
+__device__ __forceinline__ WarpLists warp_lists_small() {
+  __shared__ uint32_t s_lists[kWarps][3][kSmallAppendCap];
+  WarpLists q;
+  for (int c = 0; c < 3; ++c) {
+    q.buf[c] = s_lists[threadIdx.x >> 5][c];
+    q.cnt[c] = 0;
+  }
+  q.cap = kSmallAppendCap;
   return q;
 }
 
@@ -861,25 +883,29 @@ __device__ __forceinline__ void lists_append(WarpLists& q, bool pred, int c, uin
     if (!m) continue;
     if (mine) q.buf[cc][q.cnt[cc] + __popc(m & lanemask_lt())] = v;
     q.cnt[cc] += __popc(m);
-    if (q.cnt[cc] + 32 > kAppendCap) lists_flush(q, cc, lists[cc], counts + cc);
+    if (q.cnt[cc] + 32 > q.cap) lists_flush(q, cc, lists[cc], counts + cc);
   }
 }
 
 template <class V>
 __device__ __forceinline__ void activate_pred(const SolveParams<V>& p, bool valid, uint32_t idx,
                                               WarpLists& q, const Frontier& t, Local& L,
-                                              bool pushing = false) {
+                                              bool pushing = false, bool cert = false) {
   const Graph& g = p.g;
   bool add = false;
   uint32_t u = 0;
   int c = 0;
   if (valid) {
-    ++L.act;
+    if (!cert) ++L.act;
     u = __ldg(g.csrc + idx);
     const uint32_t bit = 1u << (u & 31u);
     // a plain read first: predecessors shared by many changed vertices (the
-    // in-hubs' neighbours) are already marked and skip the atomic
-    if (!(ldcg(t.frb + (u >> 5)) & bit) && gather(p.f + u) != Top<V>::v) {
+    // in-hubs' neighbours) are already marked and skip the atomic.  The
+    // certificate's re-check queue takes the owned candidates instead of the
+    // non-top vertices.
+    const bool want = cert ? owned(p, u) && ((ldcg(p.cand + (u >> 5)) >> (u & 31u)) & 1u)
+                           : gather(p.f + u) != Top<V>::v;
+    if (!(ldcg(t.frb + (u >> 5)) & bit) && want) {
       add = !(atomicOr(t.frb + (u >> 5), bit) & bit);
       c = size_class(g, u);
     }
@@ -889,6 +915,22 @@ __device__ __forceinline__ void activate_pred(const SolveParams<V>& p, bool vali
     L.pushed += add;
   else
     L.phase_count += add;
+}
+
+// Certificate passes push the candidate predecessors of each removed vertex
+// into the next pass's re-check queue `t` (dedup bitmap t.frb).  Warp-uniform.
+template <class V>
+__device__ __forceinline__ void push_cert_preds(const SolveParams<V>& p, bool removed, uint32_t v,
+                                                WarpLists& q, const Frontier& t, Local& L) {
+  if (!t.cnt || !__any_sync(0xffffffffu, removed)) return;
+  uint32_t b = 0, e = 0;
+  if (removed) {
+    b = __ldg(p.g.coff + v);
+    e = __ldg(p.g.coff + v + 1);
+  }
+  warp_expand(b, e, [&](bool valid, uint32_t idx, uint32_t) {
+    activate_pred<V>(p, valid, idx, q, t, L, true, true);
+  });
 }
 
 // Push activation of a sparse round: the predecessors of the vertices of the
@@ -1546,7 +1588,8 @@ __device__ __forceinline__ bool cert_check_thread(const SolveParams<V>& p, uint3
 template <class V, class ItemsH, class ItemsM>
 __device__ __forceinline__ void cert_long_rows(const SolveParams<V>& p, uint32_t nH,
                                                ItemsH itemsH, uint32_t nM, ItemsM itemsM,
-                                               unsigned int* slot_dyn, uint32_t* rbm, Local& L) {
+                                               unsigned int* slot_dyn, uint32_t* rbm, Local& L,
+                                               WarpLists& q, const Frontier& qt) {
   __shared__ unsigned int s_item;
   const Graph& g = p.g;
   for (;;) {
@@ -1569,6 +1612,7 @@ __device__ __forceinline__ void cert_long_rows(const SolveParams<V>& p, uint32_t
         ++L.phase_count;
       }
     }
+    if (threadIdx.x < 32) push_cert_preds<V>(p, !keep && threadIdx.x == 0, v, q, qt, L);
   }
   __syncthreads();
   WarpClaim wc;
@@ -1588,6 +1632,7 @@ __device__ __forceinline__ void cert_long_rows(const SolveParams<V>& p, uint32_t
         ++L.phase_count;
       }
     }
+    push_cert_preds<V>(p, !keep && lane_id() == 0, v, q, qt, L);
   }
 }
 
@@ -1596,17 +1641,24 @@ __device__ __forceinline__ void cert_long_rows(const SolveParams<V>& p, uint32_t
 template <class V>
 __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned int* slot_sum,
                                               unsigned int* slot_dyn, uint32_t* rbm,
-                                              uint32_t* rbm_clear) {
+                                              uint32_t* rbm_clear, Frontier qt = Frontier{},
+                                              uint32_t* qclear = nullptr) {
   __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   const Graph& g = p.g;
   const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
   const uint32_t nthreads = gridDim.x * kBlock;
   const uint32_t nwords = (g.n + 31) >> 5;
   Local L;
-  for (uint32_t w = tid; w < nwords; w += nthreads) rbm_clear[w] = 0u;
+  WarpLists q = warp_lists_small();
+  // (a dense pass leaves the last pass's re-check queue unread: its dedup
+  // bitmap is cleared whole)
+  for (uint32_t w = tid; w < nwords; w += nthreads) {
+    rbm_clear[w] = 0u;
+    if (qclear) qclear[w] = 0u;
+  }
   auto itH = [gp = &g](uint32_t i) { return class_item(*gp, 2, i); };
   auto itM = [gp = &g](uint32_t i) { return class_item(*gp, 1, i); };
-  cert_long_rows<V>(p, class_size(g, 2), itH, class_size(g, 1), itM, slot_dyn, rbm, L);
+  cert_long_rows<V>(p, class_size(g, 2), itH, class_size(g, 1), itM, slot_dyn, rbm, L, q, qt);
   // light candidates: one row per lane through the TMA tile pipeline (tiles
   // without a candidate are skipped); removals are published in rbm
   {
@@ -1655,91 +1707,92 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
       return !keep;
     };
     auto fallback = [&](uint32_t v, V) { return cert_check_thread<V>(p, v, L); };
+    auto after = [&](uint32_t v, bool removed) { push_cert_preds<V>(p, removed, v, q, qt, L); };
     tma_tiles<V>(p, (p.use_tma & kTmaCert) != 0, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]),
                  clip_lo(p, g.rb[kP1L]),
                  clip_hi(p, g.rb[kP1M]), slot_dyn + kTileCursor, p.cand, rbm, L, load, test,
-                 row, fallback);
+                 row, fallback, after);
   }
+  if (qt.cnt)
+    for (int c = 0; c < 3; ++c) lists_flush(q, c, qt.list[c], qt.cnt + c);
   block_flush(L, p.ctr, slot_sum + 1, s_cnt);
 }
 
-// Sparse pass, step 1: the candidate predecessors of the vertices removed in
-// the last pass (bits of `rbm_in`) are queued once each (dedup bitmap cbm)
-// into the class sublists of p.fr[0], sized by qcnt[0..2] (this phase's
-// zeroed cursor slot); count -> slot_sum[2].
+// After a dense pass (which does not push: its removals are many, and the
+// pushes would stall its tile pipeline) the first sparse pass's queue is
+// built here from the removal bits `rbm_in`: the owned candidate
+// predecessors of every removed vertex, once each (dedup t.frb).
 template <class V>
 __device__ __noinline__ void phase_cert_mark(const SolveParams<V>& p, const uint32_t* rbm_in,
-                                             unsigned int* slot_sum, unsigned int* qcnt) {
+                                             Frontier t, unsigned int* slot_sum) {
   __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
-  const Graph& g = p.g;
-  const uint32_t nwords = (g.n + 31) >> 5;
+  const uint32_t nwords = (p.g.n + 31) >> 5;
   const uint32_t nwarps = gridDim.x * kWarps;
   const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5;
   Local L;
+  WarpLists q = warp_lists();
   for (uint32_t w0 = gw * 32; w0 < nwords; w0 += nwarps * 32) {
     const uint32_t wi = w0 + lane_id();
     uint32_t bits = wi < nwords ? ldcg(rbm_in + wi) : 0u;
     while (__any_sync(0xffffffffu, bits != 0u)) {
-      uint32_t b = 0, e = 0;
+      uint32_t u = 0;
+      bool any = false;
       if (bits) {
-        const uint32_t u = (wi << 5) + (__ffs(bits) - 1);
+        u = (wi << 5) + (__ffs(bits) - 1);
         bits &= bits - 1;
-        b = __ldg(g.coff + u);
-        e = __ldg(g.coff + u + 1);
+        any = true;
       }
-      warp_expand(b, e, [&](bool valid, uint32_t idx, uint32_t) {
-        bool add = false;
-        uint32_t v = 0;
-        int c = 0;
-        if (valid) {
-          v = __ldg(g.csrc + idx);
-          if (owned(p, v) && cand_bit(p, v)) {
-            const uint32_t bit = 1u << (v & 31u);
-            add = !(atomicOr(p.cbm + (v >> 5), bit) & bit);
-            c = size_class(g, v);
-          }
-        }
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc)
-          warp_append(add && c == cc, v, p.fr[0] + p.cbase[cc], qcnt + cc);
-        L.phase_count += add;
-      });
+      push_cert_preds<V>(p, any, u, q, t, L);
     }
   }
+  for (int c = 0; c < 3; ++c) lists_flush(q, c, t.list[c], t.cnt + c);
   block_flush(L, p.ctr, slot_sum + 2, s_cnt);
 }
 
-// Sparse pass, step 2: re-check the queued candidates (removed -> slot_sum[1],
-// bits -> rbm); clears their dedup bits and the stale bitmap rbm_clear.
+// Sparse pass: re-check the queued candidates -- the candidate predecessors
+// of the last pass's removals, pushed by that pass (queue `cur`, counts
+// qcnt) -- and push the candidate predecessors of this pass's removals into
+// queue `nxt`; removed -> slot_sum[1], bits -> rbm.  Clears the dedup bits of
+// the entries it reads and the stale bitmap rbm_clear.
 template <class V>
-__device__ __noinline__ void phase_cert_check(const SolveParams<V>& p, const unsigned int* qcnt,
-                                              unsigned int* slot_sum, unsigned int* slot_dyn,
-                                              uint32_t* rbm, uint32_t* rbm_clear) {
+__device__ __noinline__ void phase_cert_check(const SolveParams<V>& p, Frontier cur,
+                                              const unsigned int* qcnt, unsigned int* slot_sum,
+                                              unsigned int* slot_dyn, uint32_t* rbm,
+                                              uint32_t* rbm_clear, Frontier nxt) {
   __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
   const uint32_t nthreads = gridDim.x * kBlock;
   const uint32_t nwords = (p.g.n + 31) >> 5;
   Local L;
+  WarpLists q = warp_lists_small();
   for (uint32_t w = tid; w < nwords; w += nthreads) rbm_clear[w] = 0u;
   const uint32_t cL = vload(qcnt + 0);
   const uint32_t cM = vload(qcnt + 1);
   const uint32_t cH = vload(qcnt + 2);
-  const uint32_t* list = p.fr[0];
-  const uint32_t* lM = list + p.cbase[1];
-  const uint32_t* lH = list + p.cbase[2];
+  const uint32_t* lL = cur.list[0];
+  const uint32_t* lM = cur.list[1];
+  const uint32_t* lH = cur.list[2];
   auto itH = [=](uint32_t i) { return ldcg(lH + i); };
   auto itM = [=](uint32_t i) { return ldcg(lM + i); };
-  cert_long_rows<V>(p, cH, itH, cM, itM, slot_dyn, rbm, L);
-  for (uint32_t i = tid; i < cL; i += nthreads) {
-    const uint32_t v = ldcg(list + i);
-    if (cert_check_thread<V>(p, v, L)) {
+  cert_long_rows<V>(p, cH, itH, cM, itM, slot_dyn, rbm, L, q, nxt);
+  for (uint32_t i0 = blockIdx.x * kBlock + (threadIdx.x & ~31u); i0 < cL; i0 += nthreads) {
+    const uint32_t i = i0 + lane_id();
+    uint32_t v = 0;
+    bool removed = false;
+    if (i < cL) {
+      v = ldcg(lL + i);
+      removed = cert_check_thread<V>(p, v, L);
+    }
+    if (removed) {
       set_bit(rbm, v);
       ++L.phase_count;
     }
+    push_cert_preds<V>(p, removed, v, q, nxt, L);
   }
+  for (int c = 0; c < 3; ++c) lists_flush(q, c, nxt.list[c], nxt.cnt + c);
   for (uint32_t i = tid; i < cL + cM + cH; i += nthreads) {
-    const uint32_t v = i < cL ? ldcg(list + i) : i < cL + cM ? ldcg(lM + (i - cL)) : ldcg(lH + (i - cL - cM));
-    atomicAnd(p.cbm + (v >> 5), ~(1u << (v & 31u)));
+    const uint32_t v = i < cL ? ldcg(lL + i) : i < cL + cM ? ldcg(lM + (i - cL)) : ldcg(lH + (i - cL - cM));
+    atomicAnd(cur.frb + (v >> 5), ~(1u << (v & 31u)));
   }
   block_flush(L, p.ctr, slot_sum + 1, s_cnt);
 }
@@ -1956,29 +2009,49 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
     bool certified_any = false;
     if (cert_now) {
       ++cert_attempts;
-      // pass 1 dense; later passes sparse while the removals are few
+      // pass 1 dense; later passes sparse while the removals are few.  Every
+      // pass pushes the candidate predecessors of its removals into the next
+      // pass's re-check queue `cq + 1` (lists p.fr[(cq + 1) & 1], dedup bitmap
+      // p.cbm[(cq + 1) & 1], counters in the pushing phase's dyn slot 3..5).
       int rb = 1;
+      unsigned int cq = 0;
+      auto queue = [&](unsigned int k, unsigned int* cnt) {
+        Frontier t;
+        for (int c = 0; c < 3; ++c) t.list[c] = p.fr[k & 1] + p.cbase[c];
+        t.cnt = cnt;
+        t.frb = p.cbm[k & 1];
+        return t;
+      };
       begin_phase();
       phase_cert_prune<V>(p, slot_sum(), slot_dyn(), p.rbm[1], p.rbm[0]);
       end_phase(2, 2);
       ++cert_passes;
+      bool queued = false;  // did the last pass push a re-check queue (token cq)?
       uint32_t removed = prev_sum(1);
       while (removed > 0) {
         const bool sparse_pass =
             p.mode != kModeDense &&
-            (double)removed * p.avg_in_deg * p.sparse_div < (double)n;
+            (double)removed * p.avg_in_deg * p.cert_sparse_div < (double)n;
         if (sparse_pass) {
+          if (!queued) {  // after a dense pass: the queue from its removal bits
+            begin_phase();
+            phase_cert_mark<V>(p, p.rbm[rb], queue(cq + 1, slot_dyn() + 3), slot_sum());
+            end_phase(2, 3);
+            ++cq;
+          }
+          unsigned int* qcnt = sh->dyn[(phase - 1) & 3] + 3;  // the queue's counters
           begin_phase();
-          phase_cert_mark<V>(p, p.rbm[rb], slot_sum(), slot_dyn());
+          phase_cert_check<V>(p, queue(cq, qcnt), qcnt, slot_sum(), slot_dyn(), p.rbm[rb ^ 1],
+                              p.rbm[rb], queue(cq + 1, slot_dyn() + 3));
           end_phase(2, 3);
-          const unsigned int* queued = sh->dyn[(phase - 1) & 3];
-          begin_phase();
-          phase_cert_check<V>(p, queued, slot_sum(), slot_dyn(), p.rbm[rb ^ 1], p.rbm[rb]);
-          end_phase(2, 3);
+          ++cq;
+          queued = true;
         } else {
           begin_phase();
-          phase_cert_prune<V>(p, slot_sum(), slot_dyn(), p.rbm[rb ^ 1], p.rbm[rb]);
+          phase_cert_prune<V>(p, slot_sum(), slot_dyn(), p.rbm[rb ^ 1], p.rbm[rb], Frontier{},
+                              queued ? p.cbm[cq & 1] : nullptr);
           end_phase(2, 2);
+          queued = false;
         }
         rb ^= 1;
         ++cert_passes;

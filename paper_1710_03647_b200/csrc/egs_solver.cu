@@ -167,7 +167,7 @@ struct egs_ctx {
   uint32_t* chg[2] = {nullptr, nullptr};
   uint32_t* frb[2] = {nullptr, nullptr};  // frontier membership bitmaps
   uint32_t* rbm[2] = {nullptr, nullptr};
-  uint32_t* cbm = nullptr;
+  uint32_t* cbm[2] = {nullptr, nullptr};
   uint32_t* cand = nullptr;  // certificate candidate bitmap (n_pad / 32 words)
   // multi-GPU sparse exchange buffers (egs_part_pack / egs_part_unpack)
   uint64_t* xsend = nullptr;
@@ -257,7 +257,7 @@ void ctx_free(egs_ctx* c) {
   if (c->device >= 0) cudaSetDevice(c->device);
   void* ptrs[] = {c->off,    c->edge,   c->coff, c->csrc,  c->perm, c->inv,
                   c->f,      c->wit,    c->chg[0], c->chg[1], c->frb[0], c->frb[1],
-                  c->fr[0],  c->fr[1],  c->stage, c->scratch, c->ctr, c->rbm[0], c->rbm[1], c->cbm, c->cand, c->xsend, c->xrecv, c->xcount, c->trace, c->longcol,
+                  c->fr[0],  c->fr[1],  c->stage, c->scratch, c->ctr, c->rbm[0], c->rbm[1], c->cbm[0], c->cbm[1], c->cand, c->xsend, c->xrecv, c->xcount, c->trace, c->longcol,
                   c->f64};
   if (c->stream) {
     for (void* p : ptrs) dfree(p, c->stream);
@@ -631,7 +631,8 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     c->frb[1] = dalloc<uint32_t>(words);
     c->rbm[0] = dalloc<uint32_t>(words);
     c->rbm[1] = dalloc<uint32_t>(words);
-    c->cbm = dalloc<uint32_t>(words);
+    c->cbm[0] = dalloc<uint32_t>(words);
+    c->cbm[1] = dalloc<uint32_t>(words);
     c->cand = dalloc<uint32_t>(std::max<size_t>(words, ((size_t)c->n_pad + 31) / 32));
     CK(cudaMemsetAsync(c->cand, 0, std::max<size_t>(words, ((size_t)c->n_pad + 31) / 32) * 4,
                        c->stream));
@@ -740,7 +741,8 @@ egs::SolveParams<V> make_params(egs_ctx* c, unsigned long long* budget_out) {
   p.frb[1] = c->frb[1];
   p.rbm[0] = c->rbm[0];
   p.rbm[1] = c->rbm[1];
-  p.cbm = c->cbm;
+  p.cbm[0] = c->cbm[0];
+  p.cbm[1] = c->cbm[1];
   p.cand = c->cand;
   p.longcol = c->longcol;
   p.fr[0] = c->fr[0];
@@ -761,6 +763,8 @@ egs::SolveParams<V> make_params(egs_ctx* c, unsigned long long* budget_out) {
   p.cert_interval = o.cert_interval > 0 ? o.cert_interval : 1;
   p.cert_growth = o.cert_growth > 0 ? o.cert_growth : 4;
   p.sparse_div = o.sparse_div > 0 ? (uint32_t)o.sparse_div : 4u;
+  p.cert_sparse_div = (float)p.sparse_div;
+  if (const char* e = std::getenv("EGS_CERT_SPARSE_DIV")) p.cert_sparse_div = (float)std::atof(e);
   p.avg_in_deg = n ? (float)((double)c->m / (double)n) : 1.0f;
   if (p.avg_in_deg < 1.0f) p.avg_in_deg = 1.0f;
   // default budget |E|*(cap+1)+1 (solver_par.cpp:94-98), saturating
@@ -845,7 +849,8 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
   CK(cudaMemsetAsync(c->chg[1], 0, words * 4, s));
   CK(cudaMemsetAsync(c->frb[0], 0, words * 4, s));
   CK(cudaMemsetAsync(c->frb[1], 0, words * 4, s));
-  CK(cudaMemsetAsync(c->cbm, 0, words * 4, s));
+  CK(cudaMemsetAsync(c->cbm[0], 0, words * 4, s));
+  CK(cudaMemsetAsync(c->cbm[1], 0, words * 4, s));
   CK(cudaMemsetAsync(c->scratch, 0, sizeof(egs::Scratch), s));
   CK(cudaMemsetAsync(c->ctr, 0, egs::kNumCounters * sizeof(unsigned long long), s));
   void* args[] = {&p};
@@ -1048,7 +1053,8 @@ void part_reset(egs_ctx* c) {
   CK(cudaMemsetAsync(c->chg[1], 0, words * 4, s));
   CK(cudaMemsetAsync(c->frb[0], 0, words * 4, s));
   CK(cudaMemsetAsync(c->frb[1], 0, words * 4, s));
-  CK(cudaMemsetAsync(c->cbm, 0, words * 4, s));
+  CK(cudaMemsetAsync(c->cbm[0], 0, words * 4, s));
+  CK(cudaMemsetAsync(c->cbm[1], 0, words * 4, s));
   CK(cudaMemsetAsync(c->ctr, 0, egs::kNumCounters * sizeof(unsigned long long), s));
   CK(cudaStreamSynchronize(s));
   c->solved = true;

@@ -89,7 +89,7 @@ struct SolveParams {
   uint32_t* chg[2];     // changed-vertex bitmaps, by round parity
   uint32_t* frb[2];     // frontier membership bitmaps [token & 1]
   uint32_t* rbm[2];     // certificate: removed-in-pass bitmaps
-  uint32_t* cbm;        // certificate: re-check dedup bitmap
+  uint32_t* cbm[2];     // certificate: re-check queue dedup bitmaps [queue & 1]
   uint32_t* cand;       // certificate: candidate bitmap
   uint32_t* longcol;    // activation: queued long CSC columns {vertex, chunk cursor}
   uint32_t* fr[2];      // frontier lists; sublist c starts at cbase[c]
@@ -103,6 +103,7 @@ struct SolveParams {
   int cert_interval;
   int cert_growth;          // interval multiplier after each attempt (4)
   uint32_t sparse_div;      // next round sparse iff est. frontier * div < n
+  float cert_sparse_div;    // certificate pass sparse iff removed * deg * div < n
   float avg_in_deg;
   unsigned long long* trace;   // optional: per-phase (kind << 56 | ns) log, kTraceCap entries
   unsigned long long round_budget;
