@@ -179,6 +179,34 @@ def test_rmat16_golden(egs, golden):
     assert f"{fnv1a64(sol):016x}" == golden[key]["solution_fnv"]
 
 
+@pytest.mark.parametrize("tma_mask", ["0", "7"])
+@pytest.mark.parametrize("cert_div", ["0.001", "1000"])
+def test_schedule_knobs_give_identical_bytes(egs, golden, oracle, monkeypatch, tma_mask,
+                                            cert_div):
+    """Every light-row phase staged by TMA (mask 7) or read with plain loads
+    (mask 0); certificate passes all dense (div 0.001) or sparse after the
+    first (div 1000: mark, then push-style re-check queues).  The bytes must
+    not move: golden vectors of the reference and random arenas vs the oracle."""
+    monkeypatch.setenv("EGS_TMA_MASK", tma_mask)
+    monkeypatch.setenv("EGS_CERT_SPARSE_DIV", cert_div)
+    for key, make in [("rmat/16/16/100/1", lambda: egs.GameArena.rmat(16, 16, 100, 1)),
+                      ("fixed/100000/16/100/1", lambda: egs.GameArena.fixed(100000, 16, 100, 1)),
+                      ("fixed/10000/4/100/1", lambda: egs.GameArena.fixed(10000, 4, 100, 1))]:
+        if key not in golden:
+            continue
+        a = make()
+        for mode in MODES:
+            rep = _solve(egs, a, mode=mode)
+            sol = egs.write_solution(a, rep).encode()
+            assert f"{fnv1a64(sol):016x}" == golden[key]["solution_fnv"], (key, mode)
+    for seed in range(40):
+        n, edges, owners = random_arena(7000 + seed, max_n=200, max_deg=40, W=60)
+        a = egs.GameArena.build(n, edges, owners)
+        g = oracle.build(n, edges, owners)
+        want, _ = oracle.solve_seq(g)
+        assert np.array_equal(_solve(egs, a, cert_interval=1).measure, want), seed
+
+
 def test_value_width_boundary(egs, oracle):
     # credit_cap = 2^31 - 2 stays on the u32 path, 2^31 - 1 takes u64 (u32
     # reserves 2^32 - 1 for top and the top bit for the certificate's mark);
