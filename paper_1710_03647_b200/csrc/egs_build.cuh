@@ -52,6 +52,11 @@ __global__ void k_permute(uint32_t n, const uint32_t* inv, const uint64_t* off64
   if (blockIdx.x == 0 && threadIdx.x == 0) deg_new[n] = 0;
 }
 
+// Rows longer than kRelabelLong (the R-MAT hubs, up to 1.6e5 edges) are not
+// expanded by one warp: the row-wise kernels queue them, and the *_long
+// kernels spread each queued row's edges over the whole grid.
+constexpr uint32_t kRelabelLong = 2048;
+
 // Edge relabelling, pipelined with the chunked upload (egs_solver.cu
 // build_arena): old rows [r0, r1) whose targets have arrived are copied to
 // their relabelled slots, targets mapped through perm, with the (dst, src)
@@ -62,7 +67,7 @@ __global__ void __launch_bounds__(256)
     k_relabel_targets(uint32_t n, uint32_t r0, uint32_t r1, const uint64_t* off64,
                       const uint32_t* dst, const uint32_t* perm, const uint32_t* off_new,
                       void* edge, uint32_t tbits, uint32_t* ckey, uint32_t* cval,
-                      unsigned int* bad) {
+                      unsigned int* bad, uint32_t* longlist, unsigned int* longcnt) {
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int* ex = static_cast<int*>(edge);
@@ -76,6 +81,10 @@ __global__ void __launch_bounds__(256)
       e = (uint32_t)off64[o + 1];
       rn = perm[o];
       delta = off_new[rn] - b;
+      if (e - b > kRelabelLong) {  // a hub: its edges go to the whole grid
+        longlist[atomicAdd(longcnt, 1u)] = o;
+        e = b;
+      }
     }
     warp_expand(b, e, [&](bool valid, uint32_t idx, uint32_t owner_lane) {
       const uint32_t d = __shfl_sync(0xffffffffu, delta, owner_lane);
@@ -105,7 +114,7 @@ template <class W>
 __global__ void __launch_bounds__(256)
     k_relabel_weights(uint32_t r0, uint32_t r1, const uint64_t* off64, const W* wn,
                       const uint32_t* perm, const uint32_t* off_new, void* edge,
-                      uint32_t tbits) {
+                      uint32_t tbits, uint32_t* longlist, unsigned int* longcnt) {
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int* ex = static_cast<int*>(edge);
@@ -117,6 +126,10 @@ __global__ void __launch_bounds__(256)
       b = (uint32_t)off64[o];
       e = (uint32_t)off64[o + 1];
       delta = off_new[perm[o]] - b;
+      if (e - b > kRelabelLong) {
+        longlist[atomicAdd(longcnt, 1u)] = o;
+        e = b;
+      }
     }
     warp_expand(b, e, [&](bool valid, uint32_t idx, uint32_t owner_lane) {
       const uint32_t d = __shfl_sync(0xffffffffu, delta, owner_lane);
@@ -127,6 +140,59 @@ __global__ void __launch_bounds__(256)
           ex[2 * (size_t)(idx + d) + 1] = (int)wn[idx];
       }
     });
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    k_relabel_targets_long(uint32_t n, const uint32_t* longlist, const unsigned int* longcnt,
+                           const uint64_t* off64, const uint32_t* dst, const uint32_t* perm,
+                           const uint32_t* off_new, void* edge, uint32_t tbits, uint32_t* ckey,
+                           uint32_t* cval, unsigned int* bad) {
+  int* ex = static_cast<int*>(edge);
+  uint32_t* px = static_cast<uint32_t*>(edge);
+  unsigned int flag = 0;
+  const uint32_t cnt = *longcnt;
+  for (uint32_t k = 0; k < cnt; ++k) {
+    const uint32_t o = longlist[k];
+    const uint32_t b = (uint32_t)off64[o], e = (uint32_t)off64[o + 1];
+    const uint32_t rn = perm[o];
+    const uint32_t d = off_new[rn] - b;
+    for (uint32_t idx = b + blockIdx.x * blockDim.x + threadIdx.x; idx < e;
+         idx += gridDim.x * blockDim.x) {
+      const uint32_t pos = idx + d;
+      const uint32_t t0 = dst[idx];
+      if (t0 >= n) flag |= 2u;
+      const uint32_t t = perm[t0 < n ? t0 : 0];
+      if (tbits)
+        px[pos] = t;
+      else
+        ex[2 * (size_t)pos] = (int)t;
+      ckey[pos] = t;
+      cval[pos] = rn;
+    }
+  }
+  if (flag) atomicOr(bad, flag);
+}
+
+template <class W>
+__global__ void __launch_bounds__(256)
+    k_relabel_weights_long(const uint32_t* longlist, const unsigned int* longcnt,
+                           const uint64_t* off64, const W* wn, const uint32_t* perm,
+                           const uint32_t* off_new, void* edge, uint32_t tbits) {
+  int* ex = static_cast<int*>(edge);
+  uint32_t* px = static_cast<uint32_t*>(edge);
+  const uint32_t cnt = *longcnt;
+  for (uint32_t k = 0; k < cnt; ++k) {
+    const uint32_t o = longlist[k];
+    const uint32_t b = (uint32_t)off64[o], e = (uint32_t)off64[o + 1];
+    const uint32_t d = off_new[perm[o]] - b;
+    for (uint32_t idx = b + blockIdx.x * blockDim.x + threadIdx.x; idx < e;
+         idx += gridDim.x * blockDim.x) {
+      if (tbits)
+        px[idx + d] |= (uint32_t)(int)wn[idx] << tbits;
+      else
+        ex[2 * (size_t)(idx + d) + 1] = (int)wn[idx];
+    }
   }
 }
 

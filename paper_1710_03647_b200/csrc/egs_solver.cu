@@ -330,10 +330,18 @@ void* pinned_stage(uint64_t bytes) {
 // checking the range; each chunk's DMA and device relabel are queued as soon
 // as it is converted, while the targets are still on the wire and the
 // transpose sorts.  C4 (|w| <= 100) sends 1 byte per weight instead of 8.
+// Queued long rows of the relabel kernels (egs_build.cuh kRelabelLong): one
+// list region of `cap` rows and one counter per chunk, for targets and weights.
+struct LongRows {
+  uint32_t* list;
+  unsigned int* cnt;
+  uint32_t cap;
+};
+
 template <class W>
 bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint32_t>& rows,
                     std::vector<cudaEvent_t>& ew, std::vector<cudaEvent_t>& et,
-                    const uint64_t* off64, void* wdev) {
+                    const uint64_t* off64, void* wdev, LongRows lw) {
   cudaStream_t sc = c->copy_stream, sw = c->aux_stream;
   const int nch = (int)rows.size() - 1;
   const uint64_t m = c->m;
@@ -381,7 +389,10 @@ bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint3
     if (c->tbits) CK(cudaStreamWaitEvent(sw, et[k], 0));
     egs::k_relabel_weights<W><<<grid_for((uint64_t)(rows[k + 1] - rows[k]) * 4, c->num_sms),
                                 256, 0, sw>>>(rows[k], rows[k + 1], off64, wd, c->perm, c->off,
-                                              c->edge, c->tbits);
+                                              c->edge, c->tbits, lw.list + (size_t)k * lw.cap,
+                                              lw.cnt + k);
+    egs::k_relabel_weights_long<W><<<2 * c->num_sms, 256, 0, sw>>>(
+        lw.list + (size_t)k * lw.cap, lw.cnt + k, off64, wd, c->perm, c->off, c->edge, c->tbits);
     CK(cudaGetLastError());
   }
   if (self_worker.joinable()) self_worker.join();
@@ -406,12 +417,18 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   cudaStream_t s = c->stream, sc = c->copy_stream, sw = c->aux_stream;
   const int sms = c->num_sms;
   DevBuf d_off64, d_dst, d_wn, d_owner, d_key, d_keys, d_val, d_misc, d_tmp, d_ck0, d_cv0,
-      d_ck1;
+      d_ck1, d_long;
   uint64_t* off64 = d_off64.alloc<uint64_t>((size_t)n + 1);
   uint32_t* dst = d_dst.alloc<uint32_t>(m);
   void* wn = d_wn.alloc<int32_t>(m);  // narrowed weights (int8/16/32)
   uint8_t* owner = d_owner.alloc<uint8_t>(n);
-  unsigned int* misc = d_misc.alloc<unsigned int>(32);  // [0..15] hist, [16] bad
+  // [0..15] class histogram, [16] bad, [32..63] long-row counters (targets,
+  // weights) of the 16 chunks
+  unsigned int* misc = d_misc.alloc<unsigned int>(64);
+  const uint32_t long_cap = (uint32_t)(m / egs::kRelabelLong + 1);
+  uint32_t* long_lists = d_long.alloc<uint32_t>((size_t)2 * 16 * long_cap);
+  const LongRows lt{long_lists, misc + 32, long_cap};
+  const LongRows lw{long_lists + (size_t)16 * long_cap, misc + 48, long_cap};
   uint8_t* key = d_key.alloc<uint8_t>(n);
   uint8_t* keys_sorted = d_keys.alloc<uint8_t>(n);
   uint32_t* val = d_val.alloc<uint32_t>(n);
@@ -434,7 +451,7 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   c->edge = dalloc<uint8_t>(m * rec_bytes(c) + 16);
   c->csrc = dalloc<uint32_t>(m);
   c->coff = dalloc<uint32_t>((size_t)n + 1);
-  CK(cudaMemsetAsync(misc, 0, 32 * sizeof(unsigned int), s));
+  CK(cudaMemsetAsync(misc, 0, 64 * sizeof(unsigned int), s));
   tm.mark("pool allocations");
   cudaEvent_t e_alloc, e_vert, e_perm, e_tail;
   CK(cudaEventCreateWithFlags(&e_alloc, cudaEventDisableTiming));
@@ -500,7 +517,10 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
     CK(cudaStreamWaitEvent(s, ex[k], 0));
     egs::k_relabel_targets<<<grid_for((uint64_t)(rows[k + 1] - rows[k]) * 4, sms), 256, 0, s>>>(
         n, rows[k], rows[k + 1], off64, dst, c->perm, c->off, c->edge, c->tbits, ck0, cv0,
-        misc + 16);
+        misc + 16, lt.list + (size_t)k * lt.cap, lt.cnt + k);
+    egs::k_relabel_targets_long<<<2 * sms, 256, 0, s>>>(
+        n, lt.list + (size_t)k * lt.cap, lt.cnt + k, off64, dst, c->perm, c->off, c->edge,
+        c->tbits, ck0, cv0, misc + 16);
     CK(cudaGetLastError());
     CK(cudaEventRecord(et[k], s));
   }
@@ -518,11 +538,11 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   {
     const int64_t mw = a->max_abs_weight;
     if (mw <= 127)
-      h_stage_bad = upload_weights<int8_t>(c, a, rows, ew, et, off64, wn);
+      h_stage_bad = upload_weights<int8_t>(c, a, rows, ew, et, off64, wn, lw);
     else if (mw <= 32767)
-      h_stage_bad = upload_weights<int16_t>(c, a, rows, ew, et, off64, wn);
+      h_stage_bad = upload_weights<int16_t>(c, a, rows, ew, et, off64, wn, lw);
     else
-      h_stage_bad = upload_weights<int32_t>(c, a, rows, ew, et, off64, wn);
+      h_stage_bad = upload_weights<int32_t>(c, a, rows, ew, et, off64, wn, lw);
   }
   tm.mark("upload + relabel + CSC sort");
   CK(cudaEventRecord(e_tail, sw));
@@ -542,6 +562,7 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   d_ck1.release();
   d_tmp.release();
   d_misc.release();
+  d_long.release();
   CK(cudaStreamSynchronize(s));
   tm.mark("weights + join");
   for (auto e : ex) cudaEventDestroy(e);
