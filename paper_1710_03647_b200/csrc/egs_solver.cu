@@ -349,38 +349,54 @@ bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint3
   std::lock_guard<std::mutex> lk(g_stage_mu);
   W* stage = static_cast<W*>(pinned_stage(m * sizeof(W)));
   W* wd = static_cast<W*>(wdev);
+  // Blocks of kBlk edges, claimed in order from one counter by the worker
+  // threads and by this thread between its DMA issues, so a descheduled
+  // thread (the host may have no spare core) delays one block, not a chunk.
   const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-  const int T = m >= (1u << 20) ? (int)hw : 1;
-  std::vector<std::atomic<int>> done(nch);
-  for (auto& d : done) d.store(0);
-  std::atomic<bool> out_of_range{false};
-  const int64_t* w = a->csr_weights;
+  const int T = m >= (1u << 20) ? (int)hw - 1 : 0;  // helpers besides this thread
+  constexpr uint64_t kBlk = 1u << 18;
   auto span_of = [&](int k) {
     return std::make_pair(a->csr_offsets[rows[k]], a->csr_offsets[rows[k + 1]]);
   };
-  auto work = [&](int t) {
+  std::vector<uint64_t> bfirst(nch + 1, 0);  // first block of each chunk
+  for (int k = 0; k < nch; ++k) {
+    const auto [e0, e1] = span_of(k);
+    bfirst[k + 1] = bfirst[k] + (e1 - e0 + kBlk - 1) / kBlk;
+  }
+  const uint64_t nblk = bfirst[nch];
+  std::vector<std::atomic<uint64_t>> left(nch);  // blocks of the chunk not yet converted
+  for (int k = 0; k < nch; ++k) left[k].store(bfirst[k + 1] - bfirst[k]);
+  std::atomic<uint64_t> next{0};
+  std::atomic<bool> out_of_range{false};
+  const int64_t* w = a->csr_weights;
+  // convert one claimed block; false when none is left
+  auto one_block = [&](int& k) {
+    const uint64_t b = next.fetch_add(1, std::memory_order_relaxed);
+    if (b >= nblk) return false;
+    while (b >= bfirst[k + 1]) ++k;
+    const auto [e0, e1] = span_of(k);
+    const uint64_t lo = e0 + (b - bfirst[k]) * kBlk, hi = std::min(e1, lo + kBlk);
     bool bad = false;
-    for (int k = 0; k < nch; ++k) {
-      const auto [e0, e1] = span_of(k);
-      const uint64_t lo = e0 + (e1 - e0) * t / T, hi = e0 + (e1 - e0) * (t + 1) / T;
-      for (uint64_t i = lo; i < hi; ++i) {
-        const int64_t x = w[i];
-        bad |= x < -wmax || x > wmax;
-        stage[i] = (W)x;
-      }
-      done[k].fetch_add(1, std::memory_order_release);
+    for (uint64_t i = lo; i < hi; ++i) {
+      const int64_t x = w[i];
+      bad |= x < -wmax || x > wmax;
+      stage[i] = (W)x;
     }
-    if (bad) out_of_range.store(true);
+    if (bad) out_of_range.store(true, std::memory_order_relaxed);
+    left[k].fetch_sub(1, std::memory_order_release);
+    return true;
+  };
+  auto work = [&]() {
+    int k = 0;
+    while (one_block(k)) {
+    }
   };
   std::vector<std::thread> pool;
-  for (int t = 1; t < T; ++t) pool.emplace_back(work, t);
-  std::thread self_worker;
-  if (T == 1)
-    work(0);
-  else
-    self_worker = std::thread(work, 0);
+  for (int t = 0; t < T; ++t) pool.emplace_back(work);
+  int kself = 0;
   for (int k = 0; k < nch; ++k) {
-    while (done[k].load(std::memory_order_acquire) < T) std::this_thread::yield();
+    while (left[k].load(std::memory_order_acquire) > 0)
+      if (!one_block(kself)) std::this_thread::yield();
     const auto [e0, e1] = span_of(k);
     CK(cudaMemcpyAsync(wd + e0, stage + e0, (e1 - e0) * sizeof(W), cudaMemcpyHostToDevice, sc));
     CK(cudaEventRecord(ew[k], sc));
@@ -395,7 +411,6 @@ bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint3
         lw.list + (size_t)k * lw.cap, lw.cnt + k, off64, wd, c->perm, c->off, c->edge, c->tbits);
     CK(cudaGetLastError());
   }
-  if (self_worker.joinable()) self_worker.join();
   for (auto& th : pool) th.join();
   // the staging buffer is re-used by the next upload: wait for its DMA
   CK(cudaStreamSynchronize(sc));
