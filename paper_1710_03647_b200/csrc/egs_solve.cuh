@@ -1108,6 +1108,18 @@ __device__ __forceinline__ bool good_edge(const SolveParams<V>& p, int64_t fv, i
 #ifndef EGS_CERT_CHUNK
 #define EGS_CERT_CHUNK 4
 #endif
+#ifndef EGS_DENSE_COMMIT_DIV
+#define EGS_DENSE_COMMIT_DIV 8
+#endif
+// a commit loads all staged slots when at least n / kDenseCommitDiv were raised
+// (0: never)
+constexpr uint64_t kDenseCommitDiv = EGS_DENSE_COMMIT_DIV;
+#ifndef EGS_PACKED_WITNESS_KEY
+#define EGS_PACKED_WITNESS_KEY 1
+#endif
+// round 1's player-0 witness as one packed min per edge (4-byte records with
+// tbits >= 5, so |w| < 2^26: round1_light)
+constexpr bool kPackedWitnessKey = EGS_PACKED_WITNESS_KEY != 0 && EGS_EDGE_BYTES == 4;
 constexpr int kCertChunk = EGS_CERT_CHUNK;  // edges tested per step (early exit between)
 #ifndef EGS_CERT_CHUNK_P0
 #define EGS_CERT_CHUNK_P0 8
@@ -1223,6 +1235,23 @@ __device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo0,
   auto row = [&](uint32_t v, const ERec* rec, uint32_t len, uint32_t, V) {
     const bool p0 = v < g.rb[kP1L];  // uniform over a tile's working lanes
     const uint32_t rot = row_rot(len);
+    if (p0 && kPackedWitnessKey && g.tbits >= 5) {
+      // packed records with |w| < 2^26 (tbits >= 5): the key and the index
+      // of a light row (< 32) in one word, so the argmin is one min per
+      // edge, and the least key's max(0, -w) is max(0, -max w), the value
+      uint32_t kb = 0xFFFFFFFFu;
+      for (uint32_t k0 = 0; k0 < len; k0 += kChunk) {
+#pragma unroll
+        for (int k = 0; k < kChunk; ++k) {
+          uint32_t j = min(k0 + k, len - 1) + rot;
+          j = j >= len ? j - len : j;
+          const int2 r = dec(g, rec[j]);
+          kb = min(kb, ((uint32_t)max(0, -r.y) << 6) |
+                           ((uint32_t)((uint32_t)r.x >= g.rb[kP1L]) << 5) | j);
+        }
+      }
+      return finish(v, true, INT32_MAX, -(int)(kb >> 6), rec[kb & 31u], len);
+    }
     int minw = INT32_MAX, maxw = INT32_MIN;
     uint32_t jbest = 0, kbest = 0xFFFFFFFFu;
     for (uint32_t k0 = 0; k0 < len; k0 += kChunk) {
@@ -1478,8 +1507,31 @@ __device__ __noinline__ void phase_lift(const SolveParams<V>& p, bool dense, Fro
 // `chg`) takes its staged value.  Lifts of the round all read the measure
 // of the previous round, exactly the synchronous rounds of solve_frontier /
 // solve_sweep (solver_par.cpp:205-228, 389-417).
+// The staged values of a commit step: only those of raised vertices (their
+// chg bit first), or -- when many vertices were raised (`dense`) -- every
+// slot at once, independent of the bitmap words so both loads are in flight
+// together; the caller reads val[k] only where the bit is set.
+template <class V, int U>
+__device__ __forceinline__ void commit_stage_loads(const SolveParams<V>& p, bool dense,
+                                                   uint32_t w0, uint32_t whi, uint32_t lane,
+                                                   const uint32_t (&bits)[U], V (&val)[U],
+                                                   V other) {
+  if (dense) {
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      val[k] = w0 + k < whi ? ldcg(p.stage + ((w0 + k) << 5) + lane) : other;
+  } else {
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const uint32_t v = ((w0 + k) << 5) + lane;
+      val[k] = ((bits[k] >> lane) & 1u) ? ldcg(p.stage + v) : other;
+    }
+  }
+}
+
 template <class V>
-__device__ __noinline__ void phase_commit(const SolveParams<V>& p, const uint32_t* chg) {
+__device__ __noinline__ void phase_commit(const SolveParams<V>& p, const uint32_t* chg,
+                                          bool dense = false) {
   constexpr int U = 8;  // words per warp step, all loads issued before any store
   const uint32_t n = p.g.n;
   const uint32_t nwords = (n + 31) >> 5;
@@ -1492,11 +1544,7 @@ __device__ __noinline__ void phase_commit(const SolveParams<V>& p, const uint32_
     V val[U];
 #pragma unroll
     for (int k = 0; k < U; ++k) bits[k] = w0 + k < whi ? ldcg(chg + w0 + k) : 0u;
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const uint32_t v = ((w0 + k) << 5) + lane;
-      val[k] = ((bits[k] >> lane) & 1u) ? ldcg(p.stage + v) : V(0);
-    }
+    commit_stage_loads<V, U>(p, dense, w0, whi, lane, bits, val, V(0));
 #pragma unroll
     for (int k = 0; k < U; ++k)
       if ((bits[k] >> lane) & 1u) stcg(p.f + ((w0 + k) << 5) + lane, val[k]);
@@ -1535,7 +1583,8 @@ __device__ __noinline__ void phase_cert_init(const SolveParams<V>& p, const uint
 // instead of two): a raised vertex publishes its staged value and, unless it
 // reached top, becomes a candidate (bit + mark).
 template <class V>
-__device__ __noinline__ void phase_commit_cert_init(const SolveParams<V>& p, const uint32_t* chg) {
+__device__ __noinline__ void phase_commit_cert_init(const SolveParams<V>& p, const uint32_t* chg,
+                                                    bool dense = false) {
   constexpr V TOP = Top<V>::v;
   constexpr int U = 8;  // words per warp step, all loads issued before any store
   const uint32_t nwords = (p.g.n + 31) >> 5;
@@ -1549,11 +1598,7 @@ __device__ __noinline__ void phase_commit_cert_init(const SolveParams<V>& p, con
     V val[U];
 #pragma unroll
     for (int k = 0; k < U; ++k) bits[k] = w0 + k < whi ? ldcg(chg + w0 + k) : 0u;
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const uint32_t v = ((w0 + k) << 5) + lane;
-      val[k] = ((bits[k] >> lane) & 1u) ? ldcg(p.stage + v) : TOP;
-    }
+    commit_stage_loads<V, U>(p, dense, w0, whi, lane, bits, val, TOP);
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       if (w0 + k >= whi) break;
@@ -1982,10 +2027,12 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
         !(p.mode == kModeAuto && (double)changed * p.avg_in_deg * p.sparse_div >= (double)n);
     if (!inplace) {  // a Jacobi round: publish its staged values
       begin_phase();
+      // (a commit of many raises loads every staged slot with its bitmap word)
+      const bool dense_commit = (uint64_t)changed * kDenseCommitDiv >= n;
       if (cert_now) {
-        phase_commit_cert_init<V>(p, chg);  // commit + certificate step 1
+        phase_commit_cert_init<V>(p, chg, dense_commit);  // commit + certificate step 1
       } else {
-        phase_commit<V>(p, chg);
+        phase_commit<V>(p, chg, dense_commit);
         if (fuse_act)
           phase_activate<V>(p, chg, frontier(tok + 1), p.frb[tok & 1], sh->fr_cnt[(tok + 2) % 3],
                             slot_sum(), slot_dyn() + 2);
