@@ -1519,7 +1519,7 @@ __device__ __forceinline__ void commit_stage_loads(const SolveParams<V>& p, bool
   if (dense) {
 #pragma unroll
     for (int k = 0; k < U; ++k)
-      val[k] = w0 + k < whi ? ldcg(p.stage + ((w0 + k) << 5) + lane) : other;
+      val[k] = ((w0 + k) << 5) + lane < p.g.n ? ldcg(p.stage + ((w0 + k) << 5) + lane) : other;
   } else {
 #pragma unroll
     for (int k = 0; k < U; ++k) {

@@ -677,6 +677,9 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     c->fr[0] = dalloc<uint32_t>(n);
     c->fr[1] = dalloc<uint32_t>(n);
     c->stage = dalloc<uint8_t>((size_t)std::max<uint32_t>(c->n_pad, 1) * vsz);
+    // dense commits read every slot of a bitmap word (egs_solve.cuh
+    // commit_stage_loads): slots never staged are read, and must be defined
+    CK(cudaMemsetAsync(c->stage, 0, (size_t)std::max<uint32_t>(c->n_pad, 1) * vsz, c->stream));
     c->f64 = dalloc<int64_t>(n);
     if (world > 1) {
       const size_t ew = c->vbits / 32;  // u64 words per entry
