@@ -677,6 +677,29 @@ __device__ __forceinline__ uint32_t row_rot(uint32_t len) {
   return (((lane_id() % G) * len) / G) % len;
 }
 
+// f(j) for every record j of a light row, in the rotated order.  A
+// power-of-two row of at least kChunk records takes j = k ^ rot instead of
+// (k + rot) mod len: the same banks (rot < len spreads the lanes that share a
+// start bank), one op per record instead of a clamp and a wrap.  Rows
+// shorter than a chunk repeat their last record (idempotent for min / max).
+template <class F>
+__device__ __forceinline__ void row_edges(uint32_t len, uint32_t rot, F&& f) {
+  if ((len & (len - 1)) == 0 && len >= (uint32_t)kChunk) {
+    for (uint32_t k0 = 0; k0 < len; k0 += kChunk) {
+#pragma unroll
+      for (int k = 0; k < kChunk; ++k) f((k0 + k) ^ rot);
+    }
+  } else {
+    for (uint32_t k0 = 0; k0 < len; k0 += kChunk) {
+#pragma unroll
+      for (int k = 0; k < kChunk; ++k) {
+        uint32_t j = min(k0 + k, len - 1) + rot;
+        f(j >= len ? j - len : j);
+      }
+    }
+  }
+}
+
 // Player-1 light rows of a dense round through the tile pipeline: tiles of
 // all-top vertices are skipped without a copy; each lane lifts its own row
 // from shared memory (reads rotated by lane so a half-warp hits distinct
@@ -1120,6 +1143,10 @@ constexpr uint64_t kDenseCommitDiv = EGS_DENSE_COMMIT_DIV;
 // round 1's player-0 witness as one packed min per edge (4-byte records with
 // tbits >= 5, so |w| < 2^26: round1_light)
 constexpr bool kPackedWitnessKey = EGS_PACKED_WITNESS_KEY != 0 && EGS_EDGE_BYTES == 4;
+#ifndef EGS_ROUND1_ROW_EDGES
+#define EGS_ROUND1_ROW_EDGES 1
+#endif
+constexpr bool kRound1RowEdges = EGS_ROUND1_ROW_EDGES != 0;  // round 1 P1 rows via row_edges
 constexpr int kCertChunk = EGS_CERT_CHUNK;  // edges tested per step (early exit between)
 #ifndef EGS_CERT_CHUNK_P0
 #define EGS_CERT_CHUNK_P0 8
@@ -1240,17 +1267,17 @@ __device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo0,
       // of a light row (< 32) in one word, so the argmin is one min per
       // edge, and the least key's max(0, -w) is max(0, -max w), the value
       uint32_t kb = 0xFFFFFFFFu;
-      for (uint32_t k0 = 0; k0 < len; k0 += kChunk) {
-#pragma unroll
-        for (int k = 0; k < kChunk; ++k) {
-          uint32_t j = min(k0 + k, len - 1) + rot;
-          j = j >= len ? j - len : j;
-          const int2 r = dec(g, rec[j]);
-          kb = min(kb, ((uint32_t)max(0, -r.y) << 6) |
-                           ((uint32_t)((uint32_t)r.x >= g.rb[kP1L]) << 5) | j);
-        }
-      }
+      const uint32_t b1 = g.rb[kP1L];
+      row_edges(len, rot, [&](uint32_t j) {
+        const int2 r = dec(g, rec[j]);
+        kb = min(kb, ((uint32_t)max(0, -r.y) << 6) | ((uint32_t)((uint32_t)r.x >= b1) << 5) | j);
+      });
       return finish(v, true, INT32_MAX, -(int)(kb >> 6), rec[kb & 31u], len);
+    }
+    if (!p0 && kRound1RowEdges) {  // player 1: the least weight, in any order
+      int mn = INT32_MAX;
+      row_edges(len, rot, [&](uint32_t j) { mn = min(mn, rec_w(g, rec[j])); });
+      return finish(v, false, mn, INT32_MIN, rec[0], len);
     }
     int minw = INT32_MAX, maxw = INT32_MIN;
     uint32_t jbest = 0, kbest = 0xFFFFFFFFu;
