@@ -157,6 +157,43 @@ __device__ __forceinline__ void warp_append(bool pred, uint32_t val,
 // lane) into a flat stream: fn(item_index, owning_lane) is called once per
 // item, 32 items per step, so one long segment (an R-MAT hub column) is
 // shared by the whole warp instead of serialising one lane.  Warp-uniform.
+// warp_expand with U items per lane per step (lane l takes items base + l,
+// base + 32 + l, ...): fn(valid[U], idx[U]) can issue the loads of all U
+// before it uses any.
+template <int U, class Fn>
+__device__ __forceinline__ void warp_expand_n(uint32_t b, uint32_t e, Fn&& fn) {
+  const uint32_t lane = lane_id();
+  const uint32_t len = e - b;
+  uint32_t incl = len;
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, s);
+    if (lane >= (uint32_t)s) incl += y;
+  }
+  const uint32_t excl = incl - len;
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  for (uint32_t base = 0; base < total; base += 32 * U) {
+    bool valid[U];
+    uint32_t idx[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t k = base + 32 * u + lane;
+      uint32_t lo = 0;
+#pragma unroll
+      for (uint32_t step = 16; step > 0; step >>= 1) {
+        const uint32_t c = lo + step;
+        const uint32_t ex = __shfl_sync(0xffffffffu, excl, c & 31u);
+        if (c < 32u && ex <= k) lo = c;
+      }
+      const uint32_t sb = __shfl_sync(0xffffffffu, b, lo);
+      const uint32_t sx = __shfl_sync(0xffffffffu, excl, lo);
+      valid[u] = k < total;
+      idx[u] = sb + (k - sx);
+    }
+    fn(valid, idx);
+  }
+}
+
 template <class Fn>
 __device__ __forceinline__ void warp_expand(uint32_t b, uint32_t e, Fn&& fn) {
   const uint32_t lane = lane_id();

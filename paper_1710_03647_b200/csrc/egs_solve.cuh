@@ -940,6 +940,67 @@ __device__ __forceinline__ void activate_pred(const SolveParams<V>& p, bool vali
     L.phase_count += add;
 }
 
+// activate_pred for U predecessor slots per lane: the source loads, then the
+// membership tests (top / candidate gathers and dedup words), then the
+// dedup atomics of all U are issued before any result is used.
+#ifndef EGS_ACT_UNROLL
+#define EGS_ACT_UNROLL 2
+#endif
+constexpr int kActUnroll = EGS_ACT_UNROLL;
+
+template <class V, int U>
+__device__ __forceinline__ void activate_preds(const SolveParams<V>& p, const bool (&valid)[U],
+                                               const uint32_t (&idx)[U], WarpLists& q,
+                                               const Frontier& t, Local& L, bool pushing,
+                                               bool cert) {
+  const Graph& g = p.g;
+  uint32_t u[U], fr[U];
+  bool want[U], add[U];
+#pragma unroll
+  for (int k = 0; k < U; ++k) u[k] = valid[k] ? __ldg(g.csrc + idx[k]) : 0u;
+#pragma unroll
+  for (int k = 0; k < U; ++k) {
+    want[k] = false;
+    fr[k] = ~0u;
+    if (valid[k]) {
+      want[k] = cert ? owned(p, u[k]) && ((ldcg(p.cand + (u[k] >> 5)) >> (u[k] & 31u)) & 1u)
+                     : gather(p.f + u[k]) != Top<V>::v;
+      fr[k] = ldcg(t.frb + (u[k] >> 5));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < U; ++k) {
+    const uint32_t bit = 1u << (u[k] & 31u);
+    add[k] = valid[k] && want[k] && !(fr[k] & bit) && !(atomicOr(t.frb + (u[k] >> 5), bit) & bit);
+  }
+#pragma unroll
+  for (int k = 0; k < U; ++k) {
+    if (valid[k] && !cert) ++L.act;
+    lists_append(q, add[k], add[k] ? size_class(g, u[k]) : 0, u[k], t.list, t.cnt);
+    if (pushing)
+      L.pushed += add[k];
+    else
+      L.phase_count += add[k];
+  }
+}
+
+// the predecessors of CSC range [b, e) of each lane, expanded by the warp
+template <class V>
+__device__ __forceinline__ void expand_preds(const SolveParams<V>& p, uint32_t b, uint32_t e,
+                                             WarpLists& q, const Frontier& t, Local& L,
+                                             bool pushing, bool cert) {
+  if (kActUnroll > 1) {
+    warp_expand_n<kActUnroll>(b, e, [&](const bool(&valid)[kActUnroll],
+                                        const uint32_t(&idx)[kActUnroll]) {
+      activate_preds<V, kActUnroll>(p, valid, idx, q, t, L, pushing, cert);
+    });
+  } else {
+    warp_expand(b, e, [&](bool valid, uint32_t idx, uint32_t) {
+      activate_pred<V>(p, valid, idx, q, t, L, pushing, cert);
+    });
+  }
+}
+
 // Certificate passes push the candidate predecessors of each removed vertex
 // into the next pass's re-check queue `t` (dedup bitmap t.frb).  Warp-uniform.
 template <class V>
@@ -951,9 +1012,7 @@ __device__ __forceinline__ void push_cert_preds(const SolveParams<V>& p, bool re
     b = __ldg(p.g.coff + v);
     e = __ldg(p.g.coff + v + 1);
   }
-  warp_expand(b, e, [&](bool valid, uint32_t idx, uint32_t) {
-    activate_pred<V>(p, valid, idx, q, t, L, true, true);
-  });
+  expand_preds<V>(p, b, e, q, t, L, true, true);
 }
 
 // Push activation of a sparse round: the predecessors of the vertices of the
@@ -976,9 +1035,7 @@ __device__ __forceinline__ void push_preds(const SolveParams<V>& p, bool raised,
       e = b;
     }
   }
-  warp_expand(b, e, [&](bool valid, uint32_t idx, uint32_t) {
-    activate_pred<V>(p, valid, idx, q, t, L, true);
-  });
+  expand_preds<V>(p, b, e, q, t, L, true, false);
 }
 
 // Light rows of a sparse frontier list, one thread each, lifted in place;
@@ -1931,9 +1988,7 @@ __device__ __noinline__ void phase_activate(const SolveParams<V>& p, const uint3
           e = b;
         }
       }
-      warp_expand(b, e, [&](bool valid, uint32_t idx, uint32_t) {
-        activate_pred<V>(p, valid, idx, q, t, L);
-      });
+      expand_preds<V>(p, b, e, q, t, L, false, false);
     }
   }
   for (int c = 0; c < 3; ++c) lists_flush(q, c, t.list[c], t.cnt + c);

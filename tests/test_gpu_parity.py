@@ -3,6 +3,8 @@
 Every case goes through the C-ABI (egs_gpu_solve / egs_ctx_*) and is compared
 bit-for-bit with the reference's least progress measure and byte-for-byte
 with its write_solution text."""
+import hashlib
+
 import numpy as np
 import pytest
 
@@ -177,6 +179,34 @@ def test_rmat16_golden(egs, golden):
     rep = _solve(egs, a)
     sol = egs.write_solution(a, rep).encode()
     assert f"{fnv1a64(sol):016x}" == golden[key]["solution_fnv"]
+
+
+GOLDEN_FULL = [
+    ("fixed/1000000/8/1000/1", (1_000_000, 8, 1000)),      # C2
+    ("fixed/1000000/8/100000/1", (1_000_000, 8, 100_000)),  # C5
+]
+
+
+@pytest.mark.parametrize("key,args", GOLDEN_FULL, ids=["C2", "C5"])
+def test_full_size_golden(egs, golden, key, args):
+    """BASELINE configs C2 and C5 at full size, bit-exact against the reference
+    solve_sweep run to its fixpoint (tests/golden/make_golden_full.py): the
+    solution bytes of the device output path and of the host formatter."""
+    if key not in golden:
+        pytest.skip("full-size golden vector not generated")
+    rec = golden[key]
+    a = egs.GameArena.fixed(*args, 1)
+    with egs.DeviceSolver(a) as ds:
+        ds.solve()
+        dev_text = ds.write_solution().encode()
+        f = ds.read_measure()
+    host_text = egs.write_solution(a, f).encode()
+    assert len(dev_text) == rec["solution_bytes"]
+    assert hashlib.sha256(dev_text).hexdigest() == rec["solution_sha256"]
+    assert host_text == dev_text
+    top = f == np.iinfo(np.int64).max
+    assert int(top.sum()) == rec["tops"]
+    assert int(f[~top].sum()) == rec["sum_finite"]
 
 
 @pytest.mark.parametrize("tma_mask", ["0", "7"])
