@@ -757,7 +757,10 @@ __device__ __noinline__ void dense_light_p1(const SolveParams<V>& p, uint32_t lo
 // witness is violated are compacted into a per-warp shared-memory queue and
 // re-lifted 32 at a time, one row per lane, so a few violated rows never
 // serialise a warp.
-constexpr int kP0Unroll = 4;
+#ifndef EGS_P0_UNROLL
+#define EGS_P0_UNROLL 2
+#endif
+constexpr int kP0Unroll = EGS_P0_UNROLL;
 
 template <class V>
 __device__ __noinline__ void dense_light_p0(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
