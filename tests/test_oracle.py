@@ -110,3 +110,16 @@ def test_oracle_slow_climb_gadget(oracle, reflib):
     fr, _, _ = reflib.solve(a, reflib.SEQ)
     assert np.array_equal(f, fr)
     assert (f[f != INT64_MAX] > 40).any()  # the climb reaches the exit cost
+
+
+@pytest.mark.parametrize("key", ["fixed/1000000/8/1000/1", "fixed/1000000/8/100000/1"])
+def test_full_size_golden_is_this_generator(oracle, golden, key):
+    """The full-size C2/C5 golden records (tests/golden/make_golden_full.py,
+    the reference run to its fixpoint) describe the canonical generator's
+    arena: same size and credit_cap as the oracle's restatement builds."""
+    if key not in golden:
+        pytest.skip("full-size golden vectors not generated")
+    rec = golden[key]
+    g = _gen(oracle, key)
+    assert (g.n, g.m, int(g.a.credit_cap)) == (rec["n"], rec["m"], rec["credit_cap"])
+    assert rec["solution_bytes"] > 0 and len(rec["solution_sha256"]) == 64
