@@ -76,11 +76,22 @@ typedef struct egs_gpu_opts {
   int32_t no_tma;          /* 1: stage no edge spans through TMA (A/B and
                               debugging); the result is identical */
   int32_t mode;            /* EGS_MODE_* */
-  int32_t debug_checks;    /* SolverOptions::debug_checks: monotonicity and
-                              fixpoint verification on the device */
+  int32_t debug_checks;    /* SolverOptions::debug_checks (solver_par.cpp:168,179):
+                              every commit checks on the device that the value
+                              it publishes is above the old one (the
+                              reference's check_monotone), and the result is
+                              checked to be a fixpoint of the capped lift;
+                              either failure returns EGS_ERR_INTERNAL */
   double timeout_seconds;  /* SolverOptions::timeout_seconds; 0 disables */
-  uint64_t round_bound;    /* SolverOptions::sweep_bound; 0 = default budget
-                              |E|*(cap+1)+1 (solver_par.cpp:94-98) */
+  uint64_t round_bound;    /* SolverOptions::sweep_bound (solver.hpp:37), used
+                              when has_round_bound != 0 -- including 0, which,
+                              as in the reference (solver_par.cpp:149-150,
+                              184-188), fails after the first round that
+                              raises something */
+  int32_t has_round_bound; /* 0: default budget |E|*(cap+1)+1
+                              (solver_par.cpp:94-98), or round_bound if it is
+                              nonzero (callers predating the flag) */
+  int32_t reserved_opts;
 } egs_gpu_opts;
 
 /* SolveReport counters (solver.hpp:47-59) plus device timings.  The whole

@@ -25,15 +25,32 @@ egs_arena_view view_of(const GameArena& a) {
   return v;
 }
 
+// The reference's validate_options (solver_par.cpp:41-51): the same
+// InvalidConfigError for the same options, although neither the worker count
+// nor the mapping changes what the device computes (results are identical
+// for every mapping, SPEC.md acceptance criterion 9).
+void validate_like_reference(const SolverOptions& o) {
+  if (o.workers < 1 || o.workers > 1024)
+    throw InvalidConfigError("worker count must be in [1, 1024]");
+  if (o.mapping.kind == Mapping::Kind::kChunked) {
+    const uint32_t h = o.mapping.chunk;
+    if (h == 0 || h > 64 || (h & (h - 1)) != 0)
+      throw InvalidConfigError("chunk size must be a power of two in [1, 64]");
+  }
+}
+
 egs_gpu_opts opts_of(const SolverOptions& o, const GpuOptions& g) {
   egs_gpu_opts c;
   egs_gpu_opts_default(&c);
-  c.n_gpus = o.workers;
+  // SolverOptions::workers counts CPU threads in the reference; this entry
+  // point drives one GPU whatever it says (multi-GPU: egs_part_*)
+  c.n_gpus = 1;
   c.device = g.device;
   c.certify = g.certify ? 1 : 0;
   c.mode = g.mode;
   c.debug_checks = o.debug_checks ? 1 : 0;
   c.timeout_seconds = o.timeout_seconds;
+  c.has_round_bound = o.sweep_bound.has_value() ? 1 : 0;
   c.round_bound = o.sweep_bound.value_or(0);
   return c;
 }
@@ -55,6 +72,7 @@ egs_gpu_opts opts_of(const SolverOptions& o, const GpuOptions& g) {
 SolveReport solve_gpu(const GameArena& arena, const SolverOptions& options,
                       const GpuOptions& gpu, egs_gpu_stats* stats) {
   const auto start = std::chrono::steady_clock::now();
+  validate_like_reference(options);
   const egs_arena_view v = view_of(arena);
   const egs_gpu_opts o = opts_of(options, gpu);
   std::vector<int64_t> raw(arena.num_vertices());
@@ -71,6 +89,7 @@ SolveReport solve_gpu(const GameArena& arena, const SolverOptions& options,
   report.rounds = st.rounds;
   report.variant = kGpuVariant;
   report.workers = options.workers;
+  report.mapping = options.mapping;
   report.wall_seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
   return report;

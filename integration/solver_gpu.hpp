@@ -27,9 +27,11 @@ struct GpuOptions {
   int mode = EGS_MODE_AUTO;
 };
 
-// SolverOptions::workers counts GPUs (1 here; multi-GPU goes through
-// paper_1710_03647_b200.distributed).  sweep_bound, timeout_seconds and
-// debug_checks keep their meaning.
+// SolverOptions::workers (CPU threads in the reference) is reported back but
+// does not select GPUs: this entry point drives one GPU (multi-GPU goes
+// through egs_part_*, paper_1710_03647_b200.distributed).  sweep_bound
+// (including an explicit 0), timeout_seconds and debug_checks keep their
+// meaning.
 SolveReport solve_gpu(const GameArena& arena, const SolverOptions& options = {},
                       const GpuOptions& gpu = {}, egs_gpu_stats* stats = nullptr);
 

@@ -98,6 +98,8 @@ class GpuOpts(C.Structure):
         ("debug_checks", C.c_int32),
         ("timeout_seconds", C.c_double),
         ("round_bound", C.c_uint64),
+        ("has_round_bound", C.c_int32),
+        ("reserved_opts", C.c_int32),
     ]
 
 
@@ -354,6 +356,9 @@ class SolverOptions:
         o.mode = _MODES[self.mode]
         o.debug_checks = int(bool(self.debug_checks))
         o.timeout_seconds = float(self.timeout_seconds)
+        # sweep_bound keeps the reference's optional semantics: None = default
+        # budget, 0 = fail after the first round that raises something
+        o.has_round_bound = int(self.sweep_bound is not None)
         o.round_bound = int(self.sweep_bound or 0)
         return o
 

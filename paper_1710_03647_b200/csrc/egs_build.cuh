@@ -220,6 +220,17 @@ __global__ void k_export(uint32_t n, const V* f, const uint32_t* perm, int64_t* 
   }
 }
 
+// out[v] = widen(f[v]) in relabelled ids (the debug_checks fixpoint test of
+// a solve's own result).
+template <class V>
+__global__ void k_widen(uint32_t n, const V* f, int64_t* out) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += gridDim.x * blockDim.x) {
+    const V x = f[v];
+    out[v] = x == Top<V>::v ? INT64_MAX : static_cast<int64_t>(x);
+  }
+}
+
 // fnew[perm[old]] = fin[old] (int64, raw encoding) for the verifier.
 __global__ void k_import(uint32_t n, const int64_t* fin, const uint32_t* perm,
                          int64_t* fnew) {

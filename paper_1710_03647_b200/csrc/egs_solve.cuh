@@ -1616,6 +1616,20 @@ __device__ __forceinline__ void commit_stage_loads(const SolveParams<V>& p, bool
   }
 }
 
+// debug_checks (the reference's check_monotone, solver_par.cpp:116-124,179):
+// a value a commit publishes must be above the one it replaces
+template <class V, int U>
+__device__ __noinline__ void debug_check_raise(const SolveParams<V>& p, uint32_t w0,
+                                               uint32_t lane, const uint32_t (&bits)[U],
+                                               const V (&val)[U]) {
+#pragma unroll
+  for (int k = 0; k < U; ++k)
+    if ((bits[k] >> lane) & 1u) {
+      const V old = ldcg(p.f + ((w0 + k) << 5) + lane);
+      if (!(val[k] > old)) atomicOr(&p.sh->bad, 1u);
+    }
+}
+
 template <class V>
 __device__ __noinline__ void phase_commit(const SolveParams<V>& p, const uint32_t* chg,
                                           bool dense = false) {
@@ -1632,6 +1646,7 @@ __device__ __noinline__ void phase_commit(const SolveParams<V>& p, const uint32_
 #pragma unroll
     for (int k = 0; k < U; ++k) bits[k] = w0 + k < whi ? ldcg(chg + w0 + k) : 0u;
     commit_stage_loads<V, U>(p, dense, w0, whi, lane, bits, val, V(0));
+    if (p.debug) debug_check_raise<V, U>(p, w0, lane, bits, val);
 #pragma unroll
     for (int k = 0; k < U; ++k)
       if ((bits[k] >> lane) & 1u) stcg(p.f + ((w0 + k) << 5) + lane, val[k]);
@@ -1686,6 +1701,7 @@ __device__ __noinline__ void phase_commit_cert_init(const SolveParams<V>& p, con
 #pragma unroll
     for (int k = 0; k < U; ++k) bits[k] = w0 + k < whi ? ldcg(chg + w0 + k) : 0u;
     commit_stage_loads<V, U>(p, dense, w0, whi, lane, bits, val, TOP);
+    if (p.debug) debug_check_raise<V, U>(p, w0, lane, bits, val);
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       if (w0 + k >= whi) break;

@@ -345,7 +345,11 @@ bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint3
   cudaStream_t sc = c->copy_stream, sw = c->aux_stream;
   const int nch = (int)rows.size() - 1;
   const uint64_t m = c->m;
-  const int64_t wmax = std::numeric_limits<W>::max();
+  // a packed record holds the weight in its top 32 - tbits bits (signed):
+  // reject what does not fit there too, whatever max_abs_weight claimed
+  const int64_t wmax =
+      c->tbits ? std::min<int64_t>(std::numeric_limits<W>::max(), (1ll << (31 - c->tbits)) - 1)
+               : (int64_t)std::numeric_limits<W>::max();
   std::lock_guard<std::mutex> lk(g_stage_mu);
   W* stage = static_cast<W*>(pinned_stage(m * sizeof(W)));
   W* wd = static_cast<W*>(wdev);
@@ -392,6 +396,18 @@ bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint3
     }
   };
   std::vector<std::thread> pool;
+  // The helpers read this frame's locals: on any error (a CK throw) stop
+  // them by exhausting the block counter and join them before unwinding.
+  struct Joiner {
+    std::vector<std::thread>& pool;
+    std::atomic<uint64_t>& next;
+    uint64_t nblk;
+    ~Joiner() {
+      next.store(nblk, std::memory_order_relaxed);
+      for (auto& th : pool)
+        if (th.joinable()) th.join();
+    }
+  } joiner{pool, next, nblk};
   for (int t = 0; t < T; ++t) pool.emplace_back(work);
   int kself = 0;
   for (int k = 0; k < nch; ++k) {
@@ -808,7 +824,7 @@ egs::SolveParams<V> make_params(egs_ctx* c, unsigned long long* budget_out) {
   if (p.avg_in_deg < 1.0f) p.avg_in_deg = 1.0f;
   // default budget |E|*(cap+1)+1 (solver_par.cpp:94-98), saturating
   unsigned long long budget = o.round_bound;
-  if (!budget) {
+  if (!o.has_round_bound && !budget) {
     const unsigned long long per = (unsigned long long)c->cap + 1ull;
     budget = (c->m && per > ~0ull / c->m) ? ~0ull : c->m * per + 1ull;
   }
@@ -816,6 +832,7 @@ egs::SolveParams<V> make_params(egs_ctx* c, unsigned long long* budget_out) {
   p.timeout_ns = o.timeout_seconds > 0 ? (unsigned long long)(o.timeout_seconds * 1e9) : 0ull;
   p.own_lo = c->world == 1 ? 0 : c->own_lo;
   p.own_hi = c->world == 1 ? n : c->own_hi;
+  p.debug = o.debug_checks ? 1 : 0;
   if (budget_out) *budget_out = budget;
   return p;
 }
@@ -874,6 +891,33 @@ void fill_stats(egs_ctx* c, const unsigned long long* h, double ms, egs_gpu_stat
   st->edge_bytes = (uint32_t)rec_bytes(c);
 }
 
+// debug_checks after a solve: no commit published a value that did not rise
+// (the device flag Scratch::bad, the reference's check_monotone), and the
+// result is a fixpoint of the capped lift (k_fixpoint); InternalInvariantError
+// otherwise (solver_par.cpp:116-124).
+template <class V>
+void debug_verify(egs_ctx* c) {
+  cudaStream_t s = c->stream;
+  g_alloc_stream = s;
+  DevBuf d_misc;
+  unsigned long long* misc = d_misc.alloc<unsigned long long>(1);
+  CK(cudaMemsetAsync(misc, 0, sizeof(unsigned long long), s));
+  egs::k_widen<V><<<grid_for(c->n, c->num_sms), 256, 0, s>>>(c->n, static_cast<const V*>(c->f),
+                                                              c->f64);
+  egs::k_fixpoint<<<grid_for((uint64_t)c->n * 32, c->num_sms), 256, 0, s>>>(c->graph(), c->f64,
+                                                                            misc);
+  CK(cudaGetLastError());
+  unsigned long long h[2] = {0, 0};
+  unsigned int bad = 0;
+  CK(cudaMemcpyAsync(&h[0], misc, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&bad, &c->scratch->bad, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (bad) throw Fail(EGS_ERR_INTERNAL, "measure decreased across a round");
+  if (h[0])
+    throw Fail(EGS_ERR_INTERNAL,
+               std::to_string(h[0]) + " vertices are not a fixpoint of the lift after the solve");
+}
+
 template <class V>
 void run_solve(egs_ctx* c, egs_gpu_stats* st) {
   cudaStream_t s = c->stream;
@@ -922,6 +966,7 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
   if (h[egs::kStatus] == 5)
     throw Fail(EGS_ERR_BOUND, "round budget of " + std::to_string(budget) +
                                   " exhausted before reaching a fixpoint");
+  if (p.debug) debug_verify<V>(c);
 }
 
 void ctx_solve(egs_ctx* c, egs_gpu_stats* st) {

@@ -78,6 +78,7 @@ struct Scratch {
                              // 2.. activation / certificate queues, 7 TMA tiles
   unsigned int fr_cnt[3][3]; // frontier sublist sizes [token % 3][L, M, H]
   unsigned int stop;         // timeout flag
+  unsigned int bad;          // debug_checks: a commit that did not raise its vertex
 };
 
 template <class V>
@@ -108,6 +109,7 @@ struct SolveParams {
   unsigned long long* trace;   // optional: per-phase (kind << 56 | ns) log, kTraceCap entries
   unsigned long long round_budget;
   unsigned long long timeout_ns;   // 0 = none; measured from kernel start
+  int debug;                // SolverOptions::debug_checks: commits check monotonicity
 };
 
 

@@ -151,6 +151,50 @@ int main() {
       thrown = true;
     }
     CHECK(thrown, "InvalidConfigError");
+    // an explicit sweep_bound of 0 fails after the first raising round, as
+    // in the reference (solver_par.cpp:149-150,184-188)
+    SolverOptions zero;
+    zero.sweep_bound = 0;
+    thrown = false;
+    try {
+      solve(a, Variant::kSweep, zero);
+    } catch (const BoundExhaustedError&) {
+      thrown = true;
+    }
+    CHECK(thrown, "reference: sweep_bound = 0 -> BoundExhaustedError");
+    thrown = false;
+    try {
+      solve_gpu(a, zero);
+    } catch (const BoundExhaustedError&) {
+      thrown = true;
+    }
+    CHECK(thrown, "gpu: sweep_bound = 0 -> BoundExhaustedError");
+    // ... and an arena already at its fixpoint passes with sweep_bound = 0
+    const GameArena calm = fixed(100, 2, 0, 1);
+    CHECK(solve_gpu(calm, zero).measure.raw() == solve(calm, Variant::kSweep, zero).measure.raw(),
+          "sweep_bound = 0 on a fixpoint");
+    SolverOptions badmap;
+    badmap.mapping = Mapping{Mapping::Kind::kChunked, 3};
+    thrown = false;
+    try {
+      solve_gpu(a, badmap);
+    } catch (const InvalidConfigError&) {
+      thrown = true;
+    }
+    CHECK(thrown, "chunk 3 -> InvalidConfigError");
+  }
+  // The reference's usual options (workers = thread count, a chunked
+  // mapping, debug checks) are accepted by the GPU entry point unchanged.
+  {
+    const GameArena a = fixed(10000, 8, 1000, 2);
+    SolverOptions ro;
+    ro.workers = 16;
+    ro.mapping = Mapping{Mapping::Kind::kChunked, 8};
+    ro.debug_checks = true;
+    const SolveReport want = solve(a, Variant::kSweep, ro);
+    const SolveReport got = solve_gpu(a, ro);
+    CHECK(got.measure.raw() == want.measure.raw(), "workers = 16, chunked(8), debug_checks");
+    CHECK(got.workers == 16 && got.mapping.kind == Mapping::Kind::kChunked, "report echoes options");
   }
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
   return g_fail ? 1 : 0;

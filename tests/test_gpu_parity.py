@@ -288,6 +288,29 @@ def test_round_bound_and_timeout(egs):
         assert ds.is_fixpoint(ds.read_measure())
 
 
+def test_sweep_bound_zero_and_debug_checks(egs, oracle):
+    """sweep_bound keeps the reference's optional semantics (solver_par.cpp:
+    149-150,184-188): 0 fails after the first round that raises something and
+    passes an arena already at its fixpoint.  debug_checks (the reference's
+    check_monotone plus a fixpoint check of the result) passes on every
+    schedule and changes nothing."""
+    a = egs.GameArena.fixed(10000, 4, 100, 1)
+    with pytest.raises(egs.BoundExhaustedError):
+        _solve(egs, a, sweep_bound=0)
+    calm = egs.GameArena.build(4, [(0, 1, 3), (1, 2, 0), (2, 3, 5), (3, 0, 1)], [0, 1, 0, 1])
+    assert _solve(egs, calm, sweep_bound=0).measure.tolist() == [0, 0, 0, 0]
+    for seed in range(40):
+        n, edges, owners = random_arena(7000 + seed, max_n=40, max_deg=6)
+        b = egs.GameArena.build(n, edges, owners)
+        want, _ = oracle.solve_seq(oracle.build(n, edges, owners))
+        for mode in MODES:
+            for certify in (True, False):
+                rep = _solve(egs, b, mode=mode, certify=certify, debug_checks=True)
+                assert np.array_equal(rep.measure, want), (seed, mode, certify)
+    base = _solve(egs, a).measure
+    assert np.array_equal(_solve(egs, a, debug_checks=True).measure, base)
+
+
 def test_weight_width_paths(egs, oracle):
     """Weights travel as int8 / int16 / int32 by max |w|; every width gives
     the reference's measure, and a weight beyond int32 is refused loudly."""
