@@ -121,8 +121,11 @@ typedef struct egs_gpu_stats {
   double lift_seconds;
   double cert_seconds;
   double activate_seconds;
-  uint64_t algo_bytes;     /* algorithmic bytes of the whole solve */
-  uint64_t lift_bytes;     /* of which the lift phases */
+  uint64_t algo_bytes;     /* algorithmic bytes of the whole solve, SURVEY.md
+                              §8(d)'s per-unit figures extended to the phases
+                              it does not name */
+  uint64_t lift_bytes;     /* of which the lift phases, edge records counted
+                              at their stored size (4 packed / 8 wide) */
   uint64_t kernel_launches;/* device kernels launched by the solve */
   uint32_t value_bits;     /* 32 or 64: device value width chosen */
   uint32_t grid_ctas;      /* CTAs of the persistent solve kernel */
@@ -133,6 +136,9 @@ typedef struct egs_gpu_stats {
                                      init, dense passes, sparse passes, apply */
   uint32_t edge_bytes;     /* 4 (packed dst | w << target bits) or 8 ({dst, w}) */
   uint32_t reserved0;
+  uint64_t algo_bytes_s8d; /* SURVEY.md §8(d) exactly: edges_relaxed * (8 + s)
+                              + applications * (4 + 2 s) + activations * 4,
+                              s = value bytes */
 } egs_gpu_stats;
 
 void egs_gpu_opts_default(egs_gpu_opts* opts);

@@ -122,14 +122,16 @@ __device__ __forceinline__ uint32_t vload(const volatile unsigned int* p) { retu
 
 // Per-CTA time spent in the sub-phases of a lift phase (thread 0 of each
 // CTA adds its own wall time; divide by the grid size for a per-CTA mean).
+// Only under EGS_TRACE (p.trace set): off the solve path otherwise.
 struct SubTimer {
   unsigned long long* ctr;
   unsigned long long t;
-  __device__ explicit SubTimer(unsigned long long* c) : ctr(c), t(0) {
-    if (threadIdx.x == 0) t = globaltimer();
+  bool on;
+  __device__ SubTimer(unsigned long long* c, bool enabled) : ctr(c), t(0), on(enabled) {
+    if (on && threadIdx.x == 0) t = globaltimer();
   }
   __device__ void lap(int k) {
-    if (threadIdx.x == 0) {
+    if (on && threadIdx.x == 0) {
       const unsigned long long now = globaltimer();
       atomicAdd(ctr + k, now - t);
       t = now;
@@ -138,9 +140,7 @@ struct SubTimer {
 };
 
 // Per-thread event counts of the current phase (u32: one phase touches every
-// row / edge at most once, so a block's sum stays below 2^32).  Flushed into
-// the u64 device counters at every phase end, so they are not live across
-// phases.
+// row / edge at most once, so a warp's sum stays below 2^32).
 struct Local {
   unsigned int lifts = 0, apps = 0, edges = 0, witness = 0, act = 0, certified = 0,
                pops = 0, cert_scanned = 0, cert_edges = 0, visits = 0;
@@ -149,35 +149,69 @@ struct Local {
 };
 constexpr int kLocalCounters = 10;
 
-// Block-wide flush of the phase's counters: one atomicAdd per CTA and
-// counter; phase_count goes to the grid-shared slot `dst`.  Block-uniform.
-__device__ __forceinline__ void block_flush(Local& L, unsigned long long* ctr,
-                                            unsigned int* dst, unsigned int* s_cnt,
+// Counters never cross a grid barrier on their own.  A warp reduces its
+// lanes' counts (REDUX) and lane 0 adds them to per-CTA shared accumulators
+// -- no __syncthreads, no global atomics inside a phase:
+//   g_stats   the SolveReport statistics, added to p.ctr once per CTA at
+//             kernel exit (stats_exit);
+//   g_psum    the phase sums the control flow reads (changed / removed /
+//             frontier sizes), one per Scratch::sum slot of the current
+//             phase, added to it by end_phase_flush right before the grid
+//             barrier (one global atomic per CTA and nonzero slot).
+// g_slot_base is the current phase's Scratch::sum row; every warp writes it
+// (the same value) before its first flush of the phase, so a read after a
+// warp's own write is always the current phase's row.
+__shared__ unsigned long long g_stats[kLocalCounters];
+__shared__ unsigned int g_psum[4];
+__shared__ unsigned int* g_slot_base;
+
+__device__ __forceinline__ void set_phase_slot(unsigned int* slot) {
+  if (lane_id() == 0) g_slot_base = slot;
+  __syncwarp();
+}
+
+__device__ __forceinline__ void stats_init() {
+  if (threadIdx.x < (unsigned)kLocalCounters) g_stats[threadIdx.x] = 0ull;
+  if (threadIdx.x < 4u) g_psum[threadIdx.x] = 0u;
+  __syncthreads();
+}
+
+__device__ __forceinline__ void stats_exit(unsigned long long* ctr) {
+  __syncthreads();
+  if (threadIdx.x < (unsigned)kLocalCounters && g_stats[threadIdx.x])
+    atomicAdd(ctr + threadIdx.x, g_stats[threadIdx.x]);
+}
+
+// Block-wide, before the grid barrier that ends a phase.
+__device__ __forceinline__ void end_phase_flush() {
+  __syncthreads();
+  if (threadIdx.x < 4u) {
+    const unsigned int v = g_psum[threadIdx.x];
+    if (v) {
+      atomicAdd(g_slot_base + threadIdx.x, v);
+      g_psum[threadIdx.x] = 0u;
+    }
+  }
+}
+
+// Warp-wide flush of the phase's counters: phase_count goes to the phase sum
+// slot `dst`, pushed to `dst2` (both in the current phase's Scratch::sum
+// row).  Warp-uniform; every lane of the warp calls it.
+__device__ __forceinline__ void block_flush(Local& L, unsigned int* dst,
                                             unsigned int* dst2 = nullptr) {
   constexpr int K = kLocalCounters + 2;  // + phase_count, pushed
   unsigned int v[K] = {L.lifts, L.apps,      L.edges,        L.witness,
                        L.act,   L.certified, L.pops,         L.cert_scanned,
                        L.cert_edges, L.visits, L.phase_count, L.pushed};
-  const uint32_t warp = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < K; ++k) v[k] = __reduce_add_sync(0xffffffffu, v[k]);
-  __syncthreads();
   if (lane_id() == 0) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) s_cnt[warp * K + k] = v[k];
-  }
-  __syncthreads();
-  if (threadIdx.x < (unsigned)K) {
-    unsigned long long sum = 0;
-    for (int w = 0; w < kWarps; ++w) sum += s_cnt[w * K + threadIdx.x];
-    if (sum) {
-      if (threadIdx.x < (unsigned)kLocalCounters)
-        atomicAdd(ctr + threadIdx.x, sum);
-      else if (threadIdx.x == (unsigned)kLocalCounters)
-        atomicAdd(dst, (unsigned int)sum);
-      else if (dst2)
-        atomicAdd(dst2, (unsigned int)sum);
-    }
+    for (int k = 0; k < kLocalCounters; ++k)
+      if (v[k]) atomicAdd(&g_stats[k], (unsigned long long)v[k]);
+    if (v[kLocalCounters]) atomicAdd(&g_psum[dst - g_slot_base], v[kLocalCounters]);
+    if (v[kLocalCounters + 1] && dst2)
+      atomicAdd(&g_psum[dst2 - g_slot_base], v[kLocalCounters + 1]);
   }
   L = Local();
 }
@@ -709,7 +743,6 @@ __device__ __noinline__ void dense_light_p1(const SolveParams<V>& p, uint32_t lo
                                             unsigned int* cursor, uint32_t* chg,
                                             unsigned int* sum_dst) {
   constexpr V TOP = Top<V>::v;
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   Local L;
   auto load = [&](uint32_t v, V& old) { old = ldcg(p.f + v); };
   auto test = [&](uint32_t, V old) { return old != TOP; };
@@ -747,7 +780,7 @@ __device__ __noinline__ void dense_light_p1(const SolveParams<V>& p, uint32_t lo
   auto fallback = [&](uint32_t v, V) { return lift_thread<V, false>(p, v, L); };
   tma_tiles<V>(p, (p.use_tma & kTmaLift) != 0, lo, hi, 0u, 0u, cursor, nullptr, chg, L, load,
                test, row, fallback);
-  block_flush(L, p.ctr, sum_dst, s_cnt);
+  block_flush(L, sum_dst);
 }
 
 // Player-0 light rows of a dense round.  Almost every player-0 lift is
@@ -767,7 +800,6 @@ __device__ __noinline__ void dense_light_p0(const SolveParams<V>& p, uint32_t lo
                                             uint32_t* chg, unsigned int* sum_dst) {
   constexpr V TOP = Top<V>::v;
   constexpr int U = kP0Unroll;
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   __shared__ uint32_t s_q[kWarps][32 * U + 32];
   Local L;
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
@@ -827,7 +859,7 @@ __device__ __noinline__ void dense_light_p0(const SolveParams<V>& p, uint32_t lo
     drain(31);  // keep fewer than a warp's worth queued
   }
   drain(0);
-  block_flush(L, p.ctr, sum_dst, s_cnt);
+  block_flush(L, sum_dst);
 }
 
 // Activation (solver_par.cpp:402-410): every non-top predecessor of a vertex
@@ -1048,7 +1080,6 @@ __device__ __noinline__ void sparse_light(const SolveParams<V>& p, const uint32_
                                           uint32_t count, uint32_t* chg,
                                           unsigned int* sum_dst, Frontier nxt,
                                           unsigned int* qlong, unsigned int* act_dst) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   Local L;
   WarpLists q = warp_lists();
   const uint32_t nthreads = gridDim.x * kBlock;
@@ -1069,7 +1100,7 @@ __device__ __noinline__ void sparse_light(const SolveParams<V>& p, const uint32_
     push_preds<V>(p, ch, v, q, nxt, qlong, L);
   }
   for (int c = 0; c < 3; ++c) lists_flush(q, c, nxt.list[c], nxt.cnt + c);
-  block_flush(L, p.ctr, sum_dst, s_cnt, act_dst);
+  block_flush(L, sum_dst, act_dst);
 }
 
 // Medium rows: warps claim rows from a per-phase cursor.  `items(i)` maps a
@@ -1083,7 +1114,6 @@ __device__ __noinline__ void warp_rows(const SolveParams<V>& p, uint32_t count,
                                           bool push = false, Frontier nxt = Frontier{},
                                           unsigned int* qlong = nullptr,
                                           unsigned int* act_dst = nullptr) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   Local L;
   WarpLists q = warp_lists();
   WarpClaim wc;
@@ -1105,7 +1135,7 @@ __device__ __noinline__ void warp_rows(const SolveParams<V>& p, uint32_t count,
   }
   if (push)
     for (int c = 0; c < 3; ++c) lists_flush(q, c, nxt.list[c], nxt.cnt + c);
-  block_flush(L, p.ctr, sum_dst, s_cnt, act_dst);
+  block_flush(L, sum_dst, act_dst);
 }
 
 template <class V, class Items>
@@ -1116,7 +1146,6 @@ __device__ __noinline__ void block_rows(const SolveParams<V>& p, uint32_t count,
                                            unsigned int* qlong = nullptr,
                                            unsigned int* act_dst = nullptr) {
   __shared__ BlockScratch<V> s;
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   Local L;
   WarpLists q = warp_lists();
   for (;;) {
@@ -1143,7 +1172,7 @@ __device__ __noinline__ void block_rows(const SolveParams<V>& p, uint32_t count,
   __syncthreads();
   if (push && threadIdx.x < 32)
     for (int c = 0; c < 3; ++c) lists_flush(q, c, nxt.list[c], nxt.cnt + c);
-  block_flush(L, p.ctr, sum_dst, s_cnt, act_dst);
+  block_flush(L, sum_dst, act_dst);
 }
 
 // ======================================================= certificate ====
@@ -1298,7 +1327,6 @@ template <class V>
 __device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo0, uint32_t hi0,
                                           uint32_t lo1, uint32_t hi1, unsigned int* cursor,
                                           uint32_t* chg, unsigned int* sum_dst) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   const Graph& g = p.g;
   Local L;
   auto load = [](uint32_t, V&) {};
@@ -1389,14 +1417,13 @@ __device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo0,
   };
   tma_tiles<V>(p, (p.use_tma & kTmaRound1) != 0, lo0, hi0, lo1, hi1, cursor, nullptr, chg, L,
                load, test, row, fallback);
-  block_flush(L, p.ctr, sum_dst, s_cnt);
+  block_flush(L, sum_dst);
 }
 
 // medium rows: one warp per row; heavy rows: one CTA per row (dynamic claims)
 template <class V>
 __device__ __noinline__ void round1_long(const SolveParams<V>& p, uint32_t* chg,
                                          unsigned int* sum_dst, unsigned int* slot_dyn) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   __shared__ int s_min[kWarps], s_max[kWarps];
   __shared__ uint32_t s_imax[kWarps];
   __shared__ unsigned int s_item;
@@ -1508,7 +1535,7 @@ __device__ __noinline__ void round1_long(const SolveParams<V>& p, uint32_t* chg,
       }
     }
   }
-  block_flush(L, p.ctr, sum_dst, s_cnt);
+  block_flush(L, sum_dst);
 }
 
 template <class V>
@@ -1532,7 +1559,6 @@ __device__ __noinline__ void phase_lift(const SolveParams<V>& p, bool dense, Fro
                                         Frontier nxt, unsigned int* cnt_after,
                                         uint32_t* chg, uint32_t* other,
                                         unsigned int* slot_sum, unsigned int* slot_dyn) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   const Graph& g = p.g;
   const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
   const uint32_t nthreads = gridDim.x * kBlock;
@@ -1547,7 +1573,7 @@ __device__ __noinline__ void phase_lift(const SolveParams<V>& p, bool dense, Fro
     }
   }
   if (dense) {
-    SubTimer st(p.ctr);
+    SubTimer st(p.ctr, p.trace != nullptr);
     block_rows<V>(p, class_size(g, 2), slot_dyn + 1,
                   [gp = &g](uint32_t i) { return class_item(*gp, 2, i); }, chg, sum_dst);
     st.lap(kSubHeavy);
@@ -1569,7 +1595,7 @@ __device__ __noinline__ void phase_lift(const SolveParams<V>& p, bool dense, Fro
     const uint32_t* lH = cur.list[2];
     unsigned int* act_dst = slot_sum + 2;
     unsigned int* qlong = slot_dyn + 2;
-    SubTimer st(p.ctr);
+    SubTimer st(p.ctr, p.trace != nullptr);
     block_rows<V>(p, cH, slot_dyn + 1, [=](uint32_t i) { return ldcg(lH + i); }, chg, sum_dst,
                   true, nxt, qlong, act_dst);
     st.lap(kSubHeavy);
@@ -1587,7 +1613,7 @@ __device__ __noinline__ void phase_lift(const SolveParams<V>& p, bool dense, Fro
     }
     if (tid == 0) L.pops += cL + cM + cH;
   }
-  block_flush(L, p.ctr, sum_dst, s_cnt);
+  block_flush(L, sum_dst);
 }
 
 // Commit of a Jacobi round: every vertex raised in the round (marked in
@@ -1660,7 +1686,6 @@ __device__ __noinline__ void phase_commit(const SolveParams<V>& p, const uint32_
 template <class V>
 __device__ __noinline__ void phase_cert_init(const SolveParams<V>& p, const uint32_t* chg,
                                              unsigned int* slot_sum) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
   const uint32_t nthreads = gridDim.x * kBlock;
   const uint32_t nwarps = gridDim.x * kWarps;
@@ -1678,7 +1703,7 @@ __device__ __noinline__ void phase_cert_init(const SolveParams<V>& p, const uint
     const uint32_t m = __ballot_sync(0xffffffffu, c);
     if (lane == 0) stcg(p.cand + w, m);
   }
-  block_flush(L, p.ctr, slot_sum + 1, s_cnt);
+  block_flush(L, slot_sum + 1);
 }
 
 // Commit fused with certificate step 1 (one pass over the words of `chg`
@@ -1791,7 +1816,6 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
                                               unsigned int* slot_dyn, uint32_t* rbm,
                                               uint32_t* rbm_clear, Frontier qt = Frontier{},
                                               uint32_t* qclear = nullptr) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   const Graph& g = p.g;
   const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
   const uint32_t nthreads = gridDim.x * kBlock;
@@ -1863,7 +1887,7 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
   }
   if (qt.cnt)
     for (int c = 0; c < 3; ++c) lists_flush(q, c, qt.list[c], qt.cnt + c);
-  block_flush(L, p.ctr, slot_sum + 1, s_cnt);
+  block_flush(L, slot_sum + 1);
 }
 
 // After a dense pass (which does not push: its removals are many, and the
@@ -1873,7 +1897,6 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
 template <class V>
 __device__ __noinline__ void phase_cert_mark(const SolveParams<V>& p, const uint32_t* rbm_in,
                                              Frontier t, unsigned int* slot_sum) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   const uint32_t nwords = (p.g.n + 31) >> 5;
   const uint32_t nwarps = gridDim.x * kWarps;
   const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5;
@@ -1894,7 +1917,7 @@ __device__ __noinline__ void phase_cert_mark(const SolveParams<V>& p, const uint
     }
   }
   for (int c = 0; c < 3; ++c) lists_flush(q, c, t.list[c], t.cnt + c);
-  block_flush(L, p.ctr, slot_sum + 2, s_cnt);
+  block_flush(L, slot_sum + 2);
 }
 
 // Sparse pass: re-check the queued candidates -- the candidate predecessors
@@ -1907,7 +1930,6 @@ __device__ __noinline__ void phase_cert_check(const SolveParams<V>& p, Frontier 
                                               const unsigned int* qcnt, unsigned int* slot_sum,
                                               unsigned int* slot_dyn, uint32_t* rbm,
                                               uint32_t* rbm_clear, Frontier nxt) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
   const uint32_t nthreads = gridDim.x * kBlock;
   const uint32_t nwords = (p.g.n + 31) >> 5;
@@ -1942,7 +1964,7 @@ __device__ __noinline__ void phase_cert_check(const SolveParams<V>& p, Frontier 
     const uint32_t v = i < cL ? ldcg(lL + i) : i < cL + cM ? ldcg(lM + (i - cL)) : ldcg(lH + (i - cL - cM));
     atomicAnd(cur.frb + (v >> 5), ~(1u << (v & 31u)));
   }
-  block_flush(L, p.ctr, slot_sum + 1, s_cnt);
+  block_flush(L, slot_sum + 1);
 }
 
 // Certificate, step 3: certified vertices jump to top and count as changed
@@ -1950,7 +1972,6 @@ __device__ __noinline__ void phase_cert_check(const SolveParams<V>& p, Frontier 
 template <class V>
 __device__ __noinline__ void phase_cert_apply(const SolveParams<V>& p, uint32_t* chg,
                                               unsigned int* slot_sum) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   const uint32_t nwarps = gridDim.x * kWarps;
   const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5;
   const uint32_t lane = lane_id();
@@ -1970,7 +1991,7 @@ __device__ __noinline__ void phase_cert_apply(const SolveParams<V>& p, uint32_t*
       L.certified += hit;
     }
   }
-  block_flush(L, p.ctr, slot_sum + 0, s_cnt);
+  block_flush(L, slot_sum + 0);
 }
 
 template <class V>
@@ -1978,7 +1999,6 @@ __device__ __noinline__ void phase_activate(const SolveParams<V>& p, const uint3
                                             Frontier t, uint32_t* frb_other,
                                             unsigned int* cnt_next, unsigned int* slot_sum,
                                             unsigned int* qlong) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   const Graph& g = p.g;
   const uint32_t nwords = (g.n + 31) >> 5;
   const uint32_t nwarps = gridDim.x * kWarps;
@@ -2011,7 +2031,7 @@ __device__ __noinline__ void phase_activate(const SolveParams<V>& p, const uint3
     }
   }
   for (int c = 0; c < 3; ++c) lists_flush(q, c, t.list[c], t.cnt + c);
-  block_flush(L, p.ctr, slot_sum + 2, s_cnt);
+  block_flush(L, slot_sum + 2);
 }
 
 // The long columns queued by phase_activate: every warp walks the queue and
@@ -2019,7 +2039,6 @@ __device__ __noinline__ void phase_activate(const SolveParams<V>& p, const uint3
 template <class V>
 __device__ __noinline__ void phase_activate_long(const SolveParams<V>& p, Frontier t,
                                                  uint32_t ncols, unsigned int* slot_sum) {
-  __shared__ unsigned int s_cnt[kWarps * (kLocalCounters + 2)];
   const Graph& g = p.g;
   Local L;
   WarpLists q = warp_lists();
@@ -2039,7 +2058,7 @@ __device__ __noinline__ void phase_activate_long(const SolveParams<V>& p, Fronti
     }
   }
   for (int c = 0; c < 3; ++c) lists_flush(q, c, t.list[c], t.cnt + c);
-  block_flush(L, p.ctr, slot_sum + 2, s_cnt);
+  block_flush(L, slot_sum + 2);
 }
 
 // ========================================================== the kernel ===
@@ -2069,8 +2088,10 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
         if (k < 4) sh->sum[(phase + 2) & 3][k] = 0;
         sh->dyn[(phase + 2) & 3][k] = 0;
       }
+    set_phase_slot(slot_sum());
   };
   auto end_phase = [&](int kind, int fine = -1) {
+    end_phase_flush();
     grid.sync();
     ++phase;
     if (leader) {
@@ -2084,6 +2105,7 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
   };
 
   tma_init_barriers();
+  stats_init();
 
   // ---- round 1: seeding + the first lift, from the weights alone
   begin_phase();
@@ -2273,6 +2295,7 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
     changed = prev_sum(0);
   }
 
+  stats_exit(p.ctr);
   if (leader) {
     p.ctr[kRounds] = round;
     p.ctr[kDenseRounds] = rounds_dense;
@@ -2301,8 +2324,10 @@ template <class V>
 __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
     k_part_step(const __grid_constant__ SolveParams<V> p, int step, int parity) {
   tma_init_barriers();
+  stats_init();
   unsigned int* sum = p.sh->sum[0];
   unsigned int* dyn = p.sh->dyn[0];
+  set_phase_slot(sum);
   uint32_t* cur = p.chg[parity & 1];
   uint32_t* other = p.chg[(parity & 1) ^ 1];
   switch (step) {
@@ -2316,6 +2341,8 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
     case kStepCertApply: phase_cert_apply<V>(p, cur, sum); break;
     default: break;
   }
+  end_phase_flush();
+  stats_exit(p.ctr);
 }
 
 }  // namespace EGS_FMT_NS

@@ -846,8 +846,10 @@ void fill_stats(egs_ctx* c, const unsigned long long* h, double ms, egs_gpu_stat
   const double sv = sizeof(V);
   // SURVEY §8(d)'s per-unit figure: an 8-byte {u32 dst, i32 w} record per
   // edge, whatever the stored format (packed arenas stream 4 bytes; the
-  // bench's `traffic` is the measured DRAM side)
+  // bench's `traffic` is the measured DRAM side).  The lift-phase figure
+  // counts records at their stored size instead (`erl`).
   const double er = 8.0;
+  const double erl = (double)rec_bytes(c);
   st->lifts = h[egs::kLifts];
   st->applications = h[egs::kApps];
   st->edges_relaxed = h[egs::kEdges];
@@ -872,16 +874,22 @@ void fill_stats(egs_ctx* c, const unsigned long long* h, double ms, egs_gpu_stat
   // round 1 (counted as one dense round: n visits, m edges) reads records
   // but neither f(v) nor f(t): drop those gathers from the lift formula
   const double r1 = (double)c->m * sv + (double)n * sv;
-  const double lift = (double)st->visits * sv + (double)st->witness_checks * (er + sv) +
-                      (double)st->applications * 8 + (double)st->edges_relaxed * (er + sv) +
-                      (double)st->lifts * sv - (st->rounds ? r1 : 0.0);
+  auto lift_with = [&](double rec) {
+    return (double)st->visits * sv + (double)st->witness_checks * (rec + sv) +
+           (double)st->applications * 8 + (double)st->edges_relaxed * (rec + sv) +
+           (double)st->lifts * sv - (st->rounds ? r1 : 0.0);
+  };
+  const double lift = lift_with(er);
   const double seed = 0.0;
   const double cert = (double)st->cert_attempts * n * (2 * (sv + 1)) +
                       (double)st->cert_rows * (1 + sv + 8) +
                       (double)st->cert_edges * (er + sv + 1);
   const double act = (double)st->activations * (4 + sv) + (double)st->sparse_rounds * words * 4;
-  st->lift_bytes = (uint64_t)lift;
+  st->lift_bytes = (uint64_t)lift_with(erl);
   st->algo_bytes = (uint64_t)(lift + seed + cert + act);
+  st->algo_bytes_s8d = (uint64_t)((double)st->edges_relaxed * (8.0 + sv) +
+                                  (double)st->applications * (4.0 + 2.0 * sv) +
+                                  (double)st->activations * 4.0);
   st->kernel_launches = 1;
   for (int k = 0; k < 5; ++k)
     st->lift_sub_seconds[k] = h[egs::kSubHeavy + k] * 1e-9 / (double)c->grid;

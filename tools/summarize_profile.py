@@ -1,6 +1,11 @@
 """Copy a gpu_bench_profile.sh run (gpurun_out/<tag>/) into profiles/:
 bench line, ncu summary of k_solve, DRAM traffic per launch, launch list,
-source hotspots.   usage: python tools/summarize_profile.py <tag>"""
+source hotspots.   usage: python tools/summarize_profile.py <tag> [round prefix, r02]
+
+profiles/lift_traffic.json is stamped with the SHA-256 of the library the
+capture ran (gpurun_out/<tag>/lib_sha256.txt, written by gpu_bench_profile.sh):
+bench.py reports it as `roofline.traffic` only while that library is the one
+it loads, so a stale capture is never paired with a newer kernel."""
 import csv
 import io
 import json
@@ -11,9 +16,10 @@ import sys
 from collections import defaultdict
 
 tag = sys.argv[1]
+RND = sys.argv[2] if len(sys.argv) > 2 else "r02"
 src = os.path.join("gpurun_out", tag)
 dst = "profiles"
-shutil.copy(os.path.join(src, "bench.json"), os.path.join(dst, f"r01_bench_{tag.split('_')[-1]}.json"))
+shutil.copy(os.path.join(src, "bench.json"), os.path.join(dst, f"{RND}_bench_{tag.split('_')[-1]}.json"))
 rep = os.path.join(src, "solve_c4.ncu-rep")
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
@@ -37,17 +43,20 @@ for i, k in enumerate(h):
 tot = sum(v for v, _ in vals) or 1
 out["stall_breakdown_pct"] = {k.replace("smsp__pcsamp_warps_issue_stalled_", ""): round(100 * v / tot, 1)
                               for v, k in sorted(vals, reverse=True)[:8]}
-json.dump(out, open(os.path.join(dst, f"r01_{tag.split('_')[-1]}_ncu_k_solve.json"), "w"), indent=1)
+json.dump(out, open(os.path.join(dst, f"{RND}_{tag.split('_')[-1]}_ncu_k_solve.json"), "w"), indent=1)
 scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}
 rd = float(out["dram__bytes_read.sum"][0].replace(",", "")) * scale[out["dram__bytes_read.sum"][1]]
 wr = float(out["dram__bytes_write.sum"][0].replace(",", "")) * scale[out["dram__bytes_write.sum"][1]]
+shafile = os.path.join(src, "lib_sha256.txt")
+lib_sha = open(shafile).read().split()[0] if os.path.exists(shafile) else None
 json.dump({"kernel": "k_solve", "bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+           "lib_sha256": lib_sha,
            "source": f"ncu --set full --clock-control none -k regex:k_solve -c 1 "
                      f"python tools/ncu_target.py C4 1 ({tag})"},
           open(os.path.join(dst, "lift_traffic.json"), "w"), indent=1)
 hot = subprocess.run([sys.executable, "tools/ncu_stalls.py", rep, "40"], capture_output=True,
                      text=True).stdout
-open(os.path.join(dst, f"r01_{tag.split('_')[-1]}_source_hotspots.txt"), "w").write(
+open(os.path.join(dst, f"{RND}_{tag.split('_')[-1]}_source_hotspots.txt"), "w").write(
     "# warp-stall samples per source line, top stall reasons (tools/ncu_stalls.py)\n" + hot)
 # C3 (R-MAT) capture: the same summary keys
 rep3 = os.path.join(src, "solve_c3.ncu-rep")
@@ -57,11 +66,11 @@ if os.path.exists(rep3):
     rows3 = list(csv.reader(io.StringIO(raw3)))
     h3, u3, r3 = rows3[0], rows3[1], rows3[2]
     json.dump({k: (r3[h3.index(k)], u3[h3.index(k)]) for k in keys if k in h3},
-              open(os.path.join(dst, f"r01_{tag.split('_')[-1]}_ncu_k_solve_c3.json"), "w"), indent=1)
+              open(os.path.join(dst, f"{RND}_{tag.split('_')[-1]}_ncu_k_solve_c3.json"), "w"), indent=1)
 for extra in ("bench_2rank_staged.json",):
     if os.path.exists(os.path.join(src, extra)) and os.path.getsize(os.path.join(src, extra)):
         shutil.copy(os.path.join(src, extra),
-                    os.path.join(dst, f"r01_{tag.split('_')[-1]}_{extra}"))
+                    os.path.join(dst, f"{RND}_{tag.split('_')[-1]}_{extra}"))
 lrows = list(csv.reader(open(os.path.join(src, "launches.csv"))))
 hdr = next(i for i, x in enumerate(lrows) if x and x[0] == "ID")
 hh, data = lrows[hdr], lrows[hdr + 1:]
@@ -72,7 +81,7 @@ for x in data:
     agg[nm][0] += 1
     agg[nm][1] += float(x[vi].replace(",", ""))
 t = sum(v[1] for v in agg.values())
-with open(os.path.join(dst, f"r01_{tag.split('_')[-1]}_launches.txt"), "w") as fh:
+with open(os.path.join(dst, f"{RND}_{tag.split('_')[-1]}_launches.txt"), "w") as fh:
     fh.write("# ncu --metrics gpu__time_duration.sum --clock-control none python tools/ncu_target.py C4 1\n")
     fh.write("# (context create = pipelined upload + device build, one solve, export); cold-cache, serialised\n")
     for k, v in sorted(agg.items(), key=lambda z: -z[1][1]):
