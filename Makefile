@@ -33,10 +33,13 @@ $(CSRC)/egs_kern_e8.o: $(CSRC)/egs_kern.cu $(CSRC)/egs_solve.cuh $(HDRS)
 $(CSRC)/egs_kern_e4.o: $(CSRC)/egs_kern.cu $(CSRC)/egs_solve.cuh $(HDRS)
 	$(NVCC) $(NVFLAGS) -DEGS_EDGE_BYTES=4 -DEGS_FMT_NS=e4 -c $< -o $@ 2> $(CSRC)/egs_kern_e4.ptxas.log || (cat $(CSRC)/egs_kern_e4.ptxas.log; false)
 
-$(CSRC)/egs_host.o: $(CSRC)/egs_host.cpp include/egs_gpu.h
+$(CSRC)/egs_host.o: $(CSRC)/egs_host.cpp $(CSRC)/egs_host_arena.h include/egs_gpu.h
 	$(CXX) -O3 -std=c++17 -fPIC -Iinclude -I/usr/local/cuda/include -c $< -o $@
 
-$(LIB): $(CSRC)/egs_solver.o $(CSRC)/egs_kern_e8.o $(CSRC)/egs_kern_e4.o $(CSRC)/egs_host.o
+$(CSRC)/egs_arena_io.o: $(CSRC)/egs_arena_io.cpp $(CSRC)/egs_host_arena.h include/egs_gpu.h
+	$(CXX) -O3 -std=c++17 -fPIC -Iinclude -c $< -o $@
+
+$(LIB): $(CSRC)/egs_solver.o $(CSRC)/egs_kern_e8.o $(CSRC)/egs_kern_e4.o $(CSRC)/egs_host.o $(CSRC)/egs_arena_io.o
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -lpthread
 
 $(ORACLE_LIB): oracle/egs_oracle.c oracle/egs_oracle.h

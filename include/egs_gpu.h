@@ -22,7 +22,9 @@
  *   EGS_ERR_TIMEOUT 2 (TimeoutError), EGS_ERR_UNSUPPORTED 3 (OverflowError:
  *   an arena outside the device representation), EGS_ERR_CUDA 4 (device or
  *   NCCL failure), EGS_ERR_BOUND 5 (BoundExhaustedError), EGS_ERR_INTERNAL 6
- *   (InternalInvariantError, debug checks).  egs_last_error() gives the text.
+ *   (InternalInvariantError, debug checks), EGS_ERR_INPUT 7 (the loader's
+ *   SyntaxError / CountMismatchError / DanglingVertexIdError /
+ *   NonTotalArenaError).  egs_last_error() gives the text.
  */
 #ifndef EGS_GPU_H
 #define EGS_GPU_H
@@ -41,6 +43,11 @@ extern "C" {
 #define EGS_ERR_CUDA 4
 #define EGS_ERR_BOUND 5
 #define EGS_ERR_INTERNAL 6
+#define EGS_ERR_INPUT 7    /* malformed arena input; egs_last_error() reads
+                              "<Kind>: <message>" with Kind one of the
+                              reference's loader errors (errors.hpp:16-46):
+                              SyntaxError ("line N: ..."), CountMismatchError,
+                              DanglingVertexIdError, NonTotalArenaError */
 
 /* Flattened GameArena (arena.hpp:37-133).  All pointers are HOST memory and
  * are only read during the call.  CSC spans are not needed: the predecessor
@@ -252,6 +259,30 @@ int egs_host_arena_rmat(uint32_t scale, uint32_t edge_factor, int64_t W,
                         uint64_t seed, int pinned, egs_host_arena** out);
 void egs_host_arena_view(const egs_host_arena* a, egs_arena_view* view);
 void egs_host_arena_free(egs_host_arena* a);
+
+/* ---------------------------------------------------------------------
+ * Arena input/output (csrc/egs_arena_io.cpp).  Each
+ * returns a host arena whose egs_host_arena_view feeds egs_gpu_solve /
+ * egs_ctx_create directly.
+ *
+ * GameArena::build(n, edges, owners) (arena.hpp:83-84, arena.cpp:17-78):
+ * edge i = (src[i], dst[i], weights[i]); rows keep input order. */
+int egs_host_arena_build(uint32_t num_vertices, uint64_t num_edges, const uint32_t* src,
+                         const uint32_t* dst, const int64_t* weights, const uint8_t* owners,
+                         int pinned, egs_host_arena** out);
+/* parse_arena(text) (io.hpp:19, io.cpp:87-149) + build, multi-threaded;
+ * the reference's records, checks and first error (EGS_ERR_INPUT). */
+int egs_arena_parse_text(const char* text, size_t len, int pinned, egs_host_arena** out);
+/* write_arena(arena) (io.cpp:151-176): text length; min(cap, length) bytes
+ * into buf when buf != NULL. */
+int64_t egs_arena_write_text(const egs_arena_view* arena, char* buf, size_t cap);
+/* Binary arena file: a 64-byte header (magic "EGSARNA1", version, weight
+ * width, n, m, credit_cap, max_abs_weight), then owners u8[n], csr_offsets
+ * u64[n+1], csr_targets u32[m], weights narrowed to int8/16/32/64 by max |w|,
+ * each span 8-byte aligned.  Loading validates the spans as build does and
+ * recomputes compute_stats against the header. */
+int egs_arena_save(const egs_arena_view* arena, const char* path);
+int egs_arena_load(const char* path, int pinned, egs_host_arena** out);
 
 /* Pinned host buffers for end-to-end timing. */
 void* egs_host_alloc_pinned(size_t bytes);

@@ -188,6 +188,28 @@ int64_t egsref_write_solution(void* a, const int64_t* f, char* buf,
   return rc ? -rc : len;
 }
 
+// parse_arena (io.hpp:19) of `text`: the arena, or nullptr with
+// egsref_last_error() = "<Kind>: <what()>" for the loader's error types.
+void* egsref_parse_arena(const char* text, size_t len) {
+  GameArena* out = nullptr;
+  try {
+    out = new GameArena(parse_arena(std::string_view(text, len)));
+  } catch (const SyntaxError& e) {
+    g_err = std::string("SyntaxError: ") + e.what();
+  } catch (const CountMismatchError& e) {
+    g_err = std::string("CountMismatchError: ") + e.what();
+  } catch (const DanglingVertexIdError& e) {
+    g_err = std::string("DanglingVertexIdError: ") + e.what();
+  } catch (const NonTotalArenaError& e) {
+    g_err = std::string("NonTotalArenaError: ") + e.what();
+  } catch (const OverflowError& e) {
+    g_err = std::string("OverflowError: ") + e.what();
+  } catch (const std::exception& e) {
+    g_err = std::string("Error: ") + e.what();
+  }
+  return out;
+}
+
 int64_t egsref_write_arena(void* a, char* buf, size_t cap) {
   std::string s = write_arena(*static_cast<GameArena*>(a));
   if (buf) std::memcpy(buf, s.data(), std::min(cap, s.size()));

@@ -21,16 +21,21 @@ from __future__ import annotations
 
 from ._native import (  # noqa: F401
     BoundExhaustedError,
+    CountMismatchError,
     CudaError,
+    DanglingVertexIdError,
     DeviceSolver,
     EgsolveError,
     GameArena,
+    InputError,
     InternalInvariantError,
     InvalidConfigError,
+    NonTotalArenaError,
     OverflowError_,
     PinnedBuffer,
     SolveReport,
     SolverOptions,
+    SyntaxError_,
     TimeoutError_,
     Variant,
     lib,

@@ -54,6 +54,26 @@ class InternalInvariantError(EgsolveError):
     """egsolve::InternalInvariantError (errors.hpp:83)."""
 
 
+class InputError(EgsolveError):
+    """Malformed arena input (EGS_ERR_INPUT): one of the loader errors below."""
+
+
+class SyntaxError_(InputError):
+    """egsolve::SyntaxError (errors.hpp:36): "line N: reason"."""
+
+
+class CountMismatchError(InputError):
+    """egsolve::CountMismatchError (errors.hpp:44)."""
+
+
+class DanglingVertexIdError(InputError):
+    """egsolve::DanglingVertexIdError (errors.hpp:24)."""
+
+
+class NonTotalArenaError(InputError):
+    """egsolve::NonTotalArenaError (errors.hpp:16)."""
+
+
 _ERRORS = {
     1: InvalidConfigError,
     2: TimeoutError_,
@@ -61,13 +81,22 @@ _ERRORS = {
     4: CudaError,
     5: BoundExhaustedError,
     6: InternalInvariantError,
+    7: InputError,
 }
+_INPUT_KINDS = {"SyntaxError": SyntaxError_, "CountMismatchError": CountMismatchError,
+                "DanglingVertexIdError": DanglingVertexIdError,
+                "NonTotalArenaError": NonTotalArenaError}
 
 
 def _check(rc: int) -> None:
     if rc != 0:
         msg = lib.egs_last_error().decode(errors="replace")
-        raise _ERRORS.get(rc, EgsolveError)(msg)
+        cls = _ERRORS.get(rc, EgsolveError)
+        if rc == 7:  # "<Kind>: <the reference's message>"
+            kind, _, rest = msg.partition(": ")
+            if kind in _INPUT_KINDS:
+                cls, msg = _INPUT_KINDS[kind], rest
+        raise cls(msg)
 
 
 # -------------------------------------------------------------- structs ----
@@ -188,6 +217,17 @@ lib.egs_host_arena_view.argtypes = [_P, C.POINTER(ArenaView)]
 lib.egs_host_arena_view.restype = None
 lib.egs_host_arena_free.argtypes = [_P]
 lib.egs_host_arena_free.restype = None
+lib.egs_host_arena_build.argtypes = [C.c_uint32, C.c_uint64, _P, _P, _P, _P, C.c_int,
+                                     C.POINTER(_P)]
+lib.egs_host_arena_build.restype = C.c_int
+lib.egs_arena_parse_text.argtypes = [C.c_char_p, C.c_size_t, C.c_int, C.POINTER(_P)]
+lib.egs_arena_parse_text.restype = C.c_int
+lib.egs_arena_write_text.argtypes = [C.POINTER(ArenaView), _P, C.c_size_t]
+lib.egs_arena_write_text.restype = C.c_int64
+lib.egs_arena_save.argtypes = [C.POINTER(ArenaView), C.c_char_p]
+lib.egs_arena_save.restype = C.c_int
+lib.egs_arena_load.argtypes = [C.c_char_p, C.c_int, C.POINTER(_P)]
+lib.egs_arena_load.restype = C.c_int
 lib.egs_host_alloc_pinned.argtypes = [C.c_size_t]
 lib.egs_host_alloc_pinned.restype = _P
 lib.egs_host_free_pinned.argtypes = [_P]
@@ -277,40 +317,59 @@ class GameArena:
 
     @classmethod
     def build(cls, num_vertices: int, edges, owners) -> "GameArena":
-        """``GameArena::build`` (arena.cpp:17-78): validation, stable CSR rows
-        in input order, ``compute_stats`` (arena.cpp:80-108) with its overflow
-        headroom.  ``edges`` is an iterable of (src, dst, weight)."""
+        """``GameArena::build`` (arena.cpp:17-78) through egs_host_arena_build:
+        validation, stable CSR rows in input order, ``compute_stats``
+        (arena.cpp:80-108) with its overflow headroom.  ``edges`` is an
+        iterable of (src, dst, weight)."""
         n = int(num_vertices)
         edges = [tuple(int(x) for x in e) for e in edges]
         own = np.asarray(owners, dtype=np.int64).reshape(-1)
         if own.shape[0] != n:
-            raise EgsolveError("owner list does not cover every vertex")
+            raise CountMismatchError("owner list does not cover every vertex")
         for s_, d_, w_ in edges:
-            if not (0 <= s_ < n) or not (0 <= d_ < n):
-                raise EgsolveError("edge references unknown vertex id")
+            for x in (s_, d_):
+                if not 0 <= x < n:
+                    raise DanglingVertexIdError(f"edge references unknown vertex id {x}")
             if not (-(2 ** 63) < w_ < 2 ** 63):
                 raise OverflowError_("edge weight magnitude not representable")
-        src = np.array([e[0] for e in edges], dtype=np.int64)
-        dst = np.array([e[1] for e in edges], dtype=np.int64)
-        w = np.array([e[2] for e in edges], dtype=np.int64)
-        counts = np.bincount(src, minlength=n) if n else np.zeros(0, np.int64)
-        if n and (counts == 0).any():
-            raise EgsolveError(f"vertex {int(np.argmax(counts == 0))} has no outgoing edge")
-        order = np.argsort(src, kind="stable")
-        off = np.zeros(n + 1, dtype=np.uint64)
-        off[1:] = np.cumsum(counts)
-        tgt = dst[order].astype(np.uint32)
-        wt = w[order]
-        cap = 0
-        maxw = 0
-        for v in range(n):
-            row = wt[int(off[v]):int(off[v + 1])]
-            worst = max(0, -int(row.min()))
-            maxw = max(maxw, int(np.abs(row).max()))
-            cap += worst
-        if cap > (2 ** 63 - 1) or cap > (2 ** 63 - 1) - maxw - 2:
-            raise OverflowError_("credit bound exceeds the representable range")
-        return cls(off, tgt, wt, (own != 0).astype(np.uint8), cap, maxw)
+        src = np.ascontiguousarray([e[0] for e in edges], dtype=np.uint32)
+        dst = np.ascontiguousarray([e[1] for e in edges], dtype=np.uint32)
+        w = np.ascontiguousarray([e[2] for e in edges], dtype=np.int64)
+        own8 = np.ascontiguousarray(own != 0, dtype=np.uint8)
+        h = _P()
+        _check(lib.egs_host_arena_build(n, len(edges), src.ctypes.data, dst.ctypes.data,
+                                        w.ctypes.data, own8.ctypes.data, 0, C.byref(h)))
+        return cls._from_native(h)
+
+    @classmethod
+    def parse(cls, text, pinned: bool = False) -> "GameArena":
+        """``parse_arena`` (io.cpp:87-149) of the reference's text format,
+        on every host thread (egs_arena_parse_text)."""
+        data = text.encode() if isinstance(text, str) else bytes(text)
+        h = _P()
+        _check(lib.egs_arena_parse_text(data, len(data), int(pinned), C.byref(h)))
+        return cls._from_native(h)
+
+    @classmethod
+    def load(cls, path: str, pinned: bool = False) -> "GameArena":
+        """An arena saved by ``save`` (binary format, egs_arena_io.cpp)."""
+        h = _P()
+        _check(lib.egs_arena_load(os.fsencode(path), int(pinned), C.byref(h)))
+        return cls._from_native(h)
+
+    def save(self, path: str) -> None:
+        v = self.view()
+        _check(lib.egs_arena_save(C.byref(v), os.fsencode(path)))
+
+    def write_text(self) -> str:
+        """``write_arena`` (io.cpp:151-176), byte-identical."""
+        v = self.view()
+        n = lib.egs_arena_write_text(C.byref(v), None, 0)
+        if n < 0:
+            _check(int(-n))
+        buf = C.create_string_buffer(max(int(n), 1))
+        lib.egs_arena_write_text(C.byref(v), buf, n)
+        return buf.raw[:n].decode()
 
 
 # -------------------------------------------------------------- options ----

@@ -23,20 +23,9 @@
 #include <cuda_runtime.h>
 
 #include "egs_gpu.h"
+#include "egs_host_arena.h"
 
 void egs_internal_set_error(const std::string& msg);
-
-struct egs_host_arena {
-  uint32_t n = 0;
-  uint64_t m = 0;
-  bool pinned = false;
-  uint64_t* off = nullptr;
-  uint32_t* dst = nullptr;
-  int64_t* w = nullptr;
-  uint8_t* owner = nullptr;
-  int64_t credit_cap = 0;
-  int64_t max_abs_weight = 0;
-};
 
 namespace {
 
@@ -92,7 +81,9 @@ void parallel_for(uint64_t count, Fn&& fn) {
   for (auto& t : pool) t.join();
 }
 
-egs_host_arena* arena_alloc(uint32_t n, uint64_t m, bool pinned) {
+}  // namespace
+
+egs_host_arena* egs_internal_arena_alloc(uint32_t n, uint64_t m, bool pinned) {
   auto* a = new egs_host_arena();
   a->n = n;
   a->m = m;
@@ -108,9 +99,11 @@ egs_host_arena* arena_alloc(uint32_t n, uint64_t m, bool pinned) {
   return a;
 }
 
+void egs_internal_arena_free(egs_host_arena* a) { egs_host_arena_free(a); }
+
 // compute_stats (arena.cpp:80-108): M_G and max |w| with the same overflow
 // checks and headroom.
-int finish_stats(egs_host_arena* a) {
+int egs_internal_finish_stats(egs_host_arena* a) {
   std::vector<int64_t> worst((size_t)a->n, 0);
   std::atomic<int64_t> maxw_all{0};
   parallel_for(a->n, [&](uint64_t lo, uint64_t hi) {
@@ -133,8 +126,9 @@ int finish_stats(egs_host_arena* a) {
   const int64_t maxw = maxw_all.load();
   for (uint32_t v = 0; v < a->n; ++v) {
     if (a->off[v + 1] == a->off[v]) {
-      egs_internal_set_error("vertex " + std::to_string(v) + " has no outgoing edge");
-      return EGS_ERR_INVALID_CONFIG;
+      egs_internal_set_error("NonTotalArenaError: vertex " + std::to_string(v) +
+                             " has no outgoing edge");
+      return EGS_ERR_INPUT;
     }
     if (__builtin_add_overflow(cap, worst[v], &cap)) {
       egs_internal_set_error("credit bound exceeds the representable range");
@@ -149,6 +143,8 @@ int finish_stats(egs_host_arena* a) {
   a->max_abs_weight = maxw;
   return EGS_OK;
 }
+
+namespace {
 
 inline void append_uint(std::string& out, uint64_t v) {
   char buf[24];
@@ -176,7 +172,7 @@ int egs_host_arena_fixed(uint64_t n, uint32_t d, int64_t W, uint64_t seed,
     return EGS_ERR_INVALID_CONFIG;
   }
   const uint64_t m = n * d;
-  egs_host_arena* a = arena_alloc((uint32_t)n, m, pinned != 0);
+  egs_host_arena* a = egs_internal_arena_alloc((uint32_t)n, m, pinned != 0);
   if (!a) {
     egs_internal_set_error("host allocation failed");
     return EGS_ERR_CUDA;
@@ -193,7 +189,7 @@ int egs_host_arena_fixed(uint64_t n, uint32_t d, int64_t W, uint64_t seed,
     }
   });
   a->off[n] = m;
-  int rc = finish_stats(a);
+  int rc = egs_internal_finish_stats(a);
   if (rc != EGS_OK) {
     egs_host_arena_free(a);
     return rc;
@@ -237,7 +233,7 @@ int egs_host_arena_rmat(uint32_t scale, uint32_t ef, int64_t W, uint64_t seed,
   uint64_t sinks = 0;
   for (uint64_t v = 0; v < n; ++v) sinks += deg[v] == 0;
   const uint64_t m = base + sinks;
-  egs_host_arena* a = arena_alloc((uint32_t)n, m, pinned != 0);
+  egs_host_arena* a = egs_internal_arena_alloc((uint32_t)n, m, pinned != 0);
   if (!a) {
     egs_internal_set_error("host allocation failed");
     return EGS_ERR_CUDA;
@@ -274,7 +270,7 @@ int egs_host_arena_rmat(uint32_t scale, uint32_t ef, int64_t W, uint64_t seed,
       ++k;
     }
   }
-  int rc = finish_stats(a);
+  int rc = egs_internal_finish_stats(a);
   if (rc != EGS_OK) {
     egs_host_arena_free(a);
     return rc;

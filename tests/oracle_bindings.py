@@ -245,6 +245,8 @@ class RefLib:
         L.egsref_is_progress_measure.argtypes = [P, P]
         L.egsref_is_progress_measure.restype = C.c_int
         L.egsref_last_error.restype = C.c_char_p
+        L.egsref_parse_arena.argtypes = [C.c_char_p, C.c_size_t]
+        L.egsref_parse_arena.restype = P
 
     def _wrap(self, h):
         if not h:
@@ -265,6 +267,13 @@ class RefLib:
         own = np.array(owners, dtype=np.uint8)
         return self._wrap(self.L.egsref_build(n, len(edges), src.ctypes.data, dst.ctypes.data,
                                               w.ctypes.data, own.ctypes.data))
+
+    def parse_arena(self, text: bytes):
+        """(arena, None) or (None, "<Kind>: <what()>") from parse_arena."""
+        h = self.L.egsref_parse_arena(text, len(text))
+        if not h:
+            return None, self.L.egsref_last_error().decode()
+        return RefArena(self.L, h), None
 
     def credit_cap(self, a) -> int:
         return int(self.L.egsref_credit_cap(a.h))
