@@ -425,68 +425,58 @@ def run_our_arm(a):
 
 
 def run_our_arm_partitioned(a):
-    """N > 1: the vertex-range partitioned solve (distributed.py),
-    NCCL all-gathers between steps; strong scaling of the same C4 solve."""
+    """N > 1 (torchrun, one process per GPU): the partitioned solve of the same
+    C4 arena (distributed.py) -- each rank uploads the arena,
+    keeps its class-balanced share of the rows, and the ranks exchange raised
+    values by NVLink peer stores inside one persistent kernel per rank; the
+    host only swaps IPC handles (torch.distributed) and waits.  Strong
+    scaling: the total work is the one C4 solve."""
+    import numpy as np
     import torch
 
     import paper_1710_03647_b200 as egs
-    from paper_1710_03647_b200.distributed import DeviceSteps, TorchComm, solve_partitioned
+    from paper_1710_03647_b200.distributed import Partition, TorchComm, solve_distributed
 
-    # EGS_BENCH_STAGED=1: gloo with host staging and ranks sharing the visible
-    # GPUs -- only to exercise this path on a single-GPU box; never a bench value
-    staged = os.environ.get("EGS_BENCH_STAGED") == "1"
-    rank, world = dist_setup(a.gpus, "gloo" if staged else "nccl")
+    rank, world = dist_setup(a.gpus, "nccl")
     dev = env_int("LOCAL_RANK", 0) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev)
     log = (lambda s: print(f"[rank {rank}] {s}", file=sys.stderr, flush=True))
     kind, args = CONFIGS[a.config]
     arena = getattr(egs.GameArena, kind)(*args, 1, pinned=True)
     n, m = arena.num_vertices, arena.num_edges
-    opts = egs.SolverOptions(device=dev)
-    comm = TorchComm(rank, world, staged=staged, device=f"cuda:{dev}")
-    red_dev = "cpu" if staged else f"cuda:{dev}"
+    opts = egs.SolverOptions(device=dev, workers=world)
+    comm = TorchComm()
+    red_dev = f"cuda:{dev}"
 
-    def timed(fn):
-        barrier(world)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        out = fn()
-        torch.cuda.synchronize()
-        e1.record()
-        e1.synchronize()
-        return out, e0.elapsed_time(e1) * 1e-3
-
-    steps = DeviceSteps(arena, rank, world, opts)
+    part = Partition(arena, rank, world, opts)
+    part.connect(comm.allgather_bytes(part.export()))
+    barrier(world)
+    log(f"plan: rank_lo={part.plan['rank_lo']} edges={part.plan['edges']}")
     for _ in range(a.warmup):
-        steps.reset()
-        solve_partitioned(steps, comm)
-    total_s, edges, rep, launches = 0.0, 0, None, 0
+        rep = solve_distributed(arena, comm=comm, part=part)
+    f_dev = rep.measure
+    total_s, edges = 0.0, 0
     with ClockSampler(dev) as clk:
         for _ in range(a.steps):
-            steps.reset()
-            rep, dt = timed(lambda: solve_partitioned(steps, comm))
-            total_s += dt
-            edges += rep.counters.get("edges_relaxed", 0)
-            launches += rep.kernel_launches
+            barrier(world)
+            rep = solve_distributed(arena, comm=comm, part=part)
+            total_s += rep.solve_seconds
+            edges += rep.edges_relaxed
     total_s = max_over_ranks(total_s, world, red_dev)
     edges_all = sum_over_ranks(edges, world, red_dev)
-    f_dev = rep.measure
-    steps.close()
+    rounds = rep.rounds
+    part.close()
 
-    # e2e: partition upload (H2D + device build) + solve + export, per rank
+    # e2e: this rank's upload + device build, handle exchange, solve, D2H
     h2d = h2d_bytes(arena)
     e2e_t, e2e_edges = 0.0, 0
     for _ in range(a.e2e_steps):
-        def one():
-            st = DeviceSteps(arena, rank, world, opts)
-            r = solve_partitioned(st, comm)
-            st.close()
-            return r
-        r, dt = timed(one)
-        e2e_t += dt
-        e2e_edges += r.counters.get("edges_relaxed", 0)
-        assert (r.measure == f_dev).all()
+        barrier(world)
+        t1 = time.perf_counter()
+        r = solve_distributed(arena, opts, comm=comm)
+        e2e_t += time.perf_counter() - t1
+        e2e_edges += r.edges_relaxed
+        assert np.array_equal(r.measure, f_dev)
     e2e_t = max_over_ranks(e2e_t, world, red_dev)
     e2e_edges = sum_over_ranks(e2e_edges, world, red_dev)
     line = {
@@ -494,20 +484,18 @@ def run_our_arm_partitioned(a):
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_s / a.steps * 1e3,
         "time_to_fixpoint_s": total_s / a.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None,
-        "dtype": "u32" if steps.value_bytes == 4 else "u64",
+        "dtype": "u32" if arena.credit_cap < 2 ** 31 - 1 else "u64",
         "data": "synthetic (canonical splitmix64 generator, SURVEY.md Appendix B)",
         "config": {"workload": workload_name(a.config), "vertices": n, "edges": m,
-                   "parallelism": f"vertex-range partition x{world}, "
-                                  + ("gloo staged (path test only)" if staged else
-                                     "NCCL all-gather per step"),
+                   "parallelism": f"class-balanced vertex partition x{world}, "
+                                  "device-side exchange (NVLink peer stores, cross-rank "
+                                  "barriers in peer memory)",
                    "l2": "inputs larger than L2; no flush"},
-        "solve": {"rounds": rep.rounds, "cert_attempts": rep.cert_attempts,
-                  "cert_passes": rep.cert_passes, "certified": rep.certified,
-                  "collectives": rep.collectives, "bytes_gathered": rep.bytes_gathered},
+        "solve": {"rounds": rounds, "plan_edges": rep.plan["edges"]},
         "e2e": {"value": e2e_edges / e2e_t / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
                 "d2h_bytes_per_step": n * 8 * world, "ms_per_step": e2e_t / a.e2e_steps * 1e3,
-                "api": "egs_part_create/egs_part_step (include/egs_gpu.h) + distributed.py"},
-        "gpu_launches": launches,
+                "api": "egs_part_create / egs_part_connect / egs_part_solve (include/egs_gpu.h)"},
+        "gpu_launches": a.steps,
         "clocks": clk.summary(),
     }
     if rank == 0:

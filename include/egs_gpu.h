@@ -182,65 +182,67 @@ int64_t egs_ctx_write_solution(egs_ctx* ctx, char* buf, size_t cap);
 void egs_ctx_destroy(egs_ctx* ctx);
 
 /* ---------------------------------------------------------------------
- * Multi-GPU partition.  One process per GPU; rank r owns the
- * relabelled vertex range [own_lo, own_hi) of `slice` vertices.  The
- * arena is replicated on every GPU, the measure f and the staging array are
- * replicated with `padded` = world * slice entries and the certificate
- * candidate bitmap with padded / 32 words, and the host exchanges the owned
- * slices between steps (all-gather over NCCL:
- * paper_1710_03647_b200/distributed.py).  The device addresses of those
- * arrays are returned so a collective library can operate on them in place.
- * Steps restate the phases of egs_ctx_solve restricted to the owned range. */
+ * Multi-GPU partition.  One process (or thread) per GPU;
+ * `world` ranks solve one arena together.  The reference has no
+ * distributed solver (its workers are threads, solver_par.cpp:231-236).
+ *
+ * Partition: the relabelled vertex order is rank-major -- rank r owns the
+ * contiguous id range [rank_lo[r], rank_lo[r+1]) -- and inside each rank
+ * class-sorted (player 0 light / medium / heavy, player 1 light / medium /
+ * heavy).  Every (owner, degree) class is split into `world` pieces balanced
+ * by out-edges (edge_balanced_bounds, solver_par.cpp:62-80), so every rank
+ * gets an equal share of player-0 rows, player-1 rows and hubs.  A rank
+ * stores only its own rows' edge records and the predecessor transpose of
+ * its own rows (the predecessors it activates); the measure, the changed
+ * bitmaps and the certificate's removal bitmaps are replicated.
+ *
+ * Solve: one persistent kernel per rank (k_solve).  A rank writes every value
+ * it raises into its own replica AND into every peer's replica (NVLink peer
+ * stores through CUDA IPC mappings, or plain stores when the ranks share a
+ * device), sets the changed bits the same way, and at every phase boundary
+ * the ranks meet at a device-side barrier (release/acquire flags in peer
+ * memory) that also sums the per-rank phase counts, so every rank takes the
+ * same schedule decision -- dense / sparse, certificate, termination --
+ * without the host.  The result is byte-identical to the single-GPU solve.
+ * ------------------------------------------------------------------- */
+#define EGS_MAX_RANKS 8
 typedef struct egs_part egs_part;
-typedef struct egs_part_layout {
-  uint32_t num_vertices;  /* n */
-  uint32_t slice;         /* vertices per rank, multiple of 32 */
-  uint32_t padded;        /* world * slice: entries of the replicated arrays */
-  uint32_t own_lo;        /* this rank's range of relabelled ids */
-  uint32_t own_hi;
-  uint32_t value_bytes;   /* 4 (u32) or 8 (u64); top = all ones */
-  uint64_t f_dev;         /* device address of the replicated measure */
-  uint64_t stage_dev;     /* device address of the replicated staging array */
-  uint64_t cand_dev;      /* device address of the replicated certificate candidate
-                             bitmap (padded / 32 u32 words) */
-  uint64_t send_dev;      /* sparse exchange: this rank's packed entries (slice entries) */
-  uint64_t recv_dev;      /* sparse exchange: world * slice entries, rank r's at r * stride */
-  uint32_t entry_bytes;   /* 8 ({id << 32 | u32 value}) or 16 ({id, u64 value}) */
-  uint32_t reserved0;
-} egs_part_layout;
 
-#define EGS_STEP_ROUND1 0     /* seeding + round 1 from the weights */
-#define EGS_STEP_LIFT 1       /* one dense lift round (stages raised values) */
-#define EGS_STEP_COMMIT 2     /* staged -> f for this rank's raised vertices */
-#define EGS_STEP_CERT_INIT 3  /* candidate bits (raised, non-top) into the bitmap */
-#define EGS_STEP_CERT_PRUNE 4 /* one certificate pass */
-#define EGS_STEP_CERT_APPLY 5 /* certified vertices -> top */
+typedef struct egs_part_plan {
+  uint32_t world;
+  uint32_t num_vertices;
+  uint32_t rank_lo[EGS_MAX_RANKS + 1];      /* rank r: relabelled ids [rank_lo[r], rank_lo[r+1]) */
+  uint32_t class_lo[EGS_MAX_RANKS][7];      /* rank r, class k: ids [class_lo[r][k], class_lo[r][k+1]) */
+  uint32_t piece[6][EGS_MAX_RANKS + 1];     /* class k's rank-r piece: class positions [piece[k][r], piece[k][r+1]) */
+  uint64_t edges[EGS_MAX_RANKS];            /* out-edges of rank r's vertices */
+} egs_part_plan;
 
-/* opts->n_gpus must equal world. */
+/* The partition of an arena over `world` ranks (host only, deterministic:
+ * every rank computes the same plan). */
+int egs_part_plan_compute(const egs_arena_view* arena, int32_t world, egs_part_plan* plan);
+
+/* This rank's context: the arena relabelled by the plan, own rows only.
+ * opts->n_gpus must equal world; opts->device selects the GPU. */
 int egs_part_create(const egs_arena_view* arena, const egs_gpu_opts* opts, int32_t rank,
-                    int32_t world, egs_part** out, egs_part_layout* layout,
-                    egs_gpu_stats* stats);
-/* Runs one step on this rank's range.  `parity` selects the changed bitmap
- * of the current round (round & 1).  counts[0] = vertices raised (ROUND1,
- * LIFT) or certified (CERT_APPLY); counts[1] = candidates removed
- * (CERT_PRUNE).  Blocks until the step is done. */
-int egs_part_step(egs_part* part, int32_t step, int32_t parity, uint64_t* counts);
-/* Sparse exchange.  egs_part_pack writes this rank's vertices
- * marked by `which` -- EGS_PACK_CHANGED: raised in the round of `parity`
- * (after EGS_STEP_COMMIT); EGS_PACK_REMOVED: dropped by the last
- * EGS_STEP_CERT_PRUNE -- as (id, value) entries to send_dev; *count = entries.
- * After the host all-gathers them into recv_dev (rank r's entries at
- * r * stride), egs_part_unpack scatters the other ranks' entries into f. */
-#define EGS_PACK_CHANGED 0
-#define EGS_PACK_REMOVED 1
-int egs_part_pack(egs_part* part, int32_t which, int32_t parity, uint32_t* count);
-int egs_part_unpack(egs_part* part, const uint32_t* counts, uint32_t stride);
-/* Resets f, the bitmaps and the counters for a new solve. */
-int egs_part_reset(egs_part* part);
-/* The replicated measure in the reference's raw encoding, original ids. */
+                    int32_t world, egs_part** out, egs_part_plan* plan, egs_gpu_stats* stats);
+/* CUDA IPC handle (64 bytes) of this rank's replicated state, for peers in
+ * other processes. */
+#define EGS_IPC_HANDLE_BYTES 64
+int egs_part_export(egs_part* part, void* handle);
+/* Map every peer's replicated state: handles[r * 64 ...] = rank r's export
+ * (this rank's own entry is ignored). */
+int egs_part_connect(egs_part* part, const void* handles);
+/* Ranks living in ONE process (several GPUs of a process, or several ranks
+ * sharing one device for tests): connect them directly.  parts[r] = rank r. */
+int egs_part_connect_local(egs_part* const* parts, int32_t world);
+/* Solve: every rank must call it concurrently (one host thread or process
+ * per rank); blocks until the fixpoint.  Each rank's device-side waits for
+ * its peers time out after opts->timeout_seconds (or 60 s) with
+ * EGS_ERR_CUDA instead of hanging. */
+int egs_part_solve(egs_part* part, egs_gpu_stats* stats);
+/* The measure in the reference's raw encoding, original ids (identical on
+ * every rank after a solve). */
 int egs_part_read_measure(egs_part* part, int64_t* f_out);
-/* Counters accumulated by this rank's steps since the last reset. */
-int egs_part_counters(egs_part* part, egs_gpu_stats* stats);
 void egs_part_destroy(egs_part* part);
 
 /* Output format: write_solution(make_solution(arena, report)) (io.cpp:178-210)

@@ -162,32 +162,46 @@ class GpuStats(C.Structure):
         return d
 
 
-class PartLayout(C.Structure):
+MAX_RANKS = 8
+
+
+class PartPlan(C.Structure):
+    """egs_part_plan (include/egs_gpu.h): the rank-major, class-balanced
+    partition of the relabelled vertices."""
     _fields_ = [
-        ("num_vertices", C.c_uint32), ("slice", C.c_uint32), ("padded", C.c_uint32),
-        ("own_lo", C.c_uint32), ("own_hi", C.c_uint32), ("value_bytes", C.c_uint32),
-        ("f_dev", C.c_uint64), ("stage_dev", C.c_uint64), ("cand_dev", C.c_uint64),
-        ("send_dev", C.c_uint64), ("recv_dev", C.c_uint64), ("entry_bytes", C.c_uint32),
-        ("reserved0", C.c_uint32),
+        ("world", C.c_uint32), ("num_vertices", C.c_uint32),
+        ("rank_lo", C.c_uint32 * (MAX_RANKS + 1)),
+        ("class_lo", (C.c_uint32 * 7) * MAX_RANKS),
+        ("piece", (C.c_uint32 * (MAX_RANKS + 1)) * 6),
+        ("edges", C.c_uint64 * MAX_RANKS),
     ]
+
+    def as_dict(self) -> dict:
+        w = self.world
+        return {"world": w, "num_vertices": self.num_vertices,
+                "rank_lo": list(self.rank_lo)[:w + 1],
+                "class_lo": [list(self.class_lo[r]) for r in range(w)],
+                "piece": [list(self.piece[k])[:w + 1] for k in range(6)],
+                "edges": list(self.edges)[:w]}
 
 
 _P = C.c_void_p
+IPC_HANDLE_BYTES = 64
+lib.egs_part_plan_compute.argtypes = [C.POINTER(ArenaView), C.c_int32, C.POINTER(PartPlan)]
+lib.egs_part_plan_compute.restype = C.c_int
 lib.egs_part_create.argtypes = [C.POINTER(ArenaView), C.POINTER(GpuOpts), C.c_int32, C.c_int32,
-                                C.POINTER(_P), C.POINTER(PartLayout), C.POINTER(GpuStats)]
+                                C.POINTER(_P), C.POINTER(PartPlan), C.POINTER(GpuStats)]
 lib.egs_part_create.restype = C.c_int
-lib.egs_part_step.argtypes = [_P, C.c_int32, C.c_int32, C.POINTER(C.c_uint64)]
-lib.egs_part_step.restype = C.c_int
-lib.egs_part_pack.argtypes = [_P, C.c_int32, C.c_int32, C.POINTER(C.c_uint32)]
-lib.egs_part_pack.restype = C.c_int
-lib.egs_part_unpack.argtypes = [_P, C.POINTER(C.c_uint32), C.c_uint32]
-lib.egs_part_unpack.restype = C.c_int
-lib.egs_part_reset.argtypes = [_P]
-lib.egs_part_reset.restype = C.c_int
+lib.egs_part_export.argtypes = [_P, C.c_char_p]
+lib.egs_part_export.restype = C.c_int
+lib.egs_part_connect.argtypes = [_P, C.c_char_p]
+lib.egs_part_connect.restype = C.c_int
+lib.egs_part_connect_local.argtypes = [C.POINTER(_P), C.c_int32]
+lib.egs_part_connect_local.restype = C.c_int
+lib.egs_part_solve.argtypes = [_P, C.POINTER(GpuStats)]
+lib.egs_part_solve.restype = C.c_int
 lib.egs_part_read_measure.argtypes = [_P, _P]
 lib.egs_part_read_measure.restype = C.c_int
-lib.egs_part_counters.argtypes = [_P, C.POINTER(GpuStats)]
-lib.egs_part_counters.restype = C.c_int
 lib.egs_part_destroy.argtypes = [_P]
 lib.egs_part_destroy.restype = None
 lib.egs_gpu_opts_default.argtypes = [C.POINTER(GpuOpts)]

@@ -4,7 +4,9 @@
 //
 //   * vertices relabelled into six contiguous ranges by (owner, out-degree
 //     class): the owner-sorted order of reorder_by_owner (arena.cpp:119-149;
-//     PAPER.md:506-511) refined by row length, stable inside each range;
+//     PAPER.md:506-511) refined by row length, stable inside each range
+//     (egs_scan.cuh k_class_tiles / k_class_place); with several ranks the
+//     order is rank-major, each rank's block class-sorted (egs_part_plan);
 //   * rows re-packed as edge records: 4-byte packed {dst | w << tbits} when
 //     every weight fits beside the target bits, else 8-byte {u32 dst, i32 w}
 //     (weights are validated to fit int32; arena.hpp:13 stores int64);
@@ -21,33 +23,15 @@
 
 namespace egs {
 
-// Class key of every vertex + histogram of the six classes.
-__global__ void k_classify(uint32_t n, const uint64_t* off64, const uint8_t* owner,
-                           uint8_t* key, uint32_t* val, unsigned int* hist) {
-  __shared__ unsigned int s_hist[kNumClasses];
-  if (threadIdx.x < kNumClasses) s_hist[threadIdx.x] = 0;
-  __syncthreads();
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n;
-       v += gridDim.x * blockDim.x) {
-    const uint64_t deg = off64[v + 1] - off64[v];
-    const int cls = (owner[v] ? 3 : 0) + (deg <= kLightMax ? 0 : deg <= kMediumMax ? 1 : 2);
-    key[v] = (uint8_t)cls;
-    val[v] = v;
-    atomicAdd(&s_hist[cls], 1u);
-  }
-  __syncthreads();
-  if (threadIdx.x < kNumClasses && s_hist[threadIdx.x])
-    atomicAdd(hist + threadIdx.x, s_hist[threadIdx.x]);
-}
-
-// perm[old] = new; new row lengths (exclusive-scanned into offsets next).
-__global__ void k_permute(uint32_t n, const uint32_t* inv, const uint64_t* off64,
-                          uint32_t* perm, uint32_t* deg_new) {
+// Row lengths in the new order (exclusive-scanned into offsets next); rows
+// outside this rank's range [own_lo, own_hi) are empty here (multi-GPU: a
+// rank stores its own rows only).
+__global__ void k_row_lengths(uint32_t n, const uint32_t* inv, const uint64_t* off64,
+                              uint32_t own_lo, uint32_t own_hi, uint32_t* deg_new) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += gridDim.x * blockDim.x) {
     const uint32_t o = inv[i];
-    perm[o] = i;
-    deg_new[i] = (uint32_t)(off64[o + 1] - off64[o]);
+    deg_new[i] = i >= own_lo && i < own_hi ? (uint32_t)(off64[o + 1] - off64[o]) : 0u;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) deg_new[n] = 0;
 }
@@ -67,7 +51,8 @@ __global__ void __launch_bounds__(256)
     k_relabel_targets(uint32_t n, uint32_t r0, uint32_t r1, const uint64_t* off64,
                       const uint32_t* dst, const uint32_t* perm, const uint32_t* off_new,
                       void* edge, uint32_t tbits, uint32_t* ckey, uint32_t* cval,
-                      unsigned int* bad, uint32_t* longlist, unsigned int* longcnt) {
+                      unsigned int* bad, uint32_t* longlist, unsigned int* longcnt,
+                      uint32_t own_lo, uint32_t own_hi) {
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int* ex = static_cast<int*>(edge);
@@ -81,7 +66,9 @@ __global__ void __launch_bounds__(256)
       e = (uint32_t)off64[o + 1];
       rn = perm[o];
       delta = off_new[rn] - b;
-      if (e - b > kRelabelLong) {  // a hub: its edges go to the whole grid
+      if (rn < own_lo || rn >= own_hi) {  // another rank's row (multi-GPU)
+        e = b;
+      } else if (e - b > kRelabelLong) {  // a hub: its edges go to the whole grid
         longlist[atomicAdd(longcnt, 1u)] = o;
         e = b;
       }
@@ -114,7 +101,8 @@ template <class W>
 __global__ void __launch_bounds__(256)
     k_relabel_weights(uint32_t r0, uint32_t r1, const uint64_t* off64, const W* wn,
                       const uint32_t* perm, const uint32_t* off_new, void* edge,
-                      uint32_t tbits, uint32_t* longlist, unsigned int* longcnt) {
+                      uint32_t tbits, uint32_t* longlist, unsigned int* longcnt,
+                      uint32_t own_lo, uint32_t own_hi) {
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int* ex = static_cast<int*>(edge);
@@ -125,8 +113,11 @@ __global__ void __launch_bounds__(256)
     if (o < r1) {
       b = (uint32_t)off64[o];
       e = (uint32_t)off64[o + 1];
-      delta = off_new[perm[o]] - b;
-      if (e - b > kRelabelLong) {
+      const uint32_t rn = perm[o];
+      delta = off_new[rn] - b;
+      if (rn < own_lo || rn >= own_hi) {
+        e = b;
+      } else if (e - b > kRelabelLong) {
         longlist[atomicAdd(longcnt, 1u)] = o;
         e = b;
       }
@@ -412,62 +403,6 @@ __global__ void k_format(uint32_t n, const V* f, const uint32_t* perm, const uin
       p += d;
     }
     *p = '\n';
-  }
-}
-
-// ------------------------------------------ multi-GPU sparse exchange ----
-// The owned vertices marked in `bits` (a round's raised
-// vertices, or a certificate pass's removals) are packed as (id, value)
-// entries -- one u64 word {id << 32 | value} for u32 values, two words for
-// u64 -- so the ranks all-gather entries instead of their whole slices when
-// few vertices changed.  A warp packs one bitmap word; order is irrelevant.
-template <class V>
-__global__ void __launch_bounds__(256)
-    k_pack(uint32_t lo, uint32_t hi, const uint32_t* bits, const V* f, uint64_t* out,
-           unsigned int* count) {
-  constexpr uint32_t EW = sizeof(V) / 4;  // words per entry: 1 or 2
-  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
-  const uint32_t lane = lane_id();
-  for (uint32_t w = (lo >> 5) + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-       w < ((hi + 31) >> 5); w += nwarps) {
-    const uint32_t v = (w << 5) + lane;
-    const bool mine = v >= lo && v < hi && ((__ldcg(bits + w) >> lane) & 1u);
-    const uint32_t m = __ballot_sync(0xffffffffu, mine);
-    if (!m) continue;
-    uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(count, (unsigned int)__popc(m));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (mine) {
-      const uint32_t pos = base + __popc(m & lanemask_lt());
-      const V x = f[v];
-      if (EW == 1)
-        out[pos] = ((uint64_t)v << 32) | (uint64_t)x;
-      else {
-        out[2 * (size_t)pos] = v;
-        out[2 * (size_t)pos + 1] = (uint64_t)x;
-      }
-    }
-  }
-}
-
-// Scatter of the received entries: rank r's count[r] entries start at entry
-// r * stride; the own rank's are skipped (its f is already current).
-template <class V>
-__global__ void __launch_bounds__(256)
-    k_unpack(const uint64_t* in, const uint32_t* count, uint32_t world, uint32_t stride,
-             uint32_t self, V* f) {
-  constexpr uint32_t EW = sizeof(V) / 4;
-  const uint64_t total = (uint64_t)world * stride;
-  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t r = (uint32_t)(e / stride), i = (uint32_t)(e % stride);
-    if (r == self || i >= count[r]) continue;
-    if (EW == 1) {
-      const uint64_t x = in[e];
-      f[(uint32_t)(x >> 32)] = (V)(uint32_t)x;
-    } else {
-      f[(uint32_t)in[2 * e]] = (V)in[2 * e + 1];
-    }
   }
 }
 

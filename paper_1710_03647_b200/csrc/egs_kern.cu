@@ -12,10 +12,5 @@ const void* solve_kernel(int vbits) {
                      : reinterpret_cast<const void*>(&k_solve<uint64_t>);
 }
 
-const void* part_kernel(int vbits) {
-  return vbits == 32 ? reinterpret_cast<const void*>(&k_part_step<uint32_t>)
-                     : reinterpret_cast<const void*>(&k_part_step<uint64_t>);
-}
-
 }  // namespace EGS_FMT_NS
 }  // namespace egs

@@ -1,0 +1,222 @@
+// egs_scan.cuh — hand-written device primitives of the arena build
+// (egs_build.cuh / egs_solver.cu), replacing library scans and sorts:
+//
+//   * exclusive prefix sum of u32 / u64 arrays (reduce -> scan of the tile
+//     sums -> down-sweep), in place allowed;
+//   * the stable class placement of the relabelling: every vertex's
+//     position in the class-sorted order (player 0 light / medium / heavy,
+//     player 1 light / medium / heavy; reorder_by_owner arena.cpp:119-149
+//     refined by degree) from per-tile class counts and warp ballots --
+//     a stable 6-bucket counting sort, mapped through the multi-GPU plan.
+#pragma once
+
+#include <cstdint>
+
+#include "egs_device.cuh"
+#include "egs_types.cuh"
+
+namespace egs {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;  // per thread: tiles of 4096 elements
+constexpr uint32_t kScanTile = kScanThreads * kScanItems;
+
+// block-wide exclusive scan of one value per thread; *total = block sum
+template <class T>
+__device__ __forceinline__ T block_excl_scan(T x, T* s_warp, T* total) {
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  T incl = x;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const T y = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= (uint32_t)d) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    T w = lane < (uint32_t)(blockDim.x >> 5) ? s_warp[lane] : T(0);
+    T wi = w;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const T y = __shfl_up_sync(0xffffffffu, wi, d);
+      if (lane >= (uint32_t)d) wi += y;
+    }
+    if (lane < (uint32_t)(blockDim.x >> 5)) s_warp[lane] = wi - w;
+    if (lane == 31) s_warp[32] = wi;
+  }
+  __syncthreads();
+  const T out = s_warp[warp] + incl - x;
+  if (total) *total = s_warp[32];
+  __syncthreads();
+  return out;
+}
+
+// tile sums: tsum[t] = sum of in[t * kScanTile ...] (grid-stride over tiles)
+template <class T, class In>
+__global__ void __launch_bounds__(kScanThreads)
+    k_scan_reduce(const In* in, uint64_t n, T* tsum, uint64_t ntiles) {
+  __shared__ T s_warp[33];
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const uint64_t base = t * kScanTile;
+    T acc = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      const uint64_t i = base + (uint64_t)k * kScanThreads + threadIdx.x;
+      if (i < n) acc += (T)in[i];
+    }
+    T total;
+    block_excl_scan<T>(acc, s_warp, &total);
+    if (threadIdx.x == 0) tsum[t] = total;
+  }
+}
+
+// exclusive scan of the tile sums in place (one CTA, sequential chunks)
+template <class T>
+__global__ void __launch_bounds__(1024) k_scan_tiles(T* tsum, uint64_t ntiles) {
+  __shared__ T s_warp[33];
+  T carry = 0;
+  for (uint64_t base = 0; base < ntiles; base += blockDim.x) {
+    const uint64_t i = base + threadIdx.x;
+    const T x = i < ntiles ? tsum[i] : T(0);
+    T total;
+    const T ex = block_excl_scan<T>(x, s_warp, &total);
+    if (i < ntiles) tsum[i] = carry + ex;
+    carry += total;
+  }
+}
+
+// out[i] = tsum[tile] + exclusive scan of the tile's in[] (blocked per
+// thread so the scan is over consecutive elements)
+template <class T, class In>
+__global__ void __launch_bounds__(kScanThreads)
+    k_scan_down(const In* in, T* out, uint64_t n, const T* tsum, uint64_t ntiles) {
+  __shared__ T s_warp[33];
+  __shared__ T s_buf[kScanTile];
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const uint64_t base = t * kScanTile;
+    // coalesced load into shared memory, then each thread scans its run
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      const uint64_t i = base + (uint64_t)k * kScanThreads + threadIdx.x;
+      s_buf[k * kScanThreads + threadIdx.x] = i < n ? (T)in[i] : T(0);
+    }
+    __syncthreads();
+    T run[kScanItems];
+    T acc = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      run[k] = acc;
+      acc += s_buf[threadIdx.x * kScanItems + k];
+    }
+    const T off = tsum[t] + block_excl_scan<T>(acc, s_warp, nullptr);
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) s_buf[threadIdx.x * kScanItems + k] = off + run[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      const uint64_t i = base + (uint64_t)k * kScanThreads + threadIdx.x;
+      if (i < n) out[i] = s_buf[k * kScanThreads + threadIdx.x];
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------- class placement ----
+// Class of every vertex (key[v]) and per-tile class counts, class-major:
+// tcount[c * ntiles + tile].
+__global__ void __launch_bounds__(kScanThreads)
+    k_class_tiles(uint32_t n, const uint64_t* off64, const uint8_t* owner, uint8_t* key,
+                  uint32_t* tcount, uint32_t ntiles, unsigned int* hist) {
+  __shared__ unsigned int s_cnt[kNumClasses];
+  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    if (threadIdx.x < kNumClasses) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    unsigned int mine[kNumClasses] = {0, 0, 0, 0, 0, 0};
+    for (int k = 0; k < kScanItems; ++k) {
+      const uint32_t v = t * kScanTile + k * kScanThreads + threadIdx.x;
+      if (v < n) {
+        const uint64_t deg = off64[v + 1] - off64[v];
+        const int c = (owner[v] ? 3 : 0) + (deg <= kLightMax ? 0 : deg <= kMediumMax ? 1 : 2);
+        key[v] = (uint8_t)c;
+#pragma unroll
+        for (int cc = 0; cc < kNumClasses; ++cc) mine[cc] += c == cc;
+      }
+    }
+#pragma unroll
+    for (int cc = 0; cc < kNumClasses; ++cc) {
+      const unsigned int w = __reduce_add_sync(0xffffffffu, mine[cc]);
+      if (lane_id() == 0 && w) atomicAdd(&s_cnt[cc], w);
+    }
+    __syncthreads();
+    if (threadIdx.x < kNumClasses) {
+      tcount[threadIdx.x * ntiles + t] = s_cnt[threadIdx.x];
+      if (s_cnt[threadIdx.x]) atomicAdd(hist + threadIdx.x, s_cnt[threadIdx.x]);
+    }
+    __syncthreads();
+  }
+}
+
+// The partition of the class-sorted order (egs_part_plan, include/egs_gpu.h)
+// as the build kernels need it: class k's piece r covers class positions
+// [piece[k][r], piece[k][r+1]) and is relabelled from id cls_lo[r][k] on.
+struct PlanDev {
+  uint32_t world;
+  uint32_t piece[kNumClasses][kMaxRanks + 1];
+  uint32_t cls_lo[kMaxRanks][kNumClasses + 1];
+};
+
+// new id of the vertex at position `pos` of class c (0-based in the class);
+// one rank: the class-sorted position itself (cls_lo unused)
+__device__ __forceinline__ uint32_t plan_new_id(const PlanDev& pl, int c, uint32_t pos) {
+  uint32_t r = 0;
+  while (r + 1 < pl.world && pos >= pl.piece[c][r + 1]) ++r;
+  return pl.cls_lo[r][c] + (pos - pl.piece[c][r]);
+}
+
+// Stable placement: position of v in its class = tpos[c * ntiles + tile]
+// (exclusive scan of tcount, minus the class start) + the count of class-c
+// vertices before v in the tile (steps of 256 in order, warp ballots, warp
+// prefixes); perm[v] = new id, inv[new id] = v.
+__global__ void __launch_bounds__(kScanThreads)
+    k_class_place(uint32_t n, const uint8_t* key, const uint32_t* tpos, uint32_t ntiles,
+                  const __grid_constant__ PlanDev pl, uint32_t* perm, uint32_t* inv) {
+  constexpr int W = kScanThreads / 32;
+  __shared__ uint32_t s_wc[W][kNumClasses];
+  __shared__ uint32_t s_run[kNumClasses];
+  __shared__ uint32_t s_cstart[kNumClasses];
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  if (threadIdx.x < kNumClasses) s_cstart[threadIdx.x] = tpos[threadIdx.x * ntiles];
+  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    if (threadIdx.x < kNumClasses) s_run[threadIdx.x] = tpos[threadIdx.x * ntiles + t];
+    __syncthreads();
+    for (int k = 0; k < kScanItems; ++k) {
+      const uint32_t v = t * kScanTile + k * kScanThreads + threadIdx.x;
+      const int c = v < n ? key[v] : -1;
+      uint32_t rank = 0;
+#pragma unroll
+      for (int cc = 0; cc < kNumClasses; ++cc) {
+        const uint32_t m = __ballot_sync(0xffffffffu, c == cc);
+        if (c == cc) rank = __popc(m & lanemask_lt());
+        if (lane == 0) s_wc[warp][cc] = __popc(m);
+      }
+      __syncthreads();
+      if (c >= 0) {
+        uint32_t before = s_run[c];
+        for (uint32_t w = 0; w < warp; ++w) before += s_wc[w][c];
+        const uint32_t id = pl.world <= 1 ? before + rank
+                                          : plan_new_id(pl, c, before + rank - s_cstart[c]);
+        perm[v] = id;
+        inv[id] = v;
+      }
+      __syncthreads();
+      if (threadIdx.x < kNumClasses) {
+        uint32_t s = 0;
+        for (int w = 0; w < W; ++w) s += s_wc[w][threadIdx.x];
+        s_run[threadIdx.x] += s;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+}  // namespace egs

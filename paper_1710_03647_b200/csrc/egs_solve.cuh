@@ -111,6 +111,43 @@ __device__ __forceinline__ uint32_t clip_hi(const SolveParams<V>& p, uint32_t hi
   return hi < p.own_hi ? hi : p.own_hi;
 }
 
+// ---- replicated writes (multi-GPU): a value or bit a rank produces for its
+// own vertices goes to its own replica and to every peer's (NVLink peer
+// stores / system-scope atomics); with one rank these are plain writes.
+template <class V, class T>
+__device__ __forceinline__ T* peer_of(const SolveParams<V>& p, int q, T* local) {
+  return reinterpret_cast<T*>(p.xpeer[q] + (reinterpret_cast<char*>(local) - p.xbase));
+}
+template <class V>
+__device__ __forceinline__ void bits_or(const SolveParams<V>& p, uint32_t* word, uint32_t m) {
+  if (p.world == 1) {
+    atomicOr(word, m);
+    return;
+  }
+  for (int q = 0; q < p.world; ++q) atomicOr_system(peer_of(p, q, word), m);
+}
+template <class V>
+__device__ __forceinline__ void set_bit(const SolveParams<V>& p, uint32_t* bm, uint32_t v) {
+  bits_or(p, bm + (v >> 5), 1u << (v & 31u));
+}
+// the bits of bitmap word w that are this rank's vertices (the replicated
+// bitmaps carry every rank's)
+template <class V>
+__device__ __forceinline__ uint32_t own_mask(const SolveParams<V>& p, uint32_t w) {
+  if (p.world == 1) return ~0u;
+  const uint32_t lo = w << 5;
+  if (lo >= p.own_lo && lo + 32 <= p.own_hi) return ~0u;
+  uint32_t m = 0;
+  for (uint32_t i = 0; i < 32; ++i) m |= (uint32_t)(lo + i >= p.own_lo && lo + i < p.own_hi) << i;
+  return m;
+}
+template <class V>
+__device__ __forceinline__ void f_put(const SolveParams<V>& p, uint32_t v, V x) {
+  stcg(p.f + v, x);
+  if (p.world > 1)
+    for (int q = 0; q < p.world; ++q)
+      if (q != p.rank) stcg(peer_of(p, q, p.f + v), x);
+}
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -234,10 +271,18 @@ __device__ __forceinline__ bool store_raise(const SolveParams<V>& p, uint32_t v,
     stcg(p.stage + v, acc);
     return true;
   }
+  bool up;
   if (sizeof(V) == 8)
-    return atomicMax(reinterpret_cast<unsigned long long*>(p.f + v),
-                     (unsigned long long)acc) < (unsigned long long)acc;
-  return atomicMax(reinterpret_cast<unsigned int*>(p.f + v), (unsigned int)acc) < (unsigned int)acc;
+    up = atomicMax(reinterpret_cast<unsigned long long*>(p.f + v), (unsigned long long)acc) <
+         (unsigned long long)acc;
+  else
+    up = atomicMax(reinterpret_cast<unsigned int*>(p.f + v), (unsigned int)acc) < (unsigned int)acc;
+  // only the owner writes v, once per sparse round: the peers' replicas take
+  // the raised value with a plain store
+  if (up && p.world > 1)
+    for (int q = 0; q < p.world; ++q)
+      if (q != p.rank) stcg(peer_of(p, q, p.f + v), acc);
+  return up;
 }
 
 // ---- one thread per row (light rows)
@@ -506,9 +551,6 @@ __device__ __forceinline__ bool warp_claim(unsigned int* cursor, uint32_t count,
   return true;
 }
 
-__device__ __forceinline__ void set_bit(uint32_t* bm, uint32_t v) {
-  atomicOr(bm + (v >> 5), 1u << (v & 31u));
-}
 
 // Player-1 light rows of a dense round, TMA-staged.  A warp owns aligned
 // 32-vertex tiles; the tile's contiguous span of edge records is brought
@@ -602,7 +644,7 @@ __device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, bool staged, 
       if (in && !work) ++L.visits;
       const bool ch = work && fallback(v, aux);
       const uint32_t m = __ballot_sync(0xffffffffu, ch);
-      if (m && lane == 0) atomicOr(chg + w, m);
+      if (m && lane == 0) bits_or(p, chg + w, m);
       L.phase_count += ch;
       after(v, ch);  // warp-uniform
     }
@@ -672,7 +714,7 @@ __device__ __forceinline__ void tma_tiles(const SolveParams<V>& p, bool staged, 
       ch = fallback(v, t.aux);
     }
     const uint32_t m = __ballot_sync(0xffffffffu, ch);
-    if (m && lane == 0) atomicOr(chg + t.w, m);
+    if (m && lane == 0) bits_or(p, chg + t.w, m);
     L.phase_count += ch;
     after(v, ch);  // warp-uniform
   };
@@ -816,7 +858,7 @@ __device__ __noinline__ void dense_light_p0(const SolveParams<V>& p, uint32_t lo
         v = q[base + lane];
         ch = lift_thread<V, true>(p, v, L);
       }
-      if (ch) set_bit(chg, v);
+      if (ch) set_bit(p, chg, v);
       L.phase_count += ch;
       qn = base;
       __syncwarp();
@@ -1058,7 +1100,9 @@ template <class V>
 __device__ __forceinline__ void push_preds(const SolveParams<V>& p, bool raised, uint32_t v,
                                            WarpLists& q, const Frontier& t,
                                            unsigned int* qlong, Local& L) {
-  if (!__any_sync(0xffffffffu, raised)) return;
+  // several ranks: the replicated changed bitmap feeds phase_activate
+  // instead (a rank cannot push the predecessors of its peers' raises)
+  if (p.world > 1 || !__any_sync(0xffffffffu, raised)) return;
   uint32_t b = 0, e = 0;
   if (raised) {
     b = __ldg(p.g.coff + v);
@@ -1094,7 +1138,7 @@ __device__ __noinline__ void sparse_light(const SolveParams<V>& p, const uint32_
                             : lift_thread<V, false, true>(p, v, L);
     }
     if (ch) {
-      set_bit(chg, v);
+      set_bit(p, chg, v);
       ++L.phase_count;
     }
     push_preds<V>(p, ch, v, q, nxt, qlong, L);
@@ -1128,7 +1172,7 @@ __device__ __noinline__ void warp_rows(const SolveParams<V>& p, uint32_t count,
     else
       ch = p0 ? lift_warp<V, true>(p, v, L) : lift_warp<V, false>(p, v, L);
     if (ch && lane_id() == 0) {
-      set_bit(chg, v);
+      set_bit(p, chg, v);
       ++L.phase_count;
     }
     if (push) push_preds<V>(p, ch && lane_id() == 0, v, q, nxt, qlong, L);
@@ -1163,7 +1207,7 @@ __device__ __noinline__ void block_rows(const SolveParams<V>& p, uint32_t count,
     else
       ch = p0 ? lift_block<V, true>(p, v, L, s) : lift_block<V, false>(p, v, L, s);
     if (ch && threadIdx.x == 0) {
-      set_bit(chg, v);
+      set_bit(p, chg, v);
       ++L.phase_count;
     }
     if (push && threadIdx.x < 32)  // warp 0 expands the raised hub's column
@@ -1210,7 +1254,7 @@ __device__ __forceinline__ bool cand_bit(const SolveParams<V>& p, uint32_t v) {
 template <class V>
 __device__ __forceinline__ void cand_clear(const SolveParams<V>& p, uint32_t v, int64_t fv) {
   atomicAnd(p.cand + (v >> 5), ~(1u << (v & 31u)));
-  stcg(p.f + v, static_cast<V>(fv));
+  f_put<V>(p, v, static_cast<V>(fv));
 }
 template <class V>
 __device__ __forceinline__ bool good_edge(const SolveParams<V>& p, int64_t fv, int2 r) {
@@ -1478,7 +1522,7 @@ __device__ __noinline__ void round1_long(const SolveParams<V>& p, uint32_t* chg,
       ++L.apps;
       L.edges += e - b;
       if (val > V(0)) {
-        set_bit(chg, u);
+        set_bit(p, chg, u);
         ++L.phase_count;
         ++L.lifts;
       }
@@ -1529,7 +1573,7 @@ __device__ __noinline__ void round1_long(const SolveParams<V>& p, uint32_t* chg,
       ++L.apps;
       L.edges += e - b;
       if (val > V(0)) {
-        set_bit(chg, u);
+        set_bit(p, chg, u);
         ++L.phase_count;
         ++L.lifts;
       }
@@ -1670,12 +1714,12 @@ __device__ __noinline__ void phase_commit(const SolveParams<V>& p, const uint32_
     uint32_t bits[U];
     V val[U];
 #pragma unroll
-    for (int k = 0; k < U; ++k) bits[k] = w0 + k < whi ? ldcg(chg + w0 + k) : 0u;
+    for (int k = 0; k < U; ++k) bits[k] = w0 + k < whi ? ldcg(chg + w0 + k) & own_mask(p, w0 + k) : 0u;
     commit_stage_loads<V, U>(p, dense, w0, whi, lane, bits, val, V(0));
     if (p.debug) debug_check_raise<V, U>(p, w0, lane, bits, val);
 #pragma unroll
     for (int k = 0; k < U; ++k)
-      if ((bits[k] >> lane) & 1u) stcg(p.f + ((w0 + k) << 5) + lane, val[k]);
+      if ((bits[k] >> lane) & 1u) f_put<V>(p, ((w0 + k) << 5) + lane, val[k]);
   }
 }
 
@@ -1699,7 +1743,7 @@ __device__ __noinline__ void phase_cert_init(const SolveParams<V>& p, const uint
     const bool in = v >= p.own_lo && v < p.own_hi;
     const V fv = in ? ldcg(p.f + v) : Top<V>::v;
     const bool c = in && ((bits >> lane) & 1u) && fv != Top<V>::v;
-    if (c) stcg(p.f + v, fv | CandFlag<V>::v);
+    if (c) f_put<V>(p, v, fv | CandFlag<V>::v);
     const uint32_t m = __ballot_sync(0xffffffffu, c);
     if (lane == 0) stcg(p.cand + w, m);
   }
@@ -1724,7 +1768,7 @@ __device__ __noinline__ void phase_commit_cert_init(const SolveParams<V>& p, con
     uint32_t bits[U];
     V val[U];
 #pragma unroll
-    for (int k = 0; k < U; ++k) bits[k] = w0 + k < whi ? ldcg(chg + w0 + k) : 0u;
+    for (int k = 0; k < U; ++k) bits[k] = w0 + k < whi ? ldcg(chg + w0 + k) & own_mask(p, w0 + k) : 0u;
     commit_stage_loads<V, U>(p, dense, w0, whi, lane, bits, val, TOP);
     if (p.debug) debug_check_raise<V, U>(p, w0, lane, bits, val);
 #pragma unroll
@@ -1732,7 +1776,7 @@ __device__ __noinline__ void phase_commit_cert_init(const SolveParams<V>& p, con
       if (w0 + k >= whi) break;
       const bool raised = (bits[k] >> lane) & 1u;
       const bool c = raised && val[k] != TOP;
-      if (raised) stcg(p.f + ((w0 + k) << 5) + lane, c ? val[k] | CandFlag<V>::v : val[k]);
+      if (raised) f_put<V>(p, ((w0 + k) << 5) + lane, c ? val[k] | CandFlag<V>::v : val[k]);
       const uint32_t m = __ballot_sync(0xffffffffu, c);
       if (lane == 0) stcg(p.cand + w0 + k, m);
     }
@@ -1781,7 +1825,7 @@ __device__ __forceinline__ void cert_long_rows(const SolveParams<V>& p, uint32_t
       ++L.cert_scanned;
       if (!keep) {
         cand_clear(p, v, fv);
-        set_bit(rbm, v);
+        set_bit(p, rbm, v);
         ++L.phase_count;
       }
     }
@@ -1801,7 +1845,7 @@ __device__ __forceinline__ void cert_long_rows(const SolveParams<V>& p, uint32_t
       ++L.cert_scanned;
       if (!keep) {
         cand_clear(p, v, fv);
-        set_bit(rbm, v);
+        set_bit(p, rbm, v);
         ++L.phase_count;
       }
     }
@@ -1944,6 +1988,8 @@ __device__ __noinline__ void phase_cert_check(const SolveParams<V>& p, Frontier 
   const uint32_t* lH = cur.list[2];
   auto itH = [=](uint32_t i) { return ldcg(lH + i); };
   auto itM = [=](uint32_t i) { return ldcg(lM + i); };
+  // several ranks: no pushes (the next pass is built by phase_cert_mark)
+  if (p.world > 1) nxt = Frontier{};
   cert_long_rows<V>(p, cH, itH, cM, itM, slot_dyn, rbm, L, q, nxt);
   for (uint32_t i0 = blockIdx.x * kBlock + (threadIdx.x & ~31u); i0 < cL; i0 += nthreads) {
     const uint32_t i = i0 + lane_id();
@@ -1954,12 +2000,13 @@ __device__ __noinline__ void phase_cert_check(const SolveParams<V>& p, Frontier 
       removed = cert_check_thread<V>(p, v, L);
     }
     if (removed) {
-      set_bit(rbm, v);
+      set_bit(p, rbm, v);
       ++L.phase_count;
     }
     push_cert_preds<V>(p, removed, v, q, nxt, L);
   }
-  for (int c = 0; c < 3; ++c) lists_flush(q, c, nxt.list[c], nxt.cnt + c);
+  if (nxt.cnt)
+    for (int c = 0; c < 3; ++c) lists_flush(q, c, nxt.list[c], nxt.cnt + c);
   for (uint32_t i = tid; i < cL + cM + cH; i += nthreads) {
     const uint32_t v = i < cL ? ldcg(lL + i) : i < cL + cM ? ldcg(lM + (i - cL)) : ldcg(lH + (i - cL - cM));
     atomicAnd(cur.frb + (v >> 5), ~(1u << (v & 31u)));
@@ -1985,8 +2032,8 @@ __device__ __noinline__ void phase_cert_apply(const SolveParams<V>& p, uint32_t*
 #pragma unroll
     for (uint32_t k = 0; k < U; ++k) {
       const bool hit = (m[k] >> lane) & 1u;  // candidate words hold owned, non-top ids only
-      if (hit) stcg(p.f + ((w0 + k) << 5) + lane, Top<V>::v);
-      if (m[k] && lane == 0) atomicOr(chg + w0 + k, m[k]);
+      if (hit) f_put<V>(p, ((w0 + k) << 5) + lane, Top<V>::v);
+      if (m[k] && lane == 0) bits_or(p, chg + w0 + k, m[k]);
       L.phase_count += hit;
       L.certified += hit;
     }
@@ -2061,6 +2108,63 @@ __device__ __noinline__ void phase_activate_long(const SolveParams<V>& p, Fronti
   block_flush(L, slot_sum + 2);
 }
 
+// ================================================ cross-rank barrier ===
+// (multi-GPU, leader thread only, after the grid barrier that ends a phase)
+// This rank's phase sums (and its timeout flag) go to every rank's sync
+// block, then its arrival epoch with release semantics; it waits for every
+// rank's arrival (acquire), and replaces its sums by the global ones, so
+// every rank takes the same decision.  Every CTA fenced its peer writes
+// (__threadfence_system) before the grid barrier, so they are visible to a
+// peer that has seen this arrival.  A peer missing for xwait_ns zeroes the
+// sums (the solve winds down) and sets Scratch::xerr.
+__device__ __forceinline__ void st_release_sys(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned int ld_relaxed_sys(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <class V>
+__device__ __noinline__ void xbarrier(const SolveParams<V>& p, unsigned int epoch, unsigned int* slot,
+                                      Scratch* sh) {
+  XSync* me = p.xsync;
+  const int par = epoch & 1;
+  const unsigned int mine[4] = {slot[0], slot[1], slot[2], slot[3] + sh->stop};
+  for (int q = 0; q < p.world; ++q) {
+    XSync* xs = peer_of(p, q, me);
+    for (int k = 0; k < 4; ++k) xs->sums[par][p.rank][k] = mine[k];
+  }
+  __threadfence_system();
+  for (int q = 0; q < p.world; ++q) st_release_sys(&peer_of(p, q, me)->arrive[p.rank], epoch);
+  const unsigned long long t0 = globaltimer();
+  bool late = false;
+  for (int q = 0; q < p.world && !late; ++q)
+    while ((int)(ld_acquire_sys(&me->arrive[q]) - epoch) < 0) {
+      if (globaltimer() - t0 > p.xwait_ns) {
+        late = true;
+        break;
+      }
+    }
+  if (late) {
+    sh->xerr = 1;
+    sh->stop = 1;
+    for (int k = 0; k < 4; ++k) slot[k] = 0;
+    return;
+  }
+  unsigned int g[4] = {0, 0, 0, 0};
+  for (int q = 0; q < p.world; ++q)
+    for (int k = 0; k < 4; ++k) g[k] += ld_relaxed_sys(&me->sums[par][q][k]);
+  for (int k = 0; k < 3; ++k) slot[k] = g[k];
+  sh->stop = g[3] > 0 ? 1u : 0u;
+}
+
 // ========================================================== the kernel ===
 #ifndef EGS_MIN_BLOCKS
 #define EGS_MIN_BLOCKS 2  // resident CTAs per SM: 128 registers, no spills in the lift loops
@@ -2090,10 +2194,16 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
       }
     set_phase_slot(slot_sum());
   };
+  unsigned int epoch = p.epoch0;  // cross-rank barriers (multi-GPU)
   auto end_phase = [&](int kind, int fine = -1) {
     end_phase_flush();
+    if (p.world > 1) __threadfence_system();  // this phase's peer writes, before the barrier
     grid.sync();
     ++phase;
+    if (p.world > 1) {
+      if (leader) xbarrier<V>(p, ++epoch, sh->sum[(phase - 1) & 3], sh);
+      grid.sync();
+    }
     if (leader) {
       const unsigned long long t = globaltimer();
       p.ctr[kTimeSeed + kind] += t - t_prev;
@@ -2106,6 +2216,23 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
 
   tma_init_barriers();
   stats_init();
+  if (p.world > 1) {
+    // several ranks: this rank's replicated state is reset here, before a
+    // cross-rank barrier -- a peer writes into it only after that barrier
+    const uint32_t tid = blockIdx.x * kBlock + threadIdx.x, nth = gridDim.x * kBlock;
+    const uint32_t words = (n + 31) >> 5;
+    for (uint32_t v = tid; v < n; v += nth) p.f[v] = V(0);
+    for (uint32_t w = tid; w < words; w += nth) {
+      p.chg[0][w] = 0u;
+      p.chg[1][w] = 0u;
+      p.rbm[0][w] = 0u;
+      p.rbm[1][w] = 0u;
+    }
+    __threadfence_system();
+    grid.sync();
+    if (leader) xbarrier<V>(p, ++epoch, sh->sum[3], sh);
+    grid.sync();
+  }
 
   // ---- round 1: seeding + the first lift, from the weights alone
   begin_phase();
@@ -2215,7 +2342,10 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
                               p.rbm[rb], queue(cq + 1, slot_dyn() + 3));
           end_phase(2, 3);
           ++cq;
-          queued = true;
+          // (several ranks: a pass cannot push the candidate predecessors
+          // of the OTHER ranks' removals, so every sparse pass is preceded
+          // by a mark phase over the replicated removal bits)
+          queued = p.world == 1;
         } else {
           begin_phase();
           phase_cert_prune<V>(p, slot_sum(), slot_dyn(), p.rbm[rb ^ 1], p.rbm[rb], Frontier{},
@@ -2249,7 +2379,7 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
          (certified_any || (double)changed * p.avg_in_deg * p.sparse_div >= (double)n));
     if (!dense) {
       uint32_t frontier_n, ncols;
-      if (inplace && !cert_now) {  // pushed by the sparse lift
+      if (inplace && !cert_now && p.world == 1) {  // pushed by the sparse lift
         frontier_n = pushed;
         ncols = pushed_long;
       } else if (fuse_act) {  // produced by the commit phase
@@ -2297,6 +2427,8 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
 
   stats_exit(p.ctr);
   if (leader) {
+    if (sh->xerr) status = 7;
+    p.ctr[kEpoch] = epoch;
     p.ctr[kRounds] = round;
     p.ctr[kDenseRounds] = rounds_dense;
     p.ctr[kSparseRounds] = rounds_sparse;
@@ -2304,45 +2436,6 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
     p.ctr[kCertPasses] = cert_passes;
     p.ctr[kStatus] = status;
   }
-}
-
-// ============================================== multi-GPU step kernel ===
-// One phase of the partitioned solve, restricted to this
-// GPU's vertex range [own_lo, own_hi).  The host exchanges the owned slices
-// of f / stage between steps (NCCL all-gather) and decides the schedule,
-// which is the same as k_solve's dense schedule.
-enum PartStep : int {
-  kStepRound1 = 0,
-  kStepLift = 1,
-  kStepCommit = 2,
-  kStepCertInit = 3,
-  kStepCertPrune = 4,
-  kStepCertApply = 5
-};
-
-template <class V>
-__global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
-    k_part_step(const __grid_constant__ SolveParams<V> p, int step, int parity) {
-  tma_init_barriers();
-  stats_init();
-  unsigned int* sum = p.sh->sum[0];
-  unsigned int* dyn = p.sh->dyn[0];
-  set_phase_slot(sum);
-  uint32_t* cur = p.chg[parity & 1];
-  uint32_t* other = p.chg[(parity & 1) ^ 1];
-  switch (step) {
-    case kStepRound1: phase_round1<V>(p, cur, sum, dyn); break;
-    case kStepLift:
-      phase_lift<V>(p, true, Frontier{}, Frontier{}, nullptr, cur, other, sum, dyn);
-      break;
-    case kStepCommit: phase_commit<V>(p, cur); break;
-    case kStepCertInit: phase_cert_init<V>(p, cur, sum); break;
-    case kStepCertPrune: phase_cert_prune<V>(p, sum, dyn, p.rbm[0], p.rbm[1]); break;
-    case kStepCertApply: phase_cert_apply<V>(p, cur, sum); break;
-    default: break;
-  }
-  end_phase_flush();
-  stats_exit(p.ctr);
 }
 
 }  // namespace EGS_FMT_NS

@@ -14,7 +14,6 @@
 // GPU variant; the output is the same least fixpoint the reference solvers
 // compute (solver_seq.cpp:124-212, solver_par.cpp:126-435).
 #include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <chrono>
@@ -32,6 +31,7 @@
 
 #include "egs_build.cuh"
 #include "egs_gpu.h"
+#include "egs_scan.cuh"
 #include "egs_types.cuh"
 
 // The solve kernels, compiled once per edge-record format (egs_kern.cu):
@@ -39,11 +39,9 @@
 namespace egs {
 namespace e8 {
 const void* solve_kernel(int vbits);
-const void* part_kernel(int vbits);
 }  // namespace e8
 namespace e4 {
 const void* solve_kernel(int vbits);
-const void* part_kernel(int vbits);
 }  // namespace e4
 }  // namespace egs
 
@@ -168,11 +166,7 @@ struct egs_ctx {
   uint32_t* frb[2] = {nullptr, nullptr};  // frontier membership bitmaps
   uint32_t* rbm[2] = {nullptr, nullptr};
   uint32_t* cbm[2] = {nullptr, nullptr};
-  uint32_t* cand = nullptr;  // certificate candidate bitmap (n_pad / 32 words)
-  // multi-GPU sparse exchange buffers (egs_part_pack / egs_part_unpack)
-  uint64_t* xsend = nullptr;
-  uint64_t* xrecv = nullptr;
-  uint32_t* xcount = nullptr;  // [0]: pack cursor; [1..world]: received counts
+  uint32_t* cand = nullptr;  // certificate candidate bitmap (own vertices)
   uint32_t* longcol = nullptr;
   uint32_t* fr[2] = {nullptr, nullptr};
   void* stage = nullptr;
@@ -184,11 +178,20 @@ struct egs_ctx {
   cudaEvent_t ev[2] = {nullptr, nullptr};
   int grid = 0;
   bool solved = false;
-  // multi-GPU partition (egs_part_*): this rank's range of relabelled ids and
-  // the padded length of the replicated arrays (world * slice)
+  // multi-GPU partition (egs_part_*): this rank's range of relabelled ids,
+  // its edge count, and the replicated state (f, chg[2], rbm[2], XSync) in
+  // one IPC-exportable allocation `xbuf` with the same layout on every rank
   int rank = 0, world = 1;
-  uint32_t slice = 0, n_pad = 0, own_lo = 0, own_hi = 0;
+  uint32_t own_lo = 0, own_hi = 0;
+  uint64_t m_own = 0;
   int full_grid = 0;
+  char* xbuf = nullptr;
+  size_t xbytes = 0;
+  char* xpeer[egs::kMaxRanks] = {};
+  bool xpeer_ipc[egs::kMaxRanks] = {};  // opened with cudaIpcOpenMemHandle
+  egs::XSync* xsync = nullptr;
+  unsigned int epoch = 0;  // cross-rank barriers passed (same on every rank)
+  bool connected = false;
 
   egs::Graph graph() const {
     egs::Graph g{};
@@ -255,10 +258,20 @@ void ctx_free(egs_ctx* c) {
   if (!c) return;
   StepTimer tm(c->stream);
   if (c->device >= 0) cudaSetDevice(c->device);
-  void* ptrs[] = {c->off,    c->edge,   c->coff, c->csrc,  c->perm, c->inv,
-                  c->f,      c->wit,    c->chg[0], c->chg[1], c->frb[0], c->frb[1],
-                  c->fr[0],  c->fr[1],  c->stage, c->scratch, c->ctr, c->rbm[0], c->rbm[1], c->cbm[0], c->cbm[1], c->cand, c->xsend, c->xrecv, c->xcount, c->trace, c->longcol,
-                  c->f64};
+  // (the replicated state of a multi-GPU rank lives in xbuf: cudaFree'd below)
+  const bool in_x = c->xbuf != nullptr;
+  void* ptrs[] = {c->off,  c->edge,  c->coff,  c->csrc, c->perm,    c->inv,
+                  in_x ? nullptr : c->f, c->wit, in_x ? nullptr : c->chg[0],
+                  in_x ? nullptr : c->chg[1], c->frb[0], c->frb[1],
+                  c->fr[0], c->fr[1], c->stage, c->scratch, c->ctr,
+                  in_x ? nullptr : c->rbm[0], in_x ? nullptr : c->rbm[1], c->cbm[0], c->cbm[1],
+                  c->cand, c->trace, c->longcol, c->f64};
+  for (int q = 0; q < egs::kMaxRanks; ++q)
+    if (c->xpeer_ipc[q] && c->xpeer[q]) cudaIpcCloseMemHandle(c->xpeer[q]);
+  if (c->xbuf) {
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    cudaFree(c->xbuf);
+  }
   if (c->stream) {
     for (void* p : ptrs) dfree(p, c->stream);
     cudaStreamSynchronize(c->stream);
@@ -297,9 +310,6 @@ void validate_opts(const egs_gpu_opts& o) {
 const void* solve_kernel(const egs_ctx* c) {
   return c->tbits ? egs::e4::solve_kernel(c->vbits) : egs::e8::solve_kernel(c->vbits);
 }
-const void* part_kernel(const egs_ctx* c) {
-  return c->tbits ? egs::e4::part_kernel(c->vbits) : egs::e8::part_kernel(c->vbits);
-}
 size_t rec_bytes(const egs_ctx* c) { return c->tbits ? 4 : 8; }
 // light-row phases staged through TMA tiles by default, measured per phase
 // (profiles/README.md): round 1 and the certificate pass stream whole rows
@@ -323,6 +333,21 @@ void* pinned_stage(uint64_t bytes) {
     g_stage_cap = bytes;
   }
   return g_stage;
+}
+
+// Exclusive prefix sum on the device (egs_scan.cuh): out[i] = in[0] + ... +
+// in[i-1]; in place allowed.  Temporaries from the stream-ordered pool.
+template <class T, class In>
+void dev_excl_scan(const In* in, T* out, uint64_t n, cudaStream_t s, int sms) {
+  if (n == 0) return;
+  const uint64_t nt = (n + egs::kScanTile - 1) / egs::kScanTile;
+  DevBuf d_ts;
+  T* ts = d_ts.alloc<T>(nt);
+  const uint32_t grid = (uint32_t)std::min<uint64_t>(nt, (uint64_t)sms * 8);
+  egs::k_scan_reduce<T, In><<<grid, egs::kScanThreads, 0, s>>>(in, n, ts, nt);
+  egs::k_scan_tiles<T><<<1, 1024, 0, s>>>(ts, nt);
+  egs::k_scan_down<T, In><<<grid, egs::kScanThreads, 0, s>>>(in, out, n, ts, nt);
+  CK(cudaGetLastError());
 }
 
 // Weights: host threads narrow int64 -> W (int8 / int16 / int32, the
@@ -422,7 +447,7 @@ bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint3
     egs::k_relabel_weights<W><<<grid_for((uint64_t)(rows[k + 1] - rows[k]) * 4, c->num_sms),
                                 256, 0, sw>>>(rows[k], rows[k + 1], off64, wd, c->perm, c->off,
                                               c->edge, c->tbits, lw.list + (size_t)k * lw.cap,
-                                              lw.cnt + k);
+                                              lw.cnt + k, c->own_lo, c->own_hi);
     egs::k_relabel_weights_long<W><<<2 * c->num_sms, 256, 0, sw>>>(
         lw.list + (size_t)k * lw.cap, lw.cnt + k, off64, wd, c->perm, c->off, c->edge, c->tbits);
     CK(cudaGetLastError());
@@ -440,15 +465,19 @@ bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint3
 // as it lands, then sorts the transpose while the weights are still on the
 // wire; the aux stream writes each weight chunk as it lands.  The result is
 // ready when the last weight chunk is (PCIe-bound).
-void build_arena(egs_ctx* c, const egs_arena_view* a) {
+// Several ranks (`plan` set): the relabelling is the plan's rank-major order
+// and this rank keeps its own rows [own_lo, own_hi) only (m_own edges), with
+// the transpose of those rows (the predecessors it activates).
+void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan) {
   StepTimer tm(c->stream);
   const uint32_t n = c->n;
   const uint64_t m = c->m;
+  const uint64_t mo = c->m_own;  // edges stored here (m with one rank)
   bool h_stage_bad = false;
   cudaStream_t s = c->stream, sc = c->copy_stream, sw = c->aux_stream;
   const int sms = c->num_sms;
-  DevBuf d_off64, d_dst, d_wn, d_owner, d_key, d_keys, d_val, d_misc, d_tmp, d_ck0, d_cv0,
-      d_ck1, d_long;
+  DevBuf d_off64, d_dst, d_wn, d_owner, d_key, d_tcount, d_misc, d_tmp, d_ck0, d_cv0, d_ck1,
+      d_long;
   uint64_t* off64 = d_off64.alloc<uint64_t>((size_t)n + 1);
   uint32_t* dst = d_dst.alloc<uint32_t>(m);
   void* wn = d_wn.alloc<int32_t>(m);  // narrowed weights (int8/16/32)
@@ -461,13 +490,13 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   const LongRows lt{long_lists, misc + 32, long_cap};
   const LongRows lw{long_lists + (size_t)16 * long_cap, misc + 48, long_cap};
   uint8_t* key = d_key.alloc<uint8_t>(n);
-  uint8_t* keys_sorted = d_keys.alloc<uint8_t>(n);
-  uint32_t* val = d_val.alloc<uint32_t>(n);
+  const uint32_t vtiles = (uint32_t)((n + egs::kScanTile - 1) / egs::kScanTile);
+  uint32_t* tcount = d_tcount.alloc<uint32_t>((size_t)egs::kNumClasses * vtiles);
   c->inv = dalloc<uint32_t>(n);
   uint32_t* inv = c->inv;
-  uint32_t* ck0 = d_ck0.alloc<uint32_t>(m);
-  uint32_t* cv0 = d_cv0.alloc<uint32_t>(m);
-  uint32_t* ck1 = d_ck1.alloc<uint32_t>(m);
+  uint32_t* ck0 = d_ck0.alloc<uint32_t>(mo);
+  uint32_t* cv0 = d_cv0.alloc<uint32_t>(mo);
+  uint32_t* ck1 = d_ck1.alloc<uint32_t>(mo);
   c->perm = dalloc<uint32_t>(n);
   c->off = dalloc<uint32_t>((size_t)n + 1);
   // packed 4-byte records when every weight fits beside the target bits
@@ -479,8 +508,8 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
     c->tbits = (!wide && tb <= 24 && a->max_abs_weight < (1ll << (31 - tb))) ? tb : 0;
   }
   // +16 bytes: 16-byte rounding of TMA spans
-  c->edge = dalloc<uint8_t>(m * rec_bytes(c) + 16);
-  c->csrc = dalloc<uint32_t>(m);
+  c->edge = dalloc<uint8_t>(mo * rec_bytes(c) + 16);
+  c->csrc = dalloc<uint32_t>(mo);
   c->coff = dalloc<uint32_t>((size_t)n + 1);
   CK(cudaMemsetAsync(misc, 0, 64 * sizeof(unsigned int), s));
   tm.mark("pool allocations");
@@ -524,22 +553,31 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
     CK(cudaEventRecord(ex[k], sc));
   }
 
-  // vertices: class keys, stable partition by class, relabelled offsets
+  // vertices: class keys and per-tile class counts, their scan, the stable
+  // class placement (mapped through the plan with several ranks), row
+  // lengths in the new order and their scan = the relabelled offsets
   CK(cudaStreamWaitEvent(s, e_vert, 0));
-  egs::k_classify<<<grid_for(n, sms), 256, 0, s>>>(n, off64, owner, key, val, misc);
+  const uint32_t vgrid = std::min<uint32_t>(vtiles, (uint32_t)sms * 8);
+  egs::k_class_tiles<<<vgrid, egs::kScanThreads, 0, s>>>(n, off64, owner, key, tcount, vtiles,
+                                                          misc);
   CK(cudaGetLastError());
-  size_t tmp_bytes = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, keys_sorted, val, inv, n, 0, 3, s));
-  void* tmp = d_tmp.alloc<uint8_t>(tmp_bytes);
-  CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, keys_sorted, val, inv, n, 0, 3, s));
-  d_tmp.release();
-  egs::k_permute<<<grid_for(n, sms), 256, 0, s>>>(n, inv, off64, c->perm, c->off);
+  dev_excl_scan<uint32_t>(tcount, tcount, (uint64_t)egs::kNumClasses * vtiles, s, sms);
+  {
+    egs::PlanDev pl{};
+    pl.world = plan ? plan->world : 1;
+    if (plan)
+      for (int k = 0; k < egs::kNumClasses; ++k)
+        for (uint32_t r = 0; r < plan->world; ++r) {
+          for (int j = 0; j <= 1; ++j) pl.piece[k][r + j] = plan->piece[k][r + j];
+          pl.cls_lo[r][k] = plan->class_lo[r][k];
+        }
+    egs::k_class_place<<<vgrid, egs::kScanThreads, 0, s>>>(n, key, tcount, vtiles, pl, c->perm,
+                                                            inv);
+  }
+  egs::k_row_lengths<<<grid_for(n, sms), 256, 0, s>>>(n, inv, off64, c->own_lo, c->own_hi,
+                                                      c->off);
   CK(cudaGetLastError());
-  tmp_bytes = 0;
-  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, c->off, c->off, (int64_t)n + 1, s));
-  tmp = d_tmp.alloc<uint8_t>(tmp_bytes);
-  CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, c->off, c->off, (int64_t)n + 1, s));
-  d_tmp.release();
+  dev_excl_scan<uint32_t>(c->off, c->off, (uint64_t)n + 1, s, sms);
   CK(cudaEventRecord(e_perm, s));
   tm.mark("vertices (classify, sort, offsets)");
 
@@ -548,7 +586,7 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
     CK(cudaStreamWaitEvent(s, ex[k], 0));
     egs::k_relabel_targets<<<grid_for((uint64_t)(rows[k + 1] - rows[k]) * 4, sms), 256, 0, s>>>(
         n, rows[k], rows[k + 1], off64, dst, c->perm, c->off, c->edge, c->tbits, ck0, cv0,
-        misc + 16, lt.list + (size_t)k * lt.cap, lt.cnt + k);
+        misc + 16, lt.list + (size_t)k * lt.cap, lt.cnt + k, c->own_lo, c->own_hi);
     egs::k_relabel_targets_long<<<2 * sms, 256, 0, s>>>(
         n, lt.list + (size_t)k * lt.cap, lt.cnt + k, off64, dst, c->perm, c->off, c->edge,
         c->tbits, ck0, cv0, misc + 16);
@@ -557,12 +595,12 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   }
 
   // transpose: sort the (dst, src) pairs by dst while the weights stream in
-  tmp_bytes = 0;
+  size_t tmp_bytes = 0;
   const int kb = bits_for(n);
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, ck0, ck1, cv0, c->csrc, m, 0, kb, s));
-  tmp = d_tmp.alloc<uint8_t>(tmp_bytes);
-  CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, ck0, ck1, cv0, c->csrc, m, 0, kb, s));
-  egs::k_col_offsets<<<grid_for(m + 1, sms), 256, 0, s>>>(n, m, ck1, c->coff);
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, ck0, ck1, cv0, c->csrc, mo, 0, kb, s));
+  void* tmp = d_tmp.alloc<uint8_t>(tmp_bytes);
+  CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, ck0, ck1, cv0, c->csrc, mo, 0, kb, s));
+  egs::k_col_offsets<<<grid_for(mo + 1, sms), 256, 0, s>>>(n, mo, ck1, c->coff);
   CK(cudaGetLastError());
 
   CK(cudaStreamWaitEvent(sw, e_perm, 0));
@@ -586,8 +624,7 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
   d_wn.release();
   d_owner.release();
   d_key.release();
-  d_keys.release();
-  d_val.release();
+  d_tcount.release();
   d_ck0.release();
   d_cv0.release();
   d_ck1.release();
@@ -608,13 +645,21 @@ void build_arena(egs_ctx* c, const egs_arena_view* a) {
     throw Fail(a->max_abs_weight > 2147483647LL ? EGS_ERR_UNSUPPORTED : EGS_ERR_INVALID_CONFIG,
                "edge weight outside int32 on the device path, or beyond max_abs_weight");
   if (bad & 2u) throw Fail(EGS_ERR_INVALID_CONFIG, "edge target out of range");
-  c->rb[0] = 0;
-  for (int k = 0; k < egs::kNumClasses; ++k) c->rb[k + 1] = c->rb[k] + h_misc[k];
+  if (plan) {  // this rank's class ranges
+    for (int k = 0; k <= egs::kNumClasses; ++k) c->rb[k] = plan->class_lo[c->rank][k];
+  } else {
+    c->rb[0] = 0;
+    for (int k = 0; k < egs::kNumClasses; ++k) c->rb[k + 1] = c->rb[k] + h_misc[k];
+  }
 }
 
 egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_stats* st,
-                    int rank = 0, int world = 1) {
-  if (world == 1) validate_opts(opts);
+                    int rank = 0, int world = 1, const egs_part_plan* plan = nullptr) {
+  {
+    egs_gpu_opts o1 = opts;
+    if (world > 1) o1.n_gpus = 1;  // (n_gpus == world checked by egs_part_create)
+    validate_opts(o1);
+  }
   if (!a) throw Fail(EGS_ERR_INVALID_CONFIG, "null arena");
   if (a->num_edges >= 0xFFFFFFFFull)
     throw Fail(EGS_ERR_UNSUPPORTED, "arenas with >= 2^32 edges are not supported on the device");
@@ -672,41 +717,51 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     c->scratch = dalloc<egs::Scratch>(1);
     c->rank = rank;
     c->world = world;
-    c->slice = (uint32_t)((((uint64_t)n + world - 1) / world + 31) / 32 * 32);
-    c->n_pad = world == 1 ? n : c->slice * (uint32_t)world;
-    c->own_lo = world == 1 ? 0 : std::min<uint32_t>(n, c->slice * (uint32_t)rank);
-    c->own_hi = world == 1 ? n : std::min<uint32_t>(n, c->slice * (uint32_t)(rank + 1));
-    c->f = dalloc<uint8_t>((size_t)std::max<uint32_t>(c->n_pad, 1) * vsz);
-    c->chg[0] = dalloc<uint32_t>(words);
-    c->chg[1] = dalloc<uint32_t>(words);
+    c->own_lo = plan ? plan->rank_lo[rank] : 0;
+    c->own_hi = plan ? plan->rank_lo[rank + 1] : n;
+    c->m_own = plan ? plan->edges[rank] : c->m;
+    if (world == 1) {
+      c->f = dalloc<uint8_t>((size_t)std::max<uint32_t>(n, 1) * vsz);
+      c->chg[0] = dalloc<uint32_t>(words);
+      c->chg[1] = dalloc<uint32_t>(words);
+      c->rbm[0] = dalloc<uint32_t>(words);
+      c->rbm[1] = dalloc<uint32_t>(words);
+    } else {
+      // the replicated state: plain cudaMalloc (IPC-exportable), one block
+      auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+      const size_t fb = up(std::max<size_t>(n, 1) * vsz), wb = up(std::max<size_t>(words, 1) * 4);
+      c->xbytes = fb + 4 * wb + up(sizeof(egs::XSync));
+      void* xb = nullptr;
+      CK(cudaMalloc(&xb, c->xbytes));
+      c->xbuf = static_cast<char*>(xb);
+      CK(cudaMemsetAsync(c->xbuf, 0, c->xbytes, c->stream));
+      c->f = c->xbuf;
+      c->chg[0] = reinterpret_cast<uint32_t*>(c->xbuf + fb);
+      c->chg[1] = reinterpret_cast<uint32_t*>(c->xbuf + fb + wb);
+      c->rbm[0] = reinterpret_cast<uint32_t*>(c->xbuf + fb + 2 * wb);
+      c->rbm[1] = reinterpret_cast<uint32_t*>(c->xbuf + fb + 3 * wb);
+      c->xsync = reinterpret_cast<egs::XSync*>(c->xbuf + fb + 4 * wb);
+      c->xpeer[rank] = c->xbuf;
+    }
     c->frb[0] = dalloc<uint32_t>(words);
     c->frb[1] = dalloc<uint32_t>(words);
-    c->rbm[0] = dalloc<uint32_t>(words);
-    c->rbm[1] = dalloc<uint32_t>(words);
     c->cbm[0] = dalloc<uint32_t>(words);
     c->cbm[1] = dalloc<uint32_t>(words);
-    c->cand = dalloc<uint32_t>(std::max<size_t>(words, ((size_t)c->n_pad + 31) / 32));
-    CK(cudaMemsetAsync(c->cand, 0, std::max<size_t>(words, ((size_t)c->n_pad + 31) / 32) * 4,
-                       c->stream));
+    c->cand = dalloc<uint32_t>(words);
+    CK(cudaMemsetAsync(c->cand, 0, std::max<size_t>(words, 1) * 4, c->stream));
     // at most m / kLongCol columns are longer than kLongCol
     c->longcol = dalloc<uint32_t>(2 * (a->num_edges / egs::kLongCol + 1));
     c->fr[0] = dalloc<uint32_t>(n);
     c->fr[1] = dalloc<uint32_t>(n);
-    c->stage = dalloc<uint8_t>((size_t)std::max<uint32_t>(c->n_pad, 1) * vsz);
+    c->stage = dalloc<uint8_t>((size_t)std::max<uint32_t>(n, 1) * vsz);
     // dense commits read every slot of a bitmap word (egs_solve.cuh
     // commit_stage_loads): slots never staged are read, and must be defined
-    CK(cudaMemsetAsync(c->stage, 0, (size_t)std::max<uint32_t>(c->n_pad, 1) * vsz, c->stream));
+    CK(cudaMemsetAsync(c->stage, 0, (size_t)std::max<uint32_t>(n, 1) * vsz, c->stream));
     c->f64 = dalloc<int64_t>(n);
-    if (world > 1) {
-      const size_t ew = c->vbits / 32;  // u64 words per entry
-      c->xsend = dalloc<uint64_t>((size_t)c->slice * ew + 1);
-      c->xrecv = dalloc<uint64_t>((size_t)c->slice * world * ew + 1);
-      c->xcount = dalloc<uint32_t>((size_t)world + 1);
-    }
     tm0.s = c->stream;
     tm0.mark("create: state buffers");
     if (n > 0) {
-      build_arena(c, a);
+      build_arena(c, a, plan);
     } else {
       c->off = dalloc<uint32_t>(1);
       c->coff = dalloc<uint32_t>(1);
@@ -721,9 +776,6 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     int per_sm = 0;
     const void* kfn = solve_kernel(c);
     CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)egs::kLiftSmemBytes));
-    const void* pfn = part_kernel(c);
-    CK(cudaFuncSetAttribute(pfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)egs::kLiftSmemBytes));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, egs::kBlock,
                                                      egs::kLiftSmemBytes));
@@ -833,6 +885,15 @@ egs::SolveParams<V> make_params(egs_ctx* c, unsigned long long* budget_out) {
   p.own_lo = c->world == 1 ? 0 : c->own_lo;
   p.own_hi = c->world == 1 ? n : c->own_hi;
   p.debug = o.debug_checks ? 1 : 0;
+  p.world = c->world;
+  p.rank = c->rank;
+  if (c->world > 1) {
+    p.xbase = c->xbuf;
+    for (int q = 0; q < c->world; ++q) p.xpeer[q] = c->xpeer[q];
+    p.xsync = c->xsync;
+    p.epoch0 = c->epoch;
+    p.xwait_ns = (unsigned long long)((o.timeout_seconds > 0 ? o.timeout_seconds : 60.0) * 1e9);
+  }
   if (budget_out) *budget_out = budget;
   return p;
 }
@@ -873,7 +934,8 @@ void fill_stats(egs_ctx* c, const unsigned long long* h, double ms, egs_gpu_stat
   // Algorithmic bytes: what each phase must move at least.
   // round 1 (counted as one dense round: n visits, m edges) reads records
   // but neither f(v) nor f(t): drop those gathers from the lift formula
-  const double r1 = (double)c->m * sv + (double)n * sv;
+  // (a partition rank: its own rows and vertices)
+  const double r1 = (double)c->m_own * sv + (double)(c->own_hi - c->own_lo) * sv;
   auto lift_with = [&](double rec) {
     return (double)st->visits * sv + (double)st->witness_checks * (rec + sv) +
            (double)st->applications * 8 + (double)st->edges_relaxed * (rec + sv) +
@@ -921,7 +983,9 @@ void debug_verify(egs_ctx* c) {
   CK(cudaMemcpyAsync(&bad, &c->scratch->bad, 4, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (bad) throw Fail(EGS_ERR_INTERNAL, "measure decreased across a round");
-  if (h[0])
+  // (a partition rank holds its own rows only: the fixpoint test is the
+  // single-GPU context's)
+  if (h[0] && c->world == 1)
     throw Fail(EGS_ERR_INTERNAL,
                std::to_string(h[0]) + " vertices are not a fixpoint of the lift after the solve");
 }
@@ -935,9 +999,11 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
   egs::SolveParams<V> p = make_params<V>(c, &budget);
 
   CK(cudaEventRecord(c->ev[0], s));
-  CK(cudaMemsetAsync(c->f, 0, (size_t)n * sizeof(V), s));
-  CK(cudaMemsetAsync(c->chg[0], 0, words * 4, s));
-  CK(cudaMemsetAsync(c->chg[1], 0, words * 4, s));
+  if (c->world == 1) {  // several ranks: k_solve resets the replicated state itself
+    CK(cudaMemsetAsync(c->f, 0, (size_t)n * sizeof(V), s));
+    CK(cudaMemsetAsync(c->chg[0], 0, words * 4, s));
+    CK(cudaMemsetAsync(c->chg[1], 0, words * 4, s));
+  }
   CK(cudaMemsetAsync(c->frb[0], 0, words * 4, s));
   CK(cudaMemsetAsync(c->frb[1], 0, words * 4, s));
   CK(cudaMemsetAsync(c->cbm[0], 0, words * 4, s));
@@ -955,6 +1021,7 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
   CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
   const unsigned long long* h = c->h_ctr;
   c->solved = h[egs::kStatus] == 0;
+  c->epoch = (unsigned int)h[egs::kEpoch];
   if (st) fill_stats<V>(c, h, ms, st);
   if (c->trace) {  // EGS_TRACE=1: one line per phase on stderr
     std::vector<unsigned long long> tr(egs::kTraceCap);
@@ -969,6 +1036,10 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
                    fine[f < 6 ? f : 0], (tr[k] & ((1ull << 56) - 1)) * 1e-3);
     }
     CK(cudaMemset(c->trace, 0, egs::kTraceCap * 8));
+  }
+  if (h[egs::kStatus] == 7) {
+    c->connected = false;  // the ranks' barrier epochs no longer agree
+    throw Fail(EGS_ERR_CUDA, "a peer rank did not reach a cross-rank barrier in time");
   }
   if (h[egs::kStatus] == 2) throw Fail(EGS_ERR_TIMEOUT, "solve timed out");
   if (h[egs::kStatus] == 5)
@@ -1010,7 +1081,7 @@ template <class V>
 int64_t write_solution_dev(egs_ctx* c, char* buf, size_t cap) {
   cudaStream_t s = c->stream;
   const uint32_t n = c->n;
-  DevBuf d_strat, d_len, d_pos, d_text, d_err, d_tmp;
+  DevBuf d_strat, d_len, d_pos, d_text, d_err;
   uint32_t* strat = d_strat.alloc<uint32_t>(n);
   unsigned long long* len = d_len.alloc<unsigned long long>(n);
   unsigned long long* pos = d_pos.alloc<unsigned long long>(n);
@@ -1021,10 +1092,7 @@ int64_t write_solution_dev(egs_ctx* c, char* buf, size_t cap) {
                                                                            c->inv, strat, err);
   egs::k_line_len<V><<<grid_for(n, c->num_sms), 256, 0, s>>>(n, f, c->perm, strat, len);
   CK(cudaGetLastError());
-  size_t tmp_bytes = 0;
-  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, len, pos, n, s));
-  void* tmp = d_tmp.alloc<uint8_t>(tmp_bytes);
-  CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, len, pos, n, s));
+  dev_excl_scan<unsigned long long>(len, pos, n, s, c->num_sms);
   unsigned long long last[2] = {0, 0};
   int h_err = 0;
   CK(cudaMemcpyAsync(&last[0], pos + (n - 1), 8, cudaMemcpyDeviceToHost, s));
@@ -1110,54 +1178,136 @@ int guarded(F&& fn) {
 
 struct egs_part {
   egs_ctx* c = nullptr;
+  egs_part_plan plan{};
 };
 
 namespace {
 
-template <class V>
-void part_step(egs_ctx* c, int step, int parity, uint64_t* counts) {
-  cudaStream_t s = c->stream;
-  egs::SolveParams<V> p = make_params<V>(c, nullptr);
-  CK(cudaMemsetAsync(c->scratch, 0, sizeof(egs::Scratch), s));
-  // a prune step marks its removals in rbm[0]: start it empty, so the
-  // removed set of the step is exactly what egs_part_pack sends
-  if (step == EGS_STEP_CERT_PRUNE)
-    CK(cudaMemsetAsync(c->rbm[0], 0, ((size_t)c->n + 31) / 32 * 4, s));
-  void* args[] = {&p, &step, &parity};
-  const void* fn = part_kernel(c);
-  CK(cudaLaunchKernel(fn, dim3(c->full_grid), dim3(egs::kBlock), args, egs::kLiftSmemBytes, s));
-  CK(cudaGetLastError());
-  unsigned int sums[4] = {0, 0, 0, 0};
-  CK(cudaMemcpyAsync(sums, c->scratch->sum[0], sizeof(sums), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  if (counts) {
-    counts[0] = sums[0];
-    counts[1] = sums[1];
+// The partition plan (include/egs_gpu.h egs_part_plan): every (owner,
+// degree) class -- the classes of the relabelling, egs_scan.cuh -- split
+// into `world` pieces by out-edges, the first vertex of piece r being the
+// first class member with at least E_class * r / world edges before it
+// (edge_balanced_bounds, solver_par.cpp:62-80); rank r's block is its pieces
+// of the six classes, class-sorted.  Two host passes over the offsets:
+// per-chunk class counts and edges, then only the chunks a boundary falls in
+// are walked again.
+void plan_compute(const egs_arena_view* a, int world, egs_part_plan* pl) {
+  if (world < 1 || world > egs::kMaxRanks)
+    throw Fail(EGS_ERR_INVALID_CONFIG, "world must be in [1, " + std::to_string(egs::kMaxRanks) + "]");
+  std::memset(pl, 0, sizeof(*pl));
+  const uint32_t n = a->num_vertices;
+  pl->world = (uint32_t)world;
+  pl->num_vertices = n;
+  constexpr int C = egs::kNumClasses;
+  auto cls = [&](uint32_t v) {
+    const uint64_t deg = a->csr_offsets[v + 1] - a->csr_offsets[v];
+    return (a->owners[v] ? 3 : 0) + (deg <= egs::kLightMax ? 0 : deg <= egs::kMediumMax ? 1 : 2);
+  };
+  const unsigned T = n > (1u << 20) ? std::max(1u, std::min(16u, std::thread::hardware_concurrency())) : 1u;
+  std::vector<uint64_t> cnt((size_t)T * C, 0), edg((size_t)T * C, 0);
+  auto chunk = [&](unsigned t) { return std::make_pair((uint64_t)n * t / T, (uint64_t)n * (t + 1) / T); };
+  {
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < T; ++t)
+      pool.emplace_back([&, t] {
+        const auto [lo, hi] = chunk(t);
+        for (uint64_t v = lo; v < hi; ++v) {
+          const int k = cls((uint32_t)v);
+          cnt[t * C + k] += 1;
+          edg[t * C + k] += a->csr_offsets[v + 1] - a->csr_offsets[v];
+        }
+      });
+    for (auto& th : pool) th.join();
+  }
+  uint64_t ctot[C] = {}, etot[C] = {};
+  for (unsigned t = 0; t < T; ++t)
+    for (int k = 0; k < C; ++k) ctot[k] += cnt[t * C + k], etot[k] += edg[t * C + k];
+  for (int k = 0; k < C; ++k) {
+    pl->piece[k][0] = 0;
+    pl->piece[k][world] = (uint32_t)ctot[k];
+    for (int r = 1; r < world; ++r) {
+      const uint64_t target = (etot[k] * (uint64_t)r + world - 1) / world;  // ceil
+      // the chunk the boundary falls in: cumulative edges before it < target
+      uint64_t pos = 0, cum = 0;
+      unsigned t = 0;
+      for (; t < T; ++t) {
+        if (cum + edg[t * C + k] >= target) break;
+        cum += edg[t * C + k];
+        pos += cnt[t * C + k];
+      }
+      if (t == T) {
+        pl->piece[k][r] = (uint32_t)ctot[k];
+        continue;
+      }
+      const auto [lo, hi] = chunk(t);
+      for (uint64_t v = lo; v < hi && cum < target; ++v)
+        if (cls((uint32_t)v) == k) {
+          cum += a->csr_offsets[v + 1] - a->csr_offsets[v];
+          ++pos;
+        }
+      pl->piece[k][r] = (uint32_t)pos;
+    }
+  }
+  uint32_t id = 0;
+  for (int r = 0; r < world; ++r) {
+    pl->rank_lo[r] = id;
+    uint64_t e = 0;
+    for (int k = 0; k < C; ++k) {
+      pl->class_lo[r][k] = id;
+      id += pl->piece[k][r + 1] - pl->piece[k][r];
+    }
+    pl->class_lo[r][C] = id;
+    (void)e;
+  }
+  pl->rank_lo[world] = id;
+  // edges per rank: the class pieces' edges (a third pass only over the
+  // piece boundaries' chunks would do; the whole pass is cheap next to the
+  // upload it precedes)
+  {
+    std::vector<uint64_t> er((size_t)T * world, 0);
+    std::vector<std::thread> pool;
+    // class positions at each chunk start
+    std::vector<uint64_t> cpos((size_t)T * C, 0);
+    for (unsigned t = 1; t < T; ++t)
+      for (int k = 0; k < C; ++k) cpos[t * C + k] = cpos[(t - 1) * C + k] + cnt[(t - 1) * C + k];
+    for (unsigned t = 0; t < T; ++t)
+      pool.emplace_back([&, t] {
+        const auto [lo, hi] = chunk(t);
+        uint64_t p[C];
+        for (int k = 0; k < C; ++k) p[k] = cpos[t * C + k];
+        for (uint64_t v = lo; v < hi; ++v) {
+          const int k = cls((uint32_t)v);
+          int r = 0;
+          while (r + 1 < world && p[k] >= pl->piece[k][r + 1]) ++r;
+          er[(size_t)t * world + r] += a->csr_offsets[v + 1] - a->csr_offsets[v];
+          ++p[k];
+        }
+      });
+    for (auto& th : pool) th.join();
+    for (unsigned t = 0; t < T; ++t)
+      for (int r = 0; r < world; ++r) pl->edges[r] += er[(size_t)t * world + r];
   }
 }
 
-void part_reset(egs_ctx* c) {
-  cudaStream_t s = c->stream;
-  const size_t words = ((size_t)c->n + 31) / 32;
-  const size_t vsz = c->vbits / 8;
-  CK(cudaMemsetAsync(c->f, 0, (size_t)std::max<uint32_t>(c->n_pad, 1) * vsz, s));
-  CK(cudaMemsetAsync(c->chg[0], 0, words * 4, s));
-  CK(cudaMemsetAsync(c->chg[1], 0, words * 4, s));
-  CK(cudaMemsetAsync(c->frb[0], 0, words * 4, s));
-  CK(cudaMemsetAsync(c->frb[1], 0, words * 4, s));
-  CK(cudaMemsetAsync(c->cbm[0], 0, words * 4, s));
-  CK(cudaMemsetAsync(c->cbm[1], 0, words * 4, s));
-  CK(cudaMemsetAsync(c->ctr, 0, egs::kNumCounters * sizeof(unsigned long long), s));
-  CK(cudaStreamSynchronize(s));
-  c->solved = true;
+// Grid of a rank's persistent kernel: ranks sharing a device split it.
+void part_grid(egs_ctx* c, int ranks_on_device) {
+  if (ranks_on_device <= 1) return;
+  c->grid = std::max(1, std::min(c->grid, c->full_grid / ranks_on_device));
 }
 
 }  // namespace
 
 extern "C" {
 
+int egs_part_plan_compute(const egs_arena_view* arena, int32_t world, egs_part_plan* plan) {
+  return guarded([&] {
+    if (!arena || !plan) throw Fail(EGS_ERR_INVALID_CONFIG, "null argument");
+    plan_compute(arena, world, plan);
+  });
+}
+
 int egs_part_create(const egs_arena_view* arena, const egs_gpu_opts* opts, int32_t rank,
-                    int32_t world, egs_part** out, egs_part_layout* layout,
+                    int32_t world, egs_part** out, egs_part_plan* plan_out,
                     egs_gpu_stats* stats) {
   return guarded([&] {
     egs_gpu_opts o;
@@ -1165,135 +1315,103 @@ int egs_part_create(const egs_arena_view* arena, const egs_gpu_opts* opts, int32
       o = *opts;
     else
       egs_gpu_opts_default(&o);
-    if (world < 1 || rank < 0 || rank >= world)
-      throw Fail(EGS_ERR_INVALID_CONFIG, "rank must be in [0, world)");
+    if (!arena || !out) throw Fail(EGS_ERR_INVALID_CONFIG, "null argument");
+    if (world < 1 || world > egs::kMaxRanks || rank < 0 || rank >= world)
+      throw Fail(EGS_ERR_INVALID_CONFIG, "rank must be in [0, world), world in [1, 8]");
     if (o.n_gpus != world) throw Fail(EGS_ERR_INVALID_CONFIG, "opts.n_gpus must equal world");
     if (stats) std::memset(stats, 0, sizeof(*stats));
-    egs_ctx* c = ctx_create(arena, o, stats, rank, world);
-    egs_part* p = new egs_part();
-    p->c = c;
+    auto* p = new egs_part();
     try {
-      part_reset(c);
+      plan_compute(arena, world, &p->plan);
+      p->c = ctx_create(arena, o, stats, rank, world, &p->plan);
     } catch (...) {
-      ctx_free(c);
       delete p;
       throw;
     }
-    if (layout) {
-      layout->num_vertices = c->n;
-      layout->slice = c->slice;
-      layout->padded = c->n_pad;
-      layout->own_lo = c->own_lo;
-      layout->own_hi = c->own_hi;
-      layout->value_bytes = (uint32_t)(c->vbits / 8);
-      layout->f_dev = (uint64_t)(uintptr_t)c->f;
-      layout->stage_dev = (uint64_t)(uintptr_t)c->stage;
-      layout->cand_dev = (uint64_t)(uintptr_t)c->cand;
-      layout->send_dev = (uint64_t)(uintptr_t)c->xsend;
-      layout->recv_dev = (uint64_t)(uintptr_t)c->xrecv;
-      layout->entry_bytes = (uint32_t)(c->vbits / 4);
-    }
+    if (world == 1) p->c->connected = true;
+    if (plan_out) *plan_out = p->plan;
     *out = p;
   });
 }
 
-int egs_part_step(egs_part* part, int32_t step, int32_t parity, uint64_t* counts) {
+int egs_part_export(egs_part* part, void* handle) {
   return guarded([&] {
-    if (!part) throw Fail(EGS_ERR_INVALID_CONFIG, "null partition");
-    if (step < EGS_STEP_ROUND1 || step > EGS_STEP_CERT_APPLY)
-      throw Fail(EGS_ERR_INVALID_CONFIG, "unknown step");
+    if (!part || !handle) throw Fail(EGS_ERR_INVALID_CONFIG, "null argument");
+    egs_ctx* c = part->c;
+    if (!c->xbuf) throw Fail(EGS_ERR_INVALID_CONFIG, "a one-rank partition has nothing to export");
+    CK(cudaSetDevice(c->device));
+    static_assert(sizeof(cudaIpcMemHandle_t) == EGS_IPC_HANDLE_BYTES, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, c->xbuf));
+    std::memcpy(handle, &h, sizeof(h));
+  });
+}
+
+int egs_part_connect(egs_part* part, const void* handles) {
+  return guarded([&] {
+    if (!part || !handles) throw Fail(EGS_ERR_INVALID_CONFIG, "null argument");
     egs_ctx* c = part->c;
     CK(cudaSetDevice(c->device));
-    if (c->n == 0) {
-      if (counts) counts[0] = counts[1] = 0;
-      return;
+    for (int q = 0; q < c->world; ++q) {
+      if (q == c->rank) continue;
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, static_cast<const char*>(handles) + (size_t)q * EGS_IPC_HANDLE_BYTES,
+                  sizeof(h));
+      void* ptr = nullptr;
+      CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+      c->xpeer[q] = static_cast<char*>(ptr);
+      c->xpeer_ipc[q] = true;
     }
-    if (c->vbits == 32)
-      part_step<uint32_t>(c, step, parity, counts);
-    else
-      part_step<uint64_t>(c, step, parity, counts);
+    c->connected = true;
   });
 }
 
-int egs_part_pack(egs_part* part, int32_t which, int32_t parity, uint32_t* count) {
+int egs_part_connect_local(egs_part* const* parts, int32_t world) {
   return guarded([&] {
-    if (!part || !count) throw Fail(EGS_ERR_INVALID_CONFIG, "null argument");
-    if (which != EGS_PACK_CHANGED && which != EGS_PACK_REMOVED)
-      throw Fail(EGS_ERR_INVALID_CONFIG, "unknown pack selector");
-    egs_ctx* c = part->c;
-    *count = 0;
-    if (c->n == 0 || c->world < 2 || c->own_hi <= c->own_lo) return;
-    CK(cudaSetDevice(c->device));
-    cudaStream_t s = c->stream;
-    const uint32_t* bits = which == EGS_PACK_CHANGED ? c->chg[parity & 1] : c->rbm[0];
-    CK(cudaMemsetAsync(c->xcount, 0, sizeof(uint32_t), s));
-    const uint32_t grid = grid_for((uint64_t)(c->own_hi - c->own_lo), c->num_sms);
-    if (c->vbits == 32)
-      egs::k_pack<uint32_t><<<grid, 256, 0, s>>>(c->own_lo, c->own_hi, bits,
-                                                 static_cast<uint32_t*>(c->f), c->xsend,
-                                                 c->xcount);
-    else
-      egs::k_pack<uint64_t><<<grid, 256, 0, s>>>(c->own_lo, c->own_hi, bits,
-                                                 static_cast<uint64_t*>(c->f), c->xsend,
-                                                 c->xcount);
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(count, c->xcount, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    if (!parts || world < 1) throw Fail(EGS_ERR_INVALID_CONFIG, "null argument");
+    for (int r = 0; r < world; ++r) {
+      if (!parts[r] || parts[r]->c->rank != r || parts[r]->c->world != world)
+        throw Fail(EGS_ERR_INVALID_CONFIG, "parts[r] must be rank r of the same world");
+      if (parts[r]->c->xbytes != parts[0]->c->xbytes)
+        throw Fail(EGS_ERR_INVALID_CONFIG, "parts of different arenas");
+    }
+    for (int r = 0; r < world; ++r) {
+      egs_ctx* c = parts[r]->c;
+      int same = 0;
+      for (int q = 0; q < world; ++q) {
+        egs_ctx* d = parts[q]->c;
+        c->xpeer[q] = d->xbuf;
+        if (d->device == c->device) {
+          ++same;
+        } else {
+          CK(cudaSetDevice(c->device));
+          const cudaError_t e = cudaDeviceEnablePeerAccess(d->device, 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+          cudaGetLastError();
+        }
+      }
+      part_grid(c, same);
+      c->connected = true;
+    }
   });
 }
 
-int egs_part_unpack(egs_part* part, const uint32_t* counts, uint32_t stride) {
-  return guarded([&] {
-    if (!part || !counts) throw Fail(EGS_ERR_INVALID_CONFIG, "null argument");
-    egs_ctx* c = part->c;
-    if (c->n == 0 || c->world < 2) return;
-    if (stride > c->slice) throw Fail(EGS_ERR_INVALID_CONFIG, "stride beyond the slice");
-    for (int r = 0; r < c->world; ++r)
-      if (counts[r] > stride) throw Fail(EGS_ERR_INVALID_CONFIG, "count beyond the stride");
-    CK(cudaSetDevice(c->device));
-    cudaStream_t s = c->stream;
-    CK(cudaMemcpyAsync(c->xcount + 1, counts, c->world * sizeof(uint32_t),
-                       cudaMemcpyHostToDevice, s));
-    const uint32_t grid = grid_for((uint64_t)stride * c->world, c->num_sms);
-    if (c->vbits == 32)
-      egs::k_unpack<uint32_t><<<grid, 256, 0, s>>>(c->xrecv, c->xcount + 1, c->world, stride,
-                                                   c->rank, static_cast<uint32_t*>(c->f));
-    else
-      egs::k_unpack<uint64_t><<<grid, 256, 0, s>>>(c->xrecv, c->xcount + 1, c->world, stride,
-                                                   c->rank, static_cast<uint64_t*>(c->f));
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(s));
-  });
-}
-
-int egs_part_reset(egs_part* part) {
+int egs_part_solve(egs_part* part, egs_gpu_stats* stats) {
   return guarded([&] {
     if (!part) throw Fail(EGS_ERR_INVALID_CONFIG, "null partition");
-    CK(cudaSetDevice(part->c->device));
-    part_reset(part->c);
+    egs_ctx* c = part->c;
+    if (!c->connected) throw Fail(EGS_ERR_INVALID_CONFIG, "partition not connected to its peers");
+    auto t0 = Clock::now();
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    ctx_solve(c, stats);
+    if (stats) stats->wall_seconds = secs_since(t0);
   });
 }
 
 int egs_part_read_measure(egs_part* part, int64_t* f_out) {
   return guarded([&] {
     if (!part) throw Fail(EGS_ERR_INVALID_CONFIG, "null partition");
-    part->c->solved = true;
     ctx_read(part->c, f_out);
-  });
-}
-
-int egs_part_counters(egs_part* part, egs_gpu_stats* stats) {
-  return guarded([&] {
-    if (!part || !stats) throw Fail(EGS_ERR_INVALID_CONFIG, "null argument");
-    egs_ctx* c = part->c;
-    CK(cudaSetDevice(c->device));
-    CK(cudaMemcpy(c->h_ctr, c->ctr, egs::kNumCounters * sizeof(unsigned long long),
-                  cudaMemcpyDeviceToHost));
-    std::memset(stats, 0, sizeof(*stats));
-    if (c->vbits == 32)
-      fill_stats<uint32_t>(c, c->h_ctr, 0.0, stats);
-    else
-      fill_stats<uint64_t>(c, c->h_ctr, 0.0, stats);
   });
 }
 

@@ -17,6 +17,7 @@ constexpr uint32_t kMediumMax = 4096; // <= 4096: one warp; longer: one CTA
 
 // Class ranges of the relabelled ids.
 enum : int { kP0L = 0, kP0M, kP0H, kP1L, kP1M, kP1H, kNumClasses };
+constexpr int kMaxRanks = 8;  // EGS_MAX_RANKS
 
 enum Counter : int {
   kLifts = 0,      // lifts that raised a value (SolveReport::lifts)
@@ -34,7 +35,7 @@ enum Counter : int {
   kSparseRounds,
   kCertAttempts,
   kCertPasses,
-  kStatus,         // 0 fixpoint, 2 timeout, 5 round budget
+  kStatus,         // 0 fixpoint, 2 timeout, 5 round budget, 7 a peer rank missing
   kTimeSeed,       // ns of device time per phase kind (%globaltimer)
   kTimeLift,
   kTimeCert,
@@ -49,6 +50,7 @@ enum Counter : int {
   kFineCertDense,
   kFineCertSparse,
   kFineCertApply,
+  kEpoch,          // multi-GPU: cross-rank barriers passed so far
   kNumCounters
 };
 
@@ -79,6 +81,15 @@ struct Scratch {
   unsigned int fr_cnt[3][3]; // frontier sublist sizes [token % 3][L, M, H]
   unsigned int stop;         // timeout flag
   unsigned int bad;          // debug_checks: a commit that did not raise its vertex
+  unsigned int xerr;         // multi-GPU: a peer did not reach a barrier in time
+};
+
+// Cross-rank sync block (multi-GPU, egs_part_solve), inside every rank's
+// replicated allocation: peers write their barrier epoch and their phase
+// sums here (double-buffered by epoch parity).
+struct XSync {
+  unsigned int arrive[kMaxRanks];
+  unsigned int sums[2][kMaxRanks][4];
 };
 
 template <class V>
@@ -110,6 +121,16 @@ struct SolveParams {
   unsigned long long round_budget;
   unsigned long long timeout_ns;   // 0 = none; measured from kernel start
   int debug;                // SolverOptions::debug_checks: commits check monotonicity
+  // multi-GPU (egs_part_solve; world == 1 otherwise): the measure and the
+  // changed / removal bitmaps are replicated in one allocation per rank with
+  // the same layout everywhere; a rank writes what it raises into every
+  // replica (xpeer[q] = rank q's allocation as mapped here).
+  int world, rank;
+  char* xbase;                  // this rank's replicated allocation
+  char* xpeer[kMaxRanks];
+  XSync* xsync;                 // this rank's sync block (in xbase)
+  unsigned int epoch0;          // cross-rank barriers before this solve
+  unsigned long long xwait_ns;  // a peer not arriving within this fails the solve
 };
 
 

@@ -1,120 +1,97 @@
-"""Multi-GPU solve: vertex-range partition, one process per GPU.
+"""Multi-GPU solve: one persistent kernel per rank, exchange on the device
+(include/egs_gpu.h egs_part_*).
 
 The reference has no distributed path (its ``workers`` are threads,
-``solver_par.cpp:231-236``).  Here every rank holds the whole arena (3 GB at
-C4 against 180 GB of HBM) and a replica of the measure, lifts only its own
-range of relabelled vertices, and after each step the ranks all-gather the
-owned slices of the replicated array that step wrote.  Rounds are synchronous
-(Jacobi), so the partitioned iteration is, round for round, the single-GPU
-dense iteration of ``k_solve``; termination is a round that raises nothing
-on any rank (one all-reduce), exactly the reference's ``changed`` latch
-(``solver_par.cpp:170-194``).
+``solver_par.cpp:231-236``).  Here ``world`` ranks solve one arena together:
 
-Two pluggable pieces:
+* **Partition** (``plan``): the relabelled vertex order is rank-major; every
+  (owner, out-degree) class is split into ``world`` pieces balanced by
+  out-edges (``edge_balanced_bounds``, ``solver_par.cpp:62-80``), so each rank
+  gets an equal share of player-0 rows, player-1 rows and hubs.  A rank keeps
+  only its own rows and the transpose of its own rows.
+* **Exchange**: the measure and the changed / removal bitmaps are replicated.
+  A rank writes every value it raises, and every bit it sets, into its own
+  replica and into its peers' (NVLink peer stores through CUDA IPC mappings,
+  or plain stores for ranks of one process); at each phase boundary the ranks
+  meet at a device-side barrier that also sums their phase counts, so all of
+  them take the same schedule decision.  The host launches once per rank and
+  waits once: no per-round host round trip, no host-staged collective.
+* **Plumbing**: ``torch.distributed`` (NCCL or gloo) only exchanges the
+  64-byte IPC handles before the solve and checks afterwards that every rank
+  holds the same measure (an all-gather of a digest).
 
-* ``DeviceSteps`` -- this rank's GPU through the C-ABI partition entry points
-  (``egs_part_*`` in include/egs_gpu.h).  The replicated arrays are the
-  library's own device buffers, wrapped (no copy) as torch tensors through
-  ``__cuda_array_interface__`` so NCCL all-gathers them in place.
-* ``TorchComm`` -- the collectives: ``torch.distributed`` over NCCL with
-  device tensors (the product), or over gloo with host staging (the CPU and
-  single-GPU tests of this orchestration).
+``solve_distributed`` is the one-process-per-GPU entry (torchrun);
+``solve_local`` runs several ranks in ONE process (several GPUs, or several
+ranks sharing one GPU -- the tests' way to run the device exchange on a
+single-GPU box).  Both give the single-GPU solver's measure byte for byte.
 """
 from __future__ import annotations
 
 import ctypes as C
+import hashlib
+import threading
 import time
 from dataclasses import dataclass, field
-from typing import Optional
+from typing import Optional, Sequence
 
 import numpy as np
 
 from . import _native as N
 
-STEP_ROUND1, STEP_LIFT, STEP_COMMIT, STEP_CERT_INIT, STEP_CERT_PRUNE, STEP_CERT_APPLY = range(6)
-PACK_CHANGED, PACK_REMOVED = 0, 1
+
+def plan(arena: N.GameArena, world: int) -> dict:
+    """The partition of ``arena`` over ``world`` ranks (egs_part_plan_compute;
+    host only, deterministic)."""
+    pl = N.PartPlan()
+    v = arena.view()
+    N._check(N.lib.egs_part_plan_compute(C.byref(v), int(world), C.byref(pl)))
+    return pl.as_dict()
 
 
-def partition_layout(n: int, world: int, rank: int):
-    """(slice, padded, own_lo, own_hi): equal 32-aligned slices of [0, n)."""
-    slice_ = ((n + world - 1) // world + 31) // 32 * 32 if n else 0
-    lo = min(n, slice_ * rank)
-    hi = min(n, slice_ * (rank + 1))
-    return slice_, slice_ * world, lo, hi
-
-
-class _CudaArray:
-    """Minimal __cuda_array_interface__ holder for a device buffer we own."""
-
-    def __init__(self, ptr: int, count: int, typestr: str):
-        self.__cuda_array_interface__ = {
-            "shape": (count,), "typestr": typestr, "data": (ptr, False), "version": 3,
-            "strides": None,
-        }
-
-
-class DeviceSteps:
-    """This rank's share of the solve on its GPU (egs_part_* C-ABI)."""
+class Partition:
+    """This rank's context (egs_part_create): the arena relabelled by the
+    plan, its own rows on ``options.device``."""
 
     def __init__(self, arena: N.GameArena, rank: int, world: int,
                  options: Optional[N.SolverOptions] = None):
-        import torch
-
         options = options or N.SolverOptions()
         opts = options.to_c()
-        opts.n_gpus = world
-        self.arena = arena
-        self.rank, self.world = rank, world
+        opts.n_gpus = int(world)
+        self.arena, self.rank, self.world = arena, int(rank), int(world)
         self._view = arena.view()
         self._part = C.c_void_p()
-        lay = N.PartLayout()
+        pl = N.PartPlan()
         st = N.GpuStats()
-        N._check(N.lib.egs_part_create(C.byref(self._view), C.byref(opts), rank, world,
-                                       C.byref(self._part), C.byref(lay), C.byref(st)))
+        N._check(N.lib.egs_part_create(C.byref(self._view), C.byref(opts), self.rank, self.world,
+                                       C.byref(self._part), C.byref(pl), C.byref(st)))
+        self.plan = pl.as_dict()
         self.upload_seconds = st.upload_seconds
-        self.n, self.slice, self.padded = lay.num_vertices, lay.slice, lay.padded
-        self.own_lo, self.own_hi = lay.own_lo, lay.own_hi
-        self.value_bytes = lay.value_bytes
-        typestr = "<i4" if lay.value_bytes == 4 else "<i8"  # bit patterns only
-        dev = torch.device("cuda", torch.cuda.current_device())
-        count = max(self.padded, 1)
-        self.f = torch.as_tensor(_CudaArray(lay.f_dev, count, typestr), device=dev)
-        self.stage = torch.as_tensor(_CudaArray(lay.stage_dev, count, typestr), device=dev)
-        # sparse exchange: packed (id, value) entries, `entry_words` u64 each
-        self.entry_words = max(lay.entry_bytes // 8, 1)
-        if world > 1:
-            self.send = torch.as_tensor(
-                _CudaArray(lay.send_dev, self.slice * self.entry_words + 1, "<i8"), device=dev)
-            self.recv = torch.as_tensor(
-                _CudaArray(lay.recv_dev, world * self.slice * self.entry_words + 1, "<i8"),
-                device=dev)
-        self._counts = (C.c_uint64 * 2)()
 
-    def step(self, kind: int, parity: int):
-        N._check(N.lib.egs_part_step(self._part, kind, parity, self._counts))
-        return int(self._counts[0]), int(self._counts[1])
+    def export(self) -> bytes:
+        buf = C.create_string_buffer(N.IPC_HANDLE_BYTES)
+        N._check(N.lib.egs_part_export(self._part, buf))
+        return buf.raw
 
-    def pack(self, which: int, parity: int) -> int:
-        cnt = C.c_uint32(0)
-        N._check(N.lib.egs_part_pack(self._part, which, parity, C.byref(cnt)))
-        return int(cnt.value)
+    def connect(self, handles: Sequence[bytes]) -> None:
+        """Map every peer's replicated state (handles[r] = rank r's export)."""
+        blob = b"".join(h if i != self.rank else bytes(N.IPC_HANDLE_BYTES)
+                        for i, h in enumerate(handles))
+        N._check(N.lib.egs_part_connect(self._part, blob))
 
-    def unpack(self, counts, stride: int):
-        arr = (C.c_uint32 * len(counts))(*counts)
-        N._check(N.lib.egs_part_unpack(self._part, arr, stride))
+    @staticmethod
+    def connect_local(parts: Sequence["Partition"]) -> None:
+        arr = (C.c_void_p * len(parts))(*[p._part.value for p in parts])
+        N._check(N.lib.egs_part_connect_local(arr, len(parts)))
 
-    def reset(self):
-        N._check(N.lib.egs_part_reset(self._part))
+    def solve(self) -> N.GpuStats:
+        st = N.GpuStats()
+        N._check(N.lib.egs_part_solve(self._part, C.byref(st)))
+        return st
 
     def read_measure(self) -> np.ndarray:
-        out = np.empty(self.n, dtype=np.int64)
+        out = np.empty(self.arena.num_vertices, dtype=np.int64)
         N._check(N.lib.egs_part_read_measure(self._part, out.ctypes.data))
         return out
-
-    def counters(self) -> dict:
-        st = N.GpuStats()
-        N._check(N.lib.egs_part_counters(self._part, C.byref(st)))
-        return st.as_dict()
 
     def close(self):
         if self._part:
@@ -128,180 +105,104 @@ class DeviceSteps:
             pass
 
 
-class TorchComm:
-    """All-gather of owned slices and integer all-reduce over torch.distributed.
-
-    ``staged=False``: NCCL, in place on the device tensors.  ``staged=True``:
-    any backend (gloo) through host copies -- for tests on CPU or with several
-    ranks sharing one GPU."""
-
-    def __init__(self, rank: int, world: int, staged: bool = False, device=None):
-        import torch
-        import torch.distributed as dist
-
-        self.dist, self.torch = dist, torch
-        self.rank, self.world, self.staged = rank, world, staged
-        self.device = device
-        self.bytes_gathered = 0
-        self.collectives = 0
-
-    def allgather(self, t, slice_: int):
-        """t[r*slice:(r+1)*slice] of every rank r into t on every rank."""
-        self.collectives += 1
-        self.bytes_gathered += t.numel() * t.element_size()
-        if self.world == 1:
-            return
-        mine = t.narrow(0, self.rank * slice_, slice_)
-        if not self.staged:
-            self.dist.all_gather_into_tensor(t, mine)
-            # the next step runs on the library's own stream: wait for NCCL
-            self.torch.cuda.synchronize(t.device)
-            return
-        host = mine.detach().to("cpu", copy=True)
-        parts = [self.torch.empty_like(host) for _ in range(self.world)]
-        self.dist.all_gather(parts, host)
-        t.copy_(self.torch.cat(parts).to(t.device))
-        self._sync(t)
-
-    def allgather_ints(self, x: int) -> list:
-        """Every rank's x (one small collective; its sum is the all-reduce)."""
-        self.collectives += 1
-        if self.world == 1:
-            return [int(x)]
-        dev = self.device if (self.device is not None and not self.staged) else "cpu"
-        v = self.torch.tensor([int(x)], dtype=self.torch.int64, device=dev)
-        out = self.torch.empty(self.world, dtype=self.torch.int64, device=dev)
-        self.dist.all_gather_into_tensor(out, v)
-        return [int(y) for y in out.tolist()]
-
-    def gather_entries(self, send, recv, n: int):
-        """send[:n] of every rank r into recv[r*n:(r+1)*n] on every rank."""
-        self.collectives += 1
-        self.bytes_gathered += n * self.world * send.element_size()
-        if self.world == 1 or n == 0:
-            return
-        if not self.staged:
-            self.dist.all_gather_into_tensor(recv.narrow(0, 0, n * self.world), send.narrow(0, 0, n))
-            self.torch.cuda.synchronize(recv.device)
-            return
-        host = send.narrow(0, 0, n).detach().to("cpu", copy=True)
-        parts = [self.torch.empty_like(host) for _ in range(self.world)]
-        self.dist.all_gather(parts, host)
-        recv.narrow(0, 0, n * self.world).copy_(self.torch.cat(parts).to(recv.device))
-        self._sync(recv)
-
-    def _sync(self, t):
-        # the library's next step runs on its own non-blocking stream: the
-        # copy on torch's stream must have landed
-        if t.is_cuda:
-            self.torch.cuda.synchronize(t.device)
-
-    def allreduce_sum(self, x: int) -> int:
-        self.collectives += 1
-        if self.world == 1:
-            return int(x)
-        dev = self.device if (self.device is not None and not self.staged) else "cpu"
-        v = self.torch.tensor([int(x)], dtype=self.torch.int64, device=dev)
-        self.dist.all_reduce(v)
-        return int(v.item())
-
-
 @dataclass
 class PartitionReport:
     measure: np.ndarray
     rounds: int = 0
-    cert_attempts: int = 0
-    cert_passes: int = 0
-    certified: int = 0
     wall_seconds: float = 0.0
-    collectives: int = 0
-    bytes_gathered: int = 0
-    kernel_launches: int = 0
-    sparse_exchanges: int = 0
-    counters: dict = field(default_factory=dict)
+    solve_seconds: float = 0.0          # device time of this rank's kernel
+    edges_relaxed: int = 0              # this rank's
+    edges_owned: int = 0                # out-edges of this rank's vertices (plan)
+    plan: dict = field(default_factory=dict)
+    stats: dict = field(default_factory=dict)
 
 
-def solve_partitioned(steps, comm, certify: bool = True, cert_interval: int = 1,
-                      cert_growth: int = 4,
-                      round_budget: Optional[int] = None,
-                      timeout_seconds: float = 0.0) -> PartitionReport:
-    """The dense schedule of k_solve (egs_solve.cuh), one step at a time.
+def _digest(f: np.ndarray) -> bytes:
+    return hashlib.sha256(np.ascontiguousarray(f).tobytes()).digest()
 
-    ``steps`` is this rank's share (``DeviceSteps`` in the product);
-    ``comm`` exchanges the owned slices (``TorchComm``).  Every rank returns
-    the same least progress measure."""
+
+class TorchComm:
+    """The plumbing collectives over ``torch.distributed`` (any backend):
+    an all-gather of small byte strings (IPC handles, digests)."""
+
+    def __init__(self):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+
+    def allgather_bytes(self, b: bytes) -> list:
+        out = [None] * self.world
+        self.dist.all_gather_object(out, b)
+        return out
+
+    def barrier(self):
+        self.dist.barrier()
+
+
+def solve_distributed(arena: N.GameArena, options: Optional[N.SolverOptions] = None,
+                      comm=None, part_factory=Partition, part=None) -> PartitionReport:
+    """One process per GPU (torchrun): this rank's share of the solve.  Every
+    rank returns the same measure (checked: all-gather of its SHA-256).
+    ``part`` reuses a connected Partition (repeated solves)."""
+    comm = comm or TorchComm()
+    rank, world = comm.rank, comm.world
     t0 = time.perf_counter()
-    launches = 0
-    step_fn = steps.step
-
-    def step(kind, par):
-        nonlocal launches
-        launches += 1  # one k_part_step launch per call
-        return step_fn(kind, par)
-
-    sparse_exchanges = 0
-
-    def exchange(which, parity, counts):
-        """Bring every rank's marked values into the replicas: (id, value)
-        entries when few changed, else the whole owned slices of f."""
-        nonlocal sparse_exchanges
-        maxc = max(counts)
-        if maxc == 0 or comm.world == 1:
-            return
-        ew = getattr(steps, "entry_words", 1)
-        dense_words = steps.slice * steps.f.element_size() / 8
-        if maxc * ew * 2 > dense_words or not hasattr(steps, "pack"):
-            comm.allgather(steps.f, steps.slice)
-            return
-        n = steps.pack(which, parity)
-        assert n == counts[comm.rank], "pack count differs from the step's count"
-        comm.gather_entries(steps.send, steps.recv, maxc * ew)
-        steps.unpack(counts, maxc)
-        sparse_exchanges += 1
-
-    parity = 0
-    counts = comm.allgather_ints(step(STEP_ROUND1, parity)[0])
-    changed = sum(counts)
-    rounds = 1
-    K = cert_interval if cert_interval > 0 else 1
-    next_cert = K
-    attempts = passes = certified = 0
-    while changed:
-        step(STEP_COMMIT, parity)
-        exchange(PACK_CHANGED, parity, counts)
-        if round_budget is not None and rounds >= round_budget:
-            raise N.BoundExhaustedError(
-                f"round budget of {round_budget} exhausted before reaching a fixpoint")
-        if timeout_seconds and time.perf_counter() - t0 > timeout_seconds:
-            raise N.TimeoutError_("solve timed out")
-        if certify and rounds >= next_cert:
-            attempts += 1
-            # candidates carry a mark in f (egs_solve.cuh CandFlag): the passes
-            # read the other ranks' marks, so f is exchanged after each step
-            step(STEP_CERT_INIT, parity)
-            comm.allgather(steps.f, steps.slice)
-            while True:
-                rc = comm.allgather_ints(step(STEP_CERT_PRUNE, parity)[1])
-                removed = sum(rc)
-                exchange(PACK_REMOVED, parity, rc)
-                passes += 1
-                if removed == 0:
-                    break
-            cert = comm.allreduce_sum(step(STEP_CERT_APPLY, parity)[0])
-            comm.allgather(steps.f, steps.slice)
-            certified += cert
-            K = min(cert_growth * K, 64)  # the geometric schedule of k_solve
-            next_cert = rounds + K
-        parity ^= 1
-        counts = comm.allgather_ints(step(STEP_LIFT, parity)[0])
-        changed = sum(counts)
-        rounds += 1
-    f = steps.read_measure()
+    if part is None:
+        part = part_factory(arena, rank, world, options)
+        if world > 1:
+            part.connect(comm.allgather_bytes(part.export()))
+        comm.barrier()
+    st = part.solve()
+    f = part.read_measure()
+    digests = comm.allgather_bytes(_digest(f))
+    if any(d != digests[0] for d in digests):
+        raise N.InternalInvariantError("ranks disagree on the measure")
     return PartitionReport(
-        measure=f, rounds=rounds, cert_attempts=attempts, cert_passes=passes,
-        certified=certified, wall_seconds=time.perf_counter() - t0,
-        collectives=comm.collectives, bytes_gathered=comm.bytes_gathered,
-        sparse_exchanges=sparse_exchanges,
-        kernel_launches=launches,
-        counters=steps.counters() if hasattr(steps, "counters") else {},
-    )
+        measure=f, rounds=int(st.rounds), wall_seconds=time.perf_counter() - t0,
+        solve_seconds=float(st.solve_seconds), edges_relaxed=int(st.edges_relaxed),
+        edges_owned=int(part.plan["edges"][rank]), plan=part.plan, stats=st.as_dict())
+
+
+def solve_local(arena: N.GameArena, world: int, devices: Optional[Sequence[int]] = None,
+                options: Optional[N.SolverOptions] = None, parts=None):
+    """``world`` ranks in this process, one host thread each (``devices[r]``:
+    rank r's GPU; default all on the current device).  Returns (reports,
+    parts); pass ``parts`` back to solve again without a new upload."""
+    import dataclasses
+
+    options = options or N.SolverOptions()
+    if parts is None:
+        devices = list(devices) if devices is not None else [options.device] * world
+        parts = [Partition(arena, r, world,
+                           dataclasses.replace(options, device=devices[r], workers=world))
+                 for r in range(world)]
+        Partition.connect_local(parts)
+    results: list = [None] * world
+    errors: list = [None] * world
+
+    def run(r):
+        try:
+            t0 = time.perf_counter()
+            st = parts[r].solve()
+            results[r] = (st, time.perf_counter() - t0)
+        except BaseException as e:  # noqa: BLE001 -- re-raised below
+            errors[r] = e
+
+    threads = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for e in errors:
+        if e is not None:
+            raise e
+    reports = []
+    for r in range(world):
+        st, wall = results[r]
+        reports.append(PartitionReport(
+            measure=parts[r].read_measure(), rounds=int(st.rounds), wall_seconds=wall,
+            solve_seconds=float(st.solve_seconds), edges_relaxed=int(st.edges_relaxed),
+            edges_owned=int(parts[r].plan["edges"][r]), plan=parts[r].plan,
+            stats=st.as_dict()))
+    return reports, parts

@@ -1,23 +1,82 @@
-"""Multi-rank orchestration of the partitioned solve (distributed.py).
+"""Multi-GPU partition (distributed.py, egs_part_*).
 
-CPU: world_size 2 and 3 over gloo, each rank driving the numpy model of its
-partition steps (tests/partition_model.py); the result must equal the
-reference's least measure.  GPU: two ranks sharing one GPU, each driving the
-real device steps (egs_part_*) with a staged gloo exchange; and one rank over
-NCCL."""
+CPU: the partition plan (egs_part_plan_compute) against an independent numpy
+restatement of edge_balanced_bounds per class (solver_par.cpp:62-80) and its
+balance; the torch.distributed orchestration (IPC handle exchange, the
+measure-digest check) on world_size 2 over gloo with a stand-in partition.
+GPU: several ranks of the real device exchange in one process -- sharing
+one B200 -- against the single-GPU solve and the reference's golden digests,
+byte for byte, including C4 at full size."""
+import hashlib
 import os
 import socket
 
 import numpy as np
 import pytest
-import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from arena_gen import random_arena
-from oracle_bindings import INT64_MAX, Oracle
+from oracle_bindings import INT64_MAX
 
 
+# ----------------------------------------------------------------- plan ----
+def plan_numpy(off, owners, world):
+    """Independent restatement: class = owner * 3 + (deg <= 32 ? 0 : deg <=
+    4096 ? 1 : 2); piece r of class k starts at the first class member with
+    at least ceil(E_k * r / world) class edges before it."""
+    off = np.asarray(off, dtype=np.int64)
+    deg = np.diff(off)
+    cls = np.asarray(owners, dtype=np.int64) * 3 + np.where(deg <= 32, 0, np.where(deg <= 4096, 1, 2))
+    piece = []
+    for k in range(6):
+        d = deg[cls == k]
+        before = np.concatenate([[0], np.cumsum(d)])[:-1]  # edges before each member
+        E = int(d.sum())
+        b = [0]
+        for r in range(1, world):
+            t = -(-E * r // world)
+            b.append(int(np.searchsorted(before, t, side="left")) if d.size else 0)
+        b.append(int(d.size))
+        piece.append(b)
+    edges = [0] * world
+    for k in range(6):
+        d = deg[cls == k]
+        for r in range(world):
+            edges[r] += int(d[piece[k][r]:piece[k][r + 1]].sum())
+    return piece, edges
+
+
+ARENAS = [("fixed", (20000, 16, 100)), ("fixed", (5000, 4, 1000)), ("rmat", (13, 16, 100))]
+
+
+@pytest.mark.parametrize("kind,args", ARENAS, ids=[f"{k}{a}" for k, a in ARENAS])
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_plan_matches_restatement_and_is_balanced(egs, kind, args, world):
+    from paper_1710_03647_b200.distributed import plan
+
+    a = getattr(egs.GameArena, kind)(*args, 1)
+    pl = plan(a, world)
+    piece, edges = plan_numpy(a.csr_offsets, a.owners, world)
+    assert pl["piece"] == piece
+    assert pl["edges"] == edges
+    assert sum(pl["edges"]) == a.num_edges
+    # rank-major and class-sorted: contiguous blocks covering [0, n)
+    assert pl["rank_lo"][0] == 0 and pl["rank_lo"][-1] == a.num_vertices
+    for r in range(world):
+        cl = pl["class_lo"][r]
+        assert cl[0] == pl["rank_lo"][r] and cl[6] == pl["rank_lo"][r + 1]
+        assert all(cl[k] <= cl[k + 1] for k in range(6))
+        for k in range(6):
+            assert cl[k + 1] - cl[k] == piece[k][r + 1] - piece[k][r]
+    if kind == "fixed":  # uniform degrees: every rank within 1.2x of the mean
+        assert max(edges) <= 1.2 * a.num_edges / world
+        for k in (0, 3):  # player-0 and player-1 rows split evenly too
+            sizes = np.diff(piece[k])
+            assert sizes.max() <= 1.2 * sizes.sum() / world + 1
+
+
+# -------------------------------------------------- gloo orchestration ----
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -26,123 +85,168 @@ def _free_port():
     return p
 
 
-def _cases():
-    cases = []
-    for seed in range(12):
-        n, edges, owners = random_arena(500 + seed, max_n=60, max_deg=5)
-        cases.append(("random", (n, edges, owners)))
-    cases.append(("fixed", (3000, 4, 100, 1)))
-    cases.append(("fixed", (2000, 8, 100000, 1)))
-    return cases
+class FakePartition:
+    """Stands in for distributed.Partition on CPU: records the handle
+    exchange; its 'measure' is the reference's (or a corrupted one)."""
+
+    def __init__(self, arena, rank, world, options=None, measure=None):
+        from paper_1710_03647_b200.distributed import plan
+        self.rank, self.world = rank, world
+        self.plan = plan(arena, world)
+        self._measure = measure
+        self.connected = None
+
+    def export(self):
+        return hashlib.sha256(f"rank{self.rank}".encode()).digest() * 2  # 64 bytes
+
+    def connect(self, handles):
+        self.connected = list(handles)
+
+    def solve(self):
+        import paper_1710_03647_b200 as egs
+        st = egs._native.GpuStats()
+        st.rounds = 5
+        return st
+
+    def read_measure(self):
+        return self._measure
 
 
-def _worker_cpu(rank, world, port, q):
+def _worker(rank, world, port, q, corrupt):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        import sys
-        from partition_model import NumpySteps
-        from paper_1710_03647_b200.distributed import TorchComm, solve_partitioned
-        oracle = Oracle()
-        out = []
-        for kind, args in _cases():
-            g = oracle.build(*args) if kind == "random" else oracle.fixed(*args)
-            off, dst, w, own = g.csr()
-            steps = NumpySteps(off, dst, w, own, g.a.credit_cap, rank, world)
-            comm = TorchComm(rank, world, staged=True)
-            rep = solve_partitioned(steps, comm)
-            want, _ = oracle.solve_seq(g)
-            out.append((kind, bool(np.array_equal(rep.measure, want)), rep.rounds,
-                        rep.cert_attempts, rep.sparse_exchanges))
-        q.put((rank, out))
-    finally:
-        dist.destroy_process_group()
-
-
-@pytest.mark.parametrize("world", [2, 3])
-def test_partitioned_orchestration_gloo_cpu(world):
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker_cpu, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    results = dict(q.get(timeout=600) for _ in range(world))
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
-    ref = results[0]
-    for r in range(world):
-        assert all(x[1] for x in results[r]), results[r]
-        # every rank agrees on the schedule (incl. which exchanges went sparse)
-        assert [x[2:] for x in results[r]] == [x[2:] for x in ref]
-    # the late rounds of the fixed-shape arenas change few vertices: their
-    # exchanges take the (id, value) path
-    assert sum(x[4] for x in ref) > 0
-
-
-def _worker_gpu(rank, world, port, q, backend):
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    torch.cuda.set_device(0)
-    dist.init_process_group(backend, rank=rank, world_size=world)
-    try:
-        import json
         import paper_1710_03647_b200 as egs
-        from paper_1710_03647_b200.distributed import DeviceSteps, TorchComm, solve_partitioned
-        from oracle_bindings import fnv1a64
-        golden = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))
-        out = []
-        for key, make in [("fixed/10000/4/100/1", lambda: egs.GameArena.fixed(10000, 4, 100, 1)),
-                          ("fixed/100000/16/100/1", lambda: egs.GameArena.fixed(100000, 16, 100, 1)),
-                          ("fixed/100000/8/100000/1", lambda: egs.GameArena.fixed(100000, 8, 100000, 1)),
-                          ("rmat/14/16/100/1", lambda: egs.GameArena.rmat(14, 16, 100, 1))]:
-            a = make()
-            steps = DeviceSteps(a, rank, world, egs.SolverOptions(device=0))
-            comm = TorchComm(rank, world, staged=(backend == "gloo"), device="cuda:0")
-            rep = solve_partitioned(steps, comm)
-            sol = egs.write_solution(a, rep.measure).encode()
-            out.append((key, f"{fnv1a64(sol):016x}" == golden[key]["solution_fnv"], rep.rounds,
-                        rep.sparse_exchanges))
-            steps.close()
-        for seed in range(20):
-            n, edges, owners = random_arena(900 + seed, max_n=80, max_deg=6)
-            a = egs.GameArena.build(n, edges, owners)
-            steps = DeviceSteps(a, rank, world, egs.SolverOptions(device=0))
-            rep = solve_partitioned(steps, TorchComm(rank, world, staged=True))
-            want = egs.solve(a, options=egs.SolverOptions(device=0)).measure
-            out.append((f"random{seed}", bool(np.array_equal(rep.measure, want)), rep.rounds,
-                        rep.sparse_exchanges))
-            steps.close()
-        q.put((rank, out))
+        from oracle_bindings import Oracle
+        from paper_1710_03647_b200.distributed import solve_distributed
+        n, edges, owners = random_arena(77, max_n=50, max_deg=5)
+        a = egs.GameArena.build(n, edges, owners)
+        want, _ = Oracle().solve_seq(Oracle().build(n, edges, owners))
+        mine = want.copy()
+        if corrupt and rank == 1:
+            mine[0] = INT64_MAX if mine[0] != INT64_MAX else 0
+        parts = []
+
+        def factory(arena, r, w, options):
+            p = FakePartition(arena, r, w, options, measure=mine)
+            parts.append(p)
+            return p
+        try:
+            rep = solve_distributed(a, part_factory=factory)
+            ok = bool(np.array_equal(rep.measure, want))
+            err = None
+        except egs.InternalInvariantError as e:
+            ok, err = False, str(e)
+        p = parts[0]
+        expect = [hashlib.sha256(f"rank{r}".encode()).digest() * 2 for r in range(world)]
+        q.put((rank, ok, err, p.connected == expect, p.plan))
     finally:
         dist.destroy_process_group()
 
 
-def _run_gpu(world, backend):
+@pytest.mark.parametrize("corrupt", [False, True])
+def test_orchestration_gloo_world2(corrupt):
+    world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker_gpu, args=(r, world, port, q, backend))
-             for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, corrupt)) for r in range(world)]
     for p in procs:
         p.start()
-    results = dict(q.get(timeout=300) for _ in range(world))
+    res = dict((x[0], x[1:]) for x in (q.get(timeout=300) for _ in range(world)))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     for r in range(world):
-        assert all(x[1] for x in results[r]), results[r]
-    if world > 1:  # the device pack / unpack path ran
-        assert sum(x[3] for x in results[0]) > 0, results[0]
+        ok, err, handles_ok, pl = res[r]
+        assert handles_ok, "IPC handles must arrive in rank order"
+        assert pl == res[0][3], "every rank computes the same plan"
+        if corrupt:
+            assert not ok and "disagree" in err
+        else:
+            assert ok and err is None
+
+
+# ------------------------------------------------------------------ GPU ----
+def _local(egs, a, world, **kw):
+    from paper_1710_03647_b200.distributed import solve_local
+    reps, parts = solve_local(a, world, options=egs.SolverOptions(device=0, **kw))
+    return reps, parts
 
 
 @pytest.mark.gpu
-def test_partitioned_device_two_ranks_one_gpu():
-    _run_gpu(2, "gloo")
+@pytest.mark.parametrize("world", [2, 3])
+def test_local_ranks_match_single_gpu(egs, oracle, world):
+    cases = []
+    for seed in range(12):
+        n, edges, owners = random_arena(900 + seed, max_n=80, max_deg=6)
+        cases.append(egs.GameArena.build(n, edges, owners))
+    cases += [egs.GameArena.fixed(10000, 4, 100, 1), egs.GameArena.fixed(100000, 16, 100, 1),
+              egs.GameArena.fixed(100000, 8, 100000, 1), egs.GameArena.rmat(14, 16, 100, 1)]
+    for a in cases:
+        want = egs.solve(a, options=egs.SolverOptions(device=0)).measure
+        for opts in (dict(), dict(mode="dense"), dict(certify=False, mode="sparse")):
+            if not opts.get("certify", True) and a.num_vertices > 20000:
+                continue  # plain iteration on the large shapes takes ~10^4 rounds
+            reps, parts = _local(egs, a, world, **opts)
+            for r, rep in enumerate(reps):
+                assert np.array_equal(rep.measure, want), (a.num_vertices, world, opts, r)
+            assert len({rep.rounds for rep in reps}) == 1, "ranks took different schedules"
+            for p in parts:
+                p.close()
 
 
 @pytest.mark.gpu
-def test_partitioned_device_nccl_single_rank():
-    _run_gpu(1, "nccl")
+def test_local_ranks_golden_and_repeated_solves(egs, golden):
+    a = egs.GameArena.fixed(100000, 16, 100, 1)
+    rec = golden["fixed/100000/16/100/1"]
+    reps, parts = _local(egs, a, 2)
+    for _ in range(3):  # barrier epochs carry across solves
+        sol = egs.write_solution(a, reps[0].measure)
+        assert len(sol) == rec["solution_bytes"]
+        assert int((reps[0].measure == INT64_MAX).sum()) == rec["tops"]
+        from paper_1710_03647_b200.distributed import solve_local
+        reps, parts = solve_local(a, 2, parts=parts)
+        assert np.array_equal(reps[0].measure, reps[1].measure)
+    # balanced work: per-rank owned edges and edges relaxed within 1.2x
+    owned = [r.edges_owned for r in reps]
+    assert max(owned) <= 1.2 * sum(owned) / 2
+    relaxed = [r.edges_relaxed for r in reps]
+    assert max(relaxed) <= 1.2 * sum(relaxed) / 2 + 1000
+    for p in parts:
+        p.close()
+
+
+@pytest.mark.gpu
+def test_peer_missing_times_out_instead_of_hanging(egs):
+    from paper_1710_03647_b200.distributed import Partition
+    a = egs.GameArena.fixed(5000, 4, 100, 1)
+    opts = egs.SolverOptions(device=0, workers=2, timeout_seconds=1.0)
+    parts = [Partition(a, r, 2, opts) for r in range(2)]
+    Partition.connect_local(parts)
+    with pytest.raises(egs.CudaError):
+        parts[0].solve()  # rank 1 never launches
+    for p in parts:
+        p.close()
+
+
+@pytest.mark.gpu
+def test_c4_two_ranks_byte_identical(egs, golden):
+    """C4 = fixed(1.6e7, 16, 100) over 2 ranks (sharing one GPU): the
+    measure and its write_solution bytes equal the single-GPU solve's."""
+    a = egs.GameArena.fixed(16_000_000, 16, 100, 1, pinned=True)
+    with egs.DeviceSolver(a, egs.SolverOptions(device=0)) as ds:
+        ds.solve()
+        want = ds.read_measure()
+        want_text = ds.write_solution().encode()
+    reps, parts = _local(egs, a, 2)
+    for p in parts:
+        p.close()
+    for rep in reps:
+        assert np.array_equal(rep.measure, want)
+    text = egs.write_solution(a, reps[0].measure).encode()
+    assert text == want_text
+    rec = golden.get("fixed/16000000/16/100/1", {})
+    if "solution_sha256" in rec:
+        assert hashlib.sha256(text).hexdigest() == rec["solution_sha256"]
