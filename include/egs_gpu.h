@@ -67,6 +67,9 @@ typedef struct egs_arena_view {
 #define EGS_MODE_AUTO 0   /* dense/sparse switch on frontier edge volume */
 #define EGS_MODE_DENSE 1  /* every round lifts every vertex (Alg. 2 shape) */
 #define EGS_MODE_SPARSE 2 /* worklist rounds only (Alg. 3 shape) */
+#define EGS_MODE_SWEEP 3  /* every round lifts every vertex IN PLACE, reading
+                             its successors' current values: the reference's
+                             solve_sweep (Alg. 2, solver_par.cpp:205-228) */
 
 /* SolverOptions (solver.hpp:33-42) plus the device knobs. */
 typedef struct egs_gpu_opts {

@@ -395,7 +395,7 @@ class Variant(enum.IntEnum):
     GPU = 3
 
 
-_MODES = {"auto": 0, "dense": 1, "sparse": 2}
+_MODES = {"auto": 0, "dense": 1, "sparse": 2, "sweep": 3}
 
 
 @dataclass

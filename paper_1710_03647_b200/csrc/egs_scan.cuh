@@ -220,3 +220,93 @@ __global__ void __launch_bounds__(kScanThreads)
 }
 
 }  // namespace egs
+
+namespace egs {
+
+// ------------------------------------------ CSC transpose: radix sort ----
+// The predecessor transpose (arena.cpp:56-74; the paper's CUSPARSE csr2csc,
+// PAPER.md:529-530) is a STABLE sort of the (dst, src) pairs of the
+// relabelled CSR by dst: within a column the sources keep CSR order, i.e.
+// ascending, exactly the reference's stable transpose.  LSD radix sort with
+// 8-bit digits; each pass is a stable counting sort:
+//   k_radix_hist     per-tile digit histogram (tiles of 4096 pairs), written
+//                    digit-major: hist[d * ntiles + tile]
+//   dev_excl_scan    of the histogram = each (digit, tile)'s output offset
+//   k_radix_scatter  warp w of a tile takes pairs [512 w, 512 w + 512) in 16
+//                    steps of 32 consecutive pairs; __match_any_sync groups a
+//                    step's lanes by digit, per-warp digit counters give each
+//                    pair its rank in (warp, step, lane) order = tile order,
+//                    a prefix over warps per digit completes the tile rank.
+constexpr int kRadixBits = 8;
+constexpr int kRadixDigits = 1 << kRadixBits;
+constexpr int kRadixSteps = kScanItems;  // 16 steps of 32 pairs per warp
+
+__global__ void __launch_bounds__(kScanThreads)
+    k_radix_hist(const uint32_t* key, uint64_t m, int shift, uint32_t* hist, uint32_t ntiles) {
+  __shared__ unsigned int s_h[kRadixDigits];
+  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (int d = threadIdx.x; d < kRadixDigits; d += kScanThreads) s_h[d] = 0;
+    __syncthreads();
+    const uint64_t base = (uint64_t)t * kScanTile;
+#pragma unroll 4
+    for (int k = 0; k < kScanItems; ++k) {
+      const uint64_t i = base + (uint64_t)k * kScanThreads + threadIdx.x;
+      if (i < m) atomicAdd(&s_h[(key[i] >> shift) & (kRadixDigits - 1)], 1u);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < kRadixDigits; d += kScanThreads)
+      hist[(uint64_t)d * ntiles + t] = s_h[d];
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+    k_radix_scatter(const uint32_t* key, const uint32_t* val, uint64_t m, int shift,
+                    const uint32_t* off, uint32_t ntiles, uint32_t* key_out, uint32_t* val_out) {
+  constexpr int W = kScanThreads / 32;
+  __shared__ uint32_t s_wc[W][kRadixDigits];  // per-warp digit counts, then warp prefixes
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (int i = threadIdx.x; i < W * kRadixDigits; i += kScanThreads) (&s_wc[0][0])[i] = 0;
+    __syncthreads();
+    const uint64_t wbase = (uint64_t)t * kScanTile + (uint64_t)warp * 32 * kRadixSteps;
+    uint32_t k_[kRadixSteps], v_[kRadixSteps], r_[kRadixSteps];
+#pragma unroll
+    for (int s = 0; s < kRadixSteps; ++s) {
+      const uint64_t i = wbase + (uint64_t)s * 32 + lane;
+      const bool in = i < m;
+      k_[s] = in ? key[i] : 0u;
+      v_[s] = in ? val[i] : 0u;
+      const uint32_t d = in ? (k_[s] >> shift) & (kRadixDigits - 1) : 0xFFFFFFFFu;
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      const uint32_t base = in ? s_wc[warp][d] : 0u;
+      __syncwarp();
+      if (in && (peers & lanemask_lt()) == 0) s_wc[warp][d] = base + __popc(peers);
+      __syncwarp();
+      r_[s] = base + __popc(peers & lanemask_lt());
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < kRadixDigits; d += kScanThreads) {
+      uint32_t acc = 0;
+      for (int w = 0; w < W; ++w) {
+        const uint32_t c = s_wc[w][d];
+        s_wc[w][d] = acc;
+        acc += c;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < kRadixSteps; ++s) {
+      const uint64_t i = wbase + (uint64_t)s * 32 + lane;
+      if (i < m) {
+        const uint32_t d = (k_[s] >> shift) & (kRadixDigits - 1);
+        const uint32_t pos = off[(uint64_t)d * ntiles + t] + s_wc[warp][d] + r_[s];
+        key_out[pos] = k_[s];
+        val_out[pos] = v_[s];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace egs

@@ -780,7 +780,7 @@ __device__ __forceinline__ void row_edges(uint32_t len, uint32_t rot, F&& f) {
 // all-top vertices are skipped without a copy; each lane lifts its own row
 // from shared memory (reads rotated by lane so a half-warp hits distinct
 // banks), 8 gathers in flight.
-template <class V>
+template <class V, bool INPLACE = false>
 __device__ __noinline__ void dense_light_p1(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
                                             unsigned int* cursor, uint32_t* chg,
                                             unsigned int* sum_dst) {
@@ -812,14 +812,13 @@ __device__ __noinline__ void dense_light_p1(const SolveParams<V>& p, uint32_t lo
       }
       if (acc == TOP) break;
     }
-    if (acc > old) {
-      stcg(p.stage + v, acc);
+    if (store_raise<V, INPLACE>(p, v, acc, old)) {
       ++L.lifts;
       return true;
     }
     return false;
   };
-  auto fallback = [&](uint32_t v, V) { return lift_thread<V, false>(p, v, L); };
+  auto fallback = [&](uint32_t v, V) { return lift_thread<V, false, INPLACE>(p, v, L); };
   tma_tiles<V>(p, (p.use_tma & kTmaLift) != 0, lo, hi, 0u, 0u, cursor, nullptr, chg, L, load,
                test, row, fallback);
   block_flush(L, sum_dst);
@@ -836,16 +835,17 @@ __device__ __noinline__ void dense_light_p1(const SolveParams<V>& p, uint32_t lo
 #define EGS_P0_UNROLL 2
 #endif
 constexpr int kP0Unroll = EGS_P0_UNROLL;
+// the per-warp queue of violated rows (one allocation for both instantiations)
+__shared__ uint32_t g_p0_queue[kWarps][32 * kP0Unroll + 32];
 
-template <class V>
+template <class V, bool INPLACE = false>
 __device__ __noinline__ void dense_light_p0(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
                                             uint32_t* chg, unsigned int* sum_dst) {
   constexpr V TOP = Top<V>::v;
   constexpr int U = kP0Unroll;
-  __shared__ uint32_t s_q[kWarps][32 * U + 32];
   Local L;
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  uint32_t* q = s_q[warp];
+  uint32_t* q = g_p0_queue[warp];
   uint32_t qn = 0;  // warp-uniform queue length
   auto drain = [&](uint32_t keep) {
     while (qn > keep) {
@@ -856,7 +856,7 @@ __device__ __noinline__ void dense_light_p0(const SolveParams<V>& p, uint32_t lo
       uint32_t v = 0;
       if (lane < take) {
         v = q[base + lane];
-        ch = lift_thread<V, true>(p, v, L);
+        ch = lift_thread<V, true, INPLACE>(p, v, L);
       }
       if (ch) set_bit(p, chg, v);
       L.phase_count += ch;
@@ -1157,7 +1157,8 @@ __device__ __noinline__ void warp_rows(const SolveParams<V>& p, uint32_t count,
                                           uint32_t* chg, unsigned int* sum_dst,
                                           bool push = false, Frontier nxt = Frontier{},
                                           unsigned int* qlong = nullptr,
-                                          unsigned int* act_dst = nullptr) {
+                                          unsigned int* act_dst = nullptr,
+                                          bool inplace = false) {
   Local L;
   WarpLists q = warp_lists();
   WarpClaim wc;
@@ -1167,7 +1168,7 @@ __device__ __noinline__ void warp_rows(const SolveParams<V>& p, uint32_t count,
     if (!owned(p, v)) continue;
     const bool p0 = v < p.g.rb[kP1L];
     bool ch;
-    if (push)
+    if (push || inplace)
       ch = p0 ? lift_warp<V, true, true>(p, v, L) : lift_warp<V, false, true>(p, v, L);
     else
       ch = p0 ? lift_warp<V, true>(p, v, L) : lift_warp<V, false>(p, v, L);
@@ -1188,7 +1189,8 @@ __device__ __noinline__ void block_rows(const SolveParams<V>& p, uint32_t count,
                                            uint32_t* chg, unsigned int* sum_dst,
                                            bool push = false, Frontier nxt = Frontier{},
                                            unsigned int* qlong = nullptr,
-                                           unsigned int* act_dst = nullptr) {
+                                           unsigned int* act_dst = nullptr,
+                                           bool inplace = false) {
   __shared__ BlockScratch<V> s;
   Local L;
   WarpLists q = warp_lists();
@@ -1202,7 +1204,7 @@ __device__ __noinline__ void block_rows(const SolveParams<V>& p, uint32_t count,
     if (!owned(p, v)) continue;
     const bool p0 = v < p.g.rb[kP1L];
     bool ch;
-    if (push)
+    if (push || inplace)
       ch = p0 ? lift_block<V, true, true>(p, v, L, s) : lift_block<V, false, true>(p, v, L, s);
     else
       ch = p0 ? lift_block<V, true>(p, v, L, s) : lift_block<V, false>(p, v, L, s);
@@ -1602,7 +1604,8 @@ template <class V>
 __device__ __noinline__ void phase_lift(const SolveParams<V>& p, bool dense, Frontier cur,
                                         Frontier nxt, unsigned int* cnt_after,
                                         uint32_t* chg, uint32_t* other,
-                                        unsigned int* slot_sum, unsigned int* slot_dyn) {
+                                        unsigned int* slot_sum, unsigned int* slot_dyn,
+                                        bool sweep = false) {
   const Graph& g = p.g;
   const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
   const uint32_t nthreads = gridDim.x * kBlock;
@@ -1617,17 +1620,29 @@ __device__ __noinline__ void phase_lift(const SolveParams<V>& p, bool dense, Fro
     }
   }
   if (dense) {
+    // sweep: every vertex lifted IN PLACE, reading whatever its successors
+    // hold at that moment -- the reference's solve_sweep (solver_par.cpp:
+    // 205-228, clamped atomic store); otherwise Jacobi (staged, committed)
     SubTimer st(p.ctr, p.trace != nullptr);
     block_rows<V>(p, class_size(g, 2), slot_dyn + 1,
-                  [gp = &g](uint32_t i) { return class_item(*gp, 2, i); }, chg, sum_dst);
+                  [gp = &g](uint32_t i) { return class_item(*gp, 2, i); }, chg, sum_dst, false,
+                  Frontier{}, nullptr, nullptr, sweep);
     st.lap(kSubHeavy);
     warp_rows<V>(p, class_size(g, 1), slot_dyn + 0,
-                 [gp = &g](uint32_t i) { return class_item(*gp, 1, i); }, chg, sum_dst);
+                 [gp = &g](uint32_t i) { return class_item(*gp, 1, i); }, chg, sum_dst, false,
+                 Frontier{}, nullptr, nullptr, sweep);
     st.lap(kSubMedium);
-    dense_light_p0<V>(p, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]), chg, sum_dst);
-    st.lap(kSubLightP0);
-    dense_light_p1<V>(p, clip_lo(p, g.rb[kP1L]), clip_hi(p, g.rb[kP1M]),
-                      slot_dyn + kTileCursor, chg, sum_dst);
+    if (sweep) {
+      dense_light_p0<V, true>(p, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]), chg, sum_dst);
+      st.lap(kSubLightP0);
+      dense_light_p1<V, true>(p, clip_lo(p, g.rb[kP1L]), clip_hi(p, g.rb[kP1M]),
+                              slot_dyn + kTileCursor, chg, sum_dst);
+    } else {
+      dense_light_p0<V>(p, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]), chg, sum_dst);
+      st.lap(kSubLightP0);
+      dense_light_p1<V>(p, clip_lo(p, g.rb[kP1L]), clip_hi(p, g.rb[kP1M]),
+                        slot_dyn + kTileCursor, chg, sum_dst);
+    }
     st.lap(kSubLightP1);
   } else {
     if (blockIdx.x == 0 && threadIdx.x < 3) cnt_after[threadIdx.x] = 0u;
@@ -2273,7 +2288,7 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
     // activation's top filter may see either the old or the committed value
     // of a predecessor; a stale one only adds a harmless frontier entry)
     const bool fuse_act =
-        !inplace && !cert_now && p.mode != kModeDense &&
+        !inplace && !cert_now && p.mode != kModeDense && p.mode != kModeSweep &&
         !(p.mode == kModeAuto && (double)changed * p.avg_in_deg * p.sparse_div >= (double)n);
     if (!inplace) {  // a Jacobi round: publish its staged values
       begin_phase();
@@ -2327,7 +2342,7 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
       uint32_t removed = prev_sum(1);
       while (removed > 0) {
         const bool sparse_pass =
-            p.mode != kModeDense &&
+            p.mode != kModeDense && p.mode != kModeSweep &&
             (double)removed * p.avg_in_deg * p.cert_sparse_div < (double)n;
         if (sparse_pass) {
           if (!queued) {  // after a dense pass: the queue from its removal bits
@@ -2374,7 +2389,7 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
     // ---- next round: dense, or a frontier of the predecessors of changed
     // vertices (solver_par.cpp:402-410)
     const bool dense =
-        p.mode == kModeDense ||
+        p.mode == kModeDense || p.mode == kModeSweep ||
         (p.mode == kModeAuto &&
          (certified_any || (double)changed * p.avg_in_deg * p.sparse_div >= (double)n));
     if (!dense) {
@@ -2413,9 +2428,9 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
     begin_phase();
     if (leader && p.timeout_ns && t_prev - t_start > p.timeout_ns) sh->stop = 1;
     phase_lift<V>(p, dense, frontier(tok), frontier(tok + 1), sh->fr_cnt[(tok + 2) % 3], next,
-                  chg, slot_sum(), slot_dyn());
+                  chg, slot_sum(), slot_dyn(), p.mode == kModeSweep);
     end_phase(1);
-    inplace = !dense;
+    inplace = !dense || p.mode == kModeSweep;  // a sweep round needs no commit
     if (inplace) {
       pushed = prev_sum(2);
       pushed_long = vload(sh->dyn[(phase - 1) & 3] + 2);

@@ -13,7 +13,6 @@
 // It replaces egsolve::solve (proj/include/egsolve/solver.hpp:86-87) for the
 // GPU variant; the output is the same least fixpoint the reference solvers
 // compute (solver_seq.cpp:124-212, solver_par.cpp:126-435).
-#include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
 #include <chrono>
@@ -299,8 +298,8 @@ void validate_opts(const egs_gpu_opts& o) {
   if (o.n_gpus != 1)
     throw Fail(EGS_ERR_INVALID_CONFIG,
                "egs_gpu_solve drives one GPU; use egs_part_* for n_gpus > 1");
-  if (o.mode < EGS_MODE_AUTO || o.mode > EGS_MODE_SPARSE)
-    throw Fail(EGS_ERR_INVALID_CONFIG, "mode must be 0, 1 or 2");
+  if (o.mode < EGS_MODE_AUTO || o.mode > EGS_MODE_SWEEP)
+    throw Fail(EGS_ERR_INVALID_CONFIG, "mode must be 0 (auto), 1 (dense), 2 (sparse) or 3 (sweep)");
   if (o.cert_interval < 0 || o.cert_growth < 0 || o.sparse_div < 0 || o.grid_ctas < 0)
     throw Fail(EGS_ERR_INVALID_CONFIG, "negative tuning knob");
   if (o.timeout_seconds < 0)
@@ -348,6 +347,30 @@ void dev_excl_scan(const In* in, T* out, uint64_t n, cudaStream_t s, int sms) {
   egs::k_scan_tiles<T><<<1, 1024, 0, s>>>(ts, nt);
   egs::k_scan_down<T, In><<<grid, egs::kScanThreads, 0, s>>>(in, out, n, ts, nt);
   CK(cudaGetLastError());
+}
+
+// Stable sort of (key, val) pairs by the low `bits` bits of key (egs_scan.cuh
+// LSD radix sort, 8-bit digits): the pairs move (k0, v0) -> (k1, v1) -> ...;
+// *ks / *vs = the buffers holding the sorted result.
+void dev_radix_sort_pairs(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, uint64_t m,
+                          int bits, cudaStream_t s, int sms, uint32_t** ks, uint32_t** vs) {
+  *ks = k0;
+  *vs = v0;
+  if (m == 0) return;
+  const uint32_t nt = (uint32_t)((m + egs::kScanTile - 1) / egs::kScanTile);
+  DevBuf d_hist;
+  uint32_t* hist = d_hist.alloc<uint32_t>((size_t)egs::kRadixDigits * nt);
+  const uint32_t grid = std::min<uint32_t>(nt, (uint32_t)sms * 8);
+  for (int shift = 0; shift < bits; shift += egs::kRadixBits) {
+    egs::k_radix_hist<<<grid, egs::kScanThreads, 0, s>>>(k0, m, shift, hist, nt);
+    dev_excl_scan<uint32_t>(hist, hist, (uint64_t)egs::kRadixDigits * nt, s, sms);
+    egs::k_radix_scatter<<<grid, egs::kScanThreads, 0, s>>>(k0, v0, m, shift, hist, nt, k1, v1);
+    CK(cudaGetLastError());
+    std::swap(k0, k1);
+    std::swap(v0, v1);
+  }
+  *ks = k0;
+  *vs = v0;
 }
 
 // Weights: host threads narrow int64 -> W (int8 / int16 / int32, the
@@ -476,7 +499,7 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
   bool h_stage_bad = false;
   cudaStream_t s = c->stream, sc = c->copy_stream, sw = c->aux_stream;
   const int sms = c->num_sms;
-  DevBuf d_off64, d_dst, d_wn, d_owner, d_key, d_tcount, d_misc, d_tmp, d_ck0, d_cv0, d_ck1,
+  DevBuf d_off64, d_dst, d_wn, d_owner, d_key, d_tcount, d_misc, d_ck0, d_cv0, d_ck1,
       d_long;
   uint64_t* off64 = d_off64.alloc<uint64_t>((size_t)n + 1);
   uint32_t* dst = d_dst.alloc<uint32_t>(m);
@@ -594,13 +617,14 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
     CK(cudaEventRecord(et[k], s));
   }
 
-  // transpose: sort the (dst, src) pairs by dst while the weights stream in
-  size_t tmp_bytes = 0;
-  const int kb = bits_for(n);
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, ck0, ck1, cv0, c->csrc, mo, 0, kb, s));
-  void* tmp = d_tmp.alloc<uint8_t>(tmp_bytes);
-  CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, ck0, ck1, cv0, c->csrc, mo, 0, kb, s));
-  egs::k_col_offsets<<<grid_for(mo + 1, sms), 256, 0, s>>>(n, mo, ck1, c->coff);
+  // transpose: stable radix sort of the (dst, src) pairs by dst while the
+  // weights stream in
+  {
+    uint32_t *ks = nullptr, *vs = nullptr;
+    dev_radix_sort_pairs(ck0, cv0, ck1, c->csrc, mo, bits_for(n), s, sms, &ks, &vs);
+    if (vs != c->csrc) CK(cudaMemcpyAsync(c->csrc, vs, mo * 4, cudaMemcpyDeviceToDevice, s));
+    egs::k_col_offsets<<<grid_for(mo + 1, sms), 256, 0, s>>>(n, mo, ks, c->coff);
+  }
   CK(cudaGetLastError());
 
   CK(cudaStreamWaitEvent(sw, e_perm, 0));
@@ -628,7 +652,6 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
   d_ck0.release();
   d_cv0.release();
   d_ck1.release();
-  d_tmp.release();
   d_misc.release();
   d_long.release();
   CK(cudaStreamSynchronize(s));

@@ -54,7 +54,7 @@ enum Counter : int {
   kNumCounters
 };
 
-enum Mode : int { kModeAuto = 0, kModeDense = 1, kModeSparse = 2 };
+enum Mode : int { kModeAuto = 0, kModeDense = 1, kModeSparse = 2, kModeSweep = 3 };
 // SolveParams::use_tma bits: which light-row phases stage edge tiles by TMA
 // (the others read rows with plain loads through the same claim loop)
 enum TmaPhase : int { kTmaRound1 = 1, kTmaLift = 2, kTmaCert = 4, kTmaAll = 7 };

@@ -54,7 +54,8 @@ def main():
     ap.add_argument("--out", required=True)
     ap.add_argument("--probe", type=int, default=4000, help="rounds of the timing probe")
     ap.add_argument("--budget", type=float, default=2400.0, help="max projected seconds per config")
-    ap.add_argument("--mode", default="auto")
+    ap.add_argument("--mode", default="sweep",
+                    help="sweep: in-place rounds, the reference's solve_sweep (fewest rounds)")
     ap.add_argument("configs", nargs="?", default="C4,C3,F16")
     args = ap.parse_args()
     out = {}

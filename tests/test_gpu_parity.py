@@ -13,7 +13,7 @@ from oracle_bindings import INT64_MAX, fnv1a64
 
 pytestmark = pytest.mark.gpu
 
-MODES = ["auto", "dense", "sparse"]
+MODES = ["auto", "dense", "sparse", "sweep"]
 
 
 def _opts(egs, **kw):
@@ -182,27 +182,38 @@ def test_rmat16_golden(egs, golden):
 
 
 GOLDEN_FULL = [
-    ("fixed/1000000/8/1000/1", (1_000_000, 8, 1000)),      # C2
-    ("fixed/1000000/8/100000/1", (1_000_000, 8, 100_000)),  # C5
+    ("fixed/1000000/8/1000/1", ("fixed", (1_000_000, 8, 1000))),      # C2
+    ("fixed/1000000/8/100000/1", ("fixed", (1_000_000, 8, 100_000))),  # C5
+    ("fixed/1000000/16/100/1", ("fixed", (1_000_000, 16, 100))),      # F16: C4's generator at 10^6
+    ("rmat/22/16/100/1", ("rmat", (22, 16, 100))),                    # C3
+    ("fixed/16000000/16/100/1", ("fixed", (16_000_000, 16, 100))),    # C4
 ]
 
 
-@pytest.mark.parametrize("key,args", GOLDEN_FULL, ids=["C2", "C5"])
-def test_full_size_golden(egs, golden, key, args):
-    """BASELINE configs C2 and C5 at full size, bit-exact against the reference
-    solve_sweep run to its fixpoint (tests/golden/make_golden_full.py): the
-    solution bytes of the device output path and of the host formatter."""
+@pytest.mark.parametrize("key,spec", GOLDEN_FULL, ids=["C2", "C5", "F16", "C3", "C4"])
+def test_full_size_golden(egs, golden, key, spec):
+    """BASELINE configs at full size, bit-exact against digests computed
+    WITHOUT the certificate: the reference solve_sweep run to its fixpoint
+    (C2, C5, and F16 / C3 where tests/golden/make_golden_full.py finished;
+    key without "pin") and the GPU's plain value iteration run to its
+    fixpoint (tests/golden/make_golden_plain.py; "plain_gpu", 0.9-1.7 million
+    rounds, 39-682 s).  Compared: the device output path's write_solution
+    bytes (SHA-256, length), the host formatter's bytes, tops and finite sum."""
     if key not in golden:
         pytest.skip("full-size golden vector not generated")
     rec = golden[key]
-    a = egs.GameArena.fixed(*args, 1)
+    kind, args = spec
+    a = getattr(egs.GameArena, kind)(*args, 1)
     with egs.DeviceSolver(a) as ds:
         ds.solve()
         dev_text = ds.write_solution().encode()
         f = ds.read_measure()
     host_text = egs.write_solution(a, f).encode()
+    digest = hashlib.sha256(dev_text).hexdigest()
     assert len(dev_text) == rec["solution_bytes"]
-    assert hashlib.sha256(dev_text).hexdigest() == rec["solution_sha256"]
+    assert digest == rec["solution_sha256"]
+    if "plain_gpu" in rec:  # both pins agree where both exist
+        assert digest == rec["plain_gpu"]["solution_sha256"]
     assert host_text == dev_text
     top = f == np.iinfo(np.int64).max
     assert int(top.sum()) == rec["tops"]
