@@ -16,6 +16,7 @@
 // Every kernel here runs once per arena upload, not per solve.
 #pragma once
 
+#include <climits>
 #include <cstdint>
 
 #include "egs_device.cuh"
@@ -183,6 +184,61 @@ __global__ void __launch_bounds__(256)
         px[idx + d] |= (uint32_t)(int)wn[idx] << tbits;
       else
         ex[2 * (size_t)(idx + d) + 1] = (int)wn[idx];
+    }
+  }
+}
+
+// Player-1 light rows (<= 32 edges) sorted by weight, ascending (ties by
+// target), once per upload.  A player-1 row's order is free: its lift is a
+// max (measure_ops.hpp:44-48) and no player-1 strategy is printed
+// (extract_strategy, measure_ops.cpp:56-80, covers player 0 only; player-0
+// rows keep the reference order).  Sorted, the first record holds the
+// row's least weight, which is round 1's value (delta(0)(v) = max(0, -w_min)),
+// and the certificate meets the likeliest good edges first (egs_solve.cuh).
+// One warp per row: a 32-lane bitonic sort of the records as signed keys
+// (packed: w in the high bits, so int32 order is (w, dst) order; wide:
+// (w, dst) as an int64).  key[o] is the class of original row o
+// (egs_scan.cuh k_class_tiles); class 3 = player-1 light.
+template <class K>
+__device__ __forceinline__ K bitonic32(K x) {
+  const uint32_t lane = lane_id();
+#pragma unroll
+  for (uint32_t k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      const K y = __shfl_xor_sync(0xffffffffu, x, j);
+      const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+      x = (lower == up) ? (y < x ? y : x) : (y > x ? y : x);
+    }
+  }
+  return x;
+}
+
+__global__ void __launch_bounds__(256)
+    k_sort_p1_rows(uint32_t r0, uint32_t r1, const uint8_t* key, const uint32_t* perm,
+                   const uint32_t* off_new, void* edge, uint32_t tbits, uint32_t own_lo,
+                   uint32_t own_hi) {
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  const uint32_t lane = lane_id();
+  for (uint32_t o = r0 + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); o < r1; o += nwarps) {
+    if (key[o] != (uint8_t)kP1L) continue;  // warp-uniform
+    const uint32_t v = perm[o];
+    if (v < own_lo || v >= own_hi) continue;
+    const uint32_t b = off_new[v], len = off_new[v + 1] - b;
+    if (len < 2) continue;
+    if (tbits) {
+      int* rec = static_cast<int*>(edge) + b;
+      const int x = bitonic32<int>(lane < len ? rec[lane] : INT32_MAX);
+      if (lane < len) rec[lane] = x;
+    } else {
+      int2* rec = static_cast<int2*>(edge) + b;
+      long long x = LLONG_MAX;
+      if (lane < len) {
+        const int2 r = rec[lane];
+        x = ((long long)r.y << 32) | (long long)(uint32_t)r.x;
+      }
+      x = bitonic32<long long>(x);
+      if (lane < len) rec[lane] = make_int2((int)(uint32_t)x, (int)(x >> 32));
     }
   }
 }

@@ -1584,13 +1584,46 @@ __device__ __noinline__ void round1_long(const SolveParams<V>& p, uint32_t* chg,
   block_flush(L, sum_dst);
 }
 
+// Player-1 light rows: sorted by weight at upload (egs_build.cuh
+// k_sort_p1_rows), so delta(0)(v) = max(0, -w_min) is read from the first
+// record -- one load per vertex instead of the row.
+template <class V>
+__device__ __noinline__ void round1_p1_light(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
+                                             uint32_t* chg, unsigned int* sum_dst) {
+  const Graph& g = p.g;
+  Local L;
+  const uint32_t nwarps = gridDim.x * kWarps;
+  const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5, lane = lane_id();
+  for (uint32_t w = (lo >> 5) + gw; w < ((hi + 31) >> 5); w += nwarps) {
+    const uint32_t v = (w << 5) + lane;
+    bool ch = false;
+    if (v >= lo && v < hi) {
+      const uint32_t b = __ldg(g.off + v), e = __ldg(g.off + v + 1);
+      const V val = ominus_cap<V>(V(0), rec_w(g, __ldcs(erecs(g) + b)), g.cap);
+      ++L.visits;
+      ++L.apps;
+      L.edges += e - b;  // one lift application relaxes the row
+      if (val > V(0)) {
+        stcg(p.stage + v, val);
+        ++L.lifts;
+        ch = true;
+      }
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, ch);
+    if (m && lane == 0) bits_or(p, chg + w, m);
+    L.phase_count += ch;
+  }
+  block_flush(L, sum_dst);
+}
+
 template <class V>
 __device__ __noinline__ void phase_round1(const SolveParams<V>& p, uint32_t* chg,
                                           unsigned int* slot_sum, unsigned int* slot_dyn) {
   const Graph& g = p.g;
   round1_long<V>(p, chg, slot_sum + 0, slot_dyn);
-  round1_light<V>(p, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]), clip_lo(p, g.rb[kP1L]),
-                  clip_hi(p, g.rb[kP1M]), slot_dyn + kTileCursor, chg, slot_sum + 0);
+  round1_light<V>(p, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]), 0u, 0u,
+                  slot_dyn + kTileCursor, chg, slot_sum + 0);
+  round1_p1_light<V>(p, clip_lo(p, g.rb[kP1L]), clip_hi(p, g.rb[kP1M]), chg, slot_sum + 0);
 }
 
 // One lift round.  Dense (Jacobi): every vertex, raised values staged for
@@ -1704,7 +1737,7 @@ __device__ __forceinline__ void commit_stage_loads(const SolveParams<V>& p, bool
 // debug_checks (the reference's check_monotone, solver_par.cpp:116-124,179):
 // a value a commit publishes must be above the one it replaces
 template <class V, int U>
-__device__ __noinline__ void debug_check_raise(const SolveParams<V>& p, uint32_t w0,
+__device__ __forceinline__ void debug_check_raise(const SolveParams<V>& p, uint32_t w0,
                                                uint32_t lane, const uint32_t (&bits)[U],
                                                const V (&val)[U]) {
 #pragma unroll
@@ -1725,16 +1758,25 @@ __device__ __noinline__ void phase_commit(const SolveParams<V>& p, const uint32_
   const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5;
   const uint32_t lane = lane_id();
   const uint32_t wlo = p.own_lo >> 5, whi = min(nwords, (p.own_hi + 31) >> 5);
+  // (scalars of p read once: stores through p.f may alias p for the compiler)
+  const bool multi = p.world > 1, debug = p.debug != 0;
+  V* const f = p.f;
   for (uint32_t w0 = wlo + gw * U; w0 < whi; w0 += nwarps * U) {
     uint32_t bits[U];
     V val[U];
 #pragma unroll
-    for (int k = 0; k < U; ++k) bits[k] = w0 + k < whi ? ldcg(chg + w0 + k) & own_mask(p, w0 + k) : 0u;
+    for (int k = 0; k < U; ++k)
+      bits[k] = w0 + k < whi ? ldcg(chg + w0 + k) & (multi ? own_mask(p, w0 + k) : ~0u) : 0u;
     commit_stage_loads<V, U>(p, dense, w0, whi, lane, bits, val, V(0));
-    if (p.debug) debug_check_raise<V, U>(p, w0, lane, bits, val);
+    if (debug) debug_check_raise<V, U>(p, w0, lane, bits, val);
 #pragma unroll
     for (int k = 0; k < U; ++k)
-      if ((bits[k] >> lane) & 1u) f_put<V>(p, ((w0 + k) << 5) + lane, val[k]);
+      if ((bits[k] >> lane) & 1u) {
+        if (multi)
+          f_put<V>(p, ((w0 + k) << 5) + lane, val[k]);
+        else
+          stcg(f + ((w0 + k) << 5) + lane, val[k]);
+      }
   }
 }
 
@@ -1779,21 +1821,31 @@ __device__ __noinline__ void phase_commit_cert_init(const SolveParams<V>& p, con
   const uint32_t gw = tid >> 5, lane = lane_id();
   for (uint32_t w = tid; w < nwords; w += gridDim.x * kBlock) p.rbm[1][w] = 0u;
   const uint32_t wlo = p.own_lo >> 5, whi = min(nwords, (p.own_hi + 31) >> 5);
+  const bool multi = p.world > 1, debug = p.debug != 0;
+  V* const f = p.f;
+  uint32_t* const cand = p.cand;
   for (uint32_t w0 = wlo + gw * U; w0 < whi; w0 += nwarps * U) {
     uint32_t bits[U];
     V val[U];
 #pragma unroll
-    for (int k = 0; k < U; ++k) bits[k] = w0 + k < whi ? ldcg(chg + w0 + k) & own_mask(p, w0 + k) : 0u;
+    for (int k = 0; k < U; ++k)
+      bits[k] = w0 + k < whi ? ldcg(chg + w0 + k) & (multi ? own_mask(p, w0 + k) : ~0u) : 0u;
     commit_stage_loads<V, U>(p, dense, w0, whi, lane, bits, val, TOP);
-    if (p.debug) debug_check_raise<V, U>(p, w0, lane, bits, val);
+    if (debug) debug_check_raise<V, U>(p, w0, lane, bits, val);
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       if (w0 + k >= whi) break;
       const bool raised = (bits[k] >> lane) & 1u;
       const bool c = raised && val[k] != TOP;
-      if (raised) f_put<V>(p, ((w0 + k) << 5) + lane, c ? val[k] | CandFlag<V>::v : val[k]);
+      const V x = c ? val[k] | CandFlag<V>::v : val[k];
+      if (raised) {
+        if (multi)
+          f_put<V>(p, ((w0 + k) << 5) + lane, x);
+        else
+          stcg(f + ((w0 + k) << 5) + lane, x);
+      }
       const uint32_t m = __ballot_sync(0xffffffffu, c);
-      if (lane == 0) stcg(p.cand + w0 + k, m);
+      if (lane == 0) stcg(cand + w0 + k, m);
     }
   }
 }
@@ -1868,6 +1920,30 @@ __device__ __forceinline__ void cert_long_rows(const SolveParams<V>& p, uint32_t
   }
 }
 
+// Player-1 light candidates of a dense certificate pass, one row per lane in
+// row order (sorted by weight: the most negative, likeliest good edges
+// first), warps striding over the candidate bitmap words; removals go to
+// rbm.  Warp-uniform.
+template <class V>
+__device__ __forceinline__ void cert_p1_light(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
+                                              uint32_t* rbm, Local& L, WarpLists& q,
+                                              const Frontier& qt) {
+  if (hi <= lo) return;
+  const uint32_t nwarps = gridDim.x * kWarps;
+  const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5, lane = lane_id();
+  for (uint32_t w = (lo >> 5) + gw; w < ((hi + 31) >> 5); w += nwarps) {
+    const uint32_t mw = ldcg(p.cand + w);
+    if (!mw) continue;  // warp-uniform
+    const uint32_t v = (w << 5) + lane;
+    bool removed = false;
+    if (((mw >> lane) & 1u) && v >= lo && v < hi) removed = cert_check_thread<V>(p, v, L);
+    const uint32_t m = __ballot_sync(0xffffffffu, removed);
+    if (m && lane == 0) bits_or(p, rbm + w, m);
+    L.phase_count += removed;
+    push_cert_preds<V>(p, removed, v, q, qt, L);
+  }
+}
+
 // Dense pass over every owned candidate (removed count -> slot_sum[1]).
 // `rbm_clear` (the bitmap two passes old) is zeroed for reuse.
 template <class V>
@@ -1939,10 +2015,14 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
     };
     auto fallback = [&](uint32_t v, V) { return cert_check_thread<V>(p, v, L); };
     auto after = [&](uint32_t v, bool removed) { push_cert_preds<V>(p, removed, v, q, qt, L); };
+    // player-0 light candidates through the tile pipeline (kept ones read
+    // their whole row); player-1 light rows are sorted by weight (build), so
+    // their first records are the likeliest good edges: a lane reads its own
+    // row start directly and most rows end with the first chunk
     tma_tiles<V>(p, (p.use_tma & kTmaCert) != 0, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]),
-                 clip_lo(p, g.rb[kP1L]),
-                 clip_hi(p, g.rb[kP1M]), slot_dyn + kTileCursor, p.cand, rbm, L, load, test,
-                 row, fallback, after);
+                 0u, 0u, slot_dyn + kTileCursor, p.cand, rbm, L, load, test, row, fallback,
+                 after);
+    cert_p1_light<V>(p, clip_lo(p, g.rb[kP1L]), clip_hi(p, g.rb[kP1M]), rbm, L, q, qt);
   }
   if (qt.cnt)
     for (int c = 0; c < 3; ++c) lists_flush(q, c, qt.list[c], qt.cnt + c);
@@ -2040,6 +2120,8 @@ __device__ __noinline__ void phase_cert_apply(const SolveParams<V>& p, uint32_t*
   Local L;
   constexpr uint32_t U = 8;  // words per warp step, loads issued together
   const uint32_t w_lo = p.own_lo >> 5, w_hi = (p.own_hi + 31) >> 5;
+  const bool multi = p.world > 1;
+  V* const f = p.f;
   for (uint32_t w0 = w_lo + gw * U; w0 < w_hi; w0 += nwarps * U) {
     uint32_t m[U];
 #pragma unroll
@@ -2047,8 +2129,13 @@ __device__ __noinline__ void phase_cert_apply(const SolveParams<V>& p, uint32_t*
 #pragma unroll
     for (uint32_t k = 0; k < U; ++k) {
       const bool hit = (m[k] >> lane) & 1u;  // candidate words hold owned, non-top ids only
-      if (hit) f_put<V>(p, ((w0 + k) << 5) + lane, Top<V>::v);
-      if (m[k] && lane == 0) bits_or(p, chg + w0 + k, m[k]);
+      if (multi) {
+        if (hit) f_put<V>(p, ((w0 + k) << 5) + lane, Top<V>::v);
+        if (m[k] && lane == 0) bits_or(p, chg + w0 + k, m[k]);
+      } else {
+        if (hit) stcg(f + ((w0 + k) << 5) + lane, Top<V>::v);
+        if (m[k] && lane == 0) atomicOr(chg + w0 + k, m[k]);
+      }
       L.phase_count += hit;
       L.certified += hit;
     }

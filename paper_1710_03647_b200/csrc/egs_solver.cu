@@ -389,7 +389,7 @@ struct LongRows {
 template <class W>
 bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint32_t>& rows,
                     std::vector<cudaEvent_t>& ew, std::vector<cudaEvent_t>& et,
-                    const uint64_t* off64, void* wdev, LongRows lw) {
+                    const uint64_t* off64, void* wdev, LongRows lw, const uint8_t* key) {
   cudaStream_t sc = c->copy_stream, sw = c->aux_stream;
   const int nch = (int)rows.size() - 1;
   const uint64_t m = c->m;
@@ -473,6 +473,11 @@ bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint3
                                               lw.cnt + k, c->own_lo, c->own_hi);
     egs::k_relabel_weights_long<W><<<2 * c->num_sms, 256, 0, sw>>>(
         lw.list + (size_t)k * lw.cap, lw.cnt + k, off64, wd, c->perm, c->off, c->edge, c->tbits);
+    // the chunk's player-1 light rows, complete now: sorted by weight
+    if (!c->tbits) CK(cudaStreamWaitEvent(sw, et[k], 0));  // (wide: targets written apart)
+    egs::k_sort_p1_rows<<<grid_for((uint64_t)(rows[k + 1] - rows[k]) * 32, c->num_sms), 256, 0,
+                          sw>>>(rows[k], rows[k + 1], key, c->perm, c->off, c->edge, c->tbits,
+                                c->own_lo, c->own_hi);
     CK(cudaGetLastError());
   }
   for (auto& th : pool) th.join();
@@ -631,11 +636,11 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
   {
     const int64_t mw = a->max_abs_weight;
     if (mw <= 127)
-      h_stage_bad = upload_weights<int8_t>(c, a, rows, ew, et, off64, wn, lw);
+      h_stage_bad = upload_weights<int8_t>(c, a, rows, ew, et, off64, wn, lw, key);
     else if (mw <= 32767)
-      h_stage_bad = upload_weights<int16_t>(c, a, rows, ew, et, off64, wn, lw);
+      h_stage_bad = upload_weights<int16_t>(c, a, rows, ew, et, off64, wn, lw, key);
     else
-      h_stage_bad = upload_weights<int32_t>(c, a, rows, ew, et, off64, wn, lw);
+      h_stage_bad = upload_weights<int32_t>(c, a, rows, ew, et, off64, wn, lw, key);
   }
   tm.mark("upload + relabel + CSC sort");
   CK(cudaEventRecord(e_tail, sw));
