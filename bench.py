@@ -467,8 +467,9 @@ def run_our_arm_partitioned(a):
     rounds = rep.rounds
     part.close()
 
-    # e2e: this rank's upload + device build, handle exchange, solve, D2H
-    h2d = h2d_bytes(arena)
+    # e2e: this rank's upload (its own rows) + device build, handle exchange,
+    # solve, D2H
+    h2d_rank = 0
     e2e_t, e2e_edges = 0.0, 0
     for _ in range(a.e2e_steps):
         barrier(world)
@@ -476,6 +477,7 @@ def run_our_arm_partitioned(a):
         r = solve_distributed(arena, opts, comm=comm)
         e2e_t += time.perf_counter() - t1
         e2e_edges += r.edges_relaxed
+        h2d_rank = r.h2d_bytes
         assert np.array_equal(r.measure, f_dev)
     e2e_t = max_over_ranks(e2e_t, world, red_dev)
     e2e_edges = sum_over_ranks(e2e_edges, world, red_dev)
@@ -492,7 +494,8 @@ def run_our_arm_partitioned(a):
                                   "barriers in peer memory)",
                    "l2": "inputs larger than L2; no flush"},
         "solve": {"rounds": rounds, "plan_edges": rep.plan["edges"]},
-        "e2e": {"value": e2e_edges / e2e_t / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
+        "e2e": {"value": e2e_edges / e2e_t / 1e9, "unit": UNIT,
+                "h2d_bytes_per_step": int(sum_over_ranks(h2d_rank, world, red_dev)),
                 "d2h_bytes_per_step": n * 8 * world, "ms_per_step": e2e_t / a.e2e_steps * 1e3,
                 "api": "egs_part_create / egs_part_connect / egs_part_solve (include/egs_gpu.h)"},
         "gpu_launches": a.steps,

@@ -149,6 +149,8 @@ typedef struct egs_gpu_stats {
   uint64_t algo_bytes_s8d; /* SURVEY.md §8(d) exactly: edges_relaxed * (8 + s)
                               + applications * (4 + 2 s) + activations * 4,
                               s = value bytes */
+  uint64_t h2d_bytes;      /* bytes the arena upload moved host -> device (a
+                              partition rank: its own rows only) */
 } egs_gpu_stats;
 
 void egs_gpu_opts_default(egs_gpu_opts* opts);

@@ -152,7 +152,7 @@ class GpuStats(C.Structure):
            ("grid_ctas", C.c_uint32), ("lift_sub_seconds", C.c_double * 5),
            ("phase_detail_seconds", C.c_double * 5),
            ("edge_bytes", C.c_uint32), ("reserved0", C.c_uint32),
-           ("algo_bytes_s8d", C.c_uint64)]
+           ("algo_bytes_s8d", C.c_uint64), ("h2d_bytes", C.c_uint64)]
     )
 
     def as_dict(self) -> dict:

@@ -191,6 +191,10 @@ struct egs_ctx {
   egs::XSync* xsync = nullptr;
   unsigned int epoch = 0;  // cross-rank barriers passed (same on every rank)
   bool connected = false;
+  // sharded upload: the original-id row ranges this rank uploads (its own
+  // rows, small gaps merged); empty = every row
+  std::vector<std::pair<uint32_t, uint32_t>> runs;
+  uint64_t h2d_bytes = 0;  // host -> device bytes of the last upload
 
   egs::Graph graph() const {
     egs::Graph g{};
@@ -388,6 +392,7 @@ struct LongRows {
 
 template <class W>
 bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint32_t>& rows,
+                    const std::vector<std::vector<std::pair<uint64_t, uint64_t>>>& spans,
                     std::vector<cudaEvent_t>& ew, std::vector<cudaEvent_t>& et,
                     const uint64_t* off64, void* wdev, LongRows lw, const uint8_t* key) {
   cudaStream_t sc = c->copy_stream, sw = c->aux_stream;
@@ -407,15 +412,19 @@ bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint3
   const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
   const int T = m >= (1u << 20) ? (int)hw - 1 : 0;  // helpers besides this thread
   constexpr uint64_t kBlk = 1u << 18;
-  auto span_of = [&](int k) {
-    return std::make_pair(a->csr_offsets[rows[k]], a->csr_offsets[rows[k + 1]]);
+  // blocks of the chunks' upload spans (block b of span s of chunk k)
+  struct Blk {
+    uint64_t lo, hi;
+    int k;
   };
+  std::vector<Blk> blocks;
   std::vector<uint64_t> bfirst(nch + 1, 0);  // first block of each chunk
   for (int k = 0; k < nch; ++k) {
-    const auto [e0, e1] = span_of(k);
-    bfirst[k + 1] = bfirst[k] + (e1 - e0 + kBlk - 1) / kBlk;
+    for (const auto& [e0, e1] : spans[k])
+      for (uint64_t lo = e0; lo < e1; lo += kBlk) blocks.push_back({lo, std::min(e1, lo + kBlk), k});
+    bfirst[k + 1] = blocks.size();
   }
-  const uint64_t nblk = bfirst[nch];
+  const uint64_t nblk = blocks.size();
   std::vector<std::atomic<uint64_t>> left(nch);  // blocks of the chunk not yet converted
   for (int k = 0; k < nch; ++k) left[k].store(bfirst[k + 1] - bfirst[k]);
   std::atomic<uint64_t> next{0};
@@ -425,9 +434,8 @@ bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint3
   auto one_block = [&](int& k) {
     const uint64_t b = next.fetch_add(1, std::memory_order_relaxed);
     if (b >= nblk) return false;
-    while (b >= bfirst[k + 1]) ++k;
-    const auto [e0, e1] = span_of(k);
-    const uint64_t lo = e0 + (b - bfirst[k]) * kBlk, hi = std::min(e1, lo + kBlk);
+    k = blocks[b].k;
+    const uint64_t lo = blocks[b].lo, hi = blocks[b].hi;
     bool bad = false;
     for (uint64_t i = lo; i < hi; ++i) {
       const int64_t x = w[i];
@@ -461,8 +469,10 @@ bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint3
   for (int k = 0; k < nch; ++k) {
     while (left[k].load(std::memory_order_acquire) > 0)
       if (!one_block(kself)) std::this_thread::yield();
-    const auto [e0, e1] = span_of(k);
-    CK(cudaMemcpyAsync(wd + e0, stage + e0, (e1 - e0) * sizeof(W), cudaMemcpyHostToDevice, sc));
+    for (const auto& [e0, e1] : spans[k]) {
+      CK(cudaMemcpyAsync(wd + e0, stage + e0, (e1 - e0) * sizeof(W), cudaMemcpyHostToDevice, sc));
+      c->h2d_bytes += (e1 - e0) * sizeof(W);
+    }
     CK(cudaEventRecord(ew[k], sc));
     CK(cudaStreamWaitEvent(sw, ew[k], 0));
     // packed records: the weight bits are or-ed into the target words
@@ -567,17 +577,36 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
     CK(cudaEventCreateWithFlags(&ew[k], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&et[k], cudaEventDisableTiming));
   }
-  auto span_of = [&](int k) {
-    return std::make_pair(a->csr_offsets[rows[k]], a->csr_offsets[rows[k + 1]]);
-  };
+  // the edge ranges each chunk uploads: the chunk's whole span, or (sharded
+  // multi-GPU upload) its intersection with this rank's row runs -- rows of
+  // other ranks never cross PCIe (the relabel kernels skip them)
+  std::vector<std::vector<std::pair<uint64_t, uint64_t>>> spans(nch);
+  {
+    size_t ri = 0;
+    for (int k = 0; k < nch; ++k) {
+      if (c->runs.empty()) {
+        spans[k].emplace_back(a->csr_offsets[rows[k]], a->csr_offsets[rows[k + 1]]);
+        continue;
+      }
+      while (ri < c->runs.size() && c->runs[ri].second <= rows[k]) ++ri;
+      for (size_t j = ri; j < c->runs.size() && c->runs[j].first < rows[k + 1]; ++j) {
+        const uint32_t v0 = std::max(c->runs[j].first, rows[k]);
+        const uint32_t v1 = std::min(c->runs[j].second, rows[k + 1]);
+        if (v1 > v0) spans[k].emplace_back(a->csr_offsets[v0], a->csr_offsets[v1]);
+      }
+    }
+  }
+  c->h2d_bytes = ((uint64_t)n + 1) * 8 + n;
 
   // upload: vertices, then targets, then weights
   CK(cudaMemcpyAsync(off64, a->csr_offsets, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice, sc));
   CK(cudaMemcpyAsync(owner, a->owners, n, cudaMemcpyHostToDevice, sc));
   CK(cudaEventRecord(e_vert, sc));
   for (int k = 0; k < nch; ++k) {
-    const auto [e0, e1] = span_of(k);
-    CK(cudaMemcpyAsync(dst + e0, a->csr_targets + e0, (e1 - e0) * 4, cudaMemcpyHostToDevice, sc));
+    for (const auto& [e0, e1] : spans[k]) {
+      CK(cudaMemcpyAsync(dst + e0, a->csr_targets + e0, (e1 - e0) * 4, cudaMemcpyHostToDevice, sc));
+      c->h2d_bytes += (e1 - e0) * 4;
+    }
     CK(cudaEventRecord(ex[k], sc));
   }
 
@@ -636,11 +665,11 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
   {
     const int64_t mw = a->max_abs_weight;
     if (mw <= 127)
-      h_stage_bad = upload_weights<int8_t>(c, a, rows, ew, et, off64, wn, lw, key);
+      h_stage_bad = upload_weights<int8_t>(c, a, rows, spans, ew, et, off64, wn, lw, key);
     else if (mw <= 32767)
-      h_stage_bad = upload_weights<int16_t>(c, a, rows, ew, et, off64, wn, lw, key);
+      h_stage_bad = upload_weights<int16_t>(c, a, rows, spans, ew, et, off64, wn, lw, key);
     else
-      h_stage_bad = upload_weights<int32_t>(c, a, rows, ew, et, off64, wn, lw, key);
+      h_stage_bad = upload_weights<int32_t>(c, a, rows, spans, ew, et, off64, wn, lw, key);
   }
   tm.mark("upload + relabel + CSC sort");
   CK(cudaEventRecord(e_tail, sw));
@@ -680,6 +709,9 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
     for (int k = 0; k < egs::kNumClasses; ++k) c->rb[k + 1] = c->rb[k] + h_misc[k];
   }
 }
+
+std::vector<std::pair<uint32_t, uint32_t>> rank_runs(const egs_arena_view* a,
+                                                     const egs_part_plan& pl, int rank);
 
 egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_stats* st,
                     int rank = 0, int world = 1, const egs_part_plan* plan = nullptr) {
@@ -748,6 +780,8 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     c->own_lo = plan ? plan->rank_lo[rank] : 0;
     c->own_hi = plan ? plan->rank_lo[rank + 1] : n;
     c->m_own = plan ? plan->edges[rank] : c->m;
+    if (plan && world > 1 && std::getenv("EGS_FULL_UPLOAD") == nullptr)
+      c->runs = rank_runs(a, *plan, rank);
     if (world == 1) {
       c->f = dalloc<uint8_t>((size_t)std::max<uint32_t>(n, 1) * vsz);
       c->chg[0] = dalloc<uint32_t>(words);
@@ -848,6 +882,7 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     }
     tm0.mark("create: occupancy, L2 window");
     if (st) {
+      st->h2d_bytes = c->h2d_bytes;
       st->upload_seconds = secs_since(t0);
       st->value_bits = (uint32_t)c->vbits;
       st->grid_ctas = (uint32_t)c->grid;
@@ -1317,6 +1352,84 @@ void plan_compute(const egs_arena_view* a, int world, egs_part_plan* pl) {
   }
 }
 
+// The original-id row ranges of rank `rank` (vertices whose class piece is
+// the rank's), for the sharded upload; runs separated by small gaps are
+// merged (their rows are uploaded and ignored) so at most kMaxRuns copies
+// are issued.
+std::vector<std::pair<uint32_t, uint32_t>> rank_runs(const egs_arena_view* a,
+                                                     const egs_part_plan& pl, int rank) {
+  constexpr size_t kMaxRuns = 2048;
+  constexpr int C = egs::kNumClasses;
+  const uint32_t n = a->num_vertices;
+  const int world = (int)pl.world;
+  auto cls = [&](uint32_t v) {
+    const uint64_t deg = a->csr_offsets[v + 1] - a->csr_offsets[v];
+    return (a->owners[v] ? 3 : 0) + (deg <= egs::kLightMax ? 0 : deg <= egs::kMediumMax ? 1 : 2);
+  };
+  const unsigned T = n > (1u << 20) ? std::max(1u, std::min(16u, std::thread::hardware_concurrency())) : 1u;
+  auto chunk = [&](unsigned t) { return std::make_pair((uint64_t)n * t / T, (uint64_t)n * (t + 1) / T); };
+  std::vector<uint64_t> cnt((size_t)T * C, 0);
+  std::vector<std::vector<std::pair<uint32_t, uint32_t>>> part(T);
+  auto run_all = [&](auto&& fn) {
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < T; ++t) pool.emplace_back([&, t] { fn(t); });
+    for (auto& th : pool) th.join();
+  };
+  run_all([&](unsigned t) {
+    const auto [lo, hi] = chunk(t);
+    for (uint64_t v = lo; v < hi; ++v) cnt[t * C + cls((uint32_t)v)] += 1;
+  });
+  run_all([&](unsigned t) {
+    uint64_t pos[C];
+    for (int k = 0; k < C; ++k) {
+      pos[k] = 0;
+      for (unsigned u = 0; u < t; ++u) pos[k] += cnt[u * C + k];
+    }
+    const auto [lo, hi] = chunk(t);
+    auto& out = part[t];
+    for (uint64_t v = lo; v < hi; ++v) {
+      const int k = cls((uint32_t)v);
+      const bool mine = pos[k] >= pl.piece[k][rank] && pos[k] < pl.piece[k][rank + 1];
+      ++pos[k];
+      if (!mine) continue;
+      if (!out.empty() && out.back().second == v)
+        out.back().second = (uint32_t)v + 1;
+      else
+        out.emplace_back((uint32_t)v, (uint32_t)v + 1);
+    }
+  });
+  std::vector<std::pair<uint32_t, uint32_t>> runs;
+  for (auto& p : part)
+    for (auto& r : p) {
+      if (!runs.empty() && runs.back().second == r.first)
+        runs.back().second = r.second;
+      else
+        runs.push_back(r);
+    }
+  (void)world;
+  if (runs.size() > kMaxRuns) {  // merge the smallest gaps (in edges)
+    std::vector<uint64_t> gaps;
+    for (size_t i = 1; i < runs.size(); ++i)
+      gaps.push_back(a->csr_offsets[runs[i].first] - a->csr_offsets[runs[i - 1].second]);
+    std::vector<uint64_t> sorted = gaps;
+    const size_t drop = runs.size() - kMaxRuns;
+    std::nth_element(sorted.begin(), sorted.begin() + (drop - 1), sorted.end());
+    const uint64_t thr = sorted[drop - 1];
+    std::vector<std::pair<uint32_t, uint32_t>> merged{runs[0]};
+    size_t budget = drop;
+    for (size_t i = 1; i < runs.size(); ++i) {
+      if (gaps[i - 1] <= thr && budget > 0) {
+        merged.back().second = runs[i].second;
+        --budget;
+      } else {
+        merged.push_back(runs[i]);
+      }
+    }
+    runs.swap(merged);
+  }
+  return runs;
+}
+
 // Grid of a rank's persistent kernel: ranks sharing a device split it.
 void part_grid(egs_ctx* c, int ranks_on_device) {
   if (ranks_on_device <= 1) return;
@@ -1542,7 +1655,9 @@ int egs_gpu_solve(const egs_arena_view* arena, const egs_gpu_opts* opts, int64_t
     egs_ctx* c = ctx_create(arena, o, st);
     try {
       const double up = st->upload_seconds;
+      const uint64_t h2d = st->h2d_bytes;
       ctx_solve(c, st);
+      st->h2d_bytes = h2d;
       auto t1 = Clock::now();
       ctx_read(c, f_out);
       st->download_seconds = secs_since(t1);

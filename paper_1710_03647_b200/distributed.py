@@ -66,6 +66,7 @@ class Partition:
                                        C.byref(self._part), C.byref(pl), C.byref(st)))
         self.plan = pl.as_dict()
         self.upload_seconds = st.upload_seconds
+        self.h2d_bytes = int(st.h2d_bytes)  # this rank's rows only (sharded upload)
 
     def export(self) -> bytes:
         buf = C.create_string_buffer(N.IPC_HANDLE_BYTES)
@@ -113,6 +114,7 @@ class PartitionReport:
     solve_seconds: float = 0.0          # device time of this rank's kernel
     edges_relaxed: int = 0              # this rank's
     edges_owned: int = 0                # out-edges of this rank's vertices (plan)
+    h2d_bytes: int = 0                  # this rank's upload (own rows + vertex arrays)
     plan: dict = field(default_factory=dict)
     stats: dict = field(default_factory=dict)
 
@@ -161,7 +163,8 @@ def solve_distributed(arena: N.GameArena, options: Optional[N.SolverOptions] = N
     return PartitionReport(
         measure=f, rounds=int(st.rounds), wall_seconds=time.perf_counter() - t0,
         solve_seconds=float(st.solve_seconds), edges_relaxed=int(st.edges_relaxed),
-        edges_owned=int(part.plan["edges"][rank]), plan=part.plan, stats=st.as_dict())
+        edges_owned=int(part.plan["edges"][rank]), h2d_bytes=part.h2d_bytes, plan=part.plan,
+        stats=st.as_dict())
 
 
 def solve_local(arena: N.GameArena, world: int, devices: Optional[Sequence[int]] = None,
@@ -203,6 +206,6 @@ def solve_local(arena: N.GameArena, world: int, devices: Optional[Sequence[int]]
         reports.append(PartitionReport(
             measure=parts[r].read_measure(), rounds=int(st.rounds), wall_seconds=wall,
             solve_seconds=float(st.solve_seconds), edges_relaxed=int(st.edges_relaxed),
-            edges_owned=int(parts[r].plan["edges"][r]), plan=parts[r].plan,
-            stats=st.as_dict()))
+            edges_owned=int(parts[r].plan["edges"][r]), h2d_bytes=parts[r].h2d_bytes,
+            plan=parts[r].plan, stats=st.as_dict()))
     return reports, parts

@@ -95,6 +95,7 @@ class FakePartition:
         self.plan = plan(arena, world)
         self._measure = measure
         self.connected = None
+        self.h2d_bytes = 0
 
     def export(self):
         return hashlib.sha256(f"rank{self.rank}".encode()).digest() * 2  # 64 bytes
@@ -214,6 +215,11 @@ def test_local_ranks_golden_and_repeated_solves(egs, golden):
     assert max(owned) <= 1.2 * sum(owned) / 2
     relaxed = [r.edges_relaxed for r in reps]
     assert max(relaxed) <= 1.2 * sum(relaxed) / 2 + 1000
+    # sharded upload: a rank moves its own rows (4-byte targets + 1-byte
+    # weights) plus the vertex arrays, not the whole arena
+    n, m = a.num_vertices, a.num_edges
+    for r in reps:
+        assert r.h2d_bytes <= (n + 1) * 8 + n + 1.2 * (m / 2) * 5
     for p in parts:
         p.close()
 
