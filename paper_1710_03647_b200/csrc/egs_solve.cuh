@@ -594,7 +594,10 @@ __device__ __forceinline__ void tma_init_barriers() {
 // tiles i+1 .. i+kStages-1 are in flight and the vertex state and row
 // offsets of the tile after them are loading: the HBM latency of a copy
 // (~1-2 us) is covered by the work of the tiles ahead of it.
-constexpr uint32_t kTileClaim = 4;
+#ifndef EGS_TILE_CLAIM
+#define EGS_TILE_CLAIM 4
+#endif
+constexpr uint32_t kTileClaim = EGS_TILE_CLAIM;
 
 struct NoAfter {
   __device__ void operator()(uint32_t, bool) const {}
@@ -832,7 +835,7 @@ __device__ __noinline__ void dense_light_p1(const SolveParams<V>& p, uint32_t lo
 // re-lifted 32 at a time, one row per lane, so a few violated rows never
 // serialise a warp.
 #ifndef EGS_P0_UNROLL
-#define EGS_P0_UNROLL 2
+#define EGS_P0_UNROLL 4
 #endif
 constexpr int kP0Unroll = EGS_P0_UNROLL;
 // the per-warp queue of violated rows (one allocation for both instantiations)
@@ -1278,10 +1281,6 @@ constexpr uint64_t kDenseCommitDiv = EGS_DENSE_COMMIT_DIV;
 // round 1's player-0 witness as one packed min per edge (4-byte records with
 // tbits >= 5, so |w| < 2^26: round1_light)
 constexpr bool kPackedWitnessKey = EGS_PACKED_WITNESS_KEY != 0 && EGS_EDGE_BYTES == 4;
-#ifndef EGS_ROUND1_ROW_EDGES
-#define EGS_ROUND1_ROW_EDGES 1
-#endif
-constexpr bool kRound1RowEdges = EGS_ROUND1_ROW_EDGES != 0;  // round 1 P1 rows via row_edges
 constexpr int kCertChunk = EGS_CERT_CHUNK;  // edges tested per step (early exit between)
 #ifndef EGS_CERT_CHUNK_P0
 #define EGS_CERT_CHUNK_P0 8
@@ -1408,11 +1407,8 @@ __device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo0,
       });
       return finish(v, true, INT32_MAX, -(int)(kb >> 6), rec[kb & 31u], len);
     }
-    if (!p0 && kRound1RowEdges) {  // player 1: the least weight, in any order
-      int mn = INT32_MAX;
-      row_edges(len, rot, [&](uint32_t j) { mn = min(mn, rec_w(g, rec[j])); });
-      return finish(v, false, mn, INT32_MIN, rec[0], len);
-    }
+    if (!p0)  // player 1: rows sorted by weight at upload, the least is first
+      return finish(v, false, rec_w(g, rec[0]), INT32_MIN, rec[0], len);
     int minw = INT32_MAX, maxw = INT32_MIN;
     uint32_t jbest = 0, kbest = 0xFFFFFFFFu;
     for (uint32_t k0 = 0; k0 < len; k0 += kChunk) {
@@ -1584,46 +1580,13 @@ __device__ __noinline__ void round1_long(const SolveParams<V>& p, uint32_t* chg,
   block_flush(L, sum_dst);
 }
 
-// Player-1 light rows: sorted by weight at upload (egs_build.cuh
-// k_sort_p1_rows), so delta(0)(v) = max(0, -w_min) is read from the first
-// record -- one load per vertex instead of the row.
-template <class V>
-__device__ __noinline__ void round1_p1_light(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
-                                             uint32_t* chg, unsigned int* sum_dst) {
-  const Graph& g = p.g;
-  Local L;
-  const uint32_t nwarps = gridDim.x * kWarps;
-  const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5, lane = lane_id();
-  for (uint32_t w = (lo >> 5) + gw; w < ((hi + 31) >> 5); w += nwarps) {
-    const uint32_t v = (w << 5) + lane;
-    bool ch = false;
-    if (v >= lo && v < hi) {
-      const uint32_t b = __ldg(g.off + v), e = __ldg(g.off + v + 1);
-      const V val = ominus_cap<V>(V(0), rec_w(g, __ldcs(erecs(g) + b)), g.cap);
-      ++L.visits;
-      ++L.apps;
-      L.edges += e - b;  // one lift application relaxes the row
-      if (val > V(0)) {
-        stcg(p.stage + v, val);
-        ++L.lifts;
-        ch = true;
-      }
-    }
-    const uint32_t m = __ballot_sync(0xffffffffu, ch);
-    if (m && lane == 0) bits_or(p, chg + w, m);
-    L.phase_count += ch;
-  }
-  block_flush(L, sum_dst);
-}
-
 template <class V>
 __device__ __noinline__ void phase_round1(const SolveParams<V>& p, uint32_t* chg,
                                           unsigned int* slot_sum, unsigned int* slot_dyn) {
   const Graph& g = p.g;
   round1_long<V>(p, chg, slot_sum + 0, slot_dyn);
-  round1_light<V>(p, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]), 0u, 0u,
-                  slot_dyn + kTileCursor, chg, slot_sum + 0);
-  round1_p1_light<V>(p, clip_lo(p, g.rb[kP1L]), clip_hi(p, g.rb[kP1M]), chg, slot_sum + 0);
+  round1_light<V>(p, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]), clip_lo(p, g.rb[kP1L]),
+                  clip_hi(p, g.rb[kP1M]), slot_dyn + kTileCursor, chg, slot_sum + 0);
 }
 
 // One lift round.  Dense (Jacobi): every vertex, raised values staged for
@@ -1735,20 +1698,21 @@ __device__ __forceinline__ void commit_stage_loads(const SolveParams<V>& p, bool
 }
 
 // debug_checks (the reference's check_monotone, solver_par.cpp:116-124,179):
-// a value a commit publishes must be above the one it replaces
-template <class V, int U>
-__device__ __forceinline__ void debug_check_raise(const SolveParams<V>& p, uint32_t w0,
-                                               uint32_t lane, const uint32_t (&bits)[U],
-                                               const V (&val)[U]) {
-#pragma unroll
-  for (int k = 0; k < U; ++k)
-    if ((bits[k] >> lane) & 1u) {
-      const V old = ldcg(p.f + ((w0 + k) << 5) + lane);
-      if (!(val[k] > old)) atomicOr(&p.sh->bad, 1u);
+// a value the next commit publishes must be above the one it replaces.  Run
+// in the commit's phase, before it (reads only).
+template <class V>
+__device__ __noinline__ void phase_debug_raise(const SolveParams<V>& p, const uint32_t* chg) {
+  const uint32_t nwarps = gridDim.x * kWarps;
+  const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5, lane = lane_id();
+  for (uint32_t w = (p.own_lo >> 5) + gw; w < ((p.own_hi + 31) >> 5); w += nwarps) {
+    const uint32_t v = (w << 5) + lane;
+    if (((ldcg(chg + w) & own_mask(p, w)) >> lane) & 1u) {
+      if (!(ldcg(p.stage + v) > ldcg(p.f + v))) atomicOr(&p.sh->bad, 1u);
     }
+  }
 }
 
-template <class V>
+template <class V, bool MULTI>
 __device__ __noinline__ void phase_commit(const SolveParams<V>& p, const uint32_t* chg,
                                           bool dense = false) {
   constexpr int U = 8;  // words per warp step, all loads issued before any store
@@ -1758,21 +1722,20 @@ __device__ __noinline__ void phase_commit(const SolveParams<V>& p, const uint32_
   const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5;
   const uint32_t lane = lane_id();
   const uint32_t wlo = p.own_lo >> 5, whi = min(nwords, (p.own_hi + 31) >> 5);
-  // (scalars of p read once: stores through p.f may alias p for the compiler)
-  const bool multi = p.world > 1, debug = p.debug != 0;
+  // (scalars of p read once: stores through p.f may alias p for the compiler;
+  // one rank or several is a template parameter)
   V* const f = p.f;
   for (uint32_t w0 = wlo + gw * U; w0 < whi; w0 += nwarps * U) {
     uint32_t bits[U];
     V val[U];
 #pragma unroll
     for (int k = 0; k < U; ++k)
-      bits[k] = w0 + k < whi ? ldcg(chg + w0 + k) & (multi ? own_mask(p, w0 + k) : ~0u) : 0u;
+      bits[k] = w0 + k < whi ? ldcg(chg + w0 + k) & (MULTI ? own_mask(p, w0 + k) : ~0u) : 0u;
     commit_stage_loads<V, U>(p, dense, w0, whi, lane, bits, val, V(0));
-    if (debug) debug_check_raise<V, U>(p, w0, lane, bits, val);
 #pragma unroll
     for (int k = 0; k < U; ++k)
       if ((bits[k] >> lane) & 1u) {
-        if (multi)
+        if (MULTI)
           f_put<V>(p, ((w0 + k) << 5) + lane, val[k]);
         else
           stcg(f + ((w0 + k) << 5) + lane, val[k]);
@@ -1810,7 +1773,7 @@ __device__ __noinline__ void phase_cert_init(const SolveParams<V>& p, const uint
 // Commit fused with certificate step 1 (one pass over the words of `chg`
 // instead of two): a raised vertex publishes its staged value and, unless it
 // reached top, becomes a candidate (bit + mark).
-template <class V>
+template <class V, bool MULTI>
 __device__ __noinline__ void phase_commit_cert_init(const SolveParams<V>& p, const uint32_t* chg,
                                                     bool dense = false) {
   constexpr V TOP = Top<V>::v;
@@ -1821,7 +1784,6 @@ __device__ __noinline__ void phase_commit_cert_init(const SolveParams<V>& p, con
   const uint32_t gw = tid >> 5, lane = lane_id();
   for (uint32_t w = tid; w < nwords; w += gridDim.x * kBlock) p.rbm[1][w] = 0u;
   const uint32_t wlo = p.own_lo >> 5, whi = min(nwords, (p.own_hi + 31) >> 5);
-  const bool multi = p.world > 1, debug = p.debug != 0;
   V* const f = p.f;
   uint32_t* const cand = p.cand;
   for (uint32_t w0 = wlo + gw * U; w0 < whi; w0 += nwarps * U) {
@@ -1829,9 +1791,8 @@ __device__ __noinline__ void phase_commit_cert_init(const SolveParams<V>& p, con
     V val[U];
 #pragma unroll
     for (int k = 0; k < U; ++k)
-      bits[k] = w0 + k < whi ? ldcg(chg + w0 + k) & (multi ? own_mask(p, w0 + k) : ~0u) : 0u;
+      bits[k] = w0 + k < whi ? ldcg(chg + w0 + k) & (MULTI ? own_mask(p, w0 + k) : ~0u) : 0u;
     commit_stage_loads<V, U>(p, dense, w0, whi, lane, bits, val, TOP);
-    if (debug) debug_check_raise<V, U>(p, w0, lane, bits, val);
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       if (w0 + k >= whi) break;
@@ -1839,7 +1800,7 @@ __device__ __noinline__ void phase_commit_cert_init(const SolveParams<V>& p, con
       const bool c = raised && val[k] != TOP;
       const V x = c ? val[k] | CandFlag<V>::v : val[k];
       if (raised) {
-        if (multi)
+        if (MULTI)
           f_put<V>(p, ((w0 + k) << 5) + lane, x);
         else
           stcg(f + ((w0 + k) << 5) + lane, x);
@@ -1920,30 +1881,6 @@ __device__ __forceinline__ void cert_long_rows(const SolveParams<V>& p, uint32_t
   }
 }
 
-// Player-1 light candidates of a dense certificate pass, one row per lane in
-// row order (sorted by weight: the most negative, likeliest good edges
-// first), warps striding over the candidate bitmap words; removals go to
-// rbm.  Warp-uniform.
-template <class V>
-__device__ __forceinline__ void cert_p1_light(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
-                                              uint32_t* rbm, Local& L, WarpLists& q,
-                                              const Frontier& qt) {
-  if (hi <= lo) return;
-  const uint32_t nwarps = gridDim.x * kWarps;
-  const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5, lane = lane_id();
-  for (uint32_t w = (lo >> 5) + gw; w < ((hi + 31) >> 5); w += nwarps) {
-    const uint32_t mw = ldcg(p.cand + w);
-    if (!mw) continue;  // warp-uniform
-    const uint32_t v = (w << 5) + lane;
-    bool removed = false;
-    if (((mw >> lane) & 1u) && v >= lo && v < hi) removed = cert_check_thread<V>(p, v, L);
-    const uint32_t m = __ballot_sync(0xffffffffu, removed);
-    if (m && lane == 0) bits_or(p, rbm + w, m);
-    L.phase_count += removed;
-    push_cert_preds<V>(p, removed, v, q, qt, L);
-  }
-}
-
 // Dense pass over every owned candidate (removed count -> slot_sum[1]).
 // `rbm_clear` (the bitmap two passes old) is zeroed for reuse.
 template <class V>
@@ -1957,6 +1894,13 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
   const uint32_t nwords = (g.n + 31) >> 5;
   Local L;
   WarpLists q = warp_lists_small();
+  // the cascade that may follow starts from an empty queue and one token
+  // per warp (phase_cert_cascade)
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p.sh->qhead = 0u;
+    p.sh->qtail = 0u;
+    p.sh->qpend = gridDim.x * kWarps;
+  }
   // (a dense pass leaves the last pass's re-check queue unread: its dedup
   // bitmap is cleared whole)
   for (uint32_t w = tid; w < nwords; w += nthreads) {
@@ -2004,7 +1948,10 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
     auto row = [&](uint32_t v, const ERec* rec, uint32_t len, uint32_t, V cv) {
       const int64_t fv = cand_value<V>(cv);
       const bool p0 = v < g.rb[kP1L];
-      const uint32_t rot = row_rot(len);
+      // player-1 rows are sorted by weight (upload): read in order, the most
+      // negative -- likeliest good -- edges first (the bank conflicts of
+      // unrotated reads cost a few cycles per step; the gathers, microseconds)
+      const uint32_t rot = p0 ? row_rot(len) : 0u;
       ++L.cert_scanned;
       const bool keep = p0 ? scan(std::integral_constant<int, kCertChunkP0>{}, true, rec, len,
                                   rot, fv)
@@ -2015,14 +1962,9 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
     };
     auto fallback = [&](uint32_t v, V) { return cert_check_thread<V>(p, v, L); };
     auto after = [&](uint32_t v, bool removed) { push_cert_preds<V>(p, removed, v, q, qt, L); };
-    // player-0 light candidates through the tile pipeline (kept ones read
-    // their whole row); player-1 light rows are sorted by weight (build), so
-    // their first records are the likeliest good edges: a lane reads its own
-    // row start directly and most rows end with the first chunk
     tma_tiles<V>(p, (p.use_tma & kTmaCert) != 0, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]),
-                 0u, 0u, slot_dyn + kTileCursor, p.cand, rbm, L, load, test, row, fallback,
-                 after);
-    cert_p1_light<V>(p, clip_lo(p, g.rb[kP1L]), clip_hi(p, g.rb[kP1M]), rbm, L, q, qt);
+                 clip_lo(p, g.rb[kP1L]), clip_hi(p, g.rb[kP1M]), slot_dyn + kTileCursor, p.cand,
+                 rbm, L, load, test, row, fallback, after);
   }
   if (qt.cnt)
     for (int c = 0; c < 3; ++c) lists_flush(q, c, qt.list[c], qt.cnt + c);
@@ -2109,9 +2051,167 @@ __device__ __noinline__ void phase_cert_check(const SolveParams<V>& p, Frontier 
   block_flush(L, slot_sum + 1);
 }
 
+// Certificate, step 2 (one rank): the cascade after a dense pass, in ONE
+// phase instead of a mark phase plus one sparse pass per removal wave.  The
+// candidate predecessors of the dense pass's removals (bitmap rbm_in, CSC)
+// enter a work queue; warps re-check queued candidates and push the
+// candidate predecessors of every removal, until the queue is empty and no
+// item is in flight -- the greatest fixpoint of the pruning, reached in any
+// order.  The queue is a ring of n slots (p.ring, kRingEmpty when free):
+// a producer reserves slots (Scratch::qtail, after counting the items in
+// Scratch::qpend) and writes them; a consumer claims a range (qhead, by CAS
+// up to qtail), waits for each slot's write, frees it, and only then clears
+// the item's dedup bit (qbits) -- so at most one queued copy per vertex and
+// at most n unfreed slots, and a vertex whose successor is removed after its
+// re-check is queued again.  qpend counts reserved items not yet finished
+// (their pushes included) plus one token per warp until its mark step is
+// done; every warp leaves when it is zero.  All CTAs are co-resident
+// (persistent cooperative launch), so every spin ends.
+__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <class V>
+__device__ __forceinline__ void ring_push(const SolveParams<V>& p, bool add, uint32_t u,
+                                          uint32_t n) {
+  const uint32_t m = __ballot_sync(0xffffffffu, add);
+  if (!m) return;
+  uint32_t base = 0;
+  if (lane_id() == 0) {
+    atomicAdd(&p.sh->qpend, (unsigned int)__popc(m));
+    base = atomicAdd(&p.sh->qtail, (unsigned int)__popc(m));
+  }
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (add) {
+    const uint32_t slot = (base + __popc(m & lanemask_lt())) % p.ring_cap;
+    // the slot's previous item (one lap back) is claimed already (at most n
+    // items are queued, each holding its dedup bit); wait until its consumer
+    // frees it.  A warp pushes only after freeing its own claims, and a
+    // consumer waits only for an earlier reservation's write: no cycle.
+    while (ld_relaxed_gpu(p.ring + slot) != kRingEmpty) __nanosleep(32);
+    __stcg(p.ring + slot, u);
+  }
+}
+
+// the candidate predecessors of the lanes with `removed` (their CSC columns,
+// expanded by the warp), each queued once (dedup bits qbits).  Warp-uniform.
+template <class V>
+__device__ __forceinline__ void cascade_push_preds(const SolveParams<V>& p, bool removed,
+                                                   uint32_t v, uint32_t* qbits) {
+  if (!__any_sync(0xffffffffu, removed)) return;
+  uint32_t b = 0, e = 0;
+  if (removed) {
+    b = __ldg(p.g.coff + v);
+    e = __ldg(p.g.coff + v + 1);
+  }
+  warp_expand(b, e, [&](bool valid, uint32_t idx, uint32_t) {
+    bool add = false;
+    uint32_t u = 0;
+    if (valid) {
+      u = __ldg(p.g.csrc + idx);
+      const uint32_t bit = 1u << (u & 31u);
+      add = ((ldcg(p.cand + (u >> 5)) & bit) != 0) && !(ldcg(qbits + (u >> 5)) & bit) &&
+            !(atomicOr(qbits + (u >> 5), bit) & bit);
+    }
+    ring_push<V>(p, add, u, p.g.n);
+  });
+}
+
+template <class V>
+__device__ __noinline__ void phase_cert_cascade(const SolveParams<V>& p, const uint32_t* rbm_in,
+                                                uint32_t* qbits, unsigned int* slot_sum) {
+  const uint32_t n = p.g.n;
+  const uint32_t nwords = (n + 31) >> 5;
+  const uint32_t nwarps = gridDim.x * kWarps;
+  const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5, lane = lane_id();
+  Scratch* sh = p.sh;
+  Local L;
+  // mark: the candidate predecessors of the dense pass's removals
+  for (uint32_t w0 = gw * 32; w0 < nwords; w0 += nwarps * 32) {
+    const uint32_t wi = w0 + lane;
+    uint32_t bits = wi < nwords ? ldcg(rbm_in + wi) : 0u;
+    while (__any_sync(0xffffffffu, bits != 0u)) {
+      uint32_t u = 0;
+      bool any = false;
+      if (bits) {
+        u = (wi << 5) + (__ffs(bits) - 1);
+        bits &= bits - 1;
+        any = true;
+      }
+      cascade_push_preds<V>(p, any, u, qbits);
+    }
+  }
+  if (lane == 0) atomicSub(&sh->qpend, 1u);  // this warp's mark token
+  // drain: every lane holds one queue position at a time (claimed with one
+  // atomicAdd per warp for the lanes that need one, possibly past the
+  // reserved positions) and polls it; lanes whose item has arrived re-check
+  // it, push, and take a new position.  A lane never blocks on its
+  // position, so an item is never waited for by the warp that must finish
+  // it.  When no item is in flight every held position is past the last
+  // reserved one (a reserved position's item is unfinished until its holder
+  // processes it), and the warp leaves.
+  const uint32_t cap = p.ring_cap;
+  constexpr uint32_t kNoPos = 0xFFFFFFFFu;
+  uint32_t pos = kNoPos;
+  unsigned ns = 32;
+  for (;;) {
+    const uint32_t need = __ballot_sync(0xffffffffu, pos == kNoPos);
+    if (need) {
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(&sh->qhead, (unsigned int)__popc(need));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (pos == kNoPos) pos = base + __popc(need & lanemask_lt());
+    }
+    uint32_t* s = p.ring + pos % cap;
+    uint32_t v = ld_relaxed_gpu(s);
+    const bool have = v != kRingEmpty;
+    if (have) {
+      __stcg(s, kRingEmpty);
+      __threadfence();
+      atomicAnd(qbits + (v >> 5), ~(1u << (v & 31u)));
+      pos = kNoPos;
+    }
+    const uint32_t got = __ballot_sync(0xffffffffu, have);
+    if (!got) {
+      if (ld_relaxed_gpu(&sh->qpend) == 0u) break;  // nothing in flight: done
+      __nanosleep(ns);
+      ns = ns < 1024 ? ns * 2 : 1024;
+      continue;
+    }
+    ns = 32;
+    const uint32_t k = __popc(got);
+    // light candidates one per lane; medium / heavy ones by the whole warp
+    const bool light = have && size_class(p.g, v) == 0;
+    bool removed = false;
+    if (light) removed = cert_check_thread<V>(p, v, L);
+    uint32_t longm = __ballot_sync(0xffffffffu, have && !light);
+    while (longm) {
+      const int src = __ffs(longm) - 1;
+      longm &= longm - 1;
+      const uint32_t u = __shfl_sync(0xffffffffu, v, src);
+      if (!cand_bit(p, u)) continue;  // warp-uniform
+      const int64_t fu = cand_value<V>(ldcg(p.f + u));
+      const bool keep = u < p.g.rb[kP1L] ? cert_keep_warp<V, true>(p, u, fu, L)
+                                         : cert_keep_warp<V, false>(p, u, fu, L);
+      if (lane == src) {
+        ++L.cert_scanned;
+        if (!keep) cand_clear(p, u, fu);
+        removed = !keep;
+      }
+    }
+    L.phase_count += removed;
+    cascade_push_preds<V>(p, removed, v, qbits);
+    __syncwarp();
+    if (lane == 0) atomicSub(&sh->qpend, k);
+  }
+  block_flush(L, slot_sum + 1);
+}
+
 // Certificate, step 3: certified vertices jump to top and count as changed
 // in this round so their predecessors are re-lifted (count -> slot_sum[0]).
-template <class V>
+template <class V, bool MULTI>
 __device__ __noinline__ void phase_cert_apply(const SolveParams<V>& p, uint32_t* chg,
                                               unsigned int* slot_sum) {
   const uint32_t nwarps = gridDim.x * kWarps;
@@ -2120,7 +2220,6 @@ __device__ __noinline__ void phase_cert_apply(const SolveParams<V>& p, uint32_t*
   Local L;
   constexpr uint32_t U = 8;  // words per warp step, loads issued together
   const uint32_t w_lo = p.own_lo >> 5, w_hi = (p.own_hi + 31) >> 5;
-  const bool multi = p.world > 1;
   V* const f = p.f;
   for (uint32_t w0 = w_lo + gw * U; w0 < w_hi; w0 += nwarps * U) {
     uint32_t m[U];
@@ -2129,7 +2228,7 @@ __device__ __noinline__ void phase_cert_apply(const SolveParams<V>& p, uint32_t*
 #pragma unroll
     for (uint32_t k = 0; k < U; ++k) {
       const bool hit = (m[k] >> lane) & 1u;  // candidate words hold owned, non-top ids only
-      if (multi) {
+      if (MULTI) {
         if (hit) f_put<V>(p, ((w0 + k) << 5) + lane, Top<V>::v);
         if (m[k] && lane == 0) bits_or(p, chg + w0 + k, m[k]);
       } else {
@@ -2375,16 +2474,23 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
     // activation's top filter may see either the old or the committed value
     // of a predecessor; a stale one only adds a harmless frontier entry)
     const bool fuse_act =
-        !inplace && !cert_now && p.mode != kModeDense && p.mode != kModeSweep &&
+        !inplace && !cert_now && !p.no_fuse && p.mode != kModeDense && p.mode != kModeSweep &&
         !(p.mode == kModeAuto && (double)changed * p.avg_in_deg * p.sparse_div >= (double)n);
     if (!inplace) {  // a Jacobi round: publish its staged values
       begin_phase();
       // (a commit of many raises loads every staged slot with its bitmap word)
       const bool dense_commit = (uint64_t)changed * kDenseCommitDiv >= n;
-      if (cert_now) {
-        phase_commit_cert_init<V>(p, chg, dense_commit);  // commit + certificate step 1
+      if (p.debug) phase_debug_raise<V>(p, chg);
+      if (cert_now) {  // commit + certificate step 1
+        if (p.world > 1)
+          phase_commit_cert_init<V, true>(p, chg, dense_commit);
+        else
+          phase_commit_cert_init<V, false>(p, chg, dense_commit);
       } else {
-        phase_commit<V>(p, chg, dense_commit);
+        if (p.world > 1)
+          phase_commit<V, true>(p, chg, dense_commit);
+        else
+          phase_commit<V, false>(p, chg, dense_commit);
         if (fuse_act)
           phase_activate<V>(p, chg, frontier(tok + 1), p.frb[tok & 1], sh->fr_cnt[(tok + 2) % 3],
                             slot_sum(), slot_dyn() + 2);
@@ -2431,6 +2537,14 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
         const bool sparse_pass =
             p.mode != kModeDense && p.mode != kModeSweep &&
             (double)removed * p.avg_in_deg * p.cert_sparse_div < (double)n;
+        if (sparse_pass && p.world == 1 && p.cascade) {
+          // one rank: the rest of the pruning in one phase (a work queue)
+          begin_phase();
+          phase_cert_cascade<V>(p, p.rbm[rb], p.cbm[0], slot_sum());
+          end_phase(2, 3);
+          ++cert_passes;
+          break;
+        }
         if (sparse_pass) {
           if (!queued) {  // after a dense pass: the queue from its removal bits
             begin_phase();
@@ -2460,7 +2574,10 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
         removed = prev_sum(1);
       }
       begin_phase();
-      phase_cert_apply<V>(p, chg, slot_sum());
+      if (p.world > 1)
+        phase_cert_apply<V, true>(p, chg, slot_sum());
+      else
+        phase_cert_apply<V, false>(p, chg, slot_sum());
       end_phase(2, 4);
       const uint32_t cert = prev_sum(0);
       certified_any = cert > 0;

@@ -166,6 +166,8 @@ struct egs_ctx {
   uint32_t* rbm[2] = {nullptr, nullptr};
   uint32_t* cbm[2] = {nullptr, nullptr};
   uint32_t* cand = nullptr;  // certificate candidate bitmap (own vertices)
+  uint32_t* ring = nullptr;  // certificate cascade queue (ring_cap slots, all-ones when free)
+  uint32_t ring_cap = 0;
   uint32_t* longcol = nullptr;
   uint32_t* fr[2] = {nullptr, nullptr};
   void* stage = nullptr;
@@ -268,7 +270,7 @@ void ctx_free(egs_ctx* c) {
                   in_x ? nullptr : c->chg[1], c->frb[0], c->frb[1],
                   c->fr[0], c->fr[1], c->stage, c->scratch, c->ctr,
                   in_x ? nullptr : c->rbm[0], in_x ? nullptr : c->rbm[1], c->cbm[0], c->cbm[1],
-                  c->cand, c->trace, c->longcol, c->f64};
+                  c->cand, c->ring, c->trace, c->longcol, c->f64};
   for (int q = 0; q < egs::kMaxRanks; ++q)
     if (c->xpeer_ipc[q] && c->xpeer[q]) cudaIpcCloseMemHandle(c->xpeer[q]);
   if (c->xbuf) {
@@ -811,6 +813,10 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     c->cbm[1] = dalloc<uint32_t>(words);
     c->cand = dalloc<uint32_t>(words);
     CK(cudaMemsetAsync(c->cand, 0, std::max<size_t>(words, 1) * 4, c->stream));
+    // every cascade leaves the ring empty again (egs_solve.cuh)
+    c->ring_cap = n + egs::kRingSlack;
+    c->ring = dalloc<uint32_t>(c->ring_cap);
+    CK(cudaMemsetAsync(c->ring, 0xFF, (size_t)c->ring_cap * 4, c->stream));
     // at most m / kLongCol columns are longer than kLongCol
     c->longcol = dalloc<uint32_t>(2 * (a->num_edges / egs::kLongCol + 1));
     c->fr[0] = dalloc<uint32_t>(n);
@@ -948,6 +954,13 @@ egs::SolveParams<V> make_params(egs_ctx* c, unsigned long long* budget_out) {
   p.own_lo = c->world == 1 ? 0 : c->own_lo;
   p.own_hi = c->world == 1 ? n : c->own_hi;
   p.debug = o.debug_checks ? 1 : 0;
+  p.no_fuse = std::getenv("EGS_NO_FUSE") != nullptr;
+  {
+    const char* e = std::getenv("EGS_CERT_CASCADE");
+    p.cascade = !(e && std::atoi(e) == 0);
+  }
+  p.ring = c->ring;
+  p.ring_cap = c->ring_cap;
   p.world = c->world;
   p.rank = c->rank;
   if (c->world > 1) {

@@ -72,6 +72,8 @@ struct Graph {
 };
 
 constexpr int kTileCursor = 7;  // Scratch::dyn slot of the TMA tile claims
+constexpr uint32_t kRingEmpty = 0xFFFFFFFFu;
+constexpr uint32_t kRingSlack = 1u << 18;  // > (max warps of a grid) * 32 positions claimed ahead
 
 // Grid-shared scratch; the host zeroes it before each launch.
 struct Scratch {
@@ -82,6 +84,9 @@ struct Scratch {
   unsigned int stop;         // timeout flag
   unsigned int bad;          // debug_checks: a commit that did not raise its vertex
   unsigned int xerr;         // multi-GPU: a peer did not reach a barrier in time
+  // the certificate cascade's work queue (egs_solve.cuh phase_cert_cascade):
+  // ring positions claimed / reserved, and items reserved but not finished
+  unsigned int qhead, qtail, qpend;
 };
 
 // Cross-rank sync block (multi-GPU, egs_part_solve), inside every rank's
@@ -105,6 +110,8 @@ struct SolveParams {
   uint32_t* cand;       // certificate: candidate bitmap
   uint32_t* longcol;    // activation: queued long CSC columns {vertex, chunk cursor}
   uint32_t* fr[2];      // frontier lists; sublist c starts at cbase[c]
+  uint32_t* ring;       // certificate cascade queue: ring_cap slots, kRingEmpty when free
+  uint32_t ring_cap;    // n + kRingSlack (claims may run ahead of the reserved slots)
   uint32_t cbase[3];
   Scratch* sh;
   unsigned long long* ctr;  // kNumCounters
@@ -121,6 +128,8 @@ struct SolveParams {
   unsigned long long round_budget;
   unsigned long long timeout_ns;   // 0 = none; measured from kernel start
   int debug;                // SolverOptions::debug_checks: commits check monotonicity
+  int no_fuse;              // EGS_NO_FUSE=1: commit and activation in separate phases (tracing)
+  int cascade;              // certificate cascade in one queue phase (EGS_CERT_CASCADE=0: passes)
   // multi-GPU (egs_part_solve; world == 1 otherwise): the measure and the
   // changed / removal bitmaps are replicated in one allocation per rank with
   // the same layout everywhere; a rank writes what it raises into every
