@@ -1580,13 +1580,68 @@ __device__ __noinline__ void round1_long(const SolveParams<V>& p, uint32_t* chg,
   block_flush(L, sum_dst);
 }
 
+// Player-1 light rows: sorted by weight at upload (egs_build.cuh
+// k_sort_p1_rows), so delta(0)(v) = max(0, -w_min) is the first record's --
+// no row is streamed.  A warp takes kR1Words bitmap words (32 vertices each)
+// per step and issues all their offset loads, then all their record loads,
+// before using any (the two loads of a vertex depend on each other).
+constexpr int kR1Words = 4;
+template <class V>
+__device__ __noinline__ void round1_p1_light(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
+                                             uint32_t* chg, unsigned int* sum_dst) {
+  const Graph& g = p.g;
+  Local L;
+  if (hi > lo) {
+    const uint32_t nwarps = gridDim.x * kWarps;
+    const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5, lane = lane_id();
+    const uint32_t w_lo = lo >> 5, w_hi = (hi + 31) >> 5;
+    for (uint32_t w0 = w_lo + gw * kR1Words; w0 < w_hi; w0 += nwarps * kR1Words) {
+      uint32_t b[kR1Words], e[kR1Words];
+      bool in[kR1Words];
+#pragma unroll
+      for (int k = 0; k < kR1Words; ++k) {
+        const uint32_t v = ((w0 + k) << 5) + lane;
+        in[k] = w0 + k < w_hi && v >= lo && v < hi;
+        b[k] = in[k] ? __ldg(g.off + v) : 0u;
+        e[k] = in[k] ? __ldg(g.off + v + 1) : 0u;
+      }
+      ERec r[kR1Words];
+#pragma unroll
+      for (int k = 0; k < kR1Words; ++k) r[k] = in[k] ? __ldcs(erecs(g) + b[k]) : ERec{};
+#pragma unroll
+      for (int k = 0; k < kR1Words; ++k) {
+        const uint32_t v = ((w0 + k) << 5) + lane;
+        bool ch = false;
+        if (in[k]) {
+          const V val = ominus_cap<V>(V(0), rec_w(g, r[k]), g.cap);
+          ++L.visits;
+          ++L.apps;
+          L.edges += e[k] - b[k];  // one lift application relaxes the row
+          if (val > V(0)) {
+            stcg(p.stage + v, val);
+            ++L.lifts;
+            ch = true;
+          }
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, ch);
+        if (m && lane == 0 && w0 + k < w_hi) bits_or(p, chg + w0 + k, m);
+        L.phase_count += ch;
+      }
+    }
+  }
+  block_flush(L, sum_dst);
+}
+
 template <class V>
 __device__ __noinline__ void phase_round1(const SolveParams<V>& p, uint32_t* chg,
                                           unsigned int* slot_sum, unsigned int* slot_dyn) {
   const Graph& g = p.g;
   round1_long<V>(p, chg, slot_sum + 0, slot_dyn);
-  round1_light<V>(p, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]), clip_lo(p, g.rb[kP1L]),
-                  clip_hi(p, g.rb[kP1M]), slot_dyn + kTileCursor, chg, slot_sum + 0);
+  // player-0 light rows stream through the tile pipeline (their witness
+  // needs the whole row); player-1 light rows read their first record
+  round1_light<V>(p, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]), 0u, 0u,
+                  slot_dyn + kTileCursor, chg, slot_sum + 0);
+  round1_p1_light<V>(p, clip_lo(p, g.rb[kP1L]), clip_hi(p, g.rb[kP1M]), chg, slot_sum + 0);
 }
 
 // One lift round.  Dense (Jacobi): every vertex, raised values staged for
