@@ -45,7 +45,10 @@ CONFIGS = {
     "C4": ("fixed", (16_000_000, 16, 100)),
     "C5": ("fixed", (1_000_000, 8, 100_000)),
 }
-# Survey projection of reference sweeps-to-fixpoint on C4.
+# Survey projection of reference sweeps-to-fixpoint on C4;
+# the GPU's in-place sweep (the reference's iteration, certify=False, mode
+# sweep) reached the fixpoint in 1,914,825 rounds
+# (profiles/r02_golden_plain_gpu_c4_sweep.json).
 C4_PROJECTED_REF_SWEEPS = 2.1e6
 FALLBACK_HBM_GBS = 6650.0
 

@@ -1,5 +1,6 @@
-# bench + launch list + ncu full captures of k_solve (C4, C3) + a 2-rank
-# staged run of the partitioned path; run from the repo root under gpurun
+# bench + launch list + ncu full captures of k_solve (C4, C3) + the
+# all-configs table + a 2-rank (one-GPU) run of the partitioned path; run from
+# the repo root under gpurun:  bash tools/gpu_bench_profile.sh <tag>
 set -u
 OUT=gpurun_out/$1
 mkdir -p $OUT
@@ -8,5 +9,9 @@ timeout 900 python bench.py --steps 20 --warmup 3 > $OUT/bench.json 2> $OUT/benc
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv python tools/ncu_target.py C4 1 > $OUT/launches.out 2>&1; echo "launches rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_solve -c 1 -o $OUT/solve_c4 python tools/ncu_target.py C4 1 > $OUT/ncu.out 2>&1; echo "ncu rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_solve -c 1 -o $OUT/solve_c3 python tools/ncu_target.py C3 1 > $OUT/ncu_c3.out 2>&1; echo "ncu c3 rc=$?"
-EGS_BENCH_STAGED=1 timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 3 --warmup 3 > $OUT/bench_2rank_staged.json 2> $OUT/bench_2rank_staged.err; echo "2-rank rc=$?"
+EGS_TRACE=1 timeout 300 python tools/ncu_target.py C4 1 > $OUT/trace_c4.txt 2>&1
+EGS_TRACE=1 timeout 300 python tools/ncu_target.py C3 1 > $OUT/trace_c3.txt 2>&1
+timeout 1200 python tools/config_table.py --out $OUT/configs.jsonl > $OUT/configs.out 2>&1; echo "configs rc=$?"
+timeout 600 python tools/part_local_bench.py C4 2 > $OUT/part_local_c4.json 2> $OUT/part_local_c4.err; echo "part-local rc=$?"
 cat $OUT/bench.json
+timeout 1500 python tests/golden/make_golden_plain.py --out $OUT/golden_plain_c3_sweep.json --mode sweep --budget 1200 C3 > $OUT/c3_sweep.out 2>&1; echo "c3 sweep rc=$?"
