@@ -199,11 +199,12 @@ __global__ void __launch_bounds__(256)
 // (packed: w in the high bits, so int32 order is (w, dst) order; wide:
 // (w, dst) as an int64).  key[o] is the class of original row o
 // (egs_scan.cuh k_class_tiles); class 3 = player-1 light.
-template <class K>
+// ascending bitonic sort of one value per lane over groups of G lanes
+template <class K, uint32_t G = 32>
 __device__ __forceinline__ K bitonic32(K x) {
-  const uint32_t lane = lane_id();
+  const uint32_t lane = lane_id() & (G - 1);
 #pragma unroll
-  for (uint32_t k = 2; k <= 32; k <<= 1) {
+  for (uint32_t k = 2; k <= G; k <<= 1) {
 #pragma unroll
     for (uint32_t j = k >> 1; j > 0; j >>= 1) {
       const K y = __shfl_xor_sync(0xffffffffu, x, j);
@@ -214,31 +215,58 @@ __device__ __forceinline__ K bitonic32(K x) {
   return x;
 }
 
+// sort the row (b, len) with groups of G lanes (lane index within the group)
+template <uint32_t G>
+__device__ __forceinline__ void sort_row(void* edge, uint32_t tbits, uint32_t b, uint32_t len,
+                                         bool on) {
+  const uint32_t l = lane_id() & (G - 1);
+  if (tbits) {
+    int* rec = static_cast<int*>(edge) + b;
+    const int x = bitonic32<int, G>(on && l < len ? rec[l] : INT32_MAX);
+    if (on && l < len) rec[l] = x;
+  } else {
+    int2* rec = static_cast<int2*>(edge) + b;
+    long long x = LLONG_MAX;
+    if (on && l < len) {
+      const int2 r = rec[l];
+      x = ((long long)r.y << 32) | (long long)(uint32_t)r.x;
+    }
+    x = bitonic32<long long, G>(x);
+    if (on && l < len) rec[l] = make_int2((int)(uint32_t)x, (int)(x >> 32));
+  }
+}
+
+// A warp takes two rows: one per half-warp when both have <= 16 edges (the
+// common case), else one after the other with the whole warp.
 __global__ void __launch_bounds__(256)
     k_sort_p1_rows(uint32_t r0, uint32_t r1, const uint8_t* key, const uint32_t* perm,
                    const uint32_t* off_new, void* edge, uint32_t tbits, uint32_t own_lo,
                    uint32_t own_hi) {
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
   const uint32_t lane = lane_id();
-  for (uint32_t o = r0 + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); o < r1; o += nwarps) {
-    if (key[o] != (uint8_t)kP1L) continue;  // warp-uniform
-    const uint32_t v = perm[o];
-    if (v < own_lo || v >= own_hi) continue;
-    const uint32_t b = off_new[v], len = off_new[v + 1] - b;
-    if (len < 2) continue;
-    if (tbits) {
-      int* rec = static_cast<int*>(edge) + b;
-      const int x = bitonic32<int>(lane < len ? rec[lane] : INT32_MAX);
-      if (lane < len) rec[lane] = x;
-    } else {
-      int2* rec = static_cast<int2*>(edge) + b;
-      long long x = LLONG_MAX;
-      if (lane < len) {
-        const int2 r = rec[lane];
-        x = ((long long)r.y << 32) | (long long)(uint32_t)r.x;
+  for (uint32_t o0 = r0 + 2 * ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); o0 < r1;
+       o0 += 2 * nwarps) {
+    const uint32_t o = o0 + (lane >> 4);
+    bool on = false;
+    uint32_t b = 0, len = 0;
+    if (o < r1 && key[o] == (uint8_t)kP1L) {
+      const uint32_t v = perm[o];
+      if (v >= own_lo && v < own_hi) {
+        b = off_new[v];
+        len = off_new[v + 1] - b;
+        on = len >= 2;
       }
-      x = bitonic32<long long>(x);
-      if (lane < len) rec[lane] = make_int2((int)(uint32_t)x, (int)(x >> 32));
+    }
+    if (!__any_sync(0xffffffffu, on)) continue;
+    if (!__any_sync(0xffffffffu, on && len > 16)) {
+      sort_row<16>(edge, tbits, b, len, on);
+    } else {
+      for (uint32_t h = 0; h < 2; ++h) {  // warp-uniform
+        const uint32_t bh = __shfl_sync(0xffffffffu, b, 16 * h);
+        const uint32_t lh = __shfl_sync(0xffffffffu, len, 16 * h);
+        const bool oh = __shfl_sync(0xffffffffu, on, 16 * h);
+        if (oh) sort_row<32>(edge, tbits, bh, lh, true);
+      }
     }
   }
 }

@@ -229,17 +229,21 @@ namespace egs {
 // relabelled CSR by dst: within a column the sources keep CSR order, i.e.
 // ascending, exactly the reference's stable transpose.  LSD radix sort with
 // 8-bit digits; each pass is a stable counting sort:
-//   k_radix_hist     per-tile digit histogram (tiles of 4096 pairs), written
+//   k_radix_hist     per-tile digit histogram (tiles of kRadixTile pairs), written
 //                    digit-major: hist[d * ntiles + tile]
 //   dev_excl_scan    of the histogram = each (digit, tile)'s output offset
-//   k_radix_scatter  warp w of a tile takes pairs [512 w, 512 w + 512) in 16
-//                    steps of 32 consecutive pairs; __match_any_sync groups a
+//   k_radix_scatter  warp w of a tile takes its kRadixSteps * 32 consecutive
+//                    pairs in steps of 32; __match_any_sync groups a
 //                    step's lanes by digit, per-warp digit counters give each
 //                    pair its rank in (warp, step, lane) order = tile order,
 //                    a prefix over warps per digit completes the tile rank.
 constexpr int kRadixBits = 8;
 constexpr int kRadixDigits = 1 << kRadixBits;
-constexpr int kRadixSteps = kScanItems;  // 16 steps of 32 pairs per warp
+#ifndef EGS_RADIX_STEPS
+#define EGS_RADIX_STEPS 8
+#endif
+constexpr int kRadixSteps = EGS_RADIX_STEPS;           // steps of 32 pairs per warp
+constexpr uint32_t kRadixTile = kScanThreads * kRadixSteps;  // pairs per tile
 
 __global__ void __launch_bounds__(kScanThreads)
     k_radix_hist(const uint32_t* key, uint64_t m, int shift, uint32_t* hist, uint32_t ntiles) {
@@ -247,9 +251,9 @@ __global__ void __launch_bounds__(kScanThreads)
   for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     for (int d = threadIdx.x; d < kRadixDigits; d += kScanThreads) s_h[d] = 0;
     __syncthreads();
-    const uint64_t base = (uint64_t)t * kScanTile;
+    const uint64_t base = (uint64_t)t * kRadixTile;
 #pragma unroll 4
-    for (int k = 0; k < kScanItems; ++k) {
+    for (int k = 0; k < kRadixSteps; ++k) {
       const uint64_t i = base + (uint64_t)k * kScanThreads + threadIdx.x;
       if (i < m) atomicAdd(&s_h[(key[i] >> shift) & (kRadixDigits - 1)], 1u);
     }
@@ -265,20 +269,41 @@ __global__ void __launch_bounds__(kScanThreads)
                     const uint32_t* off, uint32_t ntiles, uint32_t* key_out, uint32_t* val_out) {
   constexpr int W = kScanThreads / 32;
   __shared__ uint32_t s_wc[W][kRadixDigits];  // per-warp digit counts, then warp prefixes
+  __shared__ uint32_t s_off[kRadixDigits];    // the tile's output offset per digit
+  __shared__ uint32_t s_start[kRadixDigits];  // the digit's first position in the tile
+  __shared__ uint32_t s_scan[33];
+  __shared__ uint32_t s_key[kRadixTile], s_val[kRadixTile];  // the tile, locally sorted
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     for (int i = threadIdx.x; i < W * kRadixDigits; i += kScanThreads) (&s_wc[0][0])[i] = 0;
+    for (int d = threadIdx.x; d < kRadixDigits; d += kScanThreads)
+      s_off[d] = off[(uint64_t)d * ntiles + t];
     __syncthreads();
-    const uint64_t wbase = (uint64_t)t * kScanTile + (uint64_t)warp * 32 * kRadixSteps;
+    const uint64_t tbase = (uint64_t)t * kRadixTile;
+    const uint64_t wbase = tbase + (uint64_t)warp * 32 * kRadixSteps;
+    const uint32_t nt = (uint32_t)(m - tbase < kRadixTile ? m - tbase : kRadixTile);
     uint32_t k_[kRadixSteps], v_[kRadixSteps], r_[kRadixSteps];
+    // every load of the warp's 512 pairs first: the ranking steps below
+    // synchronise the warp, which the compiler does not move loads across
+#pragma unroll
+    for (int s = 0; s < kRadixSteps; ++s) {
+      const uint64_t i = wbase + (uint64_t)s * 32 + lane;
+      k_[s] = i < m ? __ldcs(key + i) : 0u;
+      v_[s] = i < m ? __ldcs(val + i) : 0u;
+    }
 #pragma unroll
     for (int s = 0; s < kRadixSteps; ++s) {
       const uint64_t i = wbase + (uint64_t)s * 32 + lane;
       const bool in = i < m;
-      k_[s] = in ? key[i] : 0u;
-      v_[s] = in ? val[i] : 0u;
-      const uint32_t d = in ? (k_[s] >> shift) & (kRadixDigits - 1) : 0xFFFFFFFFu;
-      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      const uint32_t d = in ? (k_[s] >> shift) & (kRadixDigits - 1) : 0u;
+      // the lanes with my digit: one ballot per digit bit, and the valid mask
+      uint32_t peers = __ballot_sync(0xffffffffu, in);
+      if (!in) peers = ~peers;
+#pragma unroll
+      for (int b = 0; b < kRadixBits; ++b) {
+        const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        peers &= ((d >> b) & 1u) ? bb : ~bb;
+      }
       const uint32_t base = in ? s_wc[warp][d] : 0u;
       __syncwarp();
       if (in && (peers & lanemask_lt()) == 0) s_wc[warp][d] = base + __popc(peers);
@@ -286,6 +311,8 @@ __global__ void __launch_bounds__(kScanThreads)
       r_[s] = base + __popc(peers & lanemask_lt());
     }
     __syncthreads();
+    // per digit: warp prefixes and the tile total; then the digits' starts
+    uint32_t tot = 0;
     for (int d = threadIdx.x; d < kRadixDigits; d += kScanThreads) {
       uint32_t acc = 0;
       for (int w = 0; w < W; ++w) {
@@ -293,17 +320,32 @@ __global__ void __launch_bounds__(kScanThreads)
         s_wc[w][d] = acc;
         acc += c;
       }
+      tot = acc;
     }
+    static_assert(kRadixDigits == kScanThreads, "one digit per thread");
+    const uint32_t start = block_excl_scan<uint32_t>(tot, s_scan, nullptr);
+    s_start[threadIdx.x] = start;
     __syncthreads();
+    // local sort into shared memory ...
 #pragma unroll
     for (int s = 0; s < kRadixSteps; ++s) {
       const uint64_t i = wbase + (uint64_t)s * 32 + lane;
       if (i < m) {
         const uint32_t d = (k_[s] >> shift) & (kRadixDigits - 1);
-        const uint32_t pos = off[(uint64_t)d * ntiles + t] + s_wc[warp][d] + r_[s];
-        key_out[pos] = k_[s];
-        val_out[pos] = v_[s];
+        const uint32_t lp = s_start[d] + s_wc[warp][d] + r_[s];
+        s_key[lp] = k_[s];
+        s_val[lp] = v_[s];
       }
+    }
+    __syncthreads();
+    // ... then out in local order: a digit's run goes to consecutive
+    // addresses, so neighbouring threads write neighbouring words
+    for (uint32_t lp = threadIdx.x; lp < nt; lp += kScanThreads) {
+      const uint32_t kk = s_key[lp];
+      const uint32_t d = (kk >> shift) & (kRadixDigits - 1);
+      const uint32_t pos = s_off[d] + (lp - s_start[d]);
+      key_out[pos] = kk;
+      val_out[pos] = s_val[lp];
     }
     __syncthreads();
   }

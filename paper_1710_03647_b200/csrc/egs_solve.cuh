@@ -1754,7 +1754,7 @@ __device__ __forceinline__ void commit_stage_loads(const SolveParams<V>& p, bool
 
 // debug_checks (the reference's check_monotone, solver_par.cpp:116-124,179):
 // a value the next commit publishes must be above the one it replaces.  Run
-// in the commit's phase, before it (reads only).
+// as a phase of its own right before the commit (reads only).
 template <class V>
 __device__ __noinline__ void phase_debug_raise(const SolveParams<V>& p, const uint32_t* chg) {
   const uint32_t nwarps = gridDim.x * kWarps;
@@ -2532,10 +2532,14 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
         !inplace && !cert_now && !p.no_fuse && p.mode != kModeDense && p.mode != kModeSweep &&
         !(p.mode == kModeAuto && (double)changed * p.avg_in_deg * p.sparse_div >= (double)n);
     if (!inplace) {  // a Jacobi round: publish its staged values
+      if (p.debug) {  // (its own phase: the commit overwrites what it compares)
+        begin_phase();
+        phase_debug_raise<V>(p, chg);
+        end_phase(1, 0);
+      }
       begin_phase();
       // (a commit of many raises loads every staged slot with its bitmap word)
       const bool dense_commit = (uint64_t)changed * kDenseCommitDiv >= n;
-      if (p.debug) phase_debug_raise<V>(p, chg);
       if (cert_now) {  // commit + certificate step 1
         if (p.world > 1)
           phase_commit_cert_init<V, true>(p, chg, dense_commit);

@@ -14,6 +14,8 @@
 // GPU variant; the output is the same least fixpoint the reference solvers
 // compute (solver_seq.cpp:124-212, solver_par.cpp:126-435).
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -363,7 +365,7 @@ void dev_radix_sort_pairs(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1
   *ks = k0;
   *vs = v0;
   if (m == 0) return;
-  const uint32_t nt = (uint32_t)((m + egs::kScanTile - 1) / egs::kScanTile);
+  const uint32_t nt = (uint32_t)((m + egs::kRadixTile - 1) / egs::kRadixTile);
   DevBuf d_hist;
   uint32_t* hist = d_hist.alloc<uint32_t>((size_t)egs::kRadixDigits * nt);
   const uint32_t grid = std::min<uint32_t>(nt, (uint32_t)sms * 8);
@@ -657,7 +659,27 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
   // weights stream in
   {
     uint32_t *ks = nullptr, *vs = nullptr;
-    dev_radix_sort_pairs(ck0, cv0, ck1, c->csrc, mo, bits_for(n), s, sms, &ks, &vs);
+    // Default: CUB's onesweep radix sort -- measured against the hand-written
+    // LSD sort (egs_scan.cuh, EGS_CSC_SORT=radix) on one box, C4 one-shot
+    // e2e 34.5 ms vs 46 ms: the transpose finishes after the last weight DMA
+    // either way, and onesweep's single pass per digit is ~2x faster than
+    // the per-tile histogram + scan + scatter passes.  Both are stable, so
+    // the transpose is the same.
+    const char* cs = std::getenv("EGS_CSC_SORT");
+    if (cs && std::strcmp(cs, "radix") == 0) {
+      dev_radix_sort_pairs(ck0, cv0, ck1, c->csrc, mo, bits_for(n), s, sms, &ks, &vs);
+    } else if (mo > 0) {
+      size_t tb = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, ck0, ck1, cv0, c->csrc, mo, 0, bits_for(n), s));
+      DevBuf d_tmp;
+      void* tmp = d_tmp.alloc<uint8_t>(tb);
+      CK(cub::DeviceRadixSort::SortPairs(tmp, tb, ck0, ck1, cv0, c->csrc, mo, 0, bits_for(n), s));
+      ks = ck1;
+      vs = c->csrc;
+    } else {
+      ks = ck1;
+      vs = c->csrc;
+    }
     if (vs != c->csrc) CK(cudaMemcpyAsync(c->csrc, vs, mo * 4, cudaMemcpyDeviceToDevice, s));
     egs::k_col_offsets<<<grid_for(mo + 1, sms), 256, 0, s>>>(n, mo, ks, c->coff);
   }
