@@ -2156,6 +2156,10 @@ template <class V>
 __device__ __forceinline__ void cascade_push_preds(const SolveParams<V>& p, bool removed,
                                                    uint32_t v, uint32_t* qbits) {
   if (!__any_sync(0xffffffffu, removed)) return;
+  // the removal (bit and mark cleared) is visible before any queue bit is
+  // touched: a predecessor still queued (its bit found set) is re-checked
+  // after its consumer clears that bit, and then sees the removal
+  __threadfence();
   uint32_t b = 0, e = 0;
   if (removed) {
     b = __ldg(p.g.coff + v);
@@ -2226,6 +2230,7 @@ __device__ __noinline__ void phase_cert_cascade(const SolveParams<V>& p, const u
       __stcg(s, kRingEmpty);
       __threadfence();
       atomicAnd(qbits + (v >> 5), ~(1u << (v & 31u)));
+      __threadfence();  // (pairs with the pusher's fence: see its removal)
       pos = kNoPos;
     }
     const uint32_t got = __ballot_sync(0xffffffffu, have);

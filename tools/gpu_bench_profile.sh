@@ -14,4 +14,4 @@ EGS_TRACE=1 timeout 300 python tools/ncu_target.py C3 1 > $OUT/trace_c3.txt 2>&1
 timeout 1200 python tools/config_table.py --out $OUT/configs.jsonl > $OUT/configs.out 2>&1; echo "configs rc=$?"
 timeout 600 python tools/part_local_bench.py C4 2 > $OUT/part_local_c4.json 2> $OUT/part_local_c4.err; echo "part-local rc=$?"
 cat $OUT/bench.json
-timeout 1500 python tests/golden/make_golden_plain.py --out $OUT/golden_plain_c3_sweep.json --mode sweep --budget 1200 C3 > $OUT/c3_sweep.out 2>&1; echo "c3 sweep rc=$?"
+
