@@ -783,6 +783,31 @@ __device__ __forceinline__ void row_edges(uint32_t len, uint32_t rot, F&& f) {
 // all-top vertices are skipped without a copy; each lane lifts its own row
 // from shared memory (reads rotated by lane so a half-warp hits distinct
 // banks), 8 gathers in flight.
+// Player-1 light rows of the dense round right after a certificate apply:
+// only the vertices the apply listed as still below top (most player-1
+// vertices were just certified), one per lane, whole warps busy.
+template <class V>
+__device__ __noinline__ void dense_light_p1_listed(const SolveParams<V>& p, const uint32_t* list,
+                                                   uint32_t count, uint32_t* chg,
+                                                   unsigned int* sum_dst) {
+  Local L;
+  const uint32_t nthreads = gridDim.x * kBlock;
+  for (uint32_t i0 = blockIdx.x * kBlock + (threadIdx.x & ~31u); i0 < count; i0 += nthreads) {
+    const uint32_t i = i0 + lane_id();
+    uint32_t v = 0;
+    bool ch = false;
+    if (i < count) {
+      v = ldcg(list + i);
+      ch = lift_thread<V, false>(p, v, L);
+    }
+    if (ch) {
+      set_bit(p, chg, v);
+      ++L.phase_count;
+    }
+  }
+  block_flush(L, sum_dst);
+}
+
 template <class V, bool INPLACE = false>
 __device__ __noinline__ void dense_light_p1(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
                                             unsigned int* cursor, uint32_t* chg,
@@ -1656,7 +1681,7 @@ __device__ __noinline__ void phase_lift(const SolveParams<V>& p, bool dense, Fro
                                         Frontier nxt, unsigned int* cnt_after,
                                         uint32_t* chg, uint32_t* other,
                                         unsigned int* slot_sum, unsigned int* slot_dyn,
-                                        bool sweep = false) {
+                                        bool sweep = false, bool p1_listed = false) {
   const Graph& g = p.g;
   const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
   const uint32_t nthreads = gridDim.x * kBlock;
@@ -1691,8 +1716,11 @@ __device__ __noinline__ void phase_lift(const SolveParams<V>& p, bool dense, Fro
     } else {
       dense_light_p0<V>(p, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]), chg, sum_dst);
       st.lap(kSubLightP0);
-      dense_light_p1<V>(p, clip_lo(p, g.rb[kP1L]), clip_hi(p, g.rb[kP1M]),
-                        slot_dyn + kTileCursor, chg, sum_dst);
+      if (p1_listed)
+        dense_light_p1_listed<V>(p, p.fr[0], vload(&p.sh->p1live), chg, sum_dst);
+      else
+        dense_light_p1<V>(p, clip_lo(p, g.rb[kP1L]), clip_hi(p, g.rb[kP1M]),
+                          slot_dyn + kTileCursor, chg, sum_dst);
     }
     st.lap(kSubLightP1);
   } else {
@@ -1955,6 +1983,7 @@ __device__ __noinline__ void phase_cert_prune(const SolveParams<V>& p, unsigned 
     p.sh->qhead = 0u;
     p.sh->qtail = 0u;
     p.sh->qpend = gridDim.x * kWarps;
+    p.sh->p1live = 0u;  // (the apply that ends this attempt lists into it)
   }
   // (a dense pass leaves the last pass's re-check queue unread: its dedup
   // bitmap is cleared whole)
@@ -2281,10 +2310,38 @@ __device__ __noinline__ void phase_cert_apply(const SolveParams<V>& p, uint32_t*
   constexpr uint32_t U = 8;  // words per warp step, loads issued together
   const uint32_t w_lo = p.own_lo >> 5, w_hi = (p.own_hi + 31) >> 5;
   V* const f = p.f;
+  // the player-1 light vertices left below top are listed for the next
+  // (dense) round, which then lifts only them among player-1 light rows
+  const uint32_t l1_lo = max(p.g.rb[kP1L], p.own_lo), l1_hi = min(p.g.rb[kP1M], p.own_hi);
   for (uint32_t w0 = w_lo + gw * U; w0 < w_hi; w0 += nwarps * U) {
     uint32_t m[U];
 #pragma unroll
     for (uint32_t k = 0; k < U; ++k) m[k] = w0 + k < w_hi ? ldcg(p.cand + w0 + k) : 0u;
+    if (((w0 + U) << 5) > l1_lo && (w0 << 5) < l1_hi) {  // warp-uniform
+      V fv[U];
+#pragma unroll
+      for (uint32_t k = 0; k < U; ++k) {
+        const uint32_t v = ((w0 + k) << 5) + lane;
+        fv[k] = v >= l1_lo && v < l1_hi ? ldcg(f + v) : Top<V>::v;
+      }
+      uint32_t b[U], tot = 0;
+#pragma unroll
+      for (uint32_t k = 0; k < U; ++k) {
+        b[k] = __ballot_sync(0xffffffffu, fv[k] != Top<V>::v && !((m[k] >> lane) & 1u));
+        tot += __popc(b[k]);
+      }
+      if (tot) {  // one reservation per warp step
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&p.sh->p1live, tot);
+        base = __shfl_sync(0xffffffffu, base, 0);
+#pragma unroll
+        for (uint32_t k = 0; k < U; ++k) {
+          if ((b[k] >> lane) & 1u)
+            p.fr[0][base + __popc(b[k] & lanemask_lt())] = ((w0 + k) << 5) + lane;
+          base += __popc(b[k]);
+        }
+      }
+    }
 #pragma unroll
     for (uint32_t k = 0; k < U; ++k) {
       const bool hit = (m[k] >> lane) & 1u;  // candidate words hold owned, non-top ids only
@@ -2695,8 +2752,11 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
     uint32_t* next = p.chg[round & 1];
     begin_phase();
     if (leader && p.timeout_ns && t_prev - t_start > p.timeout_ns) sh->stop = 1;
+    // (right after a certificate apply, a Jacobi dense round lifts only the
+    // player-1 light vertices the apply listed below top)
     phase_lift<V>(p, dense, frontier(tok), frontier(tok + 1), sh->fr_cnt[(tok + 2) % 3], next,
-                  chg, slot_sum(), slot_dyn(), p.mode == kModeSweep);
+                  chg, slot_sum(), slot_dyn(), p.mode == kModeSweep,
+                  dense && cert_now && p.mode != kModeSweep);
     end_phase(1);
     inplace = !dense || p.mode == kModeSweep;  // a sweep round needs no commit
     if (inplace) {

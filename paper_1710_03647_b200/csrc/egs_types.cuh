@@ -87,6 +87,9 @@ struct Scratch {
   // the certificate cascade's work queue (egs_solve.cuh phase_cert_cascade):
   // ring positions claimed / reserved, and items reserved but not finished
   unsigned int qhead, qtail, qpend;
+  // the player-1 light vertices still below top after a certificate apply,
+  // listed (in SolveParams::fr[0]) for the dense round that follows
+  unsigned int p1live;
 };
 
 // Cross-rank sync block (multi-GPU, egs_part_solve), inside every rank's
