@@ -23,7 +23,7 @@ all: $(LIB) $(ORACLE_LIB) $(ORACLE_CLI) ref
 
 HDRS := $(CSRC)/egs_types.cuh $(CSRC)/egs_device.cuh include/egs_gpu.h
 
-$(CSRC)/egs_solver.o: $(CSRC)/egs_solver.cu $(CSRC)/egs_build.cuh $(CSRC)/egs_scan.cuh $(HDRS)
+$(CSRC)/egs_solver.o: $(CSRC)/egs_solver.cu $(CSRC)/egs_build.cuh $(CSRC)/egs_scan.cuh $(CSRC)/egs_narrow.h $(HDRS)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/egs_solver.ptxas.log || (cat $(CSRC)/egs_solver.ptxas.log; false)
 
 # the solve kernels, once per edge-record format (8-byte int2 / packed 4-byte)
@@ -39,7 +39,10 @@ $(CSRC)/egs_host.o: $(CSRC)/egs_host.cpp $(CSRC)/egs_host_arena.h include/egs_gp
 $(CSRC)/egs_arena_io.o: $(CSRC)/egs_arena_io.cpp $(CSRC)/egs_host_arena.h include/egs_gpu.h
 	$(CXX) -O3 -std=c++17 -fPIC -Iinclude -c $< -o $@
 
-$(LIB): $(CSRC)/egs_solver.o $(CSRC)/egs_kern_e8.o $(CSRC)/egs_kern_e4.o $(CSRC)/egs_host.o $(CSRC)/egs_arena_io.o
+$(CSRC)/egs_narrow.o: $(CSRC)/egs_narrow.cpp $(CSRC)/egs_narrow.h
+	$(CXX) -O3 -std=c++17 -fPIC -c $< -o $@
+
+$(LIB): $(CSRC)/egs_solver.o $(CSRC)/egs_kern_e8.o $(CSRC)/egs_kern_e4.o $(CSRC)/egs_host.o $(CSRC)/egs_arena_io.o $(CSRC)/egs_narrow.o
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -lpthread
 
 $(ORACLE_LIB): oracle/egs_oracle.c oracle/egs_oracle.h

@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(256)
                       const uint32_t* dst, const uint32_t* perm, const uint32_t* off_new,
                       void* edge, uint32_t tbits, uint32_t* ckey, uint32_t* cval,
                       unsigned int* bad, uint32_t* longlist, unsigned int* longcnt,
-                      uint32_t own_lo, uint32_t own_hi) {
+                      uint32_t own_lo, uint32_t own_hi, bool key_at_orig) {
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int* ex = static_cast<int*>(edge);
@@ -86,8 +86,9 @@ __global__ void __launch_bounds__(256)
           px[pos] = t;  // the weight half is or-ed in by k_relabel_weights
         else
           ex[2 * (size_t)pos] = (int)t;
-        ckey[pos] = t;
-        cval[pos] = src;
+        const uint32_t kp = key_at_orig ? idx : pos;  // (see k_csc_runs)
+        ckey[kp] = t;
+        cval[kp] = src;
       }
     });
   }
@@ -139,7 +140,7 @@ __global__ void __launch_bounds__(256)
     k_relabel_targets_long(uint32_t n, const uint32_t* longlist, const unsigned int* longcnt,
                            const uint64_t* off64, const uint32_t* dst, const uint32_t* perm,
                            const uint32_t* off_new, void* edge, uint32_t tbits, uint32_t* ckey,
-                           uint32_t* cval, unsigned int* bad) {
+                           uint32_t* cval, unsigned int* bad, bool key_at_orig) {
   int* ex = static_cast<int*>(edge);
   uint32_t* px = static_cast<uint32_t*>(edge);
   unsigned int flag = 0;
@@ -159,8 +160,9 @@ __global__ void __launch_bounds__(256)
         px[pos] = t;
       else
         ex[2 * (size_t)pos] = (int)t;
-      ckey[pos] = t;
-      cval[pos] = rn;
+      const uint32_t kp = key_at_orig ? idx : pos;
+      ckey[kp] = t;
+      cval[kp] = rn;
     }
   }
   if (flag) atomicOr(bad, flag);
@@ -271,6 +273,90 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Transpose built chunk by chunk while the upload runs (single-rank build,
+// egs_solver.cu build_arena).  Each target chunk's (target, source) pairs sit
+// at their original edge positions; once sorted by target (stably: original
+// order within a target), every element gets its slot inside its column
+// relative to the column start -- the column's edges from earlier chunks
+// (cnt) plus its rank in this chunk's run of that target.  After the last
+// chunk the column offsets are the scan of cnt and one scatter places every
+// source.  A column lists its sources in original edge order, which for a
+// CSR is ascending original source id.
+// Heads of the runs of the sorted chunk: rb[t] = {run start, edges of t in
+// earlier chunks}.
+__global__ void k_csc_runs(const uint32_t* key, uint64_t len, const uint32_t* cnt, uint2* rb) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += stride) {
+    const uint32_t t = key[i];
+    if (i == 0 || key[i - 1] != t) rb[t] = make_uint2((uint32_t)i, cnt[t]);
+  }
+}
+// rel[i] = the element's slot in its column; the run's last element adds the
+// run to cnt (read above only by the heads, so no element races its update)
+__global__ void k_csc_rel(const uint32_t* key, uint64_t len, const uint2* rb, uint32_t* cnt,
+                          uint32_t* rel) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += stride) {
+    const uint32_t t = key[i];
+    const uint2 h = rb[t];
+    const uint32_t r = h.y + (uint32_t)(i - h.x);
+    rel[i] = r;
+    if (i + 1 == len || key[i + 1] != t) cnt[t] = r + 1;
+  }
+}
+// csrc[coff[t] + rel] = source.  A plain scatter writes 4 bytes per 32-byte
+// sector (a chunk holds ~one edge per column): 5.6 ms at C4.  Instead each
+// CTA assembles kMergeSpan consecutive output slots in shared memory and
+// stores them coalesced.  Within one chunk's sorted pairs the slot
+// pos(i) = coff[key[i]] + rel[i] strictly increases with i (rel counts up
+// inside a run, and a column's slots end before the next column's start), so
+// the pairs landing in [p0, p1) are one contiguous range per chunk: two
+// binary searches, one lane per chunk.  Each pair is read once, hubs
+// included.
+constexpr uint32_t kMergeSpan = 8192;
+constexpr int kMaxChunks = 32;
+struct ChunkStarts {
+  uint64_t e[kMaxChunks + 1];  // chunk k's sorted pairs: [e[k], e[k+1])
+  int nch;
+};
+// first i in [lo, hi) with coff[key[i]] + rel[i] >= p
+__device__ __forceinline__ uint64_t lower_slot(const uint32_t* key, const uint32_t* rel,
+                                               const uint32_t* coff, uint64_t lo, uint64_t hi,
+                                               uint64_t p) {
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if ((uint64_t)coff[key[mid]] + rel[mid] < p)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+__global__ void __launch_bounds__(512)
+    k_csc_merge(const uint32_t* key, const uint32_t* val, const uint32_t* rel, uint64_t m,
+                const uint32_t* coff, ChunkStarts cs, uint32_t* csrc) {
+  __shared__ uint32_t slot[kMergeSpan];
+  __shared__ uint64_t rlo[kMaxChunks], rhi[kMaxChunks];
+  for (uint64_t p0 = (uint64_t)blockIdx.x * kMergeSpan; p0 < m;
+       p0 += (uint64_t)gridDim.x * kMergeSpan) {
+    const uint64_t p1 = min(m, p0 + (uint64_t)kMergeSpan);
+    if (threadIdx.x < 2u * cs.nch) {
+      const int k = threadIdx.x >> 1;
+      if (threadIdx.x & 1)
+        rhi[k] = lower_slot(key, rel, coff, cs.e[k], cs.e[k + 1], p1);
+      else
+        rlo[k] = lower_slot(key, rel, coff, cs.e[k], cs.e[k + 1], p0);
+    }
+    __syncthreads();
+    for (int k = 0; k < cs.nch; ++k)
+      for (uint64_t i = rlo[k] + threadIdx.x; i < rhi[k]; i += blockDim.x)
+        slot[coff[key[i]] + rel[i] - p0] = val[i];
+    __syncthreads();
+    for (uint64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) csrc[p] = slot[p - p0];
+    __syncthreads();
+  }
+}
+
 // CSC column offsets from the dst-sorted keys: coff[t] = first j with
 // key[j] >= t, coff[n] = m.
 __global__ void k_col_offsets(uint32_t n, uint64_t m, const uint32_t* key,
@@ -293,6 +379,14 @@ __global__ void k_export(uint32_t n, const V* f, const uint32_t* perm, int64_t* 
     const V x = f[perm[v]];
     out[v] = x == Top<V>::v ? INT64_MAX : static_cast<int64_t>(x);
   }
+}
+
+// 32-bit values in original ids, top kept as all ones (widened on the host:
+// egs_internal_widen_u32)
+__global__ void k_export_u32(uint32_t n, const uint32_t* f, const uint32_t* perm, uint32_t* out) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += gridDim.x * blockDim.x)
+    out[v] = f[perm[v]];
 }
 
 // out[v] = widen(f[v]) in relabelled ids (the debug_checks fixpoint test of
@@ -391,6 +485,32 @@ __global__ void __launch_bounds__(256)
     if (lane_id() == 0 && acc != f[v]) ++nb;
   }
   if (nb) atomicAdd(bad, nb);
+}
+
+// The transpose holds exactly the CSR's edges: an order-free fingerprint,
+// sum[0] over the CSR rows and sum[1] over the CSC columns of
+// mix(source, target), plus sum[2] = columns whose offsets decrease.  One warp
+// per vertex (debug checks only).
+__device__ __forceinline__ unsigned long long edge_mix(uint32_t s, uint32_t t) {
+  unsigned long long x = ((unsigned long long)s << 32 | t) + 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+__global__ void __launch_bounds__(256)
+    k_csc_check(Graph g, unsigned long long* sum) {
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  unsigned long long a = 0, b = 0, bad = 0;
+  for (uint32_t v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < g.n; v += nwarps) {
+    for (uint32_t i = g.off[v] + lane_id(); i < g.off[v + 1]; i += 32)
+      a += edge_mix(v, (uint32_t)edge_at(g, i).x);
+    const uint32_t cb = g.coff[v], ce = g.coff[v + 1];
+    if (lane_id() == 0 && ce < cb) ++bad;
+    for (uint32_t j = cb + lane_id(); j < ce; j += 32) b += edge_mix(g.csrc[j], v);
+  }
+  if (a) atomicAdd(sum, a);
+  if (b) atomicAdd(sum + 1, b);
+  if (bad) atomicAdd(sum + 2, bad);
 }
 
 // ---------------------------------------------- solution output ----

@@ -32,6 +32,7 @@
 
 #include "egs_build.cuh"
 #include "egs_gpu.h"
+#include "egs_narrow.h"
 #include "egs_scan.cuh"
 #include "egs_types.cuh"
 
@@ -218,6 +219,31 @@ namespace {
 
 // EGS_VERBOSE=1 prints the device arena construction steps (host clock,
 // stream-synchronised) to stderr.
+// EGS_TIMELINE=1: stream-order event marks of the build, printed relative
+// to the first (timing events; no synchronisation between marks)
+struct Timeline {
+  bool on = std::getenv("EGS_TIMELINE") != nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> ev;
+  void mark(const std::string& what, cudaStream_t s) {
+    if (!on) return;
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(e, s));
+    ev.emplace_back(what, e);
+  }
+  ~Timeline() {
+    if (ev.empty()) return;
+    cudaEventSynchronize(ev.back().second);
+    for (auto& [w, e] : ev) {
+      cudaEventSynchronize(e);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[0].second, e);
+      std::fprintf(stderr, "[egs timeline] %8.3f ms  %s\n", ms, w.c_str());
+    }
+    for (auto& [w, e] : ev) cudaEventDestroy(e);
+  }
+};
+
 struct StepTimer {
   cudaStream_t s;
   bool on;
@@ -394,11 +420,22 @@ struct LongRows {
   uint32_t cap;
 };
 
+inline bool narrow_weights(const int64_t* in, int8_t* out, size_t k, int64_t wmax) {
+  return egs_internal_narrow_i8(in, out, k, wmax);
+}
+inline bool narrow_weights(const int64_t* in, int16_t* out, size_t k, int64_t wmax) {
+  return egs_internal_narrow_i16(in, out, k, wmax);
+}
+inline bool narrow_weights(const int64_t* in, int32_t* out, size_t k, int64_t wmax) {
+  return egs_internal_narrow_i32(in, out, k, wmax);
+}
+
 template <class W>
 bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint32_t>& rows,
                     const std::vector<std::vector<std::pair<uint64_t, uint64_t>>>& spans,
                     std::vector<cudaEvent_t>& ew, std::vector<cudaEvent_t>& et,
-                    const uint64_t* off64, void* wdev, LongRows lw, const uint8_t* key) {
+                    const uint64_t* off64, void* wdev, LongRows lw, const uint8_t* key,
+                    Timeline& tl) {
   cudaStream_t sc = c->copy_stream, sw = c->aux_stream;
   const int nch = (int)rows.size() - 1;
   const uint64_t m = c->m;
@@ -440,13 +477,7 @@ bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint3
     if (b >= nblk) return false;
     k = blocks[b].k;
     const uint64_t lo = blocks[b].lo, hi = blocks[b].hi;
-    bool bad = false;
-    for (uint64_t i = lo; i < hi; ++i) {
-      const int64_t x = w[i];
-      bad |= x < -wmax || x > wmax;
-      stage[i] = (W)x;
-    }
-    if (bad) out_of_range.store(true, std::memory_order_relaxed);
+    if (narrow_weights(w + lo, stage + lo, hi - lo, wmax)) out_of_range.store(true, std::memory_order_relaxed);
     left[k].fetch_sub(1, std::memory_order_release);
     return true;
   };
@@ -478,6 +509,7 @@ bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint3
       c->h2d_bytes += (e1 - e0) * sizeof(W);
     }
     CK(cudaEventRecord(ew[k], sc));
+    tl.mark("copy: weights chunk " + std::to_string(k), sc);
     CK(cudaStreamWaitEvent(sw, ew[k], 0));
     // packed records: the weight bits are or-ed into the target words
     if (c->tbits) CK(cudaStreamWaitEvent(sw, et[k], 0));
@@ -503,10 +535,13 @@ bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint3
 // Build the relabelled device arena from the reference CSR (host spans),
 // pipelined with the upload: the copy stream brings offsets + owners, then
 // the targets and the weights in row-range chunks of ~m/16 edges; the main
-// stream classifies and relabels the vertices and relabels each target chunk
-// as it lands, then sorts the transpose while the weights are still on the
-// wire; the aux stream writes each weight chunk as it lands.  The result is
-// ready when the last weight chunk is (PCIe-bound).
+// stream classifies and relabels the vertices, and relabels each target
+// chunk as it lands and sorts and ranks its transpose pairs (k_csc_runs)
+// before the next one lands; the last chunk's merge (k_csc_merge) runs while
+// the weights are on the wire, which host threads narrow from int64 as the
+// targets go (egs_narrow.cpp); the aux stream writes each weight chunk as it
+// lands.  The result is ready shortly after the last weight chunk is
+// (PCIe-bound: C4's 1.42 GB take 25.6 ms at 55.6 GB/s).
 // Several ranks (`plan` set): the relabelling is the plan's rank-major order
 // and this rank keeps its own rows [own_lo, own_hi) only (m_own edges), with
 // the transpose of those rows (the predecessors it activates).
@@ -519,7 +554,7 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
   cudaStream_t s = c->stream, sc = c->copy_stream, sw = c->aux_stream;
   const int sms = c->num_sms;
   DevBuf d_off64, d_dst, d_wn, d_owner, d_key, d_tcount, d_misc, d_ck0, d_cv0, d_ck1,
-      d_long;
+      d_long, d_cv1, d_rel, d_cnt, d_rb, d_stmp;
   uint64_t* off64 = d_off64.alloc<uint64_t>((size_t)n + 1);
   uint32_t* dst = d_dst.alloc<uint32_t>(m);
   void* wn = d_wn.alloc<int32_t>(m);  // narrowed weights (int8/16/32)
@@ -539,6 +574,19 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
   uint32_t* ck0 = d_ck0.alloc<uint32_t>(mo);
   uint32_t* cv0 = d_cv0.alloc<uint32_t>(mo);
   uint32_t* ck1 = d_ck1.alloc<uint32_t>(mo);
+  // transpose: chunk by chunk during the upload (one rank; k_csc_runs), or
+  // one sort of all pairs at the end (several ranks -- a rank's own rows are
+  // not chunk-contiguous -- or EGS_CSC_SORT=end (CUB) | radix (egs_scan.cuh))
+  const char* csc_sort = std::getenv("EGS_CSC_SORT");
+  const bool csc_inc = c->runs.empty() && mo > 0 && !csc_sort;
+  uint32_t *cv1 = nullptr, *rel = nullptr, *ccnt = nullptr;
+  uint2* rb = nullptr;
+  if (csc_inc) {
+    cv1 = d_cv1.alloc<uint32_t>(mo);
+    rel = d_rel.alloc<uint32_t>(mo);
+    ccnt = d_cnt.alloc<uint32_t>((size_t)n + 1);
+    rb = d_rb.alloc<uint2>(n);
+  }
   c->perm = dalloc<uint32_t>(n);
   c->off = dalloc<uint32_t>((size_t)n + 1);
   // packed 4-byte records when every weight fits beside the target bits
@@ -554,6 +602,7 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
   c->csrc = dalloc<uint32_t>(mo);
   c->coff = dalloc<uint32_t>((size_t)n + 1);
   CK(cudaMemsetAsync(misc, 0, 64 * sizeof(unsigned int), s));
+  if (csc_inc) CK(cudaMemsetAsync(ccnt, 0, ((size_t)n + 1) * sizeof(uint32_t), s));
   tm.mark("pool allocations");
   cudaEvent_t e_alloc, e_vert, e_perm, e_tail;
   CK(cudaEventCreateWithFlags(&e_alloc, cudaEventDisableTiming));
@@ -561,11 +610,14 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
   CK(cudaEventCreateWithFlags(&e_perm, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&e_tail, cudaEventDisableTiming));
   CK(cudaEventRecord(e_alloc, s));
+  Timeline tl;
+  tl.mark("start", s);
   CK(cudaStreamWaitEvent(sc, e_alloc, 0));
   CK(cudaStreamWaitEvent(sw, e_alloc, 0));
 
   // row-range chunks of ~m/16 edges (host offsets are at hand)
   constexpr int kChunks = 16;
+  static_assert(kChunks <= egs::kMaxChunks, "k_csc_merge's chunk table");
   std::vector<uint32_t> rows{0};
   for (int k = 1; k < kChunks; ++k) {
     const uint64_t target = m * (uint64_t)k / kChunks;
@@ -606,12 +658,14 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
   CK(cudaMemcpyAsync(off64, a->csr_offsets, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice, sc));
   CK(cudaMemcpyAsync(owner, a->owners, n, cudaMemcpyHostToDevice, sc));
   CK(cudaEventRecord(e_vert, sc));
+  tl.mark("copy: vertices landed", sc);
   for (int k = 0; k < nch; ++k) {
     for (const auto& [e0, e1] : spans[k]) {
       CK(cudaMemcpyAsync(dst + e0, a->csr_targets + e0, (e1 - e0) * 4, cudaMemcpyHostToDevice, sc));
       c->h2d_bytes += (e1 - e0) * 4;
     }
     CK(cudaEventRecord(ex[k], sc));
+    tl.mark("copy: targets chunk " + std::to_string(k), sc);
   }
 
   // vertices: class keys and per-tile class counts, their scan, the stable
@@ -640,33 +694,65 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
   CK(cudaGetLastError());
   dev_excl_scan<uint32_t>(c->off, c->off, (uint64_t)n + 1, s, sms);
   CK(cudaEventRecord(e_perm, s));
+  tl.mark("main: vertex relabel done", s);
   tm.mark("vertices (classify, sort, offsets)");
 
-  // targets as they land (main stream)
+  // the incremental transpose's sort temporaries, sized for the largest chunk
+  void* sort_tmp = nullptr;
+  size_t sort_tb = 0;
+  if (csc_inc) {
+    uint64_t maxlen = 0;
+    for (int k = 0; k < nch; ++k)
+      maxlen = std::max<uint64_t>(maxlen, a->csr_offsets[rows[k + 1]] - a->csr_offsets[rows[k]]);
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, sort_tb, ck0, ck1, cv0, cv1, (int64_t)maxlen, 0,
+                                       bits_for(n), s));
+    sort_tmp = d_stmp.alloc<uint8_t>(sort_tb);
+  }
+
+  // targets as they land (main stream); with the incremental transpose each
+  // chunk's pairs are sorted and ranked before the next chunk lands
   for (int k = 0; k < nch; ++k) {
     CK(cudaStreamWaitEvent(s, ex[k], 0));
     egs::k_relabel_targets<<<grid_for((uint64_t)(rows[k + 1] - rows[k]) * 4, sms), 256, 0, s>>>(
         n, rows[k], rows[k + 1], off64, dst, c->perm, c->off, c->edge, c->tbits, ck0, cv0,
-        misc + 16, lt.list + (size_t)k * lt.cap, lt.cnt + k, c->own_lo, c->own_hi);
+        misc + 16, lt.list + (size_t)k * lt.cap, lt.cnt + k, c->own_lo, c->own_hi, csc_inc);
     egs::k_relabel_targets_long<<<2 * sms, 256, 0, s>>>(
         n, lt.list + (size_t)k * lt.cap, lt.cnt + k, off64, dst, c->perm, c->off, c->edge,
-        c->tbits, ck0, cv0, misc + 16);
+        c->tbits, ck0, cv0, misc + 16, csc_inc);
     CK(cudaGetLastError());
     CK(cudaEventRecord(et[k], s));
+    tl.mark("main: targets relabelled " + std::to_string(k), s);
+    if (csc_inc) {
+      const uint64_t e0 = a->csr_offsets[rows[k]], len = a->csr_offsets[rows[k + 1]] - e0;
+      if (len == 0) continue;
+      CK(cub::DeviceRadixSort::SortPairs(sort_tmp, sort_tb, ck0 + e0, ck1 + e0, cv0 + e0,
+                                         cv1 + e0, (int64_t)len, 0, bits_for(n), s));
+      egs::k_csc_runs<<<grid_for(len, sms), 256, 0, s>>>(ck1 + e0, len, ccnt, rb);
+      egs::k_csc_rel<<<grid_for(len, sms), 256, 0, s>>>(ck1 + e0, len, rb, ccnt, rel + e0);
+      CK(cudaGetLastError());
+      tl.mark("main: transpose chunk " + std::to_string(k), s);
+    }
   }
 
-  // transpose: stable radix sort of the (dst, src) pairs by dst while the
-  // weights stream in
-  {
+  if (csc_inc) {
+    dev_excl_scan<uint32_t>(ccnt, c->coff, (uint64_t)n + 1, s, sms);
+    egs::ChunkStarts cs{};
+    cs.nch = nch;
+    for (int k = 0; k <= nch; ++k) cs.e[k] = a->csr_offsets[rows[k]];
+    const uint64_t spans_n = (mo + egs::kMergeSpan - 1) / egs::kMergeSpan;
+    egs::k_csc_merge<<<(uint32_t)std::min<uint64_t>(spans_n, (uint64_t)sms * 4), 512, 0, s>>>(
+        ck1, cv1, rel, mo, c->coff, cs, c->csrc);
+    CK(cudaGetLastError());
+  } else {
+    // transpose: stable radix sort of the (dst, src) pairs by dst while the
+    // weights stream in
     uint32_t *ks = nullptr, *vs = nullptr;
-    // Default: CUB's onesweep radix sort -- measured against the hand-written
-    // LSD sort (egs_scan.cuh, EGS_CSC_SORT=radix) on one box, C4 one-shot
-    // e2e 34.5 ms vs 46 ms: the transpose finishes after the last weight DMA
-    // either way, and onesweep's single pass per digit is ~2x faster than
-    // the per-tile histogram + scan + scatter passes.  Both are stable, so
-    // the transpose is the same.
-    const char* cs = std::getenv("EGS_CSC_SORT");
-    if (cs && std::strcmp(cs, "radix") == 0) {
+    // CUB's onesweep radix sort, or the hand-written LSD sort (egs_scan.cuh,
+    // EGS_CSC_SORT=radix) -- measured on one box, C4 one-shot e2e 34.5 ms vs
+    // 46 ms: onesweep's single pass per digit is ~2x faster than the per-tile
+    // histogram + scan + scatter passes.  Both are stable, so the transpose
+    // is the same (columns in ascending relabelled source order).
+    if (csc_sort && std::strcmp(csc_sort, "radix") == 0) {
       dev_radix_sort_pairs(ck0, cv0, ck1, c->csrc, mo, bits_for(n), s, sms, &ks, &vs);
     } else if (mo > 0) {
       size_t tb = 0;
@@ -683,20 +769,22 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
     if (vs != c->csrc) CK(cudaMemcpyAsync(c->csrc, vs, mo * 4, cudaMemcpyDeviceToDevice, s));
     egs::k_col_offsets<<<grid_for(mo + 1, sms), 256, 0, s>>>(n, mo, ks, c->coff);
   }
+  tl.mark("main: transpose done", s);
   CK(cudaGetLastError());
 
   CK(cudaStreamWaitEvent(sw, e_perm, 0));
   {
     const int64_t mw = a->max_abs_weight;
     if (mw <= 127)
-      h_stage_bad = upload_weights<int8_t>(c, a, rows, spans, ew, et, off64, wn, lw, key);
+      h_stage_bad = upload_weights<int8_t>(c, a, rows, spans, ew, et, off64, wn, lw, key, tl);
     else if (mw <= 32767)
-      h_stage_bad = upload_weights<int16_t>(c, a, rows, spans, ew, et, off64, wn, lw, key);
+      h_stage_bad = upload_weights<int16_t>(c, a, rows, spans, ew, et, off64, wn, lw, key, tl);
     else
-      h_stage_bad = upload_weights<int32_t>(c, a, rows, spans, ew, et, off64, wn, lw, key);
+      h_stage_bad = upload_weights<int32_t>(c, a, rows, spans, ew, et, off64, wn, lw, key, tl);
   }
   tm.mark("upload + relabel + CSC sort");
   CK(cudaEventRecord(e_tail, sw));
+  tl.mark("aux: weights relabelled, rows sorted", sw);
   CK(cudaStreamWaitEvent(s, e_tail, 0));
   unsigned int h_misc[32] = {0};
   CK(cudaMemcpyAsync(h_misc, misc, sizeof(h_misc), cudaMemcpyDeviceToHost, s));
@@ -712,7 +800,13 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
   d_ck1.release();
   d_misc.release();
   d_long.release();
+  d_cv1.release();
+  d_rel.release();
+  d_cnt.release();
+  d_rb.release();
+  d_stmp.release();
   CK(cudaStreamSynchronize(s));
+  tl.mark("main: joined", s);
   tm.mark("weights + join");
   for (auto e : ex) cudaEventDestroy(e);
   for (auto e : ew) cudaEventDestroy(e);
@@ -1068,19 +1162,23 @@ void debug_verify(egs_ctx* c) {
   cudaStream_t s = c->stream;
   g_alloc_stream = s;
   DevBuf d_misc;
-  unsigned long long* misc = d_misc.alloc<unsigned long long>(1);
-  CK(cudaMemsetAsync(misc, 0, sizeof(unsigned long long), s));
+  unsigned long long* misc = d_misc.alloc<unsigned long long>(4);
+  CK(cudaMemsetAsync(misc, 0, 4 * sizeof(unsigned long long), s));
+  // (a partition rank's transpose covers its own rows only, as its CSR does)
+  egs::k_csc_check<<<grid_for((uint64_t)c->n * 32, c->num_sms), 256, 0, s>>>(c->graph(), misc + 1);
   egs::k_widen<V><<<grid_for(c->n, c->num_sms), 256, 0, s>>>(c->n, static_cast<const V*>(c->f),
                                                               c->f64);
   egs::k_fixpoint<<<grid_for((uint64_t)c->n * 32, c->num_sms), 256, 0, s>>>(c->graph(), c->f64,
                                                                             misc);
   CK(cudaGetLastError());
-  unsigned long long h[2] = {0, 0};
+  unsigned long long h[4] = {0, 0, 0, 0};
   unsigned int bad = 0;
-  CK(cudaMemcpyAsync(&h[0], misc, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h, misc, sizeof(h), cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(&bad, &c->scratch->bad, 4, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (bad) throw Fail(EGS_ERR_INTERNAL, "measure decreased across a round");
+  if (h[1] != h[2] || h[3])
+    throw Fail(EGS_ERR_INTERNAL, "the transpose does not hold the arena's edges");
   // (a partition rank holds its own rows only: the fixpoint test is the
   // single-GPU context's)
   if (h[0] && c->world == 1)
@@ -1163,16 +1261,53 @@ void ctx_read(egs_ctx* c, int64_t* out) {
   if (c->n == 0) return;
   CK(cudaSetDevice(c->device));
   cudaStream_t s = c->stream;
-  const uint32_t grid = grid_for(c->n, c->num_sms);
-  if (c->vbits == 32)
-    egs::k_export<uint32_t><<<grid, 256, 0, s>>>(c->n, static_cast<uint32_t*>(c->f), c->perm,
+  const uint32_t n = c->n, grid = grid_for(n, c->num_sms);
+  if (c->vbits == 64) {
+    egs::k_export<uint64_t><<<grid, 256, 0, s>>>(n, static_cast<uint64_t*>(c->f), c->perm,
                                                   c->f64);
-  else
-    egs::k_export<uint64_t><<<grid, 256, 0, s>>>(c->n, static_cast<uint64_t*>(c->f), c->perm,
-                                                  c->f64);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, c->f64, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return;
+  }
+  // 32-bit values cross PCIe at 4 bytes (half the int64 encoding) in chunks
+  // into the pinned stage; host threads widen each chunk as it lands
+  // (egs_internal_widen_u32: top -> INT64_MAX) while the next is on the wire.
+  uint32_t* dev = reinterpret_cast<uint32_t*>(c->f64);
+  egs::k_export_u32<<<grid, 256, 0, s>>>(n, static_cast<uint32_t*>(c->f), c->perm, dev);
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(out, c->f64, (size_t)c->n * 8, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  uint32_t* stage = static_cast<uint32_t*>(pinned_stage((uint64_t)n * 4));
+  constexpr int kParts = 8;
+  cudaEvent_t ev[kParts];
+  auto lo = [&](int k) { return (uint64_t)n * k / kParts; };
+  for (int k = 0; k < kParts; ++k) {
+    CK(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
+    CK(cudaMemcpyAsync(stage + lo(k), dev + lo(k), (lo(k + 1) - lo(k)) * 4,
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(ev[k], s));
+  }
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const unsigned T = n >= (1u << 20) ? hw : 1;
+  auto work = [&](unsigned t) {  // slice t of every part, in landing order
+    for (int k = 0; k < kParts; ++k) {
+      cudaEventSynchronize(ev[k]);
+      const uint64_t a = lo(k) + (lo(k + 1) - lo(k)) * t / T;
+      const uint64_t b = lo(k) + (lo(k + 1) - lo(k)) * (t + 1) / T;
+      egs_internal_widen_u32(stage + a, out + a, b - a);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < T; ++t) pool.emplace_back(work, t);
+  work(0);
+  for (auto& th : pool) th.join();
+  cudaError_t err = cudaSuccess;
+  for (int k = 0; k < kParts; ++k) {
+    const cudaError_t e = cudaEventQuery(ev[k]);
+    if (e != cudaSuccess && err == cudaSuccess) err = e;
+    cudaEventDestroy(ev[k]);
+  }
+  CK(err);
 }
 
 template <class V>

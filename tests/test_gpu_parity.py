@@ -435,23 +435,31 @@ def test_full_size_configs_properties(egs, name, spec):
                 assert np.array_equal(f, base), opts
 
 
-@pytest.mark.parametrize("make", [lambda e: e.GameArena.fixed(100000, 16, 100, 1),
-                                  lambda e: e.GameArena.rmat(14, 16, 100, 1)],
-                         ids=["fixed-1e5-16", "rmat14"])
-def test_transpose_sorts_agree(egs, monkeypatch, make):
-    """The predecessor transpose built by the hand-written LSD radix sort
-    (EGS_CSC_SORT=radix, egs_scan.cuh) and by the default library sort give
-    the identical measure and the identical dense-round work (the sparse
-    rounds and the certificate cascade are order-dependent in their counts)."""
+TRANSPOSE_ARENAS = [lambda e: e.GameArena.fixed(100000, 16, 100, 1),
+                    lambda e: e.GameArena.rmat(14, 16, 100, 1),
+                    lambda e: e.GameArena.rmat(16, 8, 1000, 3),   # hubs spanning merge blocks
+                    lambda e: e.GameArena.fixed(3000, 1, 10, 2)]
+
+
+@pytest.mark.parametrize("make", TRANSPOSE_ARENAS, ids=["fixed-1e5-16", "rmat14", "rmat16", "fixed-d1"])
+def test_transpose_builds_agree(egs, monkeypatch, make):
+    """The predecessor transpose built chunk by chunk during the upload (the
+    default: per-chunk sort, rank, merge -- egs_build.cuh k_csc_*), by one
+    library sort at the end (EGS_CSC_SORT=end) and by the hand-written LSD
+    radix sort (EGS_CSC_SORT=radix, egs_scan.cuh) holds exactly the arena's
+    edges (debug_checks: an order-free CSR/CSC fingerprint) and gives the
+    identical measure and dense-round work (the sparse rounds and the
+    certificate cascade are order-dependent in their counts)."""
     a = make(egs)
     out = {}
-    for mode in ("radix", "default"):
-        if mode == "radix":
-            monkeypatch.setenv("EGS_CSC_SORT", "radix")
-        else:
+    for mode in ("radix", "end", "default"):
+        if mode == "default":
             monkeypatch.delenv("EGS_CSC_SORT", raising=False)
-        with egs.DeviceSolver(a) as ds:
+        else:
+            monkeypatch.setenv("EGS_CSC_SORT", mode)
+        with egs.DeviceSolver(a, egs.SolverOptions(debug_checks=True)) as ds:
             st = ds.solve()
             out[mode] = (ds.read_measure(), st.rounds, st.dense_rounds)
-    assert np.array_equal(out["radix"][0], out["default"][0])
-    assert out["radix"][1:] == out["default"][1:]
+    for mode in ("radix", "end"):
+        assert np.array_equal(out[mode][0], out["default"][0]), mode
+        assert out[mode][1:] == out["default"][1:], mode
