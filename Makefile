@@ -25,13 +25,16 @@ HDRS := $(CSRC)/egs_types.cuh $(CSRC)/egs_device.cuh include/egs_gpu.h
 
 $(CSRC)/egs_solver.o: $(CSRC)/egs_solver.cu $(CSRC)/egs_build.cuh $(CSRC)/egs_scan.cuh $(CSRC)/egs_narrow.h $(HDRS)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/egs_solver.ptxas.log || (cat $(CSRC)/egs_solver.ptxas.log; false)
+	sed -i '/Compile time/d' $(CSRC)/egs_solver.ptxas.log
 
 # the solve kernels, once per edge-record format (8-byte int2 / packed 4-byte)
 $(CSRC)/egs_kern_e8.o: $(CSRC)/egs_kern.cu $(CSRC)/egs_solve.cuh $(HDRS)
 	$(NVCC) $(NVFLAGS) -DEGS_EDGE_BYTES=8 -DEGS_FMT_NS=e8 -c $< -o $@ 2> $(CSRC)/egs_kern_e8.ptxas.log || (cat $(CSRC)/egs_kern_e8.ptxas.log; false)
+	sed -i '/Compile time/d' $(CSRC)/egs_kern_e8.ptxas.log
 
 $(CSRC)/egs_kern_e4.o: $(CSRC)/egs_kern.cu $(CSRC)/egs_solve.cuh $(HDRS)
 	$(NVCC) $(NVFLAGS) -DEGS_EDGE_BYTES=4 -DEGS_FMT_NS=e4 -c $< -o $@ 2> $(CSRC)/egs_kern_e4.ptxas.log || (cat $(CSRC)/egs_kern_e4.ptxas.log; false)
+	sed -i '/Compile time/d' $(CSRC)/egs_kern_e4.ptxas.log
 
 $(CSRC)/egs_host.o: $(CSRC)/egs_host.cpp $(CSRC)/egs_host_arena.h include/egs_gpu.h
 	$(CXX) -O3 -std=c++17 -fPIC -Iinclude -I/usr/local/cuda/include -c $< -o $@
