@@ -217,15 +217,17 @@ __device__ __forceinline__ K bitonic32(K x) {
   return x;
 }
 
-// sort the row (b, len) with groups of G lanes (lane index within the group)
+// sort the row (b, len) with groups of G lanes (lane index within the group);
+// the group's first lane also mirrors the sorted first record into rec0[v]
 template <uint32_t G>
 __device__ __forceinline__ void sort_row(void* edge, uint32_t tbits, uint32_t b, uint32_t len,
-                                         bool on) {
+                                         bool on, void* rec0, uint32_t v) {
   const uint32_t l = lane_id() & (G - 1);
   if (tbits) {
     int* rec = static_cast<int*>(edge) + b;
     const int x = bitonic32<int, G>(on && l < len ? rec[l] : INT32_MAX);
     if (on && l < len) rec[l] = x;
+    if (on && l == 0) static_cast<int*>(rec0)[v] = x;
   } else {
     int2* rec = static_cast<int2*>(edge) + b;
     long long x = LLONG_MAX;
@@ -234,40 +236,53 @@ __device__ __forceinline__ void sort_row(void* edge, uint32_t tbits, uint32_t b,
       x = ((long long)r.y << 32) | (long long)(uint32_t)r.x;
     }
     x = bitonic32<long long, G>(x);
-    if (on && l < len) rec[l] = make_int2((int)(uint32_t)x, (int)(x >> 32));
+    const int2 r = make_int2((int)(uint32_t)x, (int)(x >> 32));
+    if (on && l < len) rec[l] = r;
+    if (on && l == 0) static_cast<int2*>(rec0)[v] = r;
   }
 }
 
 // A warp takes two rows: one per half-warp when both have <= 16 edges (the
-// common case), else one after the other with the whole warp.
+// common case), else one after the other with the whole warp.  Each row's
+// first record after the sort -- its least weight, all that round 1 needs of
+// a player-1 row (egs_solve.cuh round1_p1_light) -- is mirrored into rec0[v]
+// (4 or 8 bytes per vertex, read coalesced, instead of a 32-byte sector of
+// the row).
 __global__ void __launch_bounds__(256)
     k_sort_p1_rows(uint32_t r0, uint32_t r1, const uint8_t* key, const uint32_t* perm,
                    const uint32_t* off_new, void* edge, uint32_t tbits, uint32_t own_lo,
-                   uint32_t own_hi) {
+                   uint32_t own_hi, void* rec0) {
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
   const uint32_t lane = lane_id();
   for (uint32_t o0 = r0 + 2 * ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); o0 < r1;
        o0 += 2 * nwarps) {
     const uint32_t o = o0 + (lane >> 4);
     bool on = false;
-    uint32_t b = 0, len = 0;
+    uint32_t b = 0, len = 0, v = 0;
     if (o < r1 && key[o] == (uint8_t)kP1L) {
-      const uint32_t v = perm[o];
+      v = perm[o];
       if (v >= own_lo && v < own_hi) {
         b = off_new[v];
         len = off_new[v + 1] - b;
         on = len >= 2;
+        if (len == 1 && (lane & 15u) == 0) {  // nothing to sort: mirror the record
+          if (tbits)
+            static_cast<int*>(rec0)[v] = static_cast<const int*>(edge)[b];
+          else
+            static_cast<int2*>(rec0)[v] = static_cast<const int2*>(edge)[b];
+        }
       }
     }
     if (!__any_sync(0xffffffffu, on)) continue;
     if (!__any_sync(0xffffffffu, on && len > 16)) {
-      sort_row<16>(edge, tbits, b, len, on);
+      sort_row<16>(edge, tbits, b, len, on, rec0, v);
     } else {
       for (uint32_t h = 0; h < 2; ++h) {  // warp-uniform
         const uint32_t bh = __shfl_sync(0xffffffffu, b, 16 * h);
         const uint32_t lh = __shfl_sync(0xffffffffu, len, 16 * h);
         const bool oh = __shfl_sync(0xffffffffu, on, 16 * h);
-        if (oh) sort_row<32>(edge, tbits, bh, lh, true);
+        const uint32_t vh = __shfl_sync(0xffffffffu, v, 16 * h);
+        if (oh) sort_row<32>(edge, tbits, bh, lh, true, rec0, vh);
       }
     }
   }

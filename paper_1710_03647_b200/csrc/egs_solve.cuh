@@ -1606,10 +1606,11 @@ __device__ __noinline__ void round1_long(const SolveParams<V>& p, uint32_t* chg,
 }
 
 // Player-1 light rows: sorted by weight at upload (egs_build.cuh
-// k_sort_p1_rows), so delta(0)(v) = max(0, -w_min) is the first record's --
-// no row is streamed.  A warp takes kR1Words bitmap words (32 vertices each)
-// per step and issues all their offset loads, then all their record loads,
-// before using any (the two loads of a vertex depend on each other).
+// k_sort_p1_rows), so delta(0)(v) = max(0, -w_min) is the first record's,
+// which the upload mirrors into g.rec0[v] -- no row is streamed: 4 (8) bytes
+// per vertex, coalesced, where a row read costs a 32-byte sector.  A warp
+// takes kR1Words bitmap words (32 vertices each) per step and issues all
+// their loads before using any.
 constexpr int kR1Words = 4;
 template <class V>
 __device__ __noinline__ void round1_p1_light(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
@@ -1621,18 +1622,20 @@ __device__ __noinline__ void round1_p1_light(const SolveParams<V>& p, uint32_t l
     const uint32_t gw = (blockIdx.x * kBlock + threadIdx.x) >> 5, lane = lane_id();
     const uint32_t w_lo = lo >> 5, w_hi = (hi + 31) >> 5;
     for (uint32_t w0 = w_lo + gw * kR1Words; w0 < w_hi; w0 += nwarps * kR1Words) {
-      uint32_t b[kR1Words], e[kR1Words];
       bool in[kR1Words];
+      ERec r[kR1Words];
+      uint32_t eb = 0, ee = 0;  // lane k < kR1Words: the edge span of word w0 + k's rows
 #pragma unroll
       for (int k = 0; k < kR1Words; ++k) {
         const uint32_t v = ((w0 + k) << 5) + lane;
         in[k] = w0 + k < w_hi && v >= lo && v < hi;
-        b[k] = in[k] ? __ldg(g.off + v) : 0u;
-        e[k] = in[k] ? __ldg(g.off + v + 1) : 0u;
+        r[k] = in[k] ? __ldcs(static_cast<const ERec*>(g.rec0) + v) : ERec{};
       }
-      ERec r[kR1Words];
-#pragma unroll
-      for (int k = 0; k < kR1Words; ++k) r[k] = in[k] ? __ldcs(erecs(g) + b[k]) : ERec{};
+      if (lane < (uint32_t)kR1Words && w0 + lane < w_hi) {
+        eb = __ldg(g.off + max(lo, (w0 + lane) << 5));
+        ee = __ldg(g.off + min(hi, ((w0 + lane) << 5) + 32));
+      }
+      L.edges += ee - eb;  // one lift application relaxes the row
 #pragma unroll
       for (int k = 0; k < kR1Words; ++k) {
         const uint32_t v = ((w0 + k) << 5) + lane;
@@ -1641,7 +1644,6 @@ __device__ __noinline__ void round1_p1_light(const SolveParams<V>& p, uint32_t l
           const V val = ominus_cap<V>(V(0), rec_w(g, r[k]), g.cap);
           ++L.visits;
           ++L.apps;
-          L.edges += e[k] - b[k];  // one lift application relaxes the row
           if (val > V(0)) {
             stcg(p.stage + v, val);
             ++L.lifts;

@@ -159,6 +159,7 @@ struct egs_ctx {
   uint32_t tbits = 0;  // 0: int2 records; else packed u32 (egs_types.cuh)
   uint32_t* coff = nullptr;
   uint32_t* csrc = nullptr;
+  void* rec0 = nullptr;      // first record of each player-1 light row (by new id)
   uint32_t* perm = nullptr;  // old id -> new id
   uint32_t* inv = nullptr;   // new id -> old id
   // solver state
@@ -210,6 +211,7 @@ struct egs_ctx {
     g.tbits = tbits;
     g.coff = coff;
     g.csrc = csrc;
+    g.rec0 = rec0;
     g.cap = cap;
     return g;
   }
@@ -298,7 +300,7 @@ void ctx_free(egs_ctx* c) {
                   in_x ? nullptr : c->chg[1], c->frb[0], c->frb[1],
                   c->fr[0], c->fr[1], c->stage, c->scratch, c->ctr,
                   in_x ? nullptr : c->rbm[0], in_x ? nullptr : c->rbm[1], c->cbm[0], c->cbm[1],
-                  c->cand, c->ring, c->trace, c->longcol, c->f64};
+                  c->cand, c->ring, c->trace, c->longcol, c->f64, c->rec0};
   for (int q = 0; q < egs::kMaxRanks; ++q)
     if (c->xpeer_ipc[q] && c->xpeer[q]) cudaIpcCloseMemHandle(c->xpeer[q]);
   if (c->xbuf) {
@@ -523,7 +525,7 @@ bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint3
     if (!c->tbits) CK(cudaStreamWaitEvent(sw, et[k], 0));  // (wide: targets written apart)
     egs::k_sort_p1_rows<<<grid_for((uint64_t)(rows[k + 1] - rows[k]) * 32, c->num_sms), 256, 0,
                           sw>>>(rows[k], rows[k + 1], key, c->perm, c->off, c->edge, c->tbits,
-                                c->own_lo, c->own_hi);
+                                c->own_lo, c->own_hi, c->rec0);
     CK(cudaGetLastError());
   }
   for (auto& th : pool) th.join();
@@ -599,6 +601,7 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
   }
   // +16 bytes: 16-byte rounding of TMA spans
   c->edge = dalloc<uint8_t>(mo * rec_bytes(c) + 16);
+  c->rec0 = dalloc<uint8_t>((size_t)n * rec_bytes(c));
   c->csrc = dalloc<uint32_t>(mo);
   c->coff = dalloc<uint32_t>((size_t)n + 1);
   CK(cudaMemsetAsync(misc, 0, 64 * sizeof(unsigned int), s));
@@ -950,6 +953,7 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
       c->off = dalloc<uint32_t>(1);
       c->coff = dalloc<uint32_t>(1);
       c->edge = dalloc<uint8_t>(16);
+      c->rec0 = dalloc<uint8_t>(16);
       c->csrc = dalloc<uint32_t>(1);
       c->perm = dalloc<uint32_t>(1);
       c->inv = dalloc<uint32_t>(1);

@@ -68,6 +68,8 @@ struct Graph {
   uint32_t tbits;                // 0: int2 {dst, w}; else u32 dst | w << tbits
   const uint32_t* coff;          // n+1 CSC column offsets
   const uint32_t* csrc;          // m   predecessors (relabelled)
+  const void* rec0;              // n   a player-1 light row's first record (its
+                                 //     least weight: rows sorted at upload)
   int64_t cap;                   // credit_cap (M_G)
 };
 
