@@ -133,7 +133,12 @@ def dist_setup(n_gpus, backend):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         if backend == "nccl":
             import torch
-            torch.cuda.set_device(env_int("LOCAL_RANK", 0))
+            ndev = max(1, torch.cuda.device_count())
+            torch.cuda.set_device(env_int("LOCAL_RANK", 0) % ndev)
+            if ndev < env_int("LOCAL_WORLD_SIZE", world):
+                # ranks sharing a GPU (a functional run on a smaller box):
+                # NCCL refuses duplicate devices; the plumbing is gloo's
+                backend = "gloo"
         dist.init_process_group(backend=backend)
     return rank, world
 
@@ -149,6 +154,8 @@ def max_over_ranks(x, world, device=None):
         return x
     import torch
     import torch.distributed as dist
+    if dist.get_backend() != "nccl":
+        device = None  # (gloo reduces host tensors)
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -159,6 +166,8 @@ def sum_over_ranks(x, world, device=None):
         return x
     import torch
     import torch.distributed as dist
+    if dist.get_backend() != "nccl":
+        device = None  # (gloo reduces host tensors)
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())

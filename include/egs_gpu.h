@@ -230,12 +230,14 @@ int egs_part_plan_compute(const egs_arena_view* arena, int32_t world, egs_part_p
  * opts->n_gpus must equal world; opts->device selects the GPU. */
 int egs_part_create(const egs_arena_view* arena, const egs_gpu_opts* opts, int32_t rank,
                     int32_t world, egs_part** out, egs_part_plan* plan, egs_gpu_stats* stats);
-/* CUDA IPC handle (64 bytes) of this rank's replicated state, for peers in
- * other processes. */
-#define EGS_IPC_HANDLE_BYTES 64
+/* Export record (128 bytes) of this rank's replicated state, for peers in
+ * other processes: its CUDA IPC handle (64 bytes) and its GPU's UUID (16
+ * bytes; ranks of different processes on one GPU split its SMs), zero
+ * padded. */
+#define EGS_IPC_HANDLE_BYTES 128
 int egs_part_export(egs_part* part, void* handle);
-/* Map every peer's replicated state: handles[r * 64 ...] = rank r's export
- * (this rank's own entry is ignored). */
+/* Map every peer's replicated state: handles[r * EGS_IPC_HANDLE_BYTES ...]
+ * = rank r's export (this rank's own entry is ignored). */
 int egs_part_connect(egs_part* part, const void* handles);
 /* Ranks living in ONE process (several GPUs of a process, or several ranks
  * sharing one device for tests): connect them directly.  parts[r] = rank r. */
@@ -248,6 +250,10 @@ int egs_part_solve(egs_part* part, egs_gpu_stats* stats);
 /* The measure in the reference's raw encoding, original ids (identical on
  * every rank after a solve). */
 int egs_part_read_measure(egs_part* part, int64_t* f_out);
+/* An order-free 64-bit digest of this rank's replica of the measure
+ * (computed on the device): equal on every rank after a solve, so ranks
+ * check agreement by exchanging 8 bytes. */
+int egs_part_digest(egs_part* part, uint64_t* digest);
 void egs_part_destroy(egs_part* part);
 
 /* Output format: write_solution(make_solution(arena, report)) (io.cpp:178-210)

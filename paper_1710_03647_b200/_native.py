@@ -186,7 +186,7 @@ class PartPlan(C.Structure):
 
 
 _P = C.c_void_p
-IPC_HANDLE_BYTES = 64
+IPC_HANDLE_BYTES = 128  # include/egs_gpu.h EGS_IPC_HANDLE_BYTES
 lib.egs_part_plan_compute.argtypes = [C.POINTER(ArenaView), C.c_int32, C.POINTER(PartPlan)]
 lib.egs_part_plan_compute.restype = C.c_int
 lib.egs_part_create.argtypes = [C.POINTER(ArenaView), C.POINTER(GpuOpts), C.c_int32, C.c_int32,
@@ -202,6 +202,8 @@ lib.egs_part_solve.argtypes = [_P, C.POINTER(GpuStats)]
 lib.egs_part_solve.restype = C.c_int
 lib.egs_part_read_measure.argtypes = [_P, _P]
 lib.egs_part_read_measure.restype = C.c_int
+lib.egs_part_digest.argtypes = [_P, C.POINTER(C.c_uint64)]
+lib.egs_part_digest.restype = C.c_int
 lib.egs_part_destroy.argtypes = [_P]
 lib.egs_part_destroy.restype = None
 lib.egs_gpu_opts_default.argtypes = [C.POINTER(GpuOpts)]

@@ -528,6 +528,19 @@ __global__ void __launch_bounds__(256)
   if (bad) atomicAdd(sum + 2, bad);
 }
 
+// sum over v of edge_mix(v, f[v]) (wrapping): egs_part_digest
+template <class V>
+__global__ void k_digest(uint32_t n, const V* f, unsigned long long* out) {
+  unsigned long long h = 0;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const uint64_t x = (uint64_t)f[v];
+    h += edge_mix(v, (uint32_t)x) ^ edge_mix((uint32_t)(x >> 32), ~v);
+  }
+#pragma unroll
+  for (int sft = 16; sft > 0; sft >>= 1) h += __shfl_xor_sync(0xffffffffu, h, sft);
+  if (lane_id() == 0 && h) atomicAdd(out, h);
+}
+
 // ---------------------------------------------- solution output ----
 // write_solution(make_solution(...)) (io.cpp:178-210) on the device.  The
 // strategy of a finite player-0 vertex is the FIRST successor in row order

@@ -29,6 +29,7 @@
 #include <atomic>
 #include <mutex>
 #include <thread>
+#include <tuple>
 
 #include "egs_build.cuh"
 #include "egs_gpu.h"
@@ -289,6 +290,43 @@ bool shell_get(int device, Shell& sh) {
   return false;
 }
 
+// The replicated-state block of a finished partition context is kept per
+// device (one, the largest) for the next one: a repeated egs_part_create --
+// the multi-GPU one-shot path -- skips the cudaMalloc of an IPC-exportable
+// block and its first export.  Freed at process exit with the context.
+std::mutex g_xcache_mu;
+std::vector<std::tuple<int, char*, size_t>> g_xcache;  // (device, block, bytes)
+
+char* xbuf_take(int device, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_xcache_mu);
+  for (size_t i = 0; i < g_xcache.size(); ++i) {
+    auto [d, ptr, sz] = g_xcache[i];
+    if (d == device && sz >= bytes) {
+      g_xcache.erase(g_xcache.begin() + i);
+      return ptr;
+    }
+  }
+  void* xb = nullptr;
+  CK(cudaMalloc(&xb, bytes));
+  return static_cast<char*>(xb);
+}
+
+void xbuf_give(int device, char* ptr, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_xcache_mu);
+  for (auto& [d, p, sz] : g_xcache)
+    if (d == device) {
+      if (sz >= bytes) {
+        cudaFree(ptr);
+      } else {
+        cudaFree(p);
+        p = ptr;
+        sz = bytes;
+      }
+      return;
+    }
+  g_xcache.emplace_back(device, ptr, bytes);
+}
+
 void ctx_free(egs_ctx* c) {
   if (!c) return;
   StepTimer tm(c->stream);
@@ -305,7 +343,7 @@ void ctx_free(egs_ctx* c) {
     if (c->xpeer_ipc[q] && c->xpeer[q]) cudaIpcCloseMemHandle(c->xpeer[q]);
   if (c->xbuf) {
     if (c->stream) cudaStreamSynchronize(c->stream);
-    cudaFree(c->xbuf);
+    xbuf_give(c->device, c->xbuf, c->xbytes);
   }
   if (c->stream) {
     for (void* p : ptrs) dfree(p, c->stream);
@@ -914,9 +952,7 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
       auto up = [](size_t x) { return (x + 255) / 256 * 256; };
       const size_t fb = up(std::max<size_t>(n, 1) * vsz), wb = up(std::max<size_t>(words, 1) * 4);
       c->xbytes = fb + 4 * wb + up(sizeof(egs::XSync));
-      void* xb = nullptr;
-      CK(cudaMalloc(&xb, c->xbytes));
-      c->xbuf = static_cast<char*>(xb);
+      c->xbuf = xbuf_take(c->device, c->xbytes);
       CK(cudaMemsetAsync(c->xbuf, 0, c->xbytes, c->stream));
       c->f = c->xbuf;
       c->chg[0] = reinterpret_cast<uint32_t*>(c->xbuf + fb);
@@ -1440,43 +1476,54 @@ void plan_compute(const egs_arena_view* a, int world, egs_part_plan* pl) {
     const uint64_t deg = a->csr_offsets[v + 1] - a->csr_offsets[v];
     return (a->owners[v] ? 3 : 0) + (deg <= egs::kLightMax ? 0 : deg <= egs::kMediumMax ? 1 : 2);
   };
+  // Per-group class counts and edges, groups of kGroup consecutive vertices
+  // (threads take contiguous group ranges): a piece boundary is then found
+  // by walking the group sums and scanning one group.
+  constexpr uint32_t kGroup = 1u << 16;
+  const uint32_t G = (n + kGroup - 1) / kGroup;
   const unsigned T = n > (1u << 20) ? std::max(1u, std::min(16u, std::thread::hardware_concurrency())) : 1u;
-  std::vector<uint64_t> cnt((size_t)T * C, 0), edg((size_t)T * C, 0);
-  auto chunk = [&](unsigned t) { return std::make_pair((uint64_t)n * t / T, (uint64_t)n * (t + 1) / T); };
-  {
+  std::vector<uint64_t> cnt((size_t)G * C, 0), edg((size_t)G * C, 0);
+  auto group = [&](uint32_t gi) {
+    return std::make_pair((uint64_t)gi * kGroup, std::min<uint64_t>(n, (uint64_t)(gi + 1) * kGroup));
+  };
+  auto run_groups = [&](auto&& fn) {  // fn(group) over all groups, T threads
     std::vector<std::thread> pool;
     for (unsigned t = 0; t < T; ++t)
       pool.emplace_back([&, t] {
-        const auto [lo, hi] = chunk(t);
-        for (uint64_t v = lo; v < hi; ++v) {
-          const int k = cls((uint32_t)v);
-          cnt[t * C + k] += 1;
-          edg[t * C + k] += a->csr_offsets[v + 1] - a->csr_offsets[v];
-        }
+        for (uint32_t gi = (uint32_t)((uint64_t)G * t / T); gi < (uint64_t)G * (t + 1) / T; ++gi) fn(gi);
       });
     for (auto& th : pool) th.join();
-  }
+  };
+  run_groups([&](uint32_t gi) {
+    const auto [lo, hi] = group(gi);
+    for (uint64_t v = lo; v < hi; ++v) {
+      const int k = cls((uint32_t)v);
+      cnt[(size_t)gi * C + k] += 1;
+      edg[(size_t)gi * C + k] += a->csr_offsets[v + 1] - a->csr_offsets[v];
+    }
+  });
   uint64_t ctot[C] = {}, etot[C] = {};
-  for (unsigned t = 0; t < T; ++t)
-    for (int k = 0; k < C; ++k) ctot[k] += cnt[t * C + k], etot[k] += edg[t * C + k];
+  for (uint32_t gi = 0; gi < G; ++gi)
+    for (int k = 0; k < C; ++k) ctot[k] += cnt[(size_t)gi * C + k], etot[k] += edg[(size_t)gi * C + k];
   for (int k = 0; k < C; ++k) {
     pl->piece[k][0] = 0;
     pl->piece[k][world] = (uint32_t)ctot[k];
     for (int r = 1; r < world; ++r) {
-      const uint64_t target = (etot[k] * (uint64_t)r + world - 1) / world;  // ceil
-      // the chunk the boundary falls in: cumulative edges before it < target
+      // edge_balanced_bounds (solver_par.cpp:62-80) per class: the first
+      // class member with at least ceil(E_k * r / world) class edges before it
+      const uint64_t target = (etot[k] * (uint64_t)r + world - 1) / world;
       uint64_t pos = 0, cum = 0;
-      unsigned t = 0;
-      for (; t < T; ++t) {
-        if (cum + edg[t * C + k] >= target) break;
-        cum += edg[t * C + k];
-        pos += cnt[t * C + k];
+      uint32_t gi = 0;
+      for (; gi < G; ++gi) {
+        if (cum + edg[(size_t)gi * C + k] >= target) break;
+        cum += edg[(size_t)gi * C + k];
+        pos += cnt[(size_t)gi * C + k];
       }
-      if (t == T) {
+      if (gi == G) {
         pl->piece[k][r] = (uint32_t)ctot[k];
         continue;
       }
-      const auto [lo, hi] = chunk(t);
+      const auto [lo, hi] = group(gi);
       for (uint64_t v = lo; v < hi && cum < target; ++v)
         if (cls((uint32_t)v) == k) {
           cum += a->csr_offsets[v + 1] - a->csr_offsets[v];
@@ -1488,42 +1535,48 @@ void plan_compute(const egs_arena_view* a, int world, egs_part_plan* pl) {
   uint32_t id = 0;
   for (int r = 0; r < world; ++r) {
     pl->rank_lo[r] = id;
-    uint64_t e = 0;
     for (int k = 0; k < C; ++k) {
       pl->class_lo[r][k] = id;
       id += pl->piece[k][r + 1] - pl->piece[k][r];
     }
     pl->class_lo[r][C] = id;
-    (void)e;
   }
   pl->rank_lo[world] = id;
-  // edges per rank: the class pieces' edges (a third pass only over the
-  // piece boundaries' chunks would do; the whole pass is cheap next to the
-  // upload it precedes)
-  {
-    std::vector<uint64_t> er((size_t)T * world, 0);
-    std::vector<std::thread> pool;
-    // class positions at each chunk start
-    std::vector<uint64_t> cpos((size_t)T * C, 0);
-    for (unsigned t = 1; t < T; ++t)
-      for (int k = 0; k < C; ++k) cpos[t * C + k] = cpos[(t - 1) * C + k] + cnt[(t - 1) * C + k];
-    for (unsigned t = 0; t < T; ++t)
-      pool.emplace_back([&, t] {
-        const auto [lo, hi] = chunk(t);
-        uint64_t p[C];
-        for (int k = 0; k < C; ++k) p[k] = cpos[t * C + k];
-        for (uint64_t v = lo; v < hi; ++v) {
-          const int k = cls((uint32_t)v);
-          int r = 0;
-          while (r + 1 < world && p[k] >= pl->piece[k][r + 1]) ++r;
-          er[(size_t)t * world + r] += a->csr_offsets[v + 1] - a->csr_offsets[v];
-          ++p[k];
-        }
-      });
-    for (auto& th : pool) th.join();
-    for (unsigned t = 0; t < T; ++t)
-      for (int r = 0; r < world; ++r) pl->edges[r] += er[(size_t)t * world + r];
-  }
+  // edges per rank: a group wholly inside one rank's piece of every class
+  // adds its sums; a group a boundary falls in is scanned
+  std::vector<uint64_t> cpos((size_t)G * C, 0);  // class positions at each group start
+  for (uint32_t gi = 1; gi < G; ++gi)
+    for (int k = 0; k < C; ++k)
+      cpos[(size_t)gi * C + k] = cpos[(size_t)(gi - 1) * C + k] + cnt[(size_t)(gi - 1) * C + k];
+  std::vector<uint64_t> er((size_t)G * world, 0);
+  auto rank_of = [&](int k, uint64_t p) {
+    int r = 0;
+    while (r + 1 < world && p >= pl->piece[k][r + 1]) ++r;
+    return r;
+  };
+  run_groups([&](uint32_t gi) {
+    bool whole = true;
+    for (int k = 0; k < C && whole; ++k) {
+      const uint64_t p0 = cpos[(size_t)gi * C + k], c = cnt[(size_t)gi * C + k];
+      if (c) whole = rank_of(k, p0) == rank_of(k, p0 + c - 1);
+    }
+    if (whole) {
+      for (int k = 0; k < C; ++k)
+        if (cnt[(size_t)gi * C + k])
+          er[(size_t)gi * world + rank_of(k, cpos[(size_t)gi * C + k])] += edg[(size_t)gi * C + k];
+      return;
+    }
+    uint64_t p[C];
+    for (int k = 0; k < C; ++k) p[k] = cpos[(size_t)gi * C + k];
+    const auto [lo, hi] = group(gi);
+    for (uint64_t v = lo; v < hi; ++v) {
+      const int k = cls((uint32_t)v);
+      er[(size_t)gi * world + rank_of(k, p[k])] += a->csr_offsets[v + 1] - a->csr_offsets[v];
+      ++p[k];
+    }
+  });
+  for (uint32_t gi = 0; gi < G; ++gi)
+    for (int r = 0; r < world; ++r) pl->edges[r] += er[(size_t)gi * world + r];
 }
 
 // The original-id row ranges of rank `rank` (vertices whose class piece is
@@ -1604,6 +1657,12 @@ std::vector<std::pair<uint32_t, uint32_t>> rank_runs(const egs_arena_view* a,
   return runs;
 }
 
+cudaUUID_t device_uuid(int device) {
+  cudaDeviceProp prop{};
+  CK(cudaGetDeviceProperties(&prop, device));
+  return prop.uuid;
+}
+
 // Grid of a rank's persistent kernel: ranks sharing a device split it.
 void part_grid(egs_ctx* c, int ranks_on_device) {
   if (ranks_on_device <= 1) return;
@@ -1655,10 +1714,14 @@ int egs_part_export(egs_part* part, void* handle) {
     egs_ctx* c = part->c;
     if (!c->xbuf) throw Fail(EGS_ERR_INVALID_CONFIG, "a one-rank partition has nothing to export");
     CK(cudaSetDevice(c->device));
-    static_assert(sizeof(cudaIpcMemHandle_t) == EGS_IPC_HANDLE_BYTES, "IPC handle size");
+    static_assert(sizeof(cudaIpcMemHandle_t) + 16 <= EGS_IPC_HANDLE_BYTES, "export record size");
     cudaIpcMemHandle_t h;
     CK(cudaIpcGetMemHandle(&h, c->xbuf));
-    std::memcpy(handle, &h, sizeof(h));
+    char rec[EGS_IPC_HANDLE_BYTES] = {};
+    std::memcpy(rec, &h, sizeof(h));
+    const cudaUUID_t u = device_uuid(c->device);
+    std::memcpy(rec + sizeof(h), &u, 16);
+    std::memcpy(handle, rec, sizeof(rec));
   });
 }
 
@@ -1667,16 +1730,20 @@ int egs_part_connect(egs_part* part, const void* handles) {
     if (!part || !handles) throw Fail(EGS_ERR_INVALID_CONFIG, "null argument");
     egs_ctx* c = part->c;
     CK(cudaSetDevice(c->device));
+    const cudaUUID_t mine = device_uuid(c->device);
+    int same = 1;  // ranks on this GPU (their persistent grids must be co-resident)
     for (int q = 0; q < c->world; ++q) {
       if (q == c->rank) continue;
+      const char* rec = static_cast<const char*>(handles) + (size_t)q * EGS_IPC_HANDLE_BYTES;
       cudaIpcMemHandle_t h;
-      std::memcpy(&h, static_cast<const char*>(handles) + (size_t)q * EGS_IPC_HANDLE_BYTES,
-                  sizeof(h));
+      std::memcpy(&h, rec, sizeof(h));
+      if (std::memcmp(rec + sizeof(h), &mine, 16) == 0) ++same;
       void* ptr = nullptr;
       CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
       c->xpeer[q] = static_cast<char*>(ptr);
       c->xpeer_ipc[q] = true;
     }
+    part_grid(c, same);
     c->connected = true;
   });
 }
@@ -1727,6 +1794,30 @@ int egs_part_read_measure(egs_part* part, int64_t* f_out) {
   return guarded([&] {
     if (!part) throw Fail(EGS_ERR_INVALID_CONFIG, "null partition");
     ctx_read(part->c, f_out);
+  });
+}
+
+int egs_part_digest(egs_part* part, uint64_t* digest) {
+  return guarded([&] {
+    if (!part || !digest) throw Fail(EGS_ERR_INVALID_CONFIG, "null argument");
+    egs_ctx* c = part->c;
+    if (!c->solved) throw Fail(EGS_ERR_INVALID_CONFIG, "partition not solved");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    g_alloc_stream = s;
+    DevBuf d_out;
+    unsigned long long* out = d_out.alloc<unsigned long long>(1);
+    CK(cudaMemsetAsync(out, 0, sizeof(unsigned long long), s));
+    const uint32_t grid = grid_for(c->n, c->num_sms);
+    if (c->vbits == 32)
+      egs::k_digest<uint32_t><<<grid, 256, 0, s>>>(c->n, static_cast<const uint32_t*>(c->f), out);
+    else
+      egs::k_digest<uint64_t><<<grid, 256, 0, s>>>(c->n, static_cast<const uint64_t*>(c->f), out);
+    CK(cudaGetLastError());
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, out, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *digest = h;
   });
 }
 

@@ -17,8 +17,9 @@ The reference has no distributed path (its ``workers`` are threads,
   them take the same schedule decision.  The host launches once per rank and
   waits once: no per-round host round trip, no host-staged collective.
 * **Plumbing**: ``torch.distributed`` (NCCL or gloo) only exchanges the
-  64-byte IPC handles before the solve and checks afterwards that every rank
-  holds the same measure (an all-gather of a digest).
+  128-byte export records (CUDA IPC handle + GPU UUID) before the solve and
+  checks afterwards that every rank holds the same measure (an all-gather of
+  a 64-bit digest computed on the device, egs_part_digest).
 
 ``solve_distributed`` is the one-process-per-GPU entry (torchrun);
 ``solve_local`` runs several ranks in ONE process (several GPUs, or several
@@ -28,7 +29,6 @@ single-GPU box).  Both give the single-GPU solver's measure byte for byte.
 from __future__ import annotations
 
 import ctypes as C
-import hashlib
 import threading
 import time
 from dataclasses import dataclass, field
@@ -89,6 +89,12 @@ class Partition:
         N._check(N.lib.egs_part_solve(self._part, C.byref(st)))
         return st
 
+    def digest(self) -> int:
+        """egs_part_digest: order-free 64-bit digest of this rank's replica."""
+        d = C.c_uint64()
+        N._check(N.lib.egs_part_digest(self._part, C.byref(d)))
+        return int(d.value)
+
     def read_measure(self) -> np.ndarray:
         out = np.empty(self.arena.num_vertices, dtype=np.int64)
         N._check(N.lib.egs_part_read_measure(self._part, out.ctypes.data))
@@ -117,10 +123,6 @@ class PartitionReport:
     h2d_bytes: int = 0                  # this rank's upload (own rows + vertex arrays)
     plan: dict = field(default_factory=dict)
     stats: dict = field(default_factory=dict)
-
-
-def _digest(f: np.ndarray) -> bytes:
-    return hashlib.sha256(np.ascontiguousarray(f).tobytes()).digest()
 
 
 class TorchComm:
@@ -156,10 +158,10 @@ def solve_distributed(arena: N.GameArena, options: Optional[N.SolverOptions] = N
             part.connect(comm.allgather_bytes(part.export()))
         comm.barrier()
     st = part.solve()
-    f = part.read_measure()
-    digests = comm.allgather_bytes(_digest(f))
+    digests = comm.allgather_bytes(part.digest().to_bytes(8, "little"))
     if any(d != digests[0] for d in digests):
         raise N.InternalInvariantError("ranks disagree on the measure")
+    f = part.read_measure()
     return PartitionReport(
         measure=f, rounds=int(st.rounds), wall_seconds=time.perf_counter() - t0,
         solve_seconds=float(st.solve_seconds), edges_relaxed=int(st.edges_relaxed),

@@ -98,7 +98,7 @@ class FakePartition:
         self.h2d_bytes = 0
 
     def export(self):
-        return hashlib.sha256(f"rank{self.rank}".encode()).digest() * 2  # 64 bytes
+        return hashlib.sha256(f"rank{self.rank}".encode()).digest() * 4  # 128 bytes
 
     def connect(self, handles):
         self.connected = list(handles)
@@ -111,6 +111,9 @@ class FakePartition:
 
     def read_measure(self):
         return self._measure
+
+    def digest(self):
+        return int.from_bytes(hashlib.sha256(self._measure.tobytes()).digest()[:8], "little")
 
 
 def _worker(rank, world, port, q, corrupt):
@@ -140,7 +143,7 @@ def _worker(rank, world, port, q, corrupt):
         except egs.InternalInvariantError as e:
             ok, err = False, str(e)
         p = parts[0]
-        expect = [hashlib.sha256(f"rank{r}".encode()).digest() * 2 for r in range(world)]
+        expect = [hashlib.sha256(f"rank{r}".encode()).digest() * 4 for r in range(world)]
         q.put((rank, ok, err, p.connected == expect, p.plan))
     finally:
         dist.destroy_process_group()
@@ -210,6 +213,7 @@ def test_local_ranks_golden_and_repeated_solves(egs, golden):
         from paper_1710_03647_b200.distributed import solve_local
         reps, parts = solve_local(a, 2, parts=parts)
         assert np.array_equal(reps[0].measure, reps[1].measure)
+        assert parts[0].digest() == parts[1].digest()
     # balanced work: per-rank owned edges and edges relaxed within 1.2x
     owned = [r.edges_owned for r in reps]
     assert max(owned) <= 1.2 * sum(owned) / 2
@@ -256,3 +260,48 @@ def test_c4_two_ranks_byte_identical(egs, golden):
     rec = golden.get("fixed/16000000/16/100/1", {})
     if "solution_sha256" in rec:
         assert hashlib.sha256(text).hexdigest() == rec["solution_sha256"]
+
+
+def _ipc_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1710_03647_b200 as egs
+        from paper_1710_03647_b200.distributed import solve_distributed
+        res = []
+        for a in (egs.GameArena.fixed(100000, 16, 100, 1), egs.GameArena.rmat(14, 16, 100, 1)):
+            want = egs.solve(a, options=egs.SolverOptions(device=0)).measure
+            opts = egs.SolverOptions(device=0, timeout_seconds=30.0)
+            rep = solve_distributed(a, opts)
+            res.append((bool(np.array_equal(rep.measure, want)), rep.rounds))
+        q.put((rank, res, None))
+    except Exception as e:  # noqa: BLE001 -- reported to the parent
+        q.put((rank, None, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_processes_one_gpu_over_ipc():
+    """The one-process-per-rank path (solve_distributed, as torchrun runs it):
+    two processes on one B200 exchange CUDA IPC handles over gloo, map each
+    other's replicated state (cudaIpcOpenMemHandle), split the GPU's SMs
+    (their export records carry the same device UUID) and solve together --
+    the measure equals the single-GPU solve's."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict((x[0], x[1:]) for x in (q.get(timeout=600) for _ in range(world)))
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        out, err = res[r]
+        assert err is None, err
+        for ok, rounds in out:
+            assert ok
+        assert [x[1] for x in out] == [x[1] for x in res[0][0]], "ranks took different schedules"
