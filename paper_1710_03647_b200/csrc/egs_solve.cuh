@@ -1487,6 +1487,151 @@ __device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo0,
   block_flush(L, sum_dst);
 }
 
+// Player-0 light rows of round 1 with packed records, two bitmap words (64
+// rows, two per lane) per TMA copy.  The tile pipeline moves one word per
+// copy -- 2 KB for C4's 16-edge rows, half a stage -- with one copy ahead per
+// warp, which holds round 1's pure stream to ~2.7 TB/s; a pair fills the
+// 4 KB stage and doubles the bytes in flight.  Same result as round1_light's
+// packed witness key.  A pair whose span exceeds a stage reads its rows
+// directly.  Needs kStages == 2 (the caller checks).
+template <class V>
+__device__ __noinline__ void round1_p0_pairs(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
+                                             unsigned int* cursor, uint32_t* chg,
+                                             unsigned int* sum_dst) {
+  extern __shared__ __align__(128) ERec dsm[];
+  const Graph& g = p.g;
+  Local L;
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  ERec* stage_base = dsm + (size_t)warp * kStages * kStageRecs;
+  uint64_t* s_bar = g_tma_bar[warp];
+  const uint32_t w_lo = lo >> 5, w_hi = hi > lo ? (hi + 31) >> 5 : w_lo;
+  const uint32_t U = (w_hi - w_lo + 1) / 2;  // pairs of words
+  const uint32_t b1 = g.rb[kP1L];
+  uint32_t c_next = 0, c_end = 0;
+  auto claim = [&]() -> uint32_t {
+    if (c_next >= c_end) {
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(cursor, kTileClaim);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      c_next = base;
+      c_end = base + kTileClaim < U ? base + kTileClaim : U;
+      if (base >= U) return 0xFFFFFFFFu;
+    }
+    return c_next++;
+  };
+  struct Pair {
+    uint32_t w, b[2], e[2], base;
+    bool valid, in[2], staged;
+  };
+  auto fetch = [&](Pair& t) {
+    const uint32_t i = claim();
+    t.valid = i < U;
+    t.in[0] = t.in[1] = false;
+    t.b[0] = t.e[0] = t.b[1] = t.e[1] = 0;
+    if (!t.valid) return;
+    t.w = w_lo + 2 * i;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t v = ((t.w + h) << 5) + lane;
+      t.in[h] = v >= lo && v < hi;
+      if (t.in[h]) {
+        t.b[h] = __ldg(g.off + v);
+        t.e[h] = __ldg(g.off + v + 1);
+      }
+    }
+  };
+  auto prepare = [&](uint32_t s, Pair& t) {
+    const uint32_t v0 = t.w << 5;
+    const uint32_t first = max(v0, lo), last = min(v0 + 64, hi) - 1;
+    const uint32_t span_lo = __shfl_sync(0xffffffffu, t.b[0], first - v0);
+    const uint32_t hi0 = __shfl_sync(0xffffffffu, t.e[0], (last - v0) & 31u);
+    const uint32_t hi1 = __shfl_sync(0xffffffffu, t.e[1], (last - v0) & 31u);
+    const uint32_t span_hi = last >= v0 + 32 ? hi1 : hi0;
+    const uint32_t a_lo = span_lo & ~(kRecAlign - 1u);
+    const uint32_t a_hi = (span_hi + kRecAlign - 1u) & ~(kRecAlign - 1u);
+    t.base = a_lo;
+    t.staged = a_hi - a_lo <= kStageRecs;
+    if (t.staged && lane == 0) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&s_bar[s], (a_hi - a_lo) * (uint32_t)sizeof(ERec));
+      bulk_g2s(stage_base + s * kStageRecs, erecs(g) + a_lo,
+               (a_hi - a_lo) * (uint32_t)sizeof(ERec), &s_bar[s]);
+    }
+  };
+  // packed witness key (round1_light): one min per edge
+  auto row = [&](uint32_t v, const ERec* rec, uint32_t len) {
+    const uint32_t rot = row_rot(len);
+    uint32_t kb = 0xFFFFFFFFu;
+    row_edges(len, rot, [&](uint32_t j) {
+      const int2 r = dec(g, rec[j]);
+      kb = min(kb, ((uint32_t)max(0, -r.y) << 6) | ((uint32_t)((uint32_t)r.x >= b1) << 5) | j);
+    });
+    const V val = ominus_cap<V>(V(0), -(int)(kb >> 6), g.cap);
+    stcg(wit_of(p) + v, rec[kb & 31u]);
+    ++L.visits;
+    ++L.apps;
+    L.edges += len;
+    if (val > V(0)) {
+      stcg(p.stage + v, val);
+      ++L.lifts;
+      return true;
+    }
+    return false;
+  };
+  auto direct = [&](uint32_t v, uint32_t b, uint32_t e) {  // the same key from global
+    uint32_t kb = 0xFFFFFFFFu;
+    for (uint32_t i = b; i < e; ++i) {
+      const int2 r = ld_rec(g, i);
+      kb = min(kb, ((uint32_t)max(0, -r.y) << 6) | ((uint32_t)((uint32_t)r.x >= b1) << 5) | (i - b));
+    }
+    const V val = ominus_cap<V>(V(0), -(int)(kb >> 6), g.cap);
+    stcg(wit_of(p) + v, __ldg(erecs(g) + b + (kb & 31u)));
+    ++L.visits;
+    ++L.apps;
+    L.edges += e - b;
+    if (val > V(0)) {
+      stcg(p.stage + v, val);
+      ++L.lifts;
+      return true;
+    }
+    return false;
+  };
+  auto compute = [&](uint32_t s, const Pair& t, uint32_t& parity) {
+    if (t.staged) {
+      mbar_wait(&s_bar[s], (parity >> s) & 1u);
+      parity ^= 1u << s;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t v = ((t.w + h) << 5) + lane;
+      bool ch = false;
+      if (t.in[h])
+        ch = t.staged ? row(v, stage_base + s * kStageRecs + (t.b[h] - t.base), t.e[h] - t.b[h])
+                      : direct(v, t.b[h], t.e[h]);
+      const uint32_t m = __ballot_sync(0xffffffffu, ch);
+      if (m && lane == 0) bits_or(p, chg + t.w + h, m);
+      L.phase_count += ch;
+    }
+  };
+  uint32_t parity = g_tma_parity[warp];
+  Pair t0, t1;
+  fetch(t0);
+  if (t0.valid) prepare(0, t0);
+  uint32_t s = 0;
+  while (t0.valid) {
+    __syncwarp();  // slot s ^ 1 was last read by this warp's previous pair
+    fetch(t1);
+    if (t1.valid) prepare(s ^ 1u, t1);
+    compute(s, t0, parity);
+    t0 = t1;
+    s ^= 1u;
+  }
+  __syncwarp();
+  if (lane == 0) g_tma_parity[warp] = parity;
+  __syncwarp();
+  block_flush(L, sum_dst);
+}
+
 // medium rows: one warp per row; heavy rows: one CTA per row (dynamic claims)
 template <class V>
 __device__ __noinline__ void round1_long(const SolveParams<V>& p, uint32_t* chg,
@@ -1612,6 +1757,10 @@ __device__ __noinline__ void round1_long(const SolveParams<V>& p, uint32_t* chg,
 // takes kR1Words bitmap words (32 vertices each) per step and issues all
 // their loads before using any.
 constexpr int kR1Words = 4;
+#ifndef EGS_R1_PAIRS
+#define EGS_R1_PAIRS 1
+#endif
+constexpr bool kR1Pairs = EGS_R1_PAIRS != 0;  // round1_p0_pairs
 template <class V>
 __device__ __noinline__ void round1_p1_light(const SolveParams<V>& p, uint32_t lo, uint32_t hi,
                                              uint32_t* chg, unsigned int* sum_dst) {
@@ -1666,8 +1815,13 @@ __device__ __noinline__ void phase_round1(const SolveParams<V>& p, uint32_t* chg
   round1_long<V>(p, chg, slot_sum + 0, slot_dyn);
   // player-0 light rows stream through the tile pipeline (their witness
   // needs the whole row); player-1 light rows read their first record
-  round1_light<V>(p, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]), 0u, 0u,
-                  slot_dyn + kTileCursor, chg, slot_sum + 0);
+  if (kR1Pairs && kStages == 2 && kPackedWitnessKey && g.tbits >= 5 &&
+      (p.use_tma & kTmaRound1) != 0)
+    round1_p0_pairs<V>(p, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]),
+                       slot_dyn + kTileCursor, chg, slot_sum + 0);
+  else
+    round1_light<V>(p, clip_lo(p, g.rb[kP0L]), clip_hi(p, g.rb[kP0M]), 0u, 0u,
+                    slot_dyn + kTileCursor, chg, slot_sum + 0);
   round1_p1_light<V>(p, clip_lo(p, g.rb[kP1L]), clip_hi(p, g.rb[kP1M]), chg, slot_sum + 0);
 }
 
