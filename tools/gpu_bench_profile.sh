@@ -13,5 +13,10 @@ EGS_TRACE=1 timeout 300 python tools/ncu_target.py C4 1 > $OUT/trace_c4.txt 2>&1
 EGS_TRACE=1 timeout 300 python tools/ncu_target.py C3 1 > $OUT/trace_c3.txt 2>&1
 timeout 1200 python tools/config_table.py --out $OUT/configs.jsonl > $OUT/configs.out 2>&1; echo "configs rc=$?"
 timeout 600 python tools/part_local_bench.py C4 2 > $OUT/part_local_c4.json 2> $OUT/part_local_c4.err; echo "part-local rc=$?"
+timeout 300 python tools/e2e_breakdown.py C4 > $OUT/e2e_breakdown.txt 2>&1; echo "e2e rc=$?"
+# two processes on the one GPU over CUDA IPC (functional: contexts of two
+# processes time-slice the GPU, so the time is not a scaling number)
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29555 bench.py --gpus 2 --steps 3 --warmup 3 > $OUT/bench_2proc_1gpu.json 2> $OUT/bench_2proc_1gpu.err; echo "2proc rc=$?"
+timeout 900 python -m pytest tests -m gpu -q > $OUT/gpu_tests.txt 2>&1; echo "gpu tests rc=$?"
 cat $OUT/bench.json
 
