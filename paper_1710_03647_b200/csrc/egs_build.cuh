@@ -37,10 +37,93 @@ __global__ void k_row_lengths(uint32_t n, const uint32_t* inv, const uint64_t* o
   if (blockIdx.x == 0 && threadIdx.x == 0) deg_new[n] = 0;
 }
 
-// Rows longer than kRelabelLong (the R-MAT hubs, up to 1.6e5 edges) are not
-// expanded by one warp: the row-wise kernels queue them, and the *_long
-// kernels spread each queued row's edges over the whole grid.
-constexpr uint32_t kRelabelLong = 2048;
+// Rows longer than kRelabelLong are not expanded by the warp that owns them
+// with 31 other rows (a warp of 32 R-MAT rows of up to 2048 edges each held
+// up a whole chunk: C3's relabel took 16 ms for 69 M edges, 20x C4's rate
+// per edge).  The row-wise kernels queue them, k_long_prefix scans the
+// queued rows' lengths, and the *_long kernels walk all their edges as one
+// flat stream over the grid: a warp takes kRelabelLong consecutive edges --
+// one binary search of the prefix, then at most one row boundary, as every
+// queued row is longer than that.
+constexpr uint32_t kRelabelLong = 256;
+
+// pref[i] = edges of the queued rows before row i, pref[cnt] = all (one CTA)
+__global__ void __launch_bounds__(1024)
+    k_long_prefix(const uint32_t* list, const unsigned int* cnt_p, const uint64_t* off64,
+                  uint64_t* pref) {
+  __shared__ uint64_t s_warp[32];
+  __shared__ uint64_t s_carry;
+  const uint32_t cnt = *cnt_p, lane = lane_id(), warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < cnt; base += blockDim.x) {
+    const uint32_t i = base + threadIdx.x;
+    uint64_t x = 0;
+    if (i < cnt) {
+      const uint32_t o = list[i];
+      x = off64[o + 1] - off64[o];
+    }
+    uint64_t inc = x;  // inclusive warp scan
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= (uint32_t)d) inc += y;
+    }
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      uint64_t w = lane < (blockDim.x >> 5) ? s_warp[lane] : 0;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, w, d);
+        if (lane >= (uint32_t)d) w += y;
+      }
+      s_warp[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    const uint64_t before = s_carry + (warp ? s_warp[warp - 1] : 0) + inc - x;
+    if (i < cnt) pref[i] = before;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) s_carry = before + x;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) pref[cnt] = s_carry;
+}
+
+// body(o, idx) for every edge idx of every queued row o, flat over the grid
+template <class Body>
+__device__ __forceinline__ void long_rows_flat(const uint32_t* list, const unsigned int* cnt_p,
+                                               const uint64_t* off64, const uint64_t* pref,
+                                               Body&& body) {
+  const uint32_t cnt = *cnt_p;
+  if (cnt == 0) return;
+  const uint64_t total = pref[cnt];
+  const uint32_t lane = lane_id();
+  const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t g0 = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * kRelabelLong;
+       g0 < total; g0 += nwarps * kRelabelLong) {
+    uint32_t lo = 0, hi = cnt - 1;  // the row holding g0: last r with pref[r] <= g0
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      if (pref[mid] <= g0) lo = mid; else hi = mid - 1;
+    }
+    uint32_t r = lo;
+    uint64_t r_end = pref[r + 1];
+    uint32_t o = list[r];
+    uint64_t b = off64[o];
+    for (uint32_t s = 0; s < kRelabelLong / 32; ++s) {
+      const uint64_t g = g0 + (uint64_t)s * 32 + lane;
+      if (g >= total) break;
+      if (g >= r_end) {  // (the next row: queued rows are longer than kRelabelLong)
+        ++r;
+        r_end = pref[r + 1];
+        o = list[r];
+        b = off64[o];
+      }
+      body(o, (uint32_t)(b + (g - pref[r])));
+    }
+  }
+}
 
 // Edge relabelling, pipelined with the chunked upload (egs_solver.cu
 // build_arena): old rows [r0, r1) whose targets have arrived are copied to
@@ -138,56 +221,45 @@ __global__ void __launch_bounds__(256)
 
 __global__ void __launch_bounds__(256)
     k_relabel_targets_long(uint32_t n, const uint32_t* longlist, const unsigned int* longcnt,
-                           const uint64_t* off64, const uint32_t* dst, const uint32_t* perm,
-                           const uint32_t* off_new, void* edge, uint32_t tbits, uint32_t* ckey,
-                           uint32_t* cval, unsigned int* bad, bool key_at_orig) {
+                           const uint64_t* pref, const uint64_t* off64, const uint32_t* dst,
+                           const uint32_t* perm, const uint32_t* off_new, void* edge,
+                           uint32_t tbits, uint32_t* ckey, uint32_t* cval, unsigned int* bad,
+                           bool key_at_orig) {
   int* ex = static_cast<int*>(edge);
   uint32_t* px = static_cast<uint32_t*>(edge);
   unsigned int flag = 0;
-  const uint32_t cnt = *longcnt;
-  for (uint32_t k = 0; k < cnt; ++k) {
-    const uint32_t o = longlist[k];
-    const uint32_t b = (uint32_t)off64[o], e = (uint32_t)off64[o + 1];
+  long_rows_flat(longlist, longcnt, off64, pref, [&](uint32_t o, uint32_t idx) {
     const uint32_t rn = perm[o];
-    const uint32_t d = off_new[rn] - b;
-    for (uint32_t idx = b + blockIdx.x * blockDim.x + threadIdx.x; idx < e;
-         idx += gridDim.x * blockDim.x) {
-      const uint32_t pos = idx + d;
-      const uint32_t t0 = dst[idx];
-      if (t0 >= n) flag |= 2u;
-      const uint32_t t = perm[t0 < n ? t0 : 0];
-      if (tbits)
-        px[pos] = t;
-      else
-        ex[2 * (size_t)pos] = (int)t;
-      const uint32_t kp = key_at_orig ? idx : pos;
-      ckey[kp] = t;
-      cval[kp] = rn;
-    }
-  }
+    const uint32_t pos = idx + (off_new[rn] - (uint32_t)off64[o]);
+    const uint32_t t0 = dst[idx];
+    if (t0 >= n) flag |= 2u;
+    const uint32_t t = perm[t0 < n ? t0 : 0];
+    if (tbits)
+      px[pos] = t;
+    else
+      ex[2 * (size_t)pos] = (int)t;
+    const uint32_t kp = key_at_orig ? idx : pos;
+    ckey[kp] = t;
+    cval[kp] = rn;
+  });
   if (flag) atomicOr(bad, flag);
 }
 
 template <class W>
 __global__ void __launch_bounds__(256)
     k_relabel_weights_long(const uint32_t* longlist, const unsigned int* longcnt,
-                           const uint64_t* off64, const W* wn, const uint32_t* perm,
-                           const uint32_t* off_new, void* edge, uint32_t tbits) {
+                           const uint64_t* pref, const uint64_t* off64, const W* wn,
+                           const uint32_t* perm, const uint32_t* off_new, void* edge,
+                           uint32_t tbits) {
   int* ex = static_cast<int*>(edge);
   uint32_t* px = static_cast<uint32_t*>(edge);
-  const uint32_t cnt = *longcnt;
-  for (uint32_t k = 0; k < cnt; ++k) {
-    const uint32_t o = longlist[k];
-    const uint32_t b = (uint32_t)off64[o], e = (uint32_t)off64[o + 1];
-    const uint32_t d = off_new[perm[o]] - b;
-    for (uint32_t idx = b + blockIdx.x * blockDim.x + threadIdx.x; idx < e;
-         idx += gridDim.x * blockDim.x) {
-      if (tbits)
-        px[idx + d] |= (uint32_t)(int)wn[idx] << tbits;
-      else
-        ex[2 * (size_t)(idx + d) + 1] = (int)wn[idx];
-    }
-  }
+  long_rows_flat(longlist, longcnt, off64, pref, [&](uint32_t o, uint32_t idx) {
+    const uint32_t d = off_new[perm[o]] - (uint32_t)off64[o];
+    if (tbits)
+      px[idx + d] |= (uint32_t)(int)wn[idx] << tbits;
+    else
+      ex[2 * (size_t)(idx + d) + 1] = (int)wn[idx];
+  });
 }
 
 // Player-1 light rows (<= 32 edges) sorted by weight, ascending (ties by

@@ -453,11 +453,13 @@ void dev_radix_sort_pairs(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1
 // as it is converted, while the targets are still on the wire and the
 // transpose sorts.  C4 (|w| <= 100) sends 1 byte per weight instead of 8.
 // Queued long rows of the relabel kernels (egs_build.cuh kRelabelLong): one
-// list region of `cap` rows and one counter per chunk, for targets and weights.
+// list region of `cap` rows, one counter and one length prefix (cap + 1) per
+// chunk, for targets and weights.
 struct LongRows {
   uint32_t* list;
   unsigned int* cnt;
   uint32_t cap;
+  uint64_t* pref;
 };
 
 inline bool narrow_weights(const int64_t* in, int8_t* out, size_t k, int64_t wmax) {
@@ -557,8 +559,11 @@ bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint3
                                 256, 0, sw>>>(rows[k], rows[k + 1], off64, wd, c->perm, c->off,
                                               c->edge, c->tbits, lw.list + (size_t)k * lw.cap,
                                               lw.cnt + k, c->own_lo, c->own_hi);
+    egs::k_long_prefix<<<1, 1024, 0, sw>>>(lw.list + (size_t)k * lw.cap, lw.cnt + k, off64,
+                                           lw.pref + (size_t)k * (lw.cap + 1));
     egs::k_relabel_weights_long<W><<<2 * c->num_sms, 256, 0, sw>>>(
-        lw.list + (size_t)k * lw.cap, lw.cnt + k, off64, wd, c->perm, c->off, c->edge, c->tbits);
+        lw.list + (size_t)k * lw.cap, lw.cnt + k, lw.pref + (size_t)k * (lw.cap + 1), off64, wd,
+        c->perm, c->off, c->edge, c->tbits);
     // the chunk's player-1 light rows, complete now: sorted by weight
     if (!c->tbits) CK(cudaStreamWaitEvent(sw, et[k], 0));  // (wide: targets written apart)
     egs::k_sort_p1_rows<<<grid_for((uint64_t)(rows[k + 1] - rows[k]) * 32, c->num_sms), 256, 0,
@@ -594,7 +599,7 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
   cudaStream_t s = c->stream, sc = c->copy_stream, sw = c->aux_stream;
   const int sms = c->num_sms;
   DevBuf d_off64, d_dst, d_wn, d_owner, d_key, d_tcount, d_misc, d_ck0, d_cv0, d_ck1,
-      d_long, d_cv1, d_rel, d_cnt, d_rb, d_stmp;
+      d_long, d_lpref, d_cv1, d_rel, d_cnt, d_rb, d_stmp;
   uint64_t* off64 = d_off64.alloc<uint64_t>((size_t)n + 1);
   uint32_t* dst = d_dst.alloc<uint32_t>(m);
   void* wn = d_wn.alloc<int32_t>(m);  // narrowed weights (int8/16/32)
@@ -602,10 +607,27 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
   // [0..15] class histogram, [16] bad, [32..63] long-row counters (targets,
   // weights) of the 16 chunks
   unsigned int* misc = d_misc.alloc<unsigned int>(64);
-  const uint32_t long_cap = (uint32_t)(m / egs::kRelabelLong + 1);
+  // row-range chunks of ~m/16 edges (host offsets are at hand)
+  constexpr int kChunks = 16;
+  static_assert(kChunks <= egs::kMaxChunks, "k_csc_merge's chunk table");
+  std::vector<uint32_t> rows{0};
+  for (int k = 1; k < kChunks; ++k) {
+    const uint64_t target = m * (uint64_t)k / kChunks;
+    const uint64_t* it = std::lower_bound(a->csr_offsets, a->csr_offsets + n + 1, target);
+    const uint32_t r = (uint32_t)std::min<uint64_t>(n, it - a->csr_offsets);
+    if (r > rows.back()) rows.push_back(r);
+  }
+  if (rows.back() < n) rows.push_back(n);
+  const int nch = (int)rows.size() - 1;
+  uint64_t max_chunk = 0;
+  for (int k = 0; k < nch; ++k)
+    max_chunk = std::max<uint64_t>(max_chunk, a->csr_offsets[rows[k + 1]] - a->csr_offsets[rows[k]]);
+  const uint32_t long_cap = (uint32_t)(max_chunk / egs::kRelabelLong + 1);
   uint32_t* long_lists = d_long.alloc<uint32_t>((size_t)2 * 16 * long_cap);
-  const LongRows lt{long_lists, misc + 32, long_cap};
-  const LongRows lw{long_lists + (size_t)16 * long_cap, misc + 48, long_cap};
+  uint64_t* long_pref = d_lpref.alloc<uint64_t>((size_t)2 * 16 * (long_cap + 1));
+  const LongRows lt{long_lists, misc + 32, long_cap, long_pref};
+  const LongRows lw{long_lists + (size_t)16 * long_cap, misc + 48, long_cap,
+                    long_pref + (size_t)16 * (long_cap + 1)};
   uint8_t* key = d_key.alloc<uint8_t>(n);
   const uint32_t vtiles = (uint32_t)((n + egs::kScanTile - 1) / egs::kScanTile);
   uint32_t* tcount = d_tcount.alloc<uint32_t>((size_t)egs::kNumClasses * vtiles);
@@ -614,11 +636,19 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
   uint32_t* ck0 = d_ck0.alloc<uint32_t>(mo);
   uint32_t* cv0 = d_cv0.alloc<uint32_t>(mo);
   uint32_t* ck1 = d_ck1.alloc<uint32_t>(mo);
-  // transpose: chunk by chunk during the upload (one rank; k_csc_runs), or
-  // one sort of all pairs at the end (several ranks -- a rank's own rows are
-  // not chunk-contiguous -- or EGS_CSC_SORT=end (CUB) | radix (egs_scan.cuh))
+  // transpose: chunk by chunk during the upload (k_csc_runs), or one sort of
+  // all pairs at the end.  Chunk by chunk pays when the end sort would be on
+  // the critical path after the last transfer, i.e. for large arenas (C4,
+  // 2.56e8 edges: one-shot 34.9 -> 31.8 ms); below kIncTransposeMinEdges the
+  // 16 per-chunk sorts cost more than they hide (C2 / C5: +0.8 ms, C3 even).
+  // Several ranks always sort at the end (a rank's own rows are not
+  // chunk-contiguous).  EGS_CSC_SORT=inc | end (CUB) | radix (egs_scan.cuh)
+  // forces a method.
+  constexpr uint64_t kIncTransposeMinEdges = 1ull << 27;
   const char* csc_sort = std::getenv("EGS_CSC_SORT");
-  const bool csc_inc = c->runs.empty() && mo > 0 && !csc_sort;
+  const bool csc_inc = c->runs.empty() && mo > 0 &&
+                       (csc_sort ? std::strcmp(csc_sort, "inc") == 0
+                                 : mo >= kIncTransposeMinEdges);
   uint32_t *cv1 = nullptr, *rel = nullptr, *ccnt = nullptr;
   uint2* rb = nullptr;
   if (csc_inc) {
@@ -656,18 +686,6 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
   CK(cudaStreamWaitEvent(sc, e_alloc, 0));
   CK(cudaStreamWaitEvent(sw, e_alloc, 0));
 
-  // row-range chunks of ~m/16 edges (host offsets are at hand)
-  constexpr int kChunks = 16;
-  static_assert(kChunks <= egs::kMaxChunks, "k_csc_merge's chunk table");
-  std::vector<uint32_t> rows{0};
-  for (int k = 1; k < kChunks; ++k) {
-    const uint64_t target = m * (uint64_t)k / kChunks;
-    const uint64_t* it = std::lower_bound(a->csr_offsets, a->csr_offsets + n + 1, target);
-    const uint32_t r = (uint32_t)std::min<uint64_t>(n, it - a->csr_offsets);
-    if (r > rows.back()) rows.push_back(r);
-  }
-  if (rows.back() < n) rows.push_back(n);
-  const int nch = (int)rows.size() - 1;
   std::vector<cudaEvent_t> ex(nch), ew(nch), et(nch);
   for (int k = 0; k < nch; ++k) {
     CK(cudaEventCreateWithFlags(&ex[k], cudaEventDisableTiming));
@@ -757,9 +775,11 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
     egs::k_relabel_targets<<<grid_for((uint64_t)(rows[k + 1] - rows[k]) * 4, sms), 256, 0, s>>>(
         n, rows[k], rows[k + 1], off64, dst, c->perm, c->off, c->edge, c->tbits, ck0, cv0,
         misc + 16, lt.list + (size_t)k * lt.cap, lt.cnt + k, c->own_lo, c->own_hi, csc_inc);
+    egs::k_long_prefix<<<1, 1024, 0, s>>>(lt.list + (size_t)k * lt.cap, lt.cnt + k, off64,
+                                          lt.pref + (size_t)k * (lt.cap + 1));
     egs::k_relabel_targets_long<<<2 * sms, 256, 0, s>>>(
-        n, lt.list + (size_t)k * lt.cap, lt.cnt + k, off64, dst, c->perm, c->off, c->edge,
-        c->tbits, ck0, cv0, misc + 16, csc_inc);
+        n, lt.list + (size_t)k * lt.cap, lt.cnt + k, lt.pref + (size_t)k * (lt.cap + 1), off64,
+        dst, c->perm, c->off, c->edge, c->tbits, ck0, cv0, misc + 16, csc_inc);
     CK(cudaGetLastError());
     CK(cudaEventRecord(et[k], s));
     tl.mark("main: targets relabelled " + std::to_string(k), s);
@@ -841,6 +861,7 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
   d_ck1.release();
   d_misc.release();
   d_long.release();
+  d_lpref.release();
   d_cv1.release();
   d_rel.release();
   d_cnt.release();

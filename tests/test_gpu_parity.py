@@ -443,16 +443,17 @@ TRANSPOSE_ARENAS = [lambda e: e.GameArena.fixed(100000, 16, 100, 1),
 
 @pytest.mark.parametrize("make", TRANSPOSE_ARENAS, ids=["fixed-1e5-16", "rmat14", "rmat16", "fixed-d1"])
 def test_transpose_builds_agree(egs, monkeypatch, make):
-    """The predecessor transpose built chunk by chunk during the upload (the
-    default: per-chunk sort, rank, merge -- egs_build.cuh k_csc_*), by one
-    library sort at the end (EGS_CSC_SORT=end) and by the hand-written LSD
-    radix sort (EGS_CSC_SORT=radix, egs_scan.cuh) holds exactly the arena's
-    edges (debug_checks: an order-free CSR/CSC fingerprint) and gives the
-    identical measure and dense-round work (the sparse rounds and the
-    certificate cascade are order-dependent in their counts)."""
+    """The predecessor transpose built chunk by chunk during the upload
+    (EGS_CSC_SORT=inc, the default for >= 2^27 edges: per-chunk sort, rank,
+    merge -- egs_build.cuh k_csc_*), by one library sort at the end
+    (EGS_CSC_SORT=end, the default below) and by the hand-written LSD radix
+    sort (EGS_CSC_SORT=radix, egs_scan.cuh) holds exactly the arena's edges
+    (debug_checks: an order-free CSR/CSC fingerprint) and gives the identical
+    measure and dense-round work (the sparse rounds and the certificate
+    cascade are order-dependent in their counts)."""
     a = make(egs)
     out = {}
-    for mode in ("radix", "end", "default"):
+    for mode in ("radix", "end", "inc", "default"):
         if mode == "default":
             monkeypatch.delenv("EGS_CSC_SORT", raising=False)
         else:
@@ -460,6 +461,6 @@ def test_transpose_builds_agree(egs, monkeypatch, make):
         with egs.DeviceSolver(a, egs.SolverOptions(debug_checks=True)) as ds:
             st = ds.solve()
             out[mode] = (ds.read_measure(), st.rounds, st.dense_rounds)
-    for mode in ("radix", "end"):
+    for mode in ("radix", "end", "inc"):
         assert np.array_equal(out[mode][0], out["default"][0]), mode
         assert out[mode][1:] == out["default"][1:], mode
