@@ -24,23 +24,27 @@ bool narrow_scalar(const int64_t* in, W* out, size_t count, int64_t wmax) {
   return lo < -wmax || hi > wmax;
 }
 
-// 8 weights per vector; the store width follows W
+// 8 weights per vector; the store width follows W.  Streaming (non-temporal)
+// stores: the stage is read next by the DMA engine, not by this core, and
+// they skip the line fill a plain store makes -- the upload is bound by
+// host-memory traffic (DMA reads + these reads of the int64 weights).
+// `out` is aligned to the store width (the caller's scalar head).
 template <class W>
 __attribute__((target("avx512f,avx512bw,avx512vl"))) inline void store8(W* out, __m512i v);
 template <>
 __attribute__((target("avx512f,avx512bw,avx512vl"))) inline void store8<int8_t>(int8_t* out,
                                                                                __m512i v) {
-  _mm_storel_epi64(reinterpret_cast<__m128i*>(out), _mm512_cvtepi64_epi8(v));
+  _mm_stream_si64(reinterpret_cast<long long*>(out), _mm_cvtsi128_si64(_mm512_cvtepi64_epi8(v)));
 }
 template <>
 __attribute__((target("avx512f,avx512bw,avx512vl"))) inline void store8<int16_t>(int16_t* out,
                                                                                 __m512i v) {
-  _mm_storeu_si128(reinterpret_cast<__m128i*>(out), _mm512_cvtepi64_epi16(v));
+  _mm_stream_si128(reinterpret_cast<__m128i*>(out), _mm512_cvtepi64_epi16(v));
 }
 template <>
 __attribute__((target("avx512f,avx512bw,avx512vl"))) inline void store8<int32_t>(int32_t* out,
                                                                                 __m512i v) {
-  _mm256_storeu_si256(reinterpret_cast<__m256i*>(out), _mm512_cvtepi64_epi32(v));
+  _mm256_stream_si256(reinterpret_cast<__m256i*>(out), _mm512_cvtepi64_epi32(v));
 }
 
 template <class W>
@@ -48,7 +52,13 @@ __attribute__((target("avx512f,avx512bw,avx512vl"))) bool narrow_avx512(const in
                                                                         size_t count,
                                                                         int64_t wmax) {
   __m512i lo0 = _mm512_setzero_si512(), hi0 = lo0, lo1 = lo0, hi1 = lo0;
+  // scalar head up to the store width's alignment of out
   size_t i = 0;
+  bool head_bad = false;
+  while (i < count && (reinterpret_cast<uintptr_t>(out + i) & (8 * sizeof(W) - 1))) {
+    head_bad |= narrow_scalar<W>(in + i, out + i, 1, wmax);
+    ++i;
+  }
   for (; i + 16 <= count; i += 16) {
     const __m512i a = _mm512_loadu_si512(in + i);
     const __m512i b = _mm512_loadu_si512(in + i + 8);
@@ -59,10 +69,11 @@ __attribute__((target("avx512f,avx512bw,avx512vl"))) bool narrow_avx512(const in
     store8<W>(out + i, a);
     store8<W>(out + i + 8, b);
   }
+  _mm_sfence();
   const int64_t lo = _mm512_reduce_min_epi64(_mm512_min_epi64(lo0, lo1));
   const int64_t hi = _mm512_reduce_max_epi64(_mm512_max_epi64(hi0, hi1));
   const bool tail_bad = narrow_scalar<W>(in + i, out + i, count - i, wmax);
-  return tail_bad || lo < -wmax || hi > wmax;
+  return head_bad || tail_bad || lo < -wmax || hi > wmax;
 }
 
 void widen_scalar(const uint32_t* in, int64_t* out, size_t count) {

@@ -564,12 +564,14 @@ bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint3
     egs::k_relabel_weights_long<W><<<2 * c->num_sms, 256, 0, sw>>>(
         lw.list + (size_t)k * lw.cap, lw.cnt + k, lw.pref + (size_t)k * (lw.cap + 1), off64, wd,
         c->perm, c->off, c->edge, c->tbits);
+    tl.mark("aux: weights relabelled " + std::to_string(k), sw);
     // the chunk's player-1 light rows, complete now: sorted by weight
     if (!c->tbits) CK(cudaStreamWaitEvent(sw, et[k], 0));  // (wide: targets written apart)
     egs::k_sort_p1_rows<<<grid_for((uint64_t)(rows[k + 1] - rows[k]) * 32, c->num_sms), 256, 0,
                           sw>>>(rows[k], rows[k + 1], key, c->perm, c->off, c->edge, c->tbits,
                                 c->own_lo, c->own_hi, c->rec0);
     CK(cudaGetLastError());
+    tl.mark("aux: rows sorted " + std::to_string(k), sw);
   }
   for (auto& th : pool) th.join();
   // the staging buffer is re-used by the next upload: wait for its DMA
@@ -800,9 +802,11 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
     egs::ChunkStarts cs{};
     cs.nch = nch;
     for (int k = 0; k <= nch; ++k) cs.e[k] = a->csr_offsets[rows[k]];
+    // one CTA per span (not a persistent grid): CTAs retire as they finish,
+    // so the weight chunks' kernels on the higher-priority aux stream get SMs
+    // while the merge runs
     const uint64_t spans_n = (mo + egs::kMergeSpan - 1) / egs::kMergeSpan;
-    egs::k_csc_merge<<<(uint32_t)std::min<uint64_t>(spans_n, (uint64_t)sms * 4), 512, 0, s>>>(
-        ck1, cv1, rel, mo, c->coff, cs, c->csrc);
+    egs::k_csc_merge<<<(uint32_t)spans_n, 512, 0, s>>>(ck1, cv1, rel, mo, c->coff, cs, c->csrc);
     CK(cudaGetLastError());
   } else {
     // transpose: stable radix sort of the (dst, src) pairs by dst while the
@@ -935,7 +939,11 @@ egs_ctx* ctx_create(const egs_arena_view* a, const egs_gpu_opts& opts, egs_gpu_s
     } else {
       CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
       CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
-      CK(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
+      {  // the weight chunks' kernels outrank the transpose merge (build_arena)
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithPriority(&c->aux_stream, cudaStreamNonBlocking, hi));
+      }
       for (auto& e : c->ev) CK(cudaEventCreate(&e));
       CK(cudaMallocHost(&c->h_ctr, egs::kNumCounters * sizeof(unsigned long long)));
     }

@@ -40,6 +40,13 @@ def test_narrow_matches_numpy(lib, dt, sym):
             assert bad == want_bad, (count, case)
             assert np.array_equal(out[:count], w.astype(dt)), (count, case)
             assert not out[count:].any(), "wrote past the end"
+        # an output not aligned to the vector store width (scalar head)
+        for shift in (1, 3, 7):
+            w = rng.integers(-wmax, wmax + 1, size=count, dtype=np.int64)
+            buf = np.zeros(count + 16, dtype=dt)
+            assert not fn(w.ctypes.data, buf[shift:].ctypes.data, count, wmax)
+            assert np.array_equal(buf[shift:shift + count], w.astype(dt)), (count, shift)
+            assert not buf[:shift].any() and not buf[shift + count:].any()
         # a tighter bound than the type's (packed records: 31 - tbits bits)
         w = np.full(max(count, 1), 100, dtype=np.int64)
         assert not fn(w.ctypes.data, np.zeros(w.size, dt).ctypes.data, w.size, 100)
