@@ -761,7 +761,13 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
   // the incremental transpose's sort temporaries, sized for the largest chunk
   void* sort_tmp = nullptr;
   size_t sort_tb = 0;
-  if (csc_inc) {
+  // The chunk sorts are the hand-written stable LSD radix sort (egs_scan.cuh)
+  // by default -- hidden under the transfer, so the library sort's speed buys
+  // nothing there; EGS_CSC_CHUNK_SORT=cub selects CUB's onesweep.
+  const char* chunk_sort = std::getenv("EGS_CSC_CHUNK_SORT");
+  const bool chunk_cub = chunk_sort && std::strcmp(chunk_sort, "cub") == 0;
+  uint32_t *sk = ck1, *sv = cv1;  // where the sorted chunks end up (the same for every chunk)
+  if (csc_inc && chunk_cub) {
     uint64_t maxlen = 0;
     for (int k = 0; k < nch; ++k)
       maxlen = std::max<uint64_t>(maxlen, a->csr_offsets[rows[k + 1]] - a->csr_offsets[rows[k]]);
@@ -788,10 +794,18 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
     if (csc_inc) {
       const uint64_t e0 = a->csr_offsets[rows[k]], len = a->csr_offsets[rows[k + 1]] - e0;
       if (len == 0) continue;
-      CK(cub::DeviceRadixSort::SortPairs(sort_tmp, sort_tb, ck0 + e0, ck1 + e0, cv0 + e0,
-                                         cv1 + e0, (int64_t)len, 0, bits_for(n), s));
-      egs::k_csc_runs<<<grid_for(len, sms), 256, 0, s>>>(ck1 + e0, len, ccnt, rb);
-      egs::k_csc_rel<<<grid_for(len, sms), 256, 0, s>>>(ck1 + e0, len, rb, ccnt, rel + e0);
+      if (chunk_cub) {
+        CK(cub::DeviceRadixSort::SortPairs(sort_tmp, sort_tb, ck0 + e0, ck1 + e0, cv0 + e0,
+                                           cv1 + e0, (int64_t)len, 0, bits_for(n), s));
+      } else {
+        uint32_t *ks = nullptr, *vs = nullptr;
+        dev_radix_sort_pairs(ck0 + e0, cv0 + e0, ck1 + e0, cv1 + e0, len, bits_for(n), s, sms,
+                             &ks, &vs);
+        sk = ks - e0;  // (an odd digit count ends in ck1 / cv1, an even one in ck0 / cv0)
+        sv = vs - e0;
+      }
+      egs::k_csc_runs<<<grid_for(len, sms), 256, 0, s>>>(sk + e0, len, ccnt, rb);
+      egs::k_csc_rel<<<grid_for(len, sms), 256, 0, s>>>(sk + e0, len, rb, ccnt, rel + e0);
       CK(cudaGetLastError());
       tl.mark("main: transpose chunk " + std::to_string(k), s);
     }
@@ -806,7 +820,7 @@ void build_arena(egs_ctx* c, const egs_arena_view* a, const egs_part_plan* plan)
     // so the weight chunks' kernels on the higher-priority aux stream get SMs
     // while the merge runs
     const uint64_t spans_n = (mo + egs::kMergeSpan - 1) / egs::kMergeSpan;
-    egs::k_csc_merge<<<(uint32_t)spans_n, 512, 0, s>>>(ck1, cv1, rel, mo, c->coff, cs, c->csrc);
+    egs::k_csc_merge<<<(uint32_t)spans_n, 512, 0, s>>>(sk, sv, rel, mo, c->coff, cs, c->csrc);
     CK(cudaGetLastError());
   } else {
     // transpose: stable radix sort of the (dst, src) pairs by dst while the
