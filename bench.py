@@ -257,25 +257,36 @@ def load_peaks():
     return FALLBACK_HBM_GBS, "fallback"
 
 
-def lib_sha256():
+def source_digest():
+    """SHA-256 over the library's sources and build recipe (csrc/, the C-ABI
+    header, Makefile): what determines k_solve's code, unlike the .so's own
+    hash, which also changes with the build directory (-lineinfo paths)."""
+    import glob
     import hashlib
-    import paper_1710_03647_b200 as egs
-    with open(egs.lib_path, "rb") as fh:
-        return hashlib.sha256(fh.read()).hexdigest()
+    h = hashlib.sha256()
+    files = sorted(glob.glob(os.path.join(ROOT, "paper_1710_03647_b200", "csrc", "*"))) + [
+        os.path.join(ROOT, "include", "egs_gpu.h"), os.path.join(ROOT, "Makefile")]
+    for f in files:
+        if f.endswith((".cu", ".cuh", ".cpp", ".h")) or f.endswith("Makefile"):
+            h.update(os.path.relpath(f, ROOT).encode())
+            with open(f, "rb") as fh:
+                h.update(fh.read())
+    return h.hexdigest()
 
 
 def load_traffic():
     """Per-launch DRAM bytes of k_solve from the committed ncu capture
-    (tools/summarize_profile.py), used only when it was captured with the very
-    library this run loads (SHA-256 stamp); otherwise None."""
+    (tools/summarize_profile.py), used only when it was captured from the
+    very sources this run's library is built from (source digest stamp);
+    otherwise None."""
     p = os.path.join(ROOT, "profiles", "lift_traffic.json")
     try:
         with open(p) as fh:
             t = json.load(fh)
     except Exception:
         return None, "no committed ncu capture"
-    if t.get("lib_sha256") != lib_sha256():
-        return None, "committed ncu capture is of another build of libegs_b200.so"
+    if t.get("source_digest") != source_digest():
+        return None, "committed ncu capture is of other library sources"
     return t, t.get("source")
 
 

@@ -5,6 +5,7 @@ set -u
 OUT=gpurun_out/$1
 mkdir -p $OUT
 sha256sum paper_1710_03647_b200/libegs_b200.so > $OUT/lib_sha256.txt
+python -c "import bench; print(bench.source_digest())" > $OUT/source_digest.txt
 timeout 900 python bench.py --steps 20 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv python tools/ncu_target.py C4 1 > $OUT/launches.out 2>&1; echo "launches rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_solve -c 1 -o $OUT/solve_c4 python tools/ncu_target.py C4 1 > $OUT/ncu.out 2>&1; echo "ncu rc=$?"

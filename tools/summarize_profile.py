@@ -2,10 +2,11 @@
 bench line, ncu summary of k_solve, DRAM traffic per launch, launch list,
 source hotspots.   usage: python tools/summarize_profile.py <tag> [round prefix, r02]
 
-profiles/lift_traffic.json is stamped with the SHA-256 of the library the
-capture ran (gpurun_out/<tag>/lib_sha256.txt, written by gpu_bench_profile.sh):
-bench.py reports it as `roofline.traffic` only while that library is the one
-it loads, so a stale capture is never paired with a newer kernel."""
+profiles/lift_traffic.json is stamped with the digest of the library sources
+the capture ran (gpurun_out/<tag>/source_digest.txt, bench.source_digest(),
+written by gpu_bench_profile.sh) and the .so's SHA-256: bench.py reports it as
+`roofline.traffic` only while the sources match, so a stale capture is never
+paired with a newer kernel."""
 import csv
 import io
 import json
@@ -49,8 +50,10 @@ rd = float(out["dram__bytes_read.sum"][0].replace(",", "")) * scale[out["dram__b
 wr = float(out["dram__bytes_write.sum"][0].replace(",", "")) * scale[out["dram__bytes_write.sum"][1]]
 shafile = os.path.join(src, "lib_sha256.txt")
 lib_sha = open(shafile).read().split()[0] if os.path.exists(shafile) else None
+digfile = os.path.join(src, "source_digest.txt")
+src_digest = open(digfile).read().split()[0] if os.path.exists(digfile) else None
 json.dump({"kernel": "k_solve", "bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
-           "lib_sha256": lib_sha,
+           "lib_sha256": lib_sha, "source_digest": src_digest,
            "source": f"ncu --set full --clock-control none -k regex:k_solve -c 1 "
                      f"python tools/ncu_target.py C4 1 ({tag})"},
           open(os.path.join(dst, "lift_traffic.json"), "w"), indent=1)
