@@ -79,9 +79,10 @@ typedef struct egs_gpu_opts {
                               0: plain value iteration up to credit_cap */
   int32_t cert_interval;   /* round of the first certificate attempt; the
                               interval then doubles (0 = 1) */
-  int32_t cert_growth;     /* interval multiplier after each attempt (0 = 4) */
+  int32_t cert_growth;     /* interval multiplier after each attempt (0 = 8) */
   int32_t sparse_div;      /* next round is sparse iff estimated frontier *
-                              sparse_div < n (0 = 4) */
+                              sparse_div < n (0 = 8; also the certificate's
+                              dense / sparse pass threshold) */
   int32_t grid_ctas;       /* persistent-kernel CTAs; 0 = auto */
   int32_t no_tma;          /* 1: stage no edge spans through TMA (A/B and
                               debugging); the result is identical */

@@ -406,8 +406,8 @@ class SolverOptions:
     workers: int = 1
     certify: bool = True
     cert_interval: int = 1
-    cert_growth: int = 4
-    sparse_div: int = 4
+    cert_growth: int = 8
+    sparse_div: int = 8
     grid_ctas: int = 0
     no_tma: bool = False
     mode: str = "auto"

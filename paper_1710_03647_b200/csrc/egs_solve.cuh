@@ -2859,7 +2859,7 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
       const uint32_t cert = prev_sum(0);
       certified_any = cert > 0;
       changed += cert;
-      // geometric schedule (rounds 1, 5, 21, 85, ... by default): the first
+      // geometric schedule (rounds 1, 9, 73, 137, ... by default): the first
       // attempt catches the regular climbs (the canonical configs certify
       // their losing region at round 1), later ones get rarer so a game
       // without a climbing region pays O(log) attempts

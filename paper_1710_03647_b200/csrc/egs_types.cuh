@@ -125,7 +125,7 @@ struct SolveParams {
   int use_tma;
   int certify;
   int cert_interval;
-  int cert_growth;          // interval multiplier after each attempt (4)
+  int cert_growth;          // interval multiplier after each attempt (8)
   uint32_t sparse_div;      // next round sparse iff est. frontier * div < n
   float cert_sparse_div;    // certificate pass sparse iff removed * deg * div < n
   float avg_in_deg;
