@@ -340,7 +340,7 @@ def run_our_arm(a):
     out, _owner = egs.pinned_empty(n)
     h2d = h2d_bytes(arena)
     d2h = n * 8
-    for _ in range(max(1, a.warmup // 2)):
+    for _ in range(max(2, a.warmup)):
         egs.solve(arena, options=opts, out=out)
     barrier(world)
     e2e_t, e2e_edges = 0.0, 0
