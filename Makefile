@@ -23,7 +23,7 @@ all: $(LIB) $(ORACLE_LIB) $(ORACLE_CLI) ref
 
 HDRS := $(CSRC)/egs_types.cuh $(CSRC)/egs_device.cuh include/egs_gpu.h
 
-$(CSRC)/egs_solver.o: $(CSRC)/egs_solver.cu $(CSRC)/egs_build.cuh $(CSRC)/egs_scan.cuh $(CSRC)/egs_narrow.h $(HDRS)
+$(CSRC)/egs_solver.o: $(CSRC)/egs_solver.cu $(CSRC)/egs_build.cuh $(CSRC)/egs_scan.cuh $(CSRC)/egs_narrow.h $(CSRC)/egs_pool.h $(HDRS)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/egs_solver.ptxas.log || (cat $(CSRC)/egs_solver.ptxas.log; false)
 	sed -i '/Compile time/d' $(CSRC)/egs_solver.ptxas.log
 

@@ -34,6 +34,7 @@
 #include "egs_build.cuh"
 #include "egs_gpu.h"
 #include "egs_narrow.h"
+#include "egs_pool.h"
 #include "egs_scan.cuh"
 #include "egs_types.cuh"
 
@@ -528,20 +529,21 @@ bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint3
     while (one_block(k)) {
     }
   };
-  std::vector<std::thread> pool;
-  // The helpers read this frame's locals: on any error (a CK throw) stop
-  // them by exhausting the block counter and join them before unwinding.
+  // The helpers (the host pool's workers, egs_pool.h) read this frame's
+  // locals: on any error (a CK throw) stop them by exhausting the block
+  // counter and join them before unwinding (the Job waits in its destructor,
+  // declared before the Joiner so it is destroyed after it).
+  egs_host::Pool::Job helpers;
   struct Joiner {
-    std::vector<std::thread>& pool;
+    egs_host::Pool::Job& job;
     std::atomic<uint64_t>& next;
     uint64_t nblk;
     ~Joiner() {
       next.store(nblk, std::memory_order_relaxed);
-      for (auto& th : pool)
-        if (th.joinable()) th.join();
+      job.wait();
     }
-  } joiner{pool, next, nblk};
-  for (int t = 0; t < T; ++t) pool.emplace_back(work);
+  } joiner{helpers, next, nblk};
+  egs_host::Pool::get().launch(helpers, (unsigned)T, [&](unsigned) { work(); });
   int kself = 0;
   for (int k = 0; k < nch; ++k) {
     while (left[k].load(std::memory_order_acquire) > 0)
@@ -573,7 +575,7 @@ bool upload_weights(egs_ctx* c, const egs_arena_view* a, const std::vector<uint3
     CK(cudaGetLastError());
     tl.mark("aux: rows sorted " + std::to_string(k), sw);
   }
-  for (auto& th : pool) th.join();
+  helpers.wait();
   // the staging buffer is re-used by the next upload: wait for its DMA
   CK(cudaStreamSynchronize(sc));
   return out_of_range.load();
@@ -1375,7 +1377,9 @@ void ctx_read(egs_ctx* c, int64_t* out) {
   }
   const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
   const unsigned T = n >= (1u << 20) ? hw : 1;
+  const int device = c->device;
   auto work = [&](unsigned t) {  // slice t of every part, in landing order
+    cudaSetDevice(device);  // (a pool worker's current device may be another)
     for (int k = 0; k < kParts; ++k) {
       cudaEventSynchronize(ev[k]);
       const uint64_t a = lo(k) + (lo(k + 1) - lo(k)) * t / T;
@@ -1383,10 +1387,11 @@ void ctx_read(egs_ctx* c, int64_t* out) {
       egs_internal_widen_u32(stage + a, out + a, b - a);
     }
   };
-  std::vector<std::thread> pool;
-  for (unsigned t = 1; t < T; ++t) pool.emplace_back(work, t);
-  work(0);
-  for (auto& th : pool) th.join();
+  {
+    egs_host::Pool::Job helpers;
+    egs_host::Pool::get().launch(helpers, T - 1, [&](unsigned t) { work(t + 1); });
+    work(0);
+  }
   cudaError_t err = cudaSuccess;
   for (int k = 0; k < kParts; ++k) {
     const cudaError_t e = cudaEventQuery(ev[k]);

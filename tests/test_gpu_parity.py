@@ -449,8 +449,10 @@ def test_transpose_builds_agree(egs, monkeypatch, make):
     (EGS_CSC_SORT=end, the default below) and by the hand-written LSD radix
     sort (EGS_CSC_SORT=radix, egs_scan.cuh) holds exactly the arena's edges
     (debug_checks: an order-free CSR/CSC fingerprint) and gives the identical
-    measure and dense-round work (the sparse rounds and the certificate
-    cascade are order-dependent in their counts)."""
+    measure.  (Round counts may differ: a column's source order sets the
+    order of a sparse round's in-place lifts, hence how much it raises and
+    the next round's dense / sparse choice -- rmat16 takes 6 or 7 dense
+    rounds.)"""
     a = make(egs)
     out = {}
     for mode in ("radix", "end", "inc", "default"):
@@ -463,4 +465,3 @@ def test_transpose_builds_agree(egs, monkeypatch, make):
             out[mode] = (ds.read_measure(), st.rounds, st.dense_rounds)
     for mode in ("radix", "end", "inc"):
         assert np.array_equal(out[mode][0], out["default"][0]), mode
-        assert out[mode][1:] == out["default"][1:], mode
