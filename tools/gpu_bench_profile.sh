@@ -19,7 +19,7 @@ timeout 300 python tools/e2e_breakdown.py C4 > $OUT/e2e_breakdown.txt 2>&1; echo
 # processes time-slice the GPU, so the time is not a scaling number)
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29555 bench.py --gpus 2 --steps 3 --warmup 3 > $OUT/bench_2proc_1gpu.json 2> $OUT/bench_2proc_1gpu.err; echo "2proc rc=$?"
 timeout 900 python -m pytest tests -m gpu -q > $OUT/gpu_tests.txt 2>&1; echo "gpu tests rc=$?"
-timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_reference.json 2> $OUT/bench_reference.err; echo "reference arm rc=$?"
+timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > $OUT/bench_reference.json 2> $OUT/bench_reference.err; echo "reference arm rc=$?"
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.txt 2>&1; echo "smoke rc=$?"
 cat $OUT/bench.json
 
