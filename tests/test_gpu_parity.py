@@ -465,3 +465,32 @@ def test_transpose_builds_agree(egs, monkeypatch, make):
             out[mode] = (ds.read_measure(), st.rounds, st.dense_rounds)
     for mode in ("radix", "end", "inc"):
         assert np.array_equal(out[mode][0], out["default"][0]), mode
+
+
+def test_concurrent_one_shot_solves(egs):
+    """One-shot solves from several host threads at once (ctypes releases the
+    GIL): the upload's narrowing helpers and the read-back's widening threads
+    come from one process-wide pool (egs_pool.h), and a caller that finds it
+    busy runs threads of its own -- every result equals the sequential one.
+    Arenas large enough (>= 2^20 vertices) for the pooled paths."""
+    import threading
+    arenas = [egs.GameArena.fixed(1_100_000, 8, 100, s) for s in (1, 2, 3)]
+    want = [egs.solve(a).measure for a in arenas]
+    got = [None] * len(arenas)
+    errs = []
+
+    def run(i):
+        try:
+            for _ in range(3):
+                got[i] = egs.solve(arenas[i]).measure
+        except BaseException as e:  # noqa: BLE001 -- reported below
+            errs.append(e)
+
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(len(arenas))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errs, errs
+    for w, g in zip(want, got):
+        assert np.array_equal(w, g)
