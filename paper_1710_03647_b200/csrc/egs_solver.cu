@@ -1715,8 +1715,19 @@ cudaUUID_t device_uuid(int device) {
 }
 
 // Grid of a rank's persistent kernel: ranks sharing a device split it.
+// Their persistent kernels must run concurrently, which needs them on
+// different hardware work queues: with the default 8 (CUDA_DEVICE_MAX_CONNECTIONS)
+// and three streams per rank, 5-7 ranks on one GPU deadlock at the first
+// cross-rank barrier (measured; 8 ranks work with 32 queues) -- refused
+// up front instead of timing out.
 void part_grid(egs_ctx* c, int ranks_on_device) {
   if (ranks_on_device <= 1) return;
+  const char* q = std::getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+  const int queues = q ? std::atoi(q) : 8;
+  if (ranks_on_device > 4 && queues < 4 * ranks_on_device)
+    throw Fail(EGS_ERR_INVALID_CONFIG,
+               std::to_string(ranks_on_device) + " ranks share one GPU: set "
+               "CUDA_DEVICE_MAX_CONNECTIONS=32 before CUDA initialises (or use at most 4)");
   c->grid = std::max(1, std::min(c->grid, c->full_grid / ranks_on_device));
 }
 

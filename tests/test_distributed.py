@@ -305,3 +305,20 @@ def test_two_processes_one_gpu_over_ipc():
         for ok, rounds in out:
             assert ok
         assert [x[1] for x in out] == [x[1] for x in res[0][0]], "ranks took different schedules"
+
+
+@pytest.mark.gpu
+def test_many_ranks_on_one_gpu_refused_not_deadlocked(egs):
+    """More than 4 ranks on one GPU need more hardware work queues than the
+    default 8 for their persistent kernels to run at once (measured: 5-7
+    ranks deadlock at the first cross-rank barrier, 8 work with
+    CUDA_DEVICE_MAX_CONNECTIONS=32): connecting them is refused up front."""
+    if int(os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS", "8")) >= 32:
+        pytest.skip("enough hardware queues configured")
+    from paper_1710_03647_b200.distributed import Partition
+    a = egs.GameArena.fixed(5000, 4, 100, 1)
+    parts = [Partition(a, r, 6, egs.SolverOptions(device=0)) for r in range(6)]
+    with pytest.raises(egs.InvalidConfigError, match="CUDA_DEVICE_MAX_CONNECTIONS"):
+        Partition.connect_local(parts)
+    for p in parts:
+        p.close()
