@@ -1383,12 +1383,30 @@ __device__ __forceinline__ bool cert_keep_block(const SolveParams<V>& p, uint32_
 // the weights is both the seeding and the first synchronous round of
 // solve_frontier / solve_sweep.  The player-0 witness starts at the argmin:
 // the first non-negative edge, else the least negative one.
+// A round-1 raise.  Round 1 reads the weights only, so with one rank it
+// writes f directly (r1_direct: no staging, no commit phase) and, when the
+// first certificate attempt follows it (r1_cand), marks the candidates as
+// the commit would -- the value's top bit here, the bitmap bit at the
+// caller's change ballot.  (A round-1 value is max(0, -w) <= max |w| <=
+// credit_cap, never top, so every raised vertex is a candidate.)
+template <class V>
+__device__ __forceinline__ void r1_store(const SolveParams<V>& p, uint32_t v, V val) {
+  if (p.r1_direct)
+    stcg(p.f + v, p.r1_cand ? (V)(val | CandFlag<V>::v) : val);
+  else
+    stcg(p.stage + v, val);
+}
+// the candidate bits of a word's raised vertices (r1_cand; warp-uniform m)
+template <class V>
+__device__ __forceinline__ void r1_cand_bits(const SolveParams<V>& p, uint32_t w, uint32_t m) {
+  if (p.r1_cand && m && lane_id() == 0) bits_or(p, p.cand + w, m);
+}
 template <class V>
 __device__ __forceinline__ void round1_finish(const SolveParams<V>& p, uint32_t v, bool p0,
                                               int minw, int maxw, uint32_t imax, V& val) {
   val = ominus_cap<V>(V(0), p0 ? maxw : minw, p.g.cap);
   if (p0) stcg(wit_of(p) + v, __ldg(erecs(p.g) + imax));
-  if (val > V(0)) stcg(p.stage + v, val);
+  if (val > V(0)) r1_store<V>(p, v, val);
 }
 
 // light rows: one thread per row over the TMA tile pipeline (the weight scan
@@ -1408,7 +1426,7 @@ __device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo0,
     ++L.apps;
     L.edges += len;
     if (val > V(0)) {
-      stcg(p.stage + v, val);
+      r1_store<V>(p, v, val);
       ++L.lifts;
       return true;
     }
@@ -1482,8 +1500,11 @@ __device__ __noinline__ void round1_light(const SolveParams<V>& p, uint32_t lo0,
     }
     return finish(v, p0, minw, maxw, __ldg(erecs(g) + ibest), e - b);
   };
+  auto after = [&](uint32_t v, bool ch) {  // warp-uniform, one tile = one word
+    r1_cand_bits<V>(p, v >> 5, __ballot_sync(0xffffffffu, ch));
+  };
   tma_tiles<V>(p, (p.use_tma & kTmaRound1) != 0, lo0, hi0, lo1, hi1, cursor, nullptr, chg, L,
-               load, test, row, fallback);
+               load, test, row, fallback, after);
   block_flush(L, sum_dst);
 }
 
@@ -1572,7 +1593,7 @@ __device__ __noinline__ void round1_p0_pairs(const SolveParams<V>& p, uint32_t l
     ++L.apps;
     L.edges += len;
     if (val > V(0)) {
-      stcg(p.stage + v, val);
+      r1_store<V>(p, v, val);
       ++L.lifts;
       return true;
     }
@@ -1590,7 +1611,7 @@ __device__ __noinline__ void round1_p0_pairs(const SolveParams<V>& p, uint32_t l
     ++L.apps;
     L.edges += e - b;
     if (val > V(0)) {
-      stcg(p.stage + v, val);
+      r1_store<V>(p, v, val);
       ++L.lifts;
       return true;
     }
@@ -1610,6 +1631,7 @@ __device__ __noinline__ void round1_p0_pairs(const SolveParams<V>& p, uint32_t l
                       : direct(v, t.b[h], t.e[h]);
       const uint32_t m = __ballot_sync(0xffffffffu, ch);
       if (m && lane == 0) bits_or(p, chg + t.w + h, m);
+      r1_cand_bits<V>(p, t.w + h, m);
       L.phase_count += ch;
     }
   };
@@ -1691,6 +1713,7 @@ __device__ __noinline__ void round1_long(const SolveParams<V>& p, uint32_t* chg,
       L.edges += e - b;
       if (val > V(0)) {
         set_bit(p, chg, u);
+        if (p.r1_cand) set_bit(p, p.cand, u);
         ++L.phase_count;
         ++L.lifts;
       }
@@ -1742,6 +1765,7 @@ __device__ __noinline__ void round1_long(const SolveParams<V>& p, uint32_t* chg,
       L.edges += e - b;
       if (val > V(0)) {
         set_bit(p, chg, u);
+        if (p.r1_cand) set_bit(p, p.cand, u);
         ++L.phase_count;
         ++L.lifts;
       }
@@ -1794,13 +1818,14 @@ __device__ __noinline__ void round1_p1_light(const SolveParams<V>& p, uint32_t l
           ++L.visits;
           ++L.apps;
           if (val > V(0)) {
-            stcg(p.stage + v, val);
+            r1_store<V>(p, v, val);
             ++L.lifts;
             ch = true;
           }
         }
         const uint32_t m = __ballot_sync(0xffffffffu, ch);
         if (m && lane == 0 && w0 + k < w_hi) bits_or(p, chg + w0 + k, m);
+        if (w0 + k < w_hi) r1_cand_bits<V>(p, w0 + k, m);
         L.phase_count += ch;
       }
     }
@@ -2740,16 +2765,19 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
     if (changed == 0) break;  // a round that raised nothing: least fixpoint
     // (no attempt in a round that stops the solve: the candidate marks in f
     // never outlive an attempt)
-    const bool cert_now = p.certify && round >= next_cert && round < p.round_budget &&
-                          !vload(&sh->stop);
+    // (round 1 written straight into f with the candidates marked: the
+    // attempt runs whatever the stop flag says, or the marks would outlive it)
+    const bool r1d = round == 1 && p.r1_direct;
+    const bool cert_now = (r1d && p.r1_cand) || (p.certify && round >= next_cert &&
+                                                 round < p.round_budget && !vload(&sh->stop));
     // without a certificate attempt the next round's mode is known already:
     // a sparse next round gets its activation in the commit phase (the
     // activation's top filter may see either the old or the committed value
     // of a predecessor; a stale one only adds a harmless frontier entry)
     const bool fuse_act =
-        !inplace && !cert_now && !p.no_fuse && p.mode != kModeDense && p.mode != kModeSweep &&
+        !inplace && !r1d && !cert_now && !p.no_fuse && p.mode != kModeDense && p.mode != kModeSweep &&
         !(p.mode == kModeAuto && (double)changed * p.avg_in_deg * p.sparse_div >= (double)n);
-    if (!inplace) {  // a Jacobi round: publish its staged values
+    if (!inplace && !r1d) {  // a Jacobi round: publish its staged values
       if (p.debug) {  // (its own phase: the commit overwrites what it compares)
         begin_phase();
         phase_debug_raise<V>(p, chg);
@@ -2773,7 +2801,7 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
                             slot_sum(), slot_dyn() + 2);
       }
       end_phase(1, 0);
-    } else if (cert_now) {  // in-place round: f is current, only mark the candidates
+    } else if (cert_now && !(r1d && p.r1_cand)) {  // f is current: only mark the candidates
       begin_phase();
       phase_cert_init<V>(p, chg, slot_sum());
       end_phase(2, 1);

@@ -1154,6 +1154,13 @@ egs::SolveParams<V> make_params(egs_ctx* c, unsigned long long* budget_out) {
     budget = (c->m && per > ~0ull / c->m) ? ~0ull : c->m * per + 1ull;
   }
   p.round_budget = budget;
+  // round 1 straight into f (one rank), marking the first attempt's
+  // candidates when the attempt follows round 1 (EGS_R1_DIRECT=0: staged)
+  {
+    const char* e = std::getenv("EGS_R1_DIRECT");
+    p.r1_direct = c->world == 1 && (e ? std::atoi(e) != 0 : true);
+    p.r1_cand = p.r1_direct && p.certify && p.cert_interval <= 1 && p.round_budget > 1;
+  }
   p.timeout_ns = o.timeout_seconds > 0 ? (unsigned long long)(o.timeout_seconds * 1e9) : 0ull;
   p.own_lo = c->world == 1 ? 0 : c->own_lo;
   p.own_hi = c->world == 1 ? n : c->own_hi;
@@ -1292,6 +1299,10 @@ void run_solve(egs_ctx* c, egs_gpu_stats* st) {
   CK(cudaMemsetAsync(c->frb[1], 0, words * 4, s));
   CK(cudaMemsetAsync(c->cbm[0], 0, words * 4, s));
   CK(cudaMemsetAsync(c->cbm[1], 0, words * 4, s));
+  if (p.r1_cand) {  // (the commit that marks candidates writes every word of these)
+    CK(cudaMemsetAsync(c->cand, 0, words * 4, s));
+    CK(cudaMemsetAsync(c->rbm[1], 0, words * 4, s));
+  }
   CK(cudaMemsetAsync(c->scratch, 0, sizeof(egs::Scratch), s));
   CK(cudaMemsetAsync(c->ctr, 0, egs::kNumCounters * sizeof(unsigned long long), s));
   void* args[] = {&p};

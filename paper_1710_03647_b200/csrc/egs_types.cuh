@@ -135,6 +135,8 @@ struct SolveParams {
   int debug;                // SolverOptions::debug_checks: commits check monotonicity
   int no_fuse;              // EGS_NO_FUSE=1: commit and activation in separate phases (tracing)
   int cascade;              // certificate cascade in one queue phase (EGS_CERT_CASCADE=0: passes)
+  int r1_direct;            // round 1 writes f itself (one rank: nothing reads f during round 1)
+  int r1_cand;              // ... and marks the first certificate attempt's candidates
   // multi-GPU (egs_part_solve; world == 1 otherwise): the measure and the
   // changed / removal bitmaps are replicated in one allocation per rank with
   // the same layout everywhere; a rank writes what it raises into every
