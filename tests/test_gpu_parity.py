@@ -194,10 +194,11 @@ GOLDEN_FULL = [
 def test_full_size_golden(egs, golden, key, spec):
     """BASELINE configs at full size, bit-exact against digests computed
     WITHOUT the certificate: the reference solve_sweep run to its fixpoint
-    (C2, C5, and F16 / C3 where tests/golden/make_golden_full.py finished;
-    key without "pin") and the GPU's plain value iteration run to its
-    fixpoint (tests/golden/make_golden_plain.py; "plain_gpu", 0.9-1.7 million
-    rounds, 39-682 s).  Compared: the device output path's write_solution
+    (C2, C5, F16, C3: tests/golden/make_golden_full.py, "ref_rounds") and
+    the GPU's plain value iteration run to its fixpoint
+    (tests/golden/make_golden_plain.py; "plain_gpu": C2, F16, C3 -- the same
+    bytes as the reference -- and C4, "pin": "plain_gpu", 1.9 million
+    in-place sweeps).  Compared: the device output path's write_solution
     bytes (SHA-256, length), the host formatter's bytes, tops and finite sum."""
     if key not in golden:
         pytest.skip("full-size golden vector not generated")
