@@ -29,11 +29,14 @@ for _p in (ROOT, os.path.join(ROOT, "tests")):
 from bench import CONFIGS, workload_name  # noqa: E402
 
 # reference sweeps to the fixpoint: C2 / C5 measured (the reference run to its
-# fixpoint on the GPU box host, tests/golden/make_golden_full.py); C4 from the
-# SURVEY.md §0.4 regression (the GPU's own in-place sweep of the same
-# iteration took 1,914,825 rounds, profiles/r02_golden_plain_gpu_c4_sweep.json)
-PROJECTED_SWEEPS = {"C2": 228296, "C4": 2.1e6, "C5": 224879}
+# fixpoint on the GPU box host, tests/golden/make_golden_full.py, 16 threads),
+# C3 measured (the same on the build container, 4 threads:
+# profiles/r02_golden_full_f16_c3.txt); C4 from the SURVEY.md §0.4
+# regression (the GPU's own in-place sweep of the same iteration took
+# 1,914,825 rounds, profiles/r02_golden_plain_gpu_c4_sweep.json)
+PROJECTED_SWEEPS = {"C2": 228296, "C3": 22036, "C4": 2.1e6, "C5": 224879}
 SWEEP_SOURCE = {"C2": "measured (reference to its fixpoint)",
+                "C3": "measured (reference to its fixpoint, 4 threads)",
                 "C5": "measured (reference to its fixpoint)",
                 "C4": "SURVEY.md §0.4 regression"}
 SAMPLE_SWEEPS = {"C2": 50, "C3": 5, "C4": 3, "C5": 50}
