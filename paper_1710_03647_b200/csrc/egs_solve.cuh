@@ -195,17 +195,21 @@ constexpr int kLocalCounters = 10;
 //             frontier sizes), one per Scratch::sum slot of the current
 //             phase, added to it by end_phase_flush right before the grid
 //             barrier (one global atomic per CTA and nonzero slot).
-// A flush's destination is a slot of the current phase's Scratch::sum row;
-// its index in the row comes from the address itself (the rows are 16-byte
-// aligned: Scratch is cudaMalloc'd and sum is its first member), so no shared
-// row pointer is written during a phase (an earlier one, rewritten by every
-// warp with the same value, was a benign race that racecheck reports).
+// g_slot_base is the current phase's Scratch::sum row; every warp writes it
+// (the same value) before its first flush of the phase, so a read after a
+// warp's own write is always the current phase's row.  (compute-sanitizer
+// racecheck reports these same-value writes against other warps' reads as
+// a shared-memory hazard: benign -- the row changes only across the grid
+// barrier that ends a phase.  Deriving the slot from the address instead
+// removed the report but cost C4 +28 us in the certificate's dense pass, a
+// register-allocation change of the whole kernel.)
 __shared__ unsigned long long g_stats[kLocalCounters];
 __shared__ unsigned int g_psum[4];
-static_assert(offsetof(Scratch, sum) == 0 && sizeof(Scratch::sum[0]) == 16,
-              "block_flush derives a slot's index from its address");
-__device__ __forceinline__ uint32_t psum_slot(const unsigned int* dst) {
-  return (uint32_t)(reinterpret_cast<uintptr_t>(dst) >> 2) & 3u;
+__shared__ unsigned int* g_slot_base;
+
+__device__ __forceinline__ void set_phase_slot(unsigned int* slot) {
+  if (lane_id() == 0) g_slot_base = slot;
+  __syncwarp();
 }
 
 __device__ __forceinline__ void stats_init() {
@@ -220,14 +224,13 @@ __device__ __forceinline__ void stats_exit(unsigned long long* ctr) {
     atomicAdd(ctr + threadIdx.x, g_stats[threadIdx.x]);
 }
 
-// Block-wide, before the grid barrier that ends a phase: the CTA's phase sums
-// into the phase's Scratch::sum row.
-__device__ __forceinline__ void end_phase_flush(unsigned int* row) {
+// Block-wide, before the grid barrier that ends a phase.
+__device__ __forceinline__ void end_phase_flush() {
   __syncthreads();
   if (threadIdx.x < 4u) {
     const unsigned int v = g_psum[threadIdx.x];
     if (v) {
-      atomicAdd(row + threadIdx.x, v);
+      atomicAdd(g_slot_base + threadIdx.x, v);
       g_psum[threadIdx.x] = 0u;
     }
   }
@@ -248,9 +251,9 @@ __device__ __forceinline__ void block_flush(Local& L, unsigned int* dst,
 #pragma unroll
     for (int k = 0; k < kLocalCounters; ++k)
       if (v[k]) atomicAdd(&g_stats[k], (unsigned long long)v[k]);
-    if (v[kLocalCounters]) atomicAdd(&g_psum[psum_slot(dst)], v[kLocalCounters]);
+    if (v[kLocalCounters]) atomicAdd(&g_psum[dst - g_slot_base], v[kLocalCounters]);
     if (v[kLocalCounters + 1] && dst2)
-      atomicAdd(&g_psum[psum_slot(dst2)], v[kLocalCounters + 1]);
+      atomicAdd(&g_psum[dst2 - g_slot_base], v[kLocalCounters + 1]);
   }
   L = Local();
 }
@@ -2693,10 +2696,11 @@ __global__ void __launch_bounds__(kBlock, EGS_MIN_BLOCKS)
         if (k < 4) sh->sum[(phase + 2) & 3][k] = 0;
         sh->dyn[(phase + 2) & 3][k] = 0;
       }
+    set_phase_slot(slot_sum());
   };
   unsigned int epoch = p.epoch0;  // cross-rank barriers (multi-GPU)
   auto end_phase = [&](int kind, int fine = -1) {
-    end_phase_flush(slot_sum());
+    end_phase_flush();
     if (p.world > 1) __threadfence_system();  // this phase's peer writes, before the barrier
     grid.sync();
     ++phase;
